@@ -1,0 +1,101 @@
+"""Seeded synthetic inputs shared by the oracle tests, the GPU tests and bench.py.
+
+This module holds NO arithmetic of the method (no encoding, no modular
+arithmetic, no packing): only numpy PCG64 draws of float matrices with the
+shapes and distributions of the paper's workloads, the 32-byte ChaCha20 keys
+derived from integer seeds, and the preset parameter *widths* (each side derives
+its own primes from them).  Recipe: DESIGN.md "Input recipe".
+"""
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def crypto_key(seed: int, config_id: int) -> bytes:
+    """key = LE64(seed) || LE64(config id) || 16 zero bytes."""
+    return struct.pack("<QQ", seed & (2**64 - 1), config_id & (2**64 - 1)) + bytes(16)
+
+
+@dataclass(frozen=True)
+class Preset:
+    name: str
+    log_n: int
+    q_bits: tuple
+    p_bits: tuple
+    dnum: int
+    log_delta: int
+
+    @property
+    def N(self):
+        return 1 << self.log_n
+
+    @property
+    def n(self):
+        return 1 << (self.log_n - 1)
+
+
+# config 1 (toy, insecure): Q = {60, 40, 40}, P = {60}, dnum = 3, Delta = 2^40
+TOY = Preset("toy", 12, (60, 40, 40), (60,), 3, 40)
+# configs 2-5: N = 2^16, Q = {60, 40 x 4}, P = {60}, dnum = 5 (alpha = 1), Delta = 2^40
+BERT = Preset("bert", 16, (60, 40, 40, 40, 40), (60,), 5, 40)
+# small presets used only by tests (a ragged/tiny ring, and alpha = 2 digits)
+TINY = Preset("tiny", 5, (50, 40, 40), (60,), 3, 30)
+MID = Preset("mid", 10, (60, 40, 40, 40), (61, 61), 2, 36)
+
+
+def rng(seed: int) -> np.random.Generator:
+    return np.random.default_rng(seed)
+
+
+def uniform(seed: int, shape, lo: float, hi: float) -> np.ndarray:
+    return rng(seed).uniform(lo, hi, size=shape).astype(np.float64)
+
+
+def normal(seed: int, shape, std: float, clip: float | None = None) -> np.ndarray:
+    x = rng(seed).normal(0.0, std, size=shape)
+    if clip is not None:
+        x = np.clip(x, -clip, clip)
+    return x.astype(np.float64)
+
+
+def gelu(x: np.ndarray) -> np.ndarray:
+    from math import erf, sqrt
+    v = np.vectorize(lambda t: 0.5 * t * (1.0 + erf(t / sqrt(2.0))))
+    return v(x).astype(np.float64)
+
+
+# ---- config 1: toy ct-pt 16x16x16 + mask ---------------------------------
+def toy_inputs():
+    X = uniform(1, (16, 16), -1.0, 1.0)
+    W = uniform(2, (16, 16), -0.5, 0.5)
+    return dict(X=X, W=W, mask_key=crypto_key(3, 1), keys_key=crypto_key(4, 1), enc_key=crypto_key(5, 1))
+
+
+# ---- config 2: BERT-base attention (QKV + Q K^T) --------------------------
+BERT_BASE = dict(L=128, d=768, H=12, ffn=3072)
+BERT_LARGE = dict(L=128, d=1024, H=16, ffn=4096)
+
+
+def bert_attention_inputs(L=128, d=768, config_id=2):
+    X = normal(11, (L, d), 1.0, clip=4.0)
+    WQ = normal(12, (d, d), 0.04)
+    WK = normal(13, (d, d), 0.04)
+    WV = normal(14, (d, d), 0.04)
+    return dict(X=X, WQ=WQ, WK=WK, WV=WV, keys_key=crypto_key(4, config_id),
+                enc_key=crypto_key(5, config_id), mask_key=crypto_key(3, config_id))
+
+
+# ---- config 3: out-proj (diagonal input) + FFN ----------------------------
+def bert_ffn_inputs(L=128, d=768, H=12, ffn=3072, config_id=3):
+    dh = d // H
+    Att = normal(21, (H, L, dh), 1.0)
+    WO = normal(22, (d, d), 0.04)
+    X2 = normal(23, (L, d), 1.0)
+    W1 = normal(24, (d, ffn), 0.04)
+    H1 = gelu(normal(25, (L, ffn), 1.0))
+    W2 = normal(26, (ffn, d), 0.02)
+    return dict(Att=Att, WO=WO, X2=X2, W1=W1, H1=H1, W2=W2, keys_key=crypto_key(4, config_id),
+                enc_key=crypto_key(5, config_id), mask_key=crypto_key(3, config_id))
