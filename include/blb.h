@@ -1,0 +1,269 @@
+/*
+ * blb.h -- C ABI of the B200-native BLB CKKS fused-linear hot path.
+ *
+ * BLB = "Breaking the Layer Barrier: Remodeling Private Transformer Inference
+ * with Hybrid CKKS and MPC" (arXiv 2508.19525).  This library evaluates, on one
+ * sm_100a GPU, the server side of the paper's fused linear blocks under CKKS:
+ * limb-batched negacyclic NTT, encode, hoisted rotations with hybrid key
+ * switching (ModUp / ModDown), the ct-pt MatMul protocol with BSGS, rescale,
+ * and the CKKS->MPC mask of Algorithm 1.  Citations: P:n = PAPER.md line n,
+ * C<k> / S<k> = the readings listed in DESIGN.md.
+ *
+ * Conventions for every entry point
+ *   * Ownership: every uint64_t* / double* / void* data argument is memory owned
+ *     by the caller (device memory unless the comment says "host").  The
+ *     library never frees or retains it.  blb_params / blb_keys /
+ *     blb_matmul_plan are library-owned (create / destroy pairs) and immutable
+ *     once built; they may be shared by threads and streams.
+ *   * Layout: a polynomial is N contiguous uint64 residues per RNS limb, limbs
+ *     consecutive ("limb-major").  Ciphertext = [2][level+1][N] (c0 then c1),
+ *     plaintext = [level+1][N], both in NTT form (NTT(a)[k] = a(psi^{2brv(k)+1})
+ *     mod q, C2) unless stated.  Every residue is canonical, in [0, q).
+ *   * Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy
+ *     default).  All device work is stream-ordered and asynchronous; argument
+ *     errors are reported synchronously before any launch; asynchronous faults
+ *     surface as BLB_E_CUDA from a later call.
+ *   * Errors: every function returns a blb_status; blb_last_error() returns a
+ *     thread-local message for the last non-OK status.
+ *   * Scratch: hot calls never allocate; they take a caller workspace `ws` of at
+ *     least the bytes the matching *_workspace_bytes query returns.
+ */
+#ifndef BLB_H
+#define BLB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BLB_MAX_PRIMES 24
+
+typedef enum {
+    BLB_OK = 0,
+    BLB_E_INVALID_ARG = 1, /* null pointer, bad size or range                        */
+    BLB_E_PARAM = 2,       /* prime != 1 mod 2N, not prime, >= 2^61, duplicate, bad N/dnum */
+    BLB_E_MISSING_KEY = 3, /* rotation / relinearisation key absent       */
+    BLB_E_LEVEL = 4,       /* level mismatch or depth exhausted    */
+    BLB_E_SCALE = 5,       /* scale mismatch                                    */
+    BLB_E_LAYOUT = 6,      /* shape / packing mismatch                  */
+    BLB_E_OVERFLOW = 7,    /* encode magnitude |round(scale * m_k)| >= 2^52     */
+    BLB_E_CUDA = 8,        /* CUDA runtime error                                        */
+    BLB_E_NOMEM = 9,       /* allocation failure / workspace too small                  */
+} blb_status;
+
+typedef struct blb_params blb_params;
+typedef struct blb_keys blb_keys;
+typedef struct blb_matmul_plan blb_matmul_plan;
+
+/* A ciphertext view (device memory owned by the caller): data = [2][level+1][N]
+ * uint64, NTT form; scale = the CKKS scaling factor Delta tracked as a double. */
+typedef struct {
+    uint64_t *data;
+    int32_t level;
+    int32_t reserved;
+    double scale;
+} blb_ct;
+
+typedef enum { BLB_PACK_SPATIAL = 0, BLB_PACK_DIAGONAL = 1 } blb_packing;
+
+typedef enum {
+    BLB_OP_ROTATE = 0,
+    BLB_OP_RESCALE = 1,
+    BLB_OP_MASK = 2,
+    BLB_OP_ENCODE = 3,
+} blb_op;
+
+/* ------------------------------------------------------------------ */
+/* errors, counters                                                     */
+/* ------------------------------------------------------------------ */
+const char *blb_last_error(void);
+
+/* Process-wide counters: [0] kernel launches, [1] key switches (rotations +
+ * relinearisations), [2] limb NTT/INTT transforms, [3] ct-pt products,
+ * [4] rescales, [5] masks.  Host memory out[6]. */
+void blb_counters_get(uint64_t out[6]);
+void blb_counters_reset(void);
+
+/* ------------------------------------------------------------------ */
+/* parameters (C1; Table 6 P:716-720 for the chain shape)               */
+/* ------------------------------------------------------------------ */
+/* Host helper, C1 prime-list rule: for each width bits[i] (chain order), the
+ * largest prime < 2^bits[i] with p == 1 (mod 2N) not already chosen.
+ * out: host [count].  BLB_E_PARAM if a width is outside [log_n+2, 61]. */
+blb_status blb_prime_chain(int log_n, const int *bits, int count, uint64_t *out);
+
+/* Create the parameter set of ring A_{N,q} = Z_q[x]/(x^N+1) in RNS:
+ * ciphertext chain q[0..nq) (q[0] first, rescale drops q[nq-1] first) and
+ * special primes p[0..np) for hybrid key switching (reading S2; P:233 says
+ * only "rotation").  dnum = number of key-switch digits; the digit size is
+ * alpha = ceil(nq / dnum), digit j = {q_i : j*alpha <= i < (j+1)*alpha}.
+ * q, p: host arrays.  log_n in [2, 16].  Uploads twiddle / base-conversion
+ * tables to `cuda_device`.  Errors: BLB_E_PARAM. */
+blb_status blb_params_create(blb_params **out, int log_n, const uint64_t *q, int nq, const uint64_t *p, int np,
+                             int dnum, int cuda_device);
+void blb_params_destroy(blb_params *params);
+
+/* Host outputs: log_n, nq, np, alpha; moduli[nq+np] (q then p) and the minimal
+ * primitive 2N-th roots psi[nq+np] (C1).  Any output pointer may be NULL. */
+blb_status blb_params_query(const blb_params *params, int *log_n, int *nq, int *np, int *alpha, uint64_t *moduli,
+                            uint64_t *psi);
+
+/* Galois element of a left rotation by `step` slots: 5^(step mod N/2) mod 2N
+ * ("by default, we use left rotation"; reading S4). */
+uint32_t blb_galois_element(const blb_params *params, int32_t step);
+
+/* ------------------------------------------------------------------ */
+/* NTT (row a1; C2)                                                     */
+/* ------------------------------------------------------------------ */
+/* In-place forward / inverse negacyclic NTT of n_polys x n_limbs rows,
+ * data = [n_polys][n_limbs][N]; row (p, l) is reduced with modulus index
+ * prime_idx[l] (host array, indices into q then p).  Input residues must be
+ * in [0, q); output is canonical.  INTT includes the factor N^{-1}. */
+blb_status blb_ntt(const blb_params *params, uint64_t *data, const int32_t *prime_idx, int n_limbs, int n_polys,
+                   void *stream);
+blb_status blb_intt(const blb_params *params, uint64_t *data, const int32_t *prime_idx, int n_limbs, int n_polys,
+                    void *stream);
+
+/* ------------------------------------------------------------------ */
+/* encode / decode (Eq. eq:ckks_encode; C3)                  */
+/* ------------------------------------------------------------------ */
+/* Encode n_pts real slot vectors slots[n_pts][N/2] (device, float64) as
+ * plaintexts out[n_pts][level+1][N] (NTT form): coefficient k is the
+ * correctly rounded (ties-to-even) integer nearest to scale * m_k with
+ * m = pi^{-1}(z), slot j <-> root zeta^{5^j}, zeta = e^{i pi / N}; the inverse
+ * canonical embedding is evaluated in double-double arithmetic.  Real slots
+ * only (footnote P:540).  BLB_E_OVERFLOW if some |scale * m_k| >= 2^52.
+ * Synchronises `stream` (to read the overflow flag). */
+blb_status blb_encode(const blb_params *params, const double *slots, int n_pts, double scale, int level,
+                      uint64_t *out, void *stream);
+
+/* Decode a plaintext pt[level+1][N] (NTT form) to slots_out[N/2] (device):
+ * z_j = Re(m(zeta^{5^j})) / scale with m the centred lift of limb q_0
+ * (precondition: every |coefficient| < q_0 / 2, true for decrypted outputs
+ * at scale ~ 2^40 with the BLB presets). */
+blb_status blb_decode(const blb_params *params, const uint64_t *pt, int level, double scale, double *slots_out,
+                      void *stream);
+
+/* ------------------------------------------------------------------ */
+/* keys (C5) -- generated by the client; the server only loads them      */
+/* ------------------------------------------------------------------ */
+blb_status blb_keys_create(const blb_params *params, blb_keys **out);
+void blb_keys_destroy(blb_keys *keys);
+
+/* Copy one switching key swk[beta_top][2][nq+np][N] (device, NTT form;
+ * [.][0] = b, [.][1] = a, beta_top = ceil(nq/alpha)) into `keys` under
+ * Galois element `galois` (0 = relinearisation key for s^2). */
+blb_status blb_keys_add(blb_keys *keys, uint32_t galois, const uint64_t *swk, void *stream);
+int blb_keys_has(const blb_keys *keys, uint32_t galois);
+
+/* Test / client helper: generate the ternary secret s from `seed` (ChaCha20,
+ * reading C4) and the switching keys for the given rotation steps (and s^2
+ * if with_relin) into `keys`.  secret_out (nullable, device) receives
+ * NTT(s) over all nq+np primes, [nq+np][N].  Synchronises `stream`. */
+blb_status blb_keygen(const blb_params *params, const uint8_t seed[32], const int32_t *rot_steps, int n_steps,
+                      int with_relin, blb_keys *keys, uint64_t *secret_out, void *stream);
+
+/* ------------------------------------------------------------------ */
+/* encrypt / decrypt (C6) -- client side, used by tests and the bench    */
+/* ------------------------------------------------------------------ */
+/* Symmetric encryption at `level`: c1 = a (uniform, NTT domain, ChaCha ENC_A),
+ * c0 = -a*s + pt + e (e centred binomial eta = 21, ChaCha ENC_E), object id =
+ * ct_id.  secret: [nq+np][N] NTT; pt: [level+1][N]; out->data [2][level+1][N]. */
+blb_status blb_encrypt(const blb_params *params, const uint64_t *secret, const uint64_t *pt, int level,
+                       const uint8_t seed[32], uint64_t ct_id, double scale, blb_ct *out, void *stream);
+/* Dec(ct) = c0 + c1*s mod Q_level (NTT form) -> pt_out [level+1][N]. */
+blb_status blb_decrypt(const blb_params *params, const uint64_t *secret, const blb_ct *ct, uint64_t *pt_out,
+                       void *stream);
+
+/* ------------------------------------------------------------------ */
+/* homomorphic operations                                               */
+/* ------------------------------------------------------------------ */
+size_t blb_workspace_bytes(const blb_params *params, blb_op op, int level);
+
+/* Left rotation by `step` slots, hoisted form (C8):
+ * (sigma_g(c0) + c0', c1') with (c0', c1') = ModDown(sum_j sigma_g(ModUp(D_j(c1))) (.) rk_{g,j}).
+ * `out` may not alias `in`.  BLB_E_MISSING_KEY if the key for g is absent. */
+blb_status blb_rotate(const blb_params *params, const blb_keys *keys, const blb_ct *in, int32_t step, blb_ct *out,
+                      void *ws, size_t ws_bytes, void *stream);
+
+/* Rescale (reading S7 / C10): out = round(in / q_level) exactly, level-1,
+ * scale / q_level.  out->data [2][level][N], may not alias in. */
+blb_status blb_rescale(const blb_params *params, const blb_ct *in, blb_ct *out, void *ws, size_t ws_bytes,
+                       void *stream);
+
+/* ct (x) pt (C9): out = (c0 * pt, c1 * pt), scale = in.scale * pt_scale. */
+blb_status blb_mul_pt(const blb_params *params, const blb_ct *in, const uint64_t *pt, double pt_scale, blb_ct *out,
+                      void *stream);
+/* ct + ct (same level): out = a + b (may alias a). BLB_E_SCALE if scales differ by > 1 bit. */
+blb_status blb_add(const blb_params *params, const blb_ct *a, const blb_ct *b, blb_ct *out, void *stream);
+
+/* CKKS->MPC masking, server half of Algorithm 1 line 1 (F_C2M items 1
+ * and 4; reading C14): for each of n_ct ciphertexts, drop to q_0,
+ * INTT both polynomials, sample r uniform over Z_{q0}^N (ChaCha20 MASK,
+ * object id first_ct_id + t), output masked[t] = (c0 + r, c1) and
+ * share[t] = -r mod q_0, coefficient form.  masked: [n_ct][2][N], share:
+ * [n_ct][N].  in[t].data must be distinct ciphertexts (not modified). */
+blb_status blb_ckks_to_mpc(const blb_params *params, const blb_ct *in, int n_ct, const uint8_t mask_key[32],
+                           uint64_t first_ct_id, uint64_t *masked, uint64_t *share, void *ws, size_t ws_bytes,
+                           void *stream);
+
+/* ------------------------------------------------------------------ */
+/* ct-pt MatMul (rows a2-a6; C11 / C12; BSGS App. C.1)      */
+/* ------------------------------------------------------------------ */
+/* MHP output-column map (reading S16): heads padded to
+ * H_p = next power of two >= heads; virtual column v = j*c + cc*H_p + h holds
+ * source column h*d_h + j*g + cc (c = N/(2L), g = c / H_p, d_h = d / heads),
+ * or -1 for padded heads.  map_out: host, capacity *len on entry; *len = the
+ * map length on return. */
+blb_status blb_mhp_column_map(int d, int heads, int L, int log_n, int32_t *map_out, int *len);
+
+/* Plan Y = X W for X in R^{L x D_in} packed in ciphertexts at `level`.
+ *  BLB_PACK_SPATIAL  (C11): input spatial-first: ciphertext b holds
+ *     column b*c + tau at slots tau*L + i.  W: w_rows x w_cols row-major with
+ *     w_rows = D_in; col_map (host, nullable) gives for each of D_out virtual
+ *     output columns the source column of W or -1 (zero) -- e.g. the MHP map;
+ *     NULL means D_out = w_cols, identity.
+ *  BLB_PACK_DIAGONAL (C12, App. C.2): input = dense multi-head diagonal
+ *     packing of Att_h (heads x L x d_h): block beta = d*heads + h holds
+ *     Att_h[i, (i+d) mod d_h]; W = W_O with w_rows = heads*d_h, D_out = w_cols.
+ *  BSGS: t = g*B + i over c = N/(2L) block rotations; all-zero diagonals are
+ *  skipped (bit-neutral).  Output: ceil(D_out / c) spatial-first ciphertexts
+ *  at level-1, scale = input scale (plaintexts are encoded at scale q_level). */
+blb_status blb_matmul_plan_create(const blb_params *params, int L, int w_rows, int w_cols, blb_packing packing,
+                                  int heads, const int32_t *col_map, int D_out, int bsgs_B, int level,
+                                  blb_matmul_plan **out);
+void blb_matmul_plan_destroy(blb_matmul_plan *plan);
+
+/* Host outputs (nullable): number of input / output ciphertexts, total
+ * non-zero plaintexts, baby / giant rotations, B, G. */
+blb_status blb_matmul_plan_info(const blb_matmul_plan *plan, int *n_in, int *n_out, int *n_pt, int *n_baby,
+                                int *n_giant, int *B, int *G);
+/* Distinct rotation steps (slots) the plan needs keys for; steps: host array of
+ * capacity *n on entry. */
+blb_status blb_matmul_plan_rotations(const blb_matmul_plan *plan, int32_t *steps, int *n);
+/* Plaintexts owned by outputs [out_first, out_first+out_count). */
+blb_status blb_matmul_pt_count(const blb_matmul_plan *plan, int out_first, int out_count, int *n_pt);
+
+/* Offline precompute (row a0): build and encode the plaintexts of outputs
+ * [out_first, out_first+out_count) from W (host, row-major w_rows x w_cols,
+ * float64) into pt_dev[n_pt][level+1][N] (device), plan order.  Synchronises. */
+blb_status blb_matmul_encode_weights(const blb_matmul_plan *plan, const double *W, int out_first, int out_count,
+                                     uint64_t *pt_dev, void *stream);
+
+size_t blb_matmul_workspace_bytes(const blb_matmul_plan *plan, int out_count);
+
+/* Evaluate outputs [out_first, out_first+out_count) of the plan on the n_in
+ * input ciphertexts (all at the plan level, NTT form): hoisted baby-step
+ * rotations of every input, the MAC against pt_dev (the slice encoded for the
+ * same output range), giant-step key switches, one rescale per output.
+ * out[t] receives output ciphertext out_first + t ([2][level][N]). */
+blb_status blb_ct_pt_matmul(const blb_matmul_plan *plan, const blb_keys *keys, const blb_ct *in, int n_in,
+                            const uint64_t *pt_dev, int out_first, int out_count, blb_ct *out, void *ws,
+                            size_t ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLB_H */

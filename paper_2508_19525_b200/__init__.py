@@ -1,0 +1,405 @@
+"""paper_2508_19525_b200 -- B200-native CKKS fused-linear hot path of BLB (arXiv 2508.19525).
+
+Thin Python binding over ``libblb.so`` (the C ABI declared in include/blb.h).
+Argument marshalling only: every step of the path runs in the library's sm_100a
+kernels; torch supplies device memory and the current CUDA stream.  There is no
+CPU fallback -- importing this package without the built library raises.
+
+Residue tensors are ``torch.int64`` holding the raw uint64 bit patterns
+(canonical residues < 2^61, so the values are also non-negative int64).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from ._build import SO, build  # noqa: F401
+from . import packing  # noqa: F401
+
+__all__ = ["BLBError", "Params", "Ciphertext", "Keys", "MatmulPlan", "lib", "SO"]
+
+
+class BLBError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__("blb status %d: %s" % (status, msg))
+        self.status = status
+
+
+STATUS = {0: "OK", 1: "INVALID_ARG", 2: "PARAM", 3: "MISSING_KEY", 4: "LEVEL", 5: "SCALE", 6: "LAYOUT",
+          7: "OVERFLOW", 8: "CUDA", 9: "NOMEM"}
+PACK_SPATIAL, PACK_DIAGONAL = 0, 1
+OP_ROTATE, OP_RESCALE, OP_MASK, OP_ENCODE = 0, 1, 2, 3
+
+
+class _Ct(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("level", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("scale", ctypes.c_double)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO):
+            raise ImportError("libblb.so is not built (run __graft_entry__.build()); no CPU fallback exists")
+        L = ctypes.CDLL(SO)
+        vp, i32, u64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double
+        ip = ctypes.POINTER(ctypes.c_int)
+        sigs = {
+            "blb_last_error": ([], ctypes.c_char_p),
+            "blb_counters_get": ([vp], None),
+            "blb_counters_reset": ([], None),
+            "blb_prime_chain": ([ctypes.c_int, vp, ctypes.c_int, vp], ctypes.c_int),
+            "blb_params_create": ([vp, ctypes.c_int, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int],
+                                  ctypes.c_int),
+            "blb_params_destroy": ([vp], None),
+            "blb_params_query": ([vp, ip, ip, ip, ip, vp, vp], ctypes.c_int),
+            "blb_galois_element": ([vp, i32], ctypes.c_uint32),
+            "blb_ntt": ([vp, vp, vp, ctypes.c_int, ctypes.c_int, vp], ctypes.c_int),
+            "blb_intt": ([vp, vp, vp, ctypes.c_int, ctypes.c_int, vp], ctypes.c_int),
+            "blb_encode": ([vp, vp, ctypes.c_int, dbl, ctypes.c_int, vp, vp], ctypes.c_int),
+            "blb_decode": ([vp, vp, ctypes.c_int, dbl, vp, vp], ctypes.c_int),
+            "blb_keys_create": ([vp, vp], ctypes.c_int),
+            "blb_keys_destroy": ([vp], None),
+            "blb_keys_add": ([vp, ctypes.c_uint32, vp, vp], ctypes.c_int),
+            "blb_keys_has": ([vp, ctypes.c_uint32], ctypes.c_int),
+            "blb_keygen": ([vp, ctypes.c_char_p, vp, ctypes.c_int, ctypes.c_int, vp, vp, vp], ctypes.c_int),
+            "blb_encrypt": ([vp, vp, vp, ctypes.c_int, ctypes.c_char_p, u64, dbl, vp, vp], ctypes.c_int),
+            "blb_decrypt": ([vp, vp, vp, vp, vp], ctypes.c_int),
+            "blb_workspace_bytes": ([vp, ctypes.c_int, ctypes.c_int], ctypes.c_size_t),
+            "blb_rotate": ([vp, vp, vp, i32, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
+            "blb_rescale": ([vp, vp, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
+            "blb_mul_pt": ([vp, vp, vp, dbl, vp, vp], ctypes.c_int),
+            "blb_add": ([vp, vp, vp, vp, vp], ctypes.c_int),
+            "blb_ckks_to_mpc": ([vp, vp, ctypes.c_int, ctypes.c_char_p, u64, vp, vp, vp, ctypes.c_size_t, vp],
+                                ctypes.c_int),
+            "blb_mhp_column_map": ([ctypes.c_int] * 4 + [vp, ip], ctypes.c_int),
+            "blb_matmul_plan_create": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp,
+                                        ctypes.c_int, ctypes.c_int, ctypes.c_int, vp], ctypes.c_int),
+            "blb_matmul_plan_destroy": ([vp], None),
+            "blb_matmul_plan_info": ([vp, ip, ip, ip, ip, ip, ip, ip], ctypes.c_int),
+            "blb_matmul_plan_rotations": ([vp, vp, ip], ctypes.c_int),
+            "blb_matmul_pt_count": ([vp, ctypes.c_int, ctypes.c_int, ip], ctypes.c_int),
+            "blb_matmul_encode_weights": ([vp, vp, ctypes.c_int, ctypes.c_int, vp, vp], ctypes.c_int),
+            "blb_matmul_workspace_bytes": ([vp, ctypes.c_int], ctypes.c_size_t),
+            "blb_ct_pt_matmul": ([vp, vp, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t,
+                                  vp], ctypes.c_int),
+        }
+        for name, (args, res) in sigs.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise BLBError(status, "%s: %s" % (STATUS.get(status, "?"), lib().blb_last_error().decode()))
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: torch.Tensor):
+    assert t.is_cuda and t.is_contiguous(), "expected a contiguous CUDA tensor"
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def counters() -> dict:
+    out = (ctypes.c_uint64 * 6)()
+    lib().blb_counters_get(out)
+    names = ["launches", "keyswitches", "limb_ntts", "ct_pt_products", "rescales", "masks"]
+    return {n: int(v) for n, v in zip(names, out)}
+
+
+def reset_counters():
+    lib().blb_counters_reset()
+
+
+def prime_chain(log_n: int, bits) -> list[int]:
+    out = (ctypes.c_uint64 * len(bits))()
+    _check(lib().blb_prime_chain(log_n, (ctypes.c_int * len(bits))(*bits), len(bits), out))
+    return [int(x) for x in out]
+
+
+def to_numpy_u64(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().contiguous().numpy().view(np.uint64)
+
+
+def from_numpy_u64(a: np.ndarray, device="cuda") -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint64).view(np.int64)).to(device)
+
+
+class Params:
+    """blb_params_create: ring degree N = 2^log_n, chain q, special primes p, dnum."""
+
+    def __init__(self, log_n: int, q, p, dnum: int, device: int | None = None):
+        self.device = torch.cuda.current_device() if device is None else device
+        qa = (ctypes.c_uint64 * len(q))(*q)
+        pa = (ctypes.c_uint64 * len(p))(*p)
+        h = ctypes.c_void_p()
+        _check(lib().blb_params_create(ctypes.byref(h), log_n, qa, len(q), pa, len(p), dnum, self.device))
+        self._h = h
+        ln, nq, npp, al = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        mods = (ctypes.c_uint64 * (len(q) + len(p)))()
+        psi = (ctypes.c_uint64 * (len(q) + len(p)))()
+        _check(lib().blb_params_query(h, ctypes.byref(ln), ctypes.byref(nq), ctypes.byref(npp), ctypes.byref(al),
+                                      mods, psi))
+        self.log_n, self.K, self.np_, self.alpha = ln.value, nq.value, npp.value, al.value
+        self.N, self.n = 1 << self.log_n, 1 << (self.log_n - 1)
+        self.moduli = [int(x) for x in mods]
+        self.q, self.p = self.moduli[:self.K], self.moduli[self.K:]
+        self.psi = [int(x) for x in psi]
+
+    @classmethod
+    def from_preset(cls, preset, device=None) -> "Params":
+        primes = prime_chain(preset.log_n, list(preset.q_bits) + list(preset.p_bits))
+        k = len(preset.q_bits)
+        return cls(preset.log_n, primes[:k], primes[k:], preset.dnum, device)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.blb_params_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def galois(self, step: int) -> int:
+        return int(lib().blb_galois_element(self._h, step))
+
+    def beta_top(self) -> int:
+        return -(-self.K // self.alpha)
+
+    def empty(self, *shape) -> torch.Tensor:
+        return torch.empty(*shape, dtype=torch.int64, device="cuda")
+
+    def workspace(self, op: int, level: int) -> torch.Tensor:
+        nbytes = lib().blb_workspace_bytes(self._h, op, level)
+        return torch.empty(max(nbytes, 8) // 8 + 1, dtype=torch.int64, device="cuda")
+
+    # --- a1 ---
+    def ntt(self, data: torch.Tensor, prime_idx, inverse: bool = False) -> torch.Tensor:
+        """In place on data [n_polys][len(prime_idx)][N]."""
+        pidx = (ctypes.c_int32 * len(prime_idx))(*prime_idx)
+        n_polys = data.numel() // (len(prime_idx) * self.N)
+        fn = lib().blb_intt if inverse else lib().blb_ntt
+        _check(fn(self._h, _ptr(data), pidx, len(prime_idx), n_polys, _stream()))
+        return data
+
+    def intt(self, data, prime_idx):
+        return self.ntt(data, prime_idx, inverse=True)
+
+    # --- encode / decode ---
+    def encode(self, slots: torch.Tensor, scale: float, level: int) -> torch.Tensor:
+        """slots float64 [n_pts][N/2] (or [N/2]) on CUDA -> plaintexts int64 [n_pts][level+1][N]."""
+        s = slots.to(device="cuda", dtype=torch.float64).contiguous()
+        n_pts = 1 if s.dim() == 1 else s.shape[0]
+        out = self.empty(n_pts, level + 1, self.N)
+        _check(lib().blb_encode(self._h, _ptr(s), n_pts, float(scale), level, _ptr(out), _stream()))
+        return out if s.dim() > 1 else out[0]
+
+    def decode(self, pt: torch.Tensor, scale: float) -> torch.Tensor:
+        level = pt.shape[0] - 1
+        out = torch.empty(self.n, dtype=torch.float64, device="cuda")
+        _check(lib().blb_decode(self._h, _ptr(pt.contiguous()), level, float(scale), _ptr(out), _stream()))
+        return out
+
+
+@dataclass
+class Ciphertext:
+    data: torch.Tensor  # int64 [2][level+1][N] CUDA
+    level: int
+    scale: float
+
+    def c(self) -> _Ct:
+        return _Ct(self.data.data_ptr(), self.level, 0, self.scale)
+
+    @staticmethod
+    def empty(params: Params, level: int, scale: float = 1.0) -> "Ciphertext":
+        return Ciphertext(params.empty(2, level + 1, params.N), level, scale)
+
+
+class Keys:
+    def __init__(self, params: Params):
+        self.params = params
+        h = ctypes.c_void_p()
+        _check(lib().blb_keys_create(params.handle, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.blb_keys_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def add(self, galois: int, swk: torch.Tensor):
+        _check(lib().blb_keys_add(self._h, galois, _ptr(swk.contiguous()), _stream()))
+
+    def has(self, galois: int) -> bool:
+        return bool(lib().blb_keys_has(self._h, galois))
+
+
+def keygen(params: Params, seed: bytes, rot_steps=(), relin: bool = False, want_secret: bool = True):
+    keys = Keys(params)
+    steps = (ctypes.c_int32 * max(1, len(rot_steps)))(*rot_steps)
+    sk = params.empty(params.K + params.np_, params.N) if want_secret else None
+    _check(lib().blb_keygen(params.handle, seed, steps, len(rot_steps), int(relin), keys.handle,
+                            _ptr(sk) if sk is not None else None, _stream()))
+    return keys, sk
+
+
+def encrypt(params: Params, secret: torch.Tensor, pt: torch.Tensor, level: int, seed: bytes, ct_id: int,
+            scale: float) -> Ciphertext:
+    ct = Ciphertext.empty(params, level, scale)
+    c = ct.c()
+    _check(lib().blb_encrypt(params.handle, _ptr(secret), _ptr(pt.contiguous()), level, seed, ct_id, float(scale),
+                             ctypes.byref(c), _stream()))
+    return ct
+
+
+def decrypt(params: Params, secret: torch.Tensor, ct: Ciphertext) -> torch.Tensor:
+    out = params.empty(ct.level + 1, params.N)
+    c = ct.c()
+    _check(lib().blb_decrypt(params.handle, _ptr(secret), ctypes.byref(c), _ptr(out), _stream()))
+    return out
+
+
+def rotate(params: Params, keys: Keys, ct: Ciphertext, step: int, ws: torch.Tensor | None = None) -> Ciphertext:
+    out = Ciphertext.empty(params, ct.level, ct.scale)
+    ws = params.workspace(OP_ROTATE, ct.level) if ws is None else ws
+    ci, co = ct.c(), out.c()
+    _check(lib().blb_rotate(params.handle, keys.handle, ctypes.byref(ci), step, ctypes.byref(co), _ptr(ws),
+                            ws.numel() * 8, _stream()))
+    out.level, out.scale = co.level, co.scale
+    return out
+
+
+def rescale(params: Params, ct: Ciphertext, ws: torch.Tensor | None = None) -> Ciphertext:
+    out = Ciphertext.empty(params, ct.level - 1)
+    ws = params.workspace(OP_RESCALE, ct.level) if ws is None else ws
+    ci, co = ct.c(), out.c()
+    _check(lib().blb_rescale(params.handle, ctypes.byref(ci), ctypes.byref(co), _ptr(ws), ws.numel() * 8, _stream()))
+    out.level, out.scale = co.level, co.scale
+    return out
+
+
+def mul_pt(params: Params, ct: Ciphertext, pt: torch.Tensor, pt_scale: float) -> Ciphertext:
+    out = Ciphertext.empty(params, ct.level)
+    ci, co = ct.c(), out.c()
+    _check(lib().blb_mul_pt(params.handle, ctypes.byref(ci), _ptr(pt.contiguous()), float(pt_scale), ctypes.byref(co),
+                            _stream()))
+    out.level, out.scale = co.level, co.scale
+    return out
+
+
+def add(params: Params, a: Ciphertext, b: Ciphertext) -> Ciphertext:
+    out = Ciphertext.empty(params, a.level)
+    ca, cb, co = a.c(), b.c(), out.c()
+    _check(lib().blb_add(params.handle, ctypes.byref(ca), ctypes.byref(cb), ctypes.byref(co), _stream()))
+    out.level, out.scale = co.level, co.scale
+    return out
+
+
+def ckks_to_mpc(params: Params, cts: list, mask_key: bytes, first_ct_id: int):
+    """Server half of Alg. 1: returns (masked int64 [n][2][N], share int64 [n][N]), coefficient form mod q0."""
+    n = len(cts)
+    arr = (_Ct * n)(*[c.c() for c in cts])
+    masked = params.empty(n, 2, params.N)
+    share = params.empty(n, params.N)
+    _check(lib().blb_ckks_to_mpc(params.handle, arr, n, mask_key, first_ct_id, _ptr(masked), _ptr(share), None, 0,
+                                 _stream()))
+    return masked, share
+
+
+def mhp_column_map(d: int, heads: int, L: int, log_n: int) -> list[int]:
+    n = ctypes.c_int(0)
+    _check(lib().blb_mhp_column_map(d, heads, L, log_n, None, ctypes.byref(n)))
+    buf = (ctypes.c_int32 * n.value)()
+    _check(lib().blb_mhp_column_map(d, heads, L, log_n, buf, ctypes.byref(n)))
+    return [int(x) for x in buf]
+
+
+class MatmulPlan:
+    """blb_matmul_plan_create (C11 spatial / C12 diagonal ct-pt MatMul with BSGS)."""
+
+    def __init__(self, params: Params, L: int, w_rows: int, w_cols: int, packing: int = PACK_SPATIAL, heads: int = 1,
+                 col_map=None, bsgs_B: int = 16, level: int | None = None):
+        self.params = params
+        self.level = params.K - 1 if level is None else level
+        self.w_shape = (w_rows, w_cols)
+        cm = None
+        d_out = w_cols
+        if col_map is not None:
+            cm = (ctypes.c_int32 * len(col_map))(*col_map)
+            d_out = len(col_map)
+        h = ctypes.c_void_p()
+        _check(lib().blb_matmul_plan_create(params.handle, L, w_rows, w_cols, packing, heads, cm, d_out, bsgs_B,
+                                            self.level, ctypes.byref(h)))
+        self._h = h
+        vals = [ctypes.c_int() for _ in range(7)]
+        _check(lib().blb_matmul_plan_info(h, *[ctypes.byref(v) for v in vals]))
+        self.n_in, self.n_out, self.n_pt, self.n_baby, self.n_giant, self.B, self.G = [v.value for v in vals]
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.blb_matmul_plan_destroy(self._h)
+            self._h = None
+
+    @property
+    def n_rotations(self) -> int:
+        return self.n_baby + self.n_giant
+
+    def rotation_steps(self) -> list[int]:
+        n = ctypes.c_int(0)
+        _check(lib().blb_matmul_plan_rotations(self._h, None, ctypes.byref(n)))
+        buf = (ctypes.c_int32 * max(1, n.value))()
+        _check(lib().blb_matmul_plan_rotations(self._h, buf, ctypes.byref(n)))
+        return [int(buf[i]) for i in range(n.value)]
+
+    def pt_count(self, out_first: int = 0, out_count: int | None = None) -> int:
+        out_count = self.n_out - out_first if out_count is None else out_count
+        n = ctypes.c_int(0)
+        _check(lib().blb_matmul_pt_count(self._h, out_first, out_count, ctypes.byref(n)))
+        return n.value
+
+    def encode_weights(self, W: np.ndarray, out_first: int = 0, out_count: int | None = None) -> torch.Tensor:
+        out_count = self.n_out - out_first if out_count is None else out_count
+        W = np.ascontiguousarray(W, dtype=np.float64)
+        assert W.shape == self.w_shape
+        npt = self.pt_count(out_first, out_count)
+        pts = self.params.empty(max(npt, 1), self.level + 1, self.params.N)
+        _check(lib().blb_matmul_encode_weights(self._h, W.ctypes.data_as(ctypes.c_void_p), out_first, out_count,
+                                               _ptr(pts), _stream()))
+        return pts
+
+    def workspace(self, out_count: int | None = None) -> torch.Tensor:
+        out_count = self.n_out if out_count is None else out_count
+        nbytes = lib().blb_matmul_workspace_bytes(self._h, out_count)
+        return torch.empty(nbytes // 8 + 1, dtype=torch.int64, device="cuda")
+
+    def __call__(self, keys: Keys, cts: list, pts: torch.Tensor, out_first: int = 0, out_count: int | None = None,
+                 ws: torch.Tensor | None = None, outs: list | None = None) -> list:
+        out_count = self.n_out - out_first if out_count is None else out_count
+        ws = self.workspace(out_count) if ws is None else ws
+        if outs is None:
+            outs = [Ciphertext.empty(self.params, self.level - 1) for _ in range(out_count)]
+        cin = (_Ct * len(cts))(*[c.c() for c in cts])
+        cout = (_Ct * max(1, out_count))(*[o.c() for o in outs])
+        _check(lib().blb_ct_pt_matmul(self._h, keys.handle, cin, len(cts), _ptr(pts), out_first, out_count, cout,
+                                      _ptr(ws), ws.numel() * 8, _stream()))
+        for o, c in zip(outs, cout):
+            o.level, o.scale = c.level, c.scale
+        return outs

@@ -1,0 +1,610 @@
+// api.cu -- the C ABI of include/blb.h: parameters, keys, encode/decode,
+// encrypt/decrypt, rotation, rescale, products and the CKKS->MPC mask.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+#include <algorithm>
+#include "blb_internal.cuh"
+
+extern "C" int blbh_is_prime(u64 n);
+extern "C" int blbh_prime_chain(int logN, const int *bits, int count, u64 *out);
+extern "C" u64 blbh_min_psi(u64 q, int logN);
+extern "C" u64 blbh_shoup(u64 w, u64 q);
+extern "C" u64 blbh_mulmod(u64 a, u64 b, u64 q);
+extern "C" u64 blbh_powmod(u64 a, u64 e, u64 q);
+extern "C" u64 blbh_invmod(u64 a, u64 q);
+extern "C" void blbh_twiddles(u64 q, u64 psi, int logN, u64 *out);
+extern "C" void blbh_zeta_dd(int logN, double *out);
+
+blb_status launch_decode(const blb_params *P, const u64 *pt, double scale, double *slots_out, void *scratch,
+                         cudaStream_t st);
+blb_status blb_launch_sample_uniform(const blb_params *P, u64 *out, long long row_stride, int n_rows, const int *prime,
+                                     const int *nonce, const uint8_t seed[32], uint32_t tag, u64 id, cudaStream_t st);
+blb_status blb_launch_sample_small(const blb_params *P, u64 *out, long long row_stride, int n_rows, const int *prime,
+                                   const uint8_t seed[32], uint32_t tag, u64 id, int mode, cudaStream_t st);
+blb_status blb_launch_keygen_combine(const blb_params *P, u64 *b, const u64 *a, const u64 *s, long long stride,
+                                     int n_rows, const int *prime, uint32_t galois, int relin, const u64 *gadget_dev,
+                                     cudaStream_t st);
+blb_status blb_launch_encrypt_combine(const blb_params *P, u64 *c0, const u64 *c1, const u64 *s, const u64 *pt, int k,
+                                      cudaStream_t st);
+blb_status blb_launch_decrypt(const blb_params *P, const u64 *c0, const u64 *c1, const u64 *s, u64 *out, int k,
+                              cudaStream_t st);
+blb_status blb_launch_mul_pt(const blb_params *P, const u64 *in, const u64 *pt, u64 *out, int k, cudaStream_t st);
+blb_status blb_launch_add(const blb_params *P, const u64 *a, const u64 *b, u64 *out, int k, int npoly,
+                          cudaStream_t st);
+blb_status blb_launch_mask(const blb_params *P, const u64 *const *in, int n, int level, const uint8_t key[32],
+                           u64 id0, u64 *masked, u64 *share, cudaStream_t st);
+
+// ------------------------------------------------------------ errors
+static thread_local char g_err[512] = "";
+unsigned long long g_blb_counters[6] = {0, 0, 0, 0, 0, 0};
+
+void blb_set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+extern "C" const char *blb_last_error(void) { return g_err; }
+extern "C" void blb_counters_get(uint64_t out[6]) {
+    for (int i = 0; i < 6; i++) out[i] = __atomic_load_n(&g_blb_counters[i], __ATOMIC_RELAXED);
+}
+extern "C" void blb_counters_reset(void) {
+    for (int i = 0; i < 6; i++) __atomic_store_n(&g_blb_counters[i], 0ull, __ATOMIC_RELAXED);
+}
+
+// ------------------------------------------------------------ params
+extern "C" blb_status blb_prime_chain(int log_n, const int *bits, int count, uint64_t *out) {
+    if (!bits || !out || count <= 0 || log_n < 2 || log_n > 16) {
+        blb_set_error("blb_prime_chain: invalid argument");
+        return BLB_E_INVALID_ARG;
+    }
+    if (blbh_prime_chain(log_n, bits, count, out) != 0) {
+        blb_set_error("blb_prime_chain: width outside [log_n+2, 61] or no prime left");
+        return BLB_E_PARAM;
+    }
+    return BLB_OK;
+}
+
+static inline u64 host_brv(u64 x, int bits) {
+    u64 r = 0;
+    for (int i = 0; i < bits; i++) r |= ((x >> i) & 1ull) << (bits - 1 - i);
+    return r;
+}
+
+static blb_status build_bconv(blb_params *P) {
+    const int K = P->K, np = P->np, alpha = P->alpha;
+    const int bt = (K + alpha - 1) / alpha;
+    std::vector<u64> tab;
+    P->bconv_off.assign((size_t)K * bt + K, 0);
+    for (int lvl = 0; lvl < K; lvl++) {
+        const int k = lvl + 1, E = k + np, beta = (k + alpha - 1) / alpha;
+        for (int j = 0; j < beta; j++) {
+            const int lo = j * alpha, hi = std::min((j + 1) * alpha, k), nd = hi - lo;
+            P->bconv_off[(size_t)lvl * bt + j] = tab.size();
+            std::vector<u64> inv(nd), invsh(nd), chat((size_t)nd * E);
+            for (int d = 0; d < nd; d++) {
+                const u64 ci = P->mod[lo + d];
+                u64 h = 1 % ci;
+                for (int e = 0; e < nd; e++)
+                    if (e != d) h = blbh_mulmod(h, P->mod[lo + e] % ci, ci);
+                inv[d] = blbh_invmod(h, ci);
+                invsh[d] = blbh_shoup(inv[d], ci);
+                for (int m = 0; m < E; m++) {
+                    const u64 tm = P->mod[m < k ? m : K + (m - k)];
+                    u64 hm = 1 % tm;
+                    for (int e = 0; e < nd; e++)
+                        if (e != d) hm = blbh_mulmod(hm, P->mod[lo + e] % tm, tm);
+                    chat[(size_t)d * E + m] = hm;
+                }
+            }
+            tab.insert(tab.end(), inv.begin(), inv.end());
+            tab.insert(tab.end(), invsh.begin(), invsh.end());
+            tab.insert(tab.end(), chat.begin(), chat.end());
+        }
+    }
+    for (int lvl = 0; lvl < K; lvl++) {
+        const int k = lvl + 1;
+        P->bconv_off[(size_t)K * bt + lvl] = tab.size();
+        std::vector<u64> inv(np), invsh(np), chat((size_t)np * k);
+        for (int d = 0; d < np; d++) {
+            const u64 pd = P->mod[K + d];
+            u64 h = 1 % pd;
+            for (int e = 0; e < np; e++)
+                if (e != d) h = blbh_mulmod(h, P->mod[K + e] % pd, pd);
+            inv[d] = blbh_invmod(h, pd);
+            invsh[d] = blbh_shoup(inv[d], pd);
+            for (int i = 0; i < k; i++) {
+                const u64 qi = P->mod[i];
+                u64 hm = 1 % qi;
+                for (int e = 0; e < np; e++)
+                    if (e != d) hm = blbh_mulmod(hm, P->mod[K + e] % qi, qi);
+                chat[(size_t)d * k + i] = hm;
+            }
+        }
+        tab.insert(tab.end(), inv.begin(), inv.end());
+        tab.insert(tab.end(), invsh.begin(), invsh.end());
+        tab.insert(tab.end(), chat.begin(), chat.end());
+    }
+    BLB_CUDA_TRY(cudaMalloc(&P->d_bconv, sizeof(u64) * std::max<size_t>(tab.size(), 1)));
+    BLB_CUDA_TRY(cudaMemcpy(P->d_bconv, tab.data(), sizeof(u64) * tab.size(), cudaMemcpyHostToDevice));
+    return BLB_OK;
+}
+
+extern "C" void blb_params_destroy(blb_params *P) {
+    if (!P) return;
+    cudaFree(P->d_tw);
+    cudaFree(P->d_zeta);
+    cudaFree(P->d_slot_pos);
+    cudaFree(P->d_bconv);
+    delete P;
+}
+
+extern "C" blb_status blb_params_create(blb_params **out, int log_n, const uint64_t *q, int nq, const uint64_t *p,
+                                        int np, int dnum, int cuda_device) {
+    if (!out || !q || !p) {
+        blb_set_error("blb_params_create: null argument");
+        return BLB_E_INVALID_ARG;
+    }
+    if (log_n < 2 || log_n > 16 || nq < 1 || np < 1 || nq + np > BLB_MAXP || dnum < 1 || dnum > nq) {
+        blb_set_error("blb_params_create: log_n=%d nq=%d np=%d dnum=%d out of range", log_n, nq, np, dnum);
+        return BLB_E_PARAM;
+    }
+    const u64 N = 1ull << log_n;
+    std::vector<u64> mods(q, q + nq);
+    mods.insert(mods.end(), p, p + np);
+    for (size_t i = 0; i < mods.size(); i++) {
+        const u64 m = mods[i];
+        if (m >= (1ull << 61) || (m - 1) % (2 * N) || !blbh_is_prime(m)) {
+            blb_set_error("modulus %llu is not a prime < 2^61 with p == 1 mod 2N", (unsigned long long)m);
+            return BLB_E_PARAM;
+        }
+        for (size_t j = 0; j < i; j++)
+            if (mods[j] == m) {
+                blb_set_error("duplicate modulus %llu", (unsigned long long)m);
+                return BLB_E_PARAM;
+            }
+    }
+    BLB_CUDA_TRY(cudaSetDevice(cuda_device));
+    auto *P = new blb_params();
+    P->logN = log_n; P->N = (int)N; P->K = nq; P->np = np; P->dnum = dnum; P->device = cuda_device;
+    P->alpha = (nq + dnum - 1) / dnum;
+    const int Lk = nq + np;
+    for (int i = 0; i < Lk; i++) {
+        const u64 m = mods[i];
+        P->mod[i] = m;
+        P->psi[i] = blbh_min_psi(m, log_n);
+        ModConst &c = P->pr.m[i];
+        c.q = m;
+        c.ninv = blbh_invmod(N % m, m);
+        c.ninv_sh = blbh_shoup(c.ninv, m);
+        c.r64 = (u64)(((u128)1 << 64) % m);
+        c.r64_sh = blbh_shoup(c.r64, m);
+        c.mu = ~0ull / m;
+    }
+    for (int i = 0; i < nq; i++) {
+        u64 Pm = 1 % P->mod[i];
+        for (int t = 0; t < np; t++) Pm = blbh_mulmod(Pm, P->mod[nq + t] % P->mod[i], P->mod[i]);
+        P->P_mod_q[i] = Pm;
+        P->Pinv[i] = blbh_invmod(Pm, P->mod[i]);
+        P->Pinv_sh[i] = blbh_shoup(P->Pinv[i], P->mod[i]);
+    }
+    // tables
+    std::vector<u64> tw((size_t)Lk * 4 * N);
+    for (int i = 0; i < Lk; i++) blbh_twiddles(P->mod[i], P->psi[i], log_n, tw.data() + (size_t)i * 4 * N);
+    std::vector<double> zeta((size_t)4 * N);
+    blbh_zeta_dd(log_n, zeta.data());
+    std::vector<int32_t> pos(N / 2);
+    u64 e = 1;
+    for (u64 j = 0; j < N / 2; j++) {
+        pos[j] = (int32_t)host_brv((e - 1) / 2, log_n);
+        e = (e * 5) % (2 * N);
+    }
+    cudaError_t err = cudaMalloc(&P->d_tw, sizeof(u64) * tw.size());
+    if (err == cudaSuccess) err = cudaMemcpy(P->d_tw, tw.data(), sizeof(u64) * tw.size(), cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMalloc(&P->d_zeta, sizeof(double) * zeta.size());
+    if (err == cudaSuccess)
+        err = cudaMemcpy(P->d_zeta, zeta.data(), sizeof(double) * zeta.size(), cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMalloc(&P->d_slot_pos, sizeof(int32_t) * pos.size());
+    if (err == cudaSuccess)
+        err = cudaMemcpy(P->d_slot_pos, pos.data(), sizeof(int32_t) * pos.size(), cudaMemcpyHostToDevice);
+    if (err != cudaSuccess) {
+        blb_set_error("blb_params_create: %s", cudaGetErrorString(err));
+        blb_params_destroy(P);
+        return BLB_E_CUDA;
+    }
+    blb_status s = build_bconv(P);
+    if (s != BLB_OK) {
+        blb_params_destroy(P);
+        return s;
+    }
+    *out = P;
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_params_query(const blb_params *P, int *log_n, int *nq, int *np, int *alpha, uint64_t *moduli,
+                                       uint64_t *psi) {
+    if (!P) return BLB_E_INVALID_ARG;
+    if (log_n) *log_n = P->logN;
+    if (nq) *nq = P->K;
+    if (np) *np = P->np;
+    if (alpha) *alpha = P->alpha;
+    for (int i = 0; i < P->K + P->np; i++) {
+        if (moduli) moduli[i] = P->mod[i];
+        if (psi) psi[i] = P->psi[i];
+    }
+    return BLB_OK;
+}
+
+extern "C" uint32_t blb_galois_element(const blb_params *P, int32_t step) {
+    const long long n = P->N / 2;
+    long long s = step % n;
+    if (s < 0) s += n;
+    return (uint32_t)blbh_powmod(5, (u64)s, 2ull * P->N);
+}
+
+// ------------------------------------------------------------ NTT
+static blb_status ntt_common(const blb_params *P, uint64_t *data, const int32_t *prime_idx, int n_limbs, int n_polys,
+                             void *stream, bool inv) {
+    if (!P || !data || !prime_idx || n_limbs < 1 || n_limbs > BLB_MAXP || n_polys < 0) {
+        blb_set_error("blb_ntt: invalid argument");
+        return BLB_E_INVALID_ARG;
+    }
+    RowBatch rb{};
+    rb.base = data; rb.poly_stride = (long long)n_limbs * P->N; rb.n_polys = n_polys; rb.limbs = n_limbs; rb.limb0 = 0;
+    for (int l = 0; l < n_limbs; l++) {
+        if (prime_idx[l] < 0 || prime_idx[l] >= P->K + P->np) {
+            blb_set_error("blb_ntt: prime index %d out of range", prime_idx[l]);
+            return BLB_E_INVALID_ARG;
+        }
+        rb.prime[l] = prime_idx[l];
+    }
+    return launch_ntt(P, rb, inv, (cudaStream_t)stream);
+}
+extern "C" blb_status blb_ntt(const blb_params *P, uint64_t *data, const int32_t *prime_idx, int n_limbs, int n_polys,
+                              void *stream) {
+    return ntt_common(P, data, prime_idx, n_limbs, n_polys, stream, false);
+}
+extern "C" blb_status blb_intt(const blb_params *P, uint64_t *data, const int32_t *prime_idx, int n_limbs, int n_polys,
+                               void *stream) {
+    return ntt_common(P, data, prime_idx, n_limbs, n_polys, stream, true);
+}
+
+// ------------------------------------------------------------ encode / decode
+extern "C" blb_status blb_encode(const blb_params *P, const double *slots, int n_pts, double scale, int level,
+                                 uint64_t *out, void *stream) {
+    if (!P || !slots || !out || n_pts < 0 || !(scale > 0)) {
+        blb_set_error("blb_encode: invalid argument");
+        return BLB_E_INVALID_ARG;
+    }
+    if (level < 0 || level >= P->K) {
+        blb_set_error("blb_encode: level %d out of range", level);
+        return BLB_E_LEVEL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const int chunk = 64;
+    double *buf = nullptr;
+    int *flag = nullptr;
+    BLB_CUDA_TRY(cudaMallocAsync(&buf, sizeof(double) * encode_scratch_doubles(P, std::min(chunk, std::max(n_pts, 1))), st));
+    BLB_CUDA_TRY(cudaMallocAsync(&flag, sizeof(int), st));
+    BLB_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    blb_status s = BLB_OK;
+    for (int p0 = 0; p0 < n_pts && s == BLB_OK; p0 += chunk) {
+        const int cnt = std::min(chunk, n_pts - p0);
+        s = launch_encode(P, slots + (size_t)p0 * (P->N / 2), cnt, scale, level, out + (size_t)p0 * (level + 1) * P->N,
+                          buf, flag, st);
+    }
+    int h = 0;
+    cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(buf, st);
+    cudaFreeAsync(flag, st);
+    BLB_CUDA_TRY(cudaStreamSynchronize(st));
+    if (s != BLB_OK) return s;
+    if (h) {
+        blb_set_error("encode overflow: |scale * m_k| >= 2^52");
+        return BLB_E_OVERFLOW;
+    }
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_decode(const blb_params *P, const uint64_t *pt, int level, double scale, double *slots_out,
+                                 void *stream) {
+    if (!P || !pt || !slots_out || !(scale > 0) || level < 0 || level >= P->K) {
+        blb_set_error("blb_decode: invalid argument");
+        return BLB_E_INVALID_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    void *scratch = nullptr;
+    BLB_CUDA_TRY(cudaMallocAsync(&scratch, (size_t)P->N * (8 + 32), st));
+    blb_status s = launch_decode(P, pt, scale, slots_out, scratch, st);
+    cudaFreeAsync(scratch, st);
+    return s;
+}
+
+// ------------------------------------------------------------ keys
+extern "C" blb_status blb_keys_create(const blb_params *P, blb_keys **out) {
+    if (!P || !out) return BLB_E_INVALID_ARG;
+    auto *k = new blb_keys();
+    k->params = P;
+    *out = k;
+    return BLB_OK;
+}
+extern "C" void blb_keys_destroy(blb_keys *k) {
+    if (!k) return;
+    for (auto *d : k->data) cudaFree(d);
+    delete k;
+}
+static size_t key_elems(const blb_params *P) { return (size_t)blb_beta_top(P) * 2 * (P->K + P->np) * P->N; }
+
+static u64 *keys_slot(blb_keys *K, uint32_t g, blb_status *st) {
+    for (size_t i = 0; i < K->galois.size(); i++)
+        if (K->galois[i] == g) return K->data[i];
+    u64 *d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(u64) * key_elems(K->params));
+    if (e != cudaSuccess) {
+        blb_set_error("key allocation: %s", cudaGetErrorString(e));
+        *st = BLB_E_NOMEM;
+        return nullptr;
+    }
+    K->galois.push_back(g);
+    K->data.push_back(d);
+    return d;
+}
+
+extern "C" blb_status blb_keys_add(blb_keys *K, uint32_t galois, const uint64_t *swk, void *stream) {
+    if (!K || !swk) return BLB_E_INVALID_ARG;
+    blb_status s = BLB_OK;
+    u64 *d = keys_slot(K, galois, &s);
+    if (!d) return s;
+    BLB_CUDA_TRY(cudaMemcpyAsync(d, swk, sizeof(u64) * key_elems(K->params), cudaMemcpyDefault, (cudaStream_t)stream));
+    return BLB_OK;
+}
+extern "C" int blb_keys_has(const blb_keys *K, uint32_t galois) {
+    if (!K) return 0;
+    for (uint32_t g : K->galois)
+        if (g == galois) return 1;
+    return 0;
+}
+
+extern "C" blb_status blb_keygen(const blb_params *P, const uint8_t seed[32], const int32_t *rot_steps, int n_steps,
+                                 int with_relin, blb_keys *K, uint64_t *secret_out, void *stream) {
+    if (!P || !seed || !K || (n_steps > 0 && !rot_steps)) return BLB_E_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int Lk = P->K + P->np, N = P->N, bt = blb_beta_top(P);
+    int prime[BLB_MAXP], nonce[BLB_MAXP];
+    for (int i = 0; i < Lk; i++) { prime[i] = i; nonce[i] = i; }
+    u64 *s = secret_out;
+    u64 *gadget = nullptr;
+    if (!s) BLB_CUDA_TRY(cudaMallocAsync(&s, sizeof(u64) * Lk * N, st));
+    BLB_TRY(blb_launch_sample_small(P, s, N, Lk, prime, seed, TAG_SECRET, 0, 0, st));
+    RowBatch rb{};
+    rb.base = s; rb.poly_stride = (long long)Lk * N; rb.n_polys = 1; rb.limbs = Lk; rb.limb0 = 0;
+    for (int i = 0; i < Lk; i++) rb.prime[i] = i;
+    BLB_TRY(launch_ntt(P, rb, false, st));
+    // gadget P * pi_j per digit: [bt][Lk]
+    std::vector<u64> gh((size_t)bt * Lk, 0);
+    for (int j = 0; j < bt; j++)
+        for (int i = j * P->alpha; i < std::min((j + 1) * P->alpha, P->K); i++) gh[(size_t)j * Lk + i] = P->P_mod_q[i];
+    BLB_CUDA_TRY(cudaMallocAsync(&gadget, sizeof(u64) * gh.size(), st));
+    BLB_CUDA_TRY(cudaMemcpyAsync(gadget, gh.data(), sizeof(u64) * gh.size(), cudaMemcpyHostToDevice, st));
+    std::vector<uint32_t> gl;
+    for (int t = 0; t < n_steps; t++) {
+        const uint32_t g = blb_galois_element(P, rot_steps[t]);
+        if (g != 1 && std::find(gl.begin(), gl.end(), g) == gl.end()) gl.push_back(g);
+    }
+    if (with_relin) gl.push_back(0);
+    blb_status status = BLB_OK;
+    for (uint32_t g : gl) {
+        u64 *key = keys_slot(K, g, &status);
+        if (!key) break;
+        for (int j = 0; j < bt && status == BLB_OK; j++) {
+            const u64 kid = (u64)g * 64 + (u64)j;
+            u64 *b = key + ((size_t)j * 2 + 0) * Lk * N, *a = key + ((size_t)j * 2 + 1) * Lk * N;
+            status = blb_launch_sample_uniform(P, a, N, Lk, prime, nonce, seed, TAG_KEY_A, kid, st);
+            if (status == BLB_OK) status = blb_launch_sample_small(P, b, N, Lk, prime, seed, TAG_KEY_E, kid, 1, st);
+            if (status == BLB_OK) {
+                RowBatch eb = rb;
+                eb.base = b;
+                status = launch_ntt(P, eb, false, st);
+            }
+            if (status == BLB_OK)
+                status = blb_launch_keygen_combine(P, b, a, s, N, Lk, prime, g == 0 ? 1u : g, g == 0,
+                                                   gadget + (size_t)j * Lk, st);
+        }
+        if (status != BLB_OK) break;
+    }
+    cudaFreeAsync(gadget, st);
+    if (!secret_out) cudaFreeAsync(s, st);
+    BLB_CUDA_TRY(cudaStreamSynchronize(st));
+    return status;
+}
+
+// ------------------------------------------------------------ encrypt / decrypt
+extern "C" blb_status blb_encrypt(const blb_params *P, const uint64_t *secret, const uint64_t *pt, int level,
+                                  const uint8_t seed[32], uint64_t ct_id, double scale, blb_ct *out, void *stream) {
+    if (!P || !secret || !pt || !seed || !out || !out->data) return BLB_E_INVALID_ARG;
+    if (level < 0 || level >= P->K) {
+        blb_set_error("blb_encrypt: level %d out of range", level);
+        return BLB_E_LEVEL;
+    }
+    if (ct_id >> 56) {
+        blb_set_error("blb_encrypt: ct_id must be < 2^56 (object id = ct_id << 8 | limb)");
+        return BLB_E_INVALID_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const int k = level + 1, N = P->N;
+    int prime[BLB_MAXP], nonce[BLB_MAXP];
+    for (int i = 0; i < k; i++) { prime[i] = i; nonce[i] = i; }
+    u64 *c0 = out->data, *c1 = out->data + (size_t)k * N;
+    BLB_TRY(blb_launch_sample_uniform(P, c1, N, k, prime, nonce, seed, TAG_ENC_A, ct_id, st));
+    BLB_TRY(blb_launch_sample_small(P, c0, N, k, prime, seed, TAG_ENC_E, ct_id, 1, st));
+    RowBatch rb{};
+    rb.base = c0; rb.poly_stride = (long long)k * N; rb.n_polys = 1; rb.limbs = k; rb.limb0 = 0;
+    for (int i = 0; i < k; i++) rb.prime[i] = i;
+    BLB_TRY(launch_ntt(P, rb, false, st));
+    BLB_TRY(blb_launch_encrypt_combine(P, c0, c1, secret, pt, k, st));
+    out->level = level;
+    out->scale = scale;
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_decrypt(const blb_params *P, const uint64_t *secret, const blb_ct *ct, uint64_t *pt_out,
+                                  void *stream) {
+    if (!P || !secret || !ct || !ct->data || !pt_out) return BLB_E_INVALID_ARG;
+    if (ct->level < 0 || ct->level >= P->K) return BLB_E_LEVEL;
+    const int k = ct->level + 1;
+    return blb_launch_decrypt(P, ct->data, ct->data + (size_t)k * P->N, secret, pt_out, k, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------ operations
+extern "C" size_t blb_workspace_bytes(const blb_params *P, blb_op op, int level) {
+    if (!P || level < 0 || level >= P->K) return 0;
+    const size_t N = P->N, k = level + 1, E = k + P->np, beta = blb_beta(P, level);
+    switch (op) {
+        case BLB_OP_ROTATE: return sizeof(u64) * (beta * E * N + k * N + keyswitch_scratch_elems(P, level, 1));
+        case BLB_OP_RESCALE: return sizeof(u64) * (2 + 2 * k) * N;
+        case BLB_OP_MASK: return 0;
+        case BLB_OP_ENCODE: return sizeof(double) * encode_scratch_doubles(P, 1);
+    }
+    return 0;
+}
+
+static const u64 *find_key(const blb_keys *K, uint32_t g) {
+    for (size_t i = 0; i < K->galois.size(); i++)
+        if (K->galois[i] == g) return K->data[i];
+    return nullptr;
+}
+
+extern "C" blb_status blb_rotate(const blb_params *P, const blb_keys *K, const blb_ct *in, int32_t step, blb_ct *out,
+                                 void *ws, size_t ws_bytes, void *stream) {
+    if (!P || !K || !in || !in->data || !out || !out->data || in->data == out->data) {
+        blb_set_error("blb_rotate: invalid argument");
+        return BLB_E_INVALID_ARG;
+    }
+    const int level = in->level;
+    if (level < 0 || level >= P->K) return BLB_E_LEVEL;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int k = level + 1, N = P->N, E = k + P->np, beta = blb_beta(P, level);
+    const uint32_t g = blb_galois_element(P, step);
+    if (g == 1) {
+        BLB_CUDA_TRY(cudaMemcpyAsync(out->data, in->data, sizeof(u64) * 2 * k * N, cudaMemcpyDeviceToDevice, st));
+        out->level = level;
+        out->scale = in->scale;
+        return BLB_OK;
+    }
+    const u64 *key = find_key(K, g);
+    if (!key) {
+        blb_set_error("missing rotation key for step %d (galois %u)", step, g);
+        return BLB_E_MISSING_KEY;
+    }
+    if (!ws || ws_bytes < blb_workspace_bytes(P, BLB_OP_ROTATE, level)) {
+        blb_set_error("blb_rotate: workspace too small");
+        return BLB_E_NOMEM;
+    }
+    u64 *ext = (u64 *)ws, *coef = ext + (size_t)beta * E * N, *u = coef + (size_t)k * N;
+    u64 *conv = u + (size_t)2 * E * N;
+    const u64 *c1 = in->data + (size_t)k * N;
+    BLB_TRY(launch_modup(P, level, &c1, 1, ext, coef, st));
+    KsJob J{};
+    J.ext = ext; J.key = key; J.c0 = in->data; J.out = out->data; J.galois = g; J.add_mode = 1;
+    BLB_TRY(launch_keyswitch(P, level, &J, 1, u, conv, st));
+    out->level = level;
+    out->scale = in->scale;
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_rescale(const blb_params *P, const blb_ct *in, blb_ct *out, void *ws, size_t ws_bytes,
+                                  void *stream) {
+    if (!P || !in || !in->data || !out || !out->data || in->data == out->data) return BLB_E_INVALID_ARG;
+    if (in->level < 1 || in->level >= P->K) {
+        blb_set_error("blb_rescale: level %d (depth exhausted)", in->level);
+        return BLB_E_LEVEL;
+    }
+    if (!ws || ws_bytes < blb_workspace_bytes(P, BLB_OP_RESCALE, in->level)) {
+        blb_set_error("blb_rescale: workspace too small");
+        return BLB_E_NOMEM;
+    }
+    BLB_TRY(launch_rescale(P, in->data, in->level, 2, out->data, (u64 *)ws, (cudaStream_t)stream));
+    out->level = in->level - 1;
+    out->scale = in->scale / (double)P->mod[in->level];
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_mul_pt(const blb_params *P, const blb_ct *in, const uint64_t *pt, double pt_scale,
+                                 blb_ct *out, void *stream) {
+    if (!P || !in || !in->data || !pt || !out || !out->data) return BLB_E_INVALID_ARG;
+    if (in->level < 0 || in->level >= P->K) return BLB_E_LEVEL;
+    BLB_TRY(blb_launch_mul_pt(P, in->data, pt, out->data, in->level + 1, (cudaStream_t)stream));
+    out->level = in->level;
+    out->scale = in->scale * pt_scale;
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_add(const blb_params *P, const blb_ct *a, const blb_ct *b, blb_ct *out, void *stream) {
+    if (!P || !a || !b || !out || !a->data || !b->data || !out->data) return BLB_E_INVALID_ARG;
+    if (a->level != b->level) {
+        blb_set_error("blb_add: level mismatch %d vs %d", a->level, b->level);
+        return BLB_E_LEVEL;
+    }
+    const double r = a->scale / b->scale;
+    if (r > 2.0 || r < 0.5) {
+        blb_set_error("blb_add: scale mismatch > 1 bit");
+        return BLB_E_SCALE;
+    }
+    BLB_TRY(blb_launch_add(P, a->data, b->data, out->data, a->level + 1, 2, (cudaStream_t)stream));
+    out->level = a->level;
+    out->scale = a->scale;
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_ckks_to_mpc(const blb_params *P, const blb_ct *in, int n_ct, const uint8_t mask_key[32],
+                                      uint64_t first_ct_id, uint64_t *masked, uint64_t *share, void *ws,
+                                      size_t ws_bytes, void *stream) {
+    (void)ws; (void)ws_bytes;
+    if (!P || !in || n_ct < 0 || !mask_key || !masked || !share) return BLB_E_INVALID_ARG;
+    if (n_ct == 0) return BLB_OK;
+    if ((first_ct_id + (u64)n_ct) >> 56) {
+        blb_set_error("blb_ckks_to_mpc: ct ids must be < 2^56");
+        return BLB_E_INVALID_ARG;
+    }
+    const int level = in[0].level;
+    std::vector<const u64 *> ptrs(n_ct);
+    for (int t = 0; t < n_ct; t++) {
+        if (!in[t].data) return BLB_E_INVALID_ARG;
+        if (in[t].level != level) {
+            blb_set_error("blb_ckks_to_mpc: all inputs must share one level");
+            return BLB_E_LEVEL;
+        }
+        ptrs[t] = in[t].data;
+    }
+    return blb_launch_mask(P, ptrs.data(), n_ct, level, mask_key, first_ct_id, masked, share, (cudaStream_t)stream);
+}
+
+extern "C" blb_status blb_mhp_column_map(int d, int heads, int L, int log_n, int32_t *map_out, int *len) {
+    if (!len || d <= 0 || heads <= 0 || d % heads || L <= 0 || log_n < 2) return BLB_E_INVALID_ARG;
+    const int n = 1 << (log_n - 1);
+    if (n % L) return BLB_E_LAYOUT;
+    const int c = n / L;
+    int Hp = 1;
+    while (Hp < heads) Hp <<= 1;
+    if (c % Hp) {
+        blb_set_error("MHP: padded heads %d must divide c = %d", Hp, c);
+        return BLB_E_LAYOUT;
+    }
+    const int dh = d / heads, g = c / Hp, J = (dh + g - 1) / g;
+    const int need = J * c;
+    if (map_out) {
+        if (*len < need) {
+            blb_set_error("MHP map buffer too small (%d < %d)", *len, need);
+            return BLB_E_INVALID_ARG;
+        }
+        for (int j = 0; j < J; j++)
+            for (int cc = 0; cc < g; cc++)
+                for (int h = 0; h < Hp; h++) {
+                    const int within = j * g + cc;
+                    map_out[j * c + cc * Hp + h] = (h < heads && within < dh) ? h * dh + within : -1;
+                }
+    }
+    *len = need;
+    return BLB_OK;
+}

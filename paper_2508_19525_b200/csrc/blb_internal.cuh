@@ -1,0 +1,205 @@
+// blb_internal.cuh -- internal types and device arithmetic of the B200 BLB
+// CKKS library (product code; shares nothing with oracle/).
+//
+// 64-bit RNS residues, primes < 2^61.  Device modular arithmetic:
+//   * Shoup multiplication for constant multiplicands (twiddles, P^{-1}, ...):
+//     w' = floor(w * 2^64 / q),  x*w mod q in [0, 2q) for any 64-bit x.
+//   * 128-bit lazy accumulation of products of canonical residues, reduced
+//     once by reduce128 (hi < 2^63 required, i.e. <= 2^(127 - 2*61) = 32
+//     products of 61-bit residues; the MAC uses <= 96 products of < 2^60
+//     operands for q_0).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <vector>
+#include <string>
+#include "../../include/blb.h"
+
+typedef uint64_t u64;
+typedef unsigned __int128 u128;
+
+#define BLB_MAXP BLB_MAX_PRIMES
+
+// ---------------------------------------------------------------------------
+// per-prime constants (passed by value to kernels)
+// ---------------------------------------------------------------------------
+struct ModConst {
+    u64 q;
+    u64 ninv, ninv_sh;   // N^{-1} mod q and its Shoup companion
+    u64 r64, r64_sh;     // 2^64 mod q and Shoup
+    u64 mu;              // floor((2^64 - 1) / q)  (Barrett for 64-bit values)
+};
+struct Primes {
+    ModConst m[BLB_MAXP];
+};
+
+__host__ __device__ __forceinline__ u64 umulhi64(u64 a, u64 b) {
+#ifdef __CUDA_ARCH__
+    return __umul64hi(a, b);
+#else
+    return (u64)(((u128)a * b) >> 64);
+#endif
+}
+
+// x mod q for any 64-bit x (Barrett, floor error <= 2)
+__device__ __forceinline__ u64 mod64(u64 x, const ModConst &c) {
+    u64 qh = umulhi64(x, c.mu);
+    u64 r = x - qh * c.q;
+    if (r >= c.q) r -= c.q;
+    if (r >= c.q) r -= c.q;
+    return r;
+}
+// Shoup: x * w mod q in [0, 2q)
+__device__ __forceinline__ u64 shoup_lazy(u64 x, u64 w, u64 wsh, u64 q) {
+    return x * w - umulhi64(x, wsh) * q;
+}
+__device__ __forceinline__ u64 shoup(u64 x, u64 w, u64 wsh, u64 q) {
+    u64 r = shoup_lazy(x, w, wsh, q);
+    return r >= q ? r - q : r;
+}
+// (hi * 2^64 + lo) mod q, hi < 2^64
+__device__ __forceinline__ u64 reduce128(u64 hi, u64 lo, const ModConst &c) {
+    u64 h = mod64(hi, c);
+    u64 t = shoup(h, c.r64, c.r64_sh, c.q);
+    u64 l = mod64(lo, c);
+    u64 r = t + l;
+    return r >= c.q ? r - c.q : r;
+}
+// a*b mod q, a, b < 2^64
+__device__ __forceinline__ u64 mulmod(u64 a, u64 b, const ModConst &c) {
+    return reduce128(umulhi64(a, b), a * b, c);
+}
+__device__ __forceinline__ u64 addmod(u64 a, u64 b, u64 q) {
+    u64 r = a + b;
+    return r >= q ? r - q : r;
+}
+__device__ __forceinline__ u64 submod(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
+
+// 128-bit accumulator
+struct Acc128 {
+    u64 lo, hi;
+    __device__ __forceinline__ void zero() { lo = 0; hi = 0; }
+    __device__ __forceinline__ void mac(u64 a, u64 b) {
+        u64 pl = a * b, ph = umulhi64(a, b);
+        u64 nl = lo + pl;
+        hi += ph + (nl < lo ? 1 : 0);
+        lo = nl;
+    }
+    __device__ __forceinline__ u64 reduce(const ModConst &c) const { return reduce128(hi, lo, c); }
+};
+
+// NTT-domain automorphism index: out[k] = in[perm(k)],
+// perm(k) = brv(((g * (2 brv(k) + 1)) mod 2N - 1) / 2)
+__device__ __forceinline__ uint32_t galois_perm(uint32_t k, uint32_t g, int logN) {
+    uint32_t e = 2u * (__brev(k) >> (32 - logN)) + 1u;
+    uint32_t e2 = (uint32_t)(((u64)g * e) & ((2ull << logN) - 1));
+    return __brev((e2 - 1u) >> 1) >> (32 - logN);
+}
+
+// ---------------------------------------------------------------------------
+// host-side objects
+// ---------------------------------------------------------------------------
+struct BconvTable;  // fwd
+
+struct blb_params {
+    int logN, N, K, np, dnum, alpha, device;
+    u64 mod[BLB_MAXP];
+    u64 psi[BLB_MAXP];
+    Primes pr;                    // by-value copy for kernel args
+    u64 *d_tw = nullptr;          // [K+np][4][N]: fwd, fwd_sh, inv, inv_sh (bit-reversed order)
+    double *d_zeta = nullptr;     // [N][4]: zeta^{brv(i)} as (re_hi, re_lo, im_hi, im_lo)
+    int32_t *d_slot_pos = nullptr; // [N/2]: NTT-domain position k of slot j (brv(k) = (5^j - 1)/2)
+    // FastBConv tables, see bconv_* in kernels.cu
+    u64 *d_bconv = nullptr;
+    std::vector<size_t> bconv_off;   // offset of table (level, digit) / moddown(level)
+    u64 P_mod_q[BLB_MAXP];           // P mod q_i
+    u64 Pinv[BLB_MAXP], Pinv_sh[BLB_MAXP];  // P^{-1} mod q_i
+};
+
+struct blb_keys {
+    const blb_params *params;
+    std::vector<uint32_t> galois;       // parallel arrays
+    std::vector<u64 *> data;            // device [beta_top][2][K+np][N]
+};
+
+// ---------------------------------------------------------------------------
+// error plumbing
+// ---------------------------------------------------------------------------
+void blb_set_error(const char *fmt, ...);
+extern unsigned long long g_blb_counters[6];
+#define BLB_COUNT_LAUNCH(n) (__atomic_fetch_add(&g_blb_counters[0], (unsigned long long)(n), __ATOMIC_RELAXED))
+#define BLB_COUNT(i, n) (__atomic_fetch_add(&g_blb_counters[i], (unsigned long long)(n), __ATOMIC_RELAXED))
+
+#define BLB_CUDA_TRY(expr)                                                                        \
+    do {                                                                                          \
+        cudaError_t _e = (expr);                                                                  \
+        if (_e != cudaSuccess) {                                                                  \
+            blb_set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(_e), __FILE__, __LINE__, \
+                          cudaGetErrorString(_e));                                                \
+            return BLB_E_CUDA;                                                                    \
+        }                                                                                         \
+    } while (0)
+#define BLB_CHECK_LAUNCH() BLB_CUDA_TRY(cudaGetLastError())
+#define BLB_TRY(expr)                     \
+    do {                                  \
+        blb_status _s = (expr);           \
+        if (_s != BLB_OK) return _s;      \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// internal launchers (kernels.cu / ntt.cu / encode.cu)
+// ---------------------------------------------------------------------------
+// A batch of NTT rows: row r = p * limbs + l is at base + p * poly_stride + (limb0 + l) * N,
+// modulus index prime[l].
+struct RowBatch {
+    u64 *base;
+    long long poly_stride;  // in u64 elements
+    int n_polys, limbs, limb0;
+    int prime[BLB_MAXP];
+    // optional: skip rows whose limb l lies in digit (p % skip_beta) of size
+    // skip_alpha among the first skip_kmax limbs (ModUp: a digit's own limbs
+    // are copied, not recomputed)
+    int skip_alpha = 0, skip_beta = 1, skip_kmax = 0;
+};
+blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cudaStream_t st);
+
+// FastBConv / ModUp / ModDown helpers
+// ModUp of n polynomials (c1_ntt[t]: [k][N], NTT, host array of device
+// pointers, n <= kMaxJobs) -> ext [n][beta][E][N] (contiguous, NTT), using
+// coef_scratch [n][k][N].
+constexpr int kMaxJobs = 32;
+blb_status launch_modup(const blb_params *P, int level, const u64 *const *c1_ntt, int n, u64 *ext,
+                        u64 *coef_scratch, cudaStream_t st);
+inline int blb_beta(const blb_params *P, int level) { return (level + 1 + P->alpha - 1) / P->alpha; }
+inline int blb_beta_top(const blb_params *P) { return (P->K + P->alpha - 1) / P->alpha; }
+inline size_t bconv_modup_off(const blb_params *P, int level, int digit) {
+    return P->bconv_off[(size_t)level * blb_beta_top(P) + digit];
+}
+inline size_t bconv_moddown_off(const blb_params *P, int level) {
+    return P->bconv_off[(size_t)P->K * blb_beta_top(P) + level];
+}
+struct KsJob {
+    const u64 *ext;   // [beta][E][N]
+    const u64 *key;   // [beta_top][2][K+np][N]
+    const u64 *c0;    // [k][N] input c0 (rotation: sigma_g(c0) is added), nullable (relin: add as is)
+    u64 *out;         // [2][k][N]
+    uint32_t galois;  // 1 = identity
+    int add_mode;     // 0 = none, 1 = add sigma_g(c0) to out0 (rotation), 2 = add c0 / c1 pair (relin)
+    const u64 *c1_add;
+};
+blb_status launch_keyswitch(const blb_params *P, int level, const KsJob *jobs, int n_jobs, u64 *u_scratch,
+                            u64 *conv_scratch, cudaStream_t st);
+size_t keyswitch_scratch_elems(const blb_params *P, int level, int n_jobs);  // u + conv, in u64
+
+blb_status launch_rescale(const blb_params *P, const u64 *in, int level, int n_polys, u64 *out, u64 *scratch,
+                          cudaStream_t st);
+blb_status launch_encode(const blb_params *P, const double *slots, int n_pts, double scale, int level, u64 *out,
+                         double *dd_scratch, int *d_flag, cudaStream_t st);
+size_t encode_scratch_doubles(const blb_params *P, int n_pts);
+
+// ChaCha / sampling
+enum { TAG_SECRET = 1, TAG_KEY_A = 2, TAG_KEY_E = 3, TAG_ENC_A = 4, TAG_ENC_E = 5, TAG_MASK = 6 };
+struct ChachaKey {
+    uint32_t k[8];
+};
+ChachaKey chacha_key_from_bytes(const uint8_t seed[32]);

@@ -1,0 +1,196 @@
+// encode.cu -- CKKS encode / decode on sm_100a (Eq. eq:ckks_encode; C3).
+//
+// Encode(z) = round(Delta * pi^{-1}(z)).  pi evaluates m(X) at the roots
+// zeta^{5^j} (slot j) and their conjugates; pi^{-1} is therefore the inverse
+// negacyclic transform with psi -> zeta = e^{i pi / N}: place z_j at the
+// "NTT-domain" position k with 2 brv(k) + 1 == 5^j (mod 2N) and its conjugate
+// at N - 1 - k, run the Gentleman-Sande network with zeta^{-brv(m+i)}
+// twiddles and divide by N.  All of it runs in double-double (~106-bit)
+// complex arithmetic so that the final rounding is correct (reading C3): a
+// plain double transform would mis-round ~1e5 coefficients per BERT layer.
+// Decode runs the Cooley-Tukey network (zeta^{brv(m+i)}) on the centred lift.
+// The transforms are radix-2 stage kernels over global memory: encode is the
+// offline weight precompute (row a0), timed separately from the hot path.
+#include "blb_internal.cuh"
+
+namespace {
+constexpr int kTB = 256;
+
+struct dd {
+    double hi, lo;
+};
+__device__ __forceinline__ dd two_sum(double a, double b) {
+    const double s = a + b;
+    const double bb = s - a;
+    return {s, (a - (s - bb)) + (b - bb)};
+}
+__device__ __forceinline__ dd quick_two_sum(double a, double b) {
+    const double s = a + b;
+    return {s, b - (s - a)};
+}
+__device__ __forceinline__ dd dd_add(dd x, dd y) {
+    dd s = two_sum(x.hi, y.hi);
+    const dd t = two_sum(x.lo, y.lo);
+    s.lo += t.hi;
+    s = quick_two_sum(s.hi, s.lo);
+    s.lo += t.lo;
+    return quick_two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ dd dd_neg(dd x) { return {-x.hi, -x.lo}; }
+__device__ __forceinline__ dd dd_sub(dd x, dd y) { return dd_add(x, dd_neg(y)); }
+__device__ __forceinline__ dd dd_mul(dd x, dd y) {
+    const double p = x.hi * y.hi;
+    double e = fma(x.hi, y.hi, -p);
+    e += x.hi * y.lo + x.lo * y.hi;
+    return quick_two_sum(p, e);
+}
+__device__ __forceinline__ dd dd_mul_d(dd x, double y) {
+    const double p = x.hi * y;
+    double e = fma(x.hi, y, -p);
+    e += x.lo * y;
+    return quick_two_sum(p, e);
+}
+struct cdd {
+    dd re, im;
+};
+__device__ __forceinline__ cdd cmul(cdd a, cdd b) {
+    return {dd_sub(dd_mul(a.re, b.re), dd_mul(a.im, b.im)), dd_add(dd_mul(a.re, b.im), dd_mul(a.im, b.re))};
+}
+__device__ __forceinline__ cdd cadd(cdd a, cdd b) { return {dd_add(a.re, b.re), dd_add(a.im, b.im)}; }
+__device__ __forceinline__ cdd csub(cdd a, cdd b) { return {dd_sub(a.re, b.re), dd_sub(a.im, b.im)}; }
+__device__ __forceinline__ cdd cld(const double *p) { return {{p[0], p[1]}, {p[2], p[3]}}; }
+__device__ __forceinline__ void cst(double *p, cdd v) {
+    p[0] = v.re.hi; p[1] = v.re.lo; p[2] = v.im.hi; p[3] = v.im.lo;
+}
+
+// buf[p][pos] = (z, 0), buf[p][N-1-pos] = (z, 0)
+__global__ void k_scatter(const double *slots, const int32_t *slot_pos, double *buf, int n_pts, int N) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int p = blockIdx.y;
+    const int n = N / 2;
+    if (j >= n) return;
+    const double z = slots[(long long)p * n + j];
+    const int pos = slot_pos[j];
+    double *b = buf + (long long)p * N * 4;
+    cst(b + 4ll * pos, {{z, 0.0}, {0.0, 0.0}});
+    cst(b + 4ll * (N - 1 - pos), {{z, 0.0}, {0.0, 0.0}});
+}
+
+// one Gentleman-Sande stage (inverse=1) or Cooley-Tukey stage (inverse=0), m blocks of 2t
+__global__ void k_stage(double *buf, const double *zeta, int m, int logN, int inverse) {
+    const int N = 1 << logN;
+    const int bidx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int p = blockIdx.y;
+    if (bidx >= N / 2) return;
+    const int t = N / (2 * m);
+    const int i = bidx / t, jj = bidx - i * t;
+    const int j = 2 * i * t + jj;
+    double *b = buf + (long long)p * N * 4;
+    cdd X = cld(b + 4ll * j), Y = cld(b + 4ll * (j + t));
+    cdd W = cld(zeta + 4ll * (m + i));
+    if (inverse) {
+        W.im = dd_neg(W.im);  // zeta^{-brv(m+i)} = conj(zeta^{brv(m+i)})
+        cst(b + 4ll * j, cadd(X, Y));
+        cst(b + 4ll * (j + t), cmul(csub(X, Y), W));
+    } else {
+        const cdd V = cmul(Y, W);
+        cst(b + 4ll * j, cadd(X, V));
+        cst(b + 4ll * (j + t), csub(X, V));
+    }
+}
+
+// coefficient k = round_half_even(Re(buf[k]) * scale / N), residues mod q_0..q_level
+__global__ void k_encode_finalize(const double *buf, u64 *out, Primes pr, double scale, int level, int logN,
+                                  int *flag) {
+    const int N = 1 << logN;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int p = blockIdx.y;
+    if (k >= N) return;
+    const double *b = buf + ((long long)p * N + k) * 4;
+    dd v = {b[0], b[1]};
+    v = dd_mul_d(v, scale);
+    v = {ldexp(v.hi, -logN), ldexp(v.lo, -logN)};  // exact division by N
+    if (!(fabs(v.hi) < 4503599627370496.0)) {     // 2^52
+        atomicExch(flag, 1);
+        return;
+    }
+    double r = rint(v.hi);
+    const double d = (v.hi - r) + v.lo;  // v.hi - r is exact
+    const bool odd = fmod(r, 2.0) != 0.0;
+    if (d > 0.5 || (d == 0.5 && odd)) r += 1.0;
+    else if (d < -0.5 || (d == -0.5 && odd)) r -= 1.0;
+    const long long c = (long long)r;
+    const int k1 = level + 1;
+    for (int i = 0; i < k1; i++) {
+        const ModConst &mc = pr.m[i];
+        u64 res;
+        if (c >= 0) res = mod64((u64)c, mc);
+        else {
+            const u64 t = mod64((u64)(-c), mc);
+            res = t ? mc.q - t : 0;
+        }
+        out[((long long)p * k1 + i) * N + k] = res;
+    }
+}
+
+// centred lift of the q_0 residue -> double-double complex (imag 0)
+__global__ void k_decode_lift(const u64 *coef, double *buf, Primes pr, int N) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= N) return;
+    const u64 q = pr.m[0].q;
+    const u64 v = coef[k];
+    long long c = v > q / 2 ? -(long long)(q - v) : (long long)v;
+    const double hi = (double)c;
+    const double lo = (double)(c - (long long)hi);
+    cst(buf + 4ll * k, {{hi, lo}, {0.0, 0.0}});
+}
+
+__global__ void k_decode_extract(const double *buf, const int32_t *slot_pos, double *out, double inv_scale, int N) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N / 2) return;
+    const double *b = buf + 4ll * slot_pos[j];
+    out[j] = (b[0] + b[1]) * inv_scale;
+}
+
+__global__ void k_copy(const u64 *src, u64 *dst, int n) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x < n) dst[x] = src[x];
+}
+}  // namespace
+
+size_t encode_scratch_doubles(const blb_params *P, int n_pts) { return (size_t)n_pts * P->N * 4; }
+
+blb_status launch_encode(const blb_params *P, const double *slots, int n_pts, double scale, int level, u64 *out,
+                         double *buf, int *d_flag, cudaStream_t st) {
+    const int N = P->N, logN = P->logN;
+    if (n_pts <= 0) return BLB_OK;
+    dim3 gs((N / 2 + kTB - 1) / kTB, n_pts);
+    k_scatter<<<gs, kTB, 0, st>>>(slots, P->d_slot_pos, buf, n_pts, N);
+    for (int m = N / 2; m >= 1; m >>= 1) k_stage<<<gs, kTB, 0, st>>>(buf, P->d_zeta, m, logN, 1);
+    k_encode_finalize<<<dim3((N + kTB - 1) / kTB, n_pts), kTB, 0, st>>>(buf, out, P->pr, scale, level, logN, d_flag);
+    BLB_COUNT_LAUNCH(2 + logN);
+    BLB_CHECK_LAUNCH();
+    RowBatch rb{};
+    rb.base = out; rb.poly_stride = (long long)(level + 1) * N; rb.n_polys = n_pts; rb.limbs = level + 1; rb.limb0 = 0;
+    for (int i = 0; i <= level; i++) rb.prime[i] = i;
+    return launch_ntt(P, rb, false, st);
+}
+
+// decode: scratch = N u64 + 4N doubles
+blb_status launch_decode(const blb_params *P, const u64 *pt, double scale, double *slots_out, void *scratch,
+                         cudaStream_t st) {
+    const int N = P->N, logN = P->logN;
+    u64 *coef = (u64 *)scratch;
+    double *buf = (double *)(coef + N);
+    k_copy<<<(N + kTB - 1) / kTB, kTB, 0, st>>>(pt, coef, N);
+    RowBatch rb{};
+    rb.base = coef; rb.poly_stride = N; rb.n_polys = 1; rb.limbs = 1; rb.limb0 = 0; rb.prime[0] = 0;
+    BLB_TRY(launch_ntt(P, rb, true, st));
+    k_decode_lift<<<(N + kTB - 1) / kTB, kTB, 0, st>>>(coef, buf, P->pr, N);
+    dim3 gs((N / 2 + kTB - 1) / kTB, 1);
+    for (int m = 1; m < N; m <<= 1) k_stage<<<gs, kTB, 0, st>>>(buf, P->d_zeta, m, logN, 0);
+    k_decode_extract<<<(N / 2 + kTB - 1) / kTB, kTB, 0, st>>>(buf, P->d_slot_pos, slots_out, 1.0 / scale, N);
+    BLB_COUNT_LAUNCH(3 + logN);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}

@@ -1,0 +1,525 @@
+// kernels.cu -- RNS pointwise kernels of the B200 BLB library:
+//   ChaCha20 samplers (C4), key generation (C5), encrypt / decrypt (C6),
+//   FastBConv ModUp / ModDown and the key-switch inner product with the
+//   NTT-domain automorphism folded into its loads (C7, C8; rows a2 / a4),
+//   rescale (C10; row a5) and the CKKS->MPC mask (C14; row a8).
+// All kernels are coefficient-parallel: thread x handles residue x of a row,
+// so every global access is coalesced along the limb-major layout.
+#include "blb_internal.cuh"
+
+namespace {
+constexpr int kTB = 256;
+
+// ---------------------------------------------------------------- ChaCha20
+__device__ __forceinline__ uint32_t rotl32(uint32_t x, int r) { return __funnelshift_l(x, x, r); }
+#define QR(a, b, c, d)                                                      \
+    a += b; d ^= a; d = rotl32(d, 16); c += d; b ^= c; b = rotl32(b, 12); \
+    a += b; d ^= a; d = rotl32(d, 8);  c += d; b ^= c; b = rotl32(b, 7);
+
+__device__ __forceinline__ void chacha_block(const ChachaKey &key, uint32_t counter, uint32_t n0, uint32_t n1,
+                                             uint32_t n2, uint32_t o[16]) {
+    uint32_t s[16] = {0x61707865u, 0x3320646eu, 0x79622d32u, 0x6b206574u, key.k[0], key.k[1], key.k[2], key.k[3],
+                      key.k[4],    key.k[5],    key.k[6],    key.k[7],    counter,  n0,       n1,       n2};
+#pragma unroll
+    for (int i = 0; i < 16; i++) o[i] = s[i];
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        QR(o[0], o[4], o[8], o[12]); QR(o[1], o[5], o[9], o[13]);
+        QR(o[2], o[6], o[10], o[14]); QR(o[3], o[7], o[11], o[15]);
+        QR(o[0], o[5], o[10], o[15]); QR(o[1], o[6], o[11], o[12]);
+        QR(o[2], o[7], o[8], o[13]); QR(o[3], o[4], o[9], o[14]);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; i++) o[i] += s[i];
+}
+// C4 layout: nonce = LE32(tag) || LE64(objid); block b = coefficients 4b..4b+3,
+// draw d = (w_{2d}, w_{2d+1}) with w_i the little-endian u64 words.
+__device__ __forceinline__ void draw_block(const ChachaKey &key, uint32_t tag, u64 objid, uint32_t blk, u64 lo[4],
+                                           u64 hi[4]) {
+    uint32_t o[16];
+    chacha_block(key, blk, tag, (uint32_t)objid, (uint32_t)(objid >> 32), o);
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        lo[d] = (u64)o[4 * d] | ((u64)o[4 * d + 1] << 32);
+        hi[d] = (u64)o[4 * d + 2] | ((u64)o[4 * d + 3] << 32);
+    }
+}
+
+struct LimbList {
+    int n;
+    int prime[BLB_MAXP];   // modulus index per row
+    int nonce[BLB_MAXP];   // limb index entering the ChaCha object id
+};
+
+// uniform mod q rows (NTT-domain "a" polynomials): out[r][x], objid = (id << 8) | nonce[r]
+__global__ void k_sample_uniform(u64 *out, long long row_stride, LimbList ll, Primes pr, ChachaKey key, uint32_t tag,
+                                 u64 id, int N) {
+    const int blk = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.y;
+    if (blk >= N / 4) return;
+    u64 lo[4], hi[4];
+    draw_block(key, tag, (id << 8) | (u64)ll.nonce[r], blk, lo, hi);
+    const ModConst &mc = pr.m[ll.prime[r]];
+    u64 *o = out + r * row_stride;
+#pragma unroll
+    for (int d = 0; d < 4; d++) o[4 * blk + d] = reduce128(hi[d], lo[d], mc);
+}
+
+// small coefficient polynomial (ternary secret: mode 0; CBD eta=21: mode 1)
+// from draws with objid = id << 8, written as residues into every listed row
+__global__ void k_sample_small(u64 *out, long long row_stride, LimbList ll, Primes pr, ChachaKey key, uint32_t tag,
+                               u64 id, int mode, int N) {
+    const int blk = blockIdx.x * blockDim.x + threadIdx.x;
+    if (blk >= N / 4) return;
+    u64 lo[4], hi[4];
+    draw_block(key, tag, id << 8, blk, lo, hi);
+    long long v[4];
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        if (mode == 0) v[d] = (long long)(lo[d] % 3ull) - 1;
+        else {
+            const u64 m = (1ull << 21) - 1;
+            v[d] = (long long)__popcll(lo[d] & m) - (long long)__popcll((lo[d] >> 21) & m);
+        }
+    }
+    for (int r = 0; r < ll.n; r++) {
+        const u64 q = pr.m[ll.prime[r]].q;
+        u64 *o = out + r * row_stride;
+#pragma unroll
+        for (int d = 0; d < 4; d++) o[4 * blk + d] = v[d] >= 0 ? (u64)v[d] : q - (u64)(-v[d]);
+    }
+}
+
+// switching key rows: b = e - a*s + gadget*s'   (s' = sigma_g(s) or s^2)
+__global__ void k_keygen_combine(u64 *b, const u64 *a, const u64 *s, long long stride, LimbList ll, Primes pr,
+                                 uint32_t galois, int relin, const u64 *gadget, int logN) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.y;
+    const int N = 1 << logN;
+    if (x >= N) return;
+    const int pi = ll.prime[r];
+    const ModConst &mc = pr.m[pi];
+    const u64 *sr = s + (long long)pi * N;
+    const u64 sx = sr[x];
+    const u64 as = mulmod(a[r * stride + x], sx, mc);
+    u64 v = submod(b[r * stride + x], as, mc.q);
+    const u64 g = gadget[pi];
+    if (g) {
+        u64 sp = relin ? mulmod(sx, sx, mc) : sr[galois_perm(x, galois, logN)];
+        v = addmod(v, mulmod(g, sp, mc), mc.q);
+    }
+    b[r * stride + x] = v;
+}
+
+// c0 = e - a*s + pt  (c0 holds NTT(e) on entry)
+__global__ void k_encrypt_combine(u64 *c0, const u64 *c1, const u64 *s, const u64 *pt, Primes pr, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y;
+    if (x >= N) return;
+    const ModConst &mc = pr.m[i];
+    const long long o = (long long)i * N + x;
+    u64 v = submod(c0[o], mulmod(c1[o], s[o], mc), mc.q);
+    c0[o] = addmod(v, pt[o], mc.q);
+}
+
+__global__ void k_decrypt(const u64 *c0, const u64 *c1, const u64 *s, u64 *out, Primes pr, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y;
+    if (x >= N) return;
+    const ModConst &mc = pr.m[i];
+    const long long o = (long long)i * N + x;
+    out[o] = addmod(c0[o], mulmod(c1[o], s[o], mc), mc.q);
+}
+
+__global__ void k_mul_pt(const u64 *in, const u64 *pt, u64 *out, Primes pr, int k, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y, p = blockIdx.z;
+    if (x >= N) return;
+    const ModConst &mc = pr.m[i];
+    const long long o = ((long long)p * k + i) * N + x;
+    out[o] = mulmod(in[o], pt[(long long)i * N + x], mc);
+}
+
+__global__ void k_add(const u64 *a, const u64 *b, u64 *out, Primes pr, int k, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y, p = blockIdx.z;
+    if (x >= N) return;
+    const long long o = ((long long)p * k + i) * N + x;
+    out[o] = addmod(a[o], b[o], pr.m[i].q);
+}
+
+// ------------------------------------------------------------ ModUp (C7)
+struct PtrList {
+    const u64 *p[kMaxJobs];
+};
+
+// coef[t][i][x] = c1[t][i][x] for i < k (copy before the INTT)
+__global__ void k_gather_rows(PtrList src, u64 *dst, int k, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y, t = blockIdx.z;
+    if (x >= N) return;
+    dst[((long long)t * k + i) * N + x] = src.p[t][(long long)i * N + x];
+}
+
+// ext[t][j][m][x]: digit j's own limbs copy the NTT-domain input; the others are
+// FastBConv_{D_j -> m}(coef) = sum_i [coef_i * dhat_i^{-1}]_{d_i} * dhat_i  mod m.
+// Table at tab + bconv_modup_off(level, j): inv[nd], inv_sh[nd], chat[nd][E].
+struct Offs {
+    long long o[BLB_MAXP];
+};
+__global__ void k_bconv_modup(PtrList c1_ntt, const u64 *coef, u64 *ext, const u64 *tab, Offs tab_off, Primes pr,
+                              int k, int np, int K, int alpha, int beta, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int m = blockIdx.y;               // ext limb
+    const int t = blockIdx.z / beta, j = blockIdx.z % beta;
+    if (x >= N) return;
+    const int E = k + np;
+    const int lo = j * alpha, hi = min((j + 1) * alpha, k), nd = hi - lo;
+    u64 *o = ext + (((long long)t * beta + j) * E + m) * N + x;
+    if (m >= lo && m < hi) {
+        *o = c1_ntt.p[t][(long long)m * N + x];
+        return;
+    }
+    const int pm = m < k ? m : K + (m - k);
+    const ModConst &mc = pr.m[pm];
+    const u64 *tb = tab + tab_off.o[j];
+    Acc128 acc;
+    acc.zero();
+    for (int d = 0; d < nd; d++) {
+        const int pi = lo + d;
+        const u64 v = coef[((long long)t * k + pi) * N + x];
+        const u64 y = shoup(v, tb[d], tb[nd + d], pr.m[pi].q);
+        acc.mac(y, tb[2 * nd + d * E + m]);
+    }
+    *o = acc.reduce(mc);
+}
+
+// ------------------------------------------------------- key switch (C7, C8)
+struct KsJobs {
+    KsJob j[kMaxJobs];
+};
+
+// u[t][b][m][x] = sum_j sigma_g(ext_j)[m][x] * key_j[b][pm][x]
+__global__ void k_ks_inner(KsJobs jobs, u64 *u, Primes pr, int k, int np, int K, int beta, int logN) {
+    const int N = 1 << logN;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int m = blockIdx.y, t = blockIdx.z;
+    if (x >= N) return;
+    const KsJob &J = jobs.j[t];
+    const int E = k + np, Lk = K + np;
+    const int pm = m < k ? m : K + (m - k);
+    const uint32_t src = J.galois == 1 ? (uint32_t)x : galois_perm(x, J.galois, logN);
+    Acc128 a0, a1;
+    a0.zero();
+    a1.zero();
+    for (int j = 0; j < beta; j++) {
+        const u64 e = J.ext[((long long)j * E + m) * N + src];
+        a0.mac(e, J.key[(((long long)j * 2 + 0) * Lk + pm) * N + x]);
+        a1.mac(e, J.key[(((long long)j * 2 + 1) * Lk + pm) * N + x]);
+    }
+    const ModConst &mc = pr.m[pm];
+    u[(((long long)t * 2 + 0) * E + m) * N + x] = a0.reduce(mc);
+    u[(((long long)t * 2 + 1) * E + m) * N + x] = a1.reduce(mc);
+}
+
+// conv[t][b][i][x] = FastBConv_{P -> q_i}(INTT(u_P))   (u P-rows already INTT'd)
+__global__ void k_bconv_moddown(const u64 *u, u64 *conv, const u64 *tb, Primes pr, int k, int np, int K, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y, tb2 = blockIdx.z;  // tb2 = t*2 + b
+    if (x >= N) return;
+    const int E = k + np;
+    Acc128 acc;
+    acc.zero();
+    for (int d = 0; d < np; d++) {
+        const u64 v = u[((long long)tb2 * E + k + d) * N + x];
+        const u64 y = shoup(v, tb[d], tb[np + d], pr.m[K + d].q);
+        acc.mac(y, tb[2 * np + d * k + i]);
+    }
+    conv[((long long)tb2 * k + i) * N + x] = acc.reduce(pr.m[i]);
+}
+
+struct PinvTab {
+    u64 v[BLB_MAXP], sh[BLB_MAXP];
+};
+
+// out = (u_Q - conv) * P^{-1}  (+ sigma_g(c0) on poly 0 for rotations, + (c0, c1) for relin)
+__global__ void k_ks_combine(KsJobs jobs, const u64 *u, const u64 *conv, PinvTab pinv, Primes pr, int k, int np,
+                             int logN) {
+    const int N = 1 << logN;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y;
+    const int t = blockIdx.z >> 1, b = blockIdx.z & 1;
+    if (x >= N) return;
+    const KsJob &J = jobs.j[t];
+    const int E = k + np;
+    const u64 q = pr.m[i].q;
+    const u64 uv = u[(((long long)t * 2 + b) * E + i) * N + x];
+    const u64 cv = conv[(((long long)t * 2 + b) * k + i) * N + x];
+    u64 r = shoup(uv + q - cv, pinv.v[i], pinv.sh[i], q);
+    if (J.add_mode == 1 && b == 0) {
+        const uint32_t src = J.galois == 1 ? (uint32_t)x : galois_perm(x, J.galois, logN);
+        r = addmod(r, J.c0[(long long)i * N + src], q);
+    } else if (J.add_mode == 2) {
+        const u64 *c = b == 0 ? J.c0 : J.c1_add;
+        r = addmod(r, c[(long long)i * N + x], q);
+    }
+    J.out[((long long)b * k + i) * N + x] = r;
+}
+
+// ------------------------------------------------------------- rescale (C10)
+// last[p][x] = in[p][level][x]
+__global__ void k_copy_limb(const u64 *in, u64 *out, int k, int limb, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int p = blockIdx.y;
+    if (x >= N) return;
+    out[(long long)p * N + x] = in[((long long)p * k + limb) * N + x];
+}
+// r[p][i][x] = centred(last[p][x]) mod q_i, i < level
+__global__ void k_rescale_lift(const u64 *last, u64 *r, Primes pr, int level, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y, p = blockIdx.z;
+    if (x >= N) return;
+    const u64 ql = pr.m[level].q;
+    const u64 v = last[(long long)p * N + x];
+    const ModConst &mc = pr.m[i];
+    u64 out;
+    if (v <= (ql - 1) / 2) out = mod64(v, mc);
+    else {
+        const u64 neg = mod64(ql - v, mc);
+        out = neg ? mc.q - neg : 0;
+    }
+    r[((long long)p * level + i) * N + x] = out;
+}
+// out[p][i][x] = (in[p][i][x] - r) * q_l^{-1} mod q_i
+__global__ void k_rescale_combine(const u64 *in, const u64 *r, u64 *out, PinvTab qlinv, Primes pr, int level, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y, p = blockIdx.z;
+    if (x >= N) return;
+    const u64 q = pr.m[i].q;
+    const u64 a = in[((long long)p * (level + 1) + i) * N + x];
+    const u64 b = r[((long long)p * level + i) * N + x];
+    out[((long long)p * level + i) * N + x] = shoup(a + q - b, qlinv.v[i], qlinv.sh[i], q);
+}
+
+// ---------------------------------------------------------------- mask (C14)
+// masked[t][0] += r, share[t] = -r mod q0 with r = ChaCha(MASK, (id0 + t) << 8) mod q0
+__global__ void k_mask(u64 *masked, u64 *share, Primes pr, ChachaKey key, u64 id0, int N) {
+    const int blk = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.y;
+    if (blk >= N / 4) return;
+    u64 lo[4], hi[4];
+    draw_block(key, TAG_MASK, (id0 + (u64)t) << 8, blk, lo, hi);
+    const ModConst &mc = pr.m[0];
+    u64 *m0 = masked + (long long)t * 2 * N;
+    u64 *sh = share + (long long)t * N;
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        const u64 r = reduce128(hi[d], lo[d], mc);
+        const int x = 4 * blk + d;
+        m0[x] = addmod(m0[x], r, mc.q);
+        sh[x] = r ? mc.q - r : 0;
+    }
+}
+// masked[t][b][x] = in_t[b][0][x]   (drop to q_0)
+__global__ void k_drop_q0(PtrList in, u64 *masked, int k, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.y, b = blockIdx.z;
+    if (x >= N) return;
+    masked[((long long)t * 2 + b) * N + x] = in.p[t][(long long)b * k * N + x];
+}
+
+inline dim3 grid_x(int N, int y = 1, int z = 1) { return dim3((N + kTB - 1) / kTB, y, z); }
+}  // namespace
+
+// ============================================================ launchers
+
+ChachaKey chacha_key_from_bytes(const uint8_t seed[32]) {
+    ChachaKey k;
+    for (int i = 0; i < 8; i++)
+        k.k[i] = (uint32_t)seed[4 * i] | ((uint32_t)seed[4 * i + 1] << 8) | ((uint32_t)seed[4 * i + 2] << 16) |
+                 ((uint32_t)seed[4 * i + 3] << 24);
+    return k;
+}
+
+blb_status launch_modup(const blb_params *P, int level, const u64 *const *c1_ntt, int n, u64 *ext, u64 *coef,
+                        cudaStream_t st) {
+    if (n <= 0) return BLB_OK;
+    if (n > kMaxJobs) {
+        blb_set_error("launch_modup: n > %d", kMaxJobs);
+        return BLB_E_INVALID_ARG;
+    }
+    const int N = P->N, k = level + 1, E = k + P->np, beta = blb_beta(P, level);
+    PtrList src{};
+    for (int t = 0; t < n; t++) src.p[t] = c1_ntt[t];
+    k_gather_rows<<<grid_x(N, k, n), kTB, 0, st>>>(src, coef, k, N);
+    BLB_COUNT_LAUNCH(1);
+    RowBatch rb{};
+    rb.base = coef; rb.poly_stride = (long long)k * N; rb.n_polys = n; rb.limbs = k; rb.limb0 = 0;
+    for (int i = 0; i < k; i++) rb.prime[i] = i;
+    BLB_TRY(launch_ntt(P, rb, true, st));
+    Offs offs{};
+    for (int j = 0; j < beta; j++) offs.o[j] = (long long)bconv_modup_off(P, level, j);
+    k_bconv_modup<<<grid_x(N, E, n * beta), kTB, 0, st>>>(src, coef, ext, P->d_bconv, offs, P->pr, k, P->np, P->K,
+                                                          P->alpha, beta, N);
+    BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    RowBatch eb{};
+    eb.base = ext; eb.poly_stride = (long long)E * N; eb.n_polys = n * beta; eb.limbs = E; eb.limb0 = 0;
+    for (int m = 0; m < E; m++) eb.prime[m] = m < k ? m : P->K + (m - k);
+    eb.skip_alpha = P->alpha; eb.skip_beta = beta; eb.skip_kmax = k;
+    return launch_ntt(P, eb, false, st);
+}
+
+size_t keyswitch_scratch_elems(const blb_params *P, int level, int n_jobs) {
+    const int k = level + 1, E = k + P->np;
+    return (size_t)n_jobs * 2 * ((size_t)E + k) * P->N;
+}
+
+blb_status launch_keyswitch(const blb_params *P, int level, const KsJob *jobs, int n, u64 *u, u64 *conv,
+                            cudaStream_t st) {
+    if (n <= 0) return BLB_OK;
+    if (n > kMaxJobs) {
+        blb_set_error("launch_keyswitch: n > %d", kMaxJobs);
+        return BLB_E_INVALID_ARG;
+    }
+    const int N = P->N, k = level + 1, np = P->np, E = k + np, beta = blb_beta(P, level);
+    KsJobs J{};
+    for (int t = 0; t < n; t++) J.j[t] = jobs[t];
+    k_ks_inner<<<grid_x(N, E, n), kTB, 0, st>>>(J, u, P->pr, k, np, P->K, beta, P->logN);
+    BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    RowBatch rb{};
+    rb.base = u; rb.poly_stride = (long long)E * N; rb.n_polys = 2 * n; rb.limbs = np; rb.limb0 = k;
+    for (int d = 0; d < np; d++) rb.prime[d] = P->K + d;
+    BLB_TRY(launch_ntt(P, rb, true, st));
+    k_bconv_moddown<<<grid_x(N, k, 2 * n), kTB, 0, st>>>(u, conv, P->d_bconv + bconv_moddown_off(P, level), P->pr, k,
+                                                         np, P->K, N);
+    BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    RowBatch cb{};
+    cb.base = conv; cb.poly_stride = (long long)k * N; cb.n_polys = 2 * n; cb.limbs = k; cb.limb0 = 0;
+    for (int i = 0; i < k; i++) cb.prime[i] = i;
+    BLB_TRY(launch_ntt(P, cb, false, st));
+    PinvTab pt{};
+    for (int i = 0; i < k; i++) { pt.v[i] = P->Pinv[i]; pt.sh[i] = P->Pinv_sh[i]; }
+    k_ks_combine<<<grid_x(N, k, 2 * n), kTB, 0, st>>>(J, u, conv, pt, P->pr, k, np, P->logN);
+    BLB_COUNT_LAUNCH(1);
+    BLB_COUNT(1, n);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+
+extern "C" u64 blbh_shoup(u64 w, u64 q);
+extern "C" u64 blbh_invmod(u64 a, u64 q);
+
+blb_status launch_rescale(const blb_params *P, const u64 *in, int level, int n_polys, u64 *out, u64 *scratch,
+                          cudaStream_t st) {
+    const int N = P->N, k = level + 1;
+    u64 *last = scratch, *r = scratch + (size_t)n_polys * N;
+    k_copy_limb<<<grid_x(N, n_polys), kTB, 0, st>>>(in, last, k, level, N);
+    BLB_COUNT_LAUNCH(1);
+    RowBatch lb{};
+    lb.base = last; lb.poly_stride = N; lb.n_polys = n_polys; lb.limbs = 1; lb.limb0 = 0; lb.prime[0] = level;
+    BLB_TRY(launch_ntt(P, lb, true, st));
+    k_rescale_lift<<<grid_x(N, level, n_polys), kTB, 0, st>>>(last, r, P->pr, level, N);
+    BLB_COUNT_LAUNCH(1);
+    RowBatch rb{};
+    rb.base = r; rb.poly_stride = (long long)level * N; rb.n_polys = n_polys; rb.limbs = level; rb.limb0 = 0;
+    for (int i = 0; i < level; i++) rb.prime[i] = i;
+    BLB_TRY(launch_ntt(P, rb, false, st));
+    PinvTab qi{};
+    const u64 ql = P->mod[level];
+    for (int i = 0; i < level; i++) {
+        qi.v[i] = blbh_invmod(ql % P->mod[i], P->mod[i]);
+        qi.sh[i] = blbh_shoup(qi.v[i], P->mod[i]);
+    }
+    k_rescale_combine<<<grid_x(N, level, n_polys), kTB, 0, st>>>(in, r, out, qi, P->pr, level, N);
+    BLB_COUNT_LAUNCH(1);
+    BLB_COUNT(4, n_polys / 2);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+
+// ------------------------------------------------ exported through api.cu
+blb_status blb_launch_sample_uniform(const blb_params *P, u64 *out, long long row_stride, int n_rows,
+                                     const int *prime, const int *nonce, const uint8_t seed[32], uint32_t tag, u64 id,
+                                     cudaStream_t st) {
+    LimbList ll{};
+    ll.n = n_rows;
+    for (int r = 0; r < n_rows; r++) { ll.prime[r] = prime[r]; ll.nonce[r] = nonce[r]; }
+    k_sample_uniform<<<dim3((P->N / 4 + kTB - 1) / kTB, n_rows), kTB, 0, st>>>(out, row_stride, ll, P->pr,
+                                                                              chacha_key_from_bytes(seed), tag, id, P->N);
+    BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+blb_status blb_launch_sample_small(const blb_params *P, u64 *out, long long row_stride, int n_rows, const int *prime,
+                                   const uint8_t seed[32], uint32_t tag, u64 id, int mode, cudaStream_t st) {
+    LimbList ll{};
+    ll.n = n_rows;
+    for (int r = 0; r < n_rows; r++) ll.prime[r] = prime[r];
+    k_sample_small<<<(P->N / 4 + kTB - 1) / kTB, kTB, 0, st>>>(out, row_stride, ll, P->pr, chacha_key_from_bytes(seed),
+                                                               tag, id, mode, P->N);
+    BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+blb_status blb_launch_keygen_combine(const blb_params *P, u64 *b, const u64 *a, const u64 *s, long long stride,
+                                     int n_rows, const int *prime, uint32_t galois, int relin, const u64 *gadget_dev,
+                                     cudaStream_t st) {
+    LimbList ll{};
+    ll.n = n_rows;
+    for (int r = 0; r < n_rows; r++) ll.prime[r] = prime[r];
+    k_keygen_combine<<<grid_x(P->N, n_rows), kTB, 0, st>>>(b, a, s, stride, ll, P->pr, galois, relin, gadget_dev,
+                                                           P->logN);
+    BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+blb_status blb_launch_encrypt_combine(const blb_params *P, u64 *c0, const u64 *c1, const u64 *s, const u64 *pt, int k,
+                                      cudaStream_t st) {
+    k_encrypt_combine<<<grid_x(P->N, k), kTB, 0, st>>>(c0, c1, s, pt, P->pr, P->N);
+    BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+blb_status blb_launch_decrypt(const blb_params *P, const u64 *c0, const u64 *c1, const u64 *s, u64 *out, int k,
+                              cudaStream_t st) {
+    k_decrypt<<<grid_x(P->N, k), kTB, 0, st>>>(c0, c1, s, out, P->pr, P->N);
+    BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+blb_status blb_launch_mul_pt(const blb_params *P, const u64 *in, const u64 *pt, u64 *out, int k, cudaStream_t st) {
+    k_mul_pt<<<grid_x(P->N, k, 2), kTB, 0, st>>>(in, pt, out, P->pr, k, P->N);
+    BLB_COUNT_LAUNCH(1);
+    BLB_COUNT(3, 1);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+blb_status blb_launch_add(const blb_params *P, const u64 *a, const u64 *b, u64 *out, int k, int npoly,
+                          cudaStream_t st) {
+    k_add<<<grid_x(P->N, k, npoly), kTB, 0, st>>>(a, b, out, P->pr, k, P->N);
+    BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+blb_status blb_launch_mask(const blb_params *P, const u64 *const *in, int n, int level, const uint8_t key[32],
+                           u64 id0, u64 *masked, u64 *share, cudaStream_t st) {
+    const int N = P->N;
+    for (int t0 = 0; t0 < n; t0 += kMaxJobs) {
+        const int cnt = (n - t0) < kMaxJobs ? (n - t0) : kMaxJobs;
+        PtrList pl{};
+        for (int t = 0; t < cnt; t++) pl.p[t] = in[t0 + t];
+        k_drop_q0<<<grid_x(N, cnt, 2), kTB, 0, st>>>(pl, masked + (size_t)t0 * 2 * N, level + 1, N);
+        BLB_COUNT_LAUNCH(1);
+    }
+    RowBatch rb{};
+    rb.base = masked; rb.poly_stride = N; rb.n_polys = 2 * n; rb.limbs = 1; rb.limb0 = 0; rb.prime[0] = 0;
+    BLB_TRY(launch_ntt(P, rb, true, st));
+    k_mask<<<dim3((N / 4 + kTB - 1) / kTB, n), kTB, 0, st>>>(masked, share, P->pr, chacha_key_from_bytes(key), id0, N);
+    BLB_COUNT_LAUNCH(1);
+    BLB_COUNT(5, n);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}

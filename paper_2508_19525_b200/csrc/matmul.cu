@@ -1,0 +1,537 @@
+// matmul.cu -- the ct-pt MatMul protocol of BLB on sm_100a (rows a2-a6).
+//
+// C11 (spatial-first input, BOLT's protocol as referenced at P:361 / P:511 /
+// P:515) and C12 (diagonal input for W_O, App. C.2), both with
+// BSGS (App. C.1):
+//     Y_b' = sum_g Rot^{gBL}( sum_b sum_i P_{b,b',g,i} (.) Rot^{iL}(X_b) ),
+//     P_{b,b',g,i} = Rot^{-gBL}(Pi_{b,b',gB+i}),
+// Pi block tau = W[b c + (tau + t) mod c, b' c + tau] (C11) or the
+// "duplicated spatial-first" vector w[i] = W_O[h d_h + (i+d) mod d_h, col]
+// with (d, h) = divmod(b c + (tau+t) mod c, heads) (C12).
+//
+// Hot path of one call:
+//   1. ModUp of every input c1, once (hoisting, C8);
+//   2. all baby-step rotations of all inputs, batched 32 key switches per
+//      launch group (inner product with the automorphism as a load gather);
+//   3. the MAC: acc[b',g] = sum_{b,i} P (.) R[b][i], one launch, 128-bit lazy
+//      accumulation, plaintexts streamed from HBM exactly once, R re-read from
+//      L2 (the output index is the fastest grid dimension);
+//   4. giant-step key switches of acc[b', g >= 1] and the sum over g;
+//   5. one rescale per output.
+#include <algorithm>
+#include <map>
+#include "blb_internal.cuh"
+
+extern "C" u64 blbh_shoup(u64 w, u64 q);
+
+struct blb_matmul_plan {
+    const blb_params *P;
+    int L, n, c, w_rows, w_cols, nblk_in, D_out, n_in, n_out, B, G, level, packing, heads, dh;
+    std::vector<int32_t> col_map;                       // D_out entries, -1 = zero column
+    std::vector<int> ent_start;                         // CSR over (b', g): n_out*G + 1
+    std::vector<int> ent_b, ent_i;                      // entries in plan order
+    std::vector<std::vector<int>> baby;                 // per input: i >= 1 used
+    std::vector<std::vector<int>> giant;                // per output: g >= 1 used
+    std::vector<int32_t> rot_steps;
+    int *d_ent = nullptr;                               // device: (b * B + i) per entry
+    int *d_ent_start = nullptr;                         // device copy of ent_start
+    int32_t *d_col_map = nullptr;
+};
+
+namespace {
+constexpr int kTB = 256;
+
+// Build the slot vectors of entries [e0, e0 + cnt) (plan order) into slots[cnt][n].
+struct PlanDev {
+    int L, n, c, B, G, w_rows, w_cols, nblk_in, D_out, packing, heads, dh;
+};
+__global__ void k_build_slots(PlanDev pd, const int *ent_bi, const int *ent_o, int e0, const double *W,
+                              const int32_t *col_map, double *slots) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    const int e = blockIdx.y;
+    if (s >= pd.n) return;
+    const int bi = ent_bi[e0 + e];
+    const int b = bi / pd.B, i = bi % pd.B;
+    const int o = ent_o[e0 + e];  // b' * G + g
+    const int bp = o / pd.G, g = o % pd.G;
+    const int t = g * pd.B + i;
+    // P[s] = Pi[(s - gBL) mod n]
+    int sp = s - g * pd.B * pd.L;
+    sp %= pd.n;
+    if (sp < 0) sp += pd.n;
+    const int tau = sp / pd.L, row = sp - tau * pd.L;
+    const int r = b * pd.c + (tau + t) % pd.c;
+    const int col = bp * pd.c + tau;
+    double v = 0.0;
+    if (col < pd.D_out) {
+        if (pd.packing == BLB_PACK_SPATIAL) {
+            const int src = col_map[col];
+            if (r < pd.w_rows && src >= 0) v = W[(long long)r * pd.w_cols + src];
+        } else {
+            if (r < pd.nblk_in) {
+                const int d = r / pd.heads, h = r % pd.heads;
+                v = W[(long long)(h * pd.dh + (row + d) % pd.dh) * pd.w_cols + col];
+            }
+        }
+    }
+    slots[(long long)e * pd.n + s] = v;
+}
+
+// acc[o][p][l][x] = sum_{e in o} pt[e][l][x] * R[bi_e][p][l][x]   (o = local (b', g))
+// 1-D grid: bid = (l * n_tiles + tile) * n_o + o  -> the output index varies
+// fastest, so concurrent CTAs share the same R tile through L2.
+__global__ void __launch_bounds__(kTB) k_mac(const u64 *__restrict__ pt, const u64 *__restrict__ R,
+                                             u64 *__restrict__ acc, const int *__restrict__ ent_bi,
+                                             const int *__restrict__ ent_start, int o0, int e_base, int n_o, int k,
+                                             int logN, Primes pr) {
+    const int N = 1 << logN;
+    const int n_tiles = N / (2 * kTB);
+    int bid = blockIdx.x;
+    const int o = bid % n_o;
+    bid /= n_o;
+    const int tile = bid % n_tiles;
+    const int l = bid / n_tiles;
+    const int x = tile * 2 * kTB + 2 * threadIdx.x;
+    const long long kN = (long long)k * N;
+    const int e_lo = ent_start[o0 + o], e_hi = ent_start[o0 + o + 1];
+    Acc128 a00, a01, a10, a11;  // [poly][coefficient]
+    a00.zero(); a01.zero(); a10.zero(); a11.zero();
+    const long long lx = (long long)l * N + x;
+#pragma unroll 4
+    for (int e = e_lo; e < e_hi; e++) {
+        const int bi = ent_bi[e];
+        const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(pt + (long long)(e - e_base) * kN + lx);
+        const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(R + (long long)bi * 2 * kN + lx);
+        const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(R + ((long long)bi * 2 + 1) * kN + lx);
+        a00.mac(pv.x, r0.x); a01.mac(pv.y, r0.y);
+        a10.mac(pv.x, r1.x); a11.mac(pv.y, r1.y);
+    }
+    const ModConst &mc = pr.m[l];
+    u64 *out = acc + (long long)o * 2 * kN + lx;
+    *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00.reduce(mc), a01.reduce(mc));
+    *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(mc), a11.reduce(mc));
+}
+
+// dst[o] += src[j] for the jobs of one giant batch (sequential per thread: no races)
+struct AccJobs {
+    int n;
+    u64 *dst[kMaxJobs];
+    const u64 *src[kMaxJobs];
+};
+__global__ void k_accumulate(AccJobs jobs, Primes pr, int k, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int l = blockIdx.y, p = blockIdx.z;
+    if (x >= N) return;
+    const u64 q = pr.m[l].q;
+    const long long off = ((long long)p * k + l) * N + x;
+    for (int j = 0; j < jobs.n; j++) jobs.dst[j][off] = addmod(jobs.dst[j][off], jobs.src[j][off], q);
+}
+
+__global__ void k_copy_ct(const u64 *src, u64 *dst, long long n) {
+    const long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x < n) dst[x] = src[x];
+}
+}  // namespace
+
+// ------------------------------------------------------------------ plan
+static bool nz_entry(const blb_matmul_plan *pl, int b, int bp, int t) {
+    for (int tau = 0; tau < pl->c; tau++) {
+        const int r = b * pl->c + (tau + t) % pl->c;
+        const int col = bp * pl->c + tau;
+        if (col >= pl->D_out) continue;
+        if (pl->packing == BLB_PACK_SPATIAL) {
+            if (r < pl->w_rows && pl->col_map[col] >= 0) return true;
+        } else {
+            if (r < pl->nblk_in) return true;
+        }
+    }
+    return false;
+}
+
+extern "C" blb_status blb_matmul_plan_create(const blb_params *P, int L, int w_rows, int w_cols, blb_packing packing,
+                                             int heads, const int32_t *col_map, int D_out, int bsgs_B, int level,
+                                             blb_matmul_plan **out) {
+    if (!P || !out || L <= 0 || w_rows <= 0 || w_cols <= 0 || bsgs_B <= 0) {
+        blb_set_error("blb_matmul_plan_create: invalid argument");
+        return BLB_E_INVALID_ARG;
+    }
+    const int n = P->N / 2;
+    if (n % L) {
+        blb_set_error("blb_matmul_plan_create: L=%d must divide N/2=%d", L, n);
+        return BLB_E_LAYOUT;
+    }
+    if (level < 1 || level >= P->K) {
+        blb_set_error("blb_matmul_plan_create: level %d must be in [1, %d) (one rescale)", level, P->K);
+        return BLB_E_LEVEL;
+    }
+    auto *pl = new blb_matmul_plan();
+    pl->P = P; pl->L = L; pl->n = n; pl->c = n / L; pl->w_rows = w_rows; pl->w_cols = w_cols;
+    pl->packing = packing; pl->level = level; pl->heads = heads > 0 ? heads : 1;
+    pl->B = std::min(bsgs_B, pl->c);
+    pl->G = (pl->c + pl->B - 1) / pl->B;
+    if (packing == BLB_PACK_SPATIAL) {
+        if (col_map) {
+            pl->D_out = D_out;
+            pl->col_map.assign(col_map, col_map + D_out);
+            for (int v : pl->col_map)
+                if (v >= w_cols) {
+                    delete pl;
+                    blb_set_error("col_map entry %d >= w_cols %d", v, w_cols);
+                    return BLB_E_LAYOUT;
+                }
+        } else {
+            pl->D_out = w_cols;
+            pl->col_map.resize(w_cols);
+            for (int i = 0; i < w_cols; i++) pl->col_map[i] = i;
+        }
+        pl->nblk_in = w_rows;
+        pl->dh = 0;
+    } else if (packing == BLB_PACK_DIAGONAL) {
+        if (w_rows % pl->heads) {
+            delete pl;
+            blb_set_error("diagonal packing: w_rows %d not divisible by heads %d", w_rows, pl->heads);
+            return BLB_E_LAYOUT;
+        }
+        pl->dh = w_rows / pl->heads;
+        pl->nblk_in = w_rows;
+        pl->D_out = w_cols;
+        pl->col_map.resize(w_cols);
+        for (int i = 0; i < w_cols; i++) pl->col_map[i] = i;
+    } else {
+        delete pl;
+        blb_set_error("unknown packing");
+        return BLB_E_LAYOUT;
+    }
+    pl->n_in = (pl->nblk_in + pl->c - 1) / pl->c;
+    pl->n_out = (pl->D_out + pl->c - 1) / pl->c;
+    pl->baby.assign(pl->n_in, {});
+    pl->giant.assign(pl->n_out, {});
+    pl->ent_start.push_back(0);
+    std::vector<int> ent_o;
+    std::vector<std::vector<char>> baby_used(pl->n_in, std::vector<char>(pl->B, 0));
+    for (int bp = 0; bp < pl->n_out; bp++) {
+        for (int g = 0; g < pl->G; g++) {
+            int cnt = 0;
+            for (int b = 0; b < pl->n_in; b++)
+                for (int i = 0; i < pl->B; i++) {
+                    const int t = g * pl->B + i;
+                    if (t >= pl->c) continue;
+                    if (!nz_entry(pl, b, bp, t)) continue;
+                    pl->ent_b.push_back(b);
+                    pl->ent_i.push_back(i);
+                    ent_o.push_back(bp * pl->G + g);
+                    baby_used[b][i] = 1;
+                    cnt++;
+                }
+            if (cnt && g > 0) pl->giant[bp].push_back(g);
+            pl->ent_start.push_back((int)pl->ent_b.size());
+        }
+    }
+    // 128-bit lazy MAC bound: (#entries per output) * (q_max - 1)^2 < 2^127
+    {
+        u128 qmax = 0;
+        for (int i = 0; i <= level; i++) qmax = std::max<u128>(qmax, P->mod[i]);
+        const u128 lim = (~(u128)0 >> 1) / ((qmax - 1) * (qmax - 1));
+        for (size_t o = 0; o + 1 < pl->ent_start.size(); o++)
+            if ((u128)(pl->ent_start[o + 1] - pl->ent_start[o]) > lim) {
+                blb_set_error("plan has %d products per output, 128-bit lazy MAC allows %llu: lower bsgs_B",
+                              pl->ent_start[o + 1] - pl->ent_start[o], (unsigned long long)lim);
+                delete pl;
+                return BLB_E_LAYOUT;
+            }
+    }
+    std::map<int32_t, int> steps;
+    for (int b = 0; b < pl->n_in; b++)
+        for (int i = 1; i < pl->B; i++)
+            if (baby_used[b][i]) {
+                pl->baby[b].push_back(i);
+                steps[i * L] = 1;
+            }
+    for (int bp = 0; bp < pl->n_out; bp++)
+        for (int g : pl->giant[bp]) steps[g * pl->B * L] = 1;
+    for (auto &kv : steps) pl->rot_steps.push_back(kv.first);
+    // device copies
+    const size_t ne = pl->ent_b.size();
+    std::vector<int> bi(ne);
+    for (size_t e = 0; e < ne; e++) bi[e] = pl->ent_b[e] * pl->B + pl->ent_i[e];
+    cudaError_t err = cudaSuccess;
+    err = cudaMalloc(&pl->d_ent, sizeof(int) * (2 * ne + 1));
+    if (err == cudaSuccess) err = cudaMalloc(&pl->d_ent_start, sizeof(int) * pl->ent_start.size());
+    if (err == cudaSuccess) err = cudaMalloc(&pl->d_col_map, sizeof(int32_t) * (pl->col_map.size() + 1));
+    if (err == cudaSuccess && ne) err = cudaMemcpy(pl->d_ent, bi.data(), sizeof(int) * ne, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess && ne)
+        err = cudaMemcpy(pl->d_ent + ne, ent_o.data(), sizeof(int) * ne, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess)
+        err = cudaMemcpy(pl->d_ent_start, pl->ent_start.data(), sizeof(int) * pl->ent_start.size(),
+                         cudaMemcpyHostToDevice);
+    if (err == cudaSuccess)
+        err = cudaMemcpy(pl->d_col_map, pl->col_map.data(), sizeof(int32_t) * pl->col_map.size(),
+                         cudaMemcpyHostToDevice);
+    if (err != cudaSuccess) {
+        blb_set_error("plan upload: %s", cudaGetErrorString(err));
+        blb_matmul_plan_destroy(pl);
+        return BLB_E_CUDA;
+    }
+    *out = pl;
+    return BLB_OK;
+}
+
+extern "C" void blb_matmul_plan_destroy(blb_matmul_plan *pl) {
+    if (!pl) return;
+    cudaFree(pl->d_ent);
+    cudaFree(pl->d_ent_start);
+    cudaFree(pl->d_col_map);
+    delete pl;
+}
+
+extern "C" blb_status blb_matmul_plan_info(const blb_matmul_plan *pl, int *n_in, int *n_out, int *n_pt, int *n_baby,
+                                           int *n_giant, int *B, int *G) {
+    if (!pl) return BLB_E_INVALID_ARG;
+    int nb = 0, ng = 0;
+    for (auto &v : pl->baby) nb += (int)v.size();
+    for (auto &v : pl->giant) ng += (int)v.size();
+    if (n_in) *n_in = pl->n_in;
+    if (n_out) *n_out = pl->n_out;
+    if (n_pt) *n_pt = (int)pl->ent_b.size();
+    if (n_baby) *n_baby = nb;
+    if (n_giant) *n_giant = ng;
+    if (B) *B = pl->B;
+    if (G) *G = pl->G;
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_matmul_plan_rotations(const blb_matmul_plan *pl, int32_t *steps, int *n) {
+    if (!pl || !n) return BLB_E_INVALID_ARG;
+    const int need = (int)pl->rot_steps.size();
+    if (steps) {
+        if (*n < need) {
+            blb_set_error("rotation buffer too small (%d < %d)", *n, need);
+            return BLB_E_INVALID_ARG;
+        }
+        for (int i = 0; i < need; i++) steps[i] = pl->rot_steps[i];
+    }
+    *n = need;
+    return BLB_OK;
+}
+
+static blb_status check_slice(const blb_matmul_plan *pl, int out_first, int out_count) {
+    if (out_first < 0 || out_count < 0 || out_first + out_count > pl->n_out) {
+        blb_set_error("output slice [%d, %d) outside [0, %d)", out_first, out_first + out_count, pl->n_out);
+        return BLB_E_INVALID_ARG;
+    }
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_matmul_pt_count(const blb_matmul_plan *pl, int out_first, int out_count, int *n_pt) {
+    if (!pl || !n_pt) return BLB_E_INVALID_ARG;
+    BLB_TRY(check_slice(pl, out_first, out_count));
+    *n_pt = pl->ent_start[(out_first + out_count) * pl->G] - pl->ent_start[out_first * pl->G];
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_matmul_encode_weights(const blb_matmul_plan *pl, const double *W, int out_first,
+                                                int out_count, u64 *pt_dev, void *stream) {
+    if (!pl || !W || !pt_dev) return BLB_E_INVALID_ARG;
+    BLB_TRY(check_slice(pl, out_first, out_count));
+    const blb_params *P = pl->P;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int e0 = pl->ent_start[out_first * pl->G];
+    const int e1 = pl->ent_start[(out_first + out_count) * pl->G];
+    const int k = pl->level + 1;
+    const size_t ne_total = pl->ent_b.size();
+    double *dW = nullptr, *slots = nullptr, *buf = nullptr;
+    int *flag = nullptr;
+    const int chunk = 64;
+    BLB_CUDA_TRY(cudaMallocAsync(&dW, sizeof(double) * (size_t)pl->w_rows * pl->w_cols, st));
+    BLB_CUDA_TRY(cudaMemcpyAsync(dW, W, sizeof(double) * (size_t)pl->w_rows * pl->w_cols, cudaMemcpyHostToDevice, st));
+    BLB_CUDA_TRY(cudaMallocAsync(&slots, sizeof(double) * (size_t)chunk * pl->n, st));
+    BLB_CUDA_TRY(cudaMallocAsync(&buf, sizeof(double) * encode_scratch_doubles(P, chunk), st));
+    BLB_CUDA_TRY(cudaMallocAsync(&flag, sizeof(int), st));
+    BLB_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    PlanDev pd{pl->L, pl->n, pl->c, pl->B, pl->G, pl->w_rows, pl->w_cols, pl->nblk_in, pl->D_out, pl->packing,
+               pl->heads, pl->dh};
+    const double scale = (double)P->mod[pl->level];  // reading S6: plaintext scale = q_level
+    blb_status s = BLB_OK;
+    for (int e = e0; e < e1 && s == BLB_OK; e += chunk) {
+        const int cnt = std::min(chunk, e1 - e);
+        k_build_slots<<<dim3((pl->n + kTB - 1) / kTB, cnt), kTB, 0, st>>>(pd, pl->d_ent, pl->d_ent + ne_total, e, dW,
+                                                                         pl->d_col_map, slots);
+        BLB_COUNT_LAUNCH(1);
+        s = launch_encode(P, slots, cnt, scale, pl->level, pt_dev + (size_t)(e - e0) * k * P->N, buf, flag, st);
+    }
+    int h_flag = 0;
+    cudaMemcpyAsync(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(dW, st);
+    cudaFreeAsync(slots, st);
+    cudaFreeAsync(buf, st);
+    cudaFreeAsync(flag, st);
+    BLB_CUDA_TRY(cudaStreamSynchronize(st));
+    if (s != BLB_OK) return s;
+    if (h_flag) {
+        blb_set_error("encode overflow: |scale * m_k| >= 2^52");
+        return BLB_E_OVERFLOW;
+    }
+    return BLB_OK;
+}
+
+// workspace layout (u64 elements)
+struct MatmulWs {
+    size_t ext_in, coef, R, ks, acc, gext, rot, resc, total;
+};
+static MatmulWs matmul_ws(const blb_matmul_plan *pl, int out_count) {
+    const blb_params *P = pl->P;
+    const size_t N = P->N, k = pl->level + 1, E = k + P->np, beta = blb_beta(P, pl->level);
+    MatmulWs w{};
+    size_t o = 0;
+    w.ext_in = o; o += (size_t)pl->n_in * beta * E * N;
+    w.coef = o; o += (size_t)kMaxJobs * k * N;
+    w.R = o; o += (size_t)pl->n_in * pl->B * 2 * k * N;
+    w.ks = o; o += keyswitch_scratch_elems(P, pl->level, kMaxJobs);
+    w.acc = o; o += (size_t)out_count * pl->G * 2 * k * N;
+    w.gext = o; o += (size_t)kMaxJobs * beta * E * N;
+    w.rot = o; o += (size_t)kMaxJobs * 2 * k * N;
+    w.resc = o; o += (2 + 2 * k) * N;
+    w.total = o;
+    return w;
+}
+
+extern "C" size_t blb_matmul_workspace_bytes(const blb_matmul_plan *pl, int out_count) {
+    if (!pl) return 0;
+    return matmul_ws(pl, out_count).total * sizeof(u64) + 256;
+}
+
+extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys *keys, const blb_ct *in, int n_in,
+                                       const u64 *pt_dev, int out_first, int out_count, blb_ct *out, void *ws,
+                                       size_t ws_bytes, void *stream) {
+    if (!pl || !keys || !in || !pt_dev || !out || !ws) {
+        blb_set_error("blb_ct_pt_matmul: null argument");
+        return BLB_E_INVALID_ARG;
+    }
+    BLB_TRY(check_slice(pl, out_first, out_count));
+    if (n_in != pl->n_in) {
+        blb_set_error("blb_ct_pt_matmul: %d inputs, plan needs %d", n_in, pl->n_in);
+        return BLB_E_LAYOUT;
+    }
+    const blb_params *P = pl->P;
+    const int level = pl->level, k = level + 1, N = P->N, E = k + P->np, beta = blb_beta(P, level);
+    for (int b = 0; b < n_in; b++)
+        if (in[b].level != level || !in[b].data) {
+            blb_set_error("input %d at level %d, plan level %d", b, in[b].level, level);
+            return BLB_E_LEVEL;
+        }
+    for (int t = 0; t < out_count; t++)
+        if (!out[t].data) return BLB_E_INVALID_ARG;
+    const MatmulWs w = matmul_ws(pl, out_count);
+    if (ws_bytes < w.total * sizeof(u64)) {
+        blb_set_error("workspace too small: %zu < %zu", ws_bytes, w.total * sizeof(u64));
+        return BLB_E_NOMEM;
+    }
+    // keys present?
+    auto find_key = [&](int32_t step) -> const u64 * {
+        const uint32_t g = blb_galois_element(P, step);
+        for (size_t i = 0; i < keys->galois.size(); i++)
+            if (keys->galois[i] == g) return keys->data[i];
+        return nullptr;
+    };
+    for (int32_t s : pl->rot_steps)
+        if (!find_key(s)) {
+            blb_set_error("missing rotation key for step %d", s);
+            return BLB_E_MISSING_KEY;
+        }
+    cudaStream_t st = (cudaStream_t)stream;
+    u64 *W = (u64 *)ws;
+    u64 *ext_in = W + w.ext_in, *coef = W + w.coef, *R = W + w.R, *ks = W + w.ks, *acc = W + w.acc;
+    u64 *gext = W + w.gext, *rot = W + w.rot, *resc = W + w.resc;
+    const size_t ctN = (size_t)2 * k * N;
+    u64 *ks_u = ks, *ks_conv = ks + (size_t)kMaxJobs * 2 * E * N;
+
+    // 1. ModUp of every input c1 (hoisted) and R[b][0] = X_b
+    {
+        std::vector<const u64 *> c1;
+        for (int b = 0; b < n_in; b++) c1.push_back(in[b].data + (size_t)k * N);
+        for (int b0 = 0; b0 < n_in; b0 += kMaxJobs) {
+            const int cnt = std::min(kMaxJobs, n_in - b0);
+            BLB_TRY(launch_modup(P, level, c1.data() + b0, cnt, ext_in + (size_t)b0 * beta * E * N, coef, st));
+        }
+        for (int b = 0; b < n_in; b++) {
+            k_copy_ct<<<(unsigned)((ctN + kTB - 1) / kTB), kTB, 0, st>>>(in[b].data, R + (size_t)b * pl->B * ctN,
+                                                                        (long long)ctN);
+            BLB_COUNT_LAUNCH(1);
+        }
+    }
+    // 2. baby steps: R[b][i] = Rot_{iL}(X_b), batched
+    {
+        std::vector<KsJob> jobs;
+        for (int b = 0; b < n_in; b++)
+            for (int i : pl->baby[b]) {
+                KsJob J{};
+                J.ext = ext_in + (size_t)b * beta * E * N;
+                J.key = find_key(i * pl->L);
+                J.c0 = in[b].data;
+                J.out = R + ((size_t)b * pl->B + i) * ctN;
+                J.galois = blb_galois_element(P, i * pl->L);
+                J.add_mode = 1;
+                jobs.push_back(J);
+            }
+        for (size_t j0 = 0; j0 < jobs.size(); j0 += kMaxJobs) {
+            const int cnt = (int)std::min<size_t>(kMaxJobs, jobs.size() - j0);
+            BLB_TRY(launch_keyswitch(P, level, jobs.data() + j0, cnt, ks_u, ks_conv, st));
+        }
+    }
+    // 3. MAC
+    {
+        const int o0 = out_first * pl->G, n_o = out_count * pl->G;
+        const int e_base = pl->ent_start[o0];
+        const int n_tiles = N / (2 * kTB);
+        if (n_o > 0) {
+            k_mac<<<(unsigned)((size_t)n_o * n_tiles * k), kTB, 0, st>>>(pt_dev, R, acc, pl->d_ent, pl->d_ent_start, o0,
+                                                                        e_base, n_o, k, P->logN, P->pr);
+            BLB_COUNT_LAUNCH(1);
+            BLB_COUNT(3, pl->ent_start[o0 + n_o] - e_base);
+            BLB_CHECK_LAUNCH();
+        }
+    }
+    // 4. giant steps: acc[b'][0] += Rot_{gBL}(acc[b'][g])
+    {
+        struct GJob {
+            int t, g;
+        };
+        std::vector<GJob> gj;
+        for (int t = 0; t < out_count; t++)
+            for (int g : pl->giant[out_first + t]) gj.push_back({t, g});
+        for (size_t j0 = 0; j0 < gj.size(); j0 += kMaxJobs) {
+            const int cnt = (int)std::min<size_t>(kMaxJobs, gj.size() - j0);
+            std::vector<const u64 *> c1(cnt);
+            std::vector<KsJob> jobs(cnt);
+            AccJobs aj{};
+            aj.n = cnt;
+            for (int j = 0; j < cnt; j++) {
+                const GJob &G = gj[j0 + j];
+                const u64 *a = acc + ((size_t)G.t * pl->G + G.g) * ctN;
+                c1[j] = a + (size_t)k * N;
+                KsJob J{};
+                J.ext = gext + (size_t)j * beta * E * N;
+                J.key = find_key(G.g * pl->B * pl->L);
+                J.c0 = a;
+                J.out = rot + (size_t)j * ctN;
+                J.galois = blb_galois_element(P, G.g * pl->B * pl->L);
+                J.add_mode = 1;
+                jobs[j] = J;
+                aj.dst[j] = acc + ((size_t)G.t * pl->G) * ctN;
+                aj.src[j] = J.out;
+            }
+            BLB_TRY(launch_modup(P, level, c1.data(), cnt, gext, coef, st));
+            BLB_TRY(launch_keyswitch(P, level, jobs.data(), cnt, ks_u, ks_conv, st));
+            k_accumulate<<<dim3((N + kTB - 1) / kTB, k, 2), kTB, 0, st>>>(aj, P->pr, k, N);
+            BLB_COUNT_LAUNCH(1);
+            BLB_CHECK_LAUNCH();
+        }
+    }
+    // 5. rescale each output
+    for (int t = 0; t < out_count; t++) {
+        BLB_TRY(launch_rescale(P, acc + (size_t)t * pl->G * ctN, level, 2, out[t].data, resc, st));
+        out[t].level = level - 1;
+        out[t].scale = in[0].scale;  // Delta * q_level / q_level, exact (reading S6)
+    }
+    return BLB_OK;
+}

@@ -1,0 +1,151 @@
+// ntt.cu -- limb-batched negacyclic NTT / INTT for sm_100a (row a1; C2).
+//
+// NTT(a)[k] = a(psi^{2 brv(k) + 1}) mod q: the in-place Cooley-Tukey network
+// (natural order in, bit-reversed order out) with twiddles psi^{brv(m+i)};
+// INTT = the Gentleman-Sande network with psi^{-brv(m+i)}, then N^{-1}.
+//
+// Design: the log N stages are split into two
+// shared-memory passes of 2^S1 and 2^S2 points (N = 2^16: 256 x 256).  Pass 1
+// transforms strided columns (elements mid*T + lo, T = N/2^S1) for 16
+// consecutive lo per CTA, so every global access is a 128-byte coalesced row
+// segment; pass 2 transforms 16 contiguous 2^S2-point blocks per CTA.  Each
+// CTA keeps 4096 residues (32 KB) in shared memory across its S stages.
+// Butterflies are Harvey-lazy with Shoup twiddles: values stay in [0, 4q)
+// (forward) / [0, 2q) (inverse) and are made canonical in the last pass.
+// N <= 2^12 runs in a single pass (one row per CTA).
+#include "blb_internal.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+
+template <bool INV>
+__global__ void __launch_bounds__(kThreads) ntt_pass(RowBatch rb, const u64 *__restrict__ tw_all, Primes pr, int logN,
+                                                     int s0, int logM, int logT, int logC, int last) {
+    extern __shared__ u64 sm[];
+    const int M = 1 << logM, C = 1 << logC;
+    const int N = 1 << logN;
+    const int row = blockIdx.y;
+    const int p = row / rb.limbs, l = row - p * rb.limbs;
+    u64 *a = rb.base + (long long)p * rb.poly_stride + (long long)(rb.limb0 + l) * N;
+    if (rb.skip_alpha) {
+        const int dig = p % rb.skip_beta;
+        if (l < rb.skip_kmax && l >= dig * rb.skip_alpha && l < (dig + 1) * rb.skip_alpha) return;
+    }
+    const int pi = rb.prime[l];
+    const u64 q = pr.m[pi].q, q2 = 2 * q;
+    const u64 *tw = tw_all + (size_t)pi * 4 * N + (INV ? 2 * N : 0);
+    const u64 *twsh = tw + N;
+    const int colg0 = blockIdx.x * C;
+    const bool strided = logT > 0;
+    const int TM = C * M;
+
+    // load: smem index == linear index within the tile
+    for (int idx = threadIdx.x; idx < TM; idx += kThreads) {
+        int col, mid;
+        if (strided) { mid = idx >> logC; col = idx & (C - 1); }
+        else { col = idx >> logM; mid = idx & (M - 1); }
+        const int colg = colg0 + col;
+        const size_t addr = ((size_t)(colg >> logT) << (logM + logT)) + ((size_t)mid << logT) + (colg & ((1 << logT) - 1));
+        sm[idx] = a[addr];
+    }
+
+    for (int rr = 0; rr < logM; rr++) {
+        const int r = INV ? (logM - 1 - rr) : rr;
+        const int logtl = logM - r - 1;
+        const int tl = 1 << logtl;
+        const int s = s0 + r;
+        __syncthreads();
+        for (int pidx = threadIdx.x; pidx < TM / 2; pidx += kThreads) {
+            int col, qq;
+            if (strided) { col = pidx & (C - 1); qq = pidx >> logC; }
+            else { col = pidx >> (logM - 1); qq = pidx & ((M >> 1) - 1); }
+            const int mid = ((qq >> logtl) << (logtl + 1)) + (qq & (tl - 1));
+            const int h = (colg0 + col) >> logT;
+            const int widx = (1 << s) + (h << r) + (qq >> logtl);
+            const u64 w = tw[widx], wsh = twsh[widx];
+            const int i0 = strided ? (mid * C + col) : (col * M + mid);
+            const int i1 = i0 + (strided ? (tl << logC) : tl);
+            u64 X = sm[i0], Y = sm[i1];
+            if (!INV) {
+                if (X >= q2) X -= q2;
+                const u64 t = shoup_lazy(Y, w, wsh, q);
+                sm[i0] = X + t;
+                sm[i1] = X - t + q2;
+            } else {
+                u64 sum = X + Y;
+                if (sum >= q2) sum -= q2;
+                sm[i0] = sum;
+                sm[i1] = shoup_lazy(X - Y + q2, w, wsh, q);
+            }
+        }
+    }
+    __syncthreads();
+    const ModConst &mc = pr.m[pi];
+    for (int idx = threadIdx.x; idx < TM; idx += kThreads) {
+        int col, mid;
+        if (strided) { mid = idx >> logC; col = idx & (C - 1); }
+        else { col = idx >> logM; mid = idx & (M - 1); }
+        const int colg = colg0 + col;
+        const size_t addr = ((size_t)(colg >> logT) << (logM + logT)) + ((size_t)mid << logT) + (colg & ((1 << logT) - 1));
+        u64 v = sm[idx];
+        if (last) {
+            if (!INV) {
+                if (v >= q2) v -= q2;
+                if (v >= q) v -= q;
+            } else {
+                v = shoup_lazy(v, mc.ninv, mc.ninv_sh, q);
+                if (v >= q) v -= q;
+            }
+        }
+        a[addr] = v;
+    }
+}
+
+}  // namespace
+
+blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cudaStream_t st) {
+    const int rows = rb.n_polys * rb.limbs;
+    if (rows == 0) return BLB_OK;
+    const int logN = P->logN;
+    if (rows > 65535) {
+        // split by polys to respect gridDim.y
+        int per = 65535 / rb.limbs;
+        for (int p0 = 0; p0 < rb.n_polys; p0 += per) {
+            RowBatch sub = rb;
+            sub.base = rb.base + (long long)p0 * rb.poly_stride;
+            sub.n_polys = (rb.n_polys - p0) < per ? (rb.n_polys - p0) : per;
+            BLB_TRY(launch_ntt(P, sub, inverse, st));
+        }
+        return BLB_OK;
+    }
+    BLB_COUNT(2, rows);
+    if (logN <= 12) {
+        const size_t smem = (size_t)8 << logN;
+        dim3 grid(1, rows);
+        if (!inverse) ntt_pass<false><<<grid, kThreads, smem, st>>>(rb, P->d_tw, P->pr, logN, 0, logN, 0, 0, 1);
+        else ntt_pass<true><<<grid, kThreads, smem, st>>>(rb, P->d_tw, P->pr, logN, 0, logN, 0, 0, 1);
+        BLB_COUNT_LAUNCH(1);
+        BLB_CHECK_LAUNCH();
+        return BLB_OK;
+    }
+    const int S1 = logN / 2, S2 = logN - S1;
+    const int logTile = 12;  // 4096 residues per CTA
+    const size_t smem = (size_t)8 << logTile;
+    // pass over the strided columns: stages [0, S1), M = 2^S1, T = 2^S2
+    const int logC1 = logTile - S1;
+    dim3 g1((1 << S2) >> logC1, rows);
+    // pass over contiguous blocks: stages [S1, logN), M = 2^S2, T = 1
+    const int logC2 = logTile - S2;
+    dim3 g2((1 << S1) >> logC2, rows);
+    if (!inverse) {
+        ntt_pass<false><<<g1, kThreads, smem, st>>>(rb, P->d_tw, P->pr, logN, 0, S1, S2, logC1, 0);
+        ntt_pass<false><<<g2, kThreads, smem, st>>>(rb, P->d_tw, P->pr, logN, S1, S2, 0, logC2, 1);
+    } else {
+        ntt_pass<true><<<g2, kThreads, smem, st>>>(rb, P->d_tw, P->pr, logN, S1, S2, 0, logC2, 0);
+        ntt_pass<true><<<g1, kThreads, smem, st>>>(rb, P->d_tw, P->pr, logN, 0, S1, S2, logC1, 1);
+    }
+    BLB_COUNT_LAUNCH(2);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
