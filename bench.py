@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""bench.py -- ms per BERT-base layer of BLB's fused-linear CKKS evaluation on B200.
+
+Metric (BASELINE.json): "ms per BERT-base layer fused-linear CKKS eval; NTT
+limbs/s and HBM GB/s fraction".  One step = one pass of the whole hot path over
+one layer's synthetic inputs: QKV ct-pt MatMul (C11, MHP) + out-projection
+(C12, diagonal input) + FFN1 + FFN2, every MatMul with hoisted baby-step
+rotations, MAC, giant-step key switches and rescale, then the CKKS->MPC masks
+(server half of Alg. 1) of every converted output.  Q K^T (row a7) is not yet
+part of the step; the JSON says so in config.layer_ops.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one rank per GPU, NCCL): outputs are sharded
+by output ciphertext, baby steps replicated, masked results all-gathered.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import blb_inputs as bi  # noqa: E402
+
+METRIC = "ms per BERT-base layer fused-linear CKKS eval"
+UNIT = "ms"
+FALLBACK_HBM = 6650.0
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# --------------------------------------------------------------------------- clocks
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.index = index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                smax.append(float(r[1]))
+                for nm, v in zip(names, r[4:8]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                pass
+        os.unlink(self.f.name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- oracle sample
+def oracle_sample_ms(dims, reps: int = 1) -> dict:
+    """Time the CPU oracle (as it stands) on a bounded sample of the layer at
+    N = 2^16, level 4, and extrapolate to ms per layer by operation counts:
+    one hoisted rotation (ModUp + key switch), P ct-pt products (mul + add), one
+    rescale, one mask.  Plaintext / key values do not change the work, so
+    uniform residues stand in for encoded weights (encode is row a0)."""
+    import oracle as O
+    import oracle.matmul as mm
+    P = bi.BERT
+    primes = O.prime_chain(P.log_n, list(P.q_bits) + list(P.p_bits))
+    ctx = O.Ctx(P.log_n, primes[:5], primes[5:], P.dnum)
+    rng = np.random.default_rng(0)
+    lvl = 4
+    k = lvl + 1
+
+    def rnd(*shape_limbs):
+        polys, limbs = shape_limbs
+        return np.stack([np.stack([rng.integers(0, ctx.mods[i], ctx.N, dtype=np.uint64) for i in limbs])
+                         for _ in range(polys)])
+
+    ct = O.Ct(rnd(2, range(k)), lvl, 2.0 ** 40)
+    g = ctx.galois(128)
+    key = np.stack([np.stack([rnd(1, range(6))[0] for _ in range(2)]) for _ in range(ctx.beta_top)])
+    keys = O.Keys(None, None, {g: key})
+    n_prod = 8
+    pts = [rnd(1, range(k))[0] for _ in range(n_prod)]
+    t = {"rot": 0.0, "prod": 0.0, "resc": 0.0, "mask": 0.0}
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.rotate(ctx, ct, keys, 128)
+        t1 = time.perf_counter()
+        acc = O.mul_pt(ctx, ct, pts[0], 1.0)
+        for p in pts[1:]:
+            acc = O.add(ctx, acc, O.mul_pt(ctx, ct, p, 1.0))
+        t2 = time.perf_counter()
+        r = O.rescale(ctx, acc)
+        t3 = time.perf_counter()
+        O.mask(ctx, r, bytes(32), 0)
+        t4 = time.perf_counter()
+        t["rot"] += (t1 - t0) / reps
+        t["prod"] += (t2 - t1) / (reps * n_prod)
+        t["resc"] += (t3 - t2) / reps
+        t["mask"] += (t4 - t3) / reps
+    # layer operation counts from the oracle's own plans (C11 / C12)
+    n = ctx.n
+    W = np.ones((dims["d"], dims["d"]))
+    cm = mm.mhp_column_map(dims["d"], dims["H"], dims["L"], n)
+    qkv_map = cm + [dims["d"] + c if c >= 0 else -1 for c in cm] + list(range(2 * dims["d"], 3 * dims["d"]))
+    plans = [mm.plan_spatial(np.ones((dims["d"], 3 * dims["d"])), dims["L"], n, 32, col_map=qkv_map),
+             mm.plan_diagonal(W, dims["H"], dims["L"], n, 16),
+             mm.plan_spatial(np.ones((dims["d"], dims["ffn"])), dims["L"], n, 32),
+             mm.plan_spatial(np.ones((dims["ffn"], dims["d"])), dims["L"], n, 8)]
+    n_rot = sum(p.n_rotations for p in plans)
+    n_pt = sum(p.n_plaintexts for p in plans)
+    n_out = sum(p.n_out for p in plans)
+    n_mask = n_out - 2 * (len(cm) // (n // dims["L"]))
+    ms = 1e3 * (n_rot * t["rot"] + n_pt * t["prod"] + n_out * t["resc"] + n_mask * t["mask"])
+    return {"ms_per_layer": ms, "per_op_s": t, "counts": {"rotations": n_rot, "plaintexts": n_pt,
+                                                          "rescales": n_out, "masks": n_mask},
+            "sample": "oracle at N=2^16, level 4 (k=5): 1 hoisted rotation + %d ct-pt products + 1 rescale + 1 mask "
+                      "per rep, x%d reps; extrapolated by the layer's operation counts (%d rotations, %d plaintexts, "
+                      "%d rescales, %d masks)" % (n_prod, reps, n_rot, n_pt, n_out, n_mask)}
+
+
+def omp_threads() -> int:
+    v = os.environ.get("OMP_NUM_THREADS")
+    return int(v) if v and v.isdigit() else (os.cpu_count() or 1)
+
+
+def run_reference(args, dims):
+    """--impl reference: the oracle timed on host cores, each step a bounded sample."""
+    samples = []
+    for s in range(args.warmup + args.steps):
+        r = oracle_sample_ms(dims, reps=1)
+        if s >= args.warmup:
+            samples.append(r["ms_per_layer"])
+    v = float(np.median(samples))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": config_dict(dims, args.gpus),
+            "cpu_baseline": {"kind": "oracle", "value": v, "unit": UNIT, "cores": omp_threads(),
+                             "sample": r["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(dims, world):
+    return {"workload": "BERT-base layer fused-linear CKKS (config 2 QKV + config 3 out-proj/FFN1/FFN2 + CKKS->MPC "
+                        "masks), N=2^16, Q={60,40x4}, P={60}, dnum=5",
+            "L": dims["L"], "d": dims["d"], "heads": dims["H"], "ffn": dims["ffn"], "log_n": 16, "limbs": 5,
+            "bsgs": {"qkv": 32, "oproj": 16, "ffn1": 32, "ffn2": 8},
+            "layer_ops": ["qkv_ct_pt(MHP)", "mask(V)", "oproj_diag_ct_pt", "mask", "ffn1_ct_pt", "mask",
+                          "ffn2_ct_pt", "mask"],
+            "not_included": "Q.K^T ct-ct MatMul (row a7) and Softmax x V (row f1)",
+            "l2": "inputs larger than L2 (~76 GB of plaintexts streamed per step)",
+            "parallelism": "dp%d (output-ciphertext sharding, NCCL all-gather of masked outputs)" % world}
+
+
+# --------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dims", default="base", choices=["base", "large"])
+    args = ap.parse_args()
+    dims = dict(L=128, d=768, H=12, ffn=3072) if args.dims == "base" else dict(L=128, d=1024, H=16, ffn=4096)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, dims)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_19525_b200 as blb
+    from paper_2508_19525_b200 import packing
+    from paper_2508_19525_b200.layer import Dims, FusedLinearLayer
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    t_setup0 = time.perf_counter()
+    params = blb.Params.from_preset(bi.BERT, device=local)
+    layer = FusedLinearLayer(params, Dims(**dims), rank, world)
+    A = bi.bert_attention_inputs(dims["L"], dims["d"])
+    F = bi.bert_ffn_inputs(dims["L"], dims["d"], dims["H"], dims["ffn"])
+    keys, sk = blb.keygen(params, A["keys_key"], layer.rotation_steps())
+    torch.cuda.synchronize()
+    t_keys = time.perf_counter() - t_setup0
+    t0 = time.perf_counter()
+    layer.load_weights(A["WQ"], A["WK"], A["WV"], F["WO"], F["W1"], F["W2"])
+    torch.cuda.synchronize()
+    t_encode = time.perf_counter() - t0
+
+    # client-side inputs: encrypt once (fresh ciphertexts at the top level)
+    delta = 2.0 ** bi.BERT.log_delta
+    lvl = layer.level
+    slots = {"qkv": packing.spatial_slots(A["X"], params.n), "oproj": packing.diagonal_slots(F["Att"], params.n),
+             "ffn1": packing.spatial_slots(F["X2"], params.n), "ffn2": packing.spatial_slots(F["H1"], params.n)}
+    inputs, cid = {}, 0
+    for name, zs in slots.items():
+        pts = params.encode(torch.tensor(zs), delta, lvl)
+        inputs[name] = []
+        for b in range(zs.shape[0]):
+            inputs[name].append(blb.encrypt(params, sk, pts[b], lvl, A["enc_key"], 4096 + cid, delta))
+            cid += 1
+    del sk
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+
+    def gather(res):
+        if world == 1:
+            return res
+        out = []
+        for name, id0, (m, s) in res:
+            buf = torch.cat([m.reshape(-1), s.reshape(-1)])
+            n = torch.tensor([buf.numel()], device="cuda")
+            sizes = [torch.zeros_like(n) for _ in range(world)]
+            dist.all_gather(sizes, n)
+            mx = int(max(x.item() for x in sizes))
+            pad = torch.zeros(mx, dtype=buf.dtype, device="cuda")
+            pad[:buf.numel()] = buf
+            allb = torch.empty(world * mx, dtype=buf.dtype, device="cuda")
+            dist.all_gather_into_tensor(allb, pad)
+            out.append((name, id0, allb))
+        return out
+
+    def step():
+        return gather(layer.step(keys, inputs, A["mask_key"]))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device events; max over ranks) ----
+    blb.reset_counters()
+    blb.timing_reset()
+    blb.timing_enable(True)
+    clocks = Clocks(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    blb.timing_enable(False)
+    ms_total = ev0.elapsed_time(ev1)
+    ctr = blb.counters()
+    mac = blb.timing_read(blb.TIMING_MAC)
+    ntt = blb.timing_read(blb.TIMING_NTT)
+    ksi = blb.timing_read(blb.TIMING_KS_INNER)
+    ms_step = ms_total / args.steps
+    if world > 1:
+        t = torch.tensor([ms_step], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+
+    # ---- e2e through the C ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        host_in = {k: [torch.empty_like(c.data, device="cpu").pin_memory() for c in v] for k, v in inputs.items()}
+        for k, v in inputs.items():
+            for h, c in zip(host_in[k], v):
+                h.copy_(c.data)
+        h2d = sum(h.numel() * 8 for v in host_in.values() for h in v)
+        d2h = 0
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            for k, v in inputs.items():
+                for h, c in zip(host_in[k], v):
+                    c.data.copy_(h, non_blocking=True)
+            res = step()
+            outs_host = []
+            for r in res:
+                for t in (r[2] if isinstance(r[2], tuple) else (r[2],)):
+                    outs_host.append(t.to("cpu"))
+            d2h = sum(t.numel() * 8 for t in outs_host)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms = e0.elapsed_time(e1) / args.steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = measured_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", FALLBACK_HBM))
+    mac_gbs = mac["alg_bytes"] / (mac["ms"] * 1e-3) / 1e9 if mac["ms"] > 0 else None
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "mac_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": ms_step, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded N(0,1) activations, N(0,0.04^2) weights)",
+        "config": config_dict(dims, world),
+        "roofline": {"kernel": "k_mac (ct-pt MAC, row a3)", "bound": "hbm", "achieved": mac_gbs, "peak": hbm_peak,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
+                     "unit": "GB/s", "frac": (mac_gbs / hbm_peak) if mac_gbs else None, "traffic": traffic,
+                     "alg_bytes_per_launch": mac["alg_bytes"] / max(1, mac["launches"]),
+                     "ms_per_launch": mac["ms"] / max(1, mac["launches"]),
+                     "share_of_step": mac["ms"] / ms_total if ms_total else None},
+        "ntt": {"limbs_per_s": (ntt["alg_bytes"] / (16.0 * params.N)) / (ntt["ms"] * 1e-3) if ntt["ms"] else None,
+                "alg_gbs": ntt["alg_bytes"] / (ntt["ms"] * 1e-3) / 1e9 if ntt["ms"] else None,
+                "share_of_step": ntt["ms"] / ms_total if ms_total else None, "launches": ntt["launches"]},
+        "ks_inner": {"alg_gbs": ksi["alg_bytes"] / (ksi["ms"] * 1e-3) / 1e9 if ksi["ms"] else None,
+                     "share_of_step": ksi["ms"] / ms_total if ms_total else None},
+        "gpu_launches": ctr["launches"],
+        "counters_per_step": {k: v / args.steps for k, v in ctr.items()},
+        "clocks": clk,
+        "setup_s": {"keygen": t_keys, "weight_encode": t_encode, "plaintexts": layer.n_plaintexts(),
+                    "plaintext_GB": layer.plaintext_bytes() / 1e9},
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        r = oracle_sample_ms(dims, reps=1)
+        line["cpu_baseline"] = {"value": r["ms_per_layer"], "unit": UNIT, "cores": omp_threads(), "kind": "oracle",
+                                "sample": r["sample"]}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -86,6 +86,18 @@ const char *blb_last_error(void);
 void blb_counters_get(uint64_t out[6]);
 void blb_counters_reset(void);
 
+/* Live kernel timing (bench instrumentation).  When enabled, the library
+ * records a CUDA event pair on the launching stream around every launch of
+ * the tracked kernels: category 0 = ct-pt MAC (k_mac), 1 = NTT/INTT passes,
+ * 2 = key-switch inner product.  blb_timing_read synchronises the recorded
+ * events and returns, for `category`, the summed device milliseconds, the
+ * number of launches and the summed ALGORITHMIC bytes (MAC: k*N*8 per
+ * plaintext; NTT: 2*N*8 per limb; inner product: 2*beta*(k+np)*N*8 key bytes
+ * per key switch).  Host outputs, nullable. */
+void blb_timing_enable(int on);
+void blb_timing_reset(void);
+blb_status blb_timing_read(int category, double *total_ms, uint64_t *launches, double *alg_bytes);
+
 /* ------------------------------------------------------------------ */
 /* parameters (C1; Table 6 P:716-720 for the chain shape)               */
 /* ------------------------------------------------------------------ */

@@ -55,6 +55,9 @@ def lib() -> ctypes.CDLL:
             "blb_last_error": ([], ctypes.c_char_p),
             "blb_counters_get": ([vp], None),
             "blb_counters_reset": ([], None),
+            "blb_timing_enable": ([ctypes.c_int], None),
+            "blb_timing_reset": ([], None),
+            "blb_timing_read": ([ctypes.c_int, vp, vp, vp], ctypes.c_int),
             "blb_prime_chain": ([ctypes.c_int, vp, ctypes.c_int, vp], ctypes.c_int),
             "blb_params_create": ([vp, ctypes.c_int, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int],
                                   ctypes.c_int),
@@ -122,6 +125,23 @@ def counters() -> dict:
 
 def reset_counters():
     lib().blb_counters_reset()
+
+
+TIMING_MAC, TIMING_NTT, TIMING_KS_INNER = 0, 1, 2
+
+
+def timing_enable(on: bool = True):
+    lib().blb_timing_enable(int(on))
+
+
+def timing_reset():
+    lib().blb_timing_reset()
+
+
+def timing_read(category: int) -> dict:
+    ms, n, by = ctypes.c_double(), ctypes.c_uint64(), ctypes.c_double()
+    _check(lib().blb_timing_read(category, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(by)))
+    return {"ms": ms.value, "launches": n.value, "alg_bytes": by.value}
 
 
 def prime_chain(log_n: int, bits) -> list[int]:
@@ -385,9 +405,12 @@ class MatmulPlan:
                                                _ptr(pts), _stream()))
         return pts
 
-    def workspace(self, out_count: int | None = None) -> torch.Tensor:
+    def workspace_bytes(self, out_count: int | None = None) -> int:
         out_count = self.n_out if out_count is None else out_count
-        nbytes = lib().blb_matmul_workspace_bytes(self._h, out_count)
+        return int(lib().blb_matmul_workspace_bytes(self._h, out_count))
+
+    def workspace(self, out_count: int | None = None) -> torch.Tensor:
+        nbytes = self.workspace_bytes(out_count)
         return torch.empty(nbytes // 8 + 1, dtype=torch.int64, device="cuda")
 
     def __call__(self, keys: Keys, cts: list, pts: torch.Tensor, out_first: int = 0, out_count: int | None = None,

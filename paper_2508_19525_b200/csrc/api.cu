@@ -53,6 +53,70 @@ extern "C" void blb_counters_reset(void) {
     for (int i = 0; i < 6; i++) __atomic_store_n(&g_blb_counters[i], 0ull, __ATOMIC_RELAXED);
 }
 
+// ------------------------------------------------------------ live timing
+#include <mutex>
+namespace {
+struct TimedLaunch {
+    cudaEvent_t a, b;
+    double bytes;
+};
+std::mutex g_tmu;
+bool g_timing = false;
+std::vector<TimedLaunch> g_tl[3];
+std::vector<cudaEvent_t> g_pool;
+cudaEvent_t take_event() {
+    if (!g_pool.empty()) {
+        cudaEvent_t e = g_pool.back();
+        g_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+}  // namespace
+cudaEvent_t blb_timing_begin(cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    if (!g_timing) return nullptr;
+    cudaEvent_t e = take_event();
+    cudaEventRecord(e, st);
+    return e;
+}
+void blb_timing_end(int cat, cudaEvent_t start, cudaStream_t st, double bytes) {
+    if (!start) return;
+    std::lock_guard<std::mutex> lk(g_tmu);
+    cudaEvent_t e = take_event();
+    cudaEventRecord(e, st);
+    g_tl[cat].push_back({start, e, bytes});
+}
+extern "C" void blb_timing_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    g_timing = on != 0;
+}
+extern "C" void blb_timing_reset(void) {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    for (auto &v : g_tl) {
+        for (auto &t : v) { g_pool.push_back(t.a); g_pool.push_back(t.b); }
+        v.clear();
+    }
+}
+extern "C" blb_status blb_timing_read(int cat, double *total_ms, uint64_t *launches, double *bytes) {
+    if (cat < 0 || cat > 2) return BLB_E_INVALID_ARG;
+    std::lock_guard<std::mutex> lk(g_tmu);
+    double ms = 0, by = 0;
+    for (auto &t : g_tl[cat]) {
+        BLB_CUDA_TRY(cudaEventSynchronize(t.b));
+        float f = 0;
+        BLB_CUDA_TRY(cudaEventElapsedTime(&f, t.a, t.b));
+        ms += f;
+        by += t.bytes;
+    }
+    if (total_ms) *total_ms = ms;
+    if (launches) *launches = g_tl[cat].size();
+    if (bytes) *bytes = by;
+    return BLB_OK;
+}
+
 // ------------------------------------------------------------ params
 extern "C" blb_status blb_prime_chain(int log_n, const int *bits, int count, uint64_t *out) {
     if (!bits || !out || count <= 0 || log_n < 2 || log_n > 16) {

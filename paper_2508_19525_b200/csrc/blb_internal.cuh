@@ -130,6 +130,10 @@ extern unsigned long long g_blb_counters[6];
 #define BLB_COUNT_LAUNCH(n) (__atomic_fetch_add(&g_blb_counters[0], (unsigned long long)(n), __ATOMIC_RELAXED))
 #define BLB_COUNT(i, n) (__atomic_fetch_add(&g_blb_counters[i], (unsigned long long)(n), __ATOMIC_RELAXED))
 
+// live timing of tracked kernels (api.cu): returns a recorded start event or nullptr
+cudaEvent_t blb_timing_begin(cudaStream_t st);
+void blb_timing_end(int category, cudaEvent_t start, cudaStream_t st, double alg_bytes);
+
 #define BLB_CUDA_TRY(expr)                                                                        \
     do {                                                                                          \
         cudaError_t _e = (expr);                                                                  \

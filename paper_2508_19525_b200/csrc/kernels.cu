@@ -385,8 +385,10 @@ blb_status launch_keyswitch(const blb_params *P, int level, const KsJob *jobs, i
     const int N = P->N, k = level + 1, np = P->np, E = k + np, beta = blb_beta(P, level);
     KsJobs J{};
     for (int t = 0; t < n; t++) J.j[t] = jobs[t];
+    cudaEvent_t t0 = blb_timing_begin(st);
     k_ks_inner<<<grid_x(N, E, n), kTB, 0, st>>>(J, u, P->pr, k, np, P->K, beta, P->logN);
     BLB_COUNT_LAUNCH(1);
+    blb_timing_end(2, t0, st, (double)n * 2.0 * beta * E * N * 8.0);
     BLB_CHECK_LAUNCH();
     RowBatch rb{};
     rb.base = u; rb.poly_stride = (long long)E * N; rb.n_polys = 2 * n; rb.limbs = np; rb.limb0 = k;

@@ -484,10 +484,12 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
         const int e_base = pl->ent_start[o0];
         const int n_tiles = N / (2 * kTB);
         if (n_o > 0) {
+            cudaEvent_t t0 = blb_timing_begin(st);
             k_mac<<<(unsigned)((size_t)n_o * n_tiles * k), kTB, 0, st>>>(pt_dev, R, acc, pl->d_ent, pl->d_ent_start, o0,
                                                                         e_base, n_o, k, P->logN, P->pr);
             BLB_COUNT_LAUNCH(1);
             BLB_COUNT(3, pl->ent_start[o0 + n_o] - e_base);
+            blb_timing_end(0, t0, st, (double)(pl->ent_start[o0 + n_o] - e_base) * k * N * 8.0);
             BLB_CHECK_LAUNCH();
         }
     }

@@ -120,12 +120,15 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
         return BLB_OK;
     }
     BLB_COUNT(2, rows);
+    cudaEvent_t t0 = blb_timing_begin(st);
+    const double alg = (double)rows * 2.0 * 8.0 * (double)(1 << logN);
     if (logN <= 12) {
         const size_t smem = (size_t)8 << logN;
         dim3 grid(1, rows);
         if (!inverse) ntt_pass<false><<<grid, kThreads, smem, st>>>(rb, P->d_tw, P->pr, logN, 0, logN, 0, 0, 1);
         else ntt_pass<true><<<grid, kThreads, smem, st>>>(rb, P->d_tw, P->pr, logN, 0, logN, 0, 0, 1);
         BLB_COUNT_LAUNCH(1);
+        blb_timing_end(1, t0, st, alg);
         BLB_CHECK_LAUNCH();
         return BLB_OK;
     }
@@ -146,6 +149,7 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
         ntt_pass<true><<<g1, kThreads, smem, st>>>(rb, P->d_tw, P->pr, logN, 0, S1, S2, logC1, 1);
     }
     BLB_COUNT_LAUNCH(2);
+    blb_timing_end(1, t0, st, alg);
     BLB_CHECK_LAUNCH();
     return BLB_OK;
 }

@@ -1,0 +1,114 @@
+"""Layer driver: the fused-linear CKKS evaluation of one Transformer layer
+(BASELINE.json configs 2 + 3) on one rank of a data-parallel group.
+
+Blocks (fig:fusion_pattern P:699-704, Table 6):
+  * attention: QKV projection (C11, MHP reorder of the Q / K columns, P:466,
+    P:511) -> [Q K^T, row a7: not yet built] -> CKKS->MPC mask of V;
+  * out-projection: diagonal-input ct-pt MatMul (C12, App. C.2) -> mask;
+  * FFN1 (d -> 4d) -> mask; FFN2 (4d -> d) -> mask.
+Each MatMul starts from a fresh ciphertext at the top level (SURVEY 8(d)
+config 3).  Work is sharded by output ciphertext (section 8(e)): rank r owns a
+contiguous slice of every plan's outputs, holds only the plaintexts of that
+slice, recomputes the (replicated) baby steps, and the masked results are
+all-gathered at the end of the layer.  The BSGS split is fixed independently of
+the number of ranks, so outputs are bit-identical at every GPU count.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+import paper_2508_19525_b200 as blb
+
+
+@dataclass
+class Dims:
+    L: int = 128
+    d: int = 768
+    H: int = 12
+    ffn: int = 3072
+
+
+BERT_BASE = Dims()
+BERT_LARGE = Dims(128, 1024, 16, 4096)
+BSGS = {"qkv": 32, "oproj": 16, "ffn1": 32, "ffn2": 8}
+PLAN_ID = {"qkv": 0, "oproj": 1, "ffn1": 2, "ffn2": 3}
+
+
+def shard(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous split of n outputs over world ranks: (first, count)."""
+    base, rem = divmod(n, world)
+    first = rank * base + min(rank, rem)
+    return first, base + (1 if rank < rem else 0)
+
+
+class FusedLinearLayer:
+    def __init__(self, params: blb.Params, dims: Dims = BERT_BASE, rank: int = 0, world: int = 1,
+                 bsgs: dict | None = None, level: int | None = None):
+        self.p, self.dims, self.rank, self.world = params, dims, rank, world
+        self.level = params.K - 1 if level is None else level
+        b = dict(BSGS, **(bsgs or {}))
+        L, d, H, ffn = dims.L, dims.d, dims.H, dims.ffn
+        cm = blb.mhp_column_map(d, H, L, params.log_n)
+        qkv_map = cm + [d + c if c >= 0 else -1 for c in cm] + list(range(2 * d, 3 * d))
+        self.n_mhp = len(cm) // (params.n // L)   # ciphertexts of Q (and of K)
+        self.plans = {
+            "qkv": blb.MatmulPlan(params, L, d, 3 * d, col_map=qkv_map, bsgs_B=b["qkv"], level=self.level),
+            "oproj": blb.MatmulPlan(params, L, d, d, packing=blb.PACK_DIAGONAL, heads=H, bsgs_B=b["oproj"],
+                                    level=self.level),
+            "ffn1": blb.MatmulPlan(params, L, d, ffn, bsgs_B=b["ffn1"], level=self.level),
+            "ffn2": blb.MatmulPlan(params, L, ffn, d, bsgs_B=b["ffn2"], level=self.level),
+        }
+        self.slices = {k: shard(pl.n_out, rank, world) for k, pl in self.plans.items()}
+        self.pts, self.ws, self.outs = {}, None, {}
+
+    # ---- setup (row a0) ----
+    def rotation_steps(self) -> list[int]:
+        s = set()
+        for pl in self.plans.values():
+            s.update(pl.rotation_steps())
+        return sorted(s)
+
+    def load_weights(self, WQ, WK, WV, WO, W1, W2):
+        Wqkv = np.concatenate([WQ, WK, WV], axis=1)
+        for name, W in (("qkv", Wqkv), ("oproj", WO), ("ffn1", W1), ("ffn2", W2)):
+            first, count = self.slices[name]
+            self.pts[name] = self.plans[name].encode_weights(W, first, count)
+        nbytes = max(pl.workspace_bytes(self.slices[k][1]) for k, pl in self.plans.items())
+        self.ws = torch.empty(nbytes // 8 + 1, dtype=torch.int64, device="cuda")
+        for k, pl in self.plans.items():
+            self.outs[k] = [blb.Ciphertext.empty(self.p, self.level - 1) for _ in range(self.slices[k][1])]
+
+    def plaintext_bytes(self) -> int:
+        return sum(int(t.numel()) * 8 for t in self.pts.values())
+
+    def n_plaintexts(self) -> int:
+        return sum(self.plans[k].pt_count(*self.slices[k]) for k in self.plans)
+
+    def mask_ids(self, name: str) -> list[int]:
+        """Global ciphertext ids of the masked outputs of this rank (PRNG key, C4)."""
+        first, count = self.slices[name]
+        outs = range(first, first + count)
+        if name == "qkv":   # only V is converted here; Q, K feed Q K^T (row a7)
+            outs = [o for o in outs if o >= 2 * self.n_mhp]
+        return [PLAN_ID[name] * 1024 + o for o in outs]
+
+    # ---- the hot path ----
+    def step(self, keys: blb.Keys, inputs: dict, mask_key: bytes) -> list:
+        """inputs: {'qkv': [ct]*3, 'oproj': [...], 'ffn1': [...], 'ffn2': [...]} -> [(masked, share)] per block."""
+        res = []
+        for name in ("qkv", "oproj", "ffn1", "ffn2"):
+            first, count = self.slices[name]
+            if count == 0:
+                continue
+            outs = self.plans[name](keys, inputs[name], self.pts[name], first, count, ws=self.ws,
+                                    outs=self.outs[name])
+            ids = self.mask_ids(name)
+            if not ids:
+                continue
+            sel = [outs[i - PLAN_ID[name] * 1024 - first] for i in ids]
+            # ids of one block are contiguous: one mask launch per block
+            res.append((name, ids[0], blb.ckks_to_mpc(self.p, sel, mask_key, ids[0])))
+        return res
