@@ -99,3 +99,13 @@ def bert_ffn_inputs(L=128, d=768, H=12, ffn=3072, config_id=3):
     W2 = normal(26, (ffn, d), 0.02)
     return dict(Att=Att, WO=WO, X2=X2, W1=W1, H1=H1, W2=W2, keys_key=crypto_key(4, config_id),
                 enc_key=crypto_key(5, config_id), mask_key=crypto_key(3, config_id))
+
+
+# a toy ring with the BERT chain shape (5 ciphertext primes): room for QKV + Q K^T (depth 4)
+QKTOY = Preset("qktoy", 12, (60, 40, 40, 40, 40), (60,), 5, 40)
+
+
+def qk_toy_inputs(H=4, L=32, dh=32):
+    Q = uniform(41, (H, L, dh), -1.0, 1.0)
+    K = uniform(42, (H, L, dh), -1.0, 1.0)
+    return dict(Q=Q, K=K, keys_key=crypto_key(4, 41), enc_key=crypto_key(5, 41), mask_key=crypto_key(3, 41))
