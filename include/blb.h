@@ -275,6 +275,39 @@ blb_status blb_ct_pt_matmul(const blb_matmul_plan *plan, const blb_keys *keys, c
                             const uint64_t *pt_dev, int out_first, int out_count, blb_ct *out, void *ws,
                             size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------------------------ */
+/* ct-ct MatMul Q_h K_h^T for all heads (row a7; sec. 5.1,    */
+/* App. C.1; reading C13)                                   */
+/* ------------------------------------------------------------------ */
+typedef struct blb_qk_plan blb_qk_plan;
+
+/* Plan C_h = Q_h K_h^T for `heads` heads of L x d_h, operands in multi-head
+ * packing: heads padded to H_p = next power of two, g = N/(2 L H_p)
+ * columns per head per ciphertext, J = ceil(d_h / g) ciphertexts per operand;
+ * block c*H_p + h of ciphertext j holds column j*g + c of head h (this is the
+ * layout blb_mhp_column_map gives the QKV ct-pt MatMul outputs).
+ * BSGS: t = u*B + i, B*G = L, g | B (bsgs_B = 0 selects B = g).  Consumes 3
+ * levels: operands at `level` >= 3, outputs at level-3.  Output o (< L/g) is
+ * diagonal-packed: block e*H_p + h, row p holds C_h[p, (p + o*g + e) mod L]. */
+blb_status blb_qk_plan_create(const blb_params *params, int L, int heads, int d_h, int bsgs_B, int level,
+                              blb_qk_plan **out);
+void blb_qk_plan_destroy(blb_qk_plan *plan);
+/* Host outputs (nullable): J, number of outputs, g, B, G, rotations, mask plaintexts. */
+blb_status blb_qk_plan_info(const blb_qk_plan *plan, int *J, int *n_out, int *g, int *B, int *G, int *n_rotations,
+                            int *n_masks);
+/* Rotation steps needed (the relinearisation key, Galois element 0, is needed too). */
+blb_status blb_qk_plan_rotations(const blb_qk_plan *plan, int32_t *steps, int *n);
+/* Offline precompute (row a0): encode all mask plaintexts into `masks` (device,
+ * blb_qk_mask_bytes bytes).  Synchronises. */
+size_t blb_qk_mask_bytes(const blb_qk_plan *plan);
+blb_status blb_qk_encode_masks(const blb_qk_plan *plan, uint64_t *masks, void *stream);
+size_t blb_qk_workspace_bytes(const blb_qk_plan *plan);
+/* Evaluate: Q[0..J), K[0..J) at the plan level -> out[0..L/g) at level-3.
+ * Scale of every output = (Q.scale * K.scale) / q_{level-1} (masks are encoded at
+ * the scale of the prime their rescale drops). */
+blb_status blb_ct_ct_qk(const blb_qk_plan *plan, const blb_keys *keys, const blb_ct *Q, const blb_ct *K, int J,
+                        const uint64_t *masks, blb_ct *out, void *ws, size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -93,6 +93,15 @@ def lib() -> ctypes.CDLL:
             "blb_matmul_workspace_bytes": ([vp, ctypes.c_int], ctypes.c_size_t),
             "blb_ct_pt_matmul": ([vp, vp, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t,
                                   vp], ctypes.c_int),
+            "blb_qk_plan_create": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp],
+                                   ctypes.c_int),
+            "blb_qk_plan_destroy": ([vp], None),
+            "blb_qk_plan_info": ([vp, ip, ip, ip, ip, ip, ip, ip], ctypes.c_int),
+            "blb_qk_plan_rotations": ([vp, vp, ip], ctypes.c_int),
+            "blb_qk_mask_bytes": ([vp], ctypes.c_size_t),
+            "blb_qk_encode_masks": ([vp, vp, vp], ctypes.c_int),
+            "blb_qk_workspace_bytes": ([vp], ctypes.c_size_t),
+            "blb_ct_ct_qk": ([vp, vp, vp, vp, ctypes.c_int, vp, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
         }
         for name, (args, res) in sigs.items():
             f = getattr(L, name)
@@ -424,5 +433,54 @@ class MatmulPlan:
         _check(lib().blb_ct_pt_matmul(self._h, keys.handle, cin, len(cts), _ptr(pts), out_first, out_count, cout,
                                       _ptr(ws), ws.numel() * 8, _stream()))
         for o, c in zip(outs, cout):
+            o.level, o.scale = c.level, c.scale
+        return outs
+
+
+class QKPlan:
+    """blb_qk_plan_create: ct-ct MatMul Q_h K_h^T for all heads (row a7, reading C13)."""
+
+    def __init__(self, params: Params, L: int, heads: int, d_h: int, bsgs_B: int = 0, level: int | None = None):
+        self.params = params
+        self.level = params.K - 2 if level is None else level
+        h = ctypes.c_void_p()
+        _check(lib().blb_qk_plan_create(params.handle, L, heads, d_h, bsgs_B, self.level, ctypes.byref(h)))
+        self._h = h
+        vals = [ctypes.c_int() for _ in range(7)]
+        _check(lib().blb_qk_plan_info(h, *[ctypes.byref(v) for v in vals]))
+        self.J, self.n_out, self.g, self.B, self.G, self.n_rotations, self.n_masks = [v.value for v in vals]
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.blb_qk_plan_destroy(self._h)
+            self._h = None
+
+    def rotation_steps(self) -> list[int]:
+        n = ctypes.c_int(0)
+        _check(lib().blb_qk_plan_rotations(self._h, None, ctypes.byref(n)))
+        buf = (ctypes.c_int32 * max(1, n.value))()
+        _check(lib().blb_qk_plan_rotations(self._h, buf, ctypes.byref(n)))
+        return [int(buf[i]) for i in range(n.value)]
+
+    def encode_masks(self) -> torch.Tensor:
+        nbytes = int(lib().blb_qk_mask_bytes(self._h))
+        masks = torch.empty(nbytes // 8, dtype=torch.int64, device="cuda")
+        _check(lib().blb_qk_encode_masks(self._h, _ptr(masks), _stream()))
+        return masks
+
+    def workspace_bytes(self) -> int:
+        return int(lib().blb_qk_workspace_bytes(self._h))
+
+    def __call__(self, keys: Keys, Q: list, K: list, masks: torch.Tensor, ws: torch.Tensor | None = None,
+                 outs: list | None = None) -> list:
+        ws = torch.empty(self.workspace_bytes() // 8 + 1, dtype=torch.int64, device="cuda") if ws is None else ws
+        if outs is None:
+            outs = [Ciphertext.empty(self.params, self.level - 3) for _ in range(self.n_out)]
+        cq = (_Ct * len(Q))(*[c.c() for c in Q])
+        ck = (_Ct * len(K))(*[c.c() for c in K])
+        co = (_Ct * self.n_out)(*[o.c() for o in outs])
+        _check(lib().blb_ct_ct_qk(self._h, keys.handle, cq, ck, len(Q), _ptr(masks), co, _ptr(ws), ws.numel() * 8,
+                                  _stream()))
+        for o, c in zip(outs, co):
             o.level, o.scale = c.level, c.scale
         return outs

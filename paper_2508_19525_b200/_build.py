@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libblb.so")
 ROOT = os.path.dirname(HERE)
 
-CU = ["ntt.cu", "kernels.cu", "encode.cu", "matmul.cu", "api.cu"]
+CU = ["ntt.cu", "kernels.cu", "encode.cu", "matmul.cu", "qk.cu", "api.cu"]
 CPP = ["host_tables.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

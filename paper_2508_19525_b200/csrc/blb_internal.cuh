@@ -201,6 +201,11 @@ blb_status launch_encode(const blb_params *P, const double *slots, int n_pts, do
                          double *dd_scratch, int *d_flag, cudaStream_t st);
 size_t encode_scratch_doubles(const blb_params *P, int n_pts);
 
+// MAC: acc[o] = sum_{e in [ent_start[o0+o], ent_start[o0+o+1])} pt[ent_pt[e] or e - e_base] (.) R[ent_r[e]]
+// (pt entries [k][N], R entries [2][k][N], acc [n_o][2][k][N]; 128-bit lazy accumulation)
+blb_status launch_mac(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc, const int *ent_r, const int *ent_pt,
+                      const int *ent_start, int o0, int e_base, int n_o, int n_entries, int k, cudaStream_t st);
+
 // ChaCha / sampling
 enum { TAG_SECRET = 1, TAG_KEY_A = 2, TAG_KEY_E = 3, TAG_ENC_A = 4, TAG_ENC_E = 5, TAG_MASK = 6 };
 struct ChachaKey {

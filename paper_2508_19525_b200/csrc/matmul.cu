@@ -77,13 +77,14 @@ __global__ void k_build_slots(PlanDev pd, const int *ent_bi, const int *ent_o, i
     slots[(long long)e * pd.n + s] = v;
 }
 
-// acc[o][p][l][x] = sum_{e in o} pt[e][l][x] * R[bi_e][p][l][x]   (o = local (b', g))
+// acc[o][p][l][x] = sum_{e in o} pt[pt_e][l][x] * R[r_e][p][l][x]   (o = local output)
+// pt_e = ent_pt[e] (or e - e_base when ent_pt == nullptr: plaintexts stored in entry order).
 // 1-D grid: bid = (l * n_tiles + tile) * n_o + o  -> the output index varies
 // fastest, so concurrent CTAs share the same R tile through L2.
 __global__ void __launch_bounds__(kTB) k_mac(const u64 *__restrict__ pt, const u64 *__restrict__ R,
-                                             u64 *__restrict__ acc, const int *__restrict__ ent_bi,
-                                             const int *__restrict__ ent_start, int o0, int e_base, int n_o, int k,
-                                             int logN, Primes pr) {
+                                             u64 *__restrict__ acc, const int *__restrict__ ent_r,
+                                             const int *__restrict__ ent_pt, const int *__restrict__ ent_start,
+                                             int o0, int e_base, int n_o, int k, int logN, Primes pr) {
     const int N = 1 << logN;
     const int n_tiles = N / (2 * kTB);
     int bid = blockIdx.x;
@@ -99,8 +100,9 @@ __global__ void __launch_bounds__(kTB) k_mac(const u64 *__restrict__ pt, const u
     const long long lx = (long long)l * N + x;
 #pragma unroll 4
     for (int e = e_lo; e < e_hi; e++) {
-        const int bi = ent_bi[e];
-        const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(pt + (long long)(e - e_base) * kN + lx);
+        const int bi = ent_r[e];
+        const int pe = ent_pt ? ent_pt[e] : e - e_base;
+        const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(pt + (long long)pe * kN + lx);
         const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(R + (long long)bi * 2 * kN + lx);
         const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(R + ((long long)bi * 2 + 1) * kN + lx);
         a00.mac(pv.x, r0.x); a01.mac(pv.y, r0.y);
@@ -132,6 +134,21 @@ __global__ void k_copy_ct(const u64 *src, u64 *dst, long long n) {
     if (x < n) dst[x] = src[x];
 }
 }  // namespace
+
+blb_status launch_mac(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc, const int *ent_r, const int *ent_pt,
+                      const int *ent_start, int o0, int e_base, int n_o, int n_entries, int k, cudaStream_t st) {
+    if (n_o <= 0) return BLB_OK;
+    const int N = P->N;
+    const int n_tiles = N / (2 * kTB);
+    cudaEvent_t t0 = blb_timing_begin(st);
+    k_mac<<<(unsigned)((size_t)n_o * n_tiles * k), kTB, 0, st>>>(pt, R, acc, ent_r, ent_pt, ent_start, o0, e_base, n_o,
+                                                                k, P->logN, P->pr);
+    BLB_COUNT_LAUNCH(1);
+    BLB_COUNT(3, n_entries);
+    blb_timing_end(0, t0, st, (double)n_entries * k * N * 8.0);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
 
 // ------------------------------------------------------------------ plan
 static bool nz_entry(const blb_matmul_plan *pl, int b, int bp, int t) {
@@ -482,16 +499,8 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
     {
         const int o0 = out_first * pl->G, n_o = out_count * pl->G;
         const int e_base = pl->ent_start[o0];
-        const int n_tiles = N / (2 * kTB);
-        if (n_o > 0) {
-            cudaEvent_t t0 = blb_timing_begin(st);
-            k_mac<<<(unsigned)((size_t)n_o * n_tiles * k), kTB, 0, st>>>(pt_dev, R, acc, pl->d_ent, pl->d_ent_start, o0,
-                                                                        e_base, n_o, k, P->logN, P->pr);
-            BLB_COUNT_LAUNCH(1);
-            BLB_COUNT(3, pl->ent_start[o0 + n_o] - e_base);
-            blb_timing_end(0, t0, st, (double)(pl->ent_start[o0 + n_o] - e_base) * k * N * 8.0);
-            BLB_CHECK_LAUNCH();
-        }
+        BLB_TRY(launch_mac(P, pt_dev, R, acc, pl->d_ent, nullptr, pl->d_ent_start, o0, e_base, n_o,
+                           pl->ent_start[o0 + n_o] - e_base, k, st));
     }
     // 4. giant steps: acc[b'][0] += Rot_{gBL}(acc[b'][g])
     {

@@ -1,0 +1,598 @@
+// qk.cu -- BLB's rotation-efficient ct-ct MatMul Q_h K_h^T for all heads (row a7).
+//
+// Sec. 5.1: Observations 1-2, the three steps, multi-head packing
+// (MHP) and BSGS with the giant step deferred into step 3 (App. C.1,
+// P:1203-1207); the masks follow DESIGN.md reading C13 (the paper's figures are
+// elided).  With t = u*B + i:
+//   K'_i  = sum_c Mnw_{c,i} (.) Rot_s(K) + Mw_{c,i} (.) Rot_{s-L}(K),  s = (c+i) mod L   (hoisted)
+//   Q_u   = Mq_{u,hi} (.) Rot_{-uB}(Q) + Mq_{u,lo} (.) Rot_{L-uB}(Q)                     (hoisted)
+//   S_ui  = rescale(relin(sum_j Q_u^(j) (x) K'_i^(j)))
+//   T_ui  = Rot_{-i H_p L}(S_ui)
+//   A_uwf = rescale(sum_i M3_{u,i,w,f} (.) T_ui);  out[(uB + wg) mod L / g] += Rot_{uB or uB-L}(A_uwf)
+// GPU mapping: every mask stage is one launch of the MAC kernel (masks are
+// plaintexts shared by all J ciphertexts), all rotations of one ciphertext
+// share one ModUp, independent rotations / relinearisations run 32 key
+// switches per launch group, the J-sum of the tensor products is one kernel
+// with 128-bit lazy accumulation, rescales are batched over all ciphertexts
+// of a stage.
+#include <algorithm>
+#include <map>
+#include <set>
+#include "blb_internal.cuh"
+
+extern "C" uint32_t blb_galois_element(const blb_params *P, int32_t step);
+
+struct MaskDesc {
+    int type;  // 0: K (c, i, wrap)  1: Q (u, low)  2: step 3 (u, i, w, f)
+    int a, b, c, d;
+};
+
+struct blb_qk_plan {
+    const blb_params *P;
+    int L, H, Hp, dh, n, g, J, B, G, level;
+    std::vector<int32_t> k_rots, q_rots;         // non-zero left rotations (slots)
+    std::vector<MaskDesc> m1, m3;                // stage-1 masks (level), stage-3 masks (level-2)
+    // MAC entry lists (CSR): K' outputs o = i*J + j; Q outputs o = (u-1)*J + j; A outputs = accumulators
+    std::vector<int> kp_start, kp_r, kp_pt, qp_start, qp_r, qp_pt, a_start, a_r, a_pt;
+    struct Acc {
+        int u, w, f, out, rot;
+    };
+    std::vector<Acc> accs;
+    std::vector<int32_t> steps;
+    int *d_ent = nullptr;  // all entry arrays, device
+    size_t off_kp_start, off_kp_r, off_kp_pt, off_qp_start, off_qp_r, off_qp_pt, off_a_start, off_a_r, off_a_pt;
+    MaskDesc *d_m1 = nullptr, *d_m3 = nullptr;
+};
+
+namespace {
+constexpr int kTB = 256;
+
+struct QKDev {
+    int L, Hp, g, B, n;
+};
+__global__ void k_mask_slots(const MaskDesc *descs, int m0, QKDev q, double *slots) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    const int e = blockIdx.y;
+    if (s >= q.n) return;
+    const MaskDesc D = descs[m0 + e];
+    const int blk = s / q.L, p = s - blk * q.L, c = blk / q.Hp;
+    bool v = false;
+    if (D.type == 0) {
+        const int sh = (D.a + D.b) % q.L;
+        v = (c == D.a) && (D.c ? (p + sh >= q.L) : (p + sh < q.L));
+    } else if (D.type == 1) {
+        const int a = D.a * q.B;
+        v = D.b ? (p < a) : (p >= a);
+    } else {
+        const int i = D.b;
+        const int cc = ((c - i) % q.g + q.g) % q.g;
+        const int w = (cc + i) / q.g;
+        const int a = D.a * q.B;
+        v = (w == D.c) && (D.d == 0 ? (p >= a) : (p < a));
+    }
+    slots[(long long)e * q.n + s] = v ? 1.0 : 0.0;
+}
+
+// D[o][0..2] = sum_j (a0 b0, a0 b1 + a1 b0, a1 b1) with a = Qp[u*J + j], b = Kp[i*J + j], o = u*B + i
+__global__ void k_tensor_sum(const u64 *Qp, const u64 *Kp, u64 *D, Primes pr, int J, int B, int k, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int l = blockIdx.y, o = blockIdx.z;
+    if (x >= N) return;
+    const int u = o / B, i = o - u * B;
+    const long long kN = (long long)k * N, lx = (long long)l * N + x;
+    Acc128 d0, d1, d2;
+    d0.zero(); d1.zero(); d2.zero();
+    for (int j = 0; j < J; j++) {
+        const u64 *a = Qp + (long long)(u * J + j) * 2 * kN + lx;
+        const u64 *b = Kp + (long long)(i * J + j) * 2 * kN + lx;
+        const u64 a0 = a[0], a1 = a[kN], b0 = b[0], b1 = b[kN];
+        d0.mac(a0, b0);
+        d1.mac(a0, b1);
+        d1.mac(a1, b0);
+        d2.mac(a1, b1);
+    }
+    const ModConst &mc = pr.m[l];
+    u64 *out = D + (long long)o * 3 * kN + lx;
+    out[0] = d0.reduce(mc);
+    out[kN] = d1.reduce(mc);
+    out[2 * kN] = d2.reduce(mc);
+}
+
+// dst[p][i][x] = src[p][i][x] for i < k_dst (src has k_src limbs per poly): exact level drop / copy
+__global__ void k_copy_limbs(const u64 *src, u64 *dst, int k_src, int k_dst, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y, p = blockIdx.z;
+    if (x >= N) return;
+    dst[((long long)p * k_dst + i) * N + x] = src[((long long)p * k_src + i) * N + x];
+}
+
+struct SumList {
+    int n;
+    const u64 *src[64];
+};
+// out = sum of the listed ciphertexts ([2][k][N] each)
+__global__ void k_sum_list(SumList sl, u64 *out, Primes pr, int k, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int l = blockIdx.y, p = blockIdx.z;
+    if (x >= N) return;
+    const long long off = ((long long)p * k + l) * N + x;
+    const u64 q = pr.m[l].q;
+    u64 acc = 0;
+    for (int t = 0; t < sl.n; t++) acc = addmod(acc, sl.src[t][off], q);
+    out[off] = acc;
+}
+inline dim3 gx(int N, int y, int z) { return dim3((N + kTB - 1) / kTB, y, z); }
+}  // namespace
+
+// ---------------------------------------------------------------- plan
+static int wrap_class(int cprime, int i, int g) {
+    const int c = ((cprime - i) % g + g) % g;
+    return (c + i) / g;
+}
+
+extern "C" void blb_qk_plan_destroy(blb_qk_plan *pl) {
+    if (!pl) return;
+    cudaFree(pl->d_ent);
+    cudaFree(pl->d_m1);
+    cudaFree(pl->d_m3);
+    delete pl;
+}
+
+extern "C" blb_status blb_qk_plan_create(const blb_params *P, int L, int heads, int d_h, int bsgs_B, int level,
+                                         blb_qk_plan **out) {
+    if (!P || !out || L <= 0 || heads <= 0 || d_h <= 0) return BLB_E_INVALID_ARG;
+    const int n = P->N / 2;
+    int Hp = 1;
+    while (Hp < heads) Hp <<= 1;
+    if (n % (L * Hp)) {
+        blb_set_error("MHP needs L * H_p | N/2 (L=%d, H_p=%d, n=%d)", L, Hp, n);
+        return BLB_E_LAYOUT;
+    }
+    const int g = n / (L * Hp);
+    const int B = bsgs_B > 0 ? bsgs_B : g;
+    if (B % g || L % B) {
+        blb_set_error("ct-ct BSGS needs g | B | L (g=%d, B=%d, L=%d)", g, B, L);
+        return BLB_E_LAYOUT;
+    }
+    if (level < 3 || level >= P->K) {
+        blb_set_error("ct-ct MatMul consumes 3 levels: input level %d must be in [3, %d)", level, P->K);
+        return BLB_E_LEVEL;
+    }
+    auto *pl = new blb_qk_plan();
+    pl->P = P; pl->L = L; pl->H = heads; pl->Hp = Hp; pl->dh = d_h; pl->n = n; pl->g = g;
+    pl->J = (d_h + g - 1) / g; pl->B = B; pl->G = L / B; pl->level = level;
+    std::set<int32_t> ks, qs;
+    for (int c = 0; c < g; c++)
+        for (int i = 0; i < B; i++) {
+            const int s = (c + i) % L;
+            if (s) { ks.insert(s); ks.insert(s - L); }
+        }
+    for (int u = 1; u < pl->G; u++) { qs.insert(-u * B); qs.insert(L - u * B); }
+    pl->k_rots.assign(ks.begin(), ks.end());
+    pl->q_rots.assign(qs.begin(), qs.end());
+    const int NKR = 1 + (int)pl->k_rots.size();
+    auto kr_index = [&](int32_t r) -> int {
+        if (r == 0) return 0;
+        return 1 + (int)(std::lower_bound(pl->k_rots.begin(), pl->k_rots.end(), r) - pl->k_rots.begin());
+    };
+    const int NQR = (int)pl->q_rots.size();
+    auto qr_index = [&](int32_t r) -> int {
+        return (int)(std::lower_bound(pl->q_rots.begin(), pl->q_rots.end(), r) - pl->q_rots.begin());
+    };
+    // stage-1 masks: K (c, i, wrap), then Q (u, low)
+    std::map<std::tuple<int, int, int>, int> kmask;
+    for (int i = 0; i < B; i++)
+        for (int c = 0; c < g; c++) {
+            const int s = (c + i) % L;
+            for (int wrap = 0; wrap < (s ? 2 : 1); wrap++) {
+                kmask[{c, i, wrap}] = (int)pl->m1.size();
+                pl->m1.push_back({0, c, i, wrap, 0});
+            }
+        }
+    std::map<std::pair<int, int>, int> qmask;
+    for (int u = 1; u < pl->G; u++)
+        for (int low = 0; low < 2; low++) {
+            qmask[{u, low}] = (int)pl->m1.size();
+            pl->m1.push_back({1, u, low, 0, 0});
+        }
+    // K' MAC: output o = i*J + j, entries over c (and wrap), R = Kr[j][kr_index(r)]
+    pl->kp_start.push_back(0);
+    for (int i = 0; i < B; i++)
+        for (int j = 0; j < pl->J; j++) {
+            for (int c = 0; c < g; c++) {
+                const int s = (c + i) % L;
+                for (int wrap = 0; wrap < (s ? 2 : 1); wrap++) {
+                    const int r = wrap ? s - L : s;
+                    pl->kp_r.push_back(j * NKR + kr_index(r));
+                    pl->kp_pt.push_back(kmask[{c, i, wrap}]);
+                }
+            }
+            pl->kp_start.push_back((int)pl->kp_r.size());
+        }
+    // Q MAC: output o = (u-1)*J + j, two entries
+    pl->qp_start.push_back(0);
+    for (int u = 1; u < pl->G; u++)
+        for (int j = 0; j < pl->J; j++) {
+            const int a = u * B;
+            pl->qp_r.push_back(j * NQR + qr_index(-a));
+            pl->qp_pt.push_back(qmask[{u, 0}]);
+            pl->qp_r.push_back(j * NQR + qr_index(L - a));
+            pl->qp_pt.push_back(qmask[{u, 1}]);
+            pl->qp_start.push_back((int)pl->qp_r.size());
+        }
+    // step 3: accumulators (u, w, f) with a non-zero mask
+    const int wmax = (g - 1 + B - 1) / g;
+    pl->a_start.push_back(0);
+    for (int u = 0; u < pl->G; u++)
+        for (int w = 0; w <= wmax; w++)
+            for (int f = 0; f < 2; f++) {
+                const int a = u * B;
+                std::vector<int> terms;
+                for (int i = 0; i < B; i++) {
+                    bool any_block = false;
+                    for (int cp = 0; cp < g && !any_block; cp++) any_block = wrap_class(cp, i, g) == w;
+                    const bool any_pos = f == 0 ? (a < L) : (a > 0);
+                    if (any_block && any_pos) terms.push_back(i);
+                }
+                if (terms.empty()) continue;
+                for (int i : terms) {
+                    pl->a_r.push_back(u * B + i);
+                    pl->a_pt.push_back((int)pl->m3.size());
+                    pl->m3.push_back({2, u, i, w, f});
+                }
+                pl->a_start.push_back((int)pl->a_r.size());
+                const int rot = f == 0 ? u * B : u * B - L;
+                pl->accs.push_back({u, w, f, ((u * B + w * g) % L) / g, rot});
+            }
+    // rotation key set
+    std::set<int32_t> st(pl->k_rots.begin(), pl->k_rots.end());
+    st.insert(pl->q_rots.begin(), pl->q_rots.end());
+    for (int i = 1; i < B; i++) st.insert(-i * Hp * L);
+    for (auto &A : pl->accs)
+        if (((A.rot % n) + n) % n) st.insert(A.rot);
+    pl->steps.assign(st.begin(), st.end());
+    // device copies
+    std::vector<int> all;
+    auto put = [&](const std::vector<int> &v) {
+        const size_t o = all.size();
+        all.insert(all.end(), v.begin(), v.end());
+        return o;
+    };
+    pl->off_kp_start = put(pl->kp_start); pl->off_kp_r = put(pl->kp_r); pl->off_kp_pt = put(pl->kp_pt);
+    pl->off_qp_start = put(pl->qp_start); pl->off_qp_r = put(pl->qp_r); pl->off_qp_pt = put(pl->qp_pt);
+    pl->off_a_start = put(pl->a_start); pl->off_a_r = put(pl->a_r); pl->off_a_pt = put(pl->a_pt);
+    cudaError_t e = cudaMalloc(&pl->d_ent, sizeof(int) * std::max<size_t>(all.size(), 1));
+    if (e == cudaSuccess) e = cudaMemcpy(pl->d_ent, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&pl->d_m1, sizeof(MaskDesc) * pl->m1.size());
+    if (e == cudaSuccess)
+        e = cudaMemcpy(pl->d_m1, pl->m1.data(), sizeof(MaskDesc) * pl->m1.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&pl->d_m3, sizeof(MaskDesc) * pl->m3.size());
+    if (e == cudaSuccess)
+        e = cudaMemcpy(pl->d_m3, pl->m3.data(), sizeof(MaskDesc) * pl->m3.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        blb_set_error("qk plan upload: %s", cudaGetErrorString(e));
+        blb_qk_plan_destroy(pl);
+        return BLB_E_CUDA;
+    }
+    *out = pl;
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_qk_plan_info(const blb_qk_plan *pl, int *J, int *n_out, int *g, int *B, int *G,
+                                       int *n_rotations, int *n_masks) {
+    if (!pl) return BLB_E_INVALID_ARG;
+    if (J) *J = pl->J;
+    if (n_out) *n_out = pl->L / pl->g;
+    if (g) *g = pl->g;
+    if (B) *B = pl->B;
+    if (G) *G = pl->G;
+    if (n_rotations) {
+        int nf = 0;
+        for (auto &A : pl->accs)
+            if (((A.rot % pl->n) + pl->n) % pl->n) nf++;
+        *n_rotations = pl->J * (int)(pl->k_rots.size() + pl->q_rots.size()) + pl->G * (pl->B - 1) + nf;
+    }
+    if (n_masks) *n_masks = (int)(pl->m1.size() + pl->m3.size());
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_qk_plan_rotations(const blb_qk_plan *pl, int32_t *steps, int *n) {
+    if (!pl || !n) return BLB_E_INVALID_ARG;
+    const int need = (int)pl->steps.size();
+    if (steps) {
+        if (*n < need) return BLB_E_INVALID_ARG;
+        for (int i = 0; i < need; i++) steps[i] = pl->steps[i];
+    }
+    *n = need;
+    return BLB_OK;
+}
+
+static size_t qk_mask_elems(const blb_qk_plan *pl) {
+    const size_t N = pl->P->N;
+    return pl->m1.size() * (size_t)(pl->level + 1) * N + pl->m3.size() * (size_t)(pl->level - 1) * N;
+}
+extern "C" size_t blb_qk_mask_bytes(const blb_qk_plan *pl) { return pl ? qk_mask_elems(pl) * sizeof(u64) : 0; }
+
+extern "C" blb_status blb_qk_encode_masks(const blb_qk_plan *pl, uint64_t *masks, void *stream) {
+    if (!pl || !masks) return BLB_E_INVALID_ARG;
+    const blb_params *P = pl->P;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int chunk = 64;
+    double *slots = nullptr, *buf = nullptr;
+    int *flag = nullptr;
+    BLB_CUDA_TRY(cudaMallocAsync(&slots, sizeof(double) * (size_t)chunk * pl->n, st));
+    BLB_CUDA_TRY(cudaMallocAsync(&buf, sizeof(double) * encode_scratch_doubles(P, chunk), st));
+    BLB_CUDA_TRY(cudaMallocAsync(&flag, sizeof(int), st));
+    BLB_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    QKDev qd{pl->L, pl->Hp, pl->g, pl->B, pl->n};
+    blb_status s = BLB_OK;
+    // stage 1 at level l (scale q_l), stage 3 at level l-2 (scale q_{l-2}): the primes the next rescales drop
+    for (int stage = 0; stage < 2 && s == BLB_OK; stage++) {
+        const MaskDesc *dm = stage == 0 ? pl->d_m1 : pl->d_m3;
+        const int cnt_all = (int)(stage == 0 ? pl->m1.size() : pl->m3.size());
+        const int lvl = stage == 0 ? pl->level : pl->level - 2;
+        u64 *base = masks + (stage == 0 ? 0 : pl->m1.size() * (size_t)(pl->level + 1) * P->N);
+        for (int m0 = 0; m0 < cnt_all && s == BLB_OK; m0 += chunk) {
+            const int cnt = std::min(chunk, cnt_all - m0);
+            k_mask_slots<<<dim3((pl->n + kTB - 1) / kTB, cnt), kTB, 0, st>>>(dm, m0, qd, slots);
+            BLB_COUNT_LAUNCH(1);
+            s = launch_encode(P, slots, cnt, (double)P->mod[lvl], lvl, base + (size_t)m0 * (lvl + 1) * P->N, buf, flag,
+                              st);
+        }
+    }
+    cudaFreeAsync(slots, st);
+    cudaFreeAsync(buf, st);
+    cudaFreeAsync(flag, st);
+    BLB_CUDA_TRY(cudaStreamSynchronize(st));
+    return s;
+}
+
+// workspace layout
+struct QKWs {
+    size_t kr, qr, kacc, kp, qacc, qp, d, s, sr, t, aacc, ar, arot, ext, coef, ks, resc, total;
+};
+static QKWs qk_ws(const blb_qk_plan *pl) {
+    const blb_params *P = pl->P;
+    const size_t N = P->N, k = pl->level + 1, k1 = k - 1, k2 = k - 2, k3 = k - 3;
+    const size_t E = k + P->np, beta = blb_beta(P, pl->level);
+    const size_t J = pl->J, B = pl->B, G = pl->G, NA = pl->accs.size();
+    const size_t NKR = 1 + pl->k_rots.size(), NQR = pl->q_rots.size();
+    QKWs w{};
+    size_t o = 0;
+    w.kr = o; o += J * NKR * 2 * k * N;
+    w.qr = o; o += J * NQR * 2 * k * N;
+    w.kacc = o; o += B * J * 2 * k * N;
+    w.kp = o; o += B * J * 2 * k1 * N;
+    w.qacc = o; o += (G > 1 ? (G - 1) : 1) * J * 2 * k * N;
+    w.qp = o; o += G * J * 2 * k1 * N;
+    w.d = o; o += G * B * 3 * k1 * N;
+    w.s = o; o += G * B * 2 * k1 * N;
+    w.sr = o; o += G * B * 2 * k2 * N;
+    w.t = o; o += G * B * 2 * k2 * N;
+    w.aacc = o; o += NA * 2 * k2 * N;
+    w.ar = o; o += NA * 2 * k3 * N;
+    w.arot = o; o += NA * 2 * k3 * N;
+    w.ext = o; o += (size_t)kMaxJobs * beta * E * N;
+    w.coef = o; o += (size_t)kMaxJobs * k * N;
+    w.ks = o; o += keyswitch_scratch_elems(P, pl->level, kMaxJobs);
+    const size_t maxct = std::max({B * J, G * J, G * B, NA});
+    w.resc = o; o += 2 * maxct * (1 + k) * N;
+    w.total = o;
+    return w;
+}
+extern "C" size_t blb_qk_workspace_bytes(const blb_qk_plan *pl) { return pl ? qk_ws(pl).total * sizeof(u64) + 256 : 0; }
+
+static const u64 *key_for(const blb_keys *K, uint32_t g) {
+    for (size_t i = 0; i < K->galois.size(); i++)
+        if (K->galois[i] == g) return K->data[i];
+    return nullptr;
+}
+
+// rotations of independent inputs (each its own ModUp), <= kMaxJobs per launch group
+static blb_status rotate_independent(const blb_params *P, const blb_keys *keys, int level, const std::vector<const u64 *> &in,
+                                     const std::vector<int32_t> &steps, const std::vector<u64 *> &out, u64 *ext, u64 *coef,
+                                     u64 *ks, cudaStream_t st) {
+    const int k = level + 1, N = P->N, E = k + P->np, beta = blb_beta(P, level);
+    u64 *ks_u = ks, *ks_conv = ks + (size_t)kMaxJobs * 2 * E * N;
+    for (size_t t0 = 0; t0 < in.size(); t0 += kMaxJobs) {
+        const int cnt = (int)std::min<size_t>(kMaxJobs, in.size() - t0);
+        std::vector<const u64 *> c1(cnt);
+        std::vector<KsJob> jobs(cnt);
+        for (int t = 0; t < cnt; t++) {
+            c1[t] = in[t0 + t] + (size_t)k * N;
+            const uint32_t g = blb_galois_element(P, steps[t0 + t]);
+            KsJob J{};
+            J.ext = ext + (size_t)t * beta * E * N;
+            J.key = key_for(keys, g);
+            J.c0 = in[t0 + t];
+            J.out = out[t0 + t];
+            J.galois = g;
+            J.add_mode = 1;
+            jobs[t] = J;
+        }
+        BLB_TRY(launch_modup(P, level, c1.data(), cnt, ext, coef, st));
+        BLB_TRY(launch_keyswitch(P, level, jobs.data(), cnt, ks_u, ks_conv, st));
+    }
+    return BLB_OK;
+}
+
+// all rotations of one ciphertext share one ModUp (hoisting, C8)
+static blb_status rotate_hoisted(const blb_params *P, const blb_keys *keys, int level, const u64 *in,
+                                 const std::vector<int32_t> &steps, u64 *out_base, size_t out_stride, u64 *ext,
+                                 u64 *coef, u64 *ks, cudaStream_t st) {
+    const int k = level + 1, N = P->N, E = k + P->np;
+    u64 *ks_u = ks, *ks_conv = ks + (size_t)kMaxJobs * 2 * E * N;
+    const u64 *c1 = in + (size_t)k * N;
+    BLB_TRY(launch_modup(P, level, &c1, 1, ext, coef, st));
+    for (size_t t0 = 0; t0 < steps.size(); t0 += kMaxJobs) {
+        const int cnt = (int)std::min<size_t>(kMaxJobs, steps.size() - t0);
+        std::vector<KsJob> jobs(cnt);
+        for (int t = 0; t < cnt; t++) {
+            const uint32_t g = blb_galois_element(P, steps[t0 + t]);
+            KsJob J{};
+            J.ext = ext;
+            J.key = key_for(keys, g);
+            J.c0 = in;
+            J.out = out_base + (t0 + t) * out_stride;
+            J.galois = g;
+            J.add_mode = 1;
+            jobs[t] = J;
+        }
+        BLB_TRY(launch_keyswitch(P, level, jobs.data(), cnt, ks_u, ks_conv, st));
+    }
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, const blb_ct *Q, const blb_ct *K, int J,
+                                   const uint64_t *masks, blb_ct *out, void *ws, size_t ws_bytes, void *stream) {
+    if (!pl || !keys || !Q || !K || !masks || !out || !ws) return BLB_E_INVALID_ARG;
+    if (J != pl->J) {
+        blb_set_error("blb_ct_ct_qk: %d ciphertexts per operand, plan needs J = %d", J, pl->J);
+        return BLB_E_LAYOUT;
+    }
+    const blb_params *P = pl->P;
+    const int lvl = pl->level, k = lvl + 1, k1 = k - 1, k2 = k - 2, k3 = k - 3, N = P->N;
+    const int B = pl->B, G = pl->G, NA = (int)pl->accs.size();
+    for (int j = 0; j < J; j++)
+        if (Q[j].level != lvl || K[j].level != lvl || !Q[j].data || !K[j].data) {
+            blb_set_error("blb_ct_ct_qk: operands must be at the plan level %d", lvl);
+            return BLB_E_LEVEL;
+        }
+    for (int32_t s : pl->steps)
+        if (!key_for(keys, blb_galois_element(P, s))) {
+            blb_set_error("missing rotation key for step %d", s);
+            return BLB_E_MISSING_KEY;
+        }
+    const u64 *rlk = key_for(keys, 0);
+    if (!rlk) {
+        blb_set_error("missing relinearisation key");
+        return BLB_E_MISSING_KEY;
+    }
+    const QKWs w = qk_ws(pl);
+    if (ws_bytes < w.total * sizeof(u64)) {
+        blb_set_error("workspace too small: %zu < %zu", ws_bytes, w.total * sizeof(u64));
+        return BLB_E_NOMEM;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    u64 *W = (u64 *)ws;
+    const int *E = pl->d_ent;
+    const size_t ct_k = (size_t)2 * k * N, ct_k1 = (size_t)2 * k1 * N, ct_k2 = (size_t)2 * k2 * N,
+                 ct_k3 = (size_t)2 * k3 * N;
+    const int NKR = 1 + (int)pl->k_rots.size(), NQR = (int)pl->q_rots.size();
+    const u64 *m1 = masks, *m3 = masks + pl->m1.size() * (size_t)k * N;
+
+    // 1. baby side: hoisted rotations of every K^(j), K' = MAC(masks, Kr), rescale
+    for (int j = 0; j < J; j++) {
+        u64 *kr = W + w.kr + (size_t)j * NKR * ct_k;
+        cudaMemcpyAsync(kr, K[j].data, ct_k * sizeof(u64), cudaMemcpyDeviceToDevice, st);
+        BLB_TRY(rotate_hoisted(P, keys, lvl, K[j].data, pl->k_rots, kr + ct_k, ct_k, W + w.ext, W + w.coef, W + w.ks, st));
+    }
+    BLB_TRY(launch_mac(P, m1, W + w.kr, W + w.kacc, E + pl->off_kp_r, E + pl->off_kp_pt, E + pl->off_kp_start, 0, 0,
+                       B * J, (int)pl->kp_r.size(), k, st));
+    BLB_TRY(launch_rescale(P, W + w.kacc, lvl, 2 * B * J, W + w.kp, W + w.resc, st));
+    // 2. giant side: Q_0 = level drop, Q_u = MAC(masks, Rot(Q)), rescale
+    for (int j = 0; j < J; j++) {
+        if (NQR)
+            BLB_TRY(rotate_hoisted(P, keys, lvl, Q[j].data, pl->q_rots, W + w.qr + (size_t)j * NQR * ct_k, ct_k,
+                                   W + w.ext, W + w.coef, W + w.ks, st));
+        k_copy_limbs<<<gx(N, k1, 2), kTB, 0, st>>>(Q[j].data, W + w.qp + (size_t)j * ct_k1, k, k1, N);
+        BLB_COUNT_LAUNCH(1);
+    }
+    if (G > 1) {
+        BLB_TRY(launch_mac(P, m1, W + w.qr, W + w.qacc, E + pl->off_qp_r, E + pl->off_qp_pt, E + pl->off_qp_start, 0, 0,
+                           (G - 1) * J, (int)pl->qp_r.size(), k, st));
+        BLB_TRY(launch_rescale(P, W + w.qacc, lvl, 2 * (G - 1) * J, W + w.qp + (size_t)J * ct_k1, W + w.resc, st));
+    }
+    // 3. products summed over j, relinearisation (one per (u, i)), rescale
+    k_tensor_sum<<<gx(N, k1, G * B), kTB, 0, st>>>(W + w.qp, W + w.kp, W + w.d, P->pr, J, B, k1, N);
+    BLB_COUNT_LAUNCH(1);
+    BLB_COUNT(3, (size_t)G * B * J);
+    BLB_CHECK_LAUNCH();
+    {
+        const int E1 = k1 + P->np, beta1 = blb_beta(P, lvl - 1);
+        u64 *ks_u = W + w.ks, *ks_conv = W + w.ks + (size_t)kMaxJobs * 2 * E1 * N;
+        for (int o0 = 0; o0 < G * B; o0 += kMaxJobs) {
+            const int cnt = std::min(kMaxJobs, G * B - o0);
+            std::vector<const u64 *> d2(cnt);
+            std::vector<KsJob> jobs(cnt);
+            for (int t = 0; t < cnt; t++) {
+                const u64 *D = W + w.d + (size_t)(o0 + t) * 3 * k1 * N;
+                d2[t] = D + (size_t)2 * k1 * N;
+                KsJob Jb{};
+                Jb.ext = W + w.ext + (size_t)t * beta1 * E1 * N;
+                Jb.key = rlk;
+                Jb.c0 = D;
+                Jb.c1_add = D + (size_t)k1 * N;
+                Jb.out = W + w.s + (size_t)(o0 + t) * ct_k1;
+                Jb.galois = 1;
+                Jb.add_mode = 2;
+                jobs[t] = Jb;
+            }
+            BLB_TRY(launch_modup(P, lvl - 1, d2.data(), cnt, W + w.ext, W + w.coef, st));
+            BLB_TRY(launch_keyswitch(P, lvl - 1, jobs.data(), cnt, ks_u, ks_conv, st));
+        }
+    }
+    BLB_TRY(launch_rescale(P, W + w.s, lvl - 1, 2 * G * B, W + w.sr, W + w.resc, st));
+    // 4. step 3: T_ui = Rot_{-i H_p L}(S_ui)
+    {
+        std::vector<const u64 *> in;
+        std::vector<int32_t> steps;
+        std::vector<u64 *> outp;
+        for (int u = 0; u < G; u++)
+            for (int i = 0; i < B; i++) {
+                const size_t o = (size_t)(u * B + i);
+                if (i == 0) {
+                    cudaMemcpyAsync(W + w.t + o * ct_k2, W + w.sr + o * ct_k2, ct_k2 * sizeof(u64),
+                                    cudaMemcpyDeviceToDevice, st);
+                    continue;
+                }
+                in.push_back(W + w.sr + o * ct_k2);
+                steps.push_back(-i * pl->Hp * pl->L);
+                outp.push_back(W + w.t + o * ct_k2);
+            }
+        BLB_TRY(rotate_independent(P, keys, lvl - 2, in, steps, outp, W + w.ext, W + w.coef, W + w.ks, st));
+    }
+    // 5. step-3 masks (MAC into the accumulators), rescale, deferred giant rotations, sums
+    BLB_TRY(launch_mac(P, m3, W + w.t, W + w.aacc, E + pl->off_a_r, E + pl->off_a_pt, E + pl->off_a_start, 0, 0, NA,
+                       (int)pl->a_r.size(), k2, st));
+    BLB_TRY(launch_rescale(P, W + w.aacc, lvl - 2, 2 * NA, W + w.ar, W + w.resc, st));
+    {
+        std::vector<const u64 *> in;
+        std::vector<int32_t> steps;
+        std::vector<u64 *> outp;
+        for (int a = 0; a < NA; a++) {
+            const int r = pl->accs[a].rot;
+            if (((r % pl->n) + pl->n) % pl->n == 0) continue;
+            in.push_back(W + w.ar + (size_t)a * ct_k3);
+            steps.push_back(r);
+            outp.push_back(W + w.arot + (size_t)a * ct_k3);
+        }
+        BLB_TRY(rotate_independent(P, keys, lvl - 3, in, steps, outp, W + w.ext, W + w.coef, W + w.ks, st));
+    }
+    const int n_out = pl->L / pl->g;
+    for (int o = 0; o < n_out; o++) {
+        if (!out[o].data) return BLB_E_INVALID_ARG;
+        SumList sl{};
+        for (int a = 0; a < NA; a++) {
+            if (pl->accs[a].out != o) continue;
+            const int r = pl->accs[a].rot;
+            const bool rotated = ((r % pl->n) + pl->n) % pl->n != 0;
+            if (sl.n >= 64) return BLB_E_LAYOUT;
+            sl.src[sl.n++] = (rotated ? W + w.arot : W + w.ar) + (size_t)a * ct_k3;
+        }
+        k_sum_list<<<gx(N, k3, 2), kTB, 0, st>>>(sl, out[o].data, P->pr, k3, N);
+        BLB_COUNT_LAUNCH(1);
+        out[o].level = lvl - 3;
+        // scale bookkeeping in the same floating-point order as the oracle: the masks
+        // (scale q_l, q_{l-2}) cancel in their rescales, the product rescale divides by q_{l-1}
+        const double ql = (double)P->mod[lvl], ql1 = (double)P->mod[lvl - 1], ql2 = (double)P->mod[lvl - 2];
+        int first_u = 0;
+        for (int a = 0; a < NA; a++)
+            if (pl->accs[a].out == o) { first_u = pl->accs[a].u; break; }
+        const double sq = first_u == 0 ? Q[0].scale : (Q[0].scale * ql) / ql;
+        const double sk = (K[0].scale * ql) / ql;
+        out[o].scale = (((sq * sk) / ql1) * ql2) / ql2;
+    }
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}

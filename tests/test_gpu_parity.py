@@ -327,3 +327,40 @@ def test_matmul_errors(toy):
     with pytest.raises(blb.BLBError) as e:
         blb.MatmulPlan(toy.g, 15, 16, 16)
     assert e.value.status == 6
+
+
+# ---------------------------------------------------------------- ct-ct Q K^T (row a7)
+@pytest.fixture(scope="module")
+def qktoy():
+    return Pair(bi.QKTOY)
+
+
+@pytest.mark.parametrize("H,L,dh,B", [(4, 32, 32, 0), (3, 16, 16, 0)])
+def test_qk_ct_ct_bit_exact(qktoy, H, L, dh, B):
+    import oracle.matmul_cc as cc
+    d = bi.qk_toy_inputs(H, L, dh)
+    plan_o = cc.plan_qk(L, H, dh, qktoy.n, B or None)
+    plan_g = blb.QKPlan(qktoy.g, L, H, dh, bsgs_B=B, level=3)
+    assert plan_g.rotation_steps() == plan_o.rotation_steps()
+    assert (plan_g.J, plan_g.n_out, plan_g.n_rotations) == (plan_o.J, plan_o.n_out, plan_o.counts()["rotations"])
+    steps = plan_g.rotation_steps()
+    okeys = O.keygen(qktoy.o, d["keys_key"], steps, relin=True)
+    gkeys, sk = blb.keygen(qktoy.g, d["keys_key"], steps, relin=True)
+    lvl, delta = 3, 2.0 ** 40
+    oq, ok, gq, gk = [], [], [], []
+    for j, (zq, zk) in enumerate(zip(cc.pack_mhp(d["Q"], plan_o), cc.pack_mhp(d["K"], plan_o))):
+        for z, cid, ol, gl in ((zq, j, oq, gq), (zk, 100 + j, ok, gk)):
+            pt = O.encode(qktoy.o, z, delta, lvl)
+            ol.append(O.encrypt(qktoy.o, d["enc_key"], okeys.s_ntt, pt, lvl, cid, delta))
+            gl.append(blb.encrypt(qktoy.g, sk, dev(pt), lvl, d["enc_key"], cid, delta))
+    masks = plan_g.encode_masks()
+    gout = plan_g(gkeys, gq, gk, masks)
+    oout = cc.qk_encrypted(qktoy.o, okeys, oq, ok, plan_o)
+    assert len(gout) == len(oout)
+    for a, b in zip(gout, oout):
+        assert a.level == b.level == 0 and a.scale == b.scale
+        assert np.array_equal(u64(a.data), b.data)
+    dec = [qktoy.g.decode(blb.decrypt(qktoy.g, sk, o), o.scale).cpu().numpy() for o in gout]
+    C = cc.unpack_diag(dec, plan_o)
+    ref = np.einsum("hik,hjk->hij", d["Q"], d["K"])
+    assert float(((C - ref) ** 2).mean()) <= 1e-11
