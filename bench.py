@@ -5,9 +5,10 @@ Metric (BASELINE.json): "ms per BERT-base layer fused-linear CKKS eval; NTT
 limbs/s and HBM GB/s fraction".  One step = one pass of the whole hot path over
 one layer's synthetic inputs: QKV ct-pt MatMul (C11, MHP) + out-projection
 (C12, diagonal input) + FFN1 + FFN2, every MatMul with hoisted baby-step
-rotations, MAC, giant-step key switches and rescale, then the CKKS->MPC masks
-(server half of Alg. 1) of every converted output.  Q K^T (row a7) is not yet
-part of the step; the JSON says so in config.layer_ops.
+rotations, MAC, giant-step key switches and rescale, the ct-ct MatMul Q_h K_h^T
+for all heads (row a7: MHP + BSGS, relinearisation), then the CKKS->MPC masks
+(server half of Alg. 1) of every converted output.  Softmax x V (row f1) is not
+yet part of the step; the JSON says so in config.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -139,16 +140,22 @@ def oracle_sample_ms(dims, reps: int = 1) -> dict:
              mm.plan_diagonal(W, dims["H"], dims["L"], n, 16),
              mm.plan_spatial(np.ones((dims["d"], dims["ffn"])), dims["L"], n, 32),
              mm.plan_spatial(np.ones((dims["ffn"], dims["d"])), dims["L"], n, 8)]
-    n_rot = sum(p.n_rotations for p in plans)
-    n_pt = sum(p.n_plaintexts for p in plans)
-    n_out = sum(p.n_out for p in plans)
-    n_mask = n_out - 2 * (len(cm) // (n // dims["L"]))
+    import oracle.matmul_cc as cc
+    qk = cc.plan_qk(dims["L"], dims["H"], dims["d"] // dims["H"], n)
+    qc = qk.counts()
+    qk_masks = qk.J * qk.B * (2 * qk.g - 1) + 2 * qk.J * (qk.G - 1) + sum(
+        1 for (u, w, f) in qk.accumulators() for i in range(qk.B) if qk.mask3(u, i, w, f).any())
+    n_rot = sum(p.n_rotations for p in plans) + qc["rotations"] + qc["relin"]   # relinearisation ~ one key switch
+    n_pt = sum(p.n_plaintexts for p in plans) + qk_masks + 3 * qc["cmult"]       # tensor ~ 3 ct-pt products
+    n_out = sum(p.n_out for p in plans) + qk.J * (qk.B + qk.G) + qk.G * qk.B + len(qk.accumulators())
+    n_mask = sum(p.n_out for p in plans) - 2 * qk.J + qk.n_out
     ms = 1e3 * (n_rot * t["rot"] + n_pt * t["prod"] + n_out * t["resc"] + n_mask * t["mask"])
     return {"ms_per_layer": ms, "per_op_s": t, "counts": {"rotations": n_rot, "plaintexts": n_pt,
                                                           "rescales": n_out, "masks": n_mask},
             "sample": "oracle at N=2^16, level 4 (k=5): 1 hoisted rotation + %d ct-pt products + 1 rescale + 1 mask "
-                      "per rep, x%d reps; extrapolated by the layer's operation counts (%d rotations, %d plaintexts, "
-                      "%d rescales, %d masks)" % (n_prod, reps, n_rot, n_pt, n_out, n_mask)}
+                      "per rep, x%d reps; extrapolated by the layer's operation counts (%d key switches, %d ct-pt "
+                      "product equivalents, %d rescales, %d masks; all at k=5, an upper bound for the lower-level "
+                      "Q.K^T stages)" % (n_prod, reps, n_rot, n_pt, n_out, n_mask)}
 
 
 def omp_threads() -> int:
@@ -175,13 +182,13 @@ def run_reference(args, dims):
 
 
 def config_dict(dims, world):
-    return {"workload": "BERT-base layer fused-linear CKKS (config 2 QKV + config 3 out-proj/FFN1/FFN2 + CKKS->MPC "
-                        "masks), N=2^16, Q={60,40x4}, P={60}, dnum=5",
+    return {"workload": "BERT-base layer fused-linear CKKS (config 2 QKV + Q.K^T + config 3 out-proj/FFN1/FFN2 + "
+                        "CKKS->MPC masks), N=2^16, Q={60,40x4}, P={60}, dnum=5",
             "L": dims["L"], "d": dims["d"], "heads": dims["H"], "ffn": dims["ffn"], "log_n": 16, "limbs": 5,
             "bsgs": {"qkv": 32, "oproj": 16, "ffn1": 32, "ffn2": 8},
-            "layer_ops": ["qkv_ct_pt(MHP)", "mask(V)", "oproj_diag_ct_pt", "mask", "ffn1_ct_pt", "mask",
-                          "ffn2_ct_pt", "mask"],
-            "not_included": "Q.K^T ct-ct MatMul (row a7) and Softmax x V (row f1)",
+            "layer_ops": ["qkv_ct_pt(MHP)", "qk_ct_ct(MHP+BSGS)", "mask(QK^T)", "mask(V)", "oproj_diag_ct_pt",
+                          "mask", "ffn1_ct_pt", "mask", "ffn2_ct_pt", "mask"],
+            "not_included": "Softmax x V ct-ct MatMul (row f1)",
             "l2": "inputs larger than L2 (~76 GB of plaintexts streamed per step)",
             "parallelism": "dp%d (output-ciphertext sharding, NCCL all-gather of masked outputs)" % world}
 

@@ -3,7 +3,8 @@
 
 Blocks (fig:fusion_pattern P:699-704, Table 6):
   * attention: QKV projection (C11, MHP reorder of the Q / K columns, P:466,
-    P:511) -> [Q K^T, row a7: not yet built] -> CKKS->MPC mask of V (P:513);
+    P:511) -> Q K^T for all heads (row a7, reading C13) -> CKKS->MPC masks of
+    the Q K^T diagonals and of V (P:511, P:513);
   * out-projection: diagonal-input ct-pt MatMul (C12, App. C.2) -> mask;
   * FFN1 (d -> 4d) -> mask; FFN2 (4d -> d) -> mask.
 Each MatMul starts from a fresh ciphertext at the top level (SURVEY 8(d)
@@ -33,8 +34,8 @@ class Dims:
 
 BERT_BASE = Dims()
 BERT_LARGE = Dims(128, 1024, 16, 4096)
-BSGS = {"qkv": 32, "oproj": 16, "ffn1": 32, "ffn2": 8}
-PLAN_ID = {"qkv": 0, "oproj": 1, "ffn1": 2, "ffn2": 3}
+BSGS = {"qkv": 32, "oproj": 16, "ffn1": 32, "ffn2": 8, "qk": 0}
+PLAN_ID = {"qkv": 0, "oproj": 1, "ffn1": 2, "ffn2": 3, "qk": 4}
 
 
 def shard(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -62,11 +63,16 @@ class FusedLinearLayer:
             "ffn2": blb.MatmulPlan(params, L, ffn, d, bsgs_B=b["ffn2"], level=self.level),
         }
         self.slices = {k: shard(pl.n_out, rank, world) for k, pl in self.plans.items()}
+        # Q K^T consumes the 2 J MHP outputs of QKV at level-1 (row a7); with more than one
+        # rank the Q / K ciphertexts are all-gathered first and Q K^T is replicated (its
+        # outputs are masked by their owner only) -- see DESIGN.md section 8.
+        self.qk = blb.QKPlan(params, L, H, d // H, bsgs_B=b["qk"], level=self.level - 1)
+        self.slices["qk"] = shard(self.qk.n_out, rank, world)
         self.pts, self.ws, self.outs = {}, None, {}
 
     # ---- setup (row a0) ----
     def rotation_steps(self) -> list[int]:
-        s = set()
+        s = set(self.qk.rotation_steps())
         for pl in self.plans.values():
             s.update(pl.rotation_steps())
         return sorted(s)
@@ -76,13 +82,17 @@ class FusedLinearLayer:
         for name, W in (("qkv", Wqkv), ("oproj", WO), ("ffn1", W1), ("ffn2", W2)):
             first, count = self.slices[name]
             self.pts[name] = self.plans[name].encode_weights(W, first, count)
-        nbytes = max(pl.workspace_bytes(self.slices[k][1]) for k, pl in self.plans.items())
+        self.qk_masks = self.qk.encode_masks()
+        nbytes = max([pl.workspace_bytes(self.slices[k][1]) for k, pl in self.plans.items()] +
+                     [self.qk.workspace_bytes()])
         self.ws = torch.empty(nbytes // 8 + 1, dtype=torch.int64, device="cuda")
         for k, pl in self.plans.items():
             self.outs[k] = [blb.Ciphertext.empty(self.p, self.level - 1) for _ in range(self.slices[k][1])]
+        self.qkv_full = [blb.Ciphertext.empty(self.p, self.level - 1) for _ in range(2 * self.n_mhp)]
+        self.outs["qk"] = [blb.Ciphertext.empty(self.p, self.level - 4) for _ in range(self.qk.n_out)]
 
     def plaintext_bytes(self) -> int:
-        return sum(int(t.numel()) * 8 for t in self.pts.values())
+        return sum(int(t.numel()) * 8 for t in self.pts.values()) + int(self.qk_masks.numel()) * 8
 
     def n_plaintexts(self) -> int:
         return sum(self.plans[k].pt_count(*self.slices[k]) for k in self.plans)
@@ -90,21 +100,55 @@ class FusedLinearLayer:
     def mask_ids(self, name: str) -> list[int]:
         """Global ciphertext ids of the masked outputs of this rank (PRNG key, C4)."""
         first, count = self.slices[name]
+        if name == "qk":
+            return [PLAN_ID[name] * 1024 + o for o in range(first, first + count)]
         outs = range(first, first + count)
         if name == "qkv":   # only V is converted here; Q, K feed Q K^T (row a7)
             outs = [o for o in outs if o >= 2 * self.n_mhp]
         return [PLAN_ID[name] * 1024 + o for o in outs]
 
     # ---- the hot path ----
+    def gather_qk_operands(self, outs: list):
+        """Q and K ciphertexts (QKV outputs 0 .. 2J-1) on every rank."""
+        first, count = self.slices["qkv"]
+        if self.world == 1:
+            return outs[:2 * self.n_mhp]
+        import torch.distributed as dist
+        N = self.p.N
+        k = self.level
+        per = 2 * k * N
+        counts = [shard(self.plans["qkv"].n_out, r, self.world)[1] for r in range(self.world)]
+        mx = max(counts)
+        buf = torch.zeros(mx * per, dtype=torch.int64, device="cuda")
+        for t, o in enumerate(outs):
+            buf[t * per:(t + 1) * per] = o.data.reshape(-1)
+        allb = torch.empty(self.world * mx * per, dtype=torch.int64, device="cuda")
+        dist.all_gather_into_tensor(allb, buf)
+        for g in range(2 * self.n_mhp):
+            r = next(r for r in range(self.world) if shard(self.plans["qkv"].n_out, r, self.world)[0] <= g <
+                     sum(shard(self.plans["qkv"].n_out, r, self.world)))
+            f = shard(self.plans["qkv"].n_out, r, self.world)[0]
+            self.qkv_full[g].data.copy_(allb[(r * mx + g - f) * per:(r * mx + g - f + 1) * per].view(2, k, N))
+            self.qkv_full[g].scale = outs[0].scale if outs else 2.0 ** 40
+        return self.qkv_full
+
     def step(self, keys: blb.Keys, inputs: dict, mask_key: bytes) -> list:
         """inputs: {'qkv': [ct]*3, 'oproj': [...], 'ffn1': [...], 'ffn2': [...]} -> [(masked, share)] per block."""
         res = []
         for name in ("qkv", "oproj", "ffn1", "ffn2"):
             first, count = self.slices[name]
-            if count == 0:
+            if count == 0 and not (name == "qkv" and self.world > 1):
                 continue
             outs = self.plans[name](keys, inputs[name], self.pts[name], first, count, ws=self.ws,
-                                    outs=self.outs[name])
+                                    outs=self.outs[name]) if count else []
+            if name == "qkv":
+                qk_in = self.gather_qk_operands(outs)
+                J = self.n_mhp
+                qk_out = self.qk(keys, qk_in[:J], qk_in[J:2 * J], self.qk_masks, ws=self.ws, outs=self.outs["qk"])
+                qf, qc = self.slices["qk"]
+                if qc:
+                    ids = self.mask_ids("qk")
+                    res.append(("qk", ids[0], blb.ckks_to_mpc(self.p, qk_out[qf:qf + qc], mask_key, ids[0])))
             ids = self.mask_ids(name)
             if not ids:
                 continue
