@@ -229,7 +229,7 @@ def main():
     layer = FusedLinearLayer(params, Dims(**dims), rank, world)
     A = bi.bert_attention_inputs(dims["L"], dims["d"])
     F = bi.bert_ffn_inputs(dims["L"], dims["d"], dims["H"], dims["ffn"])
-    keys, sk = blb.keygen(params, A["keys_key"], layer.rotation_steps())
+    keys, sk = blb.keygen(params, A["keys_key"], layer.rotation_steps(), relin=True)
     torch.cuda.synchronize()
     t_keys = time.perf_counter() - t_setup0
     t0 = time.perf_counter()
@@ -292,8 +292,10 @@ def main():
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
+    torch.cuda.nvtx.range_push("timed_steps")
     for _ in range(args.steps):
         step()
+    torch.cuda.nvtx.range_pop()
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()

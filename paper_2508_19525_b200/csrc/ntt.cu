@@ -102,6 +102,130 @@ __global__ void __launch_bounds__(kThreads) ntt_pass(RowBatch rb, const u64 *__r
     }
 }
 
+// ---------------------------------------------------------------------------
+// N = 2^16 fast path: each pass is a 256-point sub-transform of 16 columns per
+// CTA, but instead of one shared-memory round trip per stage every thread keeps
+// 16 residues in registers and runs 4 radix-2 stages in registers ("round A":
+// the 16 residues mid = tc + 16 m of its column, pairs 16*dist apart; "round B":
+// mid = 16 tc + m, pairs dist apart), with two swizzled shared-memory exchanges
+// per pass (A -> B, B -> A) so that global loads and stores both use the
+// coalesced A mapping.  Twiddle index of stage s = s0 + r (generic formula):
+// (1 << s) + (h << r) + mid / (2 t_l).
+__device__ __forceinline__ int swz(int col, int mid) { return (col << 8) | (mid & 0xF0) | ((mid ^ (mid >> 4) ^ col) & 15); }
+
+template <bool INV>
+__device__ __forceinline__ void bfly(u64 &X, u64 &Y, u64 w, u64 wsh, u64 q, u64 q2) {
+    if (!INV) {
+        if (X >= q2) X -= q2;
+        const u64 t = shoup_lazy(Y, w, wsh, q);
+        Y = X - t + q2;
+        X = X + t;
+    } else {
+        u64 s = X + Y;
+        if (s >= q2) s -= q2;
+        const u64 d = X - Y + q2;
+        X = s;
+        Y = shoup_lazy(d, w, wsh, q);
+    }
+}
+
+template <bool INV, bool STRIDED>
+__global__ void __launch_bounds__(256) ntt16_pass(RowBatch rb, const u64 *__restrict__ tw_all, Primes pr, int s0,
+                                                  int last) {
+    __shared__ u64 sm[16 * 256];
+    constexpr int logN = 16, N = 1 << logN;
+    const int row = blockIdx.y;
+    const int p = row / rb.limbs, l = row - p * rb.limbs;
+    if (rb.skip_alpha) {
+        const int dig = p % rb.skip_beta;
+        if (l < rb.skip_kmax && l >= dig * rb.skip_alpha && l < (dig + 1) * rb.skip_alpha) return;
+    }
+    u64 *a = rb.base + (long long)p * rb.poly_stride + (long long)(rb.limb0 + l) * N;
+    const int pi = rb.prime[l];
+    const u64 q = pr.m[pi].q, q2 = 2 * q;
+    const u64 *tw = tw_all + (size_t)pi * 4 * N + (INV ? 2 * N : 0);
+    const u64 *twsh = tw + N;
+    const int t = threadIdx.x;
+    const int c0 = blockIdx.x * 16;  // first column of the tile (lo0 for STRIDED, h0 otherwise)
+    // A mapping (coalesced global access)
+    const int colA = STRIDED ? (t & 15) : (t >> 4);
+    const int tcA = STRIDED ? (t >> 4) : (t & 15);
+    // B mapping
+    const int colB = t >> 4, tcB = t & 15;
+    const int hA = STRIDED ? 0 : (c0 + colA);
+    const int hB = STRIDED ? 0 : (c0 + colB);
+    u64 v[16];
+#pragma unroll
+    for (int m = 0; m < 16; m++) {
+        const int mid = tcA + 16 * m;
+        const size_t addr = STRIDED ? (((size_t)mid << 8) + c0 + colA) : (((size_t)(c0 + colA) << 8) + mid);
+        v[m] = a[addr];
+    }
+    auto roundA = [&](int r) {
+        const int dist = 8 >> r;
+        const int s = s0 + r;
+#pragma unroll
+        for (int m = 0; m < 16; m++) {
+            if (m & dist) continue;
+            const int widx = (1 << s) + (hA << r) + (m >> (4 - r));
+            bfly<INV>(v[m], v[m + dist], tw[widx], twsh[widx], q, q2);
+        }
+    };
+    auto roundB = [&](int r) {
+        const int dist = 8 >> (r - 4);
+        const int s = s0 + r;
+#pragma unroll
+        for (int m = 0; m < 16; m++) {
+            if (m & dist) continue;
+            const int widx = (1 << s) + (hB << r) + ((16 * tcB + m) >> (8 - r));
+            bfly<INV>(v[m], v[m + dist], tw[widx], twsh[widx], q, q2);
+        }
+    };
+    if (!INV) {
+#pragma unroll
+        for (int r = 0; r < 4; r++) roundA(r);
+    }
+#pragma unroll
+    for (int m = 0; m < 16; m++) sm[swz(colA, tcA + 16 * m)] = v[m];
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 16; m++) v[m] = sm[swz(colB, 16 * tcB + m)];
+    if (!INV) {
+#pragma unroll
+        for (int r = 4; r < 8; r++) roundB(r);
+    } else {
+#pragma unroll
+        for (int r = 7; r >= 4; r--) roundB(r);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 16; m++) sm[swz(colB, 16 * tcB + m)] = v[m];
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 16; m++) v[m] = sm[swz(colA, tcA + 16 * m)];
+    if (INV) {
+#pragma unroll
+        for (int r = 3; r >= 0; r--) roundA(r);
+    }
+    const ModConst &mc = pr.m[pi];
+#pragma unroll
+    for (int m = 0; m < 16; m++) {
+        u64 x = v[m];
+        if (last) {
+            if (!INV) {
+                if (x >= q2) x -= q2;
+                if (x >= q) x -= q;
+            } else {
+                x = shoup_lazy(x, mc.ninv, mc.ninv_sh, q);
+                if (x >= q) x -= q;
+            }
+        }
+        const int mid = tcA + 16 * m;
+        const size_t addr = STRIDED ? (((size_t)mid << 8) + c0 + colA) : (((size_t)(c0 + colA) << 8) + mid);
+        a[addr] = x;
+    }
+}
+
 }  // namespace
 
 blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cudaStream_t st) {
@@ -128,6 +252,20 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
         if (!inverse) ntt_pass<false><<<grid, kThreads, smem, st>>>(rb, P->d_tw, P->pr, logN, 0, logN, 0, 0, 1);
         else ntt_pass<true><<<grid, kThreads, smem, st>>>(rb, P->d_tw, P->pr, logN, 0, logN, 0, 0, 1);
         BLB_COUNT_LAUNCH(1);
+        blb_timing_end(1, t0, st, alg);
+        BLB_CHECK_LAUNCH();
+        return BLB_OK;
+    }
+    if (logN == 16) {
+        dim3 g(16, rows);
+        if (!inverse) {
+            ntt16_pass<false, true><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 0, 0);
+            ntt16_pass<false, false><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 8, 1);
+        } else {
+            ntt16_pass<true, false><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 8, 0);
+            ntt16_pass<true, true><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 0, 1);
+        }
+        BLB_COUNT_LAUNCH(2);
         blb_timing_end(1, t0, st, alg);
         BLB_CHECK_LAUNCH();
         return BLB_OK;
