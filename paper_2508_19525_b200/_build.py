@@ -29,10 +29,12 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """defines: extra -D flags (kernel tuning variants, e.g. BLB_NTT_MINB=3); out: alternative .so path."""
+    so = out or SO
+    if not force and not defines and out is None and not needs_build():
         return SO
-    bdir = os.path.join(HERE, "build")
+    bdir = os.path.join(HERE, "build" if not defines else "build_" + "_".join(d.replace("=", "") for d in defines))
     os.makedirs(bdir, exist_ok=True)
     objs = []
     for f in CPP:
@@ -42,13 +44,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for f in CU:
         o = os.path.join(bdir, f + ".o")
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
-               "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, f), "-o", o]
+               *["-D" + d for d in defines], "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, f), "-o", o]
         subprocess.check_call(cmd)
         objs.append(o)
-    tmp = SO + ".tmp%d" % os.getpid()
+    tmp = so + ".tmp%d" % os.getpid()
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lquadmath", "-lcudart"])
-    os.replace(tmp, SO)
-    return SO
+    os.replace(tmp, so)
+    return so
 
 
 if __name__ == "__main__":

@@ -182,6 +182,10 @@ __global__ void k_bconv_modup(PtrList c1_ntt, const u64 *coef, u64 *ext, const u
     }
     const int pm = m < k ? m : K + (m - k);
     const ModConst &mc = pr.m[pm];
+    if (nd == 1) {  // alpha = 1: dhat = 1, dhat^{-1} = 1 -> FastBConv(x) = x mod m
+        *o = mod64(coef[((long long)t * k + lo) * N + x], mc);
+        return;
+    }
     const u64 *tb = tab + tab_off.o[j];
     Acc128 acc;
     acc.zero();
@@ -228,6 +232,10 @@ __global__ void k_bconv_moddown(const u64 *u, u64 *conv, const u64 *tb, Primes p
     const int i = blockIdx.y, tb2 = blockIdx.z;  // tb2 = t*2 + b
     if (x >= N) return;
     const int E = k + np;
+    if (np == 1) {  // single special prime: FastBConv_{P -> q_i}(y) = y mod q_i
+        conv[((long long)tb2 * k + i) * N + x] = mod64(u[((long long)tb2 * E + k) * N + x], pr.m[i]);
+        return;
+    }
     Acc128 acc;
     acc.zero();
     for (int d = 0; d < np; d++) {

@@ -129,8 +129,11 @@ __device__ __forceinline__ void bfly(u64 &X, u64 &Y, u64 w, u64 wsh, u64 q, u64 
     }
 }
 
+#ifndef BLB_NTT_MINB
+#define BLB_NTT_MINB 2
+#endif
 template <bool INV, bool STRIDED>
-__global__ void __launch_bounds__(256) ntt16_pass(RowBatch rb, const u64 *__restrict__ tw_all, Primes pr, int s0,
+__global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, const u64 *__restrict__ tw_all, Primes pr, int s0,
                                                   int last) {
     __shared__ u64 sm[16 * 256];
     constexpr int logN = 16, N = 1 << logN;
