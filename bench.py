@@ -254,21 +254,18 @@ def main():
 
     stream = torch.cuda.current_stream()
 
+    from paper_2508_19525_b200.layer import allgather_ragged
+
     def gather(res):
+        """End-of-layer exchange: every rank receives all masked outputs + server shares."""
         if world == 1:
             return res
         out = []
         for name, id0, (m, s) in res:
-            buf = torch.cat([m.reshape(-1), s.reshape(-1)])
-            n = torch.tensor([buf.numel()], device="cuda")
-            sizes = [torch.zeros_like(n) for _ in range(world)]
-            dist.all_gather(sizes, n)
-            mx = int(max(x.item() for x in sizes))
-            pad = torch.zeros(mx, dtype=buf.dtype, device="cuda")
-            pad[:buf.numel()] = buf
-            allb = torch.empty(world * mx, dtype=buf.dtype, device="cuda")
-            dist.all_gather_into_tensor(allb, pad)
-            out.append((name, id0, allb))
+            items = [torch.cat([m[t].reshape(-1), s[t].reshape(-1)]) for t in range(m.shape[0])]
+            out.append((name, id0, allgather_ragged(items, layer.mask_counts(name),
+                                                    like=torch.empty(3 * params.N, dtype=torch.int64,
+                                                                     device="cuda"))))
         return out
 
     def step():
@@ -332,7 +329,7 @@ def main():
             res = step()
             outs_host = []
             for r in res:
-                for t in (r[2] if isinstance(r[2], tuple) else (r[2],)):
+                for t in (r[2] if isinstance(r[2], (tuple, list)) else (r[2],)):
                     outs_host.append(t.to("cpu"))
             d2h = sum(t.numel() * 8 for t in outs_host)
         e1.record(stream)

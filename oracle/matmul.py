@@ -229,10 +229,13 @@ def matmul_cp(ctx: Ctx, keys: Keys, cts: list[Ct], plan: Plan, out_ids=None) -> 
         Y = None
         for g in range(plan.G):
             lst = plan.entries.get((bp, g), [])
+            # encodes are independent: run them on a thread pool (the C encoder releases the GIL)
+            from concurrent.futures import ThreadPoolExecutor
+            with ThreadPoolExecutor() as ex:
+                pts = list(ex.map(lambda bi: encode(ctx, plan.pt_vector(bp, g, bi[0], bi[1]), pt_scale, level), lst))
             acc = None
-            for b, i in lst:
-                P = plan.pt_vector(bp, g, b, i)
-                term = mul_pt(ctx, R[(b, i)], encode(ctx, P, pt_scale, level), pt_scale)
+            for (b, i), pt in zip(lst, pts):
+                term = mul_pt(ctx, R[(b, i)], pt, pt_scale)
                 acc = term if acc is None else add(ctx, acc, term)
             if acc is None:
                 continue

@@ -24,6 +24,10 @@ import torch
 import paper_2508_19525_b200 as blb
 
 
+def bi_log_delta() -> int:
+    return 40
+
+
 @dataclass
 class Dims:
     L: int = 128
@@ -43,6 +47,31 @@ def shard(n: int, rank: int, world: int) -> tuple[int, int]:
     base, rem = divmod(n, world)
     first = rank * base + min(rank, rem)
     return first, base + (1 if rank < rem else 0)
+
+
+def allgather_ragged(local: list, counts: list, like=None) -> list:
+    """All-gather a rank-ordered ragged list (rank r holds counts[r] items, every item a
+    tensor of one common shape) into the full list, ordered by rank, on every rank.
+    One padded all_gather_into_tensor (NCCL over NVLink on GPUs, gloo on CPU)."""
+    import torch
+    import torch.distributed as dist
+    world = len(counts)
+    if world == 1:
+        return list(local)
+    ref = local[0] if local else like
+    shape, dtype, device = ref.shape, ref.dtype, ref.device
+    per = ref.numel()
+    mx = max(counts)
+    buf = torch.zeros(mx * per, dtype=dtype, device=device)
+    for t, x in enumerate(local):
+        buf[t * per:(t + 1) * per] = x.reshape(-1)
+    allb = torch.empty(world * mx * per, dtype=dtype, device=device)
+    dist.all_gather_into_tensor(allb, buf)
+    out = []
+    for r in range(world):
+        for t in range(counts[r]):
+            out.append(allb[(r * mx + t) * per:(r * mx + t + 1) * per].view(shape))
+    return out
 
 
 class FusedLinearLayer:
@@ -97,6 +126,16 @@ class FusedLinearLayer:
     def n_plaintexts(self) -> int:
         return sum(self.plans[k].pt_count(*self.slices[k]) for k in self.plans)
 
+    def mask_counts(self, name: str) -> list[int]:
+        """Number of masked outputs of a block on every rank (for the end-of-layer all-gather)."""
+        out = []
+        for r in range(self.world):
+            n = self.qk.n_out if name == "qk" else self.plans[name].n_out
+            f, c = shard(n, r, self.world)
+            lo = 2 * self.n_mhp if name == "qkv" else 0
+            out.append(len([o for o in range(f, f + c) if o >= lo]))
+        return out
+
     def mask_ids(self, name: str) -> list[int]:
         """Global ciphertext ids of the masked outputs of this rank (PRNG key, C4)."""
         first, count = self.slices[name]
@@ -110,26 +149,14 @@ class FusedLinearLayer:
     # ---- the hot path ----
     def gather_qk_operands(self, outs: list):
         """Q and K ciphertexts (QKV outputs 0 .. 2J-1) on every rank."""
-        first, count = self.slices["qkv"]
         if self.world == 1:
             return outs[:2 * self.n_mhp]
-        import torch.distributed as dist
-        N = self.p.N
-        k = self.level
-        per = 2 * k * N
         counts = [shard(self.plans["qkv"].n_out, r, self.world)[1] for r in range(self.world)]
-        mx = max(counts)
-        buf = torch.zeros(mx * per, dtype=torch.int64, device="cuda")
-        for t, o in enumerate(outs):
-            buf[t * per:(t + 1) * per] = o.data.reshape(-1)
-        allb = torch.empty(self.world * mx * per, dtype=torch.int64, device="cuda")
-        dist.all_gather_into_tensor(allb, buf)
+        full = allgather_ragged([o.data for o in outs], counts, like=self.qkv_full[0].data)
+        scale = outs[0].scale if outs else 2.0 ** bi_log_delta()
         for g in range(2 * self.n_mhp):
-            r = next(r for r in range(self.world) if shard(self.plans["qkv"].n_out, r, self.world)[0] <= g <
-                     sum(shard(self.plans["qkv"].n_out, r, self.world)))
-            f = shard(self.plans["qkv"].n_out, r, self.world)[0]
-            self.qkv_full[g].data.copy_(allb[(r * mx + g - f) * per:(r * mx + g - f + 1) * per].view(2, k, N))
-            self.qkv_full[g].scale = outs[0].scale if outs else 2.0 ** 40
+            self.qkv_full[g].data.copy_(full[g])
+            self.qkv_full[g].scale = scale
         return self.qkv_full
 
     def step(self, keys: blb.Keys, inputs: dict, mask_key: bytes) -> list:
