@@ -36,9 +36,6 @@ struct blb_matmul_plan {
     int *d_ent = nullptr;                               // device: (b * B + i) per entry
     int *d_ent_start = nullptr;                         // device copy of ent_start
     int32_t *d_col_map = nullptr;
-    // MAC output groups: up to 4 consecutive (b', g) of one b' with identical (b, i) entry lists
-    std::vector<int> grp_o, grp_n, grp_first;           // group start output, size; first group of each b'
-    int *d_grp = nullptr;                               // device: [n_grp][2] = (start o, count)
 };
 
 namespace {
@@ -115,58 +112,6 @@ __global__ void __launch_bounds__(kTB) k_mac(const u64 *__restrict__ pt, const u
     u64 *out = acc + (long long)o * 2 * kN + lx;
     *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00.reduce(mc), a01.reduce(mc));
     *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(mc), a11.reduce(mc));
-}
-
-// Grouped MAC: a CTA computes up to 4 outputs (b', g) whose entry lists are identical,
-// so every R tile is loaded once per group and re-used from registers:
-// acc[o][p][l][x] = sum_e pt[pb_o + e][l][x] * R[ent_r[e]][p][l][x].
-__global__ void __launch_bounds__(kTB) k_mac_grp(const u64 *__restrict__ pt, const u64 *__restrict__ R,
-                                                 u64 *__restrict__ acc, const int *__restrict__ ent_r,
-                                                 const int *__restrict__ ent_start, const int *__restrict__ grp,
-                                                 int g0, int o0, int e_base, int n_grp, int k, int logN, Primes pr) {
-    const int N = 1 << logN;
-    const int n_tiles = N / (2 * kTB);
-    int bid = blockIdx.x;
-    const int gi = bid % n_grp;
-    bid /= n_grp;
-    const int tile = bid % n_tiles;
-    const int l = bid / n_tiles;
-    const int x = tile * 2 * kTB + 2 * threadIdx.x;
-    const long long kN = (long long)k * N;
-    const int of = grp[2 * (g0 + gi)], cnt = grp[2 * (g0 + gi) + 1];
-    const int e_lo = ent_start[of], n_e = ent_start[of + 1] - e_lo;
-    long long pb[4];
-#pragma unroll
-    for (int q = 0; q < 4; q++) pb[q] = (long long)(q < cnt ? ent_start[of + q] - e_base : 0) * kN;
-    Acc128 a[4][4];
-#pragma unroll
-    for (int q = 0; q < 4; q++)
-#pragma unroll
-        for (int c = 0; c < 4; c++) a[q][c].zero();
-    const long long lx = (long long)l * N + x;
-#pragma unroll 2
-    for (int e = 0; e < n_e; e++) {
-        const int bi = ent_r[e_lo + e];
-        const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(R + (long long)bi * 2 * kN + lx);
-        const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(R + ((long long)bi * 2 + 1) * kN + lx);
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-            if (q < cnt) {
-                const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(pt + pb[q] + (long long)e * kN + lx);
-                a[q][0].mac(pv.x, r0.x); a[q][1].mac(pv.y, r0.y);
-                a[q][2].mac(pv.x, r1.x); a[q][3].mac(pv.y, r1.y);
-            }
-        }
-    }
-    const ModConst &mc = pr.m[l];
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-        if (q < cnt) {
-            u64 *out = acc + (long long)(of + q - o0) * 2 * kN + lx;
-            *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a[q][0].reduce(mc), a[q][1].reduce(mc));
-            *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a[q][2].reduce(mc), a[q][3].reduce(mc));
-        }
-    }
 }
 
 // dst[o] += src[j] for the jobs of one giant batch (sequential per thread: no races)
@@ -322,29 +267,6 @@ extern "C" blb_status blb_matmul_plan_create(const blb_params *P, int L, int w_r
     for (int bp = 0; bp < pl->n_out; bp++)
         for (int g : pl->giant[bp]) steps[g * pl->B * L] = 1;
     for (auto &kv : steps) pl->rot_steps.push_back(kv.first);
-    // MAC groups
-    for (int bp = 0; bp < pl->n_out; bp++) {
-        pl->grp_first.push_back((int)pl->grp_o.size());
-        int g = 0;
-        while (g < pl->G) {
-            const int o = bp * pl->G + g;
-            int cnt = 1;
-            while (cnt < 4 && g + cnt < pl->G) {
-                const int o2 = o + cnt;
-                const int n1 = pl->ent_start[o + 1] - pl->ent_start[o], n2 = pl->ent_start[o2 + 1] - pl->ent_start[o2];
-                bool same = n1 == n2;
-                for (int e = 0; same && e < n1; e++)
-                    same = pl->ent_b[pl->ent_start[o] + e] == pl->ent_b[pl->ent_start[o2] + e] &&
-                           pl->ent_i[pl->ent_start[o] + e] == pl->ent_i[pl->ent_start[o2] + e];
-                if (!same) break;
-                cnt++;
-            }
-            pl->grp_o.push_back(o);
-            pl->grp_n.push_back(cnt);
-            g += cnt;
-        }
-    }
-    pl->grp_first.push_back((int)pl->grp_o.size());
     // device copies
     const size_t ne = pl->ent_b.size();
     std::vector<int> bi(ne);
@@ -362,11 +284,6 @@ extern "C" blb_status blb_matmul_plan_create(const blb_params *P, int L, int w_r
     if (err == cudaSuccess)
         err = cudaMemcpy(pl->d_col_map, pl->col_map.data(), sizeof(int32_t) * pl->col_map.size(),
                          cudaMemcpyHostToDevice);
-    std::vector<int> grp;
-    for (size_t gi = 0; gi < pl->grp_o.size(); gi++) { grp.push_back(pl->grp_o[gi]); grp.push_back(pl->grp_n[gi]); }
-    if (err == cudaSuccess) err = cudaMalloc(&pl->d_grp, sizeof(int) * std::max<size_t>(grp.size(), 1));
-    if (err == cudaSuccess && !grp.empty())
-        err = cudaMemcpy(pl->d_grp, grp.data(), sizeof(int) * grp.size(), cudaMemcpyHostToDevice);
     if (err != cudaSuccess) {
         blb_set_error("plan upload: %s", cudaGetErrorString(err));
         blb_matmul_plan_destroy(pl);
@@ -381,7 +298,6 @@ extern "C" void blb_matmul_plan_destroy(blb_matmul_plan *pl) {
     cudaFree(pl->d_ent);
     cudaFree(pl->d_ent_start);
     cudaFree(pl->d_col_map);
-    cudaFree(pl->d_grp);
     delete pl;
 }
 
@@ -583,18 +499,8 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
     {
         const int o0 = out_first * pl->G, n_o = out_count * pl->G;
         const int e_base = pl->ent_start[o0];
-        const int g0 = pl->grp_first[out_first], n_grp = pl->grp_first[out_first + out_count] - g0;
-        const int n_entries = pl->ent_start[o0 + n_o] - e_base;
-        if (n_grp > 0) {
-            const int n_tiles = N / (2 * kTB);
-            cudaEvent_t t0 = blb_timing_begin(st);
-            k_mac_grp<<<(unsigned)((size_t)n_grp * n_tiles * k), kTB, 0, st>>>(
-                pt_dev, R, acc, pl->d_ent, pl->d_ent_start, pl->d_grp, g0, o0, e_base, n_grp, k, P->logN, P->pr);
-            BLB_COUNT_LAUNCH(1);
-            BLB_COUNT(3, n_entries);
-            blb_timing_end(0, t0, st, (double)n_entries * k * N * 8.0);
-            BLB_CHECK_LAUNCH();
-        }
+        BLB_TRY(launch_mac(P, pt_dev, R, acc, pl->d_ent, nullptr, pl->d_ent_start, o0, e_base, n_o,
+                           pl->ent_start[o0 + n_o] - e_base, k, st));
     }
     // 4. giant steps: acc[b'][0] += Rot_{gBL}(acc[b'][g])
     {
