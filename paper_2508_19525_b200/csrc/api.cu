@@ -233,7 +233,7 @@ extern "C" blb_status blb_params_create(blb_params **out, int log_n, const uint6
     BLB_CUDA_TRY(cudaSetDevice(cuda_device));
     auto *P = new blb_params();
     cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
-    if (const char *v = getenv("BLB_NTT_VARIANT")) P->ntt_variant = atoi(v);
+    if (const char *v = getenv("BLB_MAC_VARIANT")) P->mac_variant = atoi(v);
     P->logN = log_n; P->N = (int)N; P->K = nq; P->np = np; P->dnum = dnum; P->device = cuda_device;
     P->alpha = (nq + dnum - 1) / dnum;
     const int Lk = nq + np;

@@ -104,7 +104,7 @@ struct BconvTable;  // fwd
 struct blb_params {
     int logN, N, K, np, dnum, alpha, device;
     int num_sms = 148;
-    int ntt_variant = 0;          // 0: pipelined bulk-copy NTT (N = 2^16), 1: non-pipelined (tuning; env BLB_NTT_VARIANT)
+    int mac_variant = 0;          // MAC kernel variant (tuning only; env BLB_MAC_VARIANT)
     u64 mod[BLB_MAXP];
     u64 psi[BLB_MAXP];
     Primes pr;                    // by-value copy for kernel args

@@ -204,26 +204,48 @@ struct KsJobs {
 };
 
 // u[t][b][m][x] = sum_j sigma_g(ext_j)[m][x] * key_j[b][pm][x]
-__global__ void k_ks_inner(KsJobs jobs, u64 *u, Primes pr, int k, int np, int K, int beta, int logN) {
+// Jobs sharing one switching key (same Galois element) form a group of <= 4:
+// every key word is loaded once per group and re-used from registers (the key
+// stream is the dominant HBM traffic of a key switch).
+constexpr int kKsGroup = 4;
+struct KsGroups {
+    int n;
+    int start[kMaxJobs + 1];
+};
+__global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, int np, int K, int beta, int logN) {
     const int N = 1 << logN;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int m = blockIdx.y, t = blockIdx.z;
+    const int m = blockIdx.y, gi = blockIdx.z;
     if (x >= N) return;
-    const KsJob &J = jobs.j[t];
+    const int t0 = grp.start[gi], cnt = grp.start[gi + 1] - t0;
     const int E = k + np, Lk = K + np;
     const int pm = m < k ? m : K + (m - k);
-    const uint32_t src = J.galois == 1 ? (uint32_t)x : galois_perm(x, J.galois, logN);
-    Acc128 a0, a1;
-    a0.zero();
-    a1.zero();
+    const KsJob &J0 = jobs.j[t0];
+    const uint32_t src = J0.galois == 1 ? (uint32_t)x : galois_perm(x, J0.galois, logN);
+    Acc128 a0[kKsGroup], a1[kKsGroup];
+#pragma unroll
+    for (int q = 0; q < kKsGroup; q++) { a0[q].zero(); a1[q].zero(); }
     for (int j = 0; j < beta; j++) {
-        const u64 e = J.ext[((long long)j * E + m) * N + src];
-        a0.mac(e, J.key[(((long long)j * 2 + 0) * Lk + pm) * N + x]);
-        a1.mac(e, J.key[(((long long)j * 2 + 1) * Lk + pm) * N + x]);
+        const u64 kb = J0.key[(((long long)j * 2 + 0) * Lk + pm) * N + x];
+        const u64 ka = J0.key[(((long long)j * 2 + 1) * Lk + pm) * N + x];
+#pragma unroll
+        for (int q = 0; q < kKsGroup; q++) {
+            if (q < cnt) {
+                const u64 e = jobs.j[t0 + q].ext[((long long)j * E + m) * N + src];
+                a0[q].mac(e, kb);
+                a1[q].mac(e, ka);
+            }
+        }
     }
     const ModConst &mc = pr.m[pm];
-    u[(((long long)t * 2 + 0) * E + m) * N + x] = a0.reduce(mc);
-    u[(((long long)t * 2 + 1) * E + m) * N + x] = a1.reduce(mc);
+#pragma unroll
+    for (int q = 0; q < kKsGroup; q++) {
+        if (q < cnt) {
+            const int t = t0 + q;
+            u[(((long long)t * 2 + 0) * E + m) * N + x] = a0[q].reduce(mc);
+            u[(((long long)t * 2 + 1) * E + m) * N + x] = a1[q].reduce(mc);
+        }
+    }
 }
 
 // conv[t][b][i][x] = FastBConv_{P -> q_i}(INTT(u_P))   (u P-rows already INTT'd)
@@ -391,12 +413,29 @@ blb_status launch_keyswitch(const blb_params *P, int level, const KsJob *jobs, i
         return BLB_E_INVALID_ARG;
     }
     const int N = P->N, k = level + 1, np = P->np, E = k + np, beta = blb_beta(P, level);
+    // group jobs that share a key (stable order by key), <= kKsGroup per group
     KsJobs J{};
-    for (int t = 0; t < n; t++) J.j[t] = jobs[t];
+    KsGroups G{};
+    {
+        bool used[kMaxJobs] = {false};
+        int t = 0;
+        for (int a = 0; a < n; a++) {
+            if (used[a]) continue;
+            G.start[G.n++] = t;
+            int cnt = 0;
+            for (int b = a; b < n && cnt < kKsGroup; b++)
+                if (!used[b] && jobs[b].key == jobs[a].key && jobs[b].galois == jobs[a].galois) {
+                    used[b] = true;
+                    J.j[t++] = jobs[b];
+                    cnt++;
+                }
+        }
+        G.start[G.n] = t;
+    }
     cudaEvent_t t0 = blb_timing_begin(st);
-    k_ks_inner<<<grid_x(N, E, n), kTB, 0, st>>>(J, u, P->pr, k, np, P->K, beta, P->logN);
+    k_ks_inner<<<grid_x(N, E, G.n), kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN);
     BLB_COUNT_LAUNCH(1);
-    blb_timing_end(2, t0, st, (double)n * 2.0 * beta * E * N * 8.0);
+    blb_timing_end(2, t0, st, (double)G.n * 2.0 * beta * E * N * 8.0);
     BLB_CHECK_LAUNCH();
     RowBatch rb{};
     rb.base = u; rb.poly_stride = (long long)E * N; rb.n_polys = 2 * n; rb.limbs = np; rb.limb0 = k;

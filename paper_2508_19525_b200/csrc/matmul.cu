@@ -36,6 +36,9 @@ struct blb_matmul_plan {
     int *d_ent = nullptr;                               // device: (b * B + i) per entry
     int *d_ent_start = nullptr;                         // device copy of ent_start
     int32_t *d_col_map = nullptr;
+    // MAC output groups (variant 1/2): consecutive (b', g) of one b' with identical entry lists
+    std::vector<int> grp_first;                         // first group of each b' (n_out + 1)
+    int *d_grp = nullptr;                               // device [n_grp][2] = (start output, count)
 };
 
 namespace {
@@ -112,6 +115,56 @@ __global__ void __launch_bounds__(kTB) k_mac(const u64 *__restrict__ pt, const u
     u64 *out = acc + (long long)o * 2 * kN + lx;
     *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00.reduce(mc), a01.reduce(mc));
     *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(mc), a11.reduce(mc));
+}
+
+// Grouped MAC (tuning variants 1 / 2): one thread = one coefficient of one limb for a
+// group of up to O outputs with identical (b, i) entry lists, so each R word is
+// read once per group (R is re-read from L2 once per output by k_mac).
+template <int O>
+__global__ void __launch_bounds__(kTB) k_mac_g(const u64 *__restrict__ pt, const u64 *__restrict__ R,
+                                               u64 *__restrict__ acc, const int *__restrict__ ent_r,
+                                               const int *__restrict__ ent_start, const int *__restrict__ grp,
+                                               int g0, int o0, int e_base, int n_grp, int k, int logN, Primes pr) {
+    const int N = 1 << logN;
+    const int n_tiles = N / kTB;
+    int bid = blockIdx.x;
+    const int gi = bid % n_grp;
+    bid /= n_grp;
+    const int tile = bid % n_tiles;
+    const int l = bid / n_tiles;
+    const int x = tile * kTB + threadIdx.x;
+    const long long kN = (long long)k * N;
+    const int of = grp[2 * (g0 + gi)], cnt = grp[2 * (g0 + gi) + 1];
+    const int e_lo = ent_start[of], n_e = ent_start[of + 1] - e_lo;
+    const long long lx = (long long)l * N + x;
+    const u64 *pp[O];
+#pragma unroll
+    for (int q = 0; q < O; q++) pp[q] = pt + (long long)(q < cnt ? ent_start[of + q] - e_base : 0) * kN + lx;
+    Acc128 a[O][2];
+#pragma unroll
+    for (int q = 0; q < O; q++) { a[q][0].zero(); a[q][1].zero(); }
+    for (int e = 0; e < n_e; e++) {
+        const int bi = ent_r[e_lo + e];
+        const u64 r0 = R[(long long)bi * 2 * kN + lx];
+        const u64 r1 = R[((long long)bi * 2 + 1) * kN + lx];
+#pragma unroll
+        for (int q = 0; q < O; q++) {
+            if (q < cnt) {
+                const u64 p = pp[q][(long long)e * kN];
+                a[q][0].mac(p, r0);
+                a[q][1].mac(p, r1);
+            }
+        }
+    }
+    const ModConst &mc = pr.m[l];
+#pragma unroll
+    for (int q = 0; q < O; q++) {
+        if (q < cnt) {
+            u64 *out = acc + (long long)(of + q - o0) * 2 * kN + lx;
+            out[0] = a[q][0].reduce(mc);
+            out[kN] = a[q][1].reduce(mc);
+        }
+    }
 }
 
 // dst[o] += src[j] for the jobs of one giant batch (sequential per thread: no races)
@@ -267,6 +320,30 @@ extern "C" blb_status blb_matmul_plan_create(const blb_params *P, int L, int w_r
     for (int bp = 0; bp < pl->n_out; bp++)
         for (int g : pl->giant[bp]) steps[g * pl->B * L] = 1;
     for (auto &kv : steps) pl->rot_steps.push_back(kv.first);
+    // MAC output groups (<= 8 (variant 2) or 4 consecutive g of one b' with identical (b, i) lists)
+    const int gcap = P->mac_variant == 2 ? 8 : 4;
+    std::vector<int> grp;
+    for (int bp = 0; bp < pl->n_out; bp++) {
+        pl->grp_first.push_back((int)grp.size() / 2);
+        for (int g = 0; g < pl->G;) {
+            const int o = bp * pl->G + g;
+            int cnt = 1;
+            while (cnt < gcap && g + cnt < pl->G) {
+                const int o2 = o + cnt;
+                const int n1 = pl->ent_start[o + 1] - pl->ent_start[o], n2 = pl->ent_start[o2 + 1] - pl->ent_start[o2];
+                bool same = n1 == n2;
+                for (int e = 0; same && e < n1; e++)
+                    same = pl->ent_b[pl->ent_start[o] + e] == pl->ent_b[pl->ent_start[o2] + e] &&
+                           pl->ent_i[pl->ent_start[o] + e] == pl->ent_i[pl->ent_start[o2] + e];
+                if (!same) break;
+                cnt++;
+            }
+            grp.push_back(o);
+            grp.push_back(cnt);
+            g += cnt;
+        }
+    }
+    pl->grp_first.push_back((int)grp.size() / 2);
     // device copies
     const size_t ne = pl->ent_b.size();
     std::vector<int> bi(ne);
@@ -284,6 +361,9 @@ extern "C" blb_status blb_matmul_plan_create(const blb_params *P, int L, int w_r
     if (err == cudaSuccess)
         err = cudaMemcpy(pl->d_col_map, pl->col_map.data(), sizeof(int32_t) * pl->col_map.size(),
                          cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMalloc(&pl->d_grp, sizeof(int) * std::max<size_t>(grp.size(), 2));
+    if (err == cudaSuccess && !grp.empty())
+        err = cudaMemcpy(pl->d_grp, grp.data(), sizeof(int) * grp.size(), cudaMemcpyHostToDevice);
     if (err != cudaSuccess) {
         blb_set_error("plan upload: %s", cudaGetErrorString(err));
         blb_matmul_plan_destroy(pl);
@@ -298,6 +378,7 @@ extern "C" void blb_matmul_plan_destroy(blb_matmul_plan *pl) {
     cudaFree(pl->d_ent);
     cudaFree(pl->d_ent_start);
     cudaFree(pl->d_col_map);
+    cudaFree(pl->d_grp);
     delete pl;
 }
 
@@ -478,9 +559,12 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
     }
     // 2. baby steps: R[b][i] = Rot_{iL}(X_b), batched
     {
+        // i-major order: the inputs that use the same baby-step key are adjacent, so one
+        // launch group loads each key once for all of them (launch_keyswitch groups by key)
         std::vector<KsJob> jobs;
-        for (int b = 0; b < n_in; b++)
-            for (int i : pl->baby[b]) {
+        for (int i = 1; i < pl->B; i++)
+            for (int b = 0; b < n_in; b++) {
+                if (!std::binary_search(pl->baby[b].begin(), pl->baby[b].end(), i)) continue;
                 KsJob J{};
                 J.ext = ext_in + (size_t)b * beta * E * N;
                 J.key = find_key(i * pl->L);
@@ -499,8 +583,26 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
     {
         const int o0 = out_first * pl->G, n_o = out_count * pl->G;
         const int e_base = pl->ent_start[o0];
-        BLB_TRY(launch_mac(P, pt_dev, R, acc, pl->d_ent, nullptr, pl->d_ent_start, o0, e_base, n_o,
-                           pl->ent_start[o0 + n_o] - e_base, k, st));
+        const int n_entries = pl->ent_start[o0 + n_o] - e_base;
+        if (P->mac_variant == 0) {
+            BLB_TRY(launch_mac(P, pt_dev, R, acc, pl->d_ent, nullptr, pl->d_ent_start, o0, e_base, n_o, n_entries, k,
+                               st));
+        } else if (n_o > 0) {
+            // grouped variants: groups of <= 8 outputs; variant 1 splits them to <= 4 via O = 4 kernels
+            const int g0 = pl->grp_first[out_first], n_grp = pl->grp_first[out_first + out_count] - g0;
+            const int n_tiles = N / kTB;
+            cudaEvent_t t0 = blb_timing_begin(st);
+            if (P->mac_variant == 2)
+                k_mac_g<8><<<(unsigned)((size_t)n_grp * n_tiles * k), kTB, 0, st>>>(
+                    pt_dev, R, acc, pl->d_ent, pl->d_ent_start, pl->d_grp, g0, o0, e_base, n_grp, k, P->logN, P->pr);
+            else
+                k_mac_g<4><<<(unsigned)((size_t)n_grp * n_tiles * k), kTB, 0, st>>>(
+                    pt_dev, R, acc, pl->d_ent, pl->d_ent_start, pl->d_grp, g0, o0, e_base, n_grp, k, P->logN, P->pr);
+            BLB_COUNT_LAUNCH(1);
+            BLB_COUNT(3, n_entries);
+            blb_timing_end(0, t0, st, (double)n_entries * k * N * 8.0);
+            BLB_CHECK_LAUNCH();
+        }
     }
     // 4. giant steps: acc[b'][0] += Rot_{gBL}(acc[b'][g])
     {
@@ -508,8 +610,10 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
             int t, g;
         };
         std::vector<GJob> gj;
-        for (int t = 0; t < out_count; t++)
-            for (int g : pl->giant[out_first + t]) gj.push_back({t, g});
+        for (int g = 1; g < pl->G; g++)   // g-major: outputs sharing a giant-step key are adjacent
+            for (int t = 0; t < out_count; t++)
+                if (std::binary_search(pl->giant[out_first + t].begin(), pl->giant[out_first + t].end(), g))
+                    gj.push_back({t, g});
         for (size_t j0 = 0; j0 < gj.size(); j0 += kMaxJobs) {
             const int cnt = (int)std::min<size_t>(kMaxJobs, gj.size() - j0);
             std::vector<const u64 *> c1(cnt);

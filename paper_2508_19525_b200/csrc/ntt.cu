@@ -229,178 +229,6 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, con
     }
 }
 
-// ---------------------------------------------------------------------------
-// N = 2^16 pipelined variant (default): a persistent CTA per half-SM walks the
-// (row, 16-column block) tiles of a batch; the next tile is streamed into a
-// second shared-memory buffer with cp.async.bulk (the TMA bulk-copy engine,
-// completion tracked by an mbarrier) while the current tile is transformed,
-// so HBM traffic overlaps the integer-bound butterflies.  Compute per tile is
-// the register-blocked scheme of ntt16_pass above.
-__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-
-__device__ __forceinline__ bool row_skipped(const RowBatch &rb, int row) {
-    if (!rb.skip_alpha) return false;
-    const int p = row / rb.limbs, l = row - p * rb.limbs;
-    const int dig = p % rb.skip_beta;
-    return l < rb.skip_kmax && l >= dig * rb.skip_alpha && l < (dig + 1) * rb.skip_alpha;
-}
-
-template <bool INV, bool STRIDED>
-__global__ void __launch_bounds__(256, 2) ntt16_pipe(RowBatch rb, const u64 *__restrict__ tw_all, Primes pr, int s0,
-                                                    int last, int rows) {
-    extern __shared__ __align__(128) unsigned char smraw[];
-    u64 *buf = reinterpret_cast<u64 *>(smraw);          // [2][4096]
-    u64 *xs = buf + 2 * 4096;                            // [4096] exchange (swizzled)
-    uint64_t *bar = reinterpret_cast<uint64_t *>(xs + 4096);
-    constexpr int N = 1 << 16;
-    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-    const int total = rows * 16;
-    if (t == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    auto row_base = [&](int row) -> u64 * {
-        const int p = row / rb.limbs, l = row - p * rb.limbs;
-        return rb.base + (long long)p * rb.poly_stride + (long long)(rb.limb0 + l) * N;
-    };
-    auto next_active = [&](int tile) -> int {
-        while (tile < total && row_skipped(rb, tile >> 4)) tile += gridDim.x;
-        return tile;
-    };
-    auto issue = [&](int tile, int slot) {
-        if (warp != 0) return;
-        const u64 *src = row_base(tile >> 4);
-        const int cb = tile & 15;
-        u64 *dst = buf + slot * 4096;
-        if (lane == 0) mbar_expect_tx(&bar[slot], 32768);
-        __syncwarp();
-        if (STRIDED) {
-            for (int r = lane; r < 256; r += 32) bulk_g2s(dst + r * 16, src + ((size_t)r << 8) + cb * 16, 128, &bar[slot]);
-        } else if (lane < 8) {
-            bulk_g2s(dst + lane * 512, src + (size_t)cb * 4096 + lane * 512, 4096, &bar[slot]);
-        }
-    };
-    // A mapping (coalesced) and B mapping, see ntt16_pass
-    const int colA = STRIDED ? (t & 15) : (t >> 4);
-    const int tcA = STRIDED ? (t >> 4) : (t & 15);
-    const int colB = t >> 4, tcB = t & 15;
-    int cur = next_active(blockIdx.x);
-    if (cur < total) issue(cur, 0);
-    int it = 0;
-    while (cur < total) {
-        const int nxt = next_active(cur + gridDim.x);
-        if (nxt < total) issue(nxt, (it + 1) & 1);
-        const int row = cur >> 4, cb = cur & 15;
-        const int l = row % rb.limbs;
-        const int pi = rb.prime[l];
-        const u64 q = pr.m[pi].q, q2 = 2 * q;
-        const u64 *tw = tw_all + (size_t)pi * 4 * N + (INV ? 2 * N : 0);
-        const u64 *twsh = tw + N;
-        const int hA = STRIDED ? 0 : (cb * 16 + colA);
-        const int hB = STRIDED ? 0 : (cb * 16 + colB);
-        mbar_wait(&bar[it & 1], (it >> 1) & 1);
-        const u64 *b = buf + (it & 1) * 4096;
-        u64 v[16];
-#pragma unroll
-        for (int m = 0; m < 16; m++) {
-            const int mid = tcA + 16 * m;
-            v[m] = STRIDED ? b[mid * 16 + colA] : b[colA * 256 + mid];
-        }
-        auto roundA = [&](int r) {
-            const int dist = 8 >> r;
-            const int s = s0 + r;
-#pragma unroll
-            for (int m = 0; m < 16; m++) {
-                if (m & dist) continue;
-                const int widx = (1 << s) + (hA << r) + (m >> (4 - r));
-                bfly<INV>(v[m], v[m + dist], tw[widx], twsh[widx], q, q2);
-            }
-        };
-        auto roundB = [&](int r) {
-            const int dist = 8 >> (r - 4);
-            const int s = s0 + r;
-#pragma unroll
-            for (int m = 0; m < 16; m++) {
-                if (m & dist) continue;
-                const int widx = (1 << s) + (hB << r) + ((16 * tcB + m) >> (8 - r));
-                bfly<INV>(v[m], v[m + dist], tw[widx], twsh[widx], q, q2);
-            }
-        };
-        if (!INV) {
-#pragma unroll
-            for (int r = 0; r < 4; r++) roundA(r);
-        }
-        __syncthreads();  // previous tile's readers of xs are done
-#pragma unroll
-        for (int m = 0; m < 16; m++) xs[swz(colA, tcA + 16 * m)] = v[m];
-        __syncthreads();
-#pragma unroll
-        for (int m = 0; m < 16; m++) v[m] = xs[swz(colB, 16 * tcB + m)];
-        if (!INV) {
-#pragma unroll
-            for (int r = 4; r < 8; r++) roundB(r);
-        } else {
-#pragma unroll
-            for (int r = 7; r >= 4; r--) roundB(r);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int m = 0; m < 16; m++) xs[swz(colB, 16 * tcB + m)] = v[m];
-        __syncthreads();
-#pragma unroll
-        for (int m = 0; m < 16; m++) v[m] = xs[swz(colA, tcA + 16 * m)];
-        if (INV) {
-#pragma unroll
-            for (int r = 3; r >= 0; r--) roundA(r);
-        }
-        const ModConst &mc = pr.m[pi];
-        u64 *a = row_base(row);
-#pragma unroll
-        for (int m = 0; m < 16; m++) {
-            u64 x = v[m];
-            if (last) {
-                if (!INV) {
-                    if (x >= q2) x -= q2;
-                    if (x >= q) x -= q;
-                } else {
-                    x = shoup_lazy(x, mc.ninv, mc.ninv_sh, q);
-                    if (x >= q) x -= q;
-                }
-            }
-            const int mid = tcA + 16 * m;
-            const size_t addr = STRIDED ? (((size_t)mid << 8) + cb * 16 + colA) : (((size_t)(cb * 16 + colA) << 8) + mid);
-            a[addr] = x;
-        }
-        cur = nxt;
-        it++;
-    }
-}
-constexpr size_t kPipeSmem = 3 * 4096 * 8 + 16;
 
 }  // namespace
 
@@ -432,7 +260,7 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
         BLB_CHECK_LAUNCH();
         return BLB_OK;
     }
-    if (logN == 16 && P->ntt_variant == 1) {
+    if (logN == 16) {
         dim3 g(16, rows);
         if (!inverse) {
             ntt16_pass<false, true><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 0, 0);
@@ -440,29 +268,6 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
         } else {
             ntt16_pass<true, false><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 8, 0);
             ntt16_pass<true, true><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 0, 1);
-        }
-        BLB_COUNT_LAUNCH(2);
-        blb_timing_end(1, t0, st, alg);
-        BLB_CHECK_LAUNCH();
-        return BLB_OK;
-    }
-    if (logN == 16) {
-        static bool attr_done = false;
-        if (!attr_done) {
-            cudaFuncSetAttribute(ntt16_pipe<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem);
-            cudaFuncSetAttribute(ntt16_pipe<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem);
-            cudaFuncSetAttribute(ntt16_pipe<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem);
-            cudaFuncSetAttribute(ntt16_pipe<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem);
-            attr_done = true;
-        }
-        const int tiles = rows * 16;
-        const int grid = tiles < 2 * P->num_sms ? tiles : 2 * P->num_sms;
-        if (!inverse) {
-            ntt16_pipe<false, true><<<grid, 256, kPipeSmem, st>>>(rb, P->d_tw, P->pr, 0, 0, rows);
-            ntt16_pipe<false, false><<<grid, 256, kPipeSmem, st>>>(rb, P->d_tw, P->pr, 8, 1, rows);
-        } else {
-            ntt16_pipe<true, false><<<grid, 256, kPipeSmem, st>>>(rb, P->d_tw, P->pr, 8, 0, rows);
-            ntt16_pipe<true, true><<<grid, 256, kPipeSmem, st>>>(rb, P->d_tw, P->pr, 0, 1, rows);
         }
         BLB_COUNT_LAUNCH(2);
         blb_timing_end(1, t0, st, alg);

@@ -538,8 +538,8 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
         std::vector<const u64 *> in;
         std::vector<int32_t> steps;
         std::vector<u64 *> outp;
-        for (int u = 0; u < G; u++)
-            for (int i = 0; i < B; i++) {
+        for (int i = 0; i < B; i++)          // i-major: the G rotations by the same step share a key
+            for (int u = 0; u < G; u++) {
                 const size_t o = (size_t)(u * B + i);
                 if (i == 0) {
                     cudaMemcpyAsync(W + w.t + o * ct_k2, W + w.sr + o * ct_k2, ct_k2 * sizeof(u64),
