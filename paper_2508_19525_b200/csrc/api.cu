@@ -198,6 +198,9 @@ static blb_status build_bconv(blb_params *P) {
 
 extern "C" void blb_params_destroy(blb_params *P) {
     if (!P) return;
+    if (P->aux) cudaStreamDestroy(P->aux);
+    for (auto &e : P->ev)
+        if (e) cudaEventDestroy(e);
     cudaFree(P->d_tw);
     cudaFree(P->d_zeta);
     cudaFree(P->d_slot_pos);
@@ -233,7 +236,9 @@ extern "C" blb_status blb_params_create(blb_params **out, int log_n, const uint6
     BLB_CUDA_TRY(cudaSetDevice(cuda_device));
     auto *P = new blb_params();
     cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
-    if (const char *v = getenv("BLB_MAC_VARIANT")) P->mac_variant = atoi(v);
+    if (const char *v = getenv("BLB_OVERLAP")) P->overlap = atoi(v);
+    if (cudaStreamCreateWithFlags(&P->aux, cudaStreamNonBlocking) != cudaSuccess) P->aux = nullptr;
+    for (auto &e : P->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     P->logN = log_n; P->N = (int)N; P->K = nq; P->np = np; P->dnum = dnum; P->device = cuda_device;
     P->alpha = (nq + dnum - 1) / dnum;
     const int Lk = nq + np;

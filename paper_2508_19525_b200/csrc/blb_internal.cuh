@@ -88,6 +88,35 @@ struct Acc128 {
     __device__ __forceinline__ u64 reduce(const ModConst &c) const { return reduce128(hi, lo, c); }
 };
 
+// Accumulator for products of residues < 2^41 (the 40-bit chain primes), with
+// 32-bit partial products: a = a1 2^32 + a0, a1 < 2^9.  lo (96 bits, 3 words)
+// += a0 b0; mid (64 bits) += a1 b0 + a0 b1 (< 2^42 each); hi (32 bits) += a1 b1
+// (< 2^18 each): 6 IMAD-class instructions per product instead of the ~13 of
+// a 64x64->128 multiply + 128-bit add.  Valid for < 2^14 products.
+struct Acc41 {
+    uint32_t l0, l1, l2, hi;
+    u64 mid;
+    __device__ __forceinline__ void zero() { l0 = l1 = l2 = hi = 0; mid = 0; }
+    __device__ __forceinline__ void mac(u64 a, u64 b) {
+        const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32), b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
+        asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
+            "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+            "addc.u32 %2, %2, 0;"
+            : "+r"(l0), "+r"(l1), "+r"(l2)
+            : "r"(a0), "r"(b0));
+        mid += (u64)a1 * b0 + (u64)a0 * b1;
+        hi += a1 * b1;
+    }
+    __device__ __forceinline__ u64 reduce(const ModConst &c) const {
+        // total = (l2:l1:l0) + mid * 2^32 + hi * 2^64
+        const u64 lo = ((u64)l1 << 32) | l0;
+        const u64 m_lo = mid << 32, m_hi = mid >> 32;
+        const u64 s = lo + m_lo;
+        const u64 H = (u64)l2 + hi + m_hi + (s < lo ? 1 : 0);
+        return reduce128(H, s, c);
+    }
+};
+
 // NTT-domain automorphism index: out[k] = in[perm(k)],
 // perm(k) = brv(((g * (2 brv(k) + 1)) mod 2N - 1) / 2)
 __device__ __forceinline__ uint32_t galois_perm(uint32_t k, uint32_t g, int logN) {
@@ -104,7 +133,11 @@ struct BconvTable;  // fwd
 struct blb_params {
     int logN, N, K, np, dnum, alpha, device;
     int num_sms = 148;
-    int mac_variant = 0;          // MAC kernel variant (tuning only; env BLB_MAC_VARIANT)
+    // auxiliary stream: integer-bound key switches overlap the HBM-bound MAC (matmul.cu)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev[64] = {};
+    mutable int ev_next = 0;
+    int overlap = 1;              // env BLB_OVERLAP=0 disables the two-stream schedule
     u64 mod[BLB_MAXP];
     u64 psi[BLB_MAXP];
     Primes pr;                    // by-value copy for kernel args

@@ -36,9 +36,6 @@ struct blb_matmul_plan {
     int *d_ent = nullptr;                               // device: (b * B + i) per entry
     int *d_ent_start = nullptr;                         // device copy of ent_start
     int32_t *d_col_map = nullptr;
-    // MAC output groups (variant 1/2): consecutive (b', g) of one b' with identical entry lists
-    std::vector<int> grp_first;                         // first group of each b' (n_out + 1)
-    int *d_grp = nullptr;                               // device [n_grp][2] = (start output, count)
 };
 
 namespace {
@@ -98,9 +95,29 @@ __global__ void __launch_bounds__(kTB) k_mac(const u64 *__restrict__ pt, const u
     const int x = tile * 2 * kTB + 2 * threadIdx.x;
     const long long kN = (long long)k * N;
     const int e_lo = ent_start[o0 + o], e_hi = ent_start[o0 + o + 1];
+    const long long lx = (long long)l * N + x;
+    const ModConst &mc = pr.m[l];
+    u64 *out = acc + (long long)o * 2 * kN + lx;
+    if (mc.q < (1ull << 41)) {
+        // 40-bit limb: split 32-bit partial products (Acc41)
+        Acc41 a00, a01, a10, a11;
+        a00.zero(); a01.zero(); a10.zero(); a11.zero();
+#pragma unroll 4
+        for (int e = e_lo; e < e_hi; e++) {
+            const int bi = ent_r[e];
+            const int pe = ent_pt ? ent_pt[e] : e - e_base;
+            const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(pt + (long long)pe * kN + lx);
+            const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(R + (long long)bi * 2 * kN + lx);
+            const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(R + ((long long)bi * 2 + 1) * kN + lx);
+            a00.mac(pv.x, r0.x); a01.mac(pv.y, r0.y);
+            a10.mac(pv.x, r1.x); a11.mac(pv.y, r1.y);
+        }
+        *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00.reduce(mc), a01.reduce(mc));
+        *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(mc), a11.reduce(mc));
+        return;
+    }
     Acc128 a00, a01, a10, a11;  // [poly][coefficient]
     a00.zero(); a01.zero(); a10.zero(); a11.zero();
-    const long long lx = (long long)l * N + x;
 #pragma unroll 4
     for (int e = e_lo; e < e_hi; e++) {
         const int bi = ent_r[e];
@@ -111,60 +128,8 @@ __global__ void __launch_bounds__(kTB) k_mac(const u64 *__restrict__ pt, const u
         a00.mac(pv.x, r0.x); a01.mac(pv.y, r0.y);
         a10.mac(pv.x, r1.x); a11.mac(pv.y, r1.y);
     }
-    const ModConst &mc = pr.m[l];
-    u64 *out = acc + (long long)o * 2 * kN + lx;
     *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00.reduce(mc), a01.reduce(mc));
     *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(mc), a11.reduce(mc));
-}
-
-// Grouped MAC (tuning variants 1 / 2): one thread = one coefficient of one limb for a
-// group of up to O outputs with identical (b, i) entry lists, so each R word is
-// read once per group (R is re-read from L2 once per output by k_mac).
-template <int O>
-__global__ void __launch_bounds__(kTB) k_mac_g(const u64 *__restrict__ pt, const u64 *__restrict__ R,
-                                               u64 *__restrict__ acc, const int *__restrict__ ent_r,
-                                               const int *__restrict__ ent_start, const int *__restrict__ grp,
-                                               int g0, int o0, int e_base, int n_grp, int k, int logN, Primes pr) {
-    const int N = 1 << logN;
-    const int n_tiles = N / kTB;
-    int bid = blockIdx.x;
-    const int gi = bid % n_grp;
-    bid /= n_grp;
-    const int tile = bid % n_tiles;
-    const int l = bid / n_tiles;
-    const int x = tile * kTB + threadIdx.x;
-    const long long kN = (long long)k * N;
-    const int of = grp[2 * (g0 + gi)], cnt = grp[2 * (g0 + gi) + 1];
-    const int e_lo = ent_start[of], n_e = ent_start[of + 1] - e_lo;
-    const long long lx = (long long)l * N + x;
-    const u64 *pp[O];
-#pragma unroll
-    for (int q = 0; q < O; q++) pp[q] = pt + (long long)(q < cnt ? ent_start[of + q] - e_base : 0) * kN + lx;
-    Acc128 a[O][2];
-#pragma unroll
-    for (int q = 0; q < O; q++) { a[q][0].zero(); a[q][1].zero(); }
-    for (int e = 0; e < n_e; e++) {
-        const int bi = ent_r[e_lo + e];
-        const u64 r0 = R[(long long)bi * 2 * kN + lx];
-        const u64 r1 = R[((long long)bi * 2 + 1) * kN + lx];
-#pragma unroll
-        for (int q = 0; q < O; q++) {
-            if (q < cnt) {
-                const u64 p = pp[q][(long long)e * kN];
-                a[q][0].mac(p, r0);
-                a[q][1].mac(p, r1);
-            }
-        }
-    }
-    const ModConst &mc = pr.m[l];
-#pragma unroll
-    for (int q = 0; q < O; q++) {
-        if (q < cnt) {
-            u64 *out = acc + (long long)(of + q - o0) * 2 * kN + lx;
-            out[0] = a[q][0].reduce(mc);
-            out[kN] = a[q][1].reduce(mc);
-        }
-    }
 }
 
 // dst[o] += src[j] for the jobs of one giant batch (sequential per thread: no races)
@@ -320,30 +285,6 @@ extern "C" blb_status blb_matmul_plan_create(const blb_params *P, int L, int w_r
     for (int bp = 0; bp < pl->n_out; bp++)
         for (int g : pl->giant[bp]) steps[g * pl->B * L] = 1;
     for (auto &kv : steps) pl->rot_steps.push_back(kv.first);
-    // MAC output groups (<= 8 (variant 2) or 4 consecutive g of one b' with identical (b, i) lists)
-    const int gcap = P->mac_variant == 2 ? 8 : 4;
-    std::vector<int> grp;
-    for (int bp = 0; bp < pl->n_out; bp++) {
-        pl->grp_first.push_back((int)grp.size() / 2);
-        for (int g = 0; g < pl->G;) {
-            const int o = bp * pl->G + g;
-            int cnt = 1;
-            while (cnt < gcap && g + cnt < pl->G) {
-                const int o2 = o + cnt;
-                const int n1 = pl->ent_start[o + 1] - pl->ent_start[o], n2 = pl->ent_start[o2 + 1] - pl->ent_start[o2];
-                bool same = n1 == n2;
-                for (int e = 0; same && e < n1; e++)
-                    same = pl->ent_b[pl->ent_start[o] + e] == pl->ent_b[pl->ent_start[o2] + e] &&
-                           pl->ent_i[pl->ent_start[o] + e] == pl->ent_i[pl->ent_start[o2] + e];
-                if (!same) break;
-                cnt++;
-            }
-            grp.push_back(o);
-            grp.push_back(cnt);
-            g += cnt;
-        }
-    }
-    pl->grp_first.push_back((int)grp.size() / 2);
     // device copies
     const size_t ne = pl->ent_b.size();
     std::vector<int> bi(ne);
@@ -361,9 +302,6 @@ extern "C" blb_status blb_matmul_plan_create(const blb_params *P, int L, int w_r
     if (err == cudaSuccess)
         err = cudaMemcpy(pl->d_col_map, pl->col_map.data(), sizeof(int32_t) * pl->col_map.size(),
                          cudaMemcpyHostToDevice);
-    if (err == cudaSuccess) err = cudaMalloc(&pl->d_grp, sizeof(int) * std::max<size_t>(grp.size(), 2));
-    if (err == cudaSuccess && !grp.empty())
-        err = cudaMemcpy(pl->d_grp, grp.data(), sizeof(int) * grp.size(), cudaMemcpyHostToDevice);
     if (err != cudaSuccess) {
         blb_set_error("plan upload: %s", cudaGetErrorString(err));
         blb_matmul_plan_destroy(pl);
@@ -378,7 +316,6 @@ extern "C" void blb_matmul_plan_destroy(blb_matmul_plan *pl) {
     cudaFree(pl->d_ent);
     cudaFree(pl->d_ent_start);
     cudaFree(pl->d_col_map);
-    cudaFree(pl->d_grp);
     delete pl;
 }
 
@@ -474,7 +411,7 @@ extern "C" blb_status blb_matmul_encode_weights(const blb_matmul_plan *pl, const
 
 // workspace layout (u64 elements)
 struct MatmulWs {
-    size_t ext_in, coef, R, ks, acc, gext, rot, resc, total;
+    size_t ext_in, coef, R, ks, acc, gext, gcoef, gks, rot, resc, total;
 };
 static MatmulWs matmul_ws(const blb_matmul_plan *pl, int out_count) {
     const blb_params *P = pl->P;
@@ -487,6 +424,8 @@ static MatmulWs matmul_ws(const blb_matmul_plan *pl, int out_count) {
     w.ks = o; o += keyswitch_scratch_elems(P, pl->level, kMaxJobs);
     w.acc = o; o += (size_t)out_count * pl->G * 2 * k * N;
     w.gext = o; o += (size_t)kMaxJobs * beta * E * N;
+    w.gcoef = o; o += (size_t)kMaxJobs * k * N;
+    w.gks = o; o += keyswitch_scratch_elems(P, pl->level, kMaxJobs);
     w.rot = o; o += (size_t)kMaxJobs * 2 * k * N;
     w.resc = o; o += (2 + 2 * k) * N;
     w.total = o;
@@ -539,7 +478,8 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
     cudaStream_t st = (cudaStream_t)stream;
     u64 *W = (u64 *)ws;
     u64 *ext_in = W + w.ext_in, *coef = W + w.coef, *R = W + w.R, *ks = W + w.ks, *acc = W + w.acc;
-    u64 *gext = W + w.gext, *rot = W + w.rot, *resc = W + w.resc;
+    u64 *gext = W + w.gext, *rot = W + w.rot, *resc = W + w.resc, *gcoef = W + w.gcoef;
+    u64 *gks_u = W + w.gks, *gks_conv = W + w.gks + (size_t)kMaxJobs * 2 * E * N;
     const size_t ctN = (size_t)2 * k * N;
     u64 *ks_u = ks, *ks_conv = ks + (size_t)kMaxJobs * 2 * E * N;
 
@@ -579,39 +519,40 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
             BLB_TRY(launch_keyswitch(P, level, jobs.data() + j0, cnt, ks_u, ks_conv, st));
         }
     }
-    // 3. MAC
-    {
-        const int o0 = out_first * pl->G, n_o = out_count * pl->G;
-        const int e_base = pl->ent_start[o0];
-        const int n_entries = pl->ent_start[o0 + n_o] - e_base;
-        if (P->mac_variant == 0) {
-            BLB_TRY(launch_mac(P, pt_dev, R, acc, pl->d_ent, nullptr, pl->d_ent_start, o0, e_base, n_o, n_entries, k,
-                               st));
-        } else if (n_o > 0) {
-            // grouped variants: groups of <= 8 outputs; variant 1 splits them to <= 4 via O = 4 kernels
-            const int g0 = pl->grp_first[out_first], n_grp = pl->grp_first[out_first + out_count] - g0;
-            const int n_tiles = N / kTB;
-            cudaEvent_t t0 = blb_timing_begin(st);
-            if (P->mac_variant == 2)
-                k_mac_g<8><<<(unsigned)((size_t)n_grp * n_tiles * k), kTB, 0, st>>>(
-                    pt_dev, R, acc, pl->d_ent, pl->d_ent_start, pl->d_grp, g0, o0, e_base, n_grp, k, P->logN, P->pr);
-            else
-                k_mac_g<4><<<(unsigned)((size_t)n_grp * n_tiles * k), kTB, 0, st>>>(
-                    pt_dev, R, acc, pl->d_ent, pl->d_ent_start, pl->d_grp, g0, o0, e_base, n_grp, k, P->logN, P->pr);
-            BLB_COUNT_LAUNCH(1);
-            BLB_COUNT(3, n_entries);
-            blb_timing_end(0, t0, st, (double)n_entries * k * N * 8.0);
-            BLB_CHECK_LAUNCH();
+    // 3-5. MAC, giant steps and rescale, in output chunks: the MAC of chunk c+1 (HBM-bound,
+    // main stream) overlaps the giant-step key switches + rescale of chunk c (integer-bound,
+    // auxiliary stream); the caller's stream waits for the auxiliary stream at the end.
+    const bool ovl = P->overlap && P->aux && out_count > 1;
+    cudaStream_t sa = ovl ? P->aux : st;
+    const int chunk = ovl ? std::max(1, std::min(3, (out_count + 1) / 2)) : out_count;
+    auto next_event = [&]() {
+        cudaEvent_t e = P->ev[P->ev_next];
+        P->ev_next = (P->ev_next + 1) % 64;
+        return e;
+    };
+    for (int c0 = 0; c0 < out_count; c0 += chunk) {
+        const int cn = std::min(chunk, out_count - c0);
+        // MAC
+        {
+            const int o0 = (out_first + c0) * pl->G, n_o = cn * pl->G;
+            const int e_base = pl->ent_start[out_first * pl->G];
+            const int n_entries = pl->ent_start[o0 + n_o] - pl->ent_start[o0];
+            u64 *acc_c = acc + (size_t)c0 * pl->G * ctN;
+            BLB_TRY(launch_mac(P, pt_dev, R, acc_c, pl->d_ent, nullptr, pl->d_ent_start, o0, e_base, n_o, n_entries,
+                               k, st));
         }
-    }
-    // 4. giant steps: acc[b'][0] += Rot_{gBL}(acc[b'][g])
-    {
+        if (ovl) {
+            cudaEvent_t e = next_event();
+            BLB_CUDA_TRY(cudaEventRecord(e, st));
+            BLB_CUDA_TRY(cudaStreamWaitEvent(sa, e, 0));
+        }
+        // giant steps: acc[b'][0] += Rot_{gBL}(acc[b'][g]), g-major so outputs sharing a key are adjacent
         struct GJob {
             int t, g;
         };
         std::vector<GJob> gj;
-        for (int g = 1; g < pl->G; g++)   // g-major: outputs sharing a giant-step key are adjacent
-            for (int t = 0; t < out_count; t++)
+        for (int g = 1; g < pl->G; g++)
+            for (int t = c0; t < c0 + cn; t++)
                 if (std::binary_search(pl->giant[out_first + t].begin(), pl->giant[out_first + t].end(), g))
                     gj.push_back({t, g});
         for (size_t j0 = 0; j0 < gj.size(); j0 += kMaxJobs) {
@@ -635,18 +576,23 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
                 aj.dst[j] = acc + ((size_t)G.t * pl->G) * ctN;
                 aj.src[j] = J.out;
             }
-            BLB_TRY(launch_modup(P, level, c1.data(), cnt, gext, coef, st));
-            BLB_TRY(launch_keyswitch(P, level, jobs.data(), cnt, ks_u, ks_conv, st));
-            k_accumulate<<<dim3((N + kTB - 1) / kTB, k, 2), kTB, 0, st>>>(aj, P->pr, k, N);
+            BLB_TRY(launch_modup(P, level, c1.data(), cnt, gext, gcoef, sa));
+            BLB_TRY(launch_keyswitch(P, level, jobs.data(), cnt, gks_u, gks_conv, sa));
+            k_accumulate<<<dim3((N + kTB - 1) / kTB, k, 2), kTB, 0, sa>>>(aj, P->pr, k, N);
             BLB_COUNT_LAUNCH(1);
             BLB_CHECK_LAUNCH();
         }
+        // rescale the chunk's outputs
+        for (int t = c0; t < c0 + cn; t++) {
+            BLB_TRY(launch_rescale(P, acc + (size_t)t * pl->G * ctN, level, 2, out[t].data, resc, sa));
+            out[t].level = level - 1;
+            out[t].scale = in[0].scale;  // Delta * q_level / q_level, exact (reading S6)
+        }
     }
-    // 5. rescale each output
-    for (int t = 0; t < out_count; t++) {
-        BLB_TRY(launch_rescale(P, acc + (size_t)t * pl->G * ctN, level, 2, out[t].data, resc, st));
-        out[t].level = level - 1;
-        out[t].scale = in[0].scale;  // Delta * q_level / q_level, exact (reading S6)
+    if (ovl) {
+        cudaEvent_t e = next_event();
+        BLB_CUDA_TRY(cudaEventRecord(e, sa));
+        BLB_CUDA_TRY(cudaStreamWaitEvent(st, e, 0));
     }
     return BLB_OK;
 }

@@ -80,6 +80,25 @@ __global__ void k_tensor_sum(const u64 *Qp, const u64 *Kp, u64 *D, Primes pr, in
     if (x >= N) return;
     const int u = o / B, i = o - u * B;
     const long long kN = (long long)k * N, lx = (long long)l * N + x;
+    const ModConst &mc = pr.m[l];
+    u64 *out = D + (long long)o * 3 * kN + lx;
+    if (mc.q < (1ull << 41)) {
+        Acc41 d0, d1, d2;
+        d0.zero(); d1.zero(); d2.zero();
+        for (int j = 0; j < J; j++) {
+            const u64 *a = Qp + (long long)(u * J + j) * 2 * kN + lx;
+            const u64 *b = Kp + (long long)(i * J + j) * 2 * kN + lx;
+            const u64 a0 = a[0], a1 = a[kN], b0 = b[0], b1 = b[kN];
+            d0.mac(a0, b0);
+            d1.mac(a0, b1);
+            d1.mac(a1, b0);
+            d2.mac(a1, b1);
+        }
+        out[0] = d0.reduce(mc);
+        out[kN] = d1.reduce(mc);
+        out[2 * kN] = d2.reduce(mc);
+        return;
+    }
     Acc128 d0, d1, d2;
     d0.zero(); d1.zero(); d2.zero();
     for (int j = 0; j < J; j++) {
@@ -91,8 +110,6 @@ __global__ void k_tensor_sum(const u64 *Qp, const u64 *Kp, u64 *D, Primes pr, in
         d1.mac(a1, b0);
         d2.mac(a1, b1);
     }
-    const ModConst &mc = pr.m[l];
-    u64 *out = D + (long long)o * 3 * kN + lx;
     out[0] = d0.reduce(mc);
     out[kN] = d1.reduce(mc);
     out[2 * kN] = d2.reduce(mc);
