@@ -260,7 +260,10 @@ blb_status blb_matmul_pt_count(const blb_matmul_plan *plan, int out_first, int o
 
 /* Offline precompute (row a0): build and encode the plaintexts of outputs
  * [out_first, out_first+out_count) from W (host, row-major w_rows x w_cols,
- * float64) into pt_dev[n_pt][level+1][N] (device), plan order.  Synchronises. */
+ * float64) into pt_dev (device, n_pt * (level+1) * N words).  The buffer is
+ * opaque: it holds the NTT-form plaintexts in the library's blocked MAC layout
+ * (per output: [limb][512-coefficient tile][plaintext][512]) so that the MAC
+ * streams each output's weights contiguously.  Synchronises. */
 blb_status blb_matmul_encode_weights(const blb_matmul_plan *plan, const double *W, int out_first, int out_count,
                                      uint64_t *pt_dev, void *stream);
 

@@ -282,3 +282,40 @@ def qk_encrypted(ctx: Ctx, keys: Keys, Q: list[Ct], K: list[Ct], plan: QKPlan) -
         o = plan.out_index(u, w)
         outs[o] = A if outs[o] is None else add(ctx, outs[o], A)
     return outs
+
+
+# ---------------------------------------------------------------------------
+# f1: Softmax x V_h with zero padding d_h -> L, dense-diagonal collapse of
+# adjacent outputs (fig:diag (b)), feeding the diagonal ct-pt W_O (C12)
+# ---------------------------------------------------------------------------
+def plan_sv(L: int, H: int, n: int, B: int | None = None) -> QKPlan:
+    """C13 with inner dimension L: operands S_h (L x L) and Vpad_h^T (L x L)."""
+    return plan_qk(L, H, L, n, B)
+
+
+def sv_operands(S: np.ndarray, V: np.ndarray):
+    """S: (H, L, L) softmax rows; V: (H, L, d_h) -> (A, Kop) both (H, L, L): C13 computes
+    C[i, i+t] = sum_k A[i,k] Kop[i+t, k], so Kop = Vpad^T gives C = S Vpad."""
+    H, L, dh = V.shape
+    Vpad = np.zeros((H, L, L))
+    Vpad[:, :, :dh] = V
+    return S, np.transpose(Vpad, (0, 2, 1)).copy()
+
+
+def collapse_dense(outs: list, plan: QKPlan, dh: int, add_fn=None) -> list:
+    """Outputs o and o + n_out/2 hold diagonals d and d + d_h (d_h = L/2) with
+    complementary support: their sum is the dense diagonal d of the L x d_h result."""
+    assert 2 * dh == plan.L, "the collapse needs padding by exactly 2x (P:1213)"
+    half = plan.n_out // 2
+    add_fn = add_fn or (lambda a, b: a + b)
+    return [add_fn(outs[o], outs[o + half]) for o in range(half)]
+
+
+def pad_heads_rows(WO: np.ndarray, H: int, Hp: int) -> np.ndarray:
+    """W_O rows reordered for the MHP-padded diagonal input: head h < H keeps its
+    d_h rows, padded heads get zero rows."""
+    D, Dout = WO.shape
+    dh = D // H
+    out = np.zeros((Hp * dh, Dout))
+    out[:H * dh] = WO
+    return out

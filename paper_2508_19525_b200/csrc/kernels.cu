@@ -223,32 +223,6 @@ __global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, 
     const KsJob &J0 = jobs.j[t0];
     const uint32_t src = J0.galois == 1 ? (uint32_t)x : galois_perm(x, J0.galois, logN);
     const ModConst &mc = pr.m[pm];
-    if (mc.q < (1ull << 41)) {  // 40-bit limb: split partial products (Acc41)
-        Acc41 a0[kKsGroup], a1[kKsGroup];
-#pragma unroll
-        for (int q = 0; q < kKsGroup; q++) { a0[q].zero(); a1[q].zero(); }
-        for (int j = 0; j < beta; j++) {
-            const u64 kb = J0.key[(((long long)j * 2 + 0) * Lk + pm) * N + x];
-            const u64 ka = J0.key[(((long long)j * 2 + 1) * Lk + pm) * N + x];
-#pragma unroll
-            for (int q = 0; q < kKsGroup; q++) {
-                if (q < cnt) {
-                    const u64 e = jobs.j[t0 + q].ext[((long long)j * E + m) * N + src];
-                    a0[q].mac(e, kb);
-                    a1[q].mac(e, ka);
-                }
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < kKsGroup; q++) {
-            if (q < cnt) {
-                const int t = t0 + q;
-                u[(((long long)t * 2 + 0) * E + m) * N + x] = a0[q].reduce(mc);
-                u[(((long long)t * 2 + 1) * E + m) * N + x] = a1[q].reduce(mc);
-            }
-        }
-        return;
-    }
     Acc128 a0[kKsGroup], a1[kKsGroup];
 #pragma unroll
     for (int q = 0; q < kKsGroup; q++) { a0[q].zero(); a1[q].zero(); }

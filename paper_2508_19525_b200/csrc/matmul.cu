@@ -20,6 +20,7 @@
 //   5. one rescale per output.
 #include <algorithm>
 #include <map>
+#include <type_traits>
 #include "blb_internal.cuh"
 
 extern "C" u64 blbh_shoup(u64 w, u64 q);
@@ -130,6 +131,84 @@ __global__ void __launch_bounds__(kTB) k_mac(const u64 *__restrict__ pt, const u
     }
     *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00.reduce(mc), a01.reduce(mc));
     *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(mc), a11.reduce(mc));
+}
+
+// Weight MAC on the blocked plaintext layout written by blb_matmul_encode_weights:
+// output o's plaintexts are stored as [l][tile][e][512] (tile = 512 coefficients),
+// so a CTA (o, tile, l) streams one contiguous n_e * 4 KB run instead of n_e
+// 4 KB pieces 2.6 MB apart (DRAM row-buffer and TLB friendly).
+template <bool SPLIT41>
+__device__ __forceinline__ void mac_run(const u64 *__restrict__ pp, const u64 *__restrict__ R,
+                                        const int *__restrict__ ent_r, int e_lo, int n_e, long long kN,
+                                        long long lx, u64 *out, const ModConst &mc) {
+    using A = typename std::conditional<SPLIT41, Acc41, Acc128>::type;
+    A a00, a01, a10, a11;
+    a00.zero(); a01.zero(); a10.zero(); a11.zero();
+    int e = 0;
+    for (; e + 4 <= n_e; e += 4) {
+        int bi[4];
+        ulonglong2 pv[4], r0[4], r1[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) bi[u] = ent_r[e_lo + e + u];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            pv[u] = *reinterpret_cast<const ulonglong2 *>(pp + (long long)(e + u) * 512);
+            r0[u] = *reinterpret_cast<const ulonglong2 *>(R + (long long)bi[u] * 2 * kN + lx);
+            r1[u] = *reinterpret_cast<const ulonglong2 *>(R + ((long long)bi[u] * 2 + 1) * kN + lx);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            a00.mac(pv[u].x, r0[u].x); a01.mac(pv[u].y, r0[u].y);
+            a10.mac(pv[u].x, r1[u].x); a11.mac(pv[u].y, r1[u].y);
+        }
+    }
+    for (; e < n_e; e++) {
+        const int bi = ent_r[e_lo + e];
+        const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(pp + (long long)e * 512);
+        const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(R + (long long)bi * 2 * kN + lx);
+        const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(R + ((long long)bi * 2 + 1) * kN + lx);
+        a00.mac(pv.x, r0.x); a01.mac(pv.y, r0.y);
+        a10.mac(pv.x, r1.x); a11.mac(pv.y, r1.y);
+    }
+    *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00.reduce(mc), a01.reduce(mc));
+    *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(mc), a11.reduce(mc));
+}
+
+__global__ void __launch_bounds__(kTB) k_mac_w(const u64 *__restrict__ pt, const u64 *__restrict__ R,
+                                               u64 *__restrict__ acc, const int *__restrict__ ent_r,
+                                               const int *__restrict__ ent_start, int o0, int e_base, int n_o, int k,
+                                               int logN, Primes pr) {
+    const int N = 1 << logN;
+    const int n_tiles = N / (2 * kTB);
+    int bid = blockIdx.x;
+    const int o = bid % n_o;
+    bid /= n_o;
+    const int tile = bid % n_tiles;
+    const int l = bid / n_tiles;
+    const long long kN = (long long)k * N;
+    const int e_lo = ent_start[o0 + o], n_e = ent_start[o0 + o + 1] - e_lo;
+    const long long lx = (long long)l * N + tile * 2 * kTB + 2 * threadIdx.x;
+    const u64 *pp = pt + (long long)(e_lo - e_base) * kN + (long long)l * n_e * N + (long long)tile * n_e * 512 +
+                    2 * threadIdx.x;
+    u64 *out = acc + (long long)o * 2 * kN + lx;
+    const ModConst &mc = pr.m[l];
+    if (mc.q < (1ull << 41)) mac_run<true>(pp, R, ent_r, e_lo, n_e, kN, lx, out, mc);
+    else mac_run<false>(pp, R, ent_r, e_lo, n_e, kN, lx, out, mc);
+}
+
+// scatter standard [cnt][k][N] plaintexts (entries e0..e0+cnt of the plan) into the blocked layout
+__global__ void k_block_pts(const u64 *src, u64 *dst, const int *ent_start, const int *ent_o, int e0, int e_base,
+                            int k, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int l = blockIdx.y, t = blockIdx.z;
+    if (x >= N) return;
+    const int e = e0 + t;
+    const int o = ent_o[e];
+    const int e_lo = ent_start[o], n_e = ent_start[o + 1] - e_lo;
+    const long long kN = (long long)k * N;
+    const long long off = (long long)(e_lo - e_base) * kN + (long long)l * n_e * N + (long long)(x >> 9) * n_e * 512 +
+                          (long long)(e - e_lo) * 512 + (x & 511);
+    dst[off] = src[(long long)t * kN + (long long)l * N + x];
 }
 
 // dst[o] += src[j] for the jobs of one giant batch (sequential per thread: no races)
@@ -383,6 +462,8 @@ extern "C" blb_status blb_matmul_encode_weights(const blb_matmul_plan *pl, const
     BLB_CUDA_TRY(cudaMallocAsync(&buf, sizeof(double) * encode_scratch_doubles(P, chunk), st));
     BLB_CUDA_TRY(cudaMallocAsync(&flag, sizeof(int), st));
     BLB_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    u64 *tmp = nullptr;
+    BLB_CUDA_TRY(cudaMallocAsync(&tmp, sizeof(u64) * (size_t)chunk * k * P->N, st));
     PlanDev pd{pl->L, pl->n, pl->c, pl->B, pl->G, pl->w_rows, pl->w_cols, pl->nblk_in, pl->D_out, pl->packing,
                pl->heads, pl->dh};
     const double scale = (double)P->mod[pl->level];  // reading S6: plaintext scale = q_level
@@ -392,11 +473,17 @@ extern "C" blb_status blb_matmul_encode_weights(const blb_matmul_plan *pl, const
         k_build_slots<<<dim3((pl->n + kTB - 1) / kTB, cnt), kTB, 0, st>>>(pd, pl->d_ent, pl->d_ent + ne_total, e, dW,
                                                                          pl->d_col_map, slots);
         BLB_COUNT_LAUNCH(1);
-        s = launch_encode(P, slots, cnt, scale, pl->level, pt_dev + (size_t)(e - e0) * k * P->N, buf, flag, st);
+        s = launch_encode(P, slots, cnt, scale, pl->level, tmp, buf, flag, st);
+        if (s == BLB_OK) {
+            k_block_pts<<<dim3((P->N + kTB - 1) / kTB, k, cnt), kTB, 0, st>>>(tmp, pt_dev, pl->d_ent_start,
+                                                                             pl->d_ent + ne_total, e, e0, k, P->N);
+            BLB_COUNT_LAUNCH(1);
+        }
     }
     int h_flag = 0;
     cudaMemcpyAsync(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
     cudaFreeAsync(dW, st);
+    cudaFreeAsync(tmp, st);
     cudaFreeAsync(slots, st);
     cudaFreeAsync(buf, st);
     cudaFreeAsync(flag, st);
@@ -538,8 +625,17 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
             const int e_base = pl->ent_start[out_first * pl->G];
             const int n_entries = pl->ent_start[o0 + n_o] - pl->ent_start[o0];
             u64 *acc_c = acc + (size_t)c0 * pl->G * ctN;
-            BLB_TRY(launch_mac(P, pt_dev, R, acc_c, pl->d_ent, nullptr, pl->d_ent_start, o0, e_base, n_o, n_entries,
-                               k, st));
+            if (n_o > 0) {
+                const int n_tiles = N / (2 * kTB);
+                cudaEvent_t t0 = blb_timing_begin(st);
+                k_mac_w<<<(unsigned)((size_t)n_o * n_tiles * k), kTB, 0, st>>>(pt_dev, R, acc_c, pl->d_ent,
+                                                                              pl->d_ent_start, o0, e_base, n_o, k,
+                                                                              P->logN, P->pr);
+                BLB_COUNT_LAUNCH(1);
+                BLB_COUNT(3, n_entries);
+                blb_timing_end(0, t0, st, (double)n_entries * k * N * 8.0);
+                BLB_CHECK_LAUNCH();
+            }
         }
         if (ovl) {
             cudaEvent_t e = next_event();

@@ -364,3 +364,51 @@ def test_qk_ct_ct_bit_exact(qktoy, H, L, dh, B):
     C = cc.unpack_diag(dec, plan_o)
     ref = np.einsum("hik,hjk->hij", d["Q"], d["K"])
     assert float(((C - ref) ** 2).mean()) <= 1e-11
+
+
+def test_softmax_v_wo_chain_bit_exact(qktoy):
+    """Row f1: Softmax x V_h (C13 with d_h zero-padded to L) -> dense-diagonal collapse
+     -> diagonal ct-pt W_O with MHP-padded rows (C12) at level 1."""
+    import oracle.matmul_cc as cc
+    L, H, n = 32, 4, qktoy.n
+    dh = L // 2
+    rng = np.random.default_rng(7)
+    S = rng.uniform(0, 1.0 / L, size=(H, L, L))
+    V = rng.normal(0, 1, size=(H, L, dh))
+    WO = rng.normal(0, 0.1, size=(H * dh, 48))
+    p = cc.plan_sv(L, H, n)
+    A, Kop = cc.sv_operands(S, V)
+    key, ekey = bi.crypto_key(4, 77), bi.crypto_key(5, 77)
+    qk_g = blb.QKPlan(qktoy.g, L, H, L, level=4)
+    WOp = cc.pad_heads_rows(WO, H, p.Hp)
+    diag_g = blb.MatmulPlan(qktoy.g, L, p.Hp * dh, 48, packing=blb.PACK_DIAGONAL, heads=p.Hp, bsgs_B=16, level=1)
+    diag_o = mm.plan_diagonal(WOp, p.Hp, L, n, 16)
+    steps = sorted(set(qk_g.rotation_steps()) | set(diag_g.rotation_steps()))
+    okeys = O.keygen(qktoy.o, key, steps, relin=True)
+    gkeys, sk = blb.keygen(qktoy.g, key, steps, relin=True)
+    lvl, delta = 4, 2.0 ** 40
+    oa, ok, ga, gk = [], [], [], []
+    for j, (za, zk) in enumerate(zip(cc.pack_mhp(A, p), cc.pack_mhp(Kop, p))):
+        for z, cid, ol, gl in ((za, j, oa, ga), (zk, 50 + j, ok, gk)):
+            pt = O.encode(qktoy.o, z, delta, lvl)
+            ol.append(O.encrypt(qktoy.o, ekey, okeys.s_ntt, pt, lvl, cid, delta))
+            gl.append(blb.encrypt(qktoy.g, sk, dev(pt), lvl, ekey, cid, delta))
+    # oracle chain
+    oout = cc.qk_encrypted(qktoy.o, okeys, oa, ok, p)
+    odense = cc.collapse_dense(oout, p, dh, add_fn=lambda a, b: O.add(qktoy.o, a, b))
+    ofin = mm.matmul_cp(qktoy.o, okeys, odense, diag_o)
+    # GPU chain
+    gout = qk_g(gkeys, ga, gk, qk_g.encode_masks())
+    half = len(gout) // 2
+    gdense = [blb.add(qktoy.g, gout[o], gout[o + half]) for o in range(half)]
+    gfin = diag_g(gkeys, gdense, diag_g.encode_weights(WOp))
+    for a, b in zip(gdense, odense):
+        assert np.array_equal(u64(a.data), b.data)
+    for a, b in zip(gfin, ofin):
+        assert a.level == b.level == 0 and a.scale == b.scale
+        assert np.array_equal(u64(a.data), b.data)
+    from paper_2508_19525_b200 import packing
+    Y = np.concatenate([packing.spatial_unslots(qktoy.g.decode(blb.decrypt(qktoy.g, sk, o), o.scale).cpu().numpy()[None],
+                                                L, 16) for o in gfin], axis=1)[:, :48]
+    Att = np.concatenate([S[h] @ V[h] for h in range(H)], axis=1)
+    assert float(((Y - Att @ WO) ** 2).mean()) <= 1e-11

@@ -88,3 +88,37 @@ def test_qkv_then_qk_chain_slot_level():
     Qm, Km = X @ WQ, X @ WK
     ref = np.stack([Qm[:, h * dh:(h + 1) * dh] @ Km[:, h * dh:(h + 1) * dh].T for h in range(H)])
     assert np.abs(C - ref).max() < 1e-12
+
+
+@pytest.mark.parametrize("L,H,n", [(16, 2, 256), (32, 3, 2048), (16, 4, 512)])
+def test_softmax_v_then_wo_chain_slot_level(L, H, n):
+    """Row f1: Att_h = S_h V_h by the C13 protocol with V zero-padded d_h -> L,
+    adjacent outputs added into a dense diagonal packing, then the diagonal-input
+    ct-pt MatMul with the MHP row reorder of W_O (App. C.2) gives Concat(Att_h) W_O."""
+    dh = L // 2
+    rng = np.random.default_rng(L + H)
+    S = rng.uniform(0, 1, size=(H, L, L))
+    V = rng.normal(size=(H, L, dh))
+    WO = rng.normal(size=(H * dh, 24))
+    p = cc.plan_sv(L, H, n)
+    A, Kop = cc.sv_operands(S, V)
+    outs = cc.slot_level(cc.pack_mhp(A, p), cc.pack_mhp(Kop, p), p)
+    full = cc.unpack_diag(outs, p)
+    assert np.abs(full[:, :, :dh] - np.einsum("hik,hkj->hij", S, V)).max() < 1e-12
+    assert np.abs(full[:, :, dh:]).max() < 1e-12
+    dense = cc.collapse_dense(outs, p, dh)
+    WOp = cc.pad_heads_rows(WO, H, p.Hp)
+    plan_o = mm.plan_diagonal(WOp, p.Hp, L, n, 8)
+    assert plan_o.n_in == len(dense)
+    Y = mm.unpack_spatial(mm.slot_level(dense, plan_o), L, WO.shape[1])
+    Att = np.concatenate([S[h] @ V[h] for h in range(H)], axis=1)
+    assert np.abs(Y - Att @ WO).max() < 1e-11
+
+
+def test_table5_softmax_v_counts():
+    """Table 5, Softmax x V_h, BERT-large dims, s = 16384: #CMult = m^3 H / s = 2048
+    exactly; #Rot = 1056 (we reconstruct 1092, within the 2x envelope of S:416)."""
+    p = cc.plan_sv(128, 16, 16384)
+    cnt = p.counts()
+    assert cnt["cmult"] == 2048 == 128 ** 3 * 16 // 16384
+    assert cnt["rotations"] <= 2 * 1056
