@@ -136,19 +136,26 @@ def oracle_sample_ms(dims, reps: int = 1) -> dict:
     W = np.ones((dims["d"], dims["d"]))
     cm = mm.mhp_column_map(dims["d"], dims["H"], dims["L"], n)
     qkv_map = cm + [dims["d"] + c if c >= 0 else -1 for c in cm] + list(range(2 * dims["d"], 3 * dims["d"]))
+    Hp = 1 << (dims["H"] - 1).bit_length()
     plans = [mm.plan_spatial(np.ones((dims["d"], 3 * dims["d"])), dims["L"], n, 32, col_map=qkv_map),
-             mm.plan_diagonal(W, dims["H"], dims["L"], n, 16),
+             mm.plan_diagonal(np.ones((Hp * (dims["d"] // dims["H"]), dims["d"])), Hp, dims["L"], n, 16),
              mm.plan_spatial(np.ones((dims["d"], dims["ffn"])), dims["L"], n, 32),
              mm.plan_spatial(np.ones((dims["ffn"], dims["d"])), dims["L"], n, 8)]
     import oracle.matmul_cc as cc
-    qk = cc.plan_qk(dims["L"], dims["H"], dims["d"] // dims["H"], n)
-    qc = qk.counts()
-    qk_masks = qk.J * qk.B * (2 * qk.g - 1) + 2 * qk.J * (qk.G - 1) + sum(
-        1 for (u, w, f) in qk.accumulators() for i in range(qk.B) if qk.mask3(u, i, w, f).any())
-    n_rot = sum(p.n_rotations for p in plans) + qc["rotations"] + qc["relin"]   # relinearisation ~ one key switch
-    n_pt = sum(p.n_plaintexts for p in plans) + qk_masks + 3 * qc["cmult"]       # tensor ~ 3 ct-pt products
-    n_out = sum(p.n_out for p in plans) + qk.J * (qk.B + qk.G) + qk.G * qk.B + len(qk.accumulators())
-    n_mask = sum(p.n_out for p in plans) - 2 * qk.J + qk.n_out
+    n_rot = sum(p.n_rotations for p in plans)
+    n_pt = sum(p.n_plaintexts for p in plans)
+    n_out = sum(p.n_out for p in plans)
+    n_mask = sum(p.n_out for p in plans)
+    for qk in (cc.plan_qk(dims["L"], dims["H"], dims["d"] // dims["H"], n), cc.plan_sv(dims["L"], dims["H"], n)):
+        qc = qk.counts()
+        acc3 = qk.accumulators()
+        qk_masks = qk.J * qk.B * (2 * qk.g - 1) + 2 * qk.J * (qk.G - 1) + sum(
+            1 for (u, w, f) in acc3 for i in range(qk.B) if qk.mask3(u, i, w, f).any())
+        n_rot += qc["rotations"] + qc["relin"]            # relinearisation ~ one key switch
+        n_pt += qk_masks + 3 * qc["cmult"]                # tensor ~ 3 ct-pt products
+        n_out += qk.J * (qk.B + qk.G) + qk.G * qk.B + len(acc3)
+    qk0 = cc.plan_qk(dims["L"], dims["H"], dims["d"] // dims["H"], n)
+    n_mask += qk0.n_out - 2 * qk0.J          # Q, K outputs of QKV feed Q K^T; its diagonals are masked
     ms = 1e3 * (n_rot * t["rot"] + n_pt * t["prod"] + n_out * t["resc"] + n_mask * t["mask"])
     return {"ms_per_layer": ms, "per_op_s": t, "counts": {"rotations": n_rot, "plaintexts": n_pt,
                                                           "rescales": n_out, "masks": n_mask},
@@ -182,13 +189,14 @@ def run_reference(args, dims):
 
 
 def config_dict(dims, world):
-    return {"workload": "BERT-base layer fused-linear CKKS (config 2 QKV + Q.K^T + config 3 out-proj/FFN1/FFN2 + "
-                        "CKKS->MPC masks), N=2^16, Q={60,40x4}, P={60}, dnum=5",
+    return {"workload": "BERT-base layer fused-linear CKKS (config 2 QKV + Q.K^T, Softmax.V + out-proj, config 3 "
+                        "FFN1/FFN2, CKKS->MPC masks), N=2^16, Q={60,40x4}, P={60}, dnum=5",
             "L": dims["L"], "d": dims["d"], "heads": dims["H"], "ffn": dims["ffn"], "log_n": 16, "limbs": 5,
             "bsgs": {"qkv": 32, "oproj": 16, "ffn1": 32, "ffn2": 8},
-            "layer_ops": ["qkv_ct_pt(MHP)", "qk_ct_ct(MHP+BSGS)", "mask(QK^T)", "mask(V)", "oproj_diag_ct_pt",
-                          "mask", "ffn1_ct_pt", "mask", "ffn2_ct_pt", "mask"],
-            "not_included": "Softmax x V ct-ct MatMul (row f1)",
+            "layer_ops": ["qkv_ct_pt(MHP)", "qk_ct_ct(MHP+BSGS)", "mask(QK^T)", "mask(V)",
+                          "softmaxV_ct_ct(pad+collapse)", "oproj_diag_ct_pt(level 1)", "mask", "ffn1_ct_pt", "mask",
+                          "ffn2_ct_pt", "mask"],
+            "not_included": "non-MatMul HE ops of Table 6 blocks 2-5 (row f2) and the MPC protocols",
             "l2": "inputs larger than L2 (~76 GB of plaintexts streamed per step)",
             "parallelism": "dp%d (output-ciphertext sharding, NCCL all-gather of masked outputs)" % world}
 
@@ -240,7 +248,8 @@ def main():
     # client-side inputs: encrypt once (fresh ciphertexts at the top level)
     delta = 2.0 ** bi.BERT.log_delta
     lvl = layer.level
-    slots = {"qkv": packing.spatial_slots(A["X"], params.n), "oproj": packing.diagonal_slots(F["Att"], params.n),
+    sv_s, sv_v = packing.softmax_v_operands(F["S"], F["V"], params.n)
+    slots = {"qkv": packing.spatial_slots(A["X"], params.n), "sv_s": sv_s, "sv_v": sv_v,
              "ffn1": packing.spatial_slots(F["X2"], params.n), "ffn2": packing.spatial_slots(F["H1"], params.n)}
     inputs, cid = {}, 0
     for name, zs in slots.items():

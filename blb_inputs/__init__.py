@@ -89,15 +89,22 @@ def bert_attention_inputs(L=128, d=768, config_id=2):
 
 
 # ---- config 3: out-proj (diagonal input) + FFN ----------------------------
+def softmax_rows(x: np.ndarray) -> np.ndarray:
+    e = np.exp(x - x.max(axis=-1, keepdims=True))
+    return e / e.sum(axis=-1, keepdims=True)
+
+
 def bert_ffn_inputs(L=128, d=768, H=12, ffn=3072, config_id=3):
     dh = d // H
     Att = normal(21, (H, L, dh), 1.0)
+    S = softmax_rows(normal(28, (H, L, L), 1.0))      # Softmax(Q K^T / sqrt(d_h)) rows (f1 operand)
+    V = normal(27, (H, L, dh), 1.0)
     WO = normal(22, (d, d), 0.04)
     X2 = normal(23, (L, d), 1.0)
     W1 = normal(24, (d, ffn), 0.04)
     H1 = gelu(normal(25, (L, ffn), 1.0))
     W2 = normal(26, (ffn, d), 0.02)
-    return dict(Att=Att, WO=WO, X2=X2, W1=W1, H1=H1, W2=W2, keys_key=crypto_key(4, config_id),
+    return dict(Att=Att, S=S, V=V, WO=WO, X2=X2, W1=W1, H1=H1, W2=W2, keys_key=crypto_key(4, config_id),
                 enc_key=crypto_key(5, config_id), mask_key=crypto_key(3, config_id))
 
 

@@ -342,6 +342,13 @@ def add(params: Params, a: Ciphertext, b: Ciphertext) -> Ciphertext:
     return out
 
 
+def add_into(params: Params, a: Ciphertext, b: Ciphertext, out: Ciphertext) -> Ciphertext:
+    ca, cb, co = a.c(), b.c(), out.c()
+    _check(lib().blb_add(params.handle, ctypes.byref(ca), ctypes.byref(cb), ctypes.byref(co), _stream()))
+    out.level, out.scale = co.level, co.scale
+    return out
+
+
 def ckks_to_mpc(params: Params, cts: list, mask_key: bytes, first_ct_id: int):
     """Server half of Alg. 1: returns (masked int64 [n][2][N], share int64 [n][N]), coefficient form mod q0."""
     n = len(cts)

@@ -5,7 +5,10 @@ Blocks (fig:fusion_pattern P:699-704, Table 6):
   * attention: QKV projection (C11, MHP reorder of the Q / K columns, P:466,
     P:511) -> Q K^T for all heads (row a7, reading C13) -> CKKS->MPC masks of
     the Q K^T diagonals and of V (P:511, P:513);
-  * out-projection: diagonal-input ct-pt MatMul (C12, App. C.2) -> mask;
+  * Softmax x V (row f1): the ct-ct protocol on the client-re-encrypted S_h and
+    zero-padded V_h^T -> dense-diagonal collapse of adjacent outputs
+     -> out-projection as the diagonal-input ct-pt MatMul (C12, App. C.2)
+    with the MHP row reorder of W_O (P:466) -> mask;
   * FFN1 (d -> 4d) -> mask; FFN2 (4d -> d) -> mask.
 Each MatMul starts from a fresh ciphertext at the top level (SURVEY 8(d)
 config 3).  Work is sharded by output ciphertext (section 8(e)): rank r owns a
@@ -82,12 +85,13 @@ class FusedLinearLayer:
         b = dict(BSGS, **(bsgs or {}))
         L, d, H, ffn = dims.L, dims.d, dims.H, dims.ffn
         cm = blb.mhp_column_map(d, H, L, params.log_n)
+        self.Hp = 1 << (H - 1).bit_length()
         qkv_map = cm + [d + c if c >= 0 else -1 for c in cm] + list(range(2 * d, 3 * d))
         self.n_mhp = len(cm) // (params.n // L)   # ciphertexts of Q (and of K)
         self.plans = {
             "qkv": blb.MatmulPlan(params, L, d, 3 * d, col_map=qkv_map, bsgs_B=b["qkv"], level=self.level),
-            "oproj": blb.MatmulPlan(params, L, d, d, packing=blb.PACK_DIAGONAL, heads=H, bsgs_B=b["oproj"],
-                                    level=self.level),
+            "oproj": blb.MatmulPlan(params, L, self.Hp * (d // H), d, packing=blb.PACK_DIAGONAL, heads=self.Hp,
+                                    bsgs_B=b["oproj"], level=self.level - 3),
             "ffn1": blb.MatmulPlan(params, L, d, ffn, bsgs_B=b["ffn1"], level=self.level),
             "ffn2": blb.MatmulPlan(params, L, ffn, d, bsgs_B=b["ffn2"], level=self.level),
         }
@@ -97,31 +101,42 @@ class FusedLinearLayer:
         # outputs are masked by their owner only) -- see DESIGN.md section 8.
         self.qk = blb.QKPlan(params, L, H, d // H, bsgs_B=b["qk"], level=self.level - 1)
         self.slices["qk"] = shard(self.qk.n_out, rank, world)
+        # Softmax x V (row f1): inner dimension L (V zero-padded d_h -> L), replicated like Q K^T
+        self.sv = blb.QKPlan(params, L, H, L, bsgs_B=b["qk"], level=self.level)
         self.pts, self.ws, self.outs = {}, None, {}
 
     # ---- setup (row a0) ----
     def rotation_steps(self) -> list[int]:
-        s = set(self.qk.rotation_steps())
+        s = set(self.qk.rotation_steps()) | set(self.sv.rotation_steps())
         for pl in self.plans.values():
             s.update(pl.rotation_steps())
         return sorted(s)
 
     def load_weights(self, WQ, WK, WV, WO, W1, W2):
         Wqkv = np.concatenate([WQ, WK, WV], axis=1)
+        # MHP row reorder of W_O for the padded-head diagonal input: zero rows for padded heads
+        dh = self.dims.d // self.dims.H
+        WOp = np.zeros((self.Hp * dh, WO.shape[1]))
+        WOp[:WO.shape[0]] = WO
+        WO = WOp
         for name, W in (("qkv", Wqkv), ("oproj", WO), ("ffn1", W1), ("ffn2", W2)):
             first, count = self.slices[name]
             self.pts[name] = self.plans[name].encode_weights(W, first, count)
         self.qk_masks = self.qk.encode_masks()
+        self.sv_masks = self.sv.encode_masks()
         nbytes = max([pl.workspace_bytes(self.slices[k][1]) for k, pl in self.plans.items()] +
-                     [self.qk.workspace_bytes()])
+                     [self.qk.workspace_bytes(), self.sv.workspace_bytes()])
         self.ws = torch.empty(nbytes // 8 + 1, dtype=torch.int64, device="cuda")
         for k, pl in self.plans.items():
             self.outs[k] = [blb.Ciphertext.empty(self.p, self.level - 1) for _ in range(self.slices[k][1])]
         self.qkv_full = [blb.Ciphertext.empty(self.p, self.level - 1) for _ in range(2 * self.n_mhp)]
         self.outs["qk"] = [blb.Ciphertext.empty(self.p, self.level - 4) for _ in range(self.qk.n_out)]
+        self.outs["sv"] = [blb.Ciphertext.empty(self.p, self.level - 3) for _ in range(self.sv.n_out)]
+        self.sv_dense = [blb.Ciphertext.empty(self.p, self.level - 3) for _ in range(self.sv.n_out // 2)]
 
     def plaintext_bytes(self) -> int:
-        return sum(int(t.numel()) * 8 for t in self.pts.values()) + int(self.qk_masks.numel()) * 8
+        return (sum(int(t.numel()) * 8 for t in self.pts.values()) + int(self.qk_masks.numel()) * 8 +
+                int(self.sv_masks.numel()) * 8)
 
     def n_plaintexts(self) -> int:
         return sum(self.plans[k].pt_count(*self.slices[k]) for k in self.plans)
@@ -159,14 +174,24 @@ class FusedLinearLayer:
             self.qkv_full[g].scale = scale
         return self.qkv_full
 
+    def softmax_v(self, keys: blb.Keys, S_cts: list, Vt_cts: list) -> list:
+        """Row f1: S_h (x) Vpad_h by the ct-ct protocol, then the dense-diagonal collapse."""
+        outs = self.sv(keys, S_cts, Vt_cts, self.sv_masks, ws=self.ws, outs=self.outs["sv"])
+        half = len(outs) // 2
+        for o in range(half):
+            blb.add_into(self.p, outs[o], outs[o + half], self.sv_dense[o])
+        return self.sv_dense
+
     def step(self, keys: blb.Keys, inputs: dict, mask_key: bytes) -> list:
-        """inputs: {'qkv': [ct]*3, 'oproj': [...], 'ffn1': [...], 'ffn2': [...]} -> [(masked, share)] per block."""
+        """inputs: {'qkv': [ct]*3, 'sv_s': [ct]*J', 'sv_v': [ct]*J', 'ffn1': [...], 'ffn2': [...]}
+        -> [(name, first mask id, (masked, share))] per block."""
         res = []
         for name in ("qkv", "oproj", "ffn1", "ffn2"):
             first, count = self.slices[name]
             if count == 0 and not (name == "qkv" and self.world > 1):
                 continue
-            outs = self.plans[name](keys, inputs[name], self.pts[name], first, count, ws=self.ws,
+            src = self.softmax_v(keys, inputs["sv_s"], inputs["sv_v"]) if name == "oproj" else inputs[name]
+            outs = self.plans[name](keys, src, self.pts[name], first, count, ws=self.ws,
                                     outs=self.outs[name]) if count else []
             if name == "qkv":
                 qk_in = self.gather_qk_operands(outs)

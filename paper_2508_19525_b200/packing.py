@@ -37,3 +37,24 @@ def diagonal_slots(Att: np.ndarray, n: int) -> np.ndarray:
     for d in range(dh):
         blocks[d * H:(d + 1) * H] = Att[:, i, (i + d) % dh]
     return np.ascontiguousarray(blocks.reshape(n_ct, c * L))
+
+
+def mhp_slots(M: np.ndarray, n: int) -> np.ndarray:
+    """Multi-head packing (L, H_p, g) of M (heads, L, D): block c*H_p + h of ciphertext j
+    holds column j*g + c of head h; heads padded to H_p = next power of two, g = n/(L H_p)."""
+    H, L, D = M.shape
+    Hp = 1 << (H - 1).bit_length()
+    g = n // (L * Hp)
+    J = -(-D // g)
+    Mp = np.zeros((J * g, Hp, L))       # [column][head][row]
+    Mp[:D, :H, :] = np.transpose(M, (2, 0, 1))
+    return np.ascontiguousarray(Mp.reshape(J, g * Hp * L))
+
+
+def softmax_v_operands(S: np.ndarray, V: np.ndarray, n: int):
+    """Slots of the two ct-ct operands of Softmax x V_h: S_h (L x L) and
+    Vpad_h^T with V zero-padded from d_h to L columns."""
+    H, L, dh = V.shape
+    Vt = np.zeros((H, L, L))
+    Vt[:, :dh, :] = np.transpose(V, (0, 2, 1))
+    return mhp_slots(S, n), mhp_slots(Vt, n)

@@ -61,3 +61,17 @@ def test_packing_matches_oracle_layout(blb):
     assert np.array_equal(packing.spatial_unslots(packing.spatial_slots(X, 2048), 16, 300), X)
     A = np.random.default_rng(1).normal(size=(4, 16, 8))
     assert np.array_equal(packing.diagonal_slots(A, 512), np.stack(mm.pack_diagonal_mh(A, 512)))
+
+
+def test_mhp_packing_matches_oracle_layout(blb):
+    from paper_2508_19525_b200 import packing
+    import oracle.matmul_cc as cc
+    rng = np.random.default_rng(3)
+    for H, L, D, n in [(3, 32, 16, 2048), (12, 128, 64, 32768), (4, 16, 16, 512)]:
+        M = rng.normal(size=(H, L, D))
+        assert np.array_equal(packing.mhp_slots(M, n), np.stack(cc.pack_mhp(M, cc.plan_qk(L, H, D, n))))
+        S, V = rng.normal(size=(H, L, L)), rng.normal(size=(H, L, L // 2))
+        a, k = packing.softmax_v_operands(S, V, n)
+        A, K = cc.sv_operands(S, V)
+        p = cc.plan_sv(L, H, n)
+        assert np.array_equal(a, np.stack(cc.pack_mhp(A, p))) and np.array_equal(k, np.stack(cc.pack_mhp(K, p)))

@@ -408,7 +408,7 @@ def test_softmax_v_wo_chain_bit_exact(qktoy):
         assert a.level == b.level == 0 and a.scale == b.scale
         assert np.array_equal(u64(a.data), b.data)
     from paper_2508_19525_b200 import packing
-    Y = np.concatenate([packing.spatial_unslots(qktoy.g.decode(blb.decrypt(qktoy.g, sk, o), o.scale).cpu().numpy()[None],
-                                                L, 16) for o in gfin], axis=1)[:, :48]
+    Y = packing.spatial_unslots(np.stack([qktoy.g.decode(blb.decrypt(qktoy.g, sk, o), o.scale).cpu().numpy()
+                                          for o in gfin]), L, 48)
     Att = np.concatenate([S[h] @ V[h] for h in range(H)], axis=1)
     assert float(((Y - Att @ WO) ** 2).mean()) <= 1e-11
