@@ -144,32 +144,37 @@ __device__ __forceinline__ void mac_run(const u64 *__restrict__ pp, const u64 *_
     using A = typename std::conditional<SPLIT41, Acc41, Acc128>::type;
     A a00, a01, a10, a11;
     a00.zero(); a01.zero(); a10.zero(); a11.zero();
+    // register double buffer: the loads of entries e+2, e+3 are in flight while e, e+1 are multiplied
+    constexpr int D = 2;
+    ulonglong2 pv[2][D], r0[2][D], r1[2][D];
+    auto load = [&](int s, int e) {
+#pragma unroll
+        for (int u = 0; u < D; u++) {
+            const int ee = e + u < n_e ? e + u : n_e - 1;
+            const int bi = ent_r[e_lo + ee];
+            pv[s][u] = *reinterpret_cast<const ulonglong2 *>(pp + (long long)ee * 512);
+            r0[s][u] = *reinterpret_cast<const ulonglong2 *>(R + (long long)bi * 2 * kN + lx);
+            r1[s][u] = *reinterpret_cast<const ulonglong2 *>(R + ((long long)bi * 2 + 1) * kN + lx);
+        }
+    };
+    auto compute = [&](int s, int e) {
+#pragma unroll
+        for (int u = 0; u < D; u++) {
+            if (e + u < n_e) {
+                a00.mac(pv[s][u].x, r0[s][u].x); a01.mac(pv[s][u].y, r0[s][u].y);
+                a10.mac(pv[s][u].x, r1[s][u].x); a11.mac(pv[s][u].y, r1[s][u].y);
+            }
+        }
+    };
+    if (n_e > 0) load(0, 0);
     int e = 0;
-    for (; e + 4 <= n_e; e += 4) {
-        int bi[4];
-        ulonglong2 pv[4], r0[4], r1[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) bi[u] = ent_r[e_lo + e + u];
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            pv[u] = *reinterpret_cast<const ulonglong2 *>(pp + (long long)(e + u) * 512);
-            r0[u] = *reinterpret_cast<const ulonglong2 *>(R + (long long)bi[u] * 2 * kN + lx);
-            r1[u] = *reinterpret_cast<const ulonglong2 *>(R + ((long long)bi[u] * 2 + 1) * kN + lx);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            a00.mac(pv[u].x, r0[u].x); a01.mac(pv[u].y, r0[u].y);
-            a10.mac(pv[u].x, r1[u].x); a11.mac(pv[u].y, r1[u].y);
-        }
+    for (; e + D < n_e; e += 2 * D) {
+        load(1, e + D);
+        compute(0, e);
+        if (e + 2 * D < n_e) load(0, e + 2 * D);
+        compute(1, e + D);
     }
-    for (; e < n_e; e++) {
-        const int bi = ent_r[e_lo + e];
-        const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(pp + (long long)e * 512);
-        const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(R + (long long)bi * 2 * kN + lx);
-        const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(R + ((long long)bi * 2 + 1) * kN + lx);
-        a00.mac(pv.x, r0.x); a01.mac(pv.y, r0.y);
-        a10.mac(pv.x, r1.x); a11.mac(pv.y, r1.y);
-    }
+    if (e < n_e) compute(0, e);
     *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00.reduce(mc), a01.reduce(mc));
     *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(mc), a11.reduce(mc));
 }
