@@ -212,8 +212,13 @@ struct KsGroups {
     int n;
     int start[kMaxJobs + 1];
 };
-__global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, int np, int K, int beta, int logN) {
+// BETA > 0: digit count known at compile time (all loads of a thread are issued
+// before the first multiply); BETA = 0: runtime beta.
+template <int BETA>
+__global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, int np, int K, int beta_rt,
+                           int logN) {
     const int N = 1 << logN;
+    const int beta = BETA > 0 ? BETA : beta_rt;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int m = blockIdx.y, gi = blockIdx.z;
     if (x >= N) return;
@@ -226,15 +231,38 @@ __global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, 
     Acc128 a0[kKsGroup], a1[kKsGroup];
 #pragma unroll
     for (int q = 0; q < kKsGroup; q++) { a0[q].zero(); a1[q].zero(); }
-    for (int j = 0; j < beta; j++) {
-        const u64 kb = J0.key[(((long long)j * 2 + 0) * Lk + pm) * N + x];
-        const u64 ka = J0.key[(((long long)j * 2 + 1) * Lk + pm) * N + x];
+    if (BETA > 0) {
+        u64 kb[BETA > 0 ? BETA : 1], ka[BETA > 0 ? BETA : 1];
+#pragma unroll
+        for (int j = 0; j < BETA; j++) {
+            kb[j] = J0.key[(((long long)j * 2 + 0) * Lk + pm) * N + x];
+            ka[j] = J0.key[(((long long)j * 2 + 1) * Lk + pm) * N + x];
+        }
 #pragma unroll
         for (int q = 0; q < kKsGroup; q++) {
             if (q < cnt) {
-                const u64 e = jobs.j[t0 + q].ext[((long long)j * E + m) * N + src];
-                a0[q].mac(e, kb);
-                a1[q].mac(e, ka);
+                u64 e[BETA > 0 ? BETA : 1];
+                const u64 *ext = jobs.j[t0 + q].ext + (long long)m * N + src;
+#pragma unroll
+                for (int j = 0; j < BETA; j++) e[j] = ext[(long long)j * E * N];
+#pragma unroll
+                for (int j = 0; j < BETA; j++) {
+                    a0[q].mac(e[j], kb[j]);
+                    a1[q].mac(e[j], ka[j]);
+                }
+            }
+        }
+    } else {
+        for (int j = 0; j < beta; j++) {
+            const u64 kb = J0.key[(((long long)j * 2 + 0) * Lk + pm) * N + x];
+            const u64 ka = J0.key[(((long long)j * 2 + 1) * Lk + pm) * N + x];
+#pragma unroll
+            for (int q = 0; q < kKsGroup; q++) {
+                if (q < cnt) {
+                    const u64 e = jobs.j[t0 + q].ext[((long long)j * E + m) * N + src];
+                    a0[q].mac(e, kb);
+                    a1[q].mac(e, ka);
+                }
             }
         }
     }
@@ -433,7 +461,16 @@ blb_status launch_keyswitch(const blb_params *P, int level, const KsJob *jobs, i
         G.start[G.n] = t;
     }
     cudaEvent_t t0 = blb_timing_begin(st);
-    k_ks_inner<<<grid_x(N, E, G.n), kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN);
+    const dim3 gks = grid_x(N, E, G.n);
+    switch (beta) {
+        case 1: k_ks_inner<1><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN); break;
+        case 2: k_ks_inner<2><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN); break;
+        case 3: k_ks_inner<3><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN); break;
+        case 4: k_ks_inner<4><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN); break;
+        case 5: k_ks_inner<5><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN); break;
+        case 6: k_ks_inner<6><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN); break;
+        default: k_ks_inner<0><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN); break;
+    }
     BLB_COUNT_LAUNCH(1);
     blb_timing_end(2, t0, st, (double)G.n * 2.0 * beta * E * N * 8.0);
     BLB_CHECK_LAUNCH();

@@ -201,6 +201,99 @@ __global__ void __launch_bounds__(kTB) k_mac_w(const u64 *__restrict__ pt, const
     else mac_run<false>(pp, R, ent_r, e_lo, n_e, kN, lx, out, mc);
 }
 
+// Warp-specialised weight MAC: warp 8 streams, per pipeline stage, two entries'
+// plaintext tiles (8 KB contiguous in the blocked layout) and their four R tiles
+// (4 KB each, L2-resident) into a 4-stage shared-memory ring with cp.async.bulk
+// (TMA bulk-copy engine, mbarrier completion); warps 0-7 multiply-accumulate
+// from shared memory and release the stage.  Global latency is hidden by the
+// ring, so the 8 consumer warps only issue LDS + integer MACs.
+constexpr int kMacStages = 4, kMacEnt = 2;
+constexpr int kMacStageWords = kMacEnt * 3 * 512;  // pt, r0, r1 per entry
+constexpr size_t kMacSmem = (size_t)kMacStages * kMacStageWords * 8 + 2 * kMacStages * 8;
+
+template <bool SPLIT41>
+__device__ __forceinline__ void mac_tma_consume(const u64 *ring, uint64_t *full, uint64_t *empty, int n_e, u64 *out,
+                                                long long kN, const ModConst &mc) {
+    using A = typename std::conditional<SPLIT41, Acc41, Acc128>::type;
+    A a00, a01, a10, a11;
+    a00.zero(); a01.zero(); a10.zero(); a11.zero();
+    const int t = threadIdx.x;
+    const int n_st = (n_e + kMacEnt - 1) / kMacEnt;
+    for (int s = 0; s < n_st; s++) {
+        const int slot = s % kMacStages;
+        mbar_wait(&full[slot], (s / kMacStages) & 1);
+        const u64 *st = ring + (size_t)slot * kMacStageWords;
+#pragma unroll
+        for (int u = 0; u < kMacEnt; u++) {
+            if (s * kMacEnt + u < n_e) {
+                const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(st + u * 512 + 2 * t);
+                const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + (kMacEnt + 2 * u) * 512 + 2 * t);
+                const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + (kMacEnt + 2 * u + 1) * 512 + 2 * t);
+                a00.mac(pv.x, r0.x); a01.mac(pv.y, r0.y);
+                a10.mac(pv.x, r1.x); a11.mac(pv.y, r1.y);
+            }
+        }
+        __syncwarp();
+        if ((t & 31) == 0) mbar_arrive(&empty[slot]);
+    }
+    *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00.reduce(mc), a01.reduce(mc));
+    *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(mc), a11.reduce(mc));
+}
+
+__global__ void __launch_bounds__(kTB + 32) k_mac_tma(const u64 *__restrict__ pt, const u64 *__restrict__ R,
+                                                      u64 *__restrict__ acc, const int *__restrict__ ent_r,
+                                                      const int *__restrict__ ent_start, int o0, int e_base, int n_o,
+                                                      int k, int logN, Primes pr) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    u64 *ring = reinterpret_cast<u64 *>(smraw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)kMacStages * kMacStageWords);
+    uint64_t *empty = full + kMacStages;
+    const int N = 1 << logN;
+    const int n_tiles = N / (2 * kTB);
+    int bid = blockIdx.x;
+    const int o = bid % n_o;
+    bid /= n_o;
+    const int tile = bid % n_tiles;
+    const int l = bid / n_tiles;
+    const long long kN = (long long)k * N;
+    const int e_lo = ent_start[o0 + o], n_e = ent_start[o0 + o + 1] - e_lo;
+    const long long lx0 = (long long)l * N + tile * 2 * kTB;
+    const u64 *pp = pt + (long long)(e_lo - e_base) * kN + (long long)l * n_e * N + (long long)tile * n_e * 512;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kMacStages; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kTB / 32);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int n_st = (n_e + kMacEnt - 1) / kMacEnt;
+    if (threadIdx.x >= kTB) {  // producer warp
+        const int lane = threadIdx.x - kTB;
+        if (lane == 0) {
+            for (int s = 0; s < n_st; s++) {
+                const int slot = s % kMacStages;
+                if (s >= kMacStages) mbar_wait(&empty[slot], ((s / kMacStages) - 1) & 1);
+                const int ne = min(kMacEnt, n_e - s * kMacEnt);
+                u64 *st = ring + (size_t)slot * kMacStageWords;
+                mbar_expect_tx(&full[slot], (unsigned)ne * 3 * 4096);
+                bulk_g2s(st, pp + (long long)s * kMacEnt * 512, (unsigned)ne * 4096, &full[slot]);
+                for (int u = 0; u < ne; u++) {
+                    const int bi = ent_r[e_lo + s * kMacEnt + u];
+                    bulk_g2s(st + (kMacEnt + 2 * u) * 512, R + (long long)bi * 2 * kN + lx0, 4096, &full[slot]);
+                    bulk_g2s(st + (kMacEnt + 2 * u + 1) * 512, R + ((long long)bi * 2 + 1) * kN + lx0, 4096,
+                             &full[slot]);
+                }
+            }
+        }
+        return;
+    }
+    u64 *out = acc + (long long)o * 2 * kN + lx0 + 2 * threadIdx.x;
+    const ModConst &mc = pr.m[l];
+    if (mc.q < (1ull << 41)) mac_tma_consume<true>(ring, full, empty, n_e, out, kN, mc);
+    else mac_tma_consume<false>(ring, full, empty, n_e, out, kN, mc);
+}
+
 // scatter standard [cnt][k][N] plaintexts (entries e0..e0+cnt of the plan) into the blocked layout
 __global__ void k_block_pts(const u64 *src, u64 *dst, const int *ent_start, const int *ent_o, int e0, int e_base,
                             int k, int N) {
@@ -633,6 +726,15 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
             if (n_o > 0) {
                 const int n_tiles = N / (2 * kTB);
                 cudaEvent_t t0 = blb_timing_begin(st);
+                if (P->mac_tma) {
+                    static bool attr = false;
+                    if (!attr) {
+                        cudaFuncSetAttribute(k_mac_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMacSmem);
+                        attr = true;
+                    }
+                    k_mac_tma<<<(unsigned)((size_t)n_o * n_tiles * k), kTB + 32, kMacSmem, st>>>(
+                        pt_dev, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN, P->pr);
+                } else
                 k_mac_w<<<(unsigned)((size_t)n_o * n_tiles * k), kTB, 0, st>>>(pt_dev, R, acc_c, pl->d_ent,
                                                                               pl->d_ent_start, o0, e_base, n_o, k,
                                                                               P->logN, P->pr);
