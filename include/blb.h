@@ -279,6 +279,30 @@ blb_status blb_ct_pt_matmul(const blb_matmul_plan *plan, const blb_keys *keys, c
                             size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------ */
+/* row f2: other HE operators of the fused blocks                       */
+/* ------------------------------------------------------------------ */
+size_t blb_f2_workspace_bytes(const blb_params *params, int level);
+
+/* ct (x) ct with relinearisation (C9; ewmul_cc of Table 2, e.g. the squarings of
+ * Softmax's negExp (1 + x/2^6)^{2^6}, and GeLU's x^2 / x^4):
+ * out = (d0, d1) + KeySwitch(d2, rlk), same level, scale a.scale * b.scale (the
+ * caller rescales).  Needs the relinearisation key (Galois element 0). */
+blb_status blb_mul_relin(const blb_params *params, const blb_keys *keys, const blb_ct *a, const blb_ct *b,
+                         blb_ct *out, void *ws, size_t ws_bytes, void *stream);
+
+/* Rotate-and-sum of BLB's summation operator (Table 3) on a
+ * spatial-first ciphertext with L rows and D (power of two) columns:
+ * m^0 = in, m^i = m^{i-1} + Rot_l^{2^{i-1} L}(m^{i-1}), out = m^{log2 D}: log2 D
+ * rotations, no multiplication -- the fused form (Table 3 "BLB (w/ fusion)": the
+ * result is replicated across the D column blocks, ready for a following scalar
+ * operator).  The unfused form multiplies by the [1..1, 0..0] mask (blb_mul_pt).
+ * blb_broadcast is the same with right rotations (m_r).  out may not alias in. */
+blb_status blb_rotate_sum(const blb_params *params, const blb_keys *keys, const blb_ct *in, int L, int D,
+                          blb_ct *out, void *ws, size_t ws_bytes, void *stream);
+blb_status blb_broadcast(const blb_params *params, const blb_keys *keys, const blb_ct *in, int L, int D,
+                         blb_ct *out, void *ws, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------ */
 /* ct-ct MatMul Q_h K_h^T for all heads (row a7; sec. 5.1,    */
 /* App. C.1; reading C13)                                   */
 /* ------------------------------------------------------------------ */

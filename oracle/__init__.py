@@ -473,3 +473,23 @@ def mask(ctx: Ctx, ct: Ct, mask_key: bytes, ct_id: int):
     share = np.empty(ctx.N, dtype=np.uint64)
     lib().orc_mask(ctx._h, _p(_u64(ct.data)), ct.level, mask_key, ct_id, _p(masked), _p(share))
     return masked, share
+
+
+# ---------------------------------------------------------------------------
+# row f2: other HE operators of the fused blocks
+# ---------------------------------------------------------------------------
+def mul_relin(ctx: Ctx, a: Ct, b: Ct, keys: Keys) -> Ct:
+    """ewmul_cc (Table 2): relinearised ct x ct product (C9), no rescale."""
+    return relinearize(ctx, tensor(ctx, a, b), keys)
+
+
+def rotate_sum(ctx: Ctx, ct: Ct, keys: Keys, L: int, D: int, broadcast: bool = False) -> Ct:
+    """m^0 = m, m^i = m^{i-1} + Rot^{2^{i-1} L}(m^{i-1}), i = 1..log2 D (left
+    rotations for sum, right rotations for broadcast); the fused form (no mask)."""
+    assert D > 0 and D & (D - 1) == 0
+    cur = ct.copy()
+    step = L
+    while step < L * D:
+        cur = add(ctx, cur, rotate(ctx, cur, keys, -step if broadcast else step))
+        step *= 2
+    return cur

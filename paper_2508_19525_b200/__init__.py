@@ -93,6 +93,10 @@ def lib() -> ctypes.CDLL:
             "blb_matmul_workspace_bytes": ([vp, ctypes.c_int], ctypes.c_size_t),
             "blb_ct_pt_matmul": ([vp, vp, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t,
                                   vp], ctypes.c_int),
+            "blb_f2_workspace_bytes": ([vp, ctypes.c_int], ctypes.c_size_t),
+            "blb_mul_relin": ([vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
+            "blb_rotate_sum": ([vp, vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
+            "blb_broadcast": ([vp, vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
             "blb_qk_plan_create": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp],
                                    ctypes.c_int),
             "blb_qk_plan_destroy": ([vp], None),
@@ -358,6 +362,34 @@ def ckks_to_mpc(params: Params, cts: list, mask_key: bytes, first_ct_id: int):
     _check(lib().blb_ckks_to_mpc(params.handle, arr, n, mask_key, first_ct_id, _ptr(masked), _ptr(share), None, 0,
                                  _stream()))
     return masked, share
+
+
+def _f2_ws(params: Params, level: int) -> torch.Tensor:
+    return torch.empty(int(lib().blb_f2_workspace_bytes(params.handle, level)) // 8 + 1, dtype=torch.int64,
+                       device="cuda")
+
+
+def mul_relin(params: Params, keys: Keys, a: Ciphertext, b: Ciphertext) -> Ciphertext:
+    """ct x ct + relinearisation (row f2, C9); the caller rescales."""
+    out = Ciphertext.empty(params, a.level)
+    ws = _f2_ws(params, a.level)
+    ca, cb, co = a.c(), b.c(), out.c()
+    _check(lib().blb_mul_relin(params.handle, keys.handle, ctypes.byref(ca), ctypes.byref(cb), ctypes.byref(co),
+                               _ptr(ws), ws.numel() * 8, _stream()))
+    out.level, out.scale = co.level, co.scale
+    return out
+
+
+def rotate_sum(params: Params, keys: Keys, ct: Ciphertext, L: int, D: int, broadcast: bool = False) -> Ciphertext:
+    """Rotate-and-sum: log2 D rotations, fused form (no mask)."""
+    out = Ciphertext.empty(params, ct.level)
+    ws = _f2_ws(params, ct.level)
+    ci, co = ct.c(), out.c()
+    fn = lib().blb_broadcast if broadcast else lib().blb_rotate_sum
+    _check(fn(params.handle, keys.handle, ctypes.byref(ci), L, D, ctypes.byref(co), _ptr(ws), ws.numel() * 8,
+              _stream()))
+    out.level, out.scale = co.level, co.scale
+    return out
 
 
 def mhp_column_map(d: int, heads: int, L: int, log_n: int) -> list[int]:

@@ -33,6 +33,7 @@ blb_status blb_launch_decrypt(const blb_params *P, const u64 *c0, const u64 *c1,
 blb_status blb_launch_mul_pt(const blb_params *P, const u64 *in, const u64 *pt, u64 *out, int k, cudaStream_t st);
 blb_status blb_launch_add(const blb_params *P, const u64 *a, const u64 *b, u64 *out, int k, int npoly,
                           cudaStream_t st);
+blb_status blb_launch_tensor(const blb_params *P, const u64 *a, const u64 *b, u64 *d, int k, cudaStream_t st);
 blb_status blb_launch_mask(const blb_params *P, const u64 *const *in, int n, int level, const uint8_t key[32],
                            u64 id0, u64 *masked, u64 *share, cudaStream_t st);
 
@@ -680,4 +681,75 @@ extern "C" blb_status blb_mhp_column_map(int d, int heads, int L, int log_n, int
     }
     *len = need;
     return BLB_OK;
+}
+
+// ------------------------------------------------------------ row f2: other fused-block HE ops
+extern "C" size_t blb_f2_workspace_bytes(const blb_params *P, int level) {
+    if (!P || level < 0 || level >= P->K) return 0;
+    const size_t N = P->N, k = level + 1;
+    // tensor [3][k][N] + one rotation workspace + a temporary ciphertext [2][k][N]
+    return sizeof(u64) * (3 * k * N + 2 * k * N) + blb_workspace_bytes(P, BLB_OP_ROTATE, level);
+}
+
+extern "C" blb_status blb_mul_relin(const blb_params *P, const blb_keys *K, const blb_ct *a, const blb_ct *b,
+                                    blb_ct *out, void *ws, size_t ws_bytes, void *stream) {
+    if (!P || !K || !a || !b || !out || !a->data || !b->data || !out->data || !ws) return BLB_E_INVALID_ARG;
+    if (a->level != b->level || a->level < 0 || a->level >= P->K) {
+        blb_set_error("blb_mul_relin: operands must share one level");
+        return BLB_E_LEVEL;
+    }
+    const u64 *rlk = find_key(K, 0);
+    if (!rlk) {
+        blb_set_error("missing relinearisation key");
+        return BLB_E_MISSING_KEY;
+    }
+    const int level = a->level, k = level + 1, N = P->N, E = k + P->np, beta = blb_beta(P, level);
+    if (ws_bytes < blb_f2_workspace_bytes(P, level)) return BLB_E_NOMEM;
+    cudaStream_t st = (cudaStream_t)stream;
+    u64 *d = (u64 *)ws;
+    u64 *ext = d + (size_t)3 * k * N, *coef = ext + (size_t)beta * E * N, *u = coef + (size_t)k * N;
+    u64 *conv = u + (size_t)2 * E * N;
+    BLB_TRY(blb_launch_tensor(P, a->data, b->data, d, k, st));
+    const u64 *d2 = d + (size_t)2 * k * N;
+    BLB_TRY(launch_modup(P, level, &d2, 1, ext, coef, st));
+    KsJob J{};
+    J.ext = ext; J.key = rlk; J.c0 = d; J.c1_add = d + (size_t)k * N; J.out = out->data; J.galois = 1; J.add_mode = 2;
+    BLB_TRY(launch_keyswitch(P, level, &J, 1, u, conv, st));
+    BLB_COUNT(3, 1);
+    out->level = level;
+    out->scale = a->scale * b->scale;
+    return BLB_OK;
+}
+
+// Rotate-and-sum: m^0 = m, m^i = m^{i-1} + Rot^{2^{i-1} L}(m^{i-1}), i = 1..log2 D,
+// left rotations for sum (direction = +1), right rotations for broadcast (direction = -1).
+static blb_status rotate_and_sum(const blb_params *P, const blb_keys *K, const blb_ct *in, int L, int D, int dir,
+                                 blb_ct *out, void *ws, size_t ws_bytes, cudaStream_t st) {
+    if (!P || !K || !in || !out || !in->data || !out->data || !ws || in->data == out->data) return BLB_E_INVALID_ARG;
+    if (L <= 0 || D <= 0 || (D & (D - 1))) {
+        blb_set_error("rotate-and-sum: D must be a power of two (pad otherwise)");
+        return BLB_E_LAYOUT;
+    }
+    const int level = in->level, k = level + 1, N = P->N;
+    if (ws_bytes < blb_f2_workspace_bytes(P, level)) return BLB_E_NOMEM;
+    u64 *tmp = (u64 *)ws + (size_t)3 * k * N;
+    u64 *rws = tmp + (size_t)2 * k * N;
+    const size_t rbytes = blb_workspace_bytes(P, BLB_OP_ROTATE, level);
+    BLB_CUDA_TRY(cudaMemcpyAsync(out->data, in->data, sizeof(u64) * 2 * k * N, cudaMemcpyDeviceToDevice, st));
+    out->level = level;
+    out->scale = in->scale;
+    for (int step = L; step < L * D; step *= 2) {
+        blb_ct cur = *out, t{tmp, level, 0, in->scale};
+        BLB_TRY(blb_rotate(P, K, &cur, dir * step, &t, rws, rbytes, st));
+        BLB_TRY(blb_launch_add(P, out->data, tmp, out->data, k, 2, st));
+    }
+    return BLB_OK;
+}
+extern "C" blb_status blb_rotate_sum(const blb_params *P, const blb_keys *K, const blb_ct *in, int L, int D,
+                                     blb_ct *out, void *ws, size_t ws_bytes, void *stream) {
+    return rotate_and_sum(P, K, in, L, D, +1, out, ws, ws_bytes, (cudaStream_t)stream);
+}
+extern "C" blb_status blb_broadcast(const blb_params *P, const blb_keys *K, const blb_ct *in, int L, int D,
+                                    blb_ct *out, void *ws, size_t ws_bytes, void *stream) {
+    return rotate_and_sum(P, K, in, L, D, -1, out, ws, ws_bytes, (cudaStream_t)stream);
 }

@@ -386,8 +386,32 @@ __global__ void k_drop_q0(PtrList in, u64 *masked, int k, int N) {
     masked[((long long)t * 2 + b) * N + x] = in.p[t][(long long)b * k * N + x];
 }
 
+// ct (x) ct tensor (C9): d = (a0 b0, a0 b1 + a1 b0, a1 b1)
+__global__ void k_tensor(const u64 *a, const u64 *b, u64 *d, Primes pr, int k, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int l = blockIdx.y;
+    if (x >= N) return;
+    const long long kN = (long long)k * N, lx = (long long)l * N + x;
+    const u64 a0 = a[lx], a1 = a[kN + lx], b0 = b[lx], b1 = b[kN + lx];
+    const ModConst &mc = pr.m[l];
+    Acc128 s;
+    s.zero();
+    s.mac(a0, b1);
+    s.mac(a1, b0);
+    d[lx] = mulmod(a0, b0, mc);
+    d[kN + lx] = s.reduce(mc);
+    d[2 * kN + lx] = mulmod(a1, b1, mc);
+}
+
 inline dim3 grid_x(int N, int y = 1, int z = 1) { return dim3((N + kTB - 1) / kTB, y, z); }
 }  // namespace
+
+blb_status blb_launch_tensor(const blb_params *P, const u64 *a, const u64 *b, u64 *d, int k, cudaStream_t st) {
+    k_tensor<<<grid_x(P->N, k), kTB, 0, st>>>(a, b, d, P->pr, k, P->N);
+    BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
 
 // ============================================================ launchers
 

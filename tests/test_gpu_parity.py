@@ -412,3 +412,22 @@ def test_softmax_v_wo_chain_bit_exact(qktoy):
                                           for o in gfin]), L, 48)
     Att = np.concatenate([S[h] @ V[h] for h in range(H)], axis=1)
     assert float(((Y - Att @ WO) ** 2).mean()) <= 1e-11
+
+
+# ---------------------------------------------------------------- row f2
+def test_f2_ops_bit_exact(qktoy):
+    key = bi.crypto_key(4, 88)
+    L, D = 32, 8
+    steps = [L, 2 * L, 4 * L, -L, -2 * L, -4 * L]
+    okeys = O.keygen(qktoy.o, key, steps, relin=True)
+    gkeys, sk = blb.keygen(qktoy.g, key, steps, relin=True)
+    lvl = 4
+    a = rand_limbs(qktoy, 2, list(range(lvl + 1)), 1)
+    b = rand_limbs(qktoy, 2, list(range(lvl + 1)), 2)
+    oa, ob = O.Ct(a, lvl, 2.0 ** 40), O.Ct(b, lvl, 2.0 ** 40)
+    ga, gb = blb.Ciphertext(dev(a), lvl, 2.0 ** 40), blb.Ciphertext(dev(b), lvl, 2.0 ** 40)
+    r = blb.mul_relin(qktoy.g, gkeys, ga, gb)
+    assert np.array_equal(u64(r.data), O.mul_relin(qktoy.o, oa, ob, okeys).data) and r.scale == 2.0 ** 80
+    for bc in (False, True):
+        r = blb.rotate_sum(qktoy.g, gkeys, ga, L, D, broadcast=bc)
+        assert np.array_equal(u64(r.data), O.rotate_sum(qktoy.o, oa, okeys, L, D, broadcast=bc).data)

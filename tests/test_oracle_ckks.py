@@ -303,3 +303,41 @@ def test_masked_decryption_uniform(toy, toy_keys, offset):
         tmp0 = toy.intt(((m0 + m1 * s0) % q0).astype(np.uint64)[None], [0])[0]
         counts += np.bincount((tmp0.astype(object) * 64 // q0).astype(np.int64), minlength=64)
     assert chisquare(counts).pvalue > 0.01
+
+
+# --------------------------------------------------------------- row f2
+def test_rotate_sum_table3_and_values(toy, toy_keys):
+    """Table 3: fused summation = log2 D rotations, 0 multiplications; the
+    first column block holds the row sums; all-ones L x D -> every slot = D."""
+    import oracle.matmul as mm
+    L, D = 16, 4
+    keys = O.keygen(toy, bi.crypto_key(4, 5), rot_steps=[L, 2 * L, -L, -2 * L])
+    X = np.random.default_rng(9).uniform(-1, 1, (L, D))
+    z = mm.pack_spatial(X, toy.n)[0]
+    ct = enc(toy, keys, z, 20)
+    out = O.rotate_sum(toy, ct, keys, L, D)
+    got = dec(toy, keys, out)
+    assert np.abs(got[:L] - X.sum(axis=1)).max() < 1e-6
+    ones = enc(toy, keys, np.concatenate([np.ones(L * D), np.zeros(toy.n - L * D)]), 21)
+    assert np.abs(dec(toy, keys, O.rotate_sum(toy, ones, keys, L, D))[:L] - D).max() < 1e-6
+    # broadcast of an (L, 1) column: replicated into D column blocks (S:175)
+    col = np.zeros(toy.n)
+    col[:L] = X[:, 0]
+    got = dec(toy, keys, O.rotate_sum(toy, enc(toy, keys, col, 22), keys, L, D, broadcast=True))
+    assert np.abs(got[:L * D] - np.tile(X[:, 0], D)).max() < 1e-6
+
+
+def test_squaring_chain(qk_ctx=None):
+    """ewmul_cc chain: three relinearised squarings + rescales (the depth pattern of
+    negExp's (1 + x/2^6)^{2^6}) decode to x^8."""
+    P = bi.QKTOY
+    q = O.prime_chain(P.log_n, list(P.q_bits) + list(P.p_bits))
+    ctx = O.Ctx(P.log_n, q[:5], q[5:], P.dnum)
+    keys = O.keygen(ctx, bi.crypto_key(4, 6), relin=True)
+    z = np.random.default_rng(10).uniform(0.5, 1.0, ctx.n)
+    ct = O.encrypt(ctx, bi.crypto_key(5, 6), keys.s_ntt, O.encode(ctx, z, 2.0 ** 40, 4), 4, 1, 2.0 ** 40)
+    for _ in range(3):
+        ct = O.rescale(ctx, O.mul_relin(ctx, ct, ct, keys))
+    assert ct.level == 1
+    got = O.decode(ctx, O.decrypt(ctx, keys.s_ntt, ct), ct.scale)
+    assert np.abs(got - z ** 8).max() < 1e-6
