@@ -361,9 +361,9 @@ def main():
     mac_gbs = mac["alg_bytes"] / (mac["ms"] * 1e-3) / 1e9 if mac["ms"] > 0 else None
     traffic = None
     tf = os.path.join(ROOT, "profiles", "mac_traffic.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf):  # DRAM bytes / algorithmic bytes of one ncu --set full capture, scaled per launch
         try:
-            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+            traffic = json.load(open(tf))["ratio"] * mac["alg_bytes"] / max(1, mac["launches"])
         except Exception:
             traffic = None
     line = {
