@@ -239,6 +239,7 @@ extern "C" blb_status blb_params_create(blb_params **out, int log_n, const uint6
     cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
     if (const char *v = getenv("BLB_OVERLAP")) P->overlap = atoi(v);
     if (const char *v = getenv("BLB_MAC_TMA")) P->mac_tma = atoi(v);
+    if (const char *v = getenv("BLB_FUSE")) P->fuse = atoi(v);
     if (cudaStreamCreateWithFlags(&P->aux, cudaStreamNonBlocking) != cudaSuccess) P->aux = nullptr;
     for (auto &e : P->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     P->logN = log_n; P->N = (int)N; P->K = nq; P->np = np; P->dnum = dnum; P->device = cuda_device;

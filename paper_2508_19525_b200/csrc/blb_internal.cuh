@@ -170,6 +170,7 @@ struct blb_params {
     cudaEvent_t ev[64] = {};
     mutable int ev_next = 0;
     int overlap = 1;              // env BLB_OVERLAP=0 disables the two-stream schedule
+    int fuse = 1;                 // fused ModUp / ModDown NTT prologue / epilogue (env BLB_FUSE=0 disables)
     int mac_tma = 1;              // warp-specialised bulk-copy MAC (env BLB_MAC_TMA=0: register double buffer)
     u64 mod[BLB_MAXP];
     u64 psi[BLB_MAXP];
@@ -261,6 +262,29 @@ struct KsJob {
 };
 blb_status launch_keyswitch(const blb_params *P, int level, const KsJob *jobs, int n_jobs, u64 *u_scratch,
                             u64 *conv_scratch, cudaStream_t st);
+struct KsJobs {
+    KsJob j[kMaxJobs];
+};
+struct PinvTab {
+    u64 v[BLB_MAXP], sh[BLB_MAXP];
+};
+// Fused prologue / epilogue of the N = 2^16 NTT (ntt.cu):
+//   pro = 1: the first pass loads row (p, l) from src + (p / src_div) * src_hi + (p % src_div) * src_lo
+//            and reduces it mod the row's modulus (FastBConv of a single-prime digit / P limb);
+//   epi = 1: the last (forward) pass finishes ModDown: out = (u_i - v) * P^{-1} (+ sigma_g(c0) / (c0, c1))
+//            written to jobs.j[p / 2].out (rows p = 2 t + b, limb i), u = [jobs][2][E][N].
+struct NttFuse {
+    int pro = 0, epi = 0;
+    const u64 *src = nullptr;
+    long long src_hi = 0, src_lo = 0;
+    int src_div = 1;
+    const u64 *u = nullptr;
+    int E = 0, k = 0;
+    PinvTab pinv;
+    KsJobs jobs;
+};
+blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool inverse, const NttFuse &fz,
+                            cudaStream_t st);
 size_t keyswitch_scratch_elems(const blb_params *P, int level, int n_jobs);  // u + conv, in u64
 
 blb_status launch_rescale(const blb_params *P, const u64 *in, int level, int n_polys, u64 *out, u64 *scratch,

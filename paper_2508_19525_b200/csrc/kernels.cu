@@ -161,6 +161,15 @@ __global__ void k_gather_rows(PtrList src, u64 *dst, int k, int N) {
     dst[((long long)t * k + i) * N + x] = src.p[t][(long long)i * N + x];
 }
 
+// alpha = 1: ext[t][j][j] = c1_t[j] (a digit's own residue row, already in NTT form)
+__global__ void k_copy_own(PtrList c1_ntt, u64 *ext, int k, int np, int beta, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, t = blockIdx.z;
+    if (x >= N) return;
+    const int E = k + np;
+    ext[(((long long)t * beta + j) * E + j) * N + x] = c1_ntt.p[t][(long long)j * N + x];
+}
+
 // ext[t][j][m][x]: digit j's own limbs copy the NTT-domain input; the others are
 // FastBConv_{D_j -> m}(coef) = sum_i [coef_i * dhat_i^{-1}]_{d_i} * dhat_i  mod m.
 // Table at tab + bconv_modup_off(level, j): inv[nd], inv_sh[nd], chat[nd][E].
@@ -199,9 +208,6 @@ __global__ void k_bconv_modup(PtrList c1_ntt, const u64 *coef, u64 *ext, const u
 }
 
 // ------------------------------------------------------- key switch (C7, C8)
-struct KsJobs {
-    KsJob j[kMaxJobs];
-};
 
 // u[t][b][m][x] = sum_j sigma_g(ext_j)[m][x] * key_j[b][pm][x]
 // Jobs sharing one switching key (same Galois element) form a group of <= 4:
@@ -295,10 +301,6 @@ __global__ void k_bconv_moddown(const u64 *u, u64 *conv, const u64 *tb, Primes p
     }
     conv[((long long)tb2 * k + i) * N + x] = acc.reduce(pr.m[i]);
 }
-
-struct PinvTab {
-    u64 v[BLB_MAXP], sh[BLB_MAXP];
-};
 
 // out = (u_Q - conv) * P^{-1}  (+ sigma_g(c0) on poly 0 for rotations, + (c0, c1) for relin)
 __global__ void k_ks_combine(KsJobs jobs, const u64 *u, const u64 *conv, PinvTab pinv, Primes pr, int k, int np,
@@ -439,6 +441,22 @@ blb_status launch_modup(const blb_params *P, int level, const u64 *const *c1_ntt
     rb.base = coef; rb.poly_stride = (long long)k * N; rb.n_polys = n; rb.limbs = k; rb.limb0 = 0;
     for (int i = 0; i < k; i++) rb.prime[i] = i;
     BLB_TRY(launch_ntt(P, rb, true, st));
+    if (P->logN == 16 && P->alpha == 1 && P->fuse) {
+        // fused: own rows copied, the others converted (x mod q_m) inside the forward NTT's first pass
+        k_copy_own<<<grid_x(N, beta, n), kTB, 0, st>>>(src, ext, k, P->np, beta, N);
+        BLB_COUNT_LAUNCH(1);
+        RowBatch eb{};
+        eb.base = ext; eb.poly_stride = (long long)E * N; eb.n_polys = n * beta; eb.limbs = E; eb.limb0 = 0;
+        for (int m = 0; m < E; m++) eb.prime[m] = m < k ? m : P->K + (m - k);
+        eb.skip_alpha = 1; eb.skip_beta = beta; eb.skip_kmax = k;
+        NttFuse fz{};
+        fz.pro = 1;
+        fz.src = coef;
+        fz.src_div = beta;
+        fz.src_hi = (long long)k * N;
+        fz.src_lo = N;
+        return launch_ntt_fused(P, eb, false, fz, st);
+    }
     Offs offs{};
     for (int j = 0; j < beta; j++) offs.o[j] = (long long)bconv_modup_off(P, level, j);
     k_bconv_modup<<<grid_x(N, E, n * beta), kTB, 0, st>>>(src, coef, ext, P->d_bconv, offs, P->pr, k, P->np, P->K,
@@ -502,6 +520,27 @@ blb_status launch_keyswitch(const blb_params *P, int level, const KsJob *jobs, i
     rb.base = u; rb.poly_stride = (long long)E * N; rb.n_polys = 2 * n; rb.limbs = np; rb.limb0 = k;
     for (int d = 0; d < np; d++) rb.prime[d] = P->K + d;
     BLB_TRY(launch_ntt(P, rb, true, st));
+    if (P->logN == 16 && np == 1 && P->fuse) {
+        // fused ModDown: conv = NTT(u_P mod q_i) with the reduction in the first pass and
+        // (u_i - conv) * P^{-1} (+ sigma(c0) / (c0, c1)) in the last pass
+        RowBatch cb{};
+        cb.base = conv; cb.poly_stride = (long long)k * N; cb.n_polys = 2 * n; cb.limbs = k; cb.limb0 = 0;
+        for (int i = 0; i < k; i++) cb.prime[i] = i;
+        NttFuse fz{};
+        fz.pro = 1;
+        fz.src = u + (long long)k * N;
+        fz.src_div = 1;
+        fz.src_hi = (long long)E * N;
+        fz.epi = 1;
+        fz.u = u;
+        fz.E = E;
+        fz.k = k;
+        for (int i = 0; i < k; i++) { fz.pinv.v[i] = P->Pinv[i]; fz.pinv.sh[i] = P->Pinv_sh[i]; }
+        fz.jobs = J;
+        BLB_TRY(launch_ntt_fused(P, cb, false, fz, st));
+        BLB_COUNT(1, n);
+        return BLB_OK;
+    }
     k_bconv_moddown<<<grid_x(N, k, 2 * n), kTB, 0, st>>>(u, conv, P->d_bconv + bconv_moddown_off(P, level), P->pr, k,
                                                          np, P->K, N);
     BLB_COUNT_LAUNCH(1);

@@ -132,9 +132,9 @@ __device__ __forceinline__ void bfly(u64 &X, u64 &Y, u64 w, u64 wsh, u64 q, u64 
 #ifndef BLB_NTT_MINB
 #define BLB_NTT_MINB 2
 #endif
-template <bool INV, bool STRIDED>
+template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0>
 __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, const u64 *__restrict__ tw_all, Primes pr, int s0,
-                                                  int last) {
+                                                  int last, const NttFuse fz) {
     __shared__ u64 sm[16 * 256];
     constexpr int logN = 16, N = 1 << logN;
     const int row = blockIdx.y;
@@ -158,11 +158,22 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, con
     const int hA = STRIDED ? 0 : (c0 + colA);
     const int hB = STRIDED ? 0 : (c0 + colB);
     u64 v[16];
+    if (PRO == 1) {
+        const u64 *src = fz.src + (long long)(p / fz.src_div) * fz.src_hi + (long long)(p % fz.src_div) * fz.src_lo;
+        const ModConst &mt = pr.m[pi];
 #pragma unroll
-    for (int m = 0; m < 16; m++) {
-        const int mid = tcA + 16 * m;
-        const size_t addr = STRIDED ? (((size_t)mid << 8) + c0 + colA) : (((size_t)(c0 + colA) << 8) + mid);
-        v[m] = a[addr];
+        for (int m = 0; m < 16; m++) {
+            const int mid = tcA + 16 * m;
+            const size_t addr = STRIDED ? (((size_t)mid << 8) + c0 + colA) : (((size_t)(c0 + colA) << 8) + mid);
+            v[m] = mod64(src[addr], mt);
+        }
+    } else {
+#pragma unroll
+        for (int m = 0; m < 16; m++) {
+            const int mid = tcA + 16 * m;
+            const size_t addr = STRIDED ? (((size_t)mid << 8) + c0 + colA) : (((size_t)(c0 + colA) << 8) + mid);
+            v[m] = a[addr];
+        }
     }
     auto roundA = [&](int r) {
         const int dist = 8 >> r;
@@ -211,6 +222,31 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, con
         for (int r = 3; r >= 0; r--) roundA(r);
     }
     const ModConst &mc = pr.m[pi];
+    if (EPI == 1) {  // ModDown combine (forward, contiguous last pass)
+        const int tj = p >> 1, b = p & 1;
+        const KsJob &J = fz.jobs.j[tj];
+        const u64 *ui = fz.u + ((long long)p * fz.E + l) * N;
+        u64 *out = J.out + ((long long)b * fz.k + l) * N;
+        const u64 pv = fz.pinv.v[l], psh = fz.pinv.sh[l];
+#pragma unroll
+        for (int m = 0; m < 16; m++) {
+            u64 x = v[m];
+            if (x >= q2) x -= q2;
+            if (x >= q) x -= q;
+            const int mid = tcA + 16 * m;
+            const uint32_t gx = (uint32_t)((c0 + colA) << 8) + mid;
+            u64 r = shoup(ui[gx] + q - x, pv, psh, q);
+            if (J.add_mode == 1 && b == 0) {
+                const uint32_t src = J.galois == 1 ? gx : galois_perm(gx, J.galois, logN);
+                r = addmod(r, J.c0[(long long)l * N + src], q);
+            } else if (J.add_mode == 2) {
+                const u64 *c = b == 0 ? J.c0 : J.c1_add;
+                r = addmod(r, c[(long long)l * N + gx], q);
+            }
+            out[gx] = r;
+        }
+        return;
+    }
 #pragma unroll
     for (int m = 0; m < 16; m++) {
         u64 x = v[m];
@@ -262,12 +298,13 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
     }
     if (logN == 16) {
         dim3 g(16, rows);
+        const NttFuse fz{};
         if (!inverse) {
-            ntt16_pass<false, true><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 0, 0);
-            ntt16_pass<false, false><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 8, 1);
+            ntt16_pass<false, true><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 0, 0, fz);
+            ntt16_pass<false, false><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 8, 1, fz);
         } else {
-            ntt16_pass<true, false><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 8, 0);
-            ntt16_pass<true, true><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 0, 1);
+            ntt16_pass<true, false><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 8, 0, fz);
+            ntt16_pass<true, true><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 0, 1, fz);
         }
         BLB_COUNT_LAUNCH(2);
         blb_timing_end(1, t0, st, alg);
@@ -292,6 +329,28 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
     }
     BLB_COUNT_LAUNCH(2);
     blb_timing_end(1, t0, st, alg);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+
+// Forward N = 2^16 NTT with a fused prologue (pro = 1) and / or ModDown epilogue (epi = 1).
+blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool inverse, const NttFuse &fz,
+                            cudaStream_t st) {
+    const int rows = rb.n_polys * rb.limbs;
+    if (rows == 0) return BLB_OK;
+    if (P->logN != 16 || inverse || rows > 65535) {
+        blb_set_error("launch_ntt_fused: N = 2^16 forward batches only");
+        return BLB_E_INVALID_ARG;
+    }
+    BLB_COUNT(2, rows);
+    cudaEvent_t t0 = blb_timing_begin(st);
+    dim3 g(16, rows);
+    if (fz.pro == 1) ntt16_pass<false, true, 1, 0><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 0, 0, fz);
+    else ntt16_pass<false, true, 0, 0><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 0, 0, fz);
+    if (fz.epi == 1) ntt16_pass<false, false, 0, 1><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 8, 1, fz);
+    else ntt16_pass<false, false, 0, 0><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 8, 1, fz);
+    BLB_COUNT_LAUNCH(2);
+    blb_timing_end(1, t0, st, (double)rows * 16.0 * (1 << 16));
     BLB_CHECK_LAUNCH();
     return BLB_OK;
 }

@@ -431,3 +431,21 @@ def test_f2_ops_bit_exact(qktoy):
     for bc in (False, True):
         r = blb.rotate_sum(qktoy.g, gkeys, ga, L, D, broadcast=bc)
         assert np.array_equal(u64(r.data), O.rotate_sum(qktoy.o, oa, okeys, L, D, broadcast=bc).data)
+
+
+def test_bert_size_keyswitch_bit_exact(bert):
+    """N = 2^16 (the fused ModUp / ModDown NTT path): rotation at every level, relinearised
+    product, rotate-and-sum, rescale -- bit-exact against the oracle."""
+    key = bi.crypto_key(4, 99)
+    steps = [128, -256, 5]
+    okeys = O.keygen(bert.o, key, steps, relin=True)
+    gkeys, sk = blb.keygen(bert.g, key, steps, relin=True)
+    for lvl in (4, 2, 0):
+        data = rand_limbs(bert, 2, list(range(lvl + 1)), 40 + lvl)
+        oc, gc = O.Ct(data, lvl, 2.0 ** 40), blb.Ciphertext(dev(data), lvl, 2.0 ** 40)
+        for s in steps:
+            assert np.array_equal(u64(blb.rotate(bert.g, gkeys, gc, s).data), O.rotate(bert.o, oc, okeys, s).data), (lvl, s)
+        assert np.array_equal(u64(blb.mul_relin(bert.g, gkeys, gc, gc).data), O.mul_relin(bert.o, oc, oc, okeys).data)
+    data = rand_limbs(bert, 2, list(range(5)), 7)
+    oc, gc = O.Ct(data, 4, 1.0), blb.Ciphertext(dev(data), 4, 1.0)
+    assert np.array_equal(u64(blb.rotate_sum(bert.g, gkeys, gc, 128, 2).data), O.rotate_sum(bert.o, oc, okeys, 128, 2).data)
