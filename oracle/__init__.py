@@ -111,6 +111,13 @@ def lib():
         L.orc_rescale.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
         L.orc_mask.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_char_p, ctypes.c_uint64,
                                ctypes.c_void_p, ctypes.c_void_p]
+        L.orc_rotate_ext.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                     ctypes.c_uint64, ctypes.c_void_p]
+        for name in ("orc_mul_pt_idx", "orc_add_idx"):
+            getattr(L, name).argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+        L.orc_encode_ext.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_int,
+                                     ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -493,3 +500,56 @@ def rotate_sum(ctx: Ctx, ct: Ct, keys: Keys, L: int, D: int, broadcast: bool = F
         cur = add(ctx, cur, rotate(ctx, cur, keys, -step if broadcast else step))
         step *= 2
     return cur
+
+
+# ---------------------------------------------------------------------------
+# extended basis Q_l u P (double hoisting, reading C13)
+# ---------------------------------------------------------------------------
+@dataclass
+class CtExt:
+    data: np.ndarray  # [2][level+1+np][N], NTT, over q_0..q_level, p_0..
+    level: int
+    scale: float
+
+
+def ext_pidx(ctx: Ctx, level: int) -> list[int]:
+    return list(range(level + 1)) + [ctx.K + t for t in range(ctx.np_)]
+
+
+def rotate_ext(ctx: Ctx, ct: Ct, keys: Keys, step: int) -> CtExt:
+    """Rotation kept in Q_l u P (no ModDown): (P sigma(c0) + u0, u1); step 0 lifts (P c0, P c1)."""
+    g = ctx.galois(step)
+    E = ct.level + 1 + ctx.np_
+    out = np.empty((2, E, ctx.N), dtype=np.uint64)
+    rk = keys.rot[g] if g != 1 else np.zeros(1, dtype=np.uint64)
+    lib().orc_rotate_ext(ctx._h, _p(_u64(ct.data)), ct.level, _p(rk), g, _p(out))
+    return CtExt(out, ct.level, ct.scale)
+
+
+def encode_ext(ctx: Ctx, z, scale: float, level: int) -> np.ndarray:
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    out = np.empty((level + 1 + ctx.np_, ctx.N), dtype=np.uint64)
+    if lib().orc_encode_ext(ctx._h, _p(z), float(scale), level, _p(out)) != 0:
+        raise EncodeOverflow("encode magnitude >= 2^62")
+    return out
+
+
+def mul_pt_ext(ctx: Ctx, a: CtExt, pt: np.ndarray, pt_scale: float) -> CtExt:
+    idx = ext_pidx(ctx, a.level)
+    pa = (ctypes.c_int * len(idx))(*idx)
+    out = np.empty_like(a.data)
+    lib().orc_mul_pt_idx(ctx._h, _p(_u64(a.data)), _p(_u64(pt)), pa, len(idx), 2, _p(out))
+    return CtExt(out, a.level, a.scale * pt_scale)
+
+
+def add_ext(ctx: Ctx, a: CtExt, b: CtExt) -> CtExt:
+    idx = ext_pidx(ctx, a.level)
+    pa = (ctypes.c_int * len(idx))(*idx)
+    out = np.empty_like(a.data)
+    lib().orc_add_idx(ctx._h, _p(_u64(a.data)), _p(_u64(b.data)), pa, len(idx), 2, _p(out))
+    return CtExt(out, a.level, a.scale)
+
+
+def moddown_ct(ctx: Ctx, a: CtExt) -> Ct:
+    """ModDown of both polynomials (C7): back to Q_l, divided by P."""
+    return Ct(np.stack([moddown(ctx, a.data[0], a.level), moddown(ctx, a.data[1], a.level)]), a.level, a.scale)

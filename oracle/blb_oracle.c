@@ -742,3 +742,66 @@ int orc_encode(const orc_ctx *c, const double *z, double scale, int lvl, u64 *ou
     free(coef);
     return st;
 }
+
+/* ------------------------------------------------------------------ */
+/* extended-basis (Q_l u P) helpers for double-hoisted rotations        */
+/* ------------------------------------------------------------------ */
+/* Rotation kept in the extended basis (no ModDown): out [2][k+np][N] =
+ * (P*sigma_g(c0) + u0, u1) with u = sum_j sigma_g(ModUp(D_j(c1))) * rk_{g,j} (C8);
+ * P*sigma_g(c0) is 0 on the P limbs.  g = 1: the lifted input (P*c0, P*c1). */
+void orc_rotate_ext(const orc_ctx *c, const u64 *ct, int lvl, const u64 *rk, u64 g, u64 *out) {
+    int k = lvl + 1, E = k + c->np, beta = (k + c->alpha - 1) / c->alpha;
+    u64 N = c->N;
+    if (g == 1) {  /* lift: (P c0, P c1) */
+        for (int p = 0; p < 2; p++)
+            for (int m = 0; m < E; m++) {
+                u64 *o = out + ((u64)p * E + m) * N;
+                if (m >= k) { memset(o, 0, N * sizeof(u64)); continue; }
+                u64 q = c->mod[m], Pm = 1;
+                for (int t = 0; t < c->np; t++) Pm = mulmod(Pm, c->mod[c->K + t] % q, q);
+                for (u64 x = 0; x < N; x++) o[x] = mulmod(ct[((u64)p * k + m) * N + x], Pm, q);
+            }
+        return;
+    }
+    u64 *ext = (u64 *)malloc((u64)beta * E * N * sizeof(u64));
+    orc_modup(c, ct + (u64)k * N, lvl, ext);
+    orc_ks_inner(c, ext, lvl, rk, g, out);
+    u64 *sc0 = (u64 *)malloc((u64)k * N * sizeof(u64));
+    orc_automorphism_ntt(c, ct, sc0, g, k);
+    for (int m = 0; m < k; m++) {
+        u64 q = c->mod[m], Pm = 1;
+        for (int t = 0; t < c->np; t++) Pm = mulmod(Pm, c->mod[c->K + t] % q, q);
+        for (u64 x = 0; x < N; x++) out[(u64)m * N + x] = addmod(out[(u64)m * N + x], mulmod(sc0[(u64)m * N + x], Pm, q), q);
+    }
+    free(ext); free(sc0);
+}
+
+/* pointwise ops over an explicit prime list: a, out [n_polys][n_limbs][N]; pt [n_limbs][N] */
+void orc_mul_pt_idx(const orc_ctx *c, const u64 *a, const u64 *pt, const int *pidx, int n_limbs, int n_polys, u64 *out) {
+    u64 N = c->N;
+    for (int p = 0; p < n_polys; p++)
+        for (int l = 0; l < n_limbs; l++) {
+            u64 q = c->mod[pidx[l]];
+            for (u64 x = 0; x < N; x++)
+                out[((u64)p * n_limbs + l) * N + x] = mulmod(a[((u64)p * n_limbs + l) * N + x], pt[(u64)l * N + x], q);
+        }
+}
+void orc_add_idx(const orc_ctx *c, const u64 *a, const u64 *b, const int *pidx, int n_limbs, int n_polys, u64 *out) {
+    u64 N = c->N;
+    for (int p = 0; p < n_polys; p++)
+        for (int l = 0; l < n_limbs; l++) {
+            u64 q = c->mod[pidx[l]];
+            for (u64 x = 0; x < N; x++)
+                out[((u64)p * n_limbs + l) * N + x] = addmod(a[((u64)p * n_limbs + l) * N + x], b[((u64)p * n_limbs + l) * N + x], q);
+        }
+}
+/* encode at level lvl over the extended basis Q_lvl u P: out [lvl+1+np][N] */
+int orc_encode_ext(const orc_ctx *c, const double *z, double scale, int lvl, u64 *out) {
+    u64 N = c->N;
+    int k = lvl + 1, E = k + c->np;
+    i64 *coef = (i64 *)malloc(N * sizeof(i64));
+    int st = orc_encode_coeffs(c, z, scale, coef);
+    for (int m = 0; m < E; m++) small_to_ntt(c, coef, m < k ? m : c->K + (m - k), out + (u64)m * N);
+    free(coef);
+    return st;
+}

@@ -13,9 +13,10 @@ J = d_h / g ciphertexts each for Q and K (both spatial-first, so K is K^T in
 reduce-first packing).  With t = u*B + i (u < G, i < B, B*G = L, g | B):
 
   baby (steps 1+2, K side): K'_i = inner rotation of block (c, h) by c + i:
-       sum_c Mnw_{c,i} (.) Rot_s(K) + Mw_{c,i} (.) Rot_{s-L}(K), s = (c+i) mod L
+       ModDown( sum_c Mnw_{c,i} (.) Rot_s(K) + Mw_{c,i} (.) Rot_{s-L}(K) ), s = (c+i) mod L,
+       the rotations double-hoisted (one ModUp, kept in Q_l u P, one ModDown per K'_i)
   giant (Q side):           Q_u  = inner rotation by -uB:
-       Mq1_u (.) Rot_{-uB}(Q) + Mq2_u (.) Rot_{L-uB}(Q)
+       ModDown( Mq1_u (.) Rot_{-uB}(Q) + Mq2_u (.) Rot_{L-uB}(Q) ) (same double hoisting)
   products:                 S_{u,i} = relin( sum_j Q_u^(j) (x) K'_i^(j) )
        -> block (c,h), row p: partial_{k == c mod g} C_h[p - uB, p + uB + i + c - uB]
   step 3:                   T_{u,i} = Rot_{-i H_p L}(S_{u,i})   (right by i block-groups)
@@ -35,6 +36,8 @@ import math
 from dataclasses import dataclass, field
 
 import numpy as np
+
+import oracle as O
 
 from . import Ct, Ctx, Keys, add, encode, mul_pt, relinearize, rescale, rotate, tensor
 
@@ -222,37 +225,39 @@ def qk_encrypted(ctx: Ctx, keys: Keys, Q: list[Ct], K: list[Ct], plan: QKPlan) -
     def drop(ct: Ct) -> Ct:   # exact level drop (C9): keep limbs 0..level-1
         return Ct(ct.data[:, : ct.level].copy(), ct.level - 1, ct.scale)
 
-    # masks at level lvl (scale q_lvl), rescale -> lvl-1
+    # Stage 1 is double-hoisted (reading C13): every rotation of K^(j) / Q^(j) shares one
+    # ModUp and stays in the extended basis Q_l u P (no ModDown); the masks (encoded over
+    # Q_l u P at scale q_l) are applied there and each masked sum gets ONE ModDown, then
+    # one rescale -> level l-1.
     s1 = float(ctx.q[lvl])
     enc1 = {}
 
     def pt1(key, vec):
         if key not in enc1:
-            enc1[key] = encode(ctx, vec, s1, lvl)
+            enc1[key] = O.encode_ext(ctx, vec, s1, lvl)
         return enc1[key]
 
     Kp = {}
     for j in range(plan.J):
-        rots = {0: K[j]}
-        for r in plan.k_rots:
-            rots[r] = rotate(ctx, K[j], keys, r)
+        rots = {r: O.rotate_ext(ctx, K[j], keys, r) for r in [0] + list(plan.k_rots)}
         for i in range(plan.B):
             acc = None
             for c in range(plan.g):
                 s = (c + i) % plan.L
                 parts = [(False, s)] + ([(True, s - plan.L)] if s else [])
                 for wrap, r in parts:
-                    term = mul_pt(ctx, rots[r], pt1(("k", c, i, wrap), plan.mask_k(c, i, wrap)), s1)
-                    acc = term if acc is None else add(ctx, acc, term)
-            Kp[(i, j)] = rescale(ctx, acc)
+                    term = O.mul_pt_ext(ctx, rots[r], pt1(("k", c, i, wrap), plan.mask_k(c, i, wrap)), s1)
+                    acc = term if acc is None else O.add_ext(ctx, acc, term)
+            Kp[(i, j)] = rescale(ctx, O.moddown_ct(ctx, acc))
     Qu = {}
     for j in range(plan.J):
         Qu[(0, j)] = drop(Q[j])
         for u in range(1, plan.G):
             a = u * plan.B
-            t1 = mul_pt(ctx, rotate(ctx, Q[j], keys, -a), pt1(("q", u, False), plan.mask_q(u, False)), s1)
-            t2 = mul_pt(ctx, rotate(ctx, Q[j], keys, plan.L - a), pt1(("q", u, True), plan.mask_q(u, True)), s1)
-            Qu[(u, j)] = rescale(ctx, add(ctx, t1, t2))
+            t1 = O.mul_pt_ext(ctx, O.rotate_ext(ctx, Q[j], keys, -a), pt1(("q", u, False), plan.mask_q(u, False)), s1)
+            t2 = O.mul_pt_ext(ctx, O.rotate_ext(ctx, Q[j], keys, plan.L - a),
+                              pt1(("q", u, True), plan.mask_q(u, True)), s1)
+            Qu[(u, j)] = rescale(ctx, O.moddown_ct(ctx, O.add_ext(ctx, t1, t2)))
     # products, relinearisation (once per (u, i), lazy over j: reading S10), rescale -> lvl-2
     T = {}
     for u in range(plan.G):

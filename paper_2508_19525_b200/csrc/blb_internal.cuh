@@ -86,6 +86,11 @@ struct Acc128 {
         lo = nl;
     }
     __device__ __forceinline__ u64 reduce(const ModConst &c) const { return reduce128(hi, lo, c); }
+    // keep the sum exact beyond 2^127 / q^2 products: replace it by its residue
+    __device__ __forceinline__ void fold(const ModConst &c) {
+        lo = reduce(c);
+        hi = 0;
+    }
 };
 
 // Accumulator for products of residues < 2^41 (the 40-bit chain primes), with
@@ -115,6 +120,7 @@ struct Acc41 {
         const u64 H = (u64)l2 + hi + m_hi + (s < lo ? 1 : 0);
         return reduce128(H, s, c);
     }
+    __device__ __forceinline__ void fold(const ModConst &) {}  // exact for < 2^14 products
 };
 
 // ---------------------------------------------------------------------------
@@ -175,7 +181,7 @@ struct blb_params {
     u64 mod[BLB_MAXP];
     u64 psi[BLB_MAXP];
     Primes pr;                    // by-value copy for kernel args
-    u64 *d_tw = nullptr;          // [K+np][4][N]: fwd, fwd_sh, inv, inv_sh (bit-reversed order)
+    u64 *d_tw = nullptr;          // [K+np][2][N][2]: (fwd, fwd Shoup), (inv, inv Shoup) pairs, bit-reversed order
     double *d_zeta = nullptr;     // [N][4]: zeta^{brv(i)} as (re_hi, re_lo, im_hi, im_lo)
     int32_t *d_slot_pos = nullptr; // [N/2]: NTT-domain position k of slot j (brv(k) = (5^j - 1)/2)
     // FastBConv tables, see bconv_* in kernels.cu
@@ -283,20 +289,28 @@ struct NttFuse {
     PinvTab pinv;
     KsJobs jobs;
 };
+// double hoisting: rotations kept in Q_l u P written to jobs[t].out ([2][E][N]);
+// ModDown of n contiguous extended ciphertexts u [n][2][E][N] -> out [n][2][k][N]
+blb_status launch_keyswitch_ext(const blb_params *P, int level, const KsJob *jobs, int n, cudaStream_t st);
+blb_status launch_moddown(const blb_params *P, int level, u64 *u, int n, u64 *out, u64 *conv, cudaStream_t st);
+blb_status launch_lift_ext(const blb_params *P, int level, const u64 *in, u64 *out, cudaStream_t st);
 blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool inverse, const NttFuse &fz,
                             cudaStream_t st);
 size_t keyswitch_scratch_elems(const blb_params *P, int level, int n_jobs);  // u + conv, in u64
 
 blb_status launch_rescale(const blb_params *P, const u64 *in, int level, int n_polys, u64 *out, u64 *scratch,
                           cudaStream_t st);
+// np_ext > 0: also write residues mod p_0..p_{np_ext-1} after the q limbs (extended-basis plaintexts)
 blb_status launch_encode(const blb_params *P, const double *slots, int n_pts, double scale, int level, u64 *out,
-                         double *dd_scratch, int *d_flag, cudaStream_t st);
+                         double *dd_scratch, int *d_flag, cudaStream_t st, int np_ext = 0);
 size_t encode_scratch_doubles(const blb_params *P, int n_pts);
 
 // MAC: acc[o] = sum_{e in [ent_start[o0+o], ent_start[o0+o+1])} pt[ent_pt[e] or e - e_base] (.) R[ent_r[e]]
 // (pt entries [k][N], R entries [2][k][N], acc [n_o][2][k][N]; 128-bit lazy accumulation)
+// kq >= 0: the first kq limbs are q_0..q_{kq-1} and limbs kq.. are p_0.. (extended basis)
 blb_status launch_mac(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc, const int *ent_r, const int *ent_pt,
-                      const int *ent_start, int o0, int e_base, int n_o, int n_entries, int k, cudaStream_t st);
+                      const int *ent_start, int o0, int e_base, int n_o, int n_entries, int k, cudaStream_t st,
+                      int kq = -1);
 
 // ChaCha / sampling
 enum { TAG_SECRET = 1, TAG_KEY_A = 2, TAG_KEY_E = 3, TAG_ENC_A = 4, TAG_ENC_E = 5, TAG_MASK = 6 };

@@ -101,7 +101,7 @@ __global__ void k_stage(double *buf, const double *zeta, int m, int logN, int in
 
 // coefficient k = round_half_even(Re(buf[k]) * scale / N), residues mod q_0..q_level
 __global__ void k_encode_finalize(const double *buf, u64 *out, Primes pr, double scale, int level, int logN,
-                                  int *flag) {
+                                  int *flag, int np_ext, int Kfull) {
     const int N = 1 << logN;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int p = blockIdx.y;
@@ -120,9 +120,9 @@ __global__ void k_encode_finalize(const double *buf, u64 *out, Primes pr, double
     if (d > 0.5 || (d == 0.5 && odd)) r += 1.0;
     else if (d < -0.5 || (d == -0.5 && odd)) r -= 1.0;
     const long long c = (long long)r;
-    const int k1 = level + 1;
+    const int k1 = level + 1 + np_ext;
     for (int i = 0; i < k1; i++) {
-        const ModConst &mc = pr.m[i];
+        const ModConst &mc = pr.m[i <= level ? i : Kfull + (i - level - 1)];
         u64 res;
         if (c >= 0) res = mod64((u64)c, mc);
         else {
@@ -161,18 +161,20 @@ __global__ void k_copy(const u64 *src, u64 *dst, int n) {
 size_t encode_scratch_doubles(const blb_params *P, int n_pts) { return (size_t)n_pts * P->N * 4; }
 
 blb_status launch_encode(const blb_params *P, const double *slots, int n_pts, double scale, int level, u64 *out,
-                         double *buf, int *d_flag, cudaStream_t st) {
+                         double *buf, int *d_flag, cudaStream_t st, int np_ext) {
     const int N = P->N, logN = P->logN;
     if (n_pts <= 0) return BLB_OK;
     dim3 gs((N / 2 + kTB - 1) / kTB, n_pts);
     k_scatter<<<gs, kTB, 0, st>>>(slots, P->d_slot_pos, buf, n_pts, N);
     for (int m = N / 2; m >= 1; m >>= 1) k_stage<<<gs, kTB, 0, st>>>(buf, P->d_zeta, m, logN, 1);
-    k_encode_finalize<<<dim3((N + kTB - 1) / kTB, n_pts), kTB, 0, st>>>(buf, out, P->pr, scale, level, logN, d_flag);
+    k_encode_finalize<<<dim3((N + kTB - 1) / kTB, n_pts), kTB, 0, st>>>(buf, out, P->pr, scale, level, logN, d_flag,
+                                                                        np_ext, P->K);
     BLB_COUNT_LAUNCH(2 + logN);
     BLB_CHECK_LAUNCH();
     RowBatch rb{};
-    rb.base = out; rb.poly_stride = (long long)(level + 1) * N; rb.n_polys = n_pts; rb.limbs = level + 1; rb.limb0 = 0;
-    for (int i = 0; i <= level; i++) rb.prime[i] = i;
+    rb.base = out; rb.poly_stride = (long long)(level + 1 + np_ext) * N; rb.n_polys = n_pts; rb.limbs = level + 1 + np_ext;
+    rb.limb0 = 0;
+    for (int i = 0; i < rb.limbs; i++) rb.prime[i] = i <= level ? i : P->K + (i - level - 1);
     return launch_ntt(P, rb, false, st);
 }
 

@@ -95,7 +95,7 @@ extern "C" u64 blbh_mulmod(u64 a, u64 b, u64 q) { return mm(a, b, q); }
 extern "C" u64 blbh_powmod(u64 a, u64 e, u64 q) { return pw(a, e, q); }
 extern "C" u64 blbh_invmod(u64 a, u64 q) { return pw(a, q - 2, q); }
 
-// out: [4][N] = psi^{brv(i)}, Shoup, psi^{-brv(i)}, Shoup
+// out: [2][N][2] = (psi^{brv(i)}, Shoup) pairs, then (psi^{-brv(i)}, Shoup) pairs
 extern "C" void blbh_twiddles(u64 q, u64 psi, int logN, u64 *out) {
     const u64 N = 1ull << logN;
     const u64 ipsi = pw(psi, q - 2, q);
@@ -103,10 +103,10 @@ extern "C" void blbh_twiddles(u64 q, u64 psi, int logN, u64 *out) {
     u64 f = 1, b = 1;
     for (u64 e = 0; e < N; ++e) {
         const u64 i = bitrev(e, logN);
-        out[i] = f;
-        out[N + i] = blbh_shoup(f, q);
-        out[2 * N + i] = b;
-        out[3 * N + i] = blbh_shoup(b, q);
+        out[2 * i] = f;
+        out[2 * i + 1] = blbh_shoup(f, q);
+        out[2 * N + 2 * i] = b;
+        out[2 * N + 2 * i + 1] = blbh_shoup(b, q);
         f = mm(f, psi, q);
         b = mm(b, ipsi, q);
     }

@@ -220,9 +220,11 @@ struct KsGroups {
 };
 // BETA > 0: digit count known at compile time (all loads of a thread are issued
 // before the first multiply); BETA = 0: runtime beta.
-template <int BETA>
+// EXT: write the extended-basis result (P sigma_g(c0) + u0, u1) over Q_l u P straight to
+// jobs.j[t].out ([2][E][N]) -- the double-hoisted rotation (no ModDown).
+template <int BETA, bool EXT = false>
 __global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, int np, int K, int beta_rt,
-                           int logN) {
+                           int logN, PinvTab pq) {
     const int N = 1 << logN;
     const int beta = BETA > 0 ? BETA : beta_rt;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -276,8 +278,16 @@ __global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, 
     for (int q = 0; q < kKsGroup; q++) {
         if (q < cnt) {
             const int t = t0 + q;
-            u[(((long long)t * 2 + 0) * E + m) * N + x] = a0[q].reduce(mc);
-            u[(((long long)t * 2 + 1) * E + m) * N + x] = a1[q].reduce(mc);
+            if (EXT) {
+                const KsJob &J = jobs.j[t];
+                u64 r0 = a0[q].reduce(mc);
+                if (m < k) r0 = addmod(r0, shoup(J.c0[(long long)m * N + src], pq.v[m], pq.sh[m], mc.q), mc.q);
+                J.out[(long long)m * N + x] = r0;
+                J.out[((long long)E + m) * N + x] = a1[q].reduce(mc);
+            } else {
+                u[(((long long)t * 2 + 0) * E + m) * N + x] = a0[q].reduce(mc);
+                u[(((long long)t * 2 + 1) * E + m) * N + x] = a1[q].reduce(mc);
+            }
         }
     }
 }
@@ -416,6 +426,8 @@ blb_status blb_launch_tensor(const blb_params *P, const u64 *a, const u64 *b, u6
 }
 
 // ============================================================ launchers
+extern "C" u64 blbh_shoup(u64 w, u64 q);
+static u64 blbh_shoup_dev_table(const blb_params *P, int i) { return blbh_shoup(P->P_mod_q[i], P->mod[i]); }
 
 ChachaKey chacha_key_from_bytes(const uint8_t seed[32]) {
     ChachaKey k;
@@ -475,47 +487,55 @@ size_t keyswitch_scratch_elems(const blb_params *P, int level, int n_jobs) {
     return (size_t)n_jobs * 2 * ((size_t)E + k) * P->N;
 }
 
-blb_status launch_keyswitch(const blb_params *P, int level, const KsJob *jobs, int n, u64 *u, u64 *conv,
-                            cudaStream_t st) {
-    if (n <= 0) return BLB_OK;
-    if (n > kMaxJobs) {
-        blb_set_error("launch_keyswitch: n > %d", kMaxJobs);
-        return BLB_E_INVALID_ARG;
+// group jobs that share a key (stable order by key), <= kKsGroup per group
+static void group_jobs(const KsJob *jobs, int n, KsJobs &J, KsGroups &G) {
+    bool used[kMaxJobs] = {false};
+    int t = 0;
+    G.n = 0;
+    for (int a = 0; a < n; a++) {
+        if (used[a]) continue;
+        G.start[G.n++] = t;
+        int cnt = 0;
+        for (int b = a; b < n && cnt < kKsGroup; b++)
+            if (!used[b] && jobs[b].key == jobs[a].key && jobs[b].galois == jobs[a].galois) {
+                used[b] = true;
+                J.j[t++] = jobs[b];
+                cnt++;
+            }
     }
+    G.start[G.n] = t;
+}
+
+template <bool EXT>
+static blb_status ks_inner_launch(const blb_params *P, int level, const KsJobs &J, const KsGroups &G, u64 *u,
+                                  cudaStream_t st) {
     const int N = P->N, k = level + 1, np = P->np, E = k + np, beta = blb_beta(P, level);
-    // group jobs that share a key (stable order by key), <= kKsGroup per group
-    KsJobs J{};
-    KsGroups G{};
-    {
-        bool used[kMaxJobs] = {false};
-        int t = 0;
-        for (int a = 0; a < n; a++) {
-            if (used[a]) continue;
-            G.start[G.n++] = t;
-            int cnt = 0;
-            for (int b = a; b < n && cnt < kKsGroup; b++)
-                if (!used[b] && jobs[b].key == jobs[a].key && jobs[b].galois == jobs[a].galois) {
-                    used[b] = true;
-                    J.j[t++] = jobs[b];
-                    cnt++;
-                }
-        }
-        G.start[G.n] = t;
+    PinvTab pq{};
+    for (int i = 0; i < k; i++) {
+        pq.v[i] = P->P_mod_q[i];
+        pq.sh[i] = blbh_shoup_dev_table(P, i);
     }
     cudaEvent_t t0 = blb_timing_begin(st);
     const dim3 gks = grid_x(N, E, G.n);
     switch (beta) {
-        case 1: k_ks_inner<1><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN); break;
-        case 2: k_ks_inner<2><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN); break;
-        case 3: k_ks_inner<3><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN); break;
-        case 4: k_ks_inner<4><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN); break;
-        case 5: k_ks_inner<5><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN); break;
-        case 6: k_ks_inner<6><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN); break;
-        default: k_ks_inner<0><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN); break;
+        case 1: k_ks_inner<1, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
+        case 2: k_ks_inner<2, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
+        case 3: k_ks_inner<3, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
+        case 4: k_ks_inner<4, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
+        case 5: k_ks_inner<5, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
+        case 6: k_ks_inner<6, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
+        default: k_ks_inner<0, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
     }
     BLB_COUNT_LAUNCH(1);
     blb_timing_end(2, t0, st, (double)G.n * 2.0 * beta * E * N * 8.0);
     BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+
+// ModDown of u[t] ([2][E][N], extended basis) into J.j[t].out with the job's add mode
+static blb_status moddown_launch(const blb_params *P, int level, const KsJobs &J, int n, u64 *u, u64 *conv,
+                                 cudaStream_t st) {
+    const int N = P->N, k = level + 1, np = P->np, E = k + np;
     RowBatch rb{};
     rb.base = u; rb.poly_stride = (long long)E * N; rb.n_polys = 2 * n; rb.limbs = np; rb.limb0 = k;
     for (int d = 0; d < np; d++) rb.prime[d] = P->K + d;
@@ -537,9 +557,7 @@ blb_status launch_keyswitch(const blb_params *P, int level, const KsJob *jobs, i
         fz.k = k;
         for (int i = 0; i < k; i++) { fz.pinv.v[i] = P->Pinv[i]; fz.pinv.sh[i] = P->Pinv_sh[i]; }
         fz.jobs = J;
-        BLB_TRY(launch_ntt_fused(P, cb, false, fz, st));
-        BLB_COUNT(1, n);
-        return BLB_OK;
+        return launch_ntt_fused(P, cb, false, fz, st);
     }
     k_bconv_moddown<<<grid_x(N, k, 2 * n), kTB, 0, st>>>(u, conv, P->d_bconv + bconv_moddown_off(P, level), P->pr, k,
                                                          np, P->K, N);
@@ -553,7 +571,68 @@ blb_status launch_keyswitch(const blb_params *P, int level, const KsJob *jobs, i
     for (int i = 0; i < k; i++) { pt.v[i] = P->Pinv[i]; pt.sh[i] = P->Pinv_sh[i]; }
     k_ks_combine<<<grid_x(N, k, 2 * n), kTB, 0, st>>>(J, u, conv, pt, P->pr, k, np, P->logN);
     BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+
+blb_status launch_keyswitch(const blb_params *P, int level, const KsJob *jobs, int n, u64 *u, u64 *conv,
+                            cudaStream_t st) {
+    if (n <= 0) return BLB_OK;
+    if (n > kMaxJobs) {
+        blb_set_error("launch_keyswitch: n > %d", kMaxJobs);
+        return BLB_E_INVALID_ARG;
+    }
+    KsJobs J{};
+    KsGroups G{};
+    group_jobs(jobs, n, J, G);
+    BLB_TRY(ks_inner_launch<false>(P, level, J, G, u, st));
+    BLB_TRY(moddown_launch(P, level, J, n, u, conv, st));
     BLB_COUNT(1, n);
+    return BLB_OK;
+}
+
+blb_status launch_keyswitch_ext(const blb_params *P, int level, const KsJob *jobs, int n, cudaStream_t st) {
+    if (n <= 0) return BLB_OK;
+    if (n > kMaxJobs) return BLB_E_INVALID_ARG;
+    KsJobs J{};
+    KsGroups G{};
+    group_jobs(jobs, n, J, G);
+    BLB_TRY(ks_inner_launch<true>(P, level, J, G, nullptr, st));
+    BLB_COUNT(1, n);
+    return BLB_OK;
+}
+
+blb_status launch_moddown(const blb_params *P, int level, u64 *u, int n, u64 *out, u64 *conv, cudaStream_t st) {
+    const int N = P->N, k = level + 1, E = k + P->np;
+    for (int t0 = 0; t0 < n; t0 += kMaxJobs) {
+        const int cnt = n - t0 < kMaxJobs ? n - t0 : kMaxJobs;
+        KsJobs J{};
+        for (int t = 0; t < cnt; t++) {
+            J.j[t].out = out + (size_t)(t0 + t) * 2 * k * N;
+            J.j[t].add_mode = 0;
+            J.j[t].galois = 1;
+        }
+        BLB_TRY(moddown_launch(P, level, J, cnt, u + (size_t)t0 * 2 * E * N, conv, st));
+    }
+    return BLB_OK;
+}
+
+// lift a Q_l ciphertext to Q_l u P: (P c0, P c1) on the q limbs, 0 on the p limbs
+__global__ void k_lift_ext(const u64 *in, u64 *out, PinvTab pq, Primes pr, int k, int np, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int m = blockIdx.y, p = blockIdx.z;
+    if (x >= N) return;
+    const int E = k + np;
+    u64 v = 0;
+    if (m < k) v = shoup(in[((long long)p * k + m) * N + x], pq.v[m], pq.sh[m], pr.m[m].q);
+    out[((long long)p * E + m) * N + x] = v;
+}
+blb_status launch_lift_ext(const blb_params *P, int level, const u64 *in, u64 *out, cudaStream_t st) {
+    const int k = level + 1;
+    PinvTab pq{};
+    for (int i = 0; i < k; i++) { pq.v[i] = P->P_mod_q[i]; pq.sh[i] = blbh_shoup_dev_table(P, i); }
+    k_lift_ext<<<grid_x(P->N, k + P->np, 2), kTB, 0, st>>>(in, out, pq, P->pr, k, P->np, P->N);
+    BLB_COUNT_LAUNCH(1);
     BLB_CHECK_LAUNCH();
     return BLB_OK;
 }

@@ -85,7 +85,8 @@ __global__ void k_build_slots(PlanDev pd, const int *ent_bi, const int *ent_o, i
 __global__ void __launch_bounds__(kTB) k_mac(const u64 *__restrict__ pt, const u64 *__restrict__ R,
                                              u64 *__restrict__ acc, const int *__restrict__ ent_r,
                                              const int *__restrict__ ent_pt, const int *__restrict__ ent_start,
-                                             int o0, int e_base, int n_o, int k, int logN, Primes pr) {
+                                             int o0, int e_base, int n_o, int k, int kq, int Kfull, int logN,
+                                             Primes pr) {
     const int N = 1 << logN;
     const int n_tiles = N / (2 * kTB);
     int bid = blockIdx.x;
@@ -97,7 +98,8 @@ __global__ void __launch_bounds__(kTB) k_mac(const u64 *__restrict__ pt, const u
     const long long kN = (long long)k * N;
     const int e_lo = ent_start[o0 + o], e_hi = ent_start[o0 + o + 1];
     const long long lx = (long long)l * N + x;
-    const ModConst &mc = pr.m[l];
+    // limbs l >= kq are the special primes of the extended basis Q_l u P (double hoisting)
+    const ModConst &mc = pr.m[l < kq ? l : Kfull + (l - kq)];
     u64 *out = acc + (long long)o * 2 * kN + lx;
     if (mc.q < (1ull << 41)) {
         // 40-bit limb: split 32-bit partial products (Acc41)
@@ -173,6 +175,9 @@ __device__ __forceinline__ void mac_run(const u64 *__restrict__ pp, const u64 *_
         compute(0, e);
         if (e + 2 * D < n_e) load(0, e + 2 * D);
         compute(1, e + D);
+        if (!SPLIT41 && (e & 63) == 60) {
+            a00.fold(mc); a01.fold(mc); a10.fold(mc); a11.fold(mc);
+        }
     }
     if (e < n_e) compute(0, e);
     *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00.reduce(mc), a01.reduce(mc));
@@ -235,6 +240,9 @@ __device__ __forceinline__ void mac_tma_consume(const u64 *ring, uint64_t *full,
         }
         __syncwarp();
         if ((t & 31) == 0) mbar_arrive(&empty[slot]);
+        if (!SPLIT41 && (s & 31) == 31) {  // 64 products < 2^126: fold before the 128-bit sum can overflow
+            a00.fold(mc); a01.fold(mc); a10.fold(mc); a11.fold(mc);
+        }
     }
     *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00.reduce(mc), a01.reduce(mc));
     *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(mc), a11.reduce(mc));
@@ -331,13 +339,14 @@ __global__ void k_copy_ct(const u64 *src, u64 *dst, long long n) {
 }  // namespace
 
 blb_status launch_mac(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc, const int *ent_r, const int *ent_pt,
-                      const int *ent_start, int o0, int e_base, int n_o, int n_entries, int k, cudaStream_t st) {
+                      const int *ent_start, int o0, int e_base, int n_o, int n_entries, int k, cudaStream_t st,
+                      int kq) {
     if (n_o <= 0) return BLB_OK;
     const int N = P->N;
     const int n_tiles = N / (2 * kTB);
     cudaEvent_t t0 = blb_timing_begin(st);
     k_mac<<<(unsigned)((size_t)n_o * n_tiles * k), kTB, 0, st>>>(pt, R, acc, ent_r, ent_pt, ent_start, o0, e_base, n_o,
-                                                                k, P->logN, P->pr);
+                                                                k, kq < 0 ? k : kq, P->K, P->logN, P->pr);
     BLB_COUNT_LAUNCH(1);
     BLB_COUNT(3, n_entries);
     blb_timing_end(0, t0, st, (double)n_entries * k * N * 8.0);
@@ -438,19 +447,6 @@ extern "C" blb_status blb_matmul_plan_create(const blb_params *P, int L, int w_r
             if (cnt && g > 0) pl->giant[bp].push_back(g);
             pl->ent_start.push_back((int)pl->ent_b.size());
         }
-    }
-    // 128-bit lazy MAC bound: (#entries per output) * (q_max - 1)^2 < 2^127
-    {
-        u128 qmax = 0;
-        for (int i = 0; i <= level; i++) qmax = std::max<u128>(qmax, P->mod[i]);
-        const u128 lim = (~(u128)0 >> 1) / ((qmax - 1) * (qmax - 1));
-        for (size_t o = 0; o + 1 < pl->ent_start.size(); o++)
-            if ((u128)(pl->ent_start[o + 1] - pl->ent_start[o]) > lim) {
-                blb_set_error("plan has %d products per output, 128-bit lazy MAC allows %llu: lower bsgs_B",
-                              pl->ent_start[o + 1] - pl->ent_start[o], (unsigned long long)lim);
-                delete pl;
-                return BLB_E_LAYOUT;
-            }
     }
     std::map<int32_t, int> steps;
     for (int b = 0; b < pl->n_in; b++)

@@ -34,8 +34,7 @@ __global__ void __launch_bounds__(kThreads) ntt_pass(RowBatch rb, const u64 *__r
     }
     const int pi = rb.prime[l];
     const u64 q = pr.m[pi].q, q2 = 2 * q;
-    const u64 *tw = tw_all + (size_t)pi * 4 * N + (INV ? 2 * N : 0);
-    const u64 *twsh = tw + N;
+    const ulonglong2 *twp = reinterpret_cast<const ulonglong2 *>(tw_all + (size_t)pi * 4 * N + (INV ? 2 * N : 0));
     const int colg0 = blockIdx.x * C;
     const bool strided = logT > 0;
     const int TM = C * M;
@@ -63,7 +62,8 @@ __global__ void __launch_bounds__(kThreads) ntt_pass(RowBatch rb, const u64 *__r
             const int mid = ((qq >> logtl) << (logtl + 1)) + (qq & (tl - 1));
             const int h = (colg0 + col) >> logT;
             const int widx = (1 << s) + (h << r) + (qq >> logtl);
-            const u64 w = tw[widx], wsh = twsh[widx];
+            const ulonglong2 tv = twp[widx];
+            const u64 w = tv.x, wsh = tv.y;
             const int i0 = strided ? (mid * C + col) : (col * M + mid);
             const int i1 = i0 + (strided ? (tl << logC) : tl);
             u64 X = sm[i0], Y = sm[i1];
@@ -146,8 +146,8 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, con
     u64 *a = rb.base + (long long)p * rb.poly_stride + (long long)(rb.limb0 + l) * N;
     const int pi = rb.prime[l];
     const u64 q = pr.m[pi].q, q2 = 2 * q;
-    const u64 *tw = tw_all + (size_t)pi * 4 * N + (INV ? 2 * N : 0);
-    const u64 *twsh = tw + N;
+    // interleaved (w, w') pairs: one 16-byte load per butterfly
+    const ulonglong2 *twp = reinterpret_cast<const ulonglong2 *>(tw_all + (size_t)pi * 4 * N + (INV ? 2 * N : 0));
     const int t = threadIdx.x;
     const int c0 = blockIdx.x * 16;  // first column of the tile (lo0 for STRIDED, h0 otherwise)
     // A mapping (coalesced global access)
@@ -182,7 +182,8 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, con
         for (int m = 0; m < 16; m++) {
             if (m & dist) continue;
             const int widx = (1 << s) + (hA << r) + (m >> (4 - r));
-            bfly<INV>(v[m], v[m + dist], tw[widx], twsh[widx], q, q2);
+            const ulonglong2 tv = twp[widx];
+            bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q2);
         }
     };
     auto roundB = [&](int r) {
@@ -192,7 +193,8 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, con
         for (int m = 0; m < 16; m++) {
             if (m & dist) continue;
             const int widx = (1 << s) + (hB << r) + ((16 * tcB + m) >> (8 - r));
-            bfly<INV>(v[m], v[m + dist], tw[widx], twsh[widx], q, q2);
+            const ulonglong2 tv = twp[widx];
+            bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q2);
         }
     };
     if (!INV) {

@@ -326,7 +326,8 @@ extern "C" blb_status blb_qk_plan_rotations(const blb_qk_plan *pl, int32_t *step
 
 static size_t qk_mask_elems(const blb_qk_plan *pl) {
     const size_t N = pl->P->N;
-    return pl->m1.size() * (size_t)(pl->level + 1) * N + pl->m3.size() * (size_t)(pl->level - 1) * N;
+    // stage-1 masks over the extended basis Q_l u P (double hoisting), stage-3 masks over Q_{l-2}
+    return pl->m1.size() * (size_t)(pl->level + 1 + pl->P->np) * N + pl->m3.size() * (size_t)(pl->level - 1) * N;
 }
 extern "C" size_t blb_qk_mask_bytes(const blb_qk_plan *pl) { return pl ? qk_mask_elems(pl) * sizeof(u64) : 0; }
 
@@ -348,13 +349,14 @@ extern "C" blb_status blb_qk_encode_masks(const blb_qk_plan *pl, uint64_t *masks
         const MaskDesc *dm = stage == 0 ? pl->d_m1 : pl->d_m3;
         const int cnt_all = (int)(stage == 0 ? pl->m1.size() : pl->m3.size());
         const int lvl = stage == 0 ? pl->level : pl->level - 2;
-        u64 *base = masks + (stage == 0 ? 0 : pl->m1.size() * (size_t)(pl->level + 1) * P->N);
+        const int npx = stage == 0 ? P->np : 0;
+        u64 *base = masks + (stage == 0 ? 0 : pl->m1.size() * (size_t)(pl->level + 1 + P->np) * P->N);
         for (int m0 = 0; m0 < cnt_all && s == BLB_OK; m0 += chunk) {
             const int cnt = std::min(chunk, cnt_all - m0);
             k_mask_slots<<<dim3((pl->n + kTB - 1) / kTB, cnt), kTB, 0, st>>>(dm, m0, qd, slots);
             BLB_COUNT_LAUNCH(1);
-            s = launch_encode(P, slots, cnt, (double)P->mod[lvl], lvl, base + (size_t)m0 * (lvl + 1) * P->N, buf, flag,
-                              st);
+            s = launch_encode(P, slots, cnt, (double)P->mod[lvl], lvl, base + (size_t)m0 * (lvl + 1 + npx) * P->N, buf,
+                              flag, st, npx);
         }
     }
     cudaFreeAsync(slots, st);
@@ -366,7 +368,7 @@ extern "C" blb_status blb_qk_encode_masks(const blb_qk_plan *pl, uint64_t *masks
 
 // workspace layout
 struct QKWs {
-    size_t kr, qr, kacc, kp, qacc, qp, d, s, sr, t, aacc, ar, arot, ext, coef, ks, resc, total;
+    size_t kr, qr, kacc, kmd, kp, qacc, qmd, qp, d, s, sr, t, aacc, ar, arot, ext, coef, ks, resc, total;
 };
 static QKWs qk_ws(const blb_qk_plan *pl) {
     const blb_params *P = pl->P;
@@ -376,11 +378,14 @@ static QKWs qk_ws(const blb_qk_plan *pl) {
     const size_t NKR = 1 + pl->k_rots.size(), NQR = pl->q_rots.size();
     QKWs w{};
     size_t o = 0;
-    w.kr = o; o += J * NKR * 2 * k * N;
-    w.qr = o; o += J * NQR * 2 * k * N;
-    w.kacc = o; o += B * J * 2 * k * N;
+    // stage 1 in the extended basis (E limbs), ModDown to k limbs, rescale to k1
+    w.kr = o; o += J * NKR * 2 * E * N;
+    w.qr = o; o += J * std::max<size_t>(NQR, 1) * 2 * E * N;
+    w.kacc = o; o += B * J * 2 * E * N;
+    w.kmd = o; o += B * J * 2 * k * N;
     w.kp = o; o += B * J * 2 * k1 * N;
-    w.qacc = o; o += (G > 1 ? (G - 1) : 1) * J * 2 * k * N;
+    w.qacc = o; o += (G > 1 ? (G - 1) : 1) * J * 2 * E * N;
+    w.qmd = o; o += (G > 1 ? (G - 1) : 1) * J * 2 * k * N;
     w.qp = o; o += G * J * 2 * k1 * N;
     w.d = o; o += G * B * 3 * k1 * N;
     w.s = o; o += G * B * 2 * k1 * N;
@@ -433,33 +438,6 @@ static blb_status rotate_independent(const blb_params *P, const blb_keys *keys, 
     return BLB_OK;
 }
 
-// all rotations of one ciphertext share one ModUp (hoisting, C8)
-static blb_status rotate_hoisted(const blb_params *P, const blb_keys *keys, int level, const u64 *in,
-                                 const std::vector<int32_t> &steps, u64 *out_base, size_t out_stride, u64 *ext,
-                                 u64 *coef, u64 *ks, cudaStream_t st) {
-    const int k = level + 1, N = P->N, E = k + P->np;
-    u64 *ks_u = ks, *ks_conv = ks + (size_t)kMaxJobs * 2 * E * N;
-    const u64 *c1 = in + (size_t)k * N;
-    BLB_TRY(launch_modup(P, level, &c1, 1, ext, coef, st));
-    for (size_t t0 = 0; t0 < steps.size(); t0 += kMaxJobs) {
-        const int cnt = (int)std::min<size_t>(kMaxJobs, steps.size() - t0);
-        std::vector<KsJob> jobs(cnt);
-        for (int t = 0; t < cnt; t++) {
-            const uint32_t g = blb_galois_element(P, steps[t0 + t]);
-            KsJob J{};
-            J.ext = ext;
-            J.key = key_for(keys, g);
-            J.c0 = in;
-            J.out = out_base + (t0 + t) * out_stride;
-            J.galois = g;
-            J.add_mode = 1;
-            jobs[t] = J;
-        }
-        BLB_TRY(launch_keyswitch(P, level, jobs.data(), cnt, ks_u, ks_conv, st));
-    }
-    return BLB_OK;
-}
-
 extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, const blb_ct *Q, const blb_ct *K, int J,
                                    const uint64_t *masks, blb_ct *out, void *ws, size_t ws_bytes, void *stream) {
     if (!pl || !keys || !Q || !K || !masks || !out || !ws) return BLB_E_INVALID_ARG;
@@ -493,32 +471,56 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
     cudaStream_t st = (cudaStream_t)stream;
     u64 *W = (u64 *)ws;
     const int *E = pl->d_ent;
-    const size_t ct_k = (size_t)2 * k * N, ct_k1 = (size_t)2 * k1 * N, ct_k2 = (size_t)2 * k2 * N,
+    const size_t ct_k1 = (size_t)2 * k1 * N, ct_k2 = (size_t)2 * k2 * N,
                  ct_k3 = (size_t)2 * k3 * N;
     const int NKR = 1 + (int)pl->k_rots.size(), NQR = (int)pl->q_rots.size();
-    const u64 *m1 = masks, *m3 = masks + pl->m1.size() * (size_t)k * N;
+    const u64 *m1 = masks, *m3 = masks + pl->m1.size() * (size_t)(k + P->np) * N;
 
-    // 1. baby side: hoisted rotations of every K^(j), K' = MAC(masks, Kr), rescale
+    // 1. baby side, double-hoisted (reading C13): one ModUp per K^(j), the 60 rotations stay in
+    //    Q_l u P (no ModDown), the masks are multiplied there, ONE ModDown per K'_i, then rescale
+    const int Ex = k + P->np;
+    const size_t ct_e = (size_t)2 * Ex * N;
+    u64 *conv = W + w.ks;  // ModDown intermediate (kMaxJobs x [2][k][N] fits the key-switch scratch)
+    auto rotate_ext_all = [&](const u64 *ct, const std::vector<int32_t> &steps, u64 *out_base) -> blb_status {
+        const u64 *c1 = ct + (size_t)k * N;
+        BLB_TRY(launch_modup(P, lvl, &c1, 1, W + w.ext, W + w.coef, st));
+        for (size_t t0 = 0; t0 < steps.size(); t0 += kMaxJobs) {
+            const int cnt = (int)std::min<size_t>(kMaxJobs, steps.size() - t0);
+            std::vector<KsJob> jobs(cnt);
+            for (int t = 0; t < cnt; t++) {
+                const uint32_t g = blb_galois_element(P, steps[t0 + t]);
+                KsJob Jb{};
+                Jb.ext = W + w.ext;
+                Jb.key = key_for(keys, g);
+                Jb.c0 = ct;
+                Jb.out = out_base + (t0 + t) * ct_e;
+                Jb.galois = g;
+                jobs[t] = Jb;
+            }
+            BLB_TRY(launch_keyswitch_ext(P, lvl, jobs.data(), cnt, st));
+        }
+        return BLB_OK;
+    };
     for (int j = 0; j < J; j++) {
-        u64 *kr = W + w.kr + (size_t)j * NKR * ct_k;
-        cudaMemcpyAsync(kr, K[j].data, ct_k * sizeof(u64), cudaMemcpyDeviceToDevice, st);
-        BLB_TRY(rotate_hoisted(P, keys, lvl, K[j].data, pl->k_rots, kr + ct_k, ct_k, W + w.ext, W + w.coef, W + w.ks, st));
+        u64 *kr = W + w.kr + (size_t)j * NKR * ct_e;
+        BLB_TRY(launch_lift_ext(P, lvl, K[j].data, kr, st));
+        BLB_TRY(rotate_ext_all(K[j].data, pl->k_rots, kr + ct_e));
     }
     BLB_TRY(launch_mac(P, m1, W + w.kr, W + w.kacc, E + pl->off_kp_r, E + pl->off_kp_pt, E + pl->off_kp_start, 0, 0,
-                       B * J, (int)pl->kp_r.size(), k, st));
-    BLB_TRY(launch_rescale(P, W + w.kacc, lvl, 2 * B * J, W + w.kp, W + w.resc, st));
-    // 2. giant side: Q_0 = level drop, Q_u = MAC(masks, Rot(Q)), rescale
+                       B * J, (int)pl->kp_r.size(), Ex, st, k));
+    BLB_TRY(launch_moddown(P, lvl, W + w.kacc, B * J, W + w.kmd, conv, st));
+    BLB_TRY(launch_rescale(P, W + w.kmd, lvl, 2 * B * J, W + w.kp, W + w.resc, st));
+    // 2. giant side: Q_0 = level drop, Q_u = ModDown(MAC(masks, Rot_ext(Q))), rescale
     for (int j = 0; j < J; j++) {
-        if (NQR)
-            BLB_TRY(rotate_hoisted(P, keys, lvl, Q[j].data, pl->q_rots, W + w.qr + (size_t)j * NQR * ct_k, ct_k,
-                                   W + w.ext, W + w.coef, W + w.ks, st));
+        if (NQR) BLB_TRY(rotate_ext_all(Q[j].data, pl->q_rots, W + w.qr + (size_t)j * NQR * ct_e));
         k_copy_limbs<<<gx(N, k1, 2), kTB, 0, st>>>(Q[j].data, W + w.qp + (size_t)j * ct_k1, k, k1, N);
         BLB_COUNT_LAUNCH(1);
     }
     if (G > 1) {
         BLB_TRY(launch_mac(P, m1, W + w.qr, W + w.qacc, E + pl->off_qp_r, E + pl->off_qp_pt, E + pl->off_qp_start, 0, 0,
-                           (G - 1) * J, (int)pl->qp_r.size(), k, st));
-        BLB_TRY(launch_rescale(P, W + w.qacc, lvl, 2 * (G - 1) * J, W + w.qp + (size_t)J * ct_k1, W + w.resc, st));
+                           (G - 1) * J, (int)pl->qp_r.size(), Ex, st, k));
+        BLB_TRY(launch_moddown(P, lvl, W + w.qacc, (G - 1) * J, W + w.qmd, conv, st));
+        BLB_TRY(launch_rescale(P, W + w.qmd, lvl, 2 * (G - 1) * J, W + w.qp + (size_t)J * ct_k1, W + w.resc, st));
     }
     // 3. products summed over j, relinearisation (one per (u, i)), rescale
     k_tensor_sum<<<gx(N, k1, G * B), kTB, 0, st>>>(W + w.qp, W + w.kp, W + w.d, P->pr, J, B, k1, N);

@@ -78,3 +78,32 @@ def test_bert_oproj_diagonal_sampled_output_bit_exact(bert):
     assert (plan_g.n_pt, plan_g.n_rotations) == (plan_o.n_plaintexts, plan_o.n_rotations) == (2304, 90)
     zs = list(packing.diagonal_slots(F["Att"], octx.n))
     run(octx, g, plan_o, plan_g, zs, F["WO"], sample=[2])
+
+
+def test_bert_size_qk_bit_exact(bert):
+    """Row a7 at N = 2^16, L = 128 (16 heads of d_h = 8: g = 16, J = 1, B = 16, G = 8): the
+    double-hoisted stage 1, relinearisation, step-3 rotations and deferred giant step on the
+    fused N = 2^16 kernels, bit-exact against the oracle."""
+    import oracle.matmul_cc as cc
+    octx, g = bert
+    L, H, dh = 128, 16, 8
+    rng = np.random.default_rng(5)
+    Q, K = rng.uniform(-1, 1, (H, L, dh)), rng.uniform(-1, 1, (H, L, dh))
+    plan_o = cc.plan_qk(L, H, dh, octx.n)
+    plan_g = blb.QKPlan(g, L, H, dh, level=3)
+    assert plan_g.rotation_steps() == plan_o.rotation_steps()
+    key, ekey = bi.crypto_key(4, 3), bi.crypto_key(5, 3)
+    steps = plan_g.rotation_steps()
+    okeys = O.keygen(octx, key, steps, relin=True)
+    gkeys, sk = blb.keygen(g, key, steps, relin=True)
+    lvl, delta = 3, 2.0 ** 40
+    oq, ok, gq, gk = [], [], [], []
+    for j, (zq, zk) in enumerate(zip(cc.pack_mhp(Q, plan_o), cc.pack_mhp(K, plan_o))):
+        for z, cid, ol, gl in ((zq, j, oq, gq), (zk, 10 + j, ok, gk)):
+            pt = O.encode(octx, z, delta, lvl)
+            ol.append(O.encrypt(octx, ekey, okeys.s_ntt, pt, lvl, cid, delta))
+            gl.append(blb.encrypt(g, sk, blb.from_numpy_u64(pt), lvl, ekey, cid, delta))
+    gout = plan_g(gkeys, gq, gk, plan_g.encode_masks())
+    oout = cc.qk_encrypted(octx, okeys, oq, ok, plan_o)
+    for a, b in zip(gout, oout):
+        assert a.scale == b.scale and np.array_equal(blb.to_numpy_u64(a.data), b.data)

@@ -449,3 +449,18 @@ def test_bert_size_keyswitch_bit_exact(bert):
     data = rand_limbs(bert, 2, list(range(5)), 7)
     oc, gc = O.Ct(data, 4, 1.0), blb.Ciphertext(dev(data), 4, 1.0)
     assert np.array_equal(u64(blb.rotate_sum(bert.g, gkeys, gc, 128, 2).data), O.rotate_sum(bert.o, oc, okeys, 128, 2).data)
+
+
+def test_matmul_long_mac_fold_bit_exact(toy):
+    """192 products per output (12 inputs x B = 16) exceed the 128-bit lazy bound for the
+    60-bit q_0 limb: the MAC folds its accumulator every 64 products."""
+    L, D, Dout = 16, 1536, 16
+    X = bi.uniform(95, (L, D), -1, 1)
+    W = bi.normal(96, (D, Dout), 0.02)
+    plan_o = mm.plan_spatial(W, L, toy.n, 16)
+    plan_g = blb.MatmulPlan(toy.g, L, D, Dout, bsgs_B=16)
+    assert plan_g.n_in == 12 and plan_g.n_pt == plan_o.n_plaintexts
+    from paper_2508_19525_b200 import packing
+    zs = list(packing.spatial_slots(X, toy.n))
+    _, _, oout, gout = run_both(toy, plan_o, plan_g, zs, W)
+    assert np.array_equal(u64(gout[0].data), oout[0].data)
