@@ -341,3 +341,30 @@ def test_squaring_chain(qk_ctx=None):
     assert ct.level == 1
     got = O.decode(ctx, O.decrypt(ctx, keys.s_ntt, ct), ct.scale)
     assert np.abs(got - z ** 8).max() < 1e-6
+
+
+def test_extended_basis_identities(toy, toy_keys):
+    """Double hoisting (DESIGN C13): ModDown(P*x + y) = x + ModDown(y) exactly, because P*x
+    vanishes mod P and (P*x)*P^-1 = x mod Q (C7).  Hence ModDown(rotate_ext(ct)) equals the
+    plain hoisted rotation bit for bit, ModDown of the step-0 lift (P c0, P c1) is ct itself,
+    and an extended-basis plaintext restricted to Q_l is the ordinary encoding (C3)."""
+    z = np.random.default_rng(21).uniform(-1, 1, toy.n)
+    for lvl in (2, 1):
+        ct = enc(toy, toy_keys, z, 7)
+        if lvl < 2:
+            ct = O.Ct(ct.data[:, :lvl + 1].copy(), lvl, ct.scale)
+        lift = O.rotate_ext(toy, ct, toy_keys, 0)
+        assert lift.data.shape == (2, lvl + 1 + toy.np_, toy.N)
+        assert np.array_equal(O.moddown_ct(toy, lift).data, ct.data)
+        for r in (1, 16, -16):
+            got = O.moddown_ct(toy, O.rotate_ext(toy, ct, toy_keys, r))
+            assert np.array_equal(got.data, O.rotate(toy, ct, toy_keys, r).data)
+        m = np.random.default_rng(22).uniform(-1, 1, toy.n)
+        pe = O.encode_ext(toy, m, float(toy.q[lvl]), lvl)
+        assert np.array_equal(pe[:lvl + 1], O.encode(toy, m, float(toy.q[lvl]), lvl))
+        # the special-prime residue is the same rounded integer mod p
+        coef_q = toy.intt(pe[:1], [0])[0]
+        coef_p = toy.intt(pe[lvl + 1:], O.ext_pidx(toy, lvl)[lvl + 1:])[0]
+        q0, p0 = int(toy.mods[0]), int(toy.mods[O.ext_pidx(toy, lvl)[lvl + 1]])
+        cq = [int(v) if int(v) < q0 // 2 else int(v) - q0 for v in coef_q]
+        assert all((c - int(v)) % p0 == 0 for c, v in zip(cq, coef_p))
