@@ -33,6 +33,8 @@ import numpy as np  # noqa: E402
 import blb_inputs as bi  # noqa: E402
 
 METRIC = "ms per BERT-base layer fused-linear CKKS eval"
+# BSGS baby-step counts B per ct-pt MatMul (C11, plan parameter S15); shared by both arms
+BSGS = {"qkv": 64, "oproj": 16, "ffn1": 64, "ffn2": 16}
 UNIT = "ms"
 FALLBACK_HBM = 6650.0
 
@@ -137,10 +139,10 @@ def oracle_sample_ms(dims, reps: int = 1) -> dict:
     cm = mm.mhp_column_map(dims["d"], dims["H"], dims["L"], n)
     qkv_map = cm + [dims["d"] + c if c >= 0 else -1 for c in cm] + list(range(2 * dims["d"], 3 * dims["d"]))
     Hp = 1 << (dims["H"] - 1).bit_length()
-    plans = [mm.plan_spatial(np.ones((dims["d"], 3 * dims["d"])), dims["L"], n, 32, col_map=qkv_map),
-             mm.plan_diagonal(np.ones((Hp * (dims["d"] // dims["H"]), dims["d"])), Hp, dims["L"], n, 16),
-             mm.plan_spatial(np.ones((dims["d"], dims["ffn"])), dims["L"], n, 32),
-             mm.plan_spatial(np.ones((dims["ffn"], dims["d"])), dims["L"], n, 8)]
+    plans = [mm.plan_spatial(np.ones((dims["d"], 3 * dims["d"])), dims["L"], n, BSGS["qkv"], col_map=qkv_map),
+             mm.plan_diagonal(np.ones((Hp * (dims["d"] // dims["H"]), dims["d"])), Hp, dims["L"], n, BSGS["oproj"]),
+             mm.plan_spatial(np.ones((dims["d"], dims["ffn"])), dims["L"], n, BSGS["ffn1"]),
+             mm.plan_spatial(np.ones((dims["ffn"], dims["d"])), dims["L"], n, BSGS["ffn2"])]
     import oracle.matmul_cc as cc
     n_rot = sum(p.n_rotations for p in plans)
     n_pt = sum(p.n_plaintexts for p in plans)
@@ -192,7 +194,7 @@ def config_dict(dims, world):
     return {"workload": "BERT-base layer fused-linear CKKS (config 2 QKV + Q.K^T, Softmax.V + out-proj, config 3 "
                         "FFN1/FFN2, CKKS->MPC masks), N=2^16, Q={60,40x4}, P={60}, dnum=5",
             "L": dims["L"], "d": dims["d"], "heads": dims["H"], "ffn": dims["ffn"], "log_n": 16, "limbs": 5,
-            "bsgs": {"qkv": 32, "oproj": 16, "ffn1": 32, "ffn2": 8},
+            "bsgs": dict(BSGS),
             "layer_ops": ["qkv_ct_pt(MHP)", "qk_ct_ct(MHP+BSGS)", "mask(QK^T)", "mask(V)",
                           "softmaxV_ct_ct(pad+collapse)", "oproj_diag_ct_pt(level 1)", "mask", "ffn1_ct_pt", "mask",
                           "ffn2_ct_pt", "mask"],
@@ -234,7 +236,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     t_setup0 = time.perf_counter()
     params = blb.Params.from_preset(bi.BERT, device=local)
-    layer = FusedLinearLayer(params, Dims(**dims), rank, world)
+    layer = FusedLinearLayer(params, Dims(**dims), rank, world, bsgs=BSGS)
     A = bi.bert_attention_inputs(dims["L"], dims["d"])
     F = bi.bert_ffn_inputs(dims["L"], dims["d"], dims["H"], dims["ffn"])
     keys, sk = blb.keygen(params, A["keys_key"], layer.rotation_steps(), relin=True)

@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import Ct, Ctx, Keys, add, encode, mul_pt, rescale, rotate
+from . import Ct, Ctx, Keys, add, add_ext, encode, moddown_ct, mul_pt, rescale, rotate, rotate_ext
 
 
 # ---------------------------------------------------------------------------
@@ -239,11 +239,14 @@ def matmul_cp(ctx: Ctx, keys: Keys, cts: list[Ct], plan: Plan, out_ids=None) -> 
                 acc = term if acc is None else add(ctx, acc, term)
             if acc is None:
                 continue
-            if g > 0:
-                acc = rotate(ctx, acc, keys, g * plan.B * plan.L)
-            Y = acc if Y is None else add(ctx, Y, acc)
+            # giant step kept in Q_l u P (reading C11, lazy ModDown): Rot_ext(acc) =
+            # (P sigma(c0) + u0, u1); g = 0 is the lift (P c0, P c1)
+            term = rotate_ext(ctx, acc, keys, g * plan.B * plan.L)
+            Y = term if Y is None else add_ext(ctx, Y, term)
         if Y is None:
             Y = Ct(np.zeros_like(cts[0].data), level, cts[0].scale * pt_scale)
+        else:
+            Y = moddown_ct(ctx, Y)       # one ModDown per output (C7)
         outs.append(rescale(ctx, Y))
     return outs
 

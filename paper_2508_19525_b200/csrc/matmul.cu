@@ -323,11 +323,12 @@ struct AccJobs {
     u64 *dst[kMaxJobs];
     const u64 *src[kMaxJobs];
 };
-__global__ void k_accumulate(AccJobs jobs, Primes pr, int k, int N) {
+// limbs l >= kq of an extended (Q_l u P) ciphertext are the special primes K + (l - kq)
+__global__ void k_accumulate(AccJobs jobs, Primes pr, int k, int N, int kq, int K) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int l = blockIdx.y, p = blockIdx.z;
     if (x >= N) return;
-    const u64 q = pr.m[l].q;
+    const u64 q = pr.m[l < kq ? l : K + (l - kq)].q;
     const long long off = ((long long)p * k + l) * N + x;
     for (int j = 0; j < jobs.n; j++) jobs.dst[j][off] = addmod(jobs.dst[j][off], jobs.src[j][off], q);
 }
@@ -592,7 +593,7 @@ extern "C" blb_status blb_matmul_encode_weights(const blb_matmul_plan *pl, const
 
 // workspace layout (u64 elements)
 struct MatmulWs {
-    size_t ext_in, coef, R, ks, acc, gext, gcoef, gks, rot, resc, total;
+    size_t ext_in, coef, R, ks, acc, gext, gcoef, gks, rot, yext, ymd, resc, total;
 };
 static MatmulWs matmul_ws(const blb_matmul_plan *pl, int out_count) {
     const blb_params *P = pl->P;
@@ -607,7 +608,9 @@ static MatmulWs matmul_ws(const blb_matmul_plan *pl, int out_count) {
     w.gext = o; o += (size_t)kMaxJobs * beta * E * N;
     w.gcoef = o; o += (size_t)kMaxJobs * k * N;
     w.gks = o; o += keyswitch_scratch_elems(P, pl->level, kMaxJobs);
-    w.rot = o; o += (size_t)kMaxJobs * 2 * k * N;
+    w.rot = o; o += (size_t)kMaxJobs * 2 * E * N;
+    w.yext = o; o += (size_t)out_count * 2 * E * N;
+    w.ymd = o; o += (size_t)out_count * 2 * k * N;
     w.resc = o; o += (2 + 2 * k) * N;
     w.total = o;
     return w;
@@ -660,7 +663,8 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
     u64 *W = (u64 *)ws;
     u64 *ext_in = W + w.ext_in, *coef = W + w.coef, *R = W + w.R, *ks = W + w.ks, *acc = W + w.acc;
     u64 *gext = W + w.gext, *rot = W + w.rot, *resc = W + w.resc, *gcoef = W + w.gcoef;
-    u64 *gks_u = W + w.gks, *gks_conv = W + w.gks + (size_t)kMaxJobs * 2 * E * N;
+    u64 *yext = W + w.yext, *ymd = W + w.ymd;
+    u64 *gks_conv = W + w.gks + (size_t)kMaxJobs * 2 * E * N;
     const size_t ctN = (size_t)2 * k * N;
     u64 *ks_u = ks, *ks_conv = ks + (size_t)kMaxJobs * 2 * E * N;
 
@@ -745,7 +749,16 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
             BLB_CUDA_TRY(cudaEventRecord(e, st));
             BLB_CUDA_TRY(cudaStreamWaitEvent(sa, e, 0));
         }
-        // giant steps: acc[b'][0] += Rot_{gBL}(acc[b'][g]), g-major so outputs sharing a key are adjacent
+        // giant steps (reading C11, lazy ModDown): Y[b'] = lift(acc[b'][0]) + sum_g Rot_ext(acc[b'][g])
+        // in Q_l u P, then ONE ModDown per output; g-major so outputs sharing a key are adjacent
+        std::vector<int> yslot(cn, -1);
+        int n_y = 0;
+        for (int t = c0; t < c0 + cn; t++)
+            if (!pl->giant[out_first + t].empty()) {
+                yslot[t - c0] = n_y;
+                BLB_TRY(launch_lift_ext(P, level, acc + (size_t)t * pl->G * ctN, yext + (size_t)n_y * 2 * E * N, sa));
+                n_y++;
+            }
         struct GJob {
             int t, g;
         };
@@ -768,22 +781,23 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
                 J.ext = gext + (size_t)j * beta * E * N;
                 J.key = find_key(G.g * pl->B * pl->L);
                 J.c0 = a;
-                J.out = rot + (size_t)j * ctN;
+                J.out = rot + (size_t)j * 2 * E * N;
                 J.galois = blb_galois_element(P, G.g * pl->B * pl->L);
-                J.add_mode = 1;
                 jobs[j] = J;
-                aj.dst[j] = acc + ((size_t)G.t * pl->G) * ctN;
+                aj.dst[j] = yext + (size_t)yslot[G.t - c0] * 2 * E * N;
                 aj.src[j] = J.out;
             }
             BLB_TRY(launch_modup(P, level, c1.data(), cnt, gext, gcoef, sa));
-            BLB_TRY(launch_keyswitch(P, level, jobs.data(), cnt, gks_u, gks_conv, sa));
-            k_accumulate<<<dim3((N + kTB - 1) / kTB, k, 2), kTB, 0, sa>>>(aj, P->pr, k, N);
+            BLB_TRY(launch_keyswitch_ext(P, level, jobs.data(), cnt, sa));
+            k_accumulate<<<dim3((N + kTB - 1) / kTB, E, 2), kTB, 0, sa>>>(aj, P->pr, E, N, k, P->K);
             BLB_COUNT_LAUNCH(1);
             BLB_CHECK_LAUNCH();
         }
-        // rescale the chunk's outputs
+        if (n_y > 0) BLB_TRY(launch_moddown(P, level, yext, n_y, ymd, gks_conv, sa));
+        // rescale the chunk's outputs (outputs without giant steps: ModDown(lift(x)) = x exactly)
         for (int t = c0; t < c0 + cn; t++) {
-            BLB_TRY(launch_rescale(P, acc + (size_t)t * pl->G * ctN, level, 2, out[t].data, resc, sa));
+            const u64 *src = yslot[t - c0] >= 0 ? ymd + (size_t)yslot[t - c0] * ctN : acc + (size_t)t * pl->G * ctN;
+            BLB_TRY(launch_rescale(P, src, level, 2, out[t].data, resc, sa));
             out[t].level = level - 1;
             out[t].scale = in[0].scale;  // Delta * q_level / q_level, exact (reading S6)
         }

@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, con
         for (int r = 3; r >= 0; r--) roundA(r);
     }
     const ModConst &mc = pr.m[pi];
-    if (EPI == 1) {  // ModDown combine (forward, contiguous last pass)
+    if constexpr (EPI == 1) {  // ModDown combine (forward, contiguous last pass)
         const int tj = p >> 1, b = p & 1;
         const KsJob &J = fz.jobs.j[tj];
         const u64 *ui = fz.u + ((long long)p * fz.E + l) * N;
@@ -247,23 +247,23 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, con
             }
             out[gx] = r;
         }
-        return;
-    }
+    } else {
 #pragma unroll
-    for (int m = 0; m < 16; m++) {
-        u64 x = v[m];
-        if (last) {
-            if (!INV) {
-                if (x >= q2) x -= q2;
-                if (x >= q) x -= q;
-            } else {
-                x = shoup_lazy(x, mc.ninv, mc.ninv_sh, q);
-                if (x >= q) x -= q;
+        for (int m = 0; m < 16; m++) {
+            u64 x = v[m];
+            if (last) {
+                if (!INV) {
+                    if (x >= q2) x -= q2;
+                    if (x >= q) x -= q;
+                } else {
+                    x = shoup_lazy(x, mc.ninv, mc.ninv_sh, q);
+                    if (x >= q) x -= q;
+                }
             }
+            const int mid = tcA + 16 * m;
+            const size_t addr = STRIDED ? (((size_t)mid << 8) + c0 + colA) : (((size_t)(c0 + colA) << 8) + mid);
+            a[addr] = x;
         }
-        const int mid = tcA + 16 * m;
-        const size_t addr = STRIDED ? (((size_t)mid << 8) + c0 + colA) : (((size_t)(c0 + colA) << 8) + mid);
-        a[addr] = x;
     }
 }
 

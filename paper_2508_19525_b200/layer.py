@@ -41,7 +41,7 @@ class Dims:
 
 BERT_BASE = Dims()
 BERT_LARGE = Dims(128, 1024, 16, 4096)
-BSGS = {"qkv": 32, "oproj": 16, "ffn1": 32, "ffn2": 8, "qk": 0}
+BSGS = {"qkv": 64, "oproj": 16, "ffn1": 64, "ffn2": 16, "qk": 0}
 PLAN_ID = {"qkv": 0, "oproj": 1, "ffn1": 2, "ffn2": 3, "qk": 4}
 
 
