@@ -118,6 +118,9 @@ def lib():
                                          ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
         L.orc_encode_ext.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_int,
                                      ctypes.c_void_p]
+        L.orc_moddown_rescale.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+        L.orc_relinearize_ext.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                          ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -548,6 +551,21 @@ def add_ext(ctx: Ctx, a: CtExt, b: CtExt) -> CtExt:
     out = np.empty_like(a.data)
     lib().orc_add_idx(ctx._h, _p(_u64(a.data)), _p(_u64(b.data)), pa, len(idx), 2, _p(out))
     return CtExt(out, a.level, a.scale)
+
+
+def relinearize_ext(ctx: Ctx, d: Ct, keys: Keys) -> CtExt:
+    """Relinearisation kept in Q_l u P: (P d0 + u0, P d1 + u1) (reading C17)."""
+    out = np.empty((2, d.level + 1 + ctx.np_, ctx.N), dtype=np.uint64)
+    lib().orc_relinearize_ext(ctx._h, _p(_u64(d.data)), d.level, _p(keys.rlk), _p(out))
+    return CtExt(out, d.level, d.scale)
+
+
+def moddown_rescale(ctx: Ctx, a: CtExt) -> Ct:
+    """ModDown fused with rescale (reading C17): round(X / (q_l P)) exactly, level l -> l - 1,
+    scale / q_l (the P factor of the extended form is the lift's, not the message's)."""
+    out = np.empty((2, a.level, ctx.N), dtype=np.uint64)
+    lib().orc_moddown_rescale(ctx._h, _p(_u64(a.data)), a.level, _p(out))
+    return Ct(out, a.level - 1, a.scale / ctx.q[a.level])
 
 
 def moddown_ct(ctx: Ctx, a: CtExt) -> Ct:

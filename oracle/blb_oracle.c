@@ -805,3 +805,75 @@ int orc_encode_ext(const orc_ctx *c, const double *z, double scale, int lvl, u64
     free(coef);
     return st;
 }
+
+/* ------------------------------------------------------------------ */
+/* ModDown fused with rescale (reading C17): one exact rounding         */
+/* ------------------------------------------------------------------ */
+/* in [2][k+np][N] NTT over Q_lvl u P (k = lvl+1) -> out [2][lvl][N] NTT over Q_{lvl-1}:
+ *   y = round(X / M),  M = q_lvl * p_0 ... p_{np-1} (odd, so no ties),
+ * computed as y = (X + h - r) / M with h = (M-1)/2 and r = (X + h) mod M, where r is
+ * rebuilt exactly from the residues of X + h at the M-moduli (Garner's mixed radix:
+ * r = d_0 + m_0 (d_1 + m_1 (d_2 + ...)), d_t < m_t).  The quotient is the same integer
+ * mod Q_{lvl-1} whichever representative of X mod Q_lvl P is taken (it shifts by
+ * multiples of Q_lvl P / M = Q_{lvl-1}). */
+void orc_moddown_rescale(const orc_ctx *c, const u64 *in, int lvl, u64 *out) {
+    int k = lvl + 1, np = c->np, E = k + np, nd = 1 + np;
+    u64 N = c->N;
+    u64 m[ORC_MAXP]; int mi[ORC_MAXP];
+    m[0] = c->mod[lvl]; mi[0] = lvl;
+    for (int t = 0; t < np; t++) { m[1 + t] = c->mod[c->K + t]; mi[1 + t] = c->K + t; }
+    u64 *drop = (u64 *)malloc((u64)nd * N * sizeof(u64));
+    u64 *w = (u64 *)malloc((u64)lvl * N * sizeof(u64));
+    for (int p = 0; p < 2; p++) {
+        const u64 *x = in + (u64)p * E * N;
+        for (int t = 0; t < nd; t++) {
+            memcpy(drop + (u64)t * N, x + (u64)(lvl + t) * N, N * sizeof(u64));  /* limbs lvl, k.. are q_lvl, P */
+            intt_limb(c, drop + (u64)t * N, mi[t]);
+        }
+        for (u64 j = 0; j < N; j++) {
+            u64 d[ORC_MAXP];
+            for (int t = 0; t < nd; t++) {
+                u64 v = addmod(drop[(u64)t * N + j], (m[t] - 1) / 2, m[t]);  /* h = -1/2 mod m_t */
+                for (int s = 0; s < t; s++) v = mulmod(submod(v, d[s] % m[t], m[t]), invmod(m[s] % m[t], m[t]), m[t]);
+                d[t] = v;
+            }
+            for (int i = 0; i < lvl; i++) {
+                u64 q = c->mod[i], r = 0, Mq = 1;
+                for (int t = nd - 1; t >= 0; t--) r = addmod(mulmod(r, m[t] % q, q), d[t] % q, q);
+                for (int t = 0; t < nd; t++) Mq = mulmod(Mq, m[t] % q, q);
+                u64 h = mulmod(submod(Mq, 1, q), invmod(2, q), q);   /* (M - 1) / 2 mod q_i */
+                w[(u64)i * N + j] = submod(h, r, q);
+            }
+        }
+        for (int i = 0; i < lvl; i++) {
+            u64 q = c->mod[i], Mq = 1;
+            for (int t = 0; t < nd; t++) Mq = mulmod(Mq, m[t] % q, q);
+            u64 Minv = invmod(Mq, q);
+            ntt_limb(c, w + (u64)i * N, i);
+            for (u64 j = 0; j < N; j++)
+                out[((u64)p * lvl + i) * N + j] = mulmod(addmod(x[(u64)i * N + j], w[(u64)i * N + j], q), Minv, q);
+        }
+    }
+    free(drop); free(w);
+}
+
+/* Relinearisation kept in Q_l u P (reading C17): d = (d0, d1, d2) [3][k][N] ->
+ * out [2][k+np][N] = (P d0 + u0, P d1 + u1), u = sum_j ModUp(D_j(d2)) * rlk_j (C7, C9);
+ * a following ModDown + rescale is then one exact rounding (orc_moddown_rescale). */
+void orc_relinearize_ext(const orc_ctx *c, const u64 *d, int lvl, const u64 *rlk, u64 *out) {
+    int k = lvl + 1, E = k + c->np, beta = (k + c->alpha - 1) / c->alpha;
+    u64 N = c->N;
+    u64 *ext = (u64 *)malloc((u64)beta * E * N * sizeof(u64));
+    orc_modup(c, d + 2ull * k * N, lvl, ext);
+    orc_ks_inner(c, ext, lvl, rlk, 1, out);
+    for (int p = 0; p < 2; p++)
+        for (int i = 0; i < k; i++) {
+            u64 q = c->mod[i], Pm = 1;
+            for (int t = 0; t < c->np; t++) Pm = mulmod(Pm, c->mod[c->K + t] % q, q);
+            for (u64 x = 0; x < N; x++) {
+                u64 *o = out + ((u64)p * E + i) * N + x;
+                *o = addmod(*o, mulmod(d[((u64)p * k + i) * N + x], Pm, q), q);
+            }
+        }
+    free(ext);
+}

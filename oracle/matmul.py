@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import Ct, Ctx, Keys, add, add_ext, encode, moddown_ct, mul_pt, rescale, rotate, rotate_ext
+from . import Ct, Ctx, Keys, add, add_ext, encode, moddown_rescale, mul_pt, rescale, rotate, rotate_ext
 
 
 # ---------------------------------------------------------------------------
@@ -245,9 +245,9 @@ def matmul_cp(ctx: Ctx, keys: Keys, cts: list[Ct], plan: Plan, out_ids=None) -> 
             Y = term if Y is None else add_ext(ctx, Y, term)
         if Y is None:
             Y = Ct(np.zeros_like(cts[0].data), level, cts[0].scale * pt_scale)
-        else:
-            Y = moddown_ct(ctx, Y)       # one ModDown per output (C7)
-        outs.append(rescale(ctx, Y))
+            outs.append(rescale(ctx, Y))
+            continue
+        outs.append(moddown_rescale(ctx, Y))   # ModDown + rescale as one exact rounding (C17)
     return outs
 
 

@@ -248,7 +248,7 @@ def qk_encrypted(ctx: Ctx, keys: Keys, Q: list[Ct], K: list[Ct], plan: QKPlan) -
                 for wrap, r in parts:
                     term = O.mul_pt_ext(ctx, rots[r], pt1(("k", c, i, wrap), plan.mask_k(c, i, wrap)), s1)
                     acc = term if acc is None else O.add_ext(ctx, acc, term)
-            Kp[(i, j)] = rescale(ctx, O.moddown_ct(ctx, acc))
+            Kp[(i, j)] = O.moddown_rescale(ctx, acc)
     Qu = {}
     for j in range(plan.J):
         Qu[(0, j)] = drop(Q[j])
@@ -257,7 +257,7 @@ def qk_encrypted(ctx: Ctx, keys: Keys, Q: list[Ct], K: list[Ct], plan: QKPlan) -
             t1 = O.mul_pt_ext(ctx, O.rotate_ext(ctx, Q[j], keys, -a), pt1(("q", u, False), plan.mask_q(u, False)), s1)
             t2 = O.mul_pt_ext(ctx, O.rotate_ext(ctx, Q[j], keys, plan.L - a),
                               pt1(("q", u, True), plan.mask_q(u, True)), s1)
-            Qu[(u, j)] = rescale(ctx, O.moddown_ct(ctx, O.add_ext(ctx, t1, t2)))
+            Qu[(u, j)] = O.moddown_rescale(ctx, O.add_ext(ctx, t1, t2))
     # products, relinearisation (once per (u, i), lazy over j: reading S10), rescale -> lvl-2
     T = {}
     for u in range(plan.G):
@@ -266,9 +266,11 @@ def qk_encrypted(ctx: Ctx, keys: Keys, Q: list[Ct], K: list[Ct], plan: QKPlan) -
             for j in range(plan.J):
                 t = tensor(ctx, Qu[(u, j)], Kp[(i, j)])
                 d = t if d is None else add(ctx, d, t)
-            S = rescale(ctx, relinearize(ctx, d, keys))
-            T[(u, i)] = rotate(ctx, S, keys, -i * plan.Hp * plan.L) if i else S
-    # step 3 masks at level lvl-2 (scale q_{lvl-2}), rescale -> lvl-3, final rotations, sums
+            S = O.moddown_rescale(ctx, O.relinearize_ext(ctx, d, keys))   # C17
+            # step-3 rotation kept in Q u P (double hoisting, C13); i = 0 is the lift
+            T[(u, i)] = O.rotate_ext(ctx, S, keys, -i * plan.Hp * plan.L)
+    # step 3 masks at level lvl-2 (scale q_{lvl-2}) in Q u P, ModDown + rescale -> lvl-3 (C17),
+    # final rotations summed in Q u P, one ModDown per output
     l3 = lvl - 2
     s3 = float(ctx.q[l3])
     outs = [None] * plan.n_out
@@ -278,15 +280,13 @@ def qk_encrypted(ctx: Ctx, keys: Keys, Q: list[Ct], K: list[Ct], plan: QKPlan) -
             m = plan.mask3(u, i, w, f)
             if not m.any():
                 continue
-            term = mul_pt(ctx, T[(u, i)], encode(ctx, m, s3, l3), s3)
-            A = term if A is None else add(ctx, A, term)
-        A = rescale(ctx, A)
-        r = plan.final_rot(u, f)
-        if r % plan.n:
-            A = rotate(ctx, A, keys, r)
+            term = O.mul_pt_ext(ctx, T[(u, i)], O.encode_ext(ctx, m, s3, l3), s3)
+            A = term if A is None else O.add_ext(ctx, A, term)
+        A = O.moddown_rescale(ctx, A)
+        Ae = O.rotate_ext(ctx, A, keys, plan.final_rot(u, f) % plan.n)
         o = plan.out_index(u, w)
-        outs[o] = A if outs[o] is None else add(ctx, outs[o], A)
-    return outs
+        outs[o] = Ae if outs[o] is None else O.add_ext(ctx, outs[o], Ae)
+    return [O.moddown_ct(ctx, e) for e in outs]
 
 
 # ---------------------------------------------------------------------------

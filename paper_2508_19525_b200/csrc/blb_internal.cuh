@@ -293,7 +293,16 @@ struct NttFuse {
 // ModDown of n contiguous extended ciphertexts u [n][2][E][N] -> out [n][2][k][N]
 blb_status launch_keyswitch_ext(const blb_params *P, int level, const KsJob *jobs, int n, cudaStream_t st);
 blb_status launch_moddown(const blb_params *P, int level, u64 *u, int n, u64 *out, u64 *conv, cudaStream_t st);
+blb_status launch_moddown(const blb_params *P, int level, u64 *u, int n, u64 *const *outs, u64 *conv,
+                          cudaStream_t st);
 blb_status launch_lift_ext(const blb_params *P, int level, const u64 *in, u64 *out, cudaStream_t st);
+// ModDown fused with rescale (reading C17): u [n][2][level+1+np][N] (its q_level and P limbs are
+// INTT'd in place) -> round(X / (q_level P)) as [2][level][N] NTT ciphertexts; conv scratch
+// kMaxJobs x [2][level][N]
+blb_status launch_moddown_rescale(const blb_params *P, int level, u64 *u, int n, u64 *const *outs, u64 *conv,
+                                  cudaStream_t st);
+blb_status launch_moddown_rescale(const blb_params *P, int level, u64 *u, int n, u64 *out, u64 *conv,
+                                  cudaStream_t st);
 blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool inverse, const NttFuse &fz,
                             cudaStream_t st);
 size_t keyswitch_scratch_elems(const blb_params *P, int level, int n_jobs);  // u + conv, in u64

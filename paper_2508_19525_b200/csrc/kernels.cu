@@ -283,7 +283,9 @@ __global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, 
                 u64 r0 = a0[q].reduce(mc);
                 if (m < k) r0 = addmod(r0, shoup(J.c0[(long long)m * N + src], pq.v[m], pq.sh[m], mc.q), mc.q);
                 J.out[(long long)m * N + x] = r0;
-                J.out[((long long)E + m) * N + x] = a1[q].reduce(mc);
+                u64 r1 = a1[q].reduce(mc);
+                if (m < k && J.c1_add) r1 = addmod(r1, shoup(J.c1_add[(long long)m * N + src], pq.v[m], pq.sh[m], mc.q), mc.q);
+                J.out[((long long)E + m) * N + x] = r1;
             } else {
                 u[(((long long)t * 2 + 0) * E + m) * N + x] = a0[q].reduce(mc);
                 u[(((long long)t * 2 + 1) * E + m) * N + x] = a1[q].reduce(mc);
@@ -427,6 +429,8 @@ blb_status blb_launch_tensor(const blb_params *P, const u64 *a, const u64 *b, u6
 
 // ============================================================ launchers
 extern "C" u64 blbh_shoup(u64 w, u64 q);
+extern "C" u64 blbh_mulmod(u64 a, u64 b, u64 q);
+extern "C" u64 blbh_invmod(u64 a, u64 q);
 static u64 blbh_shoup_dev_table(const blb_params *P, int i) { return blbh_shoup(P->P_mod_q[i], P->mod[i]); }
 
 ChachaKey chacha_key_from_bytes(const uint8_t seed[32]) {
@@ -609,6 +613,156 @@ blb_status launch_moddown(const blb_params *P, int level, u64 *u, int n, u64 *ou
         KsJobs J{};
         for (int t = 0; t < cnt; t++) {
             J.j[t].out = out + (size_t)(t0 + t) * 2 * k * N;
+            J.j[t].add_mode = 0;
+            J.j[t].galois = 1;
+        }
+        BLB_TRY(moddown_launch(P, level, J, cnt, u + (size_t)t0 * 2 * E * N, conv, st));
+    }
+    return BLB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// ModDown fused with rescale (reading C17): y = round(X / M), M = q_l * p_0 ... (odd: no ties),
+// y = (X + h - r) / M with h = (M - 1) / 2 and r = (X + h) mod M rebuilt exactly from the
+// residues at the M-moduli by Garner's mixed radix (digits d_t < m_t), reduced mod q_i by Horner.
+// ---------------------------------------------------------------------------
+constexpr int kMdrMax = 4;
+struct MdrTab {
+    int nd;
+    ModConst md[kMdrMax];                          // m_0 = q_l, m_1.. = p_0..
+    u64 hd[kMdrMax];                               // h mod m_t = (m_t - 1) / 2
+    u64 gi[kMdrMax][kMdrMax], gish[kMdrMax][kMdrMax];  // m_s^{-1} mod m_t (s < t), Shoup
+    u64 mq[kMdrMax][BLB_MAXP], mqsh[kMdrMax][BLB_MAXP];  // m_t mod q_i, Shoup
+    u64 hq[BLB_MAXP];                              // h mod q_i
+};
+// u: [2n][E][N], limbs k-1 .. E-1 (q_l, P) already INTT'd in place;  conv [2n][level][N] = (r - h) mod q_i
+__global__ void k_mdr_lift(const u64 *u, u64 *conv, MdrTab T, Primes pr, int k, int E, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int pp = blockIdx.z;
+    if (x >= N) return;
+    const int level = k - 1;
+    const u64 *base = u + ((long long)pp * E + level) * N + x;
+    u64 d[kMdrMax];
+#pragma unroll
+    for (int t = 0; t < kMdrMax; t++) {
+        if (t >= T.nd) break;
+        const u64 mt = T.md[t].q;
+        u64 v = base[(long long)t * N] + T.hd[t];
+        if (v >= mt) v -= mt;
+#pragma unroll
+        for (int s2 = 0; s2 < kMdrMax; s2++) {
+            if (s2 >= t) break;
+            v = submod(v, mod64(d[s2], T.md[t]), mt);
+            v = shoup(v, T.gi[s2][t], T.gish[s2][t], mt);
+        }
+        d[t] = v;
+    }
+    for (int i = 0; i < level; i++) {
+        const ModConst &mc = pr.m[i];
+        u64 r = mod64(d[T.nd - 1], mc);
+        for (int t = T.nd - 2; t >= 0; t--) r = addmod(shoup(r, T.mq[t][i], T.mqsh[t][i], mc.q), mod64(d[t], mc), mc.q);
+        conv[((long long)pp * level + i) * N + x] = submod(r, T.hq[i], mc.q);
+    }
+}
+// out_i = (u_i - NTT(conv)_i) * M^{-1}  (generic-N path; N = 2^16 fuses this into the NTT epilogue)
+__global__ void k_mdr_combine(const u64 *u, const u64 *conv, KsJobs J, PinvTab mi, Primes pr, int level, int E,
+                              int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int l = blockIdx.y, pp = blockIdx.z;
+    if (x >= N) return;
+    const u64 q = pr.m[l].q;
+    const u64 v = submod(u[((long long)pp * E + l) * N + x], conv[((long long)pp * level + l) * N + x], q);
+    J.j[pp >> 1].out[((long long)(pp & 1) * level + l) * N + x] = shoup(v, mi.v[l], mi.sh[l], q);
+}
+
+// u [n][2][E][N] (modified: its q_l and P limbs are INTT'd in place) -> outs[t] [2][level][N]
+blb_status launch_moddown_rescale(const blb_params *P, int level, u64 *u, int n, u64 *const *outs, u64 *conv,
+                                  cudaStream_t st) {
+    if (n <= 0) return BLB_OK;
+    const int N = P->N, k = level + 1, np = P->np, E = k + np, nd = 1 + np;
+    if (level < 1 || nd > kMdrMax) {
+        blb_set_error("moddown_rescale: level %d / %d special primes unsupported", level, np);
+        return BLB_E_INVALID_ARG;
+    }
+    MdrTab T{};
+    T.nd = nd;
+    u64 m[kMdrMax];
+    for (int t = 0; t < nd; t++) {
+        m[t] = t == 0 ? P->mod[level] : P->mod[P->K + t - 1];
+        T.md[t] = P->pr.m[t == 0 ? level : P->K + t - 1];
+        T.hd[t] = (m[t] - 1) / 2;
+    }
+    for (int t = 0; t < nd; t++)
+        for (int s2 = 0; s2 < t; s2++) {
+            T.gi[s2][t] = blbh_invmod(m[s2] % m[t], m[t]);
+            T.gish[s2][t] = blbh_shoup(T.gi[s2][t], m[t]);
+        }
+    PinvTab mi{};
+    for (int i = 0; i < level; i++) {
+        const u64 qi = P->mod[i];
+        u64 Mq = 1;
+        for (int t = 0; t < nd; t++) {
+            T.mq[t][i] = m[t] % qi;
+            T.mqsh[t][i] = blbh_shoup(T.mq[t][i], qi);
+            Mq = blbh_mulmod(Mq, T.mq[t][i], qi);
+        }
+        T.hq[i] = blbh_mulmod((Mq + qi - 1) % qi, blbh_invmod(2, qi), qi);
+        mi.v[i] = blbh_invmod(Mq, qi);
+        mi.sh[i] = blbh_shoup(mi.v[i], qi);
+    }
+    for (int t0 = 0; t0 < n; t0 += kMaxJobs) {
+        const int cnt = n - t0 < kMaxJobs ? n - t0 : kMaxJobs;
+        u64 *ub = u + (size_t)t0 * 2 * E * N;
+        RowBatch rb{};
+        rb.base = ub; rb.poly_stride = (long long)E * N; rb.n_polys = 2 * cnt; rb.limbs = nd; rb.limb0 = level;
+        for (int t = 0; t < nd; t++) rb.prime[t] = t == 0 ? level : P->K + t - 1;
+        BLB_TRY(launch_ntt(P, rb, true, st));
+        k_mdr_lift<<<grid_x(N, 1, 2 * cnt), kTB, 0, st>>>(ub, conv, T, P->pr, k, E, N);
+        BLB_COUNT_LAUNCH(1);
+        BLB_CHECK_LAUNCH();
+        KsJobs J{};
+        for (int t = 0; t < cnt; t++) {
+            J.j[t].out = outs[t0 + t];
+            J.j[t].add_mode = 0;
+            J.j[t].galois = 1;
+        }
+        RowBatch cb{};
+        cb.base = conv; cb.poly_stride = (long long)level * N; cb.n_polys = 2 * cnt; cb.limbs = level; cb.limb0 = 0;
+        for (int i = 0; i < level; i++) cb.prime[i] = i;
+        if (P->logN == 16 && P->fuse) {
+            NttFuse fz{};
+            fz.epi = 1;
+            fz.u = ub;
+            fz.E = E;
+            fz.k = level;
+            fz.pinv = mi;
+            fz.jobs = J;
+            BLB_TRY(launch_ntt_fused(P, cb, false, fz, st));
+        } else {
+            BLB_TRY(launch_ntt(P, cb, false, st));
+            k_mdr_combine<<<grid_x(N, level, 2 * cnt), kTB, 0, st>>>(ub, conv, J, mi, P->pr, level, E, N);
+            BLB_COUNT_LAUNCH(1);
+            BLB_CHECK_LAUNCH();
+        }
+    }
+    BLB_COUNT(4, n);
+    return BLB_OK;
+}
+blb_status launch_moddown_rescale(const blb_params *P, int level, u64 *u, int n, u64 *out, u64 *conv,
+                                  cudaStream_t st) {
+    std::vector<u64 *> o(n);
+    for (int t = 0; t < n; t++) o[t] = out + (size_t)t * 2 * level * P->N;
+    return launch_moddown_rescale(P, level, u, n, o.data(), conv, st);
+}
+// ModDown of n extended ciphertexts into separate outputs
+blb_status launch_moddown(const blb_params *P, int level, u64 *u, int n, u64 *const *outs, u64 *conv,
+                          cudaStream_t st) {
+    const int N = P->N, k = level + 1, E = k + P->np;
+    for (int t0 = 0; t0 < n; t0 += kMaxJobs) {
+        const int cnt = n - t0 < kMaxJobs ? n - t0 : kMaxJobs;
+        KsJobs J{};
+        for (int t = 0; t < cnt; t++) {
+            J.j[t].out = outs[t0 + t];
             J.j[t].add_mode = 0;
             J.j[t].galois = 1;
         }

@@ -593,7 +593,7 @@ extern "C" blb_status blb_matmul_encode_weights(const blb_matmul_plan *pl, const
 
 // workspace layout (u64 elements)
 struct MatmulWs {
-    size_t ext_in, coef, R, ks, acc, gext, gcoef, gks, rot, yext, ymd, resc, total;
+    size_t ext_in, coef, R, ks, acc, gext, gcoef, gks, rot, yext, resc, total;
 };
 static MatmulWs matmul_ws(const blb_matmul_plan *pl, int out_count) {
     const blb_params *P = pl->P;
@@ -610,7 +610,6 @@ static MatmulWs matmul_ws(const blb_matmul_plan *pl, int out_count) {
     w.gks = o; o += keyswitch_scratch_elems(P, pl->level, kMaxJobs);
     w.rot = o; o += (size_t)kMaxJobs * 2 * E * N;
     w.yext = o; o += (size_t)out_count * 2 * E * N;
-    w.ymd = o; o += (size_t)out_count * 2 * k * N;
     w.resc = o; o += (2 + 2 * k) * N;
     w.total = o;
     return w;
@@ -663,7 +662,7 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
     u64 *W = (u64 *)ws;
     u64 *ext_in = W + w.ext_in, *coef = W + w.coef, *R = W + w.R, *ks = W + w.ks, *acc = W + w.acc;
     u64 *gext = W + w.gext, *rot = W + w.rot, *resc = W + w.resc, *gcoef = W + w.gcoef;
-    u64 *yext = W + w.yext, *ymd = W + w.ymd;
+    u64 *yext = W + w.yext;
     u64 *gks_conv = W + w.gks + (size_t)kMaxJobs * 2 * E * N;
     const size_t ctN = (size_t)2 * k * N;
     u64 *ks_u = ks, *ks_conv = ks + (size_t)kMaxJobs * 2 * E * N;
@@ -793,14 +792,16 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
             BLB_COUNT_LAUNCH(1);
             BLB_CHECK_LAUNCH();
         }
-        if (n_y > 0) BLB_TRY(launch_moddown(P, level, yext, n_y, ymd, gks_conv, sa));
-        // rescale the chunk's outputs (outputs without giant steps: ModDown(lift(x)) = x exactly)
+        // ModDown + rescale as one exact rounding (reading C17); outputs without giant steps are
+        // rescaled directly (round(P x / (q_l P)) = round(x / q_l), pinned in the oracle tests)
+        std::vector<u64 *> youts;
         for (int t = c0; t < c0 + cn; t++) {
-            const u64 *src = yslot[t - c0] >= 0 ? ymd + (size_t)yslot[t - c0] * ctN : acc + (size_t)t * pl->G * ctN;
-            BLB_TRY(launch_rescale(P, src, level, 2, out[t].data, resc, sa));
+            if (yslot[t - c0] >= 0) youts.push_back(out[t].data);
+            else BLB_TRY(launch_rescale(P, acc + (size_t)t * pl->G * ctN, level, 2, out[t].data, resc, sa));
             out[t].level = level - 1;
             out[t].scale = in[0].scale;  // Delta * q_level / q_level, exact (reading S6)
         }
+        if (n_y > 0) BLB_TRY(launch_moddown_rescale(P, level, yext, n_y, youts.data(), gks_conv, sa));
     }
     if (ovl) {
         cudaEvent_t e = next_event();

@@ -127,13 +127,13 @@ struct SumList {
     int n;
     const u64 *src[64];
 };
-// out = sum of the listed ciphertexts ([2][k][N] each)
-__global__ void k_sum_list(SumList sl, u64 *out, Primes pr, int k, int N) {
+// out = sum of the listed ciphertexts ([2][k][N] each; limbs l >= kq are special primes K + l - kq)
+__global__ void k_sum_list(SumList sl, u64 *out, Primes pr, int k, int N, int kq, int K) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int l = blockIdx.y, p = blockIdx.z;
     if (x >= N) return;
     const long long off = ((long long)p * k + l) * N + x;
-    const u64 q = pr.m[l].q;
+    const u64 q = pr.m[l < kq ? l : K + (l - kq)].q;
     u64 acc = 0;
     for (int t = 0; t < sl.n; t++) acc = addmod(acc, sl.src[t][off], q);
     out[off] = acc;
@@ -327,7 +327,7 @@ extern "C" blb_status blb_qk_plan_rotations(const blb_qk_plan *pl, int32_t *step
 static size_t qk_mask_elems(const blb_qk_plan *pl) {
     const size_t N = pl->P->N;
     // stage-1 masks over the extended basis Q_l u P (double hoisting), stage-3 masks over Q_{l-2}
-    return pl->m1.size() * (size_t)(pl->level + 1 + pl->P->np) * N + pl->m3.size() * (size_t)(pl->level - 1) * N;
+    return pl->m1.size() * (size_t)(pl->level + 1 + pl->P->np) * N + pl->m3.size() * (size_t)(pl->level - 1 + pl->P->np) * N;
 }
 extern "C" size_t blb_qk_mask_bytes(const blb_qk_plan *pl) { return pl ? qk_mask_elems(pl) * sizeof(u64) : 0; }
 
@@ -349,7 +349,7 @@ extern "C" blb_status blb_qk_encode_masks(const blb_qk_plan *pl, uint64_t *masks
         const MaskDesc *dm = stage == 0 ? pl->d_m1 : pl->d_m3;
         const int cnt_all = (int)(stage == 0 ? pl->m1.size() : pl->m3.size());
         const int lvl = stage == 0 ? pl->level : pl->level - 2;
-        const int npx = stage == 0 ? P->np : 0;
+        const int npx = P->np;  // both stages act on extended-basis (Q u P) rotations (C13)
         u64 *base = masks + (stage == 0 ? 0 : pl->m1.size() * (size_t)(pl->level + 1 + P->np) * P->N);
         for (int m0 = 0; m0 < cnt_all && s == BLB_OK; m0 += chunk) {
             const int cnt = std::min(chunk, cnt_all - m0);
@@ -368,12 +368,12 @@ extern "C" blb_status blb_qk_encode_masks(const blb_qk_plan *pl, uint64_t *masks
 
 // workspace layout
 struct QKWs {
-    size_t kr, qr, kacc, kmd, kp, qacc, qmd, qp, d, s, sr, t, aacc, ar, arot, ext, coef, ks, resc, total;
+    size_t kr, qr, kacc, kp, qacc, qp, d, s, sr, t, aacc, ar, arot, oext, ext, coef, ks, resc, total;
 };
 static QKWs qk_ws(const blb_qk_plan *pl) {
     const blb_params *P = pl->P;
     const size_t N = P->N, k = pl->level + 1, k1 = k - 1, k2 = k - 2, k3 = k - 3;
-    const size_t E = k + P->np, beta = blb_beta(P, pl->level);
+    const size_t np = P->np, E = k + np, E1 = k1 + np, E2 = k2 + np, E3 = k3 + np, beta = blb_beta(P, pl->level);
     const size_t J = pl->J, B = pl->B, G = pl->G, NA = pl->accs.size();
     const size_t NKR = 1 + pl->k_rots.size(), NQR = pl->q_rots.size();
     QKWs w{};
@@ -382,18 +382,17 @@ static QKWs qk_ws(const blb_qk_plan *pl) {
     w.kr = o; o += J * NKR * 2 * E * N;
     w.qr = o; o += J * std::max<size_t>(NQR, 1) * 2 * E * N;
     w.kacc = o; o += B * J * 2 * E * N;
-    w.kmd = o; o += B * J * 2 * k * N;
     w.kp = o; o += B * J * 2 * k1 * N;
     w.qacc = o; o += (G > 1 ? (G - 1) : 1) * J * 2 * E * N;
-    w.qmd = o; o += (G > 1 ? (G - 1) : 1) * J * 2 * k * N;
     w.qp = o; o += G * J * 2 * k1 * N;
     w.d = o; o += G * B * 3 * k1 * N;
-    w.s = o; o += G * B * 2 * k1 * N;
+    w.s = o; o += G * B * 2 * E1 * N;      // relinearised products in Q u P (C17)
     w.sr = o; o += G * B * 2 * k2 * N;
-    w.t = o; o += G * B * 2 * k2 * N;
-    w.aacc = o; o += NA * 2 * k2 * N;
+    w.t = o; o += G * B * 2 * E2 * N;      // step-3 rotations in Q u P (double hoisting)
+    w.aacc = o; o += NA * 2 * E2 * N;
     w.ar = o; o += NA * 2 * k3 * N;
-    w.arot = o; o += NA * 2 * k3 * N;
+    w.arot = o; o += NA * 2 * E3 * N;      // final rotations in Q u P
+    w.oext = o; o += (size_t)(pl->L / pl->g) * 2 * E3 * N;
     w.ext = o; o += (size_t)kMaxJobs * beta * E * N;
     w.coef = o; o += (size_t)kMaxJobs * k * N;
     w.ks = o; o += keyswitch_scratch_elems(P, pl->level, kMaxJobs);
@@ -410,12 +409,11 @@ static const u64 *key_for(const blb_keys *K, uint32_t g) {
     return nullptr;
 }
 
-// rotations of independent inputs (each its own ModUp), <= kMaxJobs per launch group
-static blb_status rotate_independent(const blb_params *P, const blb_keys *keys, int level, const std::vector<const u64 *> &in,
-                                     const std::vector<int32_t> &steps, const std::vector<u64 *> &out, u64 *ext, u64 *coef,
-                                     u64 *ks, cudaStream_t st) {
+// rotations of independent inputs (each its own ModUp) kept in Q u P: out[t] [2][E][N]
+static blb_status rotate_independent_ext(const blb_params *P, const blb_keys *keys, int level,
+                                         const std::vector<const u64 *> &in, const std::vector<int32_t> &steps,
+                                         const std::vector<u64 *> &out, u64 *ext, u64 *coef, cudaStream_t st) {
     const int k = level + 1, N = P->N, E = k + P->np, beta = blb_beta(P, level);
-    u64 *ks_u = ks, *ks_conv = ks + (size_t)kMaxJobs * 2 * E * N;
     for (size_t t0 = 0; t0 < in.size(); t0 += kMaxJobs) {
         const int cnt = (int)std::min<size_t>(kMaxJobs, in.size() - t0);
         std::vector<const u64 *> c1(cnt);
@@ -429,11 +427,10 @@ static blb_status rotate_independent(const blb_params *P, const blb_keys *keys, 
             J.c0 = in[t0 + t];
             J.out = out[t0 + t];
             J.galois = g;
-            J.add_mode = 1;
             jobs[t] = J;
         }
         BLB_TRY(launch_modup(P, level, c1.data(), cnt, ext, coef, st));
-        BLB_TRY(launch_keyswitch(P, level, jobs.data(), cnt, ks_u, ks_conv, st));
+        BLB_TRY(launch_keyswitch_ext(P, level, jobs.data(), cnt, st));
     }
     return BLB_OK;
 }
@@ -508,8 +505,7 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
     }
     BLB_TRY(launch_mac(P, m1, W + w.kr, W + w.kacc, E + pl->off_kp_r, E + pl->off_kp_pt, E + pl->off_kp_start, 0, 0,
                        B * J, (int)pl->kp_r.size(), Ex, st, k));
-    BLB_TRY(launch_moddown(P, lvl, W + w.kacc, B * J, W + w.kmd, conv, st));
-    BLB_TRY(launch_rescale(P, W + w.kmd, lvl, 2 * B * J, W + w.kp, W + w.resc, st));
+    BLB_TRY(launch_moddown_rescale(P, lvl, W + w.kacc, B * J, W + w.kp, conv, st));  // C17
     // 2. giant side: Q_0 = level drop, Q_u = ModDown(MAC(masks, Rot_ext(Q))), rescale
     for (int j = 0; j < J; j++) {
         if (NQR) BLB_TRY(rotate_ext_all(Q[j].data, pl->q_rots, W + w.qr + (size_t)j * NQR * ct_e));
@@ -519,17 +515,17 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
     if (G > 1) {
         BLB_TRY(launch_mac(P, m1, W + w.qr, W + w.qacc, E + pl->off_qp_r, E + pl->off_qp_pt, E + pl->off_qp_start, 0, 0,
                            (G - 1) * J, (int)pl->qp_r.size(), Ex, st, k));
-        BLB_TRY(launch_moddown(P, lvl, W + w.qacc, (G - 1) * J, W + w.qmd, conv, st));
-        BLB_TRY(launch_rescale(P, W + w.qmd, lvl, 2 * (G - 1) * J, W + w.qp + (size_t)J * ct_k1, W + w.resc, st));
+        BLB_TRY(launch_moddown_rescale(P, lvl, W + w.qacc, (G - 1) * J, W + w.qp + (size_t)J * ct_k1, conv, st));
     }
     // 3. products summed over j, relinearisation (one per (u, i)), rescale
     k_tensor_sum<<<gx(N, k1, G * B), kTB, 0, st>>>(W + w.qp, W + w.kp, W + w.d, P->pr, J, B, k1, N);
     BLB_COUNT_LAUNCH(1);
     BLB_COUNT(3, (size_t)G * B * J);
     BLB_CHECK_LAUNCH();
+    // relinearisation kept in Q u P: (P d0 + u0, P d1 + u1), then ModDown + rescale (C17)
+    const int E1 = k1 + P->np, E2 = k2 + P->np, E3 = k3 + P->np;
     {
-        const int E1 = k1 + P->np, beta1 = blb_beta(P, lvl - 1);
-        u64 *ks_u = W + w.ks, *ks_conv = W + w.ks + (size_t)kMaxJobs * 2 * E1 * N;
+        const int beta1 = blb_beta(P, lvl - 1);
         for (int o0 = 0; o0 < G * B; o0 += kMaxJobs) {
             const int cnt = std::min(kMaxJobs, G * B - o0);
             std::vector<const u64 *> d2(cnt);
@@ -542,17 +538,16 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
                 Jb.key = rlk;
                 Jb.c0 = D;
                 Jb.c1_add = D + (size_t)k1 * N;
-                Jb.out = W + w.s + (size_t)(o0 + t) * ct_k1;
+                Jb.out = W + w.s + (size_t)(o0 + t) * 2 * E1 * N;
                 Jb.galois = 1;
-                Jb.add_mode = 2;
                 jobs[t] = Jb;
             }
             BLB_TRY(launch_modup(P, lvl - 1, d2.data(), cnt, W + w.ext, W + w.coef, st));
-            BLB_TRY(launch_keyswitch(P, lvl - 1, jobs.data(), cnt, ks_u, ks_conv, st));
+            BLB_TRY(launch_keyswitch_ext(P, lvl - 1, jobs.data(), cnt, st));
         }
     }
-    BLB_TRY(launch_rescale(P, W + w.s, lvl - 1, 2 * G * B, W + w.sr, W + w.resc, st));
-    // 4. step 3: T_ui = Rot_{-i H_p L}(S_ui)
+    BLB_TRY(launch_moddown_rescale(P, lvl - 1, W + w.s, G * B, W + w.sr, conv, st));
+    // 4. step 3: T_ui = Rot_{-i H_p L}(S_ui) kept in Q u P (double hoisting); i = 0 is the lift
     {
         std::vector<const u64 *> in;
         std::vector<int32_t> steps;
@@ -560,46 +555,51 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
         for (int i = 0; i < B; i++)          // i-major: the G rotations by the same step share a key
             for (int u = 0; u < G; u++) {
                 const size_t o = (size_t)(u * B + i);
+                u64 *dst = W + w.t + o * 2 * E2 * N;
                 if (i == 0) {
-                    cudaMemcpyAsync(W + w.t + o * ct_k2, W + w.sr + o * ct_k2, ct_k2 * sizeof(u64),
-                                    cudaMemcpyDeviceToDevice, st);
+                    BLB_TRY(launch_lift_ext(P, lvl - 2, W + w.sr + o * ct_k2, dst, st));
                     continue;
                 }
                 in.push_back(W + w.sr + o * ct_k2);
                 steps.push_back(-i * pl->Hp * pl->L);
-                outp.push_back(W + w.t + o * ct_k2);
+                outp.push_back(dst);
             }
-        BLB_TRY(rotate_independent(P, keys, lvl - 2, in, steps, outp, W + w.ext, W + w.coef, W + w.ks, st));
+        BLB_TRY(rotate_independent_ext(P, keys, lvl - 2, in, steps, outp, W + w.ext, W + w.coef, st));
     }
     // 5. step-3 masks (MAC into the accumulators), rescale, deferred giant rotations, sums
     BLB_TRY(launch_mac(P, m3, W + w.t, W + w.aacc, E + pl->off_a_r, E + pl->off_a_pt, E + pl->off_a_start, 0, 0, NA,
-                       (int)pl->a_r.size(), k2, st));
-    BLB_TRY(launch_rescale(P, W + w.aacc, lvl - 2, 2 * NA, W + w.ar, W + w.resc, st));
+                       (int)pl->a_r.size(), E2, st, k2));
+    BLB_TRY(launch_moddown_rescale(P, lvl - 2, W + w.aacc, NA, W + w.ar, conv, st));  // C17
+    // deferred giant rotations kept in Q u P, summed per output, one ModDown per output
     {
         std::vector<const u64 *> in;
         std::vector<int32_t> steps;
         std::vector<u64 *> outp;
         for (int a = 0; a < NA; a++) {
             const int r = pl->accs[a].rot;
-            if (((r % pl->n) + pl->n) % pl->n == 0) continue;
+            u64 *dst = W + w.arot + (size_t)a * 2 * E3 * N;
+            if (((r % pl->n) + pl->n) % pl->n == 0) {
+                BLB_TRY(launch_lift_ext(P, lvl - 3, W + w.ar + (size_t)a * ct_k3, dst, st));
+                continue;
+            }
             in.push_back(W + w.ar + (size_t)a * ct_k3);
             steps.push_back(r);
-            outp.push_back(W + w.arot + (size_t)a * ct_k3);
+            outp.push_back(dst);
         }
-        BLB_TRY(rotate_independent(P, keys, lvl - 3, in, steps, outp, W + w.ext, W + w.coef, W + w.ks, st));
+        BLB_TRY(rotate_independent_ext(P, keys, lvl - 3, in, steps, outp, W + w.ext, W + w.coef, st));
     }
     const int n_out = pl->L / pl->g;
+    std::vector<u64 *> outs(n_out);
     for (int o = 0; o < n_out; o++) {
         if (!out[o].data) return BLB_E_INVALID_ARG;
+        outs[o] = out[o].data;
         SumList sl{};
         for (int a = 0; a < NA; a++) {
             if (pl->accs[a].out != o) continue;
-            const int r = pl->accs[a].rot;
-            const bool rotated = ((r % pl->n) + pl->n) % pl->n != 0;
             if (sl.n >= 64) return BLB_E_LAYOUT;
-            sl.src[sl.n++] = (rotated ? W + w.arot : W + w.ar) + (size_t)a * ct_k3;
+            sl.src[sl.n++] = W + w.arot + (size_t)a * 2 * E3 * N;
         }
-        k_sum_list<<<gx(N, k3, 2), kTB, 0, st>>>(sl, out[o].data, P->pr, k3, N);
+        k_sum_list<<<gx(N, E3, 2), kTB, 0, st>>>(sl, W + w.oext + (size_t)o * 2 * E3 * N, P->pr, E3, N, k3, P->K);
         BLB_COUNT_LAUNCH(1);
         out[o].level = lvl - 3;
         // scale bookkeeping in the same floating-point order as the oracle: the masks
@@ -612,6 +612,7 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
         const double sk = (K[0].scale * ql) / ql;
         out[o].scale = (((sq * sk) / ql1) * ql2) / ql2;
     }
+    BLB_TRY(launch_moddown(P, lvl - 3, W + w.oext, n_out, outs.data(), conv, st));
     BLB_CHECK_LAUNCH();
     return BLB_OK;
 }

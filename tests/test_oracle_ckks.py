@@ -368,3 +368,33 @@ def test_extended_basis_identities(toy, toy_keys):
         q0, p0 = int(toy.mods[0]), int(toy.mods[O.ext_pidx(toy, lvl)[lvl + 1]])
         cq = [int(v) if int(v) < q0 // 2 else int(v) - q0 for v in coef_q]
         assert all((c - int(v)) % p0 == 0 for c, v in zip(cq, coef_p))
+
+
+@pytest.mark.parametrize("lvl", [1, 2])
+def test_moddown_rescale_is_exact_rounding(mid, lvl):
+    """C17: out == round(X / (q_l P)) mod q_i for every coefficient, X the CRT integer of the
+    input over Q_l u P (big-integer CRT, independent of the oracle's Garner code); np = 2 here."""
+    rng = np.random.default_rng(30 + lvl)
+    k = lvl + 1
+    pidx = list(range(k)) + [mid.K + t for t in range(mid.np_)]
+    mods = [mid.mods[i] for i in pidx]
+    y = np.stack([np.stack([rng.integers(0, m, mid.N, dtype=np.uint64) for m in mods]) for _ in range(2)])
+    out = O.moddown_rescale(mid, O.CtExt(y, lvl, 1.0))
+    assert out.level == lvl - 1 and out.data.shape == (2, lvl, mid.N)
+    M = int(mid.mods[lvl]) * mid.P()
+    for p in range(2):
+        ycoef = mid.intt(y[p], pidx)
+        ocoef = mid.intt(out.data[p], list(range(lvl)))
+        for x in list(range(0, mid.N, 37)) + [mid.N - 1]:
+            X, _ = crt([ycoef[m, x] for m in range(len(pidx))], mods)
+            want = (X + (M - 1) // 2) // M
+            assert all(int(ocoef[i, x]) == want % int(mid.mods[i]) for i in range(lvl))
+
+
+def test_moddown_rescale_of_lift_is_rescale(toy, toy_keys):
+    """round(P x / (q_l P)) = round(x / q_l): on the step-0 lift C17 reduces to C10 exactly."""
+    z = np.random.default_rng(23).uniform(-1, 1, toy.n)
+    ct = enc(toy, toy_keys, z, 9)
+    got = O.moddown_rescale(toy, O.rotate_ext(toy, ct, toy_keys, 0))
+    want = O.rescale(toy, ct)
+    assert np.array_equal(got.data, want.data) and got.scale == want.scale and got.level == want.level
