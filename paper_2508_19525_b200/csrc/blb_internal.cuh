@@ -182,6 +182,7 @@ struct blb_params {
     u64 psi[BLB_MAXP];
     Primes pr;                    // by-value copy for kernel args
     u64 *d_tw = nullptr;          // [K+np][2][N][2]: (fwd, fwd Shoup), (inv, inv Shoup) pairs, bit-reversed order
+    u64 *d_tw16 = nullptr;        // same, companion = bits of double(w / q) for primes < 2^41 (ntt16_pass)
     double *d_zeta = nullptr;     // [N][4]: zeta^{brv(i)} as (re_hi, re_lo, im_hi, im_lo)
     int32_t *d_slot_pos = nullptr; // [N/2]: NTT-domain position k of slot j (brv(k) = (5^j - 1)/2)
     // FastBConv tables, see bconv_* in kernels.cu

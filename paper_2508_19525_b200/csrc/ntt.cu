@@ -129,20 +129,56 @@ __device__ __forceinline__ void bfly(u64 &X, u64 &Y, u64 w, u64 wsh, u64 q, u64 
     }
 }
 
+// ---------------------------------------------------------------------------
+// FP64 butterflies for the primes < 2^41 (4 of the 5 BERT chain primes).  The B200 FP64 pipe
+// (64 DFMA/clk/SM) is separate from the fma-heavy pipe that the 64-bit integer multiplies of
+// the Shoup butterfly saturate, and residues < 2^41 with their lazy growth stay exact integers
+// in a double.  y * w mod q = (p - c q) + e with p = fl(y w), e = y w - p (exact, one fma),
+// c = round(y fl(w / q)) (one fma against 1.5 * 2^52): |c - y w / q| < 3/4, so the remainder
+// lies in (-3q/4, 3q/4) and every step is exact.  Values are signed and unreduced: forward
+// |x| grows by < q per stage (< 13 q after 16 stages), inverse sums double per stage and are
+// re-centred between the two passes, so all inputs stay below 2^50.
+// ---------------------------------------------------------------------------
+constexpr double kTwo52 = 4503599627370496.0, kMagic = 6755399441055744.0;  // 2^52, 1.5 * 2^52
+__device__ __forceinline__ double u2d(u64 x) {  // x < 2^52
+    return __dsub_rn(__hiloint2double(0x43300000 | (int)(x >> 32), (int)(uint32_t)x), kTwo52);
+}
+__device__ __forceinline__ double mulr(double y, double w, double wq, double q) {
+    const double p = __dmul_rn(y, w);
+    const double e = __fma_rn(y, w, -p);
+    const double c = __dsub_rn(__fma_rn(y, wq, kMagic), kMagic);
+    return __dadd_rn(__fma_rn(-c, q, p), e);
+}
+__device__ __forceinline__ double centre(double x, double q, double qinv) {  // x - round(x / q) q
+    const double c = __dsub_rn(__fma_rn(x, qinv, kMagic), kMagic);
+    return __fma_rn(-c, q, x);
+}
+__device__ __forceinline__ u64 canon(double x, double q, double qinv) {  // x mod q in [0, q)
+    double r = centre(x, q, qinv);
+    if (r < 0.0) r = __dadd_rn(r, q);
+    if (r >= q) r = __dsub_rn(r, q);
+    return (u64)__double_as_longlong(__dadd_rn(r, kTwo52)) & 0x000FFFFFFFFFFFFFull;
+}
+template <bool INV>
+__device__ __forceinline__ void bfly_f64(double &X, double &Y, double w, double wq, double q) {
+    if (!INV) {
+        const double r = mulr(Y, w, wq, q), x = X;
+        X = __dadd_rn(x, r);
+        Y = __dsub_rn(x, r);
+    } else {
+        const double s = __dadd_rn(X, Y), d = __dsub_rn(X, Y);
+        X = s;
+        Y = mulr(d, w, wq, q);
+    }
+}
+
 #ifndef BLB_NTT_MINB
 #define BLB_NTT_MINB 2
 #endif
-template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0>
-__global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, const u64 *__restrict__ tw_all, Primes pr, int s0,
-                                                  int last, const NttFuse fz) {
-    __shared__ u64 sm[16 * 256];
+template <bool INV, bool STRIDED, int PRO, int EPI, bool SMALL>
+__device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u64 *__restrict__ tw_all,
+                                           const Primes &pr, int s0, int last, const NttFuse &fz, int p, int l) {
     constexpr int logN = 16, N = 1 << logN;
-    const int row = blockIdx.y;
-    const int p = row / rb.limbs, l = row - p * rb.limbs;
-    if (rb.skip_alpha) {
-        const int dig = p % rb.skip_beta;
-        if (l < rb.skip_kmax && l >= dig * rb.skip_alpha && l < (dig + 1) * rb.skip_alpha) return;
-    }
     u64 *a = rb.base + (long long)p * rb.poly_stride + (long long)(rb.limb0 + l) * N;
     const int pi = rb.prime[l];
     const u64 q = pr.m[pi].q, q2 = 2 * q;
@@ -157,7 +193,22 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, con
     const int colB = t >> 4, tcB = t & 15;
     const int hA = STRIDED ? 0 : (c0 + colA);
     const int hB = STRIDED ? 0 : (c0 + colB);
-    u64 v[16];
+    // SMALL (q < 2^41): values are doubles; between the two passes they are stored as double bits
+    using V = typename std::conditional<SMALL, double, u64>::type;
+    const double qd = (double)q, qinv = 1.0 / qd;
+    V v[16];
+    auto from_u64 = [&](u64 x) -> V {
+        if constexpr (SMALL) return u2d(x);
+        else return x;
+    };
+    auto to_bits = [&](V x) -> u64 {
+        if constexpr (SMALL) return (u64)__double_as_longlong(x);
+        else return x;
+    };
+    auto from_bits = [&](u64 x) -> V {
+        if constexpr (SMALL) return __longlong_as_double((long long)x);
+        else return x;
+    };
     if (PRO == 1) {
         const u64 *src = fz.src + (long long)(p / fz.src_div) * fz.src_hi + (long long)(p % fz.src_div) * fz.src_lo;
         const ModConst &mt = pr.m[pi];
@@ -165,14 +216,14 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, con
         for (int m = 0; m < 16; m++) {
             const int mid = tcA + 16 * m;
             const size_t addr = STRIDED ? (((size_t)mid << 8) + c0 + colA) : (((size_t)(c0 + colA) << 8) + mid);
-            v[m] = mod64(src[addr], mt);
+            v[m] = from_u64(mod64(src[addr], mt));
         }
     } else {
 #pragma unroll
         for (int m = 0; m < 16; m++) {
             const int mid = tcA + 16 * m;
             const size_t addr = STRIDED ? (((size_t)mid << 8) + c0 + colA) : (((size_t)(c0 + colA) << 8) + mid);
-            v[m] = a[addr];
+            v[m] = last ? from_bits(a[addr]) : from_u64(a[addr]);  // second pass: the first pass's format
         }
     }
     auto roundA = [&](int r) {
@@ -183,7 +234,11 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, con
             if (m & dist) continue;
             const int widx = (1 << s) + (hA << r) + (m >> (4 - r));
             const ulonglong2 tv = twp[widx];
-            bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q2);
+            if constexpr (SMALL)
+                bfly_f64<INV>(v[m], v[m + dist], __longlong_as_double((long long)tv.x),
+                              __longlong_as_double((long long)tv.y), qd);
+            else
+                bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q2);
         }
     };
     auto roundB = [&](int r) {
@@ -194,7 +249,11 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, con
             if (m & dist) continue;
             const int widx = (1 << s) + (hB << r) + ((16 * tcB + m) >> (8 - r));
             const ulonglong2 tv = twp[widx];
-            bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q2);
+            if constexpr (SMALL)
+                bfly_f64<INV>(v[m], v[m + dist], __longlong_as_double((long long)tv.x),
+                              __longlong_as_double((long long)tv.y), qd);
+            else
+                bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q2);
         }
     };
     if (!INV) {
@@ -202,10 +261,10 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, con
         for (int r = 0; r < 4; r++) roundA(r);
     }
 #pragma unroll
-    for (int m = 0; m < 16; m++) sm[swz(colA, tcA + 16 * m)] = v[m];
+    for (int m = 0; m < 16; m++) sm[swz(colA, tcA + 16 * m)] = to_bits(v[m]);
     __syncthreads();
 #pragma unroll
-    for (int m = 0; m < 16; m++) v[m] = sm[swz(colB, 16 * tcB + m)];
+    for (int m = 0; m < 16; m++) v[m] = from_bits(sm[swz(colB, 16 * tcB + m)]);
     if (!INV) {
 #pragma unroll
         for (int r = 4; r < 8; r++) roundB(r);
@@ -215,10 +274,10 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, con
     }
     __syncthreads();
 #pragma unroll
-    for (int m = 0; m < 16; m++) sm[swz(colB, 16 * tcB + m)] = v[m];
+    for (int m = 0; m < 16; m++) sm[swz(colB, 16 * tcB + m)] = to_bits(v[m]);
     __syncthreads();
 #pragma unroll
-    for (int m = 0; m < 16; m++) v[m] = sm[swz(colA, tcA + 16 * m)];
+    for (int m = 0; m < 16; m++) v[m] = from_bits(sm[swz(colA, tcA + 16 * m)]);
     if (INV) {
 #pragma unroll
         for (int r = 3; r >= 0; r--) roundA(r);
@@ -232,9 +291,13 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, con
         const u64 pv = fz.pinv.v[l], psh = fz.pinv.sh[l];
 #pragma unroll
         for (int m = 0; m < 16; m++) {
-            u64 x = v[m];
-            if (x >= q2) x -= q2;
-            if (x >= q) x -= q;
+            u64 x;
+            if constexpr (SMALL) x = canon(v[m], qd, qinv);
+            else {
+                x = v[m];
+                if (x >= q2) x -= q2;
+                if (x >= q) x -= q;
+            }
             const int mid = tcA + 16 * m;
             const uint32_t gx = (uint32_t)((c0 + colA) << 8) + mid;
             u64 r = shoup(ui[gx] + q - x, pv, psh, q);
@@ -250,14 +313,20 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, con
     } else {
 #pragma unroll
         for (int m = 0; m < 16; m++) {
-            u64 x = v[m];
-            if (last) {
-                if (!INV) {
-                    if (x >= q2) x -= q2;
-                    if (x >= q) x -= q;
-                } else {
-                    x = shoup_lazy(x, mc.ninv, mc.ninv_sh, q);
-                    if (x >= q) x -= q;
+            u64 x;
+            if constexpr (SMALL) {
+                if (last) x = canon(INV ? mulr(v[m], (double)mc.ninv, (double)mc.ninv / qd, qd) : v[m], qd, qinv);
+                else x = to_bits(INV ? centre(v[m], qd, qinv) : v[m]);  // inverse sums re-centred for pass 2
+            } else {
+                x = v[m];
+                if (last) {
+                    if (!INV) {
+                        if (x >= q2) x -= q2;
+                        if (x >= q) x -= q;
+                    } else {
+                        x = shoup_lazy(x, mc.ninv, mc.ninv_sh, q);
+                        if (x >= q) x -= q;
+                    }
                 }
             }
             const int mid = tcA + 16 * m;
@@ -265,6 +334,20 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, con
             a[addr] = x;
         }
     }
+}
+
+template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0>
+__global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, const u64 *__restrict__ tw_all, Primes pr, int s0,
+                                                  int last, const NttFuse fz) {
+    __shared__ u64 sm[16 * 256];
+    const int row = blockIdx.y;
+    const int p = row / rb.limbs, l = row - p * rb.limbs;
+    if (rb.skip_alpha) {
+        const int dig = p % rb.skip_beta;
+        if (l < rb.skip_kmax && l >= dig * rb.skip_alpha && l < (dig + 1) * rb.skip_alpha) return;
+    }
+    if (pr.m[rb.prime[l]].q < (1ull << 41)) ntt16_body<INV, STRIDED, PRO, EPI, true>(sm, rb, tw_all, pr, s0, last, fz, p, l);
+    else ntt16_body<INV, STRIDED, PRO, EPI, false>(sm, rb, tw_all, pr, s0, last, fz, p, l);
 }
 
 
@@ -302,11 +385,11 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
         dim3 g(16, rows);
         const NttFuse fz{};
         if (!inverse) {
-            ntt16_pass<false, true><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 0, 0, fz);
-            ntt16_pass<false, false><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 8, 1, fz);
+            ntt16_pass<false, true><<<g, 256, 0, st>>>(rb, P->d_tw16, P->pr, 0, 0, fz);
+            ntt16_pass<false, false><<<g, 256, 0, st>>>(rb, P->d_tw16, P->pr, 8, 1, fz);
         } else {
-            ntt16_pass<true, false><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 8, 0, fz);
-            ntt16_pass<true, true><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 0, 1, fz);
+            ntt16_pass<true, false><<<g, 256, 0, st>>>(rb, P->d_tw16, P->pr, 8, 0, fz);
+            ntt16_pass<true, true><<<g, 256, 0, st>>>(rb, P->d_tw16, P->pr, 0, 1, fz);
         }
         BLB_COUNT_LAUNCH(2);
         blb_timing_end(1, t0, st, alg);
@@ -347,10 +430,10 @@ blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool invers
     BLB_COUNT(2, rows);
     cudaEvent_t t0 = blb_timing_begin(st);
     dim3 g(16, rows);
-    if (fz.pro == 1) ntt16_pass<false, true, 1, 0><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 0, 0, fz);
-    else ntt16_pass<false, true, 0, 0><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 0, 0, fz);
-    if (fz.epi == 1) ntt16_pass<false, false, 0, 1><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 8, 1, fz);
-    else ntt16_pass<false, false, 0, 0><<<g, 256, 0, st>>>(rb, P->d_tw, P->pr, 8, 1, fz);
+    if (fz.pro == 1) ntt16_pass<false, true, 1, 0><<<g, 256, 0, st>>>(rb, P->d_tw16, P->pr, 0, 0, fz);
+    else ntt16_pass<false, true, 0, 0><<<g, 256, 0, st>>>(rb, P->d_tw16, P->pr, 0, 0, fz);
+    if (fz.epi == 1) ntt16_pass<false, false, 0, 1><<<g, 256, 0, st>>>(rb, P->d_tw16, P->pr, 8, 1, fz);
+    else ntt16_pass<false, false, 0, 0><<<g, 256, 0, st>>>(rb, P->d_tw16, P->pr, 8, 1, fz);
     BLB_COUNT_LAUNCH(2);
     blb_timing_end(1, t0, st, (double)rows * 16.0 * (1 << 16));
     BLB_CHECK_LAUNCH();
