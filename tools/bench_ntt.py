@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--lib", default=os.path.join(ROOT, "paper_2508_19525_b200", "libblb.so"))
     ap.add_argument("--rows", default="60,300,960,1920")
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--prime", type=int, default=-1, help="run every row on this prime index (default: all six)")
     args = ap.parse_args()
     L = ctypes.CDLL(args.lib)
     vp = ctypes.c_void_p
@@ -41,21 +42,22 @@ def main():
     res = {}
     st = torch.cuda.current_stream()
     for rows in [int(r) for r in args.rows.split(",")]:
-        polys = rows // 6
-        data = torch.randint(0, 2 ** 39, (polys, 6, N), dtype=torch.int64, device="cuda")
-        pidx = (ctypes.c_int32 * 6)(*range(6))
+        nl = 6 if args.prime < 0 else 1
+        polys = rows // nl
+        data = torch.randint(0, 2 ** 39, (polys, nl, N), dtype=torch.int64, device="cuda")
+        pidx = (ctypes.c_int32 * nl)(*(range(6) if args.prime < 0 else [args.prime]))
         for name, fn in (("ntt", L.blb_ntt), ("intt", L.blb_intt)):
             for _ in range(3):
-                fn(h, ctypes.c_void_p(data.data_ptr()), pidx, 6, polys, ctypes.c_void_p(st.cuda_stream))
+                fn(h, ctypes.c_void_p(data.data_ptr()), pidx, nl, polys, ctypes.c_void_p(st.cuda_stream))
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
             for _ in range(args.iters):
-                fn(h, ctypes.c_void_p(data.data_ptr()), pidx, 6, polys, ctypes.c_void_p(st.cuda_stream))
+                fn(h, ctypes.c_void_p(data.data_ptr()), pidx, nl, polys, ctypes.c_void_p(st.cuda_stream))
             e1.record(st)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / args.iters
-            limbs = polys * 6
+            limbs = polys * nl
             res["%s_%d" % (name, limbs)] = {"us": ms * 1e3, "limbs_per_s": limbs / (ms * 1e-3),
                                             "alg_GBps": limbs * 16 * N / (ms * 1e-3) / 1e9}
     print(json.dumps({"lib": os.path.basename(args.lib), "results": res}))
