@@ -221,6 +221,31 @@ blb_status blb_ckks_to_mpc(const blb_params *params, const blb_ct *in, int n_ct,
                            uint64_t first_ct_id, uint64_t *masked, uint64_t *share, void *ws, size_t ws_bytes,
                            void *stream);
 
+/* Row f3, MPC -> CKKS ingest (Algorithm 2; ring-to-field, App. C.3).
+ * blb_share_to_rns: a secret share x over Z_{2^w} (device u64 [N], values < 2^w, 1 <= w <= 64,
+ * coefficient order) mapped to the field per limb i <= level: x mod q_i (P0's share, sub = 0)
+ * or x - 2^w mod q_i (P1's share, sub = 1), then NTT (C2).  out: device [level+1][N].
+ * blb_mpc_to_ckks: the server (P1) half of Alg. 2 line 4 -- ct (the client's encryption of
+ * its field share, level l, NTT) is updated in place: c0 += NTT(x1 - 2^w mod q_i).  The result
+ * encrypts x0 + x1 - 2^w = m whenever x0 + x1 = m + 2^w (probability >= 1 - 2^-40 for
+ * w = l + 40).  ws: device scratch >= (level+1) * N * 8 bytes.  Errors:
+ * BLB_E_INVALID_ARG (null / w out of range), BLB_E_LEVEL, BLB_E_NOMEM (workspace). */
+blb_status blb_share_to_rns(const blb_params *params, const uint64_t *x, int w, int sub, int level, uint64_t *out,
+                            void *stream);
+blb_status blb_mpc_to_ckks(const blb_params *params, blb_ct *ct, const uint64_t *x1, int w, void *ws,
+                           size_t ws_bytes, void *stream);
+/* Row f3, local fixed-point Decode of a share ("O(N log N) FFT ... extend the shares to
+ * a larger ring and conduct local truncations"; App. C.4; reading C18).  Each MPC party
+ * runs it on its own share; the outputs are additive shares of the real slots of Decode(m) scaled
+ * by 2^-s_out (with plaintext scale Delta = 2^d: fixed-point precision d - s_out bits).
+ * x: device [N][2] u64 = little-endian Z_{2^128} share of the coefficient vector.  Cooley-Tukey
+ * network over Z_{2^128}[i] with twiddles W = round(2^ft zeta^{brv(m+i)}) and an arithmetic right
+ * shift by ft after every twiddle product; slot j is read at the position of zeta^{5^j} (C3) and
+ * shifted right by s_out.  y: device [N/2][2] u64.  ws: device scratch >= 48 N bytes.
+ * 1 <= ft <= 52, 0 <= s_out <= 126, else BLB_E_INVALID_ARG; BLB_E_NOMEM (workspace). */
+blb_status blb_share_decode(const blb_params *params, const uint64_t *x, int ft, int s_out, uint64_t *y, void *ws,
+                            size_t ws_bytes, void *stream);
+
 /* ------------------------------------------------------------------ */
 /* ct-pt MatMul (rows a2-a6; C11 / C12; BSGS App. C.1)      */
 /* ------------------------------------------------------------------ */

@@ -119,6 +119,9 @@ def lib():
         L.orc_encode_ext.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_int,
                                      ctypes.c_void_p]
         L.orc_moddown_rescale.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+        L.orc_share_decode.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+        L.orc_share_to_rns.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_void_p]
         L.orc_relinearize_ext.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                                           ctypes.c_void_p]
         _lib = L
@@ -571,3 +574,52 @@ def moddown_rescale(ctx: Ctx, a: CtExt) -> Ct:
 def moddown_ct(ctx: Ctx, a: CtExt) -> Ct:
     """ModDown of both polynomials (C7): back to Q_l, divided by P."""
     return Ct(np.stack([moddown(ctx, a.data[0], a.level), moddown(ctx, a.data[1], a.level)]), a.level, a.scale)
+
+
+# ---------------------------------------------------------------------------
+# f3: MPC -> CKKS ingest (Algorithm 2, P:641-657; ring-to-field, App. C.3 P:1222-1232)
+# ---------------------------------------------------------------------------
+def share_to_rns(ctx: Ctx, x, w: int, sub: bool, level: int) -> np.ndarray:
+    """[x]^q = x mod q (P0) or x - 2^w mod q (P1, sub) per limb, NTT form [level+1][N]."""
+    x = np.ascontiguousarray(x, dtype=np.uint64)
+    assert x.shape == (ctx.N,) and 1 <= w <= 64
+    out = np.empty((level + 1, ctx.N), dtype=np.uint64)
+    lib().orc_share_to_rns(ctx._h, _p(x), int(w), int(bool(sub)), level, _p(out))
+    return out
+
+
+def mpc_to_ckks(ctx: Ctx, ct: Ct, x1, w: int) -> Ct:
+    """Server half of Alg. 2 line 4: Enc([tmp]_0^q) (+) [tmp]_1^q, i.e. c0 += NTT(x1 - 2^w mod q_i)."""
+    s = share_to_rns(ctx, x1, w, True, ct.level)
+    idx = list(range(ct.level + 1))
+    pa = (ctypes.c_int * len(idx))(*idx)
+    c0 = np.empty_like(s)
+    lib().orc_add_idx(ctx._h, _p(_u64(ct.data[0])), _p(s), pa, len(idx), 1, _p(c0))
+    return Ct(np.stack([c0, ct.data[1].copy()]), ct.level, ct.scale)
+
+
+def share_decode(ctx: Ctx, x: np.ndarray, ft: int, s_out: int) -> np.ndarray:
+    """Row f3: local fixed-point Decode of a share over Z_{2^128} (x: uint64 [N][2] = lo, hi words)
+    -> uint64 [N/2][2] share of the real slots scaled by 2^-s_out (reading C18)."""
+    x = np.ascontiguousarray(x, dtype=np.uint64)
+    assert x.shape == (ctx.N, 2) and 1 <= ft <= 62 and 0 <= s_out < 127
+    y = np.empty((ctx.n, 2), dtype=np.uint64)
+    lib().orc_share_decode(ctx._h, _p(x), int(ft), int(s_out), _p(y))
+    return y
+
+
+def u128_to_int(a: np.ndarray) -> list[int]:
+    """[..][2] uint64 words -> signed Python ints (two's complement, 128 bits)."""
+    out = []
+    for lo, hi in a.reshape(-1, 2):
+        v = int(lo) | (int(hi) << 64)
+        out.append(v - (1 << 128) if v >> 127 else v)
+    return out
+
+
+def int_to_u128(vals) -> np.ndarray:
+    a = np.empty((len(vals), 2), dtype=np.uint64)
+    for i, v in enumerate(vals):
+        v %= 1 << 128
+        a[i, 0], a[i, 1] = v & (2 ** 64 - 1), v >> 64
+    return a

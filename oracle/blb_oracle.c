@@ -877,3 +877,67 @@ void orc_relinearize_ext(const orc_ctx *c, const u64 *d, int lvl, const u64 *rlk
         }
     free(ext);
 }
+
+/* ------------------------------------------------------------------ */
+/* f3: MPC -> CKKS ingest (Alg. 2 line 4; ring-to-field eq. P:1222-1232) */
+/* ------------------------------------------------------------------ */
+/* A share x in Z_{2^w} (w <= 64, x < 2^w) mapped to the field: x mod q_i (P0's share) or
+ * x - 2^w mod q_i (P1's share, sub = 1), per limb i <= lvl, then NTT (C2): out [lvl+1][N]. */
+void orc_share_to_rns(const orc_ctx *c, const u64 *x, int w, int sub, int lvl, u64 *out) {
+    u64 N = c->N;
+    for (int i = 0; i <= lvl; i++) {
+        u64 q = c->mod[i];
+        u64 two_w = (u64)(((u128)1 << w) % q);
+        u64 *o = out + (u64)i * N;
+        for (u64 j = 0; j < N; j++) {
+            u64 v = x[j] % q;
+            o[j] = sub ? submod(v, two_w, q) : v;
+        }
+        ntt_limb(c, o, i);
+    }
+}
+
+/* ------------------------------------------------------------------ */
+/* f3: local fixed-point Decode of a share over Z_{2^128}               */
+/* ("O(N log N) FFT ... extend the shares to a larger ring and  */
+/* conduct local truncations"; App. C.4 P:1246-1262 extend-then-truncate) */
+/* ------------------------------------------------------------------ */
+typedef __int128 i128;
+/* arithmetic right shift of a ring element read as a signed 128-bit integer (SecureML-style local
+ * truncation, App. C.4: [m']_b = [m]_b >>_a s) */
+static inline u128 ashr128(u128 v, int s) { return (u128)(((i128)v) >> s); }
+/* x: [N][2] u64 = little-endian u128 share of the coefficient vector; y: [N/2][2] share of the
+ * real slots.  Cooley-Tukey network over Z_{2^128}[i] (stage m = 1, 2, .., N/2, block i, twiddle
+ * W = round(2^ft zeta^{brv(m+i)}), zeta = e^{i pi / N}): V = (Y * W) >>_a ft (each component),
+ * X' = X + V, Y' = X - V, so position k ends with sum_j x_j zeta^{(2 brv(k)+1) j} (C2 / C3
+ * ordering); slot j (zeta^{5^j}) sits at k with 2 brv(k) + 1 = 5^j mod 2N; y_j = Re >>_a s_out. */
+void orc_share_decode(const orc_ctx *c, const u64 *x, int ft, int s_out, u64 *y) {
+    u64 N = c->N, twoN = 2 * N;
+    int logN = c->logN;
+    u128 *re = (u128 *)malloc(N * sizeof(u128)), *im = (u128 *)malloc(N * sizeof(u128));
+    for (u64 k = 0; k < N; k++) { re[k] = (u128)x[2 * k] | ((u128)x[2 * k + 1] << 64); im[k] = 0; }
+    __float128 sc = ldexpq(1.0Q, ft);
+    for (u64 m = 1; m < N; m <<= 1) {
+        u64 t = N / (2 * m);
+        for (u64 i = 0; i < m; i++) {
+            __float128 ang = M_PIq * (__float128)brv(m + i, logN) / (__float128)N;
+            long long wr = (long long)roundq(sc * cosq(ang)), wi = (long long)roundq(sc * sinq(ang));
+            u128 Wr = (u128)(i128)wr, Wi = (u128)(i128)wi;
+            for (u64 j = 2 * i * t; j < 2 * i * t + t; j++) {
+                u128 yr = re[j + t], yi = im[j + t];
+                u128 vr = ashr128(yr * Wr - yi * Wi, ft), vi = ashr128(yr * Wi + yi * Wr, ft);
+                u128 xr = re[j], xi = im[j];
+                re[j] = xr + vr; im[j] = xi + vi;
+                re[j + t] = xr - vr; im[j + t] = xi - vi;
+            }
+        }
+    }
+    u64 e = 1;  /* 5^j mod 2N */
+    for (u64 j = 0; j < N / 2; j++) {
+        u64 k = brv((e - 1) / 2, logN);
+        u128 v = ashr128(re[k], s_out);
+        y[2 * j] = (u64)v; y[2 * j + 1] = (u64)(v >> 64);
+        e = (e * 5) % twoN;
+    }
+    free(re); free(im);
+}

@@ -83,6 +83,9 @@ def lib() -> ctypes.CDLL:
             "blb_ckks_to_mpc": ([vp, vp, ctypes.c_int, ctypes.c_char_p, u64, vp, vp, vp, ctypes.c_size_t, vp],
                                 ctypes.c_int),
             "blb_mhp_column_map": ([ctypes.c_int] * 4 + [vp, ip], ctypes.c_int),
+            "blb_share_to_rns": ([vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp], ctypes.c_int),
+            "blb_mpc_to_ckks": ([vp, vp, vp, ctypes.c_int, vp, ctypes.c_size_t, vp], ctypes.c_int),
+            "blb_share_decode": ([vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
             "blb_matmul_plan_create": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp,
                                         ctypes.c_int, ctypes.c_int, ctypes.c_int, vp], ctypes.c_int),
             "blb_matmul_plan_destroy": ([vp], None),
@@ -362,6 +365,34 @@ def ckks_to_mpc(params: Params, cts: list, mask_key: bytes, first_ct_id: int):
     _check(lib().blb_ckks_to_mpc(params.handle, arr, n, mask_key, first_ct_id, _ptr(masked), _ptr(share), None, 0,
                                  _stream()))
     return masked, share
+
+
+def share_to_rns(params: Params, x: torch.Tensor, w: int, sub: bool, level: int) -> torch.Tensor:
+    """Row f3: a share over Z_{2^w} (int64 [N] CUDA, the u64 bit pattern) -> NTT residues [level+1][N]
+    of x mod q_i (P0) or x - 2^w mod q_i (P1, sub)."""
+    out = params.empty(level + 1, params.N)
+    _check(lib().blb_share_to_rns(params.handle, _ptr(x.contiguous()), int(w), int(bool(sub)), level, _ptr(out),
+                                  _stream()))
+    return out
+
+
+def mpc_to_ckks(params: Params, ct: Ciphertext, x1: torch.Tensor, w: int) -> Ciphertext:
+    """Row f3, server half of Alg. 2 line 4: ct (+) [tmp]_1^q, in place (c0 += NTT(x1 - 2^w mod q_i))."""
+    ws = params.empty(ct.level + 1, params.N)
+    c = ct.c()
+    _check(lib().blb_mpc_to_ckks(params.handle, ctypes.byref(c), _ptr(x1.contiguous()), int(w), _ptr(ws),
+                                 ws.numel() * 8, _stream()))
+    return ct
+
+
+def share_decode(params: Params, x: torch.Tensor, ft: int, s_out: int) -> torch.Tensor:
+    """Row f3: local fixed-point Decode of a Z_{2^128} share (int64 [N][2] CUDA: lo, hi words) ->
+    int64 [N/2][2] share of the real slots scaled by 2^-s_out (reading C18)."""
+    y = torch.empty(params.N // 2, 2, dtype=torch.int64, device="cuda")
+    ws = torch.empty(params.N * 6, dtype=torch.int64, device="cuda")
+    _check(lib().blb_share_decode(params.handle, _ptr(x.contiguous()), int(ft), int(s_out), _ptr(y), _ptr(ws),
+                                  ws.numel() * 8, _stream()))
+    return y
 
 
 def _f2_ws(params: Params, level: int) -> torch.Tensor:

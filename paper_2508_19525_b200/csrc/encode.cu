@@ -156,6 +156,60 @@ __global__ void k_copy(const u64 *src, u64 *dst, int n) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x < n) dst[x] = src[x];
 }
+
+// ---------------------------------------------------------------------------
+// Row f3: local fixed-point Decode of a secret share over Z_{2^128} (reading C18; P:684-685,
+// App. C.4).  Same Cooley-Tukey network as the decode above (zeta^{brv(m+i)} twiddles), in
+// wrapping 128-bit integer complex arithmetic with an arithmetic right shift by ft after each
+// twiddle product (local truncation).  Twiddles W = round(2^ft zeta^e) from the double-double
+// zeta table (no ties: the entries are irrational or exact integers).
+// ---------------------------------------------------------------------------
+typedef unsigned __int128 u128d;
+typedef __int128 i128d;
+__device__ __forceinline__ long long dd_round_scaled(double hi, double lo, int ft) {
+    const double h = ldexp(hi, ft), l = ldexp(lo, ft);  // exact (power-of-two scaling)
+    double r = rint(h);
+    const double d = (h - r) + l;
+    if (d > 0.5) r += 1.0;
+    else if (d < -0.5) r -= 1.0;
+    return (long long)r;
+}
+__global__ void k_fxp_tw(const double *zeta, long long *tw, int ft, int N) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const double *z = zeta + 4ll * i;
+    tw[2 * i] = dd_round_scaled(z[0], z[1], ft);
+    tw[2 * i + 1] = dd_round_scaled(z[2], z[3], ft);
+}
+__global__ void k_fxp_lift(const u64 *x, u128d *re, u128d *im, int N) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= N) return;
+    re[k] = (u128d)x[2 * k] | ((u128d)x[2 * k + 1] << 64);
+    im[k] = 0;
+}
+__global__ void k_fxp_stage(u128d *re, u128d *im, const long long *tw, int m, int N, int ft) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= N / 2) return;
+    const int t = N / (2 * m);
+    const int i = b / t, jj = b - i * t;
+    const int j = 2 * i * t + jj;
+    const u128d Wr = (u128d)(i128d)tw[2 * (m + i)], Wi = (u128d)(i128d)tw[2 * (m + i) + 1];
+    const u128d yr = re[j + t], yi = im[j + t];
+    const u128d vr = (u128d)((i128d)(yr * Wr - yi * Wi) >> ft);
+    const u128d vi = (u128d)((i128d)(yr * Wi + yi * Wr) >> ft);
+    const u128d xr = re[j], xi = im[j];
+    re[j] = xr + vr;
+    im[j] = xi + vi;
+    re[j + t] = xr - vr;
+    im[j + t] = xi - vi;
+}
+__global__ void k_fxp_extract(const u128d *re, const int32_t *slot_pos, u64 *y, int N, int s_out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N / 2) return;
+    const u128d v = (u128d)((i128d)re[slot_pos[j]] >> s_out);
+    y[2 * j] = (u64)v;
+    y[2 * j + 1] = (u64)(v >> 64);
+}
 }  // namespace
 
 size_t encode_scratch_doubles(const blb_params *P, int n_pts) { return (size_t)n_pts * P->N * 4; }
@@ -192,6 +246,26 @@ blb_status launch_decode(const blb_params *P, const u64 *pt, double scale, doubl
     dim3 gs((N / 2 + kTB - 1) / kTB, 1);
     for (int m = 1; m < N; m <<= 1) k_stage<<<gs, kTB, 0, st>>>(buf, P->d_zeta, m, logN, 0);
     k_decode_extract<<<(N / 2 + kTB - 1) / kTB, kTB, 0, st>>>(buf, P->d_slot_pos, slots_out, 1.0 / scale, N);
+    BLB_COUNT_LAUNCH(3 + logN);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_share_decode(const blb_params *P, const uint64_t *x, int ft, int s_out, uint64_t *y, void *ws,
+                                       size_t ws_bytes, void *stream) {
+    if (!P || !x || !y || !ws || ft < 1 || ft > 52 || s_out < 0 || s_out > 126) return BLB_E_INVALID_ARG;
+    const int N = P->N, logN = P->logN;
+    if (ws_bytes < (size_t)N * 48) {
+        blb_set_error("blb_share_decode: workspace needs %zu bytes", (size_t)N * 48);
+        return BLB_E_NOMEM;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    u128d *re = (u128d *)ws, *im = re + N;
+    long long *tw = (long long *)(im + N);
+    k_fxp_tw<<<(N + kTB - 1) / kTB, kTB, 0, st>>>(P->d_zeta, tw, ft, N);
+    k_fxp_lift<<<(N + kTB - 1) / kTB, kTB, 0, st>>>(x, re, im, N);
+    for (int m = 1; m < N; m <<= 1) k_fxp_stage<<<(N / 2 + kTB - 1) / kTB, kTB, 0, st>>>(re, im, tw, m, N, ft);
+    k_fxp_extract<<<(N / 2 + kTB - 1) / kTB, kTB, 0, st>>>(re, P->d_slot_pos, y, N, s_out);
     BLB_COUNT_LAUNCH(3 + logN);
     BLB_CHECK_LAUNCH();
     return BLB_OK;

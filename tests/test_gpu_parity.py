@@ -464,3 +464,41 @@ def test_matmul_long_mac_fold_bit_exact(toy):
     zs = list(packing.spatial_slots(X, toy.n))
     _, _, oout, gout = run_both(toy, plan_o, plan_g, zs, W)
     assert np.array_equal(u64(gout[0].data), oout[0].data)
+
+
+# ---------------------------------------------------------------- row f3: MPC -> CKKS ingest
+@pytest.mark.parametrize("name,w", [("toy", 64), ("toy", 41), ("bert", 64)])
+def test_mpc_to_ckks_bit_exact(name, w, request):
+    pair = request.getfixturevalue(name)
+    rng = np.random.default_rng(60 + w)
+    lvl = pair.K - 1
+    x = rng.integers(0, 2 ** min(w, 63), pair.N, dtype=np.uint64)
+    if w == 64:
+        x |= rng.integers(0, 2, pair.N, dtype=np.uint64) << np.uint64(63)
+    x[:4] = [0, 1, (2 ** w - 1) if w < 64 else 2 ** 64 - 1, 2 ** (w - 1)]
+    for sub in (False, True):
+        got = u64(blb.share_to_rns(pair.g, dev(x), w, sub, lvl))
+        assert np.array_equal(got, O.share_to_rns(pair.o, x, w, sub, lvl))
+    c = rand_limbs(pair, 2, list(range(lvl + 1)), 61)
+    gct = blb.Ciphertext(dev(c), lvl, 2.0 ** 40)
+    blb.mpc_to_ckks(pair.g, gct, dev(x), w)
+    want = O.mpc_to_ckks(pair.o, O.Ct(c, lvl, 2.0 ** 40), x, w)
+    assert np.array_equal(u64(gct.data), want.data)
+
+
+@pytest.mark.parametrize("name", ["toy", "bert"])
+def test_share_decode_bit_exact(name, request):
+    """Row f3 local fixed-point Decode (C18): bit-exact over Z_{2^128} for a uniform share and
+    for a small signed message, incl. the extreme words."""
+    pair = request.getfixturevalue(name)
+    rng = np.random.default_rng(70)
+    x = rng.integers(0, 2 ** 63, (pair.N, 2), dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, (pair.N, 2),
+                                                                                            dtype=np.uint64)
+    x[0] = [0, 0]
+    x[1] = [2 ** 64 - 1, 2 ** 64 - 1]
+    x[2] = [0, 2 ** 63]
+    z = rng.uniform(-1, 1, pair.n)
+    m = O.int_to_u128([int(v) for v in O.encode_coeffs(pair.o, z, 2.0 ** 30)])
+    for xs, ft, s_out in ((x, 30, 18), (m, 30, 18), (m, 40, 0), (x, 52, 126)):
+        got = u64(blb.share_decode(pair.g, dev(xs), ft, s_out))
+        assert np.array_equal(got, O.share_decode(pair.o, xs, ft, s_out))
