@@ -216,11 +216,16 @@ constexpr int kMacStages = 4, kMacEnt = 2;
 constexpr int kMacStageWords = kMacEnt * 3 * 512;  // pt, r0, r1 per entry
 constexpr size_t kMacSmem = (size_t)kMacStages * kMacStageWords * 8 + 2 * kMacStages * 8;
 
+// SPLIT41 (40-bit limbs): the c0 products on the integer pipe (Acc41), the c1 products on the
+// FP64 pipe (AccF64) -- the two pipes run side by side; 60-bit limbs: Acc128 for all four.
 template <bool SPLIT41>
 __device__ __forceinline__ void mac_tma_consume(const u64 *ring, uint64_t *full, uint64_t *empty, int n_e, u64 *out,
                                                 long long kN, const ModConst &mc) {
     using A = typename std::conditional<SPLIT41, Acc41, Acc128>::type;
-    A a00, a01, a10, a11;
+    using A1 = typename std::conditional<SPLIT41, AccF64, Acc128>::type;
+    const double qd = (double)mc.q, qinv = 1.0 / qd;
+    A a00, a01;
+    A1 a10, a11;
     a00.zero(); a01.zero(); a10.zero(); a11.zero();
     const int t = threadIdx.x;
     const int n_st = (n_e + kMacEnt - 1) / kMacEnt;
@@ -235,17 +240,30 @@ __device__ __forceinline__ void mac_tma_consume(const u64 *ring, uint64_t *full,
                 const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + (kMacEnt + 2 * u) * 512 + 2 * t);
                 const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + (kMacEnt + 2 * u + 1) * 512 + 2 * t);
                 a00.mac(pv.x, r0.x); a01.mac(pv.y, r0.y);
-                a10.mac(pv.x, r1.x); a11.mac(pv.y, r1.y);
+                if constexpr (SPLIT41) {
+                    a10.mac(pv.x, r1.x, qd, qinv); a11.mac(pv.y, r1.y, qd, qinv);
+                } else {
+                    a10.mac(pv.x, r1.x); a11.mac(pv.y, r1.y);
+                }
             }
         }
         __syncwarp();
         if ((t & 31) == 0) mbar_arrive(&empty[slot]);
-        if (!SPLIT41 && (s & 31) == 31) {  // 64 products < 2^126: fold before the 128-bit sum can overflow
-            a00.fold(mc); a01.fold(mc); a10.fold(mc); a11.fold(mc);
+        if constexpr (!SPLIT41) {
+            if ((s & 31) == 31) {  // 64 products < 2^126: fold before the 128-bit sum can overflow
+                a00.fold(mc); a01.fold(mc); a10.fold(mc); a11.fold(mc);
+            }
+        } else {
+            if ((s & 255) == 255) {  // 512 products: keep the FP64 sums below 2^51
+                a10.fold(qd, qinv); a11.fold(qd, qinv);
+            }
         }
     }
     *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00.reduce(mc), a01.reduce(mc));
-    *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(mc), a11.reduce(mc));
+    if constexpr (SPLIT41)
+        *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(qd, qinv), a11.reduce(qd, qinv));
+    else
+        *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(mc), a11.reduce(mc));
 }
 
 __global__ void __launch_bounds__(kTB + 32) k_mac_tma(const u64 *__restrict__ pt, const u64 *__restrict__ R,

@@ -466,6 +466,21 @@ def test_matmul_long_mac_fold_bit_exact(toy):
     assert np.array_equal(u64(gout[0].data), oout[0].data)
 
 
+def test_matmul_fp64_fold_bit_exact(toy):
+    """640 products per output (40 inputs x B = 16): the FP64-pipe accumulator of the 40-bit limbs
+    folds every 512 products (AccF64), the 60-bit limb every 64 (Acc128)."""
+    L, D, Dout = 16, 5120, 16
+    X = bi.uniform(97, (L, D), -1, 1)
+    W = bi.normal(98, (D, Dout), 0.01)
+    plan_o = mm.plan_spatial(W, L, toy.n, 16)
+    plan_g = blb.MatmulPlan(toy.g, L, D, Dout, bsgs_B=16)
+    assert plan_g.n_in == 40 and plan_g.n_pt == plan_o.n_plaintexts
+    from paper_2508_19525_b200 import packing
+    zs = list(packing.spatial_slots(X, toy.n))
+    _, _, oout, gout = run_both(toy, plan_o, plan_g, zs, W)
+    assert np.array_equal(u64(gout[0].data), oout[0].data)
+
+
 # ---------------------------------------------------------------- row f3: MPC -> CKKS ingest
 @pytest.mark.parametrize("name,w", [("toy", 64), ("toy", 41), ("bert", 64)])
 def test_mpc_to_ckks_bit_exact(name, w, request):
