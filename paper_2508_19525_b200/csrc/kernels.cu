@@ -222,21 +222,24 @@ struct KsGroups {
 // before the first multiply); BETA = 0: runtime beta.
 // EXT: write the extended-basis result (P sigma_g(c0) + u0, u1) over Q_l u P straight to
 // jobs.j[t].out ([2][E][N]) -- the double-hoisted rotation (no ModDown).
-template <int BETA, bool EXT = false>
-__global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, int np, int K, int beta_rt,
-                           int logN, PinvTab pq) {
+// SMALL (prime < 2^41): the a-part products run on the FP64 pipe (AccF64), the b-part on the
+// integer pipe, so the two pipes share the 2 beta products per job.
+template <int BETA, bool EXT, bool SMALL>
+__device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups &grp, u64 *u, const Primes &pr, int k,
+                                              int np, int K, int beta_rt, int logN, const PinvTab &pq, int x, int m,
+                                              int gi) {
     const int N = 1 << logN;
     const int beta = BETA > 0 ? BETA : beta_rt;
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int m = blockIdx.y, gi = blockIdx.z;
-    if (x >= N) return;
     const int t0 = grp.start[gi], cnt = grp.start[gi + 1] - t0;
     const int E = k + np, Lk = K + np;
     const int pm = m < k ? m : K + (m - k);
     const KsJob &J0 = jobs.j[t0];
     const uint32_t src = J0.galois == 1 ? (uint32_t)x : galois_perm(x, J0.galois, logN);
     const ModConst &mc = pr.m[pm];
-    Acc128 a0[kKsGroup], a1[kKsGroup];
+    using A1 = typename std::conditional<SMALL, AccF64, Acc128>::type;
+    const double qd = (double)mc.q, qinv = 1.0 / qd;
+    Acc128 a0[kKsGroup];
+    A1 a1[kKsGroup];
 #pragma unroll
     for (int q = 0; q < kKsGroup; q++) { a0[q].zero(); a1[q].zero(); }
     if (BETA > 0) {
@@ -256,7 +259,8 @@ __global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, 
 #pragma unroll
                 for (int j = 0; j < BETA; j++) {
                     a0[q].mac(e[j], kb[j]);
-                    a1[q].mac(e[j], ka[j]);
+                    if constexpr (SMALL) a1[q].mac(e[j], ka[j], qd, qinv);
+                    else a1[q].mac(e[j], ka[j]);
                 }
             }
         }
@@ -269,11 +273,16 @@ __global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, 
                 if (q < cnt) {
                     const u64 e = jobs.j[t0 + q].ext[((long long)j * E + m) * N + src];
                     a0[q].mac(e, kb);
-                    a1[q].mac(e, ka);
+                    if constexpr (SMALL) a1[q].mac(e, ka, qd, qinv);
+                    else a1[q].mac(e, ka);
                 }
             }
         }
     }
+    auto a1r = [&](int q) -> u64 {
+        if constexpr (SMALL) return a1[q].reduce(qd, qinv);
+        else return a1[q].reduce(mc);
+    };
 #pragma unroll
     for (int q = 0; q < kKsGroup; q++) {
         if (q < cnt) {
@@ -283,15 +292,26 @@ __global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, 
                 u64 r0 = a0[q].reduce(mc);
                 if (m < k) r0 = addmod(r0, shoup(J.c0[(long long)m * N + src], pq.v[m], pq.sh[m], mc.q), mc.q);
                 J.out[(long long)m * N + x] = r0;
-                u64 r1 = a1[q].reduce(mc);
+                u64 r1 = a1r(q);
                 if (m < k && J.c1_add) r1 = addmod(r1, shoup(J.c1_add[(long long)m * N + src], pq.v[m], pq.sh[m], mc.q), mc.q);
                 J.out[((long long)E + m) * N + x] = r1;
             } else {
                 u[(((long long)t * 2 + 0) * E + m) * N + x] = a0[q].reduce(mc);
-                u[(((long long)t * 2 + 1) * E + m) * N + x] = a1[q].reduce(mc);
+                u[(((long long)t * 2 + 1) * E + m) * N + x] = a1r(q);
             }
         }
     }
+}
+
+template <int BETA, bool EXT = false>
+__global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, int np, int K, int beta_rt,
+                           int logN, PinvTab pq) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int m = blockIdx.y, gi = blockIdx.z;
+    if (x >= (1 << logN)) return;
+    const int pm = m < k ? m : K + (m - k);
+    if (pr.m[pm].q < (1ull << 41)) ks_inner_body<BETA, EXT, true>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi);
+    else ks_inner_body<BETA, EXT, false>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi);
 }
 
 // conv[t][b][i][x] = FastBConv_{P -> q_i}(INTT(u_P))   (u P-rows already INTT'd)

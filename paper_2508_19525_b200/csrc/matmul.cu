@@ -102,9 +102,13 @@ __global__ void __launch_bounds__(kTB) k_mac(const u64 *__restrict__ pt, const u
     const ModConst &mc = pr.m[l < kq ? l : Kfull + (l - kq)];
     u64 *out = acc + (long long)o * 2 * kN + lx;
     if (mc.q < (1ull << 41)) {
-        // 40-bit limb: split 32-bit partial products (Acc41)
-        Acc41 a00, a01, a10, a11;
+        // 40-bit limb: c0 products with split 32-bit partial products (Acc41, integer pipe),
+        // c1 products on the FP64 pipe (AccF64)
+        const double qd = (double)mc.q, qinv = 1.0 / qd;
+        Acc41 a00, a01;
+        AccF64 a10, a11;
         a00.zero(); a01.zero(); a10.zero(); a11.zero();
+        int cnt = 0;
 #pragma unroll 4
         for (int e = e_lo; e < e_hi; e++) {
             const int bi = ent_r[e];
@@ -113,10 +117,14 @@ __global__ void __launch_bounds__(kTB) k_mac(const u64 *__restrict__ pt, const u
             const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(R + (long long)bi * 2 * kN + lx);
             const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(R + ((long long)bi * 2 + 1) * kN + lx);
             a00.mac(pv.x, r0.x); a01.mac(pv.y, r0.y);
-            a10.mac(pv.x, r1.x); a11.mac(pv.y, r1.y);
+            a10.mac(pv.x, r1.x, qd, qinv); a11.mac(pv.y, r1.y, qd, qinv);
+            if (++cnt == 512) {  // keep the FP64 sums below 2^51
+                a10.fold(qd, qinv); a11.fold(qd, qinv);
+                cnt = 0;
+            }
         }
         *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00.reduce(mc), a01.reduce(mc));
-        *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(mc), a11.reduce(mc));
+        *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(qd, qinv), a11.reduce(qd, qinv));
         return;
     }
     Acc128 a00, a01, a10, a11;  // [poly][coefficient]
