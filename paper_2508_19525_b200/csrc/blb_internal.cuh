@@ -129,28 +129,25 @@ struct Acc41 {
 // 1.5 * 2^52 (|error| < 2^-11, so p - c q lies in (-q, q) and is exact); sums of the remainders
 // and of the e's stay exact integers below 2^51 for < 2^10 products.
 struct AccF64 {
-    double r, e;
-    __device__ __forceinline__ void zero() { r = 0.0; e = 0.0; }
+    double r;  // sum of the exact remainders (p - c q) + e
+    __device__ __forceinline__ void zero() { r = 0.0; }
     __device__ __forceinline__ static double u2d(u64 x) {  // x < 2^52
         return __dsub_rn(__hiloint2double(0x43300000 | (int)(x >> 32), (int)(uint32_t)x), 4503599627370496.0);
     }
     __device__ __forceinline__ void mac(u64 a, u64 b, double qd, double qinv) {
         const double A = u2d(a), B = u2d(b);
         const double p = __dmul_rn(A, B);
-        e = __dadd_rn(e, __fma_rn(A, B, -p));
+        const double e = __fma_rn(A, B, -p);
         const double c = __dsub_rn(__fma_rn(p, qinv, 6755399441055744.0), 6755399441055744.0);
-        r = __dadd_rn(r, __fma_rn(-c, qd, p));
+        r = __dadd_rn(r, __dadd_rn(__fma_rn(-c, qd, p), e));  // |p - c q + e| < q + 2^30: exact
     }
-    __device__ __forceinline__ void fold(double qd, double qinv) {  // back to |r| < q, e = 0
-        const double t = __dadd_rn(r, e);
-        const double c = __dsub_rn(__fma_rn(t, qinv, 6755399441055744.0), 6755399441055744.0);
-        r = __fma_rn(-c, qd, t);
-        e = 0.0;
+    __device__ __forceinline__ void fold(double qd, double qinv) {  // back to |r| <= q/2
+        const double c = __dsub_rn(__fma_rn(r, qinv, 6755399441055744.0), 6755399441055744.0);
+        r = __fma_rn(-c, qd, r);
     }
     __device__ __forceinline__ u64 reduce(double qd, double qinv) const {
-        const double t = __dadd_rn(r, e);
-        const double c = __dsub_rn(__fma_rn(t, qinv, 6755399441055744.0), 6755399441055744.0);
-        double v = __fma_rn(-c, qd, t);
+        const double c = __dsub_rn(__fma_rn(r, qinv, 6755399441055744.0), 6755399441055744.0);
+        double v = __fma_rn(-c, qd, r);
         if (v < 0.0) v = __dadd_rn(v, qd);
         if (v >= qd) v = __dsub_rn(v, qd);
         return (u64)__double_as_longlong(__dadd_rn(v, 4503599627370496.0)) & 0x000FFFFFFFFFFFFFull;

@@ -34,6 +34,7 @@ struct blb_matmul_plan {
     std::vector<std::vector<int>> baby;                 // per input: i >= 1 used
     std::vector<std::vector<int>> giant;                // per output: g >= 1 used
     std::vector<int32_t> rot_steps;
+    std::vector<char> same_next;                        // entry list of (b', g) == that of the next one
     int *d_ent = nullptr;                               // device: (b * B + i) per entry
     int *d_ent_start = nullptr;                         // device copy of ent_start
     int32_t *d_col_map = nullptr;
@@ -328,6 +329,144 @@ __global__ void __launch_bounds__(kTB + 32) k_mac_tma(const u64 *__restrict__ pt
     else mac_tma_consume<false>(ring, full, empty, n_e, out, kN, mc);
 }
 
+// Multi-output variant: a CTA accumulates kMacP outputs (b', g) that share the same (b, i) entry
+// list (so the same R tiles) for one (tile, limb): per pipeline stage one entry = kMacP
+// plaintext tiles + the two R tiles.  R is staged once per kMacP outputs instead of once per
+// output, so two thirds of the bytes in flight are the HBM plaintext stream (one third before):
+// the single-output kernel's consumers sat on the full barrier waiting for data.
+template <int PP, int STG>
+constexpr size_t mac4_smem() { return (size_t)STG * (PP + 2) * 512 * 8 + 2 * STG * 8; }
+
+template <bool SPLIT41, int kMacP, int kM4Stages>
+__device__ __forceinline__ void mac4_consume(const u64 *ring, uint64_t *full, uint64_t *empty, int n_e, int nP,
+                                             u64 *const *outs, long long kN, const ModConst &mc) {
+    using A = typename std::conditional<SPLIT41, Acc41, Acc128>::type;
+    using A1 = typename std::conditional<SPLIT41, AccF64, Acc128>::type;
+    const double qd = (double)mc.q, qinv = 1.0 / qd;
+    A a00[kMacP], a01[kMacP];
+    A1 a10[kMacP], a11[kMacP];
+#pragma unroll
+    for (int j = 0; j < kMacP; j++) { a00[j].zero(); a01[j].zero(); a10[j].zero(); a11[j].zero(); }
+    constexpr int kM4StageWords = (kMacP + 2) * 512;
+    const int t = threadIdx.x;
+    for (int s = 0; s < n_e; s++) {
+        const int slot = s % kM4Stages;
+        mbar_wait(&full[slot], (s / kM4Stages) & 1);
+        const u64 *st = ring + (size_t)slot * kM4StageWords;
+        const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + kMacP * 512 + 2 * t);
+        const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + (kMacP + 1) * 512 + 2 * t);
+#pragma unroll
+        for (int j = 0; j < kMacP; j++) {
+            if (j < nP) {
+                const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(st + j * 512 + 2 * t);
+                a00[j].mac(pv.x, r0.x); a01[j].mac(pv.y, r0.y);
+                if constexpr (SPLIT41) {
+                    a10[j].mac(pv.x, r1.x, qd, qinv); a11[j].mac(pv.y, r1.y, qd, qinv);
+                } else {
+                    a10[j].mac(pv.x, r1.x); a11[j].mac(pv.y, r1.y);
+                }
+            }
+        }
+        __syncwarp();
+        if ((t & 31) == 0) mbar_arrive(&empty[slot]);
+        if constexpr (!SPLIT41) {
+            if ((s & 63) == 63) {  // 64 products < 2^126
+#pragma unroll
+                for (int j = 0; j < kMacP; j++) { a00[j].fold(mc); a01[j].fold(mc); a10[j].fold(mc); a11[j].fold(mc); }
+            }
+        } else {
+            if ((s & 511) == 511) {  // 512 products: FP64 sums below 2^51
+#pragma unroll
+                for (int j = 0; j < kMacP; j++) { a10[j].fold(qd, qinv); a11[j].fold(qd, qinv); }
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kMacP; j++) {
+        if (j < nP) {
+            u64 *out = outs[j] + 2 * t;
+            *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00[j].reduce(mc), a01[j].reduce(mc));
+            if constexpr (SPLIT41)
+                *reinterpret_cast<ulonglong2 *>(out + kN) =
+                    make_ulonglong2(a10[j].reduce(qd, qinv), a11[j].reduce(qd, qinv));
+            else
+                *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10[j].reduce(mc), a11[j].reduce(mc));
+        }
+    }
+}
+
+template <int kMacP, int kM4Stages, int MINB>
+__global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const u64 *__restrict__ pt, const u64 *__restrict__ R,
+                                                       u64 *__restrict__ acc, const int *__restrict__ ent_r,
+                                                       const int *__restrict__ ent_start, int o0, int e_base, int n_o,
+                                                       int k, int logN, Primes pr) {
+    constexpr int kM4StageWords = (kMacP + 2) * 512;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    u64 *ring = reinterpret_cast<u64 *>(smraw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)kM4Stages * kM4StageWords);
+    uint64_t *empty = full + kM4Stages;
+    const int N = 1 << logN;
+    const int n_tiles = N / (2 * kTB);
+    const int n_grp = (n_o + kMacP - 1) / kMacP;
+    int bid = blockIdx.x;
+    const int og = bid % n_grp;
+    bid /= n_grp;
+    const int tile = bid % n_tiles;
+    const int l = bid / n_tiles;
+    const int oa = og * kMacP, nP = min(kMacP, n_o - oa);
+    const long long kN = (long long)k * N;
+    const int e_lo = ent_start[o0 + oa], n_e = ent_start[o0 + oa + 1] - e_lo;
+    const long long lx0 = (long long)l * N + tile * 2 * kTB;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kM4Stages; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kTB / 32);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x >= kTB) {  // producer warp
+        if (threadIdx.x == kTB) {
+            const u64 *pp[kMacP];
+#pragma unroll
+            for (int j = 0; j < kMacP; j++)
+                pp[j] = pt + (long long)(ent_start[o0 + oa + (j < nP ? j : 0)] - e_base) * kN + (long long)l * n_e * N +
+                        (long long)tile * n_e * 512;
+            for (int s = 0; s < n_e; s++) {
+                const int slot = s % kM4Stages;
+                if (s >= kM4Stages) mbar_wait(&empty[slot], ((s / kM4Stages) - 1) & 1);
+                u64 *st = ring + (size_t)slot * kM4StageWords;
+                mbar_expect_tx(&full[slot], (unsigned)(nP + 2) * 4096);
+                for (int j = 0; j < nP; j++) bulk_g2s(st + j * 512, pp[j] + (long long)s * 512, 4096, &full[slot]);
+                const int bi = ent_r[e_lo + s];
+                bulk_g2s(st + kMacP * 512, R + (long long)bi * 2 * kN + lx0, 4096, &full[slot]);
+                bulk_g2s(st + (kMacP + 1) * 512, R + ((long long)bi * 2 + 1) * kN + lx0, 4096, &full[slot]);
+            }
+        }
+        return;
+    }
+    u64 *outs[kMacP];
+#pragma unroll
+    for (int j = 0; j < kMacP; j++) outs[j] = acc + (long long)(oa + (j < nP ? j : 0)) * 2 * kN + lx0;
+    const ModConst &mc = pr.m[l];
+    if (mc.q < (1ull << 41)) mac4_consume<true, kMacP, kM4Stages>(ring, full, empty, n_e, nP, outs, kN, mc);
+    else mac4_consume<false, kMacP, kM4Stages>(ring, full, empty, n_e, nP, outs, kN, mc);
+}
+
+template <int PP, int STG, int MINB>
+static void launch_mac4(const u64 *pt, const u64 *R, u64 *acc, const int *ent_r, const int *ent_start, int o0,
+                        int e_base, int n_o, int k, int logN, const Primes &pr, int n_tiles, cudaStream_t st) {
+    static bool attr = false;
+    constexpr size_t smem = mac4_smem<PP, STG>();
+    if (!attr) {
+        cudaFuncSetAttribute(k_mac_tma4<PP, STG, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const size_t n_grp = (size_t)(n_o + PP - 1) / PP;
+    k_mac_tma4<PP, STG, MINB><<<(unsigned)(n_grp * n_tiles * k), kTB + 32, smem, st>>>(pt, R, acc, ent_r, ent_start, o0,
+                                                                                      e_base, n_o, k, logN, pr);
+}
+
 // scatter standard [cnt][k][N] plaintexts (entries e0..e0+cnt of the plan) into the blocked layout
 __global__ void k_block_pts(const u64 *src, u64 *dst, const int *ent_start, const int *ent_o, int e0, int e_base,
                             int k, int N) {
@@ -489,6 +628,12 @@ extern "C" blb_status blb_matmul_plan_create(const blb_params *P, int L, int w_r
     const size_t ne = pl->ent_b.size();
     std::vector<int> bi(ne);
     for (size_t e = 0; e < ne; e++) bi[e] = pl->ent_b[e] * pl->B + pl->ent_i[e];
+    const int n_og = pl->n_out * pl->G;
+    pl->same_next.assign(n_og, 0);
+    for (int o = 0; o + 1 < n_og; o++) {
+        const int a0 = pl->ent_start[o], a1 = pl->ent_start[o + 1], b1 = pl->ent_start[o + 2];
+        pl->same_next[o] = (a1 - a0 == b1 - a1) && std::equal(bi.begin() + a0, bi.begin() + a1, bi.begin() + a1);
+    }
     cudaError_t err = cudaSuccess;
     err = cudaMalloc(&pl->d_ent, sizeof(int) * (2 * ne + 1));
     if (err == cudaSuccess) err = cudaMalloc(&pl->d_ent_start, sizeof(int) * pl->ent_start.size());
@@ -751,7 +896,20 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
             if (n_o > 0) {
                 const int n_tiles = N / (2 * kTB);
                 cudaEvent_t t0 = blb_timing_begin(st);
-                if (P->mac_tma) {
+                // groups of PP consecutive (b', g) with one entry list -> the multi-output kernel
+                // (BLB_MAC_TMA: 1 = 2 outputs x 3 CTAs/SM (default), 4 = 4 outputs x 1 CTA/SM x 8 stages,
+                //  2 = single-output TMA kernel, 0 = k_mac_w)
+                const int PP = P->mac_tma == 4 ? 4 : 2;
+                bool grouped = P->mac_tma == 1 || P->mac_tma == 4;
+                for (int j = 0; j < n_o && grouped; j++)
+                    if (j % PP != PP - 1 && j + 1 < n_o && !pl->same_next[o0 + j]) grouped = false;
+                if (grouped && PP == 2)
+                    launch_mac4<2, 4, 3>(pt_dev, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
+                                         P->pr, n_tiles, st);
+                else if (grouped)
+                    launch_mac4<4, 8, 1>(pt_dev, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
+                                         P->pr, n_tiles, st);
+                else if (P->mac_tma) {
                     static bool attr = false;
                     if (!attr) {
                         cudaFuncSetAttribute(k_mac_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMacSmem);
