@@ -203,7 +203,7 @@ extern "C" void blb_params_destroy(blb_params *P) {
     for (auto &e : P->ev)
         if (e) cudaEventDestroy(e);
     cudaFree(P->d_tw);
-    cudaFree(P->d_tw16);
+    cudaFree(P->d_twd);
     cudaFree(P->d_zeta);
     cudaFree(P->d_slot_pos);
     cudaFree(P->d_bconv);
@@ -276,21 +276,16 @@ extern "C" blb_status blb_params_create(blb_params **out, int log_n, const uint6
         pos[j] = (int32_t)host_brv((e - 1) / 2, log_n);
         e = (e * 5) % (2 * N);
     }
-    // N = 2^16 kernel table: for primes < 2^41 the pair is (w, w / q) as doubles (FP64 butterflies, ntt.cu)
-    std::vector<u64> tw16(tw);
+    // FP64 NTT table (ntt.cu): the twiddles of the primes < 2^41 as doubles, [prime][2][N]
+    std::vector<double> twd((size_t)Lk * 2 * N, 0.0);
     for (int i = 0; i < Lk; i++) {
         if (P->mod[i] >= (1ull << 41)) continue;
-        for (size_t j = 0; j < (size_t)2 * N; j++) {
-            u64 *e2 = tw16.data() + (size_t)i * 4 * N + 2 * j;
-            const double wd = (double)e2[0], wq = wd / (double)P->mod[i];  // both exact / correctly rounded
-            memcpy(&e2[0], &wd, sizeof(double));
-            memcpy(&e2[1], &wq, sizeof(double));
-        }
+        for (size_t j = 0; j < (size_t)2 * N; j++) twd[(size_t)i * 2 * N + j] = (double)tw[(size_t)i * 4 * N + 2 * j];
     }
     cudaError_t err = cudaMalloc(&P->d_tw, sizeof(u64) * tw.size());
     if (err == cudaSuccess) err = cudaMemcpy(P->d_tw, tw.data(), sizeof(u64) * tw.size(), cudaMemcpyHostToDevice);
-    if (err == cudaSuccess) err = cudaMalloc(&P->d_tw16, sizeof(u64) * tw16.size());
-    if (err == cudaSuccess) err = cudaMemcpy(P->d_tw16, tw16.data(), sizeof(u64) * tw16.size(), cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMalloc(&P->d_twd, sizeof(double) * twd.size());
+    if (err == cudaSuccess) err = cudaMemcpy(P->d_twd, twd.data(), sizeof(double) * twd.size(), cudaMemcpyHostToDevice);
     if (err == cudaSuccess) err = cudaMalloc(&P->d_zeta, sizeof(double) * zeta.size());
     if (err == cudaSuccess)
         err = cudaMemcpy(P->d_zeta, zeta.data(), sizeof(double) * zeta.size(), cudaMemcpyHostToDevice);

@@ -213,7 +213,7 @@ struct blb_params {
     u64 psi[BLB_MAXP];
     Primes pr;                    // by-value copy for kernel args
     u64 *d_tw = nullptr;          // [K+np][2][N][2]: (fwd, fwd Shoup), (inv, inv Shoup) pairs, bit-reversed order
-    u64 *d_tw16 = nullptr;        // same, companion = bits of double(w / q) for primes < 2^41 (ntt16_pass)
+    double *d_twd = nullptr;      // [K+np][2][N] twiddles as doubles (fwd, inv) for the primes < 2^41 (FP64 NTT)
     double *d_zeta = nullptr;     // [N][4]: zeta^{brv(i)} as (re_hi, re_lo, im_hi, im_lo)
     int32_t *d_slot_pos = nullptr; // [N/2]: NTT-domain position k of slot j (brv(k) = (5^j - 1)/2)
     // FastBConv tables, see bconv_* in kernels.cu
@@ -271,6 +271,9 @@ struct RowBatch {
     // skip_alpha among the first skip_kmax limbs (ModUp: a digit's own limbs
     // are copied, not recomputed)
     int skip_alpha = 0, skip_beta = 1, skip_kmax = 0;
+    // optional limb selection (N = 2^16 kernels): nsel > 0 -> rows = n_polys * nsel, row -> limb sel[row % nsel]
+    int nsel = 0;
+    int sel[BLB_MAXP];
 };
 blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cudaStream_t st);
 

@@ -134,8 +134,8 @@ __device__ __forceinline__ void bfly(u64 &X, u64 &Y, u64 w, u64 wsh, u64 q, u64 
 // (64 DFMA/clk/SM) is separate from the fma-heavy pipe that the 64-bit integer multiplies of
 // the Shoup butterfly saturate, and residues < 2^41 with their lazy growth stay exact integers
 // in a double.  y * w mod q = (p - c q) + e with p = fl(y w), e = y w - p (exact, one fma),
-// c = round(y fl(w / q)) (one fma against 1.5 * 2^52): |c - y w / q| < 3/4, so the remainder
-// lies in (-3q/4, 3q/4) and every step is exact.  Values are signed and unreduced: forward
+// c = round(fl(y w) / q) (one fma against 1.5 * 2^52): |c - y w / q| < 5/8, so the remainder
+// lies in (-5q/8, 5q/8) and every step is exact (twiddles are plain doubles: 8-byte loads).  Values are signed and unreduced: forward
 // |x| grows by < q per stage (< 13 q after 16 stages), inverse sums double per stage and are
 // re-centred between the two passes, so all inputs stay below 2^50.
 // ---------------------------------------------------------------------------
@@ -143,10 +143,10 @@ constexpr double kTwo52 = 4503599627370496.0, kMagic = 6755399441055744.0;  // 2
 __device__ __forceinline__ double u2d(u64 x) {  // x < 2^52
     return __dsub_rn(__hiloint2double(0x43300000 | (int)(x >> 32), (int)(uint32_t)x), kTwo52);
 }
-__device__ __forceinline__ double mulr(double y, double w, double wq, double q) {
+__device__ __forceinline__ double mulr(double y, double w, double q, double qinv) {
     const double p = __dmul_rn(y, w);
     const double e = __fma_rn(y, w, -p);
-    const double c = __dsub_rn(__fma_rn(y, wq, kMagic), kMagic);
+    const double c = __dsub_rn(__fma_rn(p, qinv, kMagic), kMagic);  // round(p / q): |c - y w / q| < 5/8
     return __dadd_rn(__fma_rn(-c, q, p), e);
 }
 __device__ __forceinline__ double centre(double x, double q, double qinv) {  // x - round(x / q) q
@@ -160,15 +160,15 @@ __device__ __forceinline__ u64 canon(double x, double q, double qinv) {  // x mo
     return (u64)__double_as_longlong(__dadd_rn(r, kTwo52)) & 0x000FFFFFFFFFFFFFull;
 }
 template <bool INV>
-__device__ __forceinline__ void bfly_f64(double &X, double &Y, double w, double wq, double q) {
+__device__ __forceinline__ void bfly_f64(double &X, double &Y, double w, double q, double qinv) {
     if (!INV) {
-        const double r = mulr(Y, w, wq, q), x = X;
+        const double r = mulr(Y, w, q, qinv), x = X;
         X = __dadd_rn(x, r);
         Y = __dsub_rn(x, r);
     } else {
         const double s = __dadd_rn(X, Y), d = __dsub_rn(X, Y);
         X = s;
-        Y = mulr(d, w, wq, q);
+        Y = mulr(d, w, q, qinv);
     }
 }
 
@@ -177,13 +177,15 @@ __device__ __forceinline__ void bfly_f64(double &X, double &Y, double w, double 
 #endif
 template <bool INV, bool STRIDED, int PRO, int EPI, bool SMALL>
 __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u64 *__restrict__ tw_all,
-                                           const Primes &pr, int s0, int last, const NttFuse &fz, int p, int l) {
+                                           const double *__restrict__ twd_all, const Primes &pr, int s0, int last,
+                                           const NttFuse &fz, int p, int l) {
     constexpr int logN = 16, N = 1 << logN;
     u64 *a = rb.base + (long long)p * rb.poly_stride + (long long)(rb.limb0 + l) * N;
     const int pi = rb.prime[l];
     const u64 q = pr.m[pi].q, q2 = 2 * q;
     // interleaved (w, w') pairs: one 16-byte load per butterfly
     const ulonglong2 *twp = reinterpret_cast<const ulonglong2 *>(tw_all + (size_t)pi * 4 * N + (INV ? 2 * N : 0));
+    const double *twd = twd_all + (size_t)pi * 2 * N + (INV ? N : 0);
     const int t = threadIdx.x;
     const int c0 = blockIdx.x * 16;  // first column of the tile (lo0 for STRIDED, h0 otherwise)
     // A mapping (coalesced global access)
@@ -233,12 +235,12 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
         for (int m = 0; m < 16; m++) {
             if (m & dist) continue;
             const int widx = (1 << s) + (hA << r) + (m >> (4 - r));
-            const ulonglong2 tv = twp[widx];
-            if constexpr (SMALL)
-                bfly_f64<INV>(v[m], v[m + dist], __longlong_as_double((long long)tv.x),
-                              __longlong_as_double((long long)tv.y), qd);
-            else
+            if constexpr (SMALL) {
+                bfly_f64<INV>(v[m], v[m + dist], twd[widx], qd, qinv);
+            } else {
+                const ulonglong2 tv = twp[widx];
                 bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q2);
+            }
         }
     };
     auto roundB = [&](int r) {
@@ -248,12 +250,12 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
         for (int m = 0; m < 16; m++) {
             if (m & dist) continue;
             const int widx = (1 << s) + (hB << r) + ((16 * tcB + m) >> (8 - r));
-            const ulonglong2 tv = twp[widx];
-            if constexpr (SMALL)
-                bfly_f64<INV>(v[m], v[m + dist], __longlong_as_double((long long)tv.x),
-                              __longlong_as_double((long long)tv.y), qd);
-            else
+            if constexpr (SMALL) {
+                bfly_f64<INV>(v[m], v[m + dist], twd[widx], qd, qinv);
+            } else {
+                const ulonglong2 tv = twp[widx];
                 bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q2);
+            }
         }
     };
     if (!INV) {
@@ -315,7 +317,7 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
         for (int m = 0; m < 16; m++) {
             u64 x;
             if constexpr (SMALL) {
-                if (last) x = canon(INV ? mulr(v[m], (double)mc.ninv, (double)mc.ninv / qd, qd) : v[m], qd, qinv);
+                if (last) x = canon(INV ? mulr(v[m], (double)mc.ninv, qd, qinv) : v[m], qd, qinv);
                 else x = to_bits(INV ? centre(v[m], qd, qinv) : v[m]);  // inverse sums re-centred for pass 2
             } else {
                 x = v[m];
@@ -336,20 +338,62 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
     }
 }
 
-template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0>
-__global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_pass(RowBatch rb, const u64 *__restrict__ tw_all, Primes pr, int s0,
-                                                  int last, const NttFuse fz) {
-    __shared__ u64 sm[16 * 256];
+__device__ __forceinline__ bool ntt16_row(const RowBatch &rb, int &p, int &l) {
     const int row = blockIdx.y;
-    const int p = row / rb.limbs, l = row - p * rb.limbs;
+    if (rb.nsel > 0) {
+        p = row / rb.nsel;
+        l = rb.sel[row - p * rb.nsel];
+    } else {
+        p = row / rb.limbs;
+        l = row - p * rb.limbs;
+    }
     if (rb.skip_alpha) {
         const int dig = p % rb.skip_beta;
-        if (l < rb.skip_kmax && l >= dig * rb.skip_alpha && l < (dig + 1) * rb.skip_alpha) return;
+        if (l < rb.skip_kmax && l >= dig * rb.skip_alpha && l < (dig + 1) * rb.skip_alpha) return false;
     }
-    if (pr.m[rb.prime[l]].q < (1ull << 41)) ntt16_body<INV, STRIDED, PRO, EPI, true>(sm, rb, tw_all, pr, s0, last, fz, p, l);
-    else ntt16_body<INV, STRIDED, PRO, EPI, false>(sm, rb, tw_all, pr, s0, last, fz, p, l);
+    return true;
+}
+#ifndef BLB_NTT_F64_MINB
+#define BLB_NTT_F64_MINB 3
+#endif
+// integer (Shoup) kernel for the primes >= 2^41, FP64 kernel for the others; a launch covers
+// rows of one kind (launch_ntt splits a mixed batch with RowBatch::sel)
+template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0>
+__global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_int(RowBatch rb, const u64 *__restrict__ tw_all,
+                                                                const double *__restrict__ twd, Primes pr, int s0,
+                                                                int last, const NttFuse fz) {
+    __shared__ u64 sm[16 * 256];
+    int p, l;
+    if (!ntt16_row(rb, p, l)) return;
+    ntt16_body<INV, STRIDED, PRO, EPI, false>(sm, rb, tw_all, twd, pr, s0, last, fz, p, l);
+}
+template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0>
+__global__ void __launch_bounds__(256, BLB_NTT_F64_MINB) ntt16_f64(RowBatch rb, const u64 *__restrict__ tw_all,
+                                                                    const double *__restrict__ twd, Primes pr, int s0,
+                                                                    int last, const NttFuse fz) {
+    __shared__ u64 sm[16 * 256];
+    int p, l;
+    if (!ntt16_row(rb, p, l)) return;
+    ntt16_body<INV, STRIDED, PRO, EPI, true>(sm, rb, tw_all, twd, pr, s0, last, fz, p, l);
 }
 
+// split the limbs of a batch by prime size: out[0] = FP64 rows (q < 2^41), out[1] = integer rows
+static int split_rows(const blb_params *P, const RowBatch &rb, RowBatch out[2]) {
+    RowBatch f = rb, g = rb;
+    f.nsel = 0; g.nsel = 0;
+    for (int l = 0; l < rb.limbs; l++) {
+        if (P->mod[rb.prime[l]] < (1ull << 41)) f.sel[f.nsel++] = l;
+        else g.sel[g.nsel++] = l;
+    }
+    int n = 0;
+    if (f.nsel) { if (f.nsel == rb.limbs) f.nsel = 0; out[n++] = f; }
+    if (g.nsel) { if (g.nsel == rb.limbs) g.nsel = 0; out[n++] = g; }
+    return n;
+}
+static inline bool rb_small(const blb_params *P, const RowBatch &r) {
+    return P->mod[r.prime[r.nsel ? r.sel[0] : 0]] < (1ull << 41);
+}
+static inline int rb_rows(const RowBatch &r) { return r.n_polys * (r.nsel ? r.nsel : r.limbs); }
 
 }  // namespace
 
@@ -382,16 +426,31 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
         return BLB_OK;
     }
     if (logN == 16) {
-        dim3 g(16, rows);
         const NttFuse fz{};
-        if (!inverse) {
-            ntt16_pass<false, true><<<g, 256, 0, st>>>(rb, P->d_tw16, P->pr, 0, 0, fz);
-            ntt16_pass<false, false><<<g, 256, 0, st>>>(rb, P->d_tw16, P->pr, 8, 1, fz);
-        } else {
-            ntt16_pass<true, false><<<g, 256, 0, st>>>(rb, P->d_tw16, P->pr, 8, 0, fz);
-            ntt16_pass<true, true><<<g, 256, 0, st>>>(rb, P->d_tw16, P->pr, 0, 1, fz);
+        RowBatch parts[2];
+        const int np2 = split_rows(P, rb, parts);
+        for (int h = 0; h < np2; h++) {
+            const RowBatch &r = parts[h];
+            dim3 g(16, rb_rows(r));
+            if (rb_small(P, r)) {
+                if (!inverse) {
+                    ntt16_f64<false, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
+                    ntt16_f64<false, false><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
+                } else {
+                    ntt16_f64<true, false><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 0, fz);
+                    ntt16_f64<true, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 1, fz);
+                }
+            } else {
+                if (!inverse) {
+                    ntt16_int<false, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
+                    ntt16_int<false, false><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
+                } else {
+                    ntt16_int<true, false><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 0, fz);
+                    ntt16_int<true, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 1, fz);
+                }
+            }
         }
-        BLB_COUNT_LAUNCH(2);
+        BLB_COUNT_LAUNCH(2 * np2);
         blb_timing_end(1, t0, st, alg);
         BLB_CHECK_LAUNCH();
         return BLB_OK;
@@ -429,12 +488,24 @@ blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool invers
     }
     BLB_COUNT(2, rows);
     cudaEvent_t t0 = blb_timing_begin(st);
-    dim3 g(16, rows);
-    if (fz.pro == 1) ntt16_pass<false, true, 1, 0><<<g, 256, 0, st>>>(rb, P->d_tw16, P->pr, 0, 0, fz);
-    else ntt16_pass<false, true, 0, 0><<<g, 256, 0, st>>>(rb, P->d_tw16, P->pr, 0, 0, fz);
-    if (fz.epi == 1) ntt16_pass<false, false, 0, 1><<<g, 256, 0, st>>>(rb, P->d_tw16, P->pr, 8, 1, fz);
-    else ntt16_pass<false, false, 0, 0><<<g, 256, 0, st>>>(rb, P->d_tw16, P->pr, 8, 1, fz);
-    BLB_COUNT_LAUNCH(2);
+    RowBatch parts[2];
+    const int np2 = split_rows(P, rb, parts);
+    for (int h = 0; h < np2; h++) {
+        const RowBatch &r = parts[h];
+        dim3 g(16, rb_rows(r));
+        if (rb_small(P, r)) {
+            if (fz.pro == 1) ntt16_f64<false, true, 1, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
+            else ntt16_f64<false, true, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
+            if (fz.epi == 1) ntt16_f64<false, false, 0, 1><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
+            else ntt16_f64<false, false, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
+        } else {
+            if (fz.pro == 1) ntt16_int<false, true, 1, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
+            else ntt16_int<false, true, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
+            if (fz.epi == 1) ntt16_int<false, false, 0, 1><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
+            else ntt16_int<false, false, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
+        }
+    }
+    BLB_COUNT_LAUNCH(2 * np2);
     blb_timing_end(1, t0, st, (double)rows * 16.0 * (1 << 16));
     BLB_CHECK_LAUNCH();
     return BLB_OK;
