@@ -164,9 +164,11 @@ blb_status blb_decode(const blb_params *params, const uint64_t *pt, int level, d
 blb_status blb_keys_create(const blb_params *params, blb_keys **out);
 void blb_keys_destroy(blb_keys *keys);
 
-/* Copy one switching key swk[beta_top][2][nq+np][N] (device, NTT form;
- * [.][0] = b, [.][1] = a, beta_top = ceil(nq/alpha)) into `keys` under
- * Galois element `galois` (0 = relinearisation key for s^2). */
+/* Copy one switching key swk[beta_top][2][nq+np][N] (device or host, NTT form, natural
+ * coefficient order; [.][0] = b, [.][1] = a, beta_top = ceil(nq/alpha)) into `keys` under
+ * Galois element `galois` (0 = relinearisation key for s^2).  Rotation keys are stored
+ * pre-permuted (row y holds entry perm_{g^-1}(y)) so the key-switch inner product reads
+ * keys and digits contiguously; the storage is internal to the library. */
 blb_status blb_keys_add(blb_keys *keys, uint32_t galois, const uint64_t *swk, void *stream);
 int blb_keys_has(const blb_keys *keys, uint32_t galois);
 

@@ -435,13 +435,51 @@ static u64 *keys_slot(blb_keys *K, uint32_t g, blb_status *st) {
     return d;
 }
 
+// Rotation keys are stored pre-permuted for the key-switch inner product (kernels.cu):
+// k'[y] = k[perm_{g^-1}(y)] on every row, so the kernel reads keys and extended digits contiguously
+// and scatters only its two outputs.  The relinearisation key (g = 0) is stored as is.
+namespace {
+__global__ void k_key_perm(const u64 *in, u64 *out, uint32_t ginv, int logN) {
+    const int y = blockIdx.x * blockDim.x + threadIdx.x;
+    const long long row = blockIdx.y;
+    const int N = 1 << logN;
+    if (y >= N) return;
+    out[row * N + y] = in[row * N + galois_perm((uint32_t)y, ginv, logN)];
+}
+uint32_t host_galois_inverse(uint32_t g, int logN) {
+    const u64 m = 2ull << logN;
+    u64 r = 1, b = g % m, e = (1ull << logN) - 1;
+    while (e) {
+        if (e & 1) r = r * b % m;
+        b = b * b % m;
+        e >>= 1;
+    }
+    return (uint32_t)r;
+}
+}  // namespace
+static blb_status store_key(const blb_params *P, u64 *slot, const u64 *natural, uint32_t g, cudaStream_t st) {
+    const size_t n = key_elems(P);
+    if (g == 0 || g == 1) {
+        if (slot != natural) BLB_CUDA_TRY(cudaMemcpyAsync(slot, natural, sizeof(u64) * n, cudaMemcpyDefault, st));
+        return BLB_OK;
+    }
+    u64 *tmp = nullptr;
+    BLB_CUDA_TRY(cudaMallocAsync(&tmp, sizeof(u64) * n, st));
+    BLB_CUDA_TRY(cudaMemcpyAsync(tmp, natural, sizeof(u64) * n, cudaMemcpyDefault, st));
+    const unsigned rows = (unsigned)(n / P->N);
+    k_key_perm<<<dim3((P->N + 255) / 256, rows), 256, 0, st>>>(tmp, slot, host_galois_inverse(g, P->logN), P->logN);
+    BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    cudaFreeAsync(tmp, st);
+    return BLB_OK;
+}
+
 extern "C" blb_status blb_keys_add(blb_keys *K, uint32_t galois, const uint64_t *swk, void *stream) {
     if (!K || !swk) return BLB_E_INVALID_ARG;
     blb_status s = BLB_OK;
     u64 *d = keys_slot(K, galois, &s);
     if (!d) return s;
-    BLB_CUDA_TRY(cudaMemcpyAsync(d, swk, sizeof(u64) * key_elems(K->params), cudaMemcpyDefault, (cudaStream_t)stream));
-    return BLB_OK;
+    return store_key(K->params, d, swk, galois, (cudaStream_t)stream);
 }
 extern "C" int blb_keys_has(const blb_keys *K, uint32_t galois) {
     if (!K) return 0;
@@ -495,6 +533,7 @@ extern "C" blb_status blb_keygen(const blb_params *P, const uint8_t seed[32], co
                 status = blb_launch_keygen_combine(P, b, a, s, N, Lk, prime, g == 0 ? 1u : g, g == 0,
                                                    gadget + (size_t)j * Lk, st);
         }
+        if (status == BLB_OK) status = store_key(P, key, key, g, st);  // pre-permuted storage
         if (status != BLB_OK) break;
     }
     cudaFreeAsync(gadget, st);

@@ -298,6 +298,7 @@ struct KsJob {
     const u64 *c0;    // [k][N] input c0 (rotation: sigma_g(c0) is added), nullable (relin: add as is)
     u64 *out;         // [2][k][N]
     uint32_t galois;  // 1 = identity
+    uint32_t galois_inv;  // g^{-1} mod 2N (filled by the key-switch launcher)
     int add_mode;     // 0 = none, 1 = add sigma_g(c0) to out0 (rotation), 2 = add c0 / c1 pair (relin)
     const u64 *c1_add;
 };

@@ -234,7 +234,9 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
     const int E = k + np, Lk = K + np;
     const int pm = m < k ? m : K + (m - k);
     const KsJob &J0 = jobs.j[t0];
-    const uint32_t src = J0.galois == 1 ? (uint32_t)x : galois_perm(x, J0.galois, logN);
+    // rotation keys are stored pre-permuted (k'[y] = k[perm_{g^-1}(y)], blb_keys): every load is
+    // contiguous and only the two outputs are scattered, to x = perm_{g^-1}(y)
+    const uint32_t dst = J0.galois == 1 ? (uint32_t)x : galois_perm(x, J0.galois_inv, logN);
     const ModConst &mc = pr.m[pm];
     using A1 = typename std::conditional<SMALL, AccF64, Acc128>::type;
     const double qd = (double)mc.q, qinv = 1.0 / qd;
@@ -253,7 +255,7 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
         for (int q = 0; q < kKsGroup; q++) {
             if (q < cnt) {
                 u64 e[BETA > 0 ? BETA : 1];
-                const u64 *ext = jobs.j[t0 + q].ext + (long long)m * N + src;
+                const u64 *ext = jobs.j[t0 + q].ext + (long long)m * N + x;
 #pragma unroll
                 for (int j = 0; j < BETA; j++) e[j] = ext[(long long)j * E * N];
 #pragma unroll
@@ -271,7 +273,7 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
 #pragma unroll
             for (int q = 0; q < kKsGroup; q++) {
                 if (q < cnt) {
-                    const u64 e = jobs.j[t0 + q].ext[((long long)j * E + m) * N + src];
+                    const u64 e = jobs.j[t0 + q].ext[((long long)j * E + m) * N + x];
                     a0[q].mac(e, kb);
                     if constexpr (SMALL) a1[q].mac(e, ka, qd, qinv);
                     else a1[q].mac(e, ka);
@@ -290,14 +292,14 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
             if (EXT) {
                 const KsJob &J = jobs.j[t];
                 u64 r0 = a0[q].reduce(mc);
-                if (m < k) r0 = addmod(r0, shoup(J.c0[(long long)m * N + src], pq.v[m], pq.sh[m], mc.q), mc.q);
-                J.out[(long long)m * N + x] = r0;
+                if (m < k) r0 = addmod(r0, shoup(J.c0[(long long)m * N + x], pq.v[m], pq.sh[m], mc.q), mc.q);
+                J.out[(long long)m * N + dst] = r0;
                 u64 r1 = a1r(q);
-                if (m < k && J.c1_add) r1 = addmod(r1, shoup(J.c1_add[(long long)m * N + src], pq.v[m], pq.sh[m], mc.q), mc.q);
-                J.out[((long long)E + m) * N + x] = r1;
+                if (m < k && J.c1_add) r1 = addmod(r1, shoup(J.c1_add[(long long)m * N + x], pq.v[m], pq.sh[m], mc.q), mc.q);
+                J.out[((long long)E + m) * N + dst] = r1;
             } else {
-                u[(((long long)t * 2 + 0) * E + m) * N + x] = a0[q].reduce(mc);
-                u[(((long long)t * 2 + 1) * E + m) * N + x] = a1r(q);
+                u[(((long long)t * 2 + 0) * E + m) * N + dst] = a0[q].reduce(mc);
+                u[(((long long)t * 2 + 1) * E + m) * N + dst] = a1r(q);
             }
         }
     }
@@ -512,7 +514,18 @@ size_t keyswitch_scratch_elems(const blb_params *P, int level, int n_jobs) {
 }
 
 // group jobs that share a key (stable order by key), <= kKsGroup per group
-static void group_jobs(const KsJob *jobs, int n, KsJobs &J, KsGroups &G) {
+// g^{-1} mod 2N (g odd): g^(N-1), the group (Z/2N)^* having exponent dividing N
+static uint32_t galois_inverse(uint32_t g, int logN) {
+    const u64 m = 2ull << logN;
+    u64 r = 1, b = g % m, e = (1ull << logN) - 1;
+    while (e) {
+        if (e & 1) r = r * b % m;
+        b = b * b % m;
+        e >>= 1;
+    }
+    return (uint32_t)r;
+}
+static void group_jobs(const KsJob *jobs, int n, KsJobs &J, KsGroups &G, int logN) {
     bool used[kMaxJobs] = {false};
     int t = 0;
     G.n = 0;
@@ -523,7 +536,9 @@ static void group_jobs(const KsJob *jobs, int n, KsJobs &J, KsGroups &G) {
         for (int b = a; b < n && cnt < kKsGroup; b++)
             if (!used[b] && jobs[b].key == jobs[a].key && jobs[b].galois == jobs[a].galois) {
                 used[b] = true;
-                J.j[t++] = jobs[b];
+                J.j[t] = jobs[b];
+                J.j[t].galois_inv = galois_inverse(jobs[b].galois, logN);
+                t++;
                 cnt++;
             }
     }
@@ -608,7 +623,7 @@ blb_status launch_keyswitch(const blb_params *P, int level, const KsJob *jobs, i
     }
     KsJobs J{};
     KsGroups G{};
-    group_jobs(jobs, n, J, G);
+    group_jobs(jobs, n, J, G, P->logN);
     BLB_TRY(ks_inner_launch<false>(P, level, J, G, u, st));
     BLB_TRY(moddown_launch(P, level, J, n, u, conv, st));
     BLB_COUNT(1, n);
@@ -620,7 +635,7 @@ blb_status launch_keyswitch_ext(const blb_params *P, int level, const KsJob *job
     if (n > kMaxJobs) return BLB_E_INVALID_ARG;
     KsJobs J{};
     KsGroups G{};
-    group_jobs(jobs, n, J, G);
+    group_jobs(jobs, n, J, G, P->logN);
     BLB_TRY(ks_inner_launch<true>(P, level, J, G, nullptr, st));
     BLB_COUNT(1, n);
     return BLB_OK;
