@@ -314,6 +314,7 @@ def main():
     mac = blb.timing_read(blb.TIMING_MAC)
     ntt = blb.timing_read(blb.TIMING_NTT)
     ksi = blb.timing_read(blb.TIMING_KS_INNER)
+    mmac = blb.timing_read(blb.TIMING_MASK_MAC)
     ms_step = ms_total / args.steps
     if world > 1:
         t = torch.tensor([ms_step], device="cuda", dtype=torch.float64)
@@ -373,7 +374,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded N(0,1) activations, N(0,0.04^2) weights)",
         "config": config_dict(dims, world),
-        "roofline": {"kernel": "k_mac (ct-pt MAC, row a3)", "bound": "hbm", "achieved": mac_gbs, "peak": hbm_peak,
+        "roofline": {"kernel": "k_mac_tma4 (ct-pt weight MAC, row a3)", "bound": "hbm", "achieved": mac_gbs, "peak": hbm_peak,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
                      "unit": "GB/s", "frac": (mac_gbs / hbm_peak) if mac_gbs else None, "traffic": traffic,
                      "alg_bytes_per_launch": mac["alg_bytes"] / max(1, mac["launches"]),
@@ -384,6 +385,9 @@ def main():
                 "share_of_step": ntt["ms"] / ms_total if ms_total else None, "launches": ntt["launches"]},
         "ks_inner": {"alg_gbs": ksi["alg_bytes"] / (ksi["ms"] * 1e-3) / 1e9 if ksi["ms"] else None,
                      "share_of_step": ksi["ms"] / ms_total if ms_total else None},
+        "mask_mac": {"kernel": "k_mac (ct-ct masks, rows a7/f1)",
+                     "alg_gbs": mmac["alg_bytes"] / (mmac["ms"] * 1e-3) / 1e9 if mmac["ms"] else None,
+                     "share_of_step": mmac["ms"] / ms_total if ms_total else None},
         "gpu_launches": ctr["launches"],
         "counters_per_step": {k: v / args.steps for k, v in ctr.items()},
         "clocks": clk,

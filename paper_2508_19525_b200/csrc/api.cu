@@ -64,7 +64,7 @@ struct TimedLaunch {
 };
 std::mutex g_tmu;
 bool g_timing = false;
-std::vector<TimedLaunch> g_tl[3];
+std::vector<TimedLaunch> g_tl[4];
 std::vector<cudaEvent_t> g_pool;
 cudaEvent_t take_event() {
     if (!g_pool.empty()) {
@@ -103,7 +103,7 @@ extern "C" void blb_timing_reset(void) {
     }
 }
 extern "C" blb_status blb_timing_read(int cat, double *total_ms, uint64_t *launches, double *bytes) {
-    if (cat < 0 || cat > 2) return BLB_E_INVALID_ARG;
+    if (cat < 0 || cat > 3) return BLB_E_INVALID_ARG;
     std::lock_guard<std::mutex> lk(g_tmu);
     double ms = 0, by = 0;
     for (auto &t : g_tl[cat]) {

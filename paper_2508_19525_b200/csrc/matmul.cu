@@ -515,7 +515,7 @@ blb_status launch_mac(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc
                                                                 k, kq < 0 ? k : kq, P->K, P->logN, P->pr);
     BLB_COUNT_LAUNCH(1);
     BLB_COUNT(3, n_entries);
-    blb_timing_end(0, t0, st, (double)n_entries * k * N * 8.0);
+    blb_timing_end(3, t0, st, (double)n_entries * k * N * 8.0);  // category 3: ct-ct mask MAC
     BLB_CHECK_LAUNCH();
     return BLB_OK;
 }
