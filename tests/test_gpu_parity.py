@@ -517,3 +517,40 @@ def test_share_decode_bit_exact(name, request):
     for xs, ft, s_out in ((x, 30, 18), (m, 30, 18), (m, 40, 0), (x, 52, 126)):
         got = u64(blb.share_decode(pair.g, dev(xs), ft, s_out))
         assert np.array_equal(got, O.share_decode(pair.o, xs, ft, s_out))
+
+
+# ---------------------------------------------------------------- error behaviour (include/blb.h)
+def test_api_error_statuses(toy):
+    """Each documented error status is raised before any launch, and degenerate calls are no-ops."""
+    g = toy.g
+    a = blb.Ciphertext(dev(rand_limbs(toy, 2, [0, 1, 2], 80)), 2, 2.0 ** 40)
+    b1 = blb.Ciphertext(dev(rand_limbs(toy, 2, [0, 1], 81)), 1, 2.0 ** 40)
+    with pytest.raises(blb.BLBError) as e:          # level mismatch
+        blb.add(g, a, b1)
+    assert e.value.status == 4
+    b2 = blb.Ciphertext(dev(rand_limbs(toy, 2, [0, 1, 2], 82)), 2, 2.0 ** 43)
+    with pytest.raises(blb.BLBError) as e:          # scale mismatch > 1 bit
+        blb.add(g, a, b2)
+    assert e.value.status == 5
+    z0 = blb.Ciphertext(dev(rand_limbs(toy, 2, [0], 83)), 0, 2.0 ** 40)
+    with pytest.raises(blb.BLBError):               # rescale below level 0
+        blb.rescale(g, z0)
+    keys = blb.Keys(g)
+    with pytest.raises(blb.BLBError) as e:          # rotation without its key
+        blb.rotate(g, keys, a, 3)
+    assert e.value.status == 3
+    plan = blb.MatmulPlan(g, 16, 16, 16, bsgs_B=16)
+    with pytest.raises(blb.BLBError) as e:          # input at the wrong level
+        plan(keys, [b1], plan.encode_weights(np.eye(16)))
+    assert e.value.status in (3, 4)
+    # degenerate inputs
+    m, s = blb.ckks_to_mpc(g, [], bytes(32), 0)
+    assert m.numel() == 0 and s.numel() == 0
+    x = dev(np.zeros(toy.N, dtype=np.uint64))
+    for w in (0, 65):
+        with pytest.raises(blb.BLBError) as e:
+            blb.share_to_rns(g, x, w, False, 2)
+        assert e.value.status == 1
+    with pytest.raises(blb.BLBError) as e:
+        blb.share_decode(g, dev(np.zeros((toy.N, 2), dtype=np.uint64)), 60, 0)
+    assert e.value.status == 1
