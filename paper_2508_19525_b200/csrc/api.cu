@@ -684,8 +684,9 @@ extern "C" blb_status blb_ckks_to_mpc(const blb_params *P, const blb_ct *in, int
                                       uint64_t first_ct_id, uint64_t *masked, uint64_t *share, void *ws,
                                       size_t ws_bytes, void *stream) {
     (void)ws; (void)ws_bytes;
-    if (!P || !in || n_ct < 0 || !mask_key || !masked || !share) return BLB_E_INVALID_ARG;
-    if (n_ct == 0) return BLB_OK;
+    if (!P || n_ct < 0) return BLB_E_INVALID_ARG;
+    if (n_ct == 0) return BLB_OK;  // nothing to mask (output pointers may be null)
+    if (!in || !mask_key || !masked || !share) return BLB_E_INVALID_ARG;
     if ((first_ct_id + (u64)n_ct) >> 56) {
         blb_set_error("blb_ckks_to_mpc: ct ids must be < 2^56");
         return BLB_E_INVALID_ARG;
