@@ -73,10 +73,16 @@ __global__ void k_mask_slots(const MaskDesc *descs, int m0, QKDev q, double *slo
     slots[(long long)e * q.n + s] = v ? 1.0 : 0.0;
 }
 
-// D[o][0..2] = sum_j (a0 b0, a0 b1 + a1 b0, a1 b1) with a = Qp[u*J + j], b = Kp[i*J + j], o = u*B + i
-__global__ void k_tensor_sum(const u64 *Qp, const u64 *Kp, u64 *D, Primes pr, int J, int B, int k, int N) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int l = blockIdx.y, o = blockIdx.z;
+// D[o][0..2] = sum_j (a0 b0, a0 b1 + a1 b0, a1 b1) with a = Qp[u*J + j], b = Kp[i*J + j], o = u*B + i.
+// 1-D grid with the output o fastest: the CTAs in flight cover all (u, i) of a few (tile, limb)
+// slices, so each Q_u / K'_i tile is read from DRAM once and reused through L2 (B and G times).
+__global__ void k_tensor_sum(const u64 *Qp, const u64 *Kp, u64 *D, Primes pr, int J, int B, int k, int N,
+                             int n_o) {
+    int bid = blockIdx.x;
+    const int o = bid % n_o;
+    bid /= n_o;
+    const int l = bid % k;
+    const int x = (bid / k) * blockDim.x + threadIdx.x;
     if (x >= N) return;
     const int u = o / B, i = o - u * B;
     const long long kN = (long long)k * N, lx = (long long)l * N + x;
@@ -518,7 +524,8 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
         BLB_TRY(launch_moddown_rescale(P, lvl, W + w.qacc, (G - 1) * J, W + w.qp + (size_t)J * ct_k1, conv, st));
     }
     // 3. products summed over j, relinearisation (one per (u, i)), rescale
-    k_tensor_sum<<<gx(N, k1, G * B), kTB, 0, st>>>(W + w.qp, W + w.kp, W + w.d, P->pr, J, B, k1, N);
+    k_tensor_sum<<<(unsigned)((size_t)((N + kTB - 1) / kTB) * k1 * G * B), kTB, 0, st>>>(W + w.qp, W + w.kp, W + w.d,
+                                                                                       P->pr, J, B, k1, N, G * B);
     BLB_COUNT_LAUNCH(1);
     BLB_COUNT(3, (size_t)G * B * J);
     BLB_CHECK_LAUNCH();

@@ -554,3 +554,25 @@ def test_api_error_statuses(toy):
     with pytest.raises(blb.BLBError) as e:
         blb.share_decode(g, dev(np.zeros((toy.N, 2), dtype=np.uint64)), 60, 0)
     assert e.value.status == 1
+
+
+# ---------------------------------------------------------------- row f4: batched inputs
+def test_batched_inputs_bit_exact(toy):
+    """Row f4 (App. D): B = 4 same-user inputs of 8 tokens packed along the spatial
+    dimension (L' = 32 rows per block) run through one ct-pt MatMul plan; bit-exact against the
+    oracle and each input's rows decode to its own X_b W."""
+    from paper_2508_19525_b200 import packing
+    Bt, L, D, Dout = 4, 8, 64, 48
+    Xs = [bi.uniform(100 + b, (L, D), -1, 1) for b in range(Bt)]
+    W = bi.normal(99, (D, Dout), 0.05)
+    X = np.concatenate(Xs, axis=0)                      # (B L) x D: spatial-first with L' = B L
+    plan_o = mm.plan_spatial(W, Bt * L, toy.n, 8)
+    plan_g = blb.MatmulPlan(toy.g, Bt * L, D, Dout, bsgs_B=8)
+    zs = list(packing.spatial_slots(X, toy.n))
+    okeys, sk, oout, gout = run_both(toy, plan_o, plan_g, zs, W)
+    for a, b in zip(gout, oout):
+        assert np.array_equal(u64(a.data), b.data)
+    dec = np.stack([toy.g.decode(blb.decrypt(toy.g, sk, c), c.scale).cpu().numpy() for c in gout])
+    Y = packing.spatial_unslots(dec, Bt * L, Dout)
+    for b in range(Bt):
+        assert np.abs(Y[b * L:(b + 1) * L] - Xs[b] @ W).max() < 1e-5
