@@ -91,6 +91,14 @@ void blb_timing_end(int cat, cudaEvent_t start, cudaStream_t st, double bytes) {
     cudaEventRecord(e, st);
     g_tl[cat].push_back({start, e, bytes});
 }
+int blb_indep_batch() {
+    static int b = [] {
+        int v = 6;
+        if (const char *e = getenv("BLB_INDEP_BATCH")) v = atoi(e);
+        return v < 1 ? 1 : (v > kMaxJobs ? kMaxJobs : v);
+    }();
+    return b;
+}
 extern "C" void blb_timing_enable(int on) {
     std::lock_guard<std::mutex> lk(g_tmu);
     g_timing = on != 0;

@@ -282,6 +282,10 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
 // pointers, n <= kMaxJobs) -> ext [n][beta][E][N] (contiguous, NTT), using
 // coef_scratch [n][k][N].
 constexpr int kMaxJobs = 32;
+// independent rotations (each with its own ModUp) are key-switched in batches of this many jobs so
+// their extended digits (beta (k+np) N 8 bytes each, 15.7 MB at k = 5) are still in L2 when the inner
+// product reads them (env BLB_INDEP_BATCH overrides, 1..kMaxJobs)
+int blb_indep_batch();
 blb_status launch_modup(const blb_params *P, int level, const u64 *const *c1_ntt, int n, u64 *ext,
                         u64 *coef_scratch, cudaStream_t st);
 inline int blb_beta(const blb_params *P, int level) { return (level + 1 + P->alpha - 1) / P->alpha; }

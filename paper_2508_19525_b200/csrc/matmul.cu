@@ -951,8 +951,9 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
             for (int t = c0; t < c0 + cn; t++)
                 if (std::binary_search(pl->giant[out_first + t].begin(), pl->giant[out_first + t].end(), g))
                     gj.push_back({t, g});
-        for (size_t j0 = 0; j0 < gj.size(); j0 += kMaxJobs) {
-            const int cnt = (int)std::min<size_t>(kMaxJobs, gj.size() - j0);
+        const int gb = blb_indep_batch();
+        for (size_t j0 = 0; j0 < gj.size(); j0 += gb) {
+            const int cnt = (int)std::min<size_t>(gb, gj.size() - j0);
             std::vector<const u64 *> c1(cnt);
             std::vector<KsJob> jobs(cnt);
             AccJobs aj{};

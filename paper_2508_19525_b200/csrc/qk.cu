@@ -420,8 +420,9 @@ static blb_status rotate_independent_ext(const blb_params *P, const blb_keys *ke
                                          const std::vector<const u64 *> &in, const std::vector<int32_t> &steps,
                                          const std::vector<u64 *> &out, u64 *ext, u64 *coef, cudaStream_t st) {
     const int k = level + 1, N = P->N, E = k + P->np, beta = blb_beta(P, level);
-    for (size_t t0 = 0; t0 < in.size(); t0 += kMaxJobs) {
-        const int cnt = (int)std::min<size_t>(kMaxJobs, in.size() - t0);
+    const int ib = blb_indep_batch();
+    for (size_t t0 = 0; t0 < in.size(); t0 += ib) {
+        const int cnt = (int)std::min<size_t>(ib, in.size() - t0);
         std::vector<const u64 *> c1(cnt);
         std::vector<KsJob> jobs(cnt);
         for (int t = 0; t < cnt; t++) {
@@ -533,8 +534,9 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
     const int E1 = k1 + P->np, E2 = k2 + P->np, E3 = k3 + P->np;
     {
         const int beta1 = blb_beta(P, lvl - 1);
-        for (int o0 = 0; o0 < G * B; o0 += kMaxJobs) {
-            const int cnt = std::min(kMaxJobs, G * B - o0);
+        const int rb = blb_indep_batch();
+        for (int o0 = 0; o0 < G * B; o0 += rb) {
+            const int cnt = std::min(rb, G * B - o0);
             std::vector<const u64 *> d2(cnt);
             std::vector<KsJob> jobs(cnt);
             for (int t = 0; t < cnt; t++) {
