@@ -281,7 +281,7 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
 // ModUp of n polynomials (c1_ntt[t]: [k][N], NTT, host array of device
 // pointers, n <= kMaxJobs) -> ext [n][beta][E][N] (contiguous, NTT), using
 // coef_scratch [n][k][N].
-constexpr int kMaxJobs = 32;
+constexpr int kMaxJobs = 64;
 // independent rotations (each with its own ModUp) are key-switched in batches of this many jobs so
 // their extended digits (beta (k+np) N 8 bytes each, 15.7 MB at k = 5) are still in L2 when the inner
 // product reads them (env BLB_INDEP_BATCH overrides, 1..kMaxJobs)
