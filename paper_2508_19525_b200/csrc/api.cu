@@ -247,6 +247,7 @@ extern "C" blb_status blb_params_create(blb_params **out, int log_n, const uint6
     auto *P = new blb_params();
     cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
     if (const char *v = getenv("BLB_OVERLAP")) P->overlap = atoi(v);
+    if (const char *v = getenv("BLB_CHUNK")) P->mac_chunk = std::max(1, atoi(v));
     if (const char *v = getenv("BLB_MAC_TMA")) P->mac_tma = atoi(v);
     if (const char *v = getenv("BLB_FUSE")) P->fuse = atoi(v);
     if (cudaStreamCreateWithFlags(&P->aux, cudaStreamNonBlocking) != cudaSuccess) P->aux = nullptr;

@@ -208,6 +208,7 @@ struct blb_params {
     mutable int ev_next = 0;
     int overlap = 1;              // env BLB_OVERLAP=0 disables the two-stream schedule
     int fuse = 1;                 // fused ModUp / ModDown NTT prologue / epilogue (env BLB_FUSE=0 disables)
+    int mac_chunk = 3;            // outputs per MAC / giant-step chunk of the two-stream schedule (env BLB_CHUNK)
     int mac_tma = 1;              // warp-specialised bulk-copy MAC (env BLB_MAC_TMA=0: register double buffer)
     u64 mod[BLB_MAXP];
     u64 psi[BLB_MAXP];
@@ -281,7 +282,7 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
 // ModUp of n polynomials (c1_ntt[t]: [k][N], NTT, host array of device
 // pointers, n <= kMaxJobs) -> ext [n][beta][E][N] (contiguous, NTT), using
 // coef_scratch [n][k][N].
-constexpr int kMaxJobs = 64;
+constexpr int kMaxJobs = 128;
 // independent rotations (each with its own ModUp) are key-switched in batches of this many jobs so
 // their extended digits (beta (k+np) N 8 bytes each, 15.7 MB at k = 5) are still in L2 when the inner
 // product reads them (env BLB_INDEP_BATCH overrides, 1..kMaxJobs)

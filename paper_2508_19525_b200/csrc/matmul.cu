@@ -880,7 +880,7 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
     // auxiliary stream); the caller's stream waits for the auxiliary stream at the end.
     const bool ovl = P->overlap && P->aux && out_count > 1;
     cudaStream_t sa = ovl ? P->aux : st;
-    const int chunk = ovl ? std::max(1, std::min(3, (out_count + 1) / 2)) : out_count;
+    const int chunk = ovl ? std::max(1, std::min(P->mac_chunk, (out_count + 1) / 2)) : out_count;
     auto next_event = [&]() {
         cudaEvent_t e = P->ev[P->ev_next];
         P->ev_next = (P->ev_next + 1) % 64;
