@@ -206,7 +206,8 @@ struct blb_params {
     cudaStream_t aux = nullptr;
     cudaEvent_t ev[64] = {};
     mutable int ev_next = 0;
-    int overlap = 1;              // env BLB_OVERLAP=0 disables the two-stream schedule
+    int overlap = 0;              // two-stream MAC / giant-step schedule (env BLB_OVERLAP=1); measured slower once the
+                                  // batches grew (71.8 ms without vs 72.5-73.2 ms with, profiles/r1_overlap.log)
     int fuse = 1;                 // fused ModUp / ModDown NTT prologue / epilogue (env BLB_FUSE=0 disables)
     int mac_chunk = 3;            // outputs per MAC / giant-step chunk of the two-stream schedule (env BLB_CHUNK)
     int mac_tma = 1;              // warp-specialised bulk-copy MAC (env BLB_MAC_TMA=0: register double buffer)
