@@ -7,8 +7,8 @@ one layer's synthetic inputs: QKV ct-pt MatMul (C11, MHP) + out-projection
 (C12, diagonal input) + FFN1 + FFN2, every MatMul with hoisted baby-step
 rotations, MAC, giant-step key switches and rescale, the ct-ct MatMul Q_h K_h^T
 for all heads (row a7: MHP + BSGS, relinearisation), then the CKKS->MPC masks
-(server half of Alg. 1) of every converted output.  Softmax x V (row f1) is not
-yet part of the step; the JSON says so in config.
+(server half of Alg. 1) of every converted output, and Softmax x V (row f1) with
+its dense-diagonal collapse feeding the out-projection.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -321,29 +321,32 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
 
-    # ---- e2e through the C ABI with host buffers ----
+    # ---- e2e through the public API with host buffers (layer.LayerPipeline) ----
+    # every step: H2D of that step's encrypted inputs from pinned memory and D2H of its masked
+    # outputs + server shares into pinned memory, on a copy stream double-buffered against compute
     e2e = None
     if not args.no_e2e:
+        from paper_2508_19525_b200.layer import LayerPipeline
         host_in = {k: [torch.empty_like(c.data, device="cpu").pin_memory() for c in v] for k, v in inputs.items()}
         for k, v in inputs.items():
             for h, c in zip(host_in[k], v):
                 h.copy_(c.data)
-        h2d = sum(h.numel() * 8 for v in host_in.values() for h in v)
-        d2h = 0
+        h2d = sum(h.numel() * h.element_size() for v in host_in.values() for h in v)
+        pipe = LayerPipeline(layer, keys, A["mask_key"], inputs)
+        for _ in range(2):  # warm-up (pinned output buffers, allocator)
+            pipe.submit(host_in, gather)
+        pipe.drain()
+        torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        pipe.copy.wait_stream(stream)
+        d2h = 0
         for _ in range(args.steps):
-            for k, v in inputs.items():
-                for h, c in zip(host_in[k], v):
-                    c.data.copy_(h, non_blocking=True)
-            res = step()
-            outs_host = []
-            for r in res:
-                for t in (r[2] if isinstance(r[2], (tuple, list)) else (r[2],)):
-                    outs_host.append(t.to("cpu"))
-            d2h = sum(t.numel() * 8 for t in outs_host)
+            outs_host = pipe.submit(host_in, gather)
+            d2h = sum(t.numel() * t.element_size() for t in outs_host)
+        pipe.drain(stream)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -352,7 +355,8 @@ def main():
             t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
-        e2e = {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+        e2e = {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "pipeline": "copy stream double-buffered against compute (layer.LayerPipeline)"}
 
     if rank != 0:
         if world > 1:

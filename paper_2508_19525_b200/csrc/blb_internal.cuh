@@ -57,6 +57,16 @@ __device__ __forceinline__ u64 shoup(u64 x, u64 w, u64 wsh, u64 q) {
     u64 r = shoup_lazy(x, w, wsh, q);
     return r >= q ? r - q : r;
 }
+// Shoup with a truncated quotient: Q' = xh sh + hi32(xh sl) + hi32(xl sh) drops the xl sl partial
+// product and the carries of the two cross terms (x s / 2^64 - Q' < 3, so Q' >= floor(x s / 2^64) - 2):
+// x * w mod q in [0, 4q) for any 64-bit x, with one 32x32->64 and two 32x32->hi32 multiplies
+// instead of the four wide multiplies of __umul64hi (the fma pipe is what bounds the 64-bit NTT).
+__device__ __forceinline__ u64 shoup_lazy4(u64 x, u64 w, u64 wsh, u64 q) {
+    const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
+    const uint32_t sl = (uint32_t)wsh, sh = (uint32_t)(wsh >> 32);
+    const u64 Q = (u64)xh * sh + (u64)__umulhi(xh, sl) + (u64)__umulhi(xl, sh);
+    return x * w - Q * q;
+}
 // (hi * 2^64 + lo) mod q, hi < 2^64
 __device__ __forceinline__ u64 reduce128(u64 hi, u64 lo, const ModConst &c) {
     u64 h = mod64(hi, c);

@@ -113,20 +113,30 @@ __global__ void __launch_bounds__(kThreads) ntt_pass(RowBatch rb, const u64 *__r
 // (1 << s) + (h << r) + mid / (2 t_l).
 __device__ __forceinline__ int swz(int col, int mid) { return (col << 8) | (mid & 0xF0) | ((mid ^ (mid >> 4) ^ col) & 15); }
 
+// Integer butterflies with the truncated-quotient Shoup product (shoup_lazy4, result in [0, 4q)):
+// forward values stay in [0, 8q) (X is brought below 4q, X + t < 8q, X - t + 4q in (0, 8q)),
+// inverse values in [0, 4q); 8q < 2^64 for every prime < 2^61.
 template <bool INV>
-__device__ __forceinline__ void bfly(u64 &X, u64 &Y, u64 w, u64 wsh, u64 q, u64 q2) {
+__device__ __forceinline__ void bfly(u64 &X, u64 &Y, u64 w, u64 wsh, u64 q, u64 q4) {
     if (!INV) {
-        if (X >= q2) X -= q2;
-        const u64 t = shoup_lazy(Y, w, wsh, q);
-        Y = X - t + q2;
+        if (X >= q4) X -= q4;
+        const u64 t = shoup_lazy4(Y, w, wsh, q);
+        Y = X - t + q4;
         X = X + t;
     } else {
         u64 s = X + Y;
-        if (s >= q2) s -= q2;
-        const u64 d = X - Y + q2;
+        if (s >= q4) s -= q4;
+        const u64 d = X - Y + q4;
         X = s;
-        Y = shoup_lazy(d, w, wsh, q);
+        Y = shoup_lazy4(d, w, wsh, q);
     }
+}
+// [0, 8q) -> [0, q)
+__device__ __forceinline__ u64 canon8(u64 x, u64 q) {
+    if (x >= 4 * q) x -= 4 * q;
+    if (x >= 2 * q) x -= 2 * q;
+    if (x >= q) x -= q;
+    return x;
 }
 
 // ---------------------------------------------------------------------------
@@ -182,7 +192,7 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
     constexpr int logN = 16, N = 1 << logN;
     u64 *a = rb.base + (long long)p * rb.poly_stride + (long long)(rb.limb0 + l) * N;
     const int pi = rb.prime[l];
-    const u64 q = pr.m[pi].q, q2 = 2 * q;
+    const u64 q = pr.m[pi].q, q4 = 4 * q;
     // interleaved (w, w') pairs: one 16-byte load per butterfly
     const ulonglong2 *twp = reinterpret_cast<const ulonglong2 *>(tw_all + (size_t)pi * 4 * N + (INV ? 2 * N : 0));
     const double *twd = twd_all + (size_t)pi * 2 * N + (INV ? N : 0);
@@ -239,7 +249,7 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
                 bfly_f64<INV>(v[m], v[m + dist], twd[widx], qd, qinv);
             } else {
                 const ulonglong2 tv = twp[widx];
-                bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q2);
+                bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q4);
             }
         }
     };
@@ -254,7 +264,7 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
                 bfly_f64<INV>(v[m], v[m + dist], twd[widx], qd, qinv);
             } else {
                 const ulonglong2 tv = twp[widx];
-                bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q2);
+                bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q4);
             }
         }
     };
@@ -295,11 +305,7 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
         for (int m = 0; m < 16; m++) {
             u64 x;
             if constexpr (SMALL) x = canon(v[m], qd, qinv);
-            else {
-                x = v[m];
-                if (x >= q2) x -= q2;
-                if (x >= q) x -= q;
-            }
+            else x = canon8(v[m], q);
             const int mid = tcA + 16 * m;
             const uint32_t gx = (uint32_t)((c0 + colA) << 8) + mid;
             u64 r = shoup(ui[gx] + q - x, pv, psh, q);
@@ -323,8 +329,7 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
                 x = v[m];
                 if (last) {
                     if (!INV) {
-                        if (x >= q2) x -= q2;
-                        if (x >= q) x -= q;
+                        x = canon8(x, q);
                     } else {
                         x = shoup_lazy(x, mc.ninv, mc.ninv_sh, q);
                         if (x >= q) x -= q;
