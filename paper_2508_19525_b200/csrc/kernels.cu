@@ -285,21 +285,39 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
         if constexpr (SMALL) return a1[q].reduce(qd, qinv);
         else return a1[q].reduce(mc);
     };
+    // The additive terms: EXT adds P c0 (and P c1_add) over the Q limbs of the extended result.  The
+    // ModDown path folds the rotation's sigma_g(c0) (add_mode 1) or the relinearisation's (c0, c1)
+    // (add_mode 2) in the same way: ModDown(u + P c) = ModDown(u) + c exactly (P P^{-1} = 1 mod q_i;
+    // the P limbs, P c = 0 mod p, are unchanged), and at output position dst = perm_{g^-1}(x)
+    // sigma_g(c0) is c0[x] -- a contiguous read instead of a gather in the ModDown epilogue.
+    // All loads of the group are issued before its first store (the stores may alias as far as the
+    // compiler knows): one exposed latency instead of one per job.
+    u64 c0v[kKsGroup], c1v[kKsGroup];
+#pragma unroll
+    for (int q = 0; q < kKsGroup; q++) {
+        c0v[q] = 0; c1v[q] = 0;
+        if (q < cnt && m < k) {
+            const KsJob &J = jobs.j[t0 + q];
+            if (EXT || J.add_mode != 0) c0v[q] = J.c0[(long long)m * N + x];
+            if (J.c1_add && (EXT || J.add_mode == 2)) c1v[q] = J.c1_add[(long long)m * N + x];
+        }
+    }
 #pragma unroll
     for (int q = 0; q < kKsGroup; q++) {
         if (q < cnt) {
             const int t = t0 + q;
+            const KsJob &J = jobs.j[t];
+            u64 r0 = a0[q].reduce(mc), r1 = a1r(q);
+            if (m < k) {
+                r0 = addmod(r0, shoup(c0v[q], pq.v[m], pq.sh[m], mc.q), mc.q);
+                r1 = addmod(r1, shoup(c1v[q], pq.v[m], pq.sh[m], mc.q), mc.q);
+            }
             if (EXT) {
-                const KsJob &J = jobs.j[t];
-                u64 r0 = a0[q].reduce(mc);
-                if (m < k) r0 = addmod(r0, shoup(J.c0[(long long)m * N + x], pq.v[m], pq.sh[m], mc.q), mc.q);
                 J.out[(long long)m * N + dst] = r0;
-                u64 r1 = a1r(q);
-                if (m < k && J.c1_add) r1 = addmod(r1, shoup(J.c1_add[(long long)m * N + x], pq.v[m], pq.sh[m], mc.q), mc.q);
                 J.out[((long long)E + m) * N + dst] = r1;
             } else {
-                u[(((long long)t * 2 + 0) * E + m) * N + dst] = a0[q].reduce(mc);
-                u[(((long long)t * 2 + 1) * E + m) * N + dst] = a1r(q);
+                u[(((long long)t * 2 + 0) * E + m) * N + dst] = r0;
+                u[(((long long)t * 2 + 1) * E + m) * N + dst] = r1;
             }
         }
     }
@@ -625,6 +643,8 @@ blb_status launch_keyswitch(const blb_params *P, int level, const KsJob *jobs, i
     KsGroups G{};
     group_jobs(jobs, n, J, G, P->logN);
     BLB_TRY(ks_inner_launch<false>(P, level, J, G, u, st));
+    // sigma_g(c0) / (c0, c1) were folded into u as P * c by the inner product: plain ModDown
+    for (int t = 0; t < n; t++) J.j[t].add_mode = 0;
     BLB_TRY(moddown_launch(P, level, J, n, u, conv, st));
     BLB_COUNT(1, n);
     return BLB_OK;
@@ -677,12 +697,14 @@ __global__ void k_mdr_lift(const u64 *u, u64 *conv, MdrTab T, Primes pr, int k, 
     if (x >= N) return;
     const int level = k - 1;
     const u64 *base = u + ((long long)pp * E + level) * N + x;
-    u64 d[kMdrMax];
+    u64 d[kMdrMax], in[kMdrMax];
+#pragma unroll
+    for (int t = 0; t < kMdrMax; t++) in[t] = t < T.nd ? base[(long long)t * N] : 0;  // loads issued together
 #pragma unroll
     for (int t = 0; t < kMdrMax; t++) {
         if (t >= T.nd) break;
         const u64 mt = T.md[t].q;
-        u64 v = base[(long long)t * N] + T.hd[t];
+        u64 v = in[t] + T.hd[t];
         if (v >= mt) v -= mt;
 #pragma unroll
         for (int s2 = 0; s2 < kMdrMax; s2++) {

@@ -301,6 +301,11 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
         const u64 *ui = fz.u + ((long long)p * fz.E + l) * N;
         u64 *out = J.out + ((long long)b * fz.k + l) * N;
         const u64 pv = fz.pinv.v[l], psh = fz.pinv.sh[l];
+        // all 16 u_i loads are issued before the first store to out (which may alias as far as the
+        // compiler knows): one exposed DRAM latency per thread instead of 16
+        u64 uv[16];
+#pragma unroll
+        for (int m = 0; m < 16; m++) uv[m] = ui[(uint32_t)((c0 + colA) << 8) + tcA + 16 * m];
 #pragma unroll
         for (int m = 0; m < 16; m++) {
             u64 x;
@@ -308,7 +313,7 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
             else x = canon8(v[m], q);
             const int mid = tcA + 16 * m;
             const uint32_t gx = (uint32_t)((c0 + colA) << 8) + mid;
-            u64 r = shoup(ui[gx] + q - x, pv, psh, q);
+            u64 r = shoup(uv[m] + q - x, pv, psh, q);
             if (J.add_mode == 1 && b == 0) {
                 const uint32_t src = J.galois == 1 ? gx : galois_perm(gx, J.galois, logN);
                 r = addmod(r, J.c0[(long long)l * N + src], q);
