@@ -485,37 +485,44 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
     const int Ex = k + P->np;
     const size_t ct_e = (size_t)2 * Ex * N;
     u64 *conv = W + w.ks;  // ModDown intermediate (kMaxJobs x [2][k][N] fits the key-switch scratch)
-    auto rotate_ext_all = [&](const u64 *ct, const std::vector<int32_t> &steps, u64 *out_base) -> blb_status {
-        const u64 *c1 = ct + (size_t)k * N;
-        BLB_TRY(launch_modup(P, lvl, &c1, 1, W + w.ext, W + w.coef, st));
-        for (size_t t0 = 0; t0 < steps.size(); t0 += kMaxJobs) {
-            const int cnt = (int)std::min<size_t>(kMaxJobs, steps.size() - t0);
-            std::vector<KsJob> jobs(cnt);
-            for (int t = 0; t < cnt; t++) {
-                const uint32_t g = blb_galois_element(P, steps[t0 + t]);
+    // hoisted rotations of all J ciphertexts of one operand: one ModUp launch for the J inputs, then
+    // the jobs step-major (the J rotations by one step are adjacent and share their key: the key
+    // switch reads each key once per step instead of once per ciphertext); rotation t of input j is
+    // written to base + j * j_stride + t * ct_e
+    auto rotate_ext_J = [&](const blb_ct *cts, const std::vector<int32_t> &steps, u64 *base,
+                            size_t j_stride) -> blb_status {
+        if (steps.empty()) return BLB_OK;
+        const int beta = blb_beta(P, lvl);
+        std::vector<const u64 *> c1(J);
+        for (int j = 0; j < J; j++) c1[j] = cts[j].data + (size_t)k * N;
+        BLB_TRY(launch_modup(P, lvl, c1.data(), J, W + w.ext, W + w.coef, st));
+        std::vector<KsJob> jobs;
+        for (size_t t = 0; t < steps.size(); t++) {
+            const uint32_t g = blb_galois_element(P, steps[t]);
+            for (int j = 0; j < J; j++) {
                 KsJob Jb{};
-                Jb.ext = W + w.ext;
+                Jb.ext = W + w.ext + (size_t)j * beta * Ex * N;
                 Jb.key = key_for(keys, g);
-                Jb.c0 = ct;
-                Jb.out = out_base + (t0 + t) * ct_e;
+                Jb.c0 = cts[j].data;
+                Jb.out = base + j * j_stride + t * ct_e;
                 Jb.galois = g;
-                jobs[t] = Jb;
+                jobs.push_back(Jb);
             }
-            BLB_TRY(launch_keyswitch_ext(P, lvl, jobs.data(), cnt, st));
+        }
+        for (size_t t0 = 0; t0 < jobs.size(); t0 += kMaxJobs) {
+            const int cnt = (int)std::min<size_t>(kMaxJobs, jobs.size() - t0);
+            BLB_TRY(launch_keyswitch_ext(P, lvl, jobs.data() + t0, cnt, st));
         }
         return BLB_OK;
     };
-    for (int j = 0; j < J; j++) {
-        u64 *kr = W + w.kr + (size_t)j * NKR * ct_e;
-        BLB_TRY(launch_lift_ext(P, lvl, K[j].data, kr, st));
-        BLB_TRY(rotate_ext_all(K[j].data, pl->k_rots, kr + ct_e));
-    }
+    for (int j = 0; j < J; j++) BLB_TRY(launch_lift_ext(P, lvl, K[j].data, W + w.kr + (size_t)j * NKR * ct_e, st));
+    BLB_TRY(rotate_ext_J(K, pl->k_rots, W + w.kr + ct_e, (size_t)NKR * ct_e));
     BLB_TRY(launch_mac(P, m1, W + w.kr, W + w.kacc, E + pl->off_kp_r, E + pl->off_kp_pt, E + pl->off_kp_start, 0, 0,
                        B * J, (int)pl->kp_r.size(), Ex, st, k));
     BLB_TRY(launch_moddown_rescale(P, lvl, W + w.kacc, B * J, W + w.kp, conv, st));  // C17
     // 2. giant side: Q_0 = level drop, Q_u = ModDown(MAC(masks, Rot_ext(Q))), rescale
+    if (NQR) BLB_TRY(rotate_ext_J(Q, pl->q_rots, W + w.qr, (size_t)NQR * ct_e));
     for (int j = 0; j < J; j++) {
-        if (NQR) BLB_TRY(rotate_ext_all(Q[j].data, pl->q_rots, W + w.qr + (size_t)j * NQR * ct_e));
         k_copy_limbs<<<gx(N, k1, 2), kTB, 0, st>>>(Q[j].data, W + w.qp + (size_t)j * ct_k1, k, k1, N);
         BLB_COUNT_LAUNCH(1);
     }
