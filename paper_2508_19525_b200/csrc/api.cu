@@ -249,6 +249,7 @@ extern "C" blb_status blb_params_create(blb_params **out, int log_n, const uint6
     if (const char *v = getenv("BLB_OVERLAP")) P->overlap = atoi(v);
     if (const char *v = getenv("BLB_CHUNK")) P->mac_chunk = std::max(1, atoi(v));
     if (const char *v = getenv("BLB_MAC_TMA")) P->mac_tma = atoi(v);
+    if (const char *v = getenv("BLB_MAC_J")) P->mac_j = atoi(v);
     if (const char *v = getenv("BLB_FUSE")) P->fuse = atoi(v);
     if (cudaStreamCreateWithFlags(&P->aux, cudaStreamNonBlocking) != cudaSuccess) P->aux = nullptr;
     for (auto &e : P->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);

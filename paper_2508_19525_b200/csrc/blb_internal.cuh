@@ -221,6 +221,7 @@ struct blb_params {
     int fuse = 1;                 // fused ModUp / ModDown NTT prologue / epilogue (env BLB_FUSE=0 disables)
     int mac_chunk = 3;            // outputs per MAC / giant-step chunk of the two-stream schedule (env BLB_CHUNK)
     int mac_tma = 1;              // warp-specialised bulk-copy MAC (env BLB_MAC_TMA=0: register double buffer)
+    int mac_j = 2;                // mask MAC over groups of mac_j (2 or 4) outputs sharing their masks (env BLB_MAC_J; 0: k_mac)
     u64 mod[BLB_MAXP];
     u64 psi[BLB_MAXP];
     Primes pr;                    // by-value copy for kernel args
@@ -371,7 +372,7 @@ size_t encode_scratch_doubles(const blb_params *P, int n_pts);
 // kq >= 0: the first kq limbs are q_0..q_{kq-1} and limbs kq.. are p_0.. (extended basis)
 blb_status launch_mac(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc, const int *ent_r, const int *ent_pt,
                       const int *ent_start, int o0, int e_base, int n_o, int n_entries, int k, cudaStream_t st,
-                      int kq = -1);
+                      int kq = -1, int jg = 1);
 
 // ChaCha / sampling
 enum { TAG_SECRET = 1, TAG_KEY_A = 2, TAG_KEY_E = 3, TAG_ENC_A = 4, TAG_ENC_E = 5, TAG_MASK = 6 };

@@ -467,6 +467,127 @@ static void launch_mac4(const u64 *pt, const u64 *R, u64 *acc, const int *ent_r,
                                                                                       e_base, n_o, k, logN, pr);
 }
 
+// Indexed mask MAC for JG consecutive outputs that share their plaintext (mask) list and differ only
+// in the rotations they multiply (the ct-ct stage-1 MACs: K'_i^(j) / Q_u^(j) for j in a group, reading
+// C13): per pipeline stage one entry = the mask tile + the JG (c0, c1) rotation tiles, staged by a
+// producer warp with cp.async.bulk into a 3-stage shared-memory ring.  Each mask tile is read once per
+// JG outputs instead of once per output, and the consumers never wait on a global load.
+constexpr int kMjStages = 3;
+template <int JG>
+constexpr size_t macj_smem() { return (size_t)kMjStages * (1 + 2 * JG) * 512 * 8 + 2 * kMjStages * 8; }
+
+template <bool SPLIT41, int JG>
+__device__ __forceinline__ void macj_consume(const u64 *ring, uint64_t *full, uint64_t *empty, int n_e, u64 *const *outs,
+                                             long long kN, const ModConst &mc) {
+    using A = typename std::conditional<SPLIT41, Acc41, Acc128>::type;
+    using A1 = typename std::conditional<SPLIT41, AccF64, Acc128>::type;
+    const double qd = (double)mc.q, qinv = 1.0 / qd;
+    A a00[JG], a01[JG];
+    A1 a10[JG], a11[JG];
+#pragma unroll
+    for (int j = 0; j < JG; j++) { a00[j].zero(); a01[j].zero(); a10[j].zero(); a11[j].zero(); }
+    constexpr int kStageWords = (1 + 2 * JG) * 512;
+    const int t = threadIdx.x;
+    for (int s = 0; s < n_e; s++) {
+        const int slot = s % kMjStages;
+        mbar_wait(&full[slot], (s / kMjStages) & 1);
+        const u64 *st = ring + (size_t)slot * kStageWords;
+        const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(st + 2 * t);
+#pragma unroll
+        for (int j = 0; j < JG; j++) {
+            const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + (1 + 2 * j) * 512 + 2 * t);
+            const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + (2 + 2 * j) * 512 + 2 * t);
+            a00[j].mac(pv.x, r0.x); a01[j].mac(pv.y, r0.y);
+            if constexpr (SPLIT41) {
+                a10[j].mac(pv.x, r1.x, qd, qinv); a11[j].mac(pv.y, r1.y, qd, qinv);
+            } else {
+                a10[j].mac(pv.x, r1.x); a11[j].mac(pv.y, r1.y);
+            }
+        }
+        __syncwarp();
+        if ((t & 31) == 0) mbar_arrive(&empty[slot]);
+        if constexpr (!SPLIT41) {
+            if ((s & 63) == 63) {  // 64 products < 2^126
+#pragma unroll
+                for (int j = 0; j < JG; j++) { a00[j].fold(mc); a01[j].fold(mc); a10[j].fold(mc); a11[j].fold(mc); }
+            }
+        } else {
+            if ((s & 511) == 511) {  // 512 products: FP64 sums below 2^51
+#pragma unroll
+                for (int j = 0; j < JG; j++) { a10[j].fold(qd, qinv); a11[j].fold(qd, qinv); }
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < JG; j++) {
+        u64 *out = outs[j] + 2 * t;
+        *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00[j].reduce(mc), a01[j].reduce(mc));
+        if constexpr (SPLIT41)
+            *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10[j].reduce(qd, qinv), a11[j].reduce(qd, qinv));
+        else
+            *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10[j].reduce(mc), a11[j].reduce(mc));
+    }
+}
+
+// grid: (group fastest, tile, limb); group gi covers outputs o0 + gi*JG .. + JG - 1 (local o)
+template <int JG, int MINB>
+__global__ void __launch_bounds__(kTB + 32, MINB) k_mac_j(const u64 *__restrict__ pt, const u64 *__restrict__ R,
+                                                     u64 *__restrict__ acc, const int *__restrict__ ent_r,
+                                                     const int *__restrict__ ent_pt, const int *__restrict__ ent_start,
+                                                     int o0, int n_grp, int k, int kq, int Kfull, int logN, Primes pr) {
+    constexpr int kStageWords = (1 + 2 * JG) * 512;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    u64 *ring = reinterpret_cast<u64 *>(smraw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)kMjStages * kStageWords);
+    uint64_t *empty = full + kMjStages;
+    const int N = 1 << logN;
+    const int n_tiles = N / (2 * kTB);
+    int bid = blockIdx.x;
+    const int gi = bid % n_grp;
+    bid /= n_grp;
+    const int tile = bid % n_tiles;
+    const int l = bid / n_tiles;
+    const int oa = gi * JG;
+    const long long kN = (long long)k * N;
+    const int e_lo = ent_start[o0 + oa], n_e = ent_start[o0 + oa + 1] - e_lo;
+    const long long lx0 = (long long)l * N + tile * 2 * kTB;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kMjStages; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kTB / 32);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x >= kTB) {  // producer warp
+        if (threadIdx.x == kTB) {
+            int eb[JG];
+#pragma unroll
+            for (int j = 0; j < JG; j++) eb[j] = ent_start[o0 + oa + j];
+            for (int s = 0; s < n_e; s++) {
+                const int slot = s % kMjStages;
+                if (s >= kMjStages) mbar_wait(&empty[slot], ((s / kMjStages) - 1) & 1);
+                u64 *st = ring + (size_t)slot * kStageWords;
+                mbar_expect_tx(&full[slot], (unsigned)(1 + 2 * JG) * 4096);
+                bulk_g2s(st, pt + (long long)ent_pt[e_lo + s] * kN + lx0, 4096, &full[slot]);
+#pragma unroll
+                for (int j = 0; j < JG; j++) {
+                    const int bi = ent_r[eb[j] + s];
+                    bulk_g2s(st + (1 + 2 * j) * 512, R + (long long)bi * 2 * kN + lx0, 4096, &full[slot]);
+                    bulk_g2s(st + (2 + 2 * j) * 512, R + ((long long)bi * 2 + 1) * kN + lx0, 4096, &full[slot]);
+                }
+            }
+        }
+        return;
+    }
+    u64 *outs[JG];
+#pragma unroll
+    for (int j = 0; j < JG; j++) outs[j] = acc + (long long)(oa + j) * 2 * kN + lx0;
+    const ModConst &mc = pr.m[l < kq ? l : Kfull + (l - kq)];
+    if (mc.q < (1ull << 41)) macj_consume<true, JG>(ring, full, empty, n_e, outs, kN, mc);
+    else macj_consume<false, JG>(ring, full, empty, n_e, outs, kN, mc);
+}
+
 // scatter standard [cnt][k][N] plaintexts (entries e0..e0+cnt of the plan) into the blocked layout
 __global__ void k_block_pts(const u64 *src, u64 *dst, const int *ent_start, const int *ent_o, int e0, int e_base,
                             int k, int N) {
@@ -506,17 +627,48 @@ __global__ void k_copy_ct(const u64 *src, u64 *dst, long long n) {
 
 blb_status launch_mac(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc, const int *ent_r, const int *ent_pt,
                       const int *ent_start, int o0, int e_base, int n_o, int n_entries, int k, cudaStream_t st,
-                      int kq) {
+                      int kq, int jg) {
     if (n_o <= 0) return BLB_OK;
     const int N = P->N;
     const int n_tiles = N / (2 * kTB);
     cudaEvent_t t0 = blb_timing_begin(st);
+    const int JGc = P->mac_j;  // outputs per CTA (2 or 4; 0 = per-output k_mac)
+    if (JGc > 0 && jg % JGc == 0 && n_o % JGc == 0 && ent_pt && P->logN >= 9) {
+        // groups of JGc outputs sharing the mask list (reading C13 stage 1): k_mac_j
+        const int n_grp = n_o / JGc;
+        const unsigned grid = (unsigned)((size_t)n_grp * n_tiles * k);
+        if (JGc == 4) {
+            static bool attr = false;
+            constexpr size_t smem = macj_smem<4>();
+            if (!attr) {
+                cudaFuncSetAttribute(k_mac_j<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                attr = true;
+            }
+            k_mac_j<4, 2><<<grid, kTB + 32, smem, st>>>(pt, R, acc, ent_r, ent_pt, ent_start, o0, n_grp, k,
+                                                        kq < 0 ? k : kq, P->K, P->logN, P->pr);
+        } else {
+            static bool attr = false;
+            constexpr size_t smem = macj_smem<2>();
+            if (!attr) {
+                cudaFuncSetAttribute(k_mac_j<2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                attr = true;
+            }
+            k_mac_j<2, 3><<<grid, kTB + 32, smem, st>>>(pt, R, acc, ent_r, ent_pt, ent_start, o0, n_grp, k,
+                                                        kq < 0 ? k : kq, P->K, P->logN, P->pr);
+        }
+        BLB_COUNT_LAUNCH(1);
+        BLB_COUNT(3, n_entries);
+        // bytes staged: one mask tile per entry per group of JGc outputs + the (c0, c1) rotation tiles
+        blb_timing_end(3, t0, st, ((double)n_entries / JGc + 2.0 * n_entries) * k * N * 8.0);
+        BLB_CHECK_LAUNCH();
+        return BLB_OK;
+    }
     // (a warp-specialised bulk-copy version of this indexed MAC measured slower: 8.1 vs 7.5 ms per step)
     k_mac<<<(unsigned)((size_t)n_o * n_tiles * k), kTB, 0, st>>>(pt, R, acc, ent_r, ent_pt, ent_start, o0, e_base,
                                                                     n_o, k, kq < 0 ? k : kq, P->K, P->logN, P->pr);
     BLB_COUNT_LAUNCH(1);
     BLB_COUNT(3, n_entries);
-    blb_timing_end(3, t0, st, (double)n_entries * k * N * 8.0);  // category 3: ct-ct mask MAC
+    blb_timing_end(3, t0, st, 3.0 * n_entries * k * N * 8.0);  // category 3: ct-ct mask MAC (mask + c0, c1 bytes)
     BLB_CHECK_LAUNCH();
     return BLB_OK;
 }

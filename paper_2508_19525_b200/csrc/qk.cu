@@ -518,7 +518,7 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
     for (int j = 0; j < J; j++) BLB_TRY(launch_lift_ext(P, lvl, K[j].data, W + w.kr + (size_t)j * NKR * ct_e, st));
     BLB_TRY(rotate_ext_J(K, pl->k_rots, W + w.kr + ct_e, (size_t)NKR * ct_e));
     BLB_TRY(launch_mac(P, m1, W + w.kr, W + w.kacc, E + pl->off_kp_r, E + pl->off_kp_pt, E + pl->off_kp_start, 0, 0,
-                       B * J, (int)pl->kp_r.size(), Ex, st, k));
+                       B * J, (int)pl->kp_r.size(), Ex, st, k, J));  // outputs i*J + j share their masks
     BLB_TRY(launch_moddown_rescale(P, lvl, W + w.kacc, B * J, W + w.kp, conv, st));  // C17
     // 2. giant side: Q_0 = level drop, Q_u = ModDown(MAC(masks, Rot_ext(Q))), rescale
     if (NQR) BLB_TRY(rotate_ext_J(Q, pl->q_rots, W + w.qr, (size_t)NQR * ct_e));
@@ -528,7 +528,7 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
     }
     if (G > 1) {
         BLB_TRY(launch_mac(P, m1, W + w.qr, W + w.qacc, E + pl->off_qp_r, E + pl->off_qp_pt, E + pl->off_qp_start, 0, 0,
-                           (G - 1) * J, (int)pl->qp_r.size(), Ex, st, k));
+                           (G - 1) * J, (int)pl->qp_r.size(), Ex, st, k, J));
         BLB_TRY(launch_moddown_rescale(P, lvl, W + w.qacc, (G - 1) * J, W + w.qp + (size_t)J * ct_k1, conv, st));
     }
     // 3. products summed over j, relinearisation (one per (u, i)), rescale
