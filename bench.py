@@ -315,6 +315,7 @@ def main():
     ntt = blb.timing_read(blb.TIMING_NTT)
     ksi = blb.timing_read(blb.TIMING_KS_INNER)
     mmac = blb.timing_read(blb.TIMING_MASK_MAC)
+    tsum = blb.timing_read(blb.TIMING_TENSOR)
     ms_step = ms_total / args.steps
     if world > 1:
         t = torch.tensor([ms_step], device="cuda", dtype=torch.float64)
@@ -389,9 +390,12 @@ def main():
                 "share_of_step": ntt["ms"] / ms_total if ms_total else None, "launches": ntt["launches"]},
         "ks_inner": {"alg_gbs": ksi["alg_bytes"] / (ksi["ms"] * 1e-3) / 1e9 if ksi["ms"] else None,
                      "share_of_step": ksi["ms"] / ms_total if ms_total else None},
-        "mask_mac": {"kernel": "k_mac (ct-ct masks, rows a7/f1)",
+        "mask_mac": {"kernel": "k_mac_j / k_mac (ct-ct masks, rows a7/f1; bytes = mask + rotation tiles staged)",
                      "alg_gbs": mmac["alg_bytes"] / (mmac["ms"] * 1e-3) / 1e9 if mmac["ms"] else None,
                      "share_of_step": mmac["ms"] / ms_total if ms_total else None},
+        "tensor_sum": {"kernel": "k_tensor_sum22 (ct-ct J-sum of tensor products, rows a7/f1)",
+                       "alg_gbs": tsum["alg_bytes"] / (tsum["ms"] * 1e-3) / 1e9 if tsum["ms"] else None,
+                       "share_of_step": tsum["ms"] / ms_total if ms_total else None},
         "gpu_launches": ctr["launches"],
         "counters_per_step": {k: v / args.steps for k, v in ctr.items()},
         "clocks": clk,

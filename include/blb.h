@@ -89,7 +89,7 @@ void blb_counters_reset(void);
 /* Live kernel timing (bench instrumentation).  When enabled, the library
  * records a CUDA event pair on the launching stream around every launch of
  * the tracked kernels: category 0 = ct-pt weight MAC (k_mac_tma4 / k_mac_tma), 1 = NTT/INTT passes,
- * 2 = key-switch inner product, 3 = ct-ct mask MAC (k_mac).  blb_timing_read synchronises the recorded
+ * 2 = key-switch inner product, 3 = ct-ct mask MAC (k_mac / k_mac_j), 4 = ct-ct tensor J-sum (k_tensor_sum).  blb_timing_read synchronises the recorded
  * events and returns, for `category`, the summed device milliseconds, the
  * number of launches and the summed ALGORITHMIC bytes (MAC: k*N*8 per
  * plaintext; NTT: 2*N*8 per limb; inner product: 2*beta*(k+np)*N*8 key bytes

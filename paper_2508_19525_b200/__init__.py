@@ -143,7 +143,7 @@ def reset_counters():
     lib().blb_counters_reset()
 
 
-TIMING_MAC, TIMING_NTT, TIMING_KS_INNER, TIMING_MASK_MAC = 0, 1, 2, 3
+TIMING_MAC, TIMING_NTT, TIMING_KS_INNER, TIMING_MASK_MAC, TIMING_TENSOR = 0, 1, 2, 3, 4
 
 
 def timing_enable(on: bool = True):

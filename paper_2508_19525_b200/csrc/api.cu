@@ -64,7 +64,7 @@ struct TimedLaunch {
 };
 std::mutex g_tmu;
 bool g_timing = false;
-std::vector<TimedLaunch> g_tl[4];
+std::vector<TimedLaunch> g_tl[5];
 std::vector<cudaEvent_t> g_pool;
 cudaEvent_t take_event() {
     if (!g_pool.empty()) {
@@ -111,7 +111,7 @@ extern "C" void blb_timing_reset(void) {
     }
 }
 extern "C" blb_status blb_timing_read(int cat, double *total_ms, uint64_t *launches, double *bytes) {
-    if (cat < 0 || cat > 3) return BLB_E_INVALID_ARG;
+    if (cat < 0 || cat > 4) return BLB_E_INVALID_ARG;
     std::lock_guard<std::mutex> lk(g_tmu);
     double ms = 0, by = 0;
     for (auto &t : g_tl[cat]) {
@@ -250,6 +250,7 @@ extern "C" blb_status blb_params_create(blb_params **out, int log_n, const uint6
     if (const char *v = getenv("BLB_CHUNK")) P->mac_chunk = std::max(1, atoi(v));
     if (const char *v = getenv("BLB_MAC_TMA")) P->mac_tma = atoi(v);
     if (const char *v = getenv("BLB_MAC_J")) P->mac_j = atoi(v);
+    if (const char *v = getenv("BLB_TSUM22")) P->tsum22 = atoi(v);
     if (const char *v = getenv("BLB_FUSE")) P->fuse = atoi(v);
     if (cudaStreamCreateWithFlags(&P->aux, cudaStreamNonBlocking) != cudaSuccess) P->aux = nullptr;
     for (auto &e : P->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);

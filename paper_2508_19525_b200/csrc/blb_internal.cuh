@@ -221,6 +221,7 @@ struct blb_params {
     int fuse = 1;                 // fused ModUp / ModDown NTT prologue / epilogue (env BLB_FUSE=0 disables)
     int mac_chunk = 3;            // outputs per MAC / giant-step chunk of the two-stream schedule (env BLB_CHUNK)
     int mac_tma = 1;              // warp-specialised bulk-copy MAC (env BLB_MAC_TMA=0: register double buffer)
+    int tsum22 = 1;               // 2 x 2 register-blocked ct-ct tensor J-sum (env BLB_TSUM22=0: one output per thread)
     int mac_j = 2;                // mask MAC over groups of mac_j (2 or 4) outputs sharing their masks (env BLB_MAC_J; 0: k_mac)
     u64 mod[BLB_MAXP];
     u64 psi[BLB_MAXP];
@@ -332,8 +333,16 @@ struct PinvTab {
 //            and reduces it mod the row's modulus (FastBConv of a single-prime digit / P limb);
 //   epi = 1: the last (forward) pass finishes ModDown: out = (u_i - v) * P^{-1} (+ sigma_g(c0) / (c0, c1))
 //            written to jobs.j[p / 2].out (rows p = 2 t + b, limb i), u = [jobs][2][E][N].
+struct PtrTab {
+    const u64 *p[kMaxJobs];
+};
+// pro = 2 (inverse, contiguous first pass): row (p, l) is loaded from srcp.p[p] + l * N (ModUp: the
+//          ciphertexts' c1 rows straight into the coefficient scratch, no gather copy);
+// copy_own (with pro = 1, alpha = 1): the rows a digit owns (skipped by the transform) are copied from
+//          srcp.p[p / src_div] + l * N by the first pass (ModUp: the digit's own residues, NTT form).
 struct NttFuse {
-    int pro = 0, epi = 0;
+    int pro = 0, epi = 0, copy_own = 0;
+    PtrTab srcp;
     const u64 *src = nullptr;
     long long src_hi = 0, src_lo = 0;
     int src_div = 1;

@@ -161,15 +161,6 @@ __global__ void k_gather_rows(PtrList src, u64 *dst, int k, int N) {
     dst[((long long)t * k + i) * N + x] = src.p[t][(long long)i * N + x];
 }
 
-// alpha = 1: ext[t][j][j] = c1_t[j] (a digit's own residue row, already in NTT form)
-__global__ void k_copy_own(PtrList c1_ntt, u64 *ext, int k, int np, int beta, int N) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y, t = blockIdx.z;
-    if (x >= N) return;
-    const int E = k + np;
-    ext[(((long long)t * beta + j) * E + j) * N + x] = c1_ntt.p[t][(long long)j * N + x];
-}
-
 // ext[t][j][m][x]: digit j's own limbs copy the NTT-domain input; the others are
 // FastBConv_{D_j -> m}(coef) = sum_i [coef_i * dhat_i^{-1}]_{d_i} * dhat_i  mod m.
 // Table at tab + bconv_modup_off(level, j): inv[nd], inv_sh[nd], chat[nd][E].
@@ -495,16 +486,16 @@ blb_status launch_modup(const blb_params *P, int level, const u64 *const *c1_ntt
     const int N = P->N, k = level + 1, E = k + P->np, beta = blb_beta(P, level);
     PtrList src{};
     for (int t = 0; t < n; t++) src.p[t] = c1_ntt[t];
-    k_gather_rows<<<grid_x(N, k, n), kTB, 0, st>>>(src, coef, k, N);
-    BLB_COUNT_LAUNCH(1);
     RowBatch rb{};
     rb.base = coef; rb.poly_stride = (long long)k * N; rb.n_polys = n; rb.limbs = k; rb.limb0 = 0;
     for (int i = 0; i < k; i++) rb.prime[i] = i;
-    BLB_TRY(launch_ntt(P, rb, true, st));
     if (P->logN == 16 && P->alpha == 1 && P->fuse) {
-        // fused: own rows copied, the others converted (x mod q_m) inside the forward NTT's first pass
-        k_copy_own<<<grid_x(N, beta, n), kTB, 0, st>>>(src, ext, k, P->np, beta, N);
-        BLB_COUNT_LAUNCH(1);
+        // fused: the INTT's first pass reads the c1 rows in place (no gather copy); in the forward
+        // NTT's first pass the own rows are copied and the others converted (x mod q_m)
+        NttFuse gz{};
+        gz.pro = 2;
+        for (int t = 0; t < n; t++) gz.srcp.p[t] = c1_ntt[t];
+        BLB_TRY(launch_ntt_fused(P, rb, true, gz, st));
         RowBatch eb{};
         eb.base = ext; eb.poly_stride = (long long)E * N; eb.n_polys = n * beta; eb.limbs = E; eb.limb0 = 0;
         for (int m = 0; m < E; m++) eb.prime[m] = m < k ? m : P->K + (m - k);
@@ -515,8 +506,13 @@ blb_status launch_modup(const blb_params *P, int level, const u64 *const *c1_ntt
         fz.src_div = beta;
         fz.src_hi = (long long)k * N;
         fz.src_lo = N;
+        fz.copy_own = 1;
+        for (int t = 0; t < n; t++) fz.srcp.p[t] = c1_ntt[t];
         return launch_ntt_fused(P, eb, false, fz, st);
     }
+    k_gather_rows<<<grid_x(N, k, n), kTB, 0, st>>>(src, coef, k, N);
+    BLB_COUNT_LAUNCH(1);
+    BLB_TRY(launch_ntt(P, rb, true, st));
     Offs offs{};
     for (int j = 0; j < beta; j++) offs.o[j] = (long long)bconv_modup_off(P, level, j);
     k_bconv_modup<<<grid_x(N, E, n * beta), kTB, 0, st>>>(src, coef, ext, P->d_bconv, offs, P->pr, k, P->np, P->K,

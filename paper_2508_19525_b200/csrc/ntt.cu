@@ -221,7 +221,15 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
         if constexpr (SMALL) return __longlong_as_double((long long)x);
         else return x;
     };
-    if (PRO == 1) {
+    if (PRO == 2) {
+        const u64 *src = fz.srcp.p[p] + (long long)(rb.limb0 + l) * N;
+#pragma unroll
+        for (int m = 0; m < 16; m++) {
+            const int mid = tcA + 16 * m;
+            const size_t addr = STRIDED ? (((size_t)mid << 8) + c0 + colA) : (((size_t)(c0 + colA) << 8) + mid);
+            v[m] = from_u64(src[addr]);
+        }
+    } else if (PRO == 1) {
         const u64 *src = fz.src + (long long)(p / fz.src_div) * fz.src_hi + (long long)(p % fz.src_div) * fz.src_lo;
         const ModConst &mt = pr.m[pi];
 #pragma unroll
@@ -363,6 +371,19 @@ __device__ __forceinline__ bool ntt16_row(const RowBatch &rb, int &p, int &l) {
     }
     return true;
 }
+// a skipped (own-digit) row of a ModUp batch: copy this CTA's 16 columns of the NTT-form input row
+__device__ __forceinline__ void copy_own_tile(const RowBatch &rb, const NttFuse &fz, int p, int l) {
+    if (!fz.copy_own) return;
+    constexpr int N = 1 << 16;
+    const u64 *src = fz.srcp.p[p / fz.src_div] + (long long)l * N;
+    u64 *a = rb.base + (long long)p * rb.poly_stride + (long long)(rb.limb0 + l) * N;
+    const int t = threadIdx.x, c0 = blockIdx.x * 16;
+#pragma unroll
+    for (int m = 0; m < 16; m++) {
+        const size_t addr = ((size_t)((t >> 4) + 16 * m) << 8) + c0 + (t & 15);
+        a[addr] = src[addr];
+    }
+}
 #ifndef BLB_NTT_F64_MINB
 #define BLB_NTT_F64_MINB 3
 #endif
@@ -374,7 +395,10 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_int(RowBatch rb, cons
                                                                 int last, const NttFuse fz) {
     __shared__ u64 sm[16 * 256];
     int p, l;
-    if (!ntt16_row(rb, p, l)) return;
+    if (!ntt16_row(rb, p, l)) {
+        if (PRO == 1 && STRIDED) copy_own_tile(rb, fz, p, l);
+        return;
+    }
     ntt16_body<INV, STRIDED, PRO, EPI, false>(sm, rb, tw_all, twd, pr, s0, last, fz, p, l);
 }
 template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0>
@@ -383,7 +407,10 @@ __global__ void __launch_bounds__(256, BLB_NTT_F64_MINB) ntt16_f64(RowBatch rb, 
                                                                     int last, const NttFuse fz) {
     __shared__ u64 sm[16 * 256];
     int p, l;
-    if (!ntt16_row(rb, p, l)) return;
+    if (!ntt16_row(rb, p, l)) {
+        if (PRO == 1 && STRIDED) copy_own_tile(rb, fz, p, l);
+        return;
+    }
     ntt16_body<INV, STRIDED, PRO, EPI, true>(sm, rb, tw_all, twd, pr, s0, last, fz, p, l);
 }
 
@@ -492,8 +519,8 @@ blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool invers
                             cudaStream_t st) {
     const int rows = rb.n_polys * rb.limbs;
     if (rows == 0) return BLB_OK;
-    if (P->logN != 16 || inverse || rows > 65535) {
-        blb_set_error("launch_ntt_fused: N = 2^16 forward batches only");
+    if (P->logN != 16 || rows > 65535 || (inverse && (fz.pro != 2 || fz.epi)) || (!inverse && fz.pro == 2)) {
+        blb_set_error("launch_ntt_fused: N = 2^16 forward batches (or inverse with pro = 2) only");
         return BLB_E_INVALID_ARG;
     }
     BLB_COUNT(2, rows);
@@ -503,6 +530,16 @@ blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool invers
     for (int h = 0; h < np2; h++) {
         const RowBatch &r = parts[h];
         dim3 g(16, rb_rows(r));
+        if (inverse) {  // pro = 2: first (contiguous) pass loads from the pointer table
+            if (rb_small(P, r)) {
+                ntt16_f64<true, false, 2, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 0, fz);
+                ntt16_f64<true, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 1, fz);
+            } else {
+                ntt16_int<true, false, 2, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 0, fz);
+                ntt16_int<true, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 1, fz);
+            }
+            continue;
+        }
         if (rb_small(P, r)) {
             if (fz.pro == 1) ntt16_f64<false, true, 1, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
             else ntt16_f64<false, true, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <map>
 #include <set>
+#include <type_traits>
 #include "blb_internal.cuh"
 
 extern "C" uint32_t blb_galois_element(const blb_params *P, int32_t step);
@@ -73,6 +74,26 @@ __global__ void k_mask_slots(const MaskDesc *descs, int m0, QKDev q, double *slo
     slots[(long long)e * q.n + s] = v ? 1.0 : 0.0;
 }
 
+// the J-sum in chunks of 4: the 16 loads of a chunk are issued before its first multiply (a runtime-J
+// loop exposed one load latency per j); missing j of the last chunk contribute 0 * 0
+#define TSUM_LOOP                                                                  \
+    for (int j0 = 0; j0 < J; j0 += 4) {                                            \
+        u64 a0[4], a1[4], b0[4], b1[4];                                            \
+        _Pragma("unroll") for (int jj = 0; jj < 4; jj++) {                         \
+            a0[jj] = a1[jj] = b0[jj] = b1[jj] = 0;                                 \
+            if (j0 + jj < J) {                                                     \
+                const u64 *a = Qp + (long long)(u * J + j0 + jj) * 2 * kN + lx;    \
+                const u64 *b = Kp + (long long)(i * J + j0 + jj) * 2 * kN + lx;    \
+                a0[jj] = a[0]; a1[jj] = a[kN]; b0[jj] = b[0]; b1[jj] = b[kN];      \
+            }                                                                      \
+        }                                                                          \
+        _Pragma("unroll") for (int jj = 0; jj < 4; jj++) {                         \
+            d0.mac(a0[jj], b0[jj]);                                                \
+            d1.mac(a0[jj], b1[jj]);                                                \
+            d1.mac(a1[jj], b0[jj]);                                                \
+            d2.mac(a1[jj], b1[jj]);                                                \
+        }                                                                          \
+    }
 // D[o][0..2] = sum_j (a0 b0, a0 b1 + a1 b0, a1 b1) with a = Qp[u*J + j], b = Kp[i*J + j], o = u*B + i.
 // 1-D grid with the output o fastest: the CTAs in flight cover all (u, i) of a few (tile, limb)
 // slices, so each Q_u / K'_i tile is read from DRAM once and reused through L2 (B and G times).
@@ -91,15 +112,7 @@ __global__ void k_tensor_sum(const u64 *Qp, const u64 *Kp, u64 *D, Primes pr, in
     if (mc.q < (1ull << 41)) {
         Acc41 d0, d1, d2;
         d0.zero(); d1.zero(); d2.zero();
-        for (int j = 0; j < J; j++) {
-            const u64 *a = Qp + (long long)(u * J + j) * 2 * kN + lx;
-            const u64 *b = Kp + (long long)(i * J + j) * 2 * kN + lx;
-            const u64 a0 = a[0], a1 = a[kN], b0 = b[0], b1 = b[kN];
-            d0.mac(a0, b0);
-            d1.mac(a0, b1);
-            d1.mac(a1, b0);
-            d2.mac(a1, b1);
-        }
+        TSUM_LOOP
         out[0] = d0.reduce(mc);
         out[kN] = d1.reduce(mc);
         out[2 * kN] = d2.reduce(mc);
@@ -107,18 +120,80 @@ __global__ void k_tensor_sum(const u64 *Qp, const u64 *Kp, u64 *D, Primes pr, in
     }
     Acc128 d0, d1, d2;
     d0.zero(); d1.zero(); d2.zero();
-    for (int j = 0; j < J; j++) {
-        const u64 *a = Qp + (long long)(u * J + j) * 2 * kN + lx;
-        const u64 *b = Kp + (long long)(i * J + j) * 2 * kN + lx;
-        const u64 a0 = a[0], a1 = a[kN], b0 = b[0], b1 = b[kN];
-        d0.mac(a0, b0);
-        d1.mac(a0, b1);
-        d1.mac(a1, b0);
-        d2.mac(a1, b1);
-    }
+    TSUM_LOOP
     out[0] = d0.reduce(mc);
     out[kN] = d1.reduce(mc);
     out[2 * kN] = d2.reduce(mc);
+}
+#undef TSUM_LOOP
+
+// 2 x 2 register-blocked J-sum: a thread owns one coefficient of the four outputs (u0 + du, i0 + di),
+// so each Q_u / K'_i word it loads feeds two outputs (half the L2 -> SM traffic of k_tensor_sum, which
+// is what bounds it: the whole J-sum is ~1.5 GB of DRAM but 8.6 GB of L2 reads one output at a time).
+// Grid: (block (u0/2, i0/2) fastest, limb, x-tile).
+// SMALL (q < 2^41): d0 and d2 on the integer pipe (Acc41), the two d1 products on the FP64 pipe
+// (AccF64, exact for < 2^10 products): the two pipes share the work.  Otherwise Acc128 throughout.
+template <bool SMALL>
+__device__ __forceinline__ void tsum22_body(const u64 *Qp, const u64 *Kp, u64 *D, int J, int B, long long kN,
+                                            long long lx, int u0, int i0, const ModConst &mc) {
+    using A = typename std::conditional<SMALL, Acc41, Acc128>::type;
+    using A1 = typename std::conditional<SMALL, AccF64, Acc128>::type;
+    const double qd = (double)mc.q, qinv = 1.0 / qd;
+    A d0[2][2], d2[2][2];
+    A1 d1[2][2];
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 2; b++) { d0[a][b].zero(); d1[a][b].zero(); d2[a][b].zero(); }
+    for (int j = 0; j < J; j++) {
+        u64 q0[2], q1[2], k0[2], k1[2];
+#pragma unroll
+        for (int a = 0; a < 2; a++) {
+            const u64 *qa = Qp + (long long)((u0 + a) * J + j) * 2 * kN + lx;
+            const u64 *kb = Kp + (long long)((i0 + a) * J + j) * 2 * kN + lx;
+            q0[a] = qa[0]; q1[a] = qa[kN]; k0[a] = kb[0]; k1[a] = kb[kN];
+        }
+#pragma unroll
+        for (int a = 0; a < 2; a++)
+#pragma unroll
+            for (int b = 0; b < 2; b++) {
+                d0[a][b].mac(q0[a], k0[b]);
+                d2[a][b].mac(q1[a], k1[b]);
+                if constexpr (SMALL) {
+                    d1[a][b].mac(q0[a], k1[b], qd, qinv);
+                    d1[a][b].mac(q1[a], k0[b], qd, qinv);
+                } else {
+                    d1[a][b].mac(q0[a], k1[b]);
+                    d1[a][b].mac(q1[a], k0[b]);
+                }
+            }
+    }
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 2; b++) {
+            u64 *out = D + (long long)((u0 + a) * B + i0 + b) * 3 * kN + lx;
+            out[0] = d0[a][b].reduce(mc);
+            if constexpr (SMALL) out[kN] = d1[a][b].reduce(qd, qinv);
+            else out[kN] = d1[a][b].reduce(mc);
+            out[2 * kN] = d2[a][b].reduce(mc);
+        }
+}
+__global__ void __launch_bounds__(kTB, 2) k_tensor_sum22(const u64 *Qp, const u64 *Kp, u64 *D, Primes pr, int J, int G,
+                                                      int B, int k, int N) {
+    const int nb = (G / 2) * (B / 2);
+    int bid = blockIdx.x;
+    const int ob = bid % nb;
+    bid /= nb;
+    const int l = bid % k;
+    const int x = (bid / k) * blockDim.x + threadIdx.x;
+    if (x >= N) return;
+    const int u0 = 2 * (ob / (B / 2)), i0 = 2 * (ob % (B / 2));
+    const long long kN = (long long)k * N, lx = (long long)l * N + x;
+    const ModConst &mc = pr.m[l];
+    // Acc41 holds < 2^14 products of 41-bit residues: 2 J per accumulator here
+    if (mc.q < (1ull << 41)) tsum22_body<true>(Qp, Kp, D, J, B, kN, lx, u0, i0, mc);
+    else tsum22_body<false>(Qp, Kp, D, J, B, kN, lx, u0, i0, mc);
 }
 
 // dst[p][i][x] = src[p][i][x] for i < k_dst (src has k_src limbs per poly): exact level drop / copy
@@ -532,8 +607,16 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
         BLB_TRY(launch_moddown_rescale(P, lvl, W + w.qacc, (G - 1) * J, W + w.qp + (size_t)J * ct_k1, conv, st));
     }
     // 3. products summed over j, relinearisation (one per (u, i)), rescale
-    k_tensor_sum<<<(unsigned)((size_t)((N + kTB - 1) / kTB) * k1 * G * B), kTB, 0, st>>>(W + w.qp, W + w.kp, W + w.d,
-                                                                                       P->pr, J, B, k1, N, G * B);
+    cudaEvent_t tt0 = blb_timing_begin(st);
+    // Acc128 without folds: <= 64 products of 61-bit residues; AccF64: < 2^10 products
+    if (G % 2 == 0 && B % 2 == 0 && 2 * J <= 64 && P->tsum22)
+        k_tensor_sum22<<<(unsigned)((size_t)((N + kTB - 1) / kTB) * k1 * (G / 2) * (B / 2)), kTB, 0, st>>>(
+            W + w.qp, W + w.kp, W + w.d, P->pr, J, G, B, k1, N);
+    else
+        k_tensor_sum<<<(unsigned)((size_t)((N + kTB - 1) / kTB) * k1 * G * B), kTB, 0, st>>>(
+            W + w.qp, W + w.kp, W + w.d, P->pr, J, B, k1, N, G * B);
+    // algorithmic bytes: the Q_u and K'_i operands once + the three-component products written
+    blb_timing_end(4, tt0, st, ((double)(G + B) * J * 2 + (double)G * B * 3) * k1 * N * 8.0);
     BLB_COUNT_LAUNCH(1);
     BLB_COUNT(3, (size_t)G * B * J);
     BLB_CHECK_LAUNCH();
