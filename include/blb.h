@@ -285,12 +285,20 @@ blb_status blb_matmul_plan_rotations(const blb_matmul_plan *plan, int32_t *steps
 /* Plaintexts owned by outputs [out_first, out_first+out_count). */
 blb_status blb_matmul_pt_count(const blb_matmul_plan *plan, int out_first, int out_count, int *n_pt);
 
+/* Bytes of the encoded plaintexts of outputs [out_first, out_first+out_count):
+ * n_pt * sum_l w_l * N with w_l = 5 bytes per coefficient for limbs whose prime
+ * is below 2^40 and 8 bytes otherwise (see blb_matmul_encode_weights).  Host out. */
+blb_status blb_matmul_pt_bytes(const blb_matmul_plan *plan, int out_first, int out_count, size_t *bytes);
+
 /* Offline precompute (row a0): build and encode the plaintexts of outputs
  * [out_first, out_first+out_count) from W (host, row-major w_rows x w_cols,
- * float64) into pt_dev (device, n_pt * (level+1) * N words).  The buffer is
- * opaque: it holds the NTT-form plaintexts in the library's blocked MAC layout
- * (per output: [limb][512-coefficient tile][plaintext][512]) so that the MAC
- * streams each output's weights contiguously.  Synchronises. */
+ * float64) into pt_dev (device, at least blb_matmul_pt_bytes bytes, 16-byte
+ * aligned).  The buffer is opaque: it holds the NTT-form plaintexts in the
+ * library's blocked MAC layout (per output: [limb][512-coefficient tile]
+ * [plaintext][tile]) so that the MAC streams each output's weights
+ * contiguously; a tile of a limb with prime < 2^40 is stored as 512 low 32-bit
+ * words followed by 512 high bytes (the residues are < 2^40: a lossless 5-byte
+ * packing of the dominant HBM stream), other limbs as 512 words.  Synchronises. */
 blb_status blb_matmul_encode_weights(const blb_matmul_plan *plan, const double *W, int out_first, int out_count,
                                      uint64_t *pt_dev, void *stream);
 

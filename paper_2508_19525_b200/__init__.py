@@ -93,6 +93,7 @@ def lib() -> ctypes.CDLL:
             "blb_matmul_plan_rotations": ([vp, vp, ip], ctypes.c_int),
             "blb_matmul_pt_count": ([vp, ctypes.c_int, ctypes.c_int, ip], ctypes.c_int),
             "blb_matmul_encode_weights": ([vp, vp, ctypes.c_int, ctypes.c_int, vp, vp], ctypes.c_int),
+            "blb_matmul_pt_bytes": ([vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
             "blb_matmul_workspace_bytes": ([vp, ctypes.c_int], ctypes.c_size_t),
             "blb_ct_pt_matmul": ([vp, vp, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t,
                                   vp], ctypes.c_int),
@@ -478,8 +479,10 @@ class MatmulPlan:
         out_count = self.n_out - out_first if out_count is None else out_count
         W = np.ascontiguousarray(W, dtype=np.float64)
         assert W.shape == self.w_shape
-        npt = self.pt_count(out_first, out_count)
-        pts = self.params.empty(max(npt, 1), self.level + 1, self.params.N)
+        nbytes = ctypes.c_size_t(0)
+        _check(lib().blb_matmul_pt_bytes(self._h, out_first, out_count, ctypes.byref(nbytes)))
+        # opaque width-packed blocked layout (include/blb.h): int64 words, 16-byte aligned
+        pts = torch.empty(max(1, (nbytes.value + 7) // 8), dtype=torch.int64, device="cuda")
         _check(lib().blb_matmul_encode_weights(self._h, W.ctypes.data_as(ctypes.c_void_p), out_first, out_count,
                                                _ptr(pts), _stream()))
         return pts

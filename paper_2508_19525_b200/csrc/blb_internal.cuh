@@ -221,6 +221,8 @@ struct blb_params {
     int fuse = 1;                 // fused ModUp / ModDown NTT prologue / epilogue (env BLB_FUSE=0 disables)
     int mac_chunk = 3;            // outputs per MAC / giant-step chunk of the two-stream schedule (env BLB_CHUNK)
     int mac_tma = 1;              // warp-specialised bulk-copy MAC (env BLB_MAC_TMA=0: register double buffer)
+    int pt_pack = 1;              // 5-byte packed plaintext limbs for primes < 2^40 (env BLB_PT_PACK=0: 8 bytes)
+    int mac_nint = 0;             // weight MAC: accumulators per output on the integer pipe, 0..2 (env BLB_MAC_NINT)
     int tsum22 = 1;               // 2 x 2 register-blocked ct-ct tensor J-sum (env BLB_TSUM22=0: one output per thread)
     int mac_j = 2;                // mask MAC over groups of mac_j (2 or 4) outputs sharing their masks (env BLB_MAC_J; 0: k_mac)
     u64 mod[BLB_MAXP];

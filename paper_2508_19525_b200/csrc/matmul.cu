@@ -144,207 +144,56 @@ __global__ void __launch_bounds__(kTB) k_mac(const u64 *__restrict__ pt, const u
     *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(mc), a11.reduce(mc));
 }
 
-// Weight MAC on the blocked plaintext layout written by blb_matmul_encode_weights:
-// output o's plaintexts are stored as [l][tile][e][512] (tile = 512 coefficients),
-// so a CTA (o, tile, l) streams one contiguous n_e * 4 KB run instead of n_e
-// 4 KB pieces 2.6 MB apart (DRAM row-buffer and TLB friendly).
-template <bool SPLIT41>
-__device__ __forceinline__ void mac_run(const u64 *__restrict__ pp, const u64 *__restrict__ R,
-                                        const int *__restrict__ ent_r, int e_lo, int n_e, long long kN,
-                                        long long lx, u64 *out, const ModConst &mc) {
-    using A = typename std::conditional<SPLIT41, Acc41, Acc128>::type;
-    A a00, a01, a10, a11;
-    a00.zero(); a01.zero(); a10.zero(); a11.zero();
-    // register double buffer: the loads of entries e+2, e+3 are in flight while e, e+1 are multiplied
-    constexpr int D = 2;
-    ulonglong2 pv[2][D], r0[2][D], r1[2][D];
-    auto load = [&](int s, int e) {
-#pragma unroll
-        for (int u = 0; u < D; u++) {
-            const int ee = e + u < n_e ? e + u : n_e - 1;
-            const int bi = ent_r[e_lo + ee];
-            pv[s][u] = *reinterpret_cast<const ulonglong2 *>(pp + (long long)ee * 512);
-            r0[s][u] = *reinterpret_cast<const ulonglong2 *>(R + (long long)bi * 2 * kN + lx);
-            r1[s][u] = *reinterpret_cast<const ulonglong2 *>(R + ((long long)bi * 2 + 1) * kN + lx);
-        }
-    };
-    auto compute = [&](int s, int e) {
-#pragma unroll
-        for (int u = 0; u < D; u++) {
-            if (e + u < n_e) {
-                a00.mac(pv[s][u].x, r0[s][u].x); a01.mac(pv[s][u].y, r0[s][u].y);
-                a10.mac(pv[s][u].x, r1[s][u].x); a11.mac(pv[s][u].y, r1[s][u].y);
-            }
-        }
-    };
-    if (n_e > 0) load(0, 0);
-    int e = 0;
-    for (; e + D < n_e; e += 2 * D) {
-        load(1, e + D);
-        compute(0, e);
-        if (e + 2 * D < n_e) load(0, e + 2 * D);
-        compute(1, e + D);
-        if (!SPLIT41 && (e & 63) == 60) {
-            a00.fold(mc); a01.fold(mc); a10.fold(mc); a11.fold(mc);
-        }
-    }
-    if (e < n_e) compute(0, e);
-    *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00.reduce(mc), a01.reduce(mc));
-    *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(mc), a11.reduce(mc));
-}
-
-__global__ void __launch_bounds__(kTB) k_mac_w(const u64 *__restrict__ pt, const u64 *__restrict__ R,
-                                               u64 *__restrict__ acc, const int *__restrict__ ent_r,
-                                               const int *__restrict__ ent_start, int o0, int e_base, int n_o, int k,
-                                               int logN, Primes pr) {
-    const int N = 1 << logN;
-    const int n_tiles = N / (2 * kTB);
-    int bid = blockIdx.x;
-    const int o = bid % n_o;
-    bid /= n_o;
-    const int tile = bid % n_tiles;
-    const int l = bid / n_tiles;
-    const long long kN = (long long)k * N;
-    const int e_lo = ent_start[o0 + o], n_e = ent_start[o0 + o + 1] - e_lo;
-    const long long lx = (long long)l * N + tile * 2 * kTB + 2 * threadIdx.x;
-    const u64 *pp = pt + (long long)(e_lo - e_base) * kN + (long long)l * n_e * N + (long long)tile * n_e * 512 +
-                    2 * threadIdx.x;
-    u64 *out = acc + (long long)o * 2 * kN + lx;
-    const ModConst &mc = pr.m[l];
-    if (mc.q < (1ull << 41)) mac_run<true>(pp, R, ent_r, e_lo, n_e, kN, lx, out, mc);
-    else mac_run<false>(pp, R, ent_r, e_lo, n_e, kN, lx, out, mc);
-}
-
-// Warp-specialised weight MAC: warp 8 streams, per pipeline stage, two entries'
-// plaintext tiles (8 KB contiguous in the blocked layout) and their four R tiles
-// (4 KB each, L2-resident) into a 4-stage shared-memory ring with cp.async.bulk
-// (TMA bulk-copy engine, mbarrier completion); warps 0-7 multiply-accumulate
-// from shared memory and release the stage.  Global latency is hidden by the
-// ring, so the 8 consumer warps only issue LDS + integer MACs.
-constexpr int kMacStages = 4, kMacEnt = 2;
-constexpr int kMacStageWords = kMacEnt * 3 * 512;  // pt, r0, r1 per entry
-constexpr size_t kMacSmem = (size_t)kMacStages * kMacStageWords * 8 + 2 * kMacStages * 8;
-
-// SPLIT41 (40-bit limbs): the c0 products on the integer pipe (Acc41), the c1 products on the
-// FP64 pipe (AccF64) -- the two pipes run side by side; 60-bit limbs: Acc128 for all four.
-template <bool SPLIT41>
-__device__ __forceinline__ void mac_tma_consume(const u64 *ring, uint64_t *full, uint64_t *empty, int n_e, u64 *out,
-                                                long long kN, const ModConst &mc) {
-    using A = typename std::conditional<SPLIT41, Acc41, Acc128>::type;
-    using A1 = typename std::conditional<SPLIT41, AccF64, Acc128>::type;
-    const double qd = (double)mc.q, qinv = 1.0 / qd;
-    A a00, a01;
-    A1 a10, a11;
-    a00.zero(); a01.zero(); a10.zero(); a11.zero();
-    const int t = threadIdx.x;
-    const int n_st = (n_e + kMacEnt - 1) / kMacEnt;
-    for (int s = 0; s < n_st; s++) {
-        const int slot = s % kMacStages;
-        mbar_wait(&full[slot], (s / kMacStages) & 1);
-        const u64 *st = ring + (size_t)slot * kMacStageWords;
-#pragma unroll
-        for (int u = 0; u < kMacEnt; u++) {
-            if (s * kMacEnt + u < n_e) {
-                const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(st + u * 512 + 2 * t);
-                const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + (kMacEnt + 2 * u) * 512 + 2 * t);
-                const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + (kMacEnt + 2 * u + 1) * 512 + 2 * t);
-                a00.mac(pv.x, r0.x); a01.mac(pv.y, r0.y);
-                if constexpr (SPLIT41) {
-                    a10.mac(pv.x, r1.x, qd, qinv); a11.mac(pv.y, r1.y, qd, qinv);
-                } else {
-                    a10.mac(pv.x, r1.x); a11.mac(pv.y, r1.y);
-                }
-            }
-        }
-        __syncwarp();
-        if ((t & 31) == 0) mbar_arrive(&empty[slot]);
-        if constexpr (!SPLIT41) {
-            if ((s & 31) == 31) {  // 64 products < 2^126: fold before the 128-bit sum can overflow
-                a00.fold(mc); a01.fold(mc); a10.fold(mc); a11.fold(mc);
-            }
-        } else {
-            if ((s & 255) == 255) {  // 512 products: keep the FP64 sums below 2^51
-                a10.fold(qd, qinv); a11.fold(qd, qinv);
-            }
-        }
-    }
-    *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00.reduce(mc), a01.reduce(mc));
-    if constexpr (SPLIT41)
-        *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(qd, qinv), a11.reduce(qd, qinv));
-    else
-        *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(mc), a11.reduce(mc));
-}
-
-__global__ void __launch_bounds__(kTB + 32) k_mac_tma(const u64 *__restrict__ pt, const u64 *__restrict__ R,
-                                                      u64 *__restrict__ acc, const int *__restrict__ ent_r,
-                                                      const int *__restrict__ ent_start, int o0, int e_base, int n_o,
-                                                      int k, int logN, Primes pr) {
-    extern __shared__ __align__(128) unsigned char smraw[];
-    u64 *ring = reinterpret_cast<u64 *>(smraw);
-    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)kMacStages * kMacStageWords);
-    uint64_t *empty = full + kMacStages;
-    const int N = 1 << logN;
-    const int n_tiles = N / (2 * kTB);
-    int bid = blockIdx.x;
-    const int o = bid % n_o;
-    bid /= n_o;
-    const int tile = bid % n_tiles;
-    const int l = bid / n_tiles;
-    const long long kN = (long long)k * N;
-    const int e_lo = ent_start[o0 + o], n_e = ent_start[o0 + o + 1] - e_lo;
-    const long long lx0 = (long long)l * N + tile * 2 * kTB;
-    const u64 *pp = pt + (long long)(e_lo - e_base) * kN + (long long)l * n_e * N + (long long)tile * n_e * 512;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kMacStages; s++) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kTB / 32);
-        }
-        mbar_fence_init();
-    }
-    __syncthreads();
-    const int n_st = (n_e + kMacEnt - 1) / kMacEnt;
-    if (threadIdx.x >= kTB) {  // producer warp
-        const int lane = threadIdx.x - kTB;
-        if (lane == 0) {
-            for (int s = 0; s < n_st; s++) {
-                const int slot = s % kMacStages;
-                if (s >= kMacStages) mbar_wait(&empty[slot], ((s / kMacStages) - 1) & 1);
-                const int ne = min(kMacEnt, n_e - s * kMacEnt);
-                u64 *st = ring + (size_t)slot * kMacStageWords;
-                mbar_expect_tx(&full[slot], (unsigned)ne * 3 * 4096);
-                bulk_g2s(st, pp + (long long)s * kMacEnt * 512, (unsigned)ne * 4096, &full[slot]);
-                for (int u = 0; u < ne; u++) {
-                    const int bi = ent_r[e_lo + s * kMacEnt + u];
-                    bulk_g2s(st + (kMacEnt + 2 * u) * 512, R + (long long)bi * 2 * kN + lx0, 4096, &full[slot]);
-                    bulk_g2s(st + (kMacEnt + 2 * u + 1) * 512, R + ((long long)bi * 2 + 1) * kN + lx0, 4096,
-                             &full[slot]);
-                }
-            }
-        }
-        return;
-    }
-    u64 *out = acc + (long long)o * 2 * kN + lx0 + 2 * threadIdx.x;
-    const ModConst &mc = pr.m[l];
-    if (mc.q < (1ull << 41)) mac_tma_consume<true>(ring, full, empty, n_e, out, kN, mc);
-    else mac_tma_consume<false>(ring, full, empty, n_e, out, kN, mc);
-}
-
-// Multi-output variant: a CTA accumulates kMacP outputs (b', g) that share the same (b, i) entry
-// list (so the same R tiles) for one (tile, limb): per pipeline stage one entry = kMacP
-// plaintext tiles + the two R tiles.  R is staged once per kMacP outputs instead of once per
-// output, so two thirds of the bytes in flight are the HBM plaintext stream (one third before):
-// the single-output kernel's consumers sat on the full barrier waiting for data.
+// Weight MAC (row a3) on the blocked, width-packed plaintext layout written by
+// blb_matmul_encode_weights.  Plaintext residues are uniform in [0, q), so a limb whose prime is
+// below 2^40 (four of the five BERT chain primes) is stored in 5 bytes per coefficient as two planes
+// per 512-coefficient tile -- 512 low 32-bit words then 512 high bytes (2560 B instead of 4096 B);
+// other limbs keep 8 bytes.  The plaintext stream is the dominant HBM traffic of the step, and the
+// split is exactly the (a0, a1) split the Acc41 accumulator multiplies with.  Layout (bytes): output
+// o's plaintexts start at (e_lo(o) - e_base) * bpp (bpp = sum_l w_l N); inside, [limb l][tile][entry]
+// [512 * w_l bytes], limb l at n_e N sum_{l' < l} w_l'.
+//
+// Multi-output kernel: a CTA accumulates kMacP outputs (b', g) that share the same (b, i) entry list
+// (so the same R tiles) for one (tile, limb): per pipeline stage one entry = kMacP plaintext tiles +
+// the two R tiles, staged by a producer warp with cp.async.bulk into a shared-memory ring (mbarrier
+// completion); 8 consumer warps multiply.  R is staged once per kMacP outputs.  kMacP = 1 is the
+// general fallback (any plan).
+struct PtLayout {
+    int w[BLB_MAXP];         // bytes per coefficient of limb l (5 = packed, 8 = plain)
+    long long loff[BLB_MAXP];  // sum_{l' < l} w_l' * N (times n_e: the limb offset inside an output block)
+    long long bpp;           // bytes per plaintext = sum_l w_l N
+};
 template <int PP, int STG>
 constexpr size_t mac4_smem() { return (size_t)STG * (PP + 2) * 512 * 8 + 2 * STG * 8; }
 
-template <bool SPLIT41, int kMacP, int kM4Stages>
+// accumulator helpers with one call signature (Acc41 / Acc128 ignore the FP64 constants)
+__device__ __forceinline__ void accm(Acc41 &a, u64 x, u64 y, double, double) { a.mac(x, y); }
+__device__ __forceinline__ void accm(Acc128 &a, u64 x, u64 y, double, double) { a.mac(x, y); }
+__device__ __forceinline__ void accm(AccF64 &a, u64 x, u64 y, double qd, double qinv) { a.mac(x, y, qd, qinv); }
+__device__ __forceinline__ u64 accr(const Acc41 &a, const ModConst &mc, double, double) { return a.reduce(mc); }
+__device__ __forceinline__ u64 accr(const Acc128 &a, const ModConst &mc, double, double) { return a.reduce(mc); }
+__device__ __forceinline__ u64 accr(const AccF64 &a, const ModConst &, double qd, double qinv) { return a.reduce(qd, qinv); }
+__device__ __forceinline__ void accf(Acc41 &, const ModConst &, double, double) {}  // exact for < 2^14 products
+__device__ __forceinline__ void accf(Acc128 &a, const ModConst &mc, double, double) { a.fold(mc); }
+__device__ __forceinline__ void accf(AccF64 &a, const ModConst &, double qd, double qinv) { a.fold(qd, qinv); }
+
+// SPLIT41 (q < 2^41): NINT of the four accumulators of an output -- (c0, x), (c0, x+1), (c1, x),
+// (c1, x+1) in that order -- run on the integer pipe (Acc41), the others on the FP64 pipe (AccF64);
+// the split balances the fma-heavy and FP64 pipes.  Otherwise Acc128 throughout.
+template <bool SPLIT41, bool PACKED, int kMacP, int kM4Stages, int NINT>
 __device__ __forceinline__ void mac4_consume(const u64 *ring, uint64_t *full, uint64_t *empty, int n_e, int nP,
                                              u64 *const *outs, long long kN, const ModConst &mc) {
-    using A = typename std::conditional<SPLIT41, Acc41, Acc128>::type;
-    using A1 = typename std::conditional<SPLIT41, AccF64, Acc128>::type;
+    using I = typename std::conditional<SPLIT41, Acc41, Acc128>::type;
+    using F = typename std::conditional<SPLIT41, AccF64, Acc128>::type;
+    using T0 = typename std::conditional<(NINT >= 1), I, F>::type;
+    using T1 = typename std::conditional<(NINT >= 2), I, F>::type;
+    using T2 = typename std::conditional<(NINT >= 3), I, F>::type;
+    using T3 = typename std::conditional<(NINT >= 4), I, F>::type;
     const double qd = (double)mc.q, qinv = 1.0 / qd;
-    A a00[kMacP], a01[kMacP];
-    A1 a10[kMacP], a11[kMacP];
+    T0 a00[kMacP];
+    T1 a01[kMacP];
+    T2 a10[kMacP];
+    T3 a11[kMacP];
 #pragma unroll
     for (int j = 0; j < kMacP; j++) { a00[j].zero(); a01[j].zero(); a10[j].zero(); a11[j].zero(); }
     constexpr int kM4StageWords = (kMacP + 2) * 512;
@@ -358,26 +207,30 @@ __device__ __forceinline__ void mac4_consume(const u64 *ring, uint64_t *full, ui
 #pragma unroll
         for (int j = 0; j < kMacP; j++) {
             if (j < nP) {
-                const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(st + j * 512 + 2 * t);
-                a00[j].mac(pv.x, r0.x); a01[j].mac(pv.y, r0.y);
-                if constexpr (SPLIT41) {
-                    a10[j].mac(pv.x, r1.x, qd, qinv); a11[j].mac(pv.y, r1.y, qd, qinv);
+                ulonglong2 pv;
+                if constexpr (PACKED) {  // slot j: 512 low words, then 512 high bytes
+                    const uint2 lo = *reinterpret_cast<const uint2 *>(reinterpret_cast<const uint32_t *>(st + j * 512) + 2 * t);
+                    const unsigned short hi =
+                        *(reinterpret_cast<const unsigned short *>(reinterpret_cast<const unsigned char *>(st + j * 512) + 2048) + t);
+                    pv.x = ((u64)(hi & 0xFF) << 32) | lo.x;
+                    pv.y = ((u64)(hi >> 8) << 32) | lo.y;
                 } else {
-                    a10[j].mac(pv.x, r1.x); a11[j].mac(pv.y, r1.y);
+                    pv = *reinterpret_cast<const ulonglong2 *>(st + j * 512 + 2 * t);
                 }
+                accm(a00[j], pv.x, r0.x, qd, qinv);
+                accm(a01[j], pv.y, r0.y, qd, qinv);
+                accm(a10[j], pv.x, r1.x, qd, qinv);
+                accm(a11[j], pv.y, r1.y, qd, qinv);
             }
         }
         __syncwarp();
         if ((t & 31) == 0) mbar_arrive(&empty[slot]);
-        if constexpr (!SPLIT41) {
-            if ((s & 63) == 63) {  // 64 products < 2^126
+        // Acc128: fold every 64 products (< 2^126); AccF64: every 512 (sums below 2^51)
+        if ((!SPLIT41 && (s & 63) == 63) || (SPLIT41 && (s & 511) == 511)) {
 #pragma unroll
-                for (int j = 0; j < kMacP; j++) { a00[j].fold(mc); a01[j].fold(mc); a10[j].fold(mc); a11[j].fold(mc); }
-            }
-        } else {
-            if ((s & 511) == 511) {  // 512 products: FP64 sums below 2^51
-#pragma unroll
-                for (int j = 0; j < kMacP; j++) { a10[j].fold(qd, qinv); a11[j].fold(qd, qinv); }
+            for (int j = 0; j < kMacP; j++) {
+                accf(a00[j], mc, qd, qinv); accf(a01[j], mc, qd, qinv);
+                accf(a10[j], mc, qd, qinv); accf(a11[j], mc, qd, qinv);
             }
         }
     }
@@ -385,21 +238,18 @@ __device__ __forceinline__ void mac4_consume(const u64 *ring, uint64_t *full, ui
     for (int j = 0; j < kMacP; j++) {
         if (j < nP) {
             u64 *out = outs[j] + 2 * t;
-            *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00[j].reduce(mc), a01[j].reduce(mc));
-            if constexpr (SPLIT41)
-                *reinterpret_cast<ulonglong2 *>(out + kN) =
-                    make_ulonglong2(a10[j].reduce(qd, qinv), a11[j].reduce(qd, qinv));
-            else
-                *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10[j].reduce(mc), a11[j].reduce(mc));
+            *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(accr(a00[j], mc, qd, qinv), accr(a01[j], mc, qd, qinv));
+            *reinterpret_cast<ulonglong2 *>(out + kN) =
+                make_ulonglong2(accr(a10[j], mc, qd, qinv), accr(a11[j], mc, qd, qinv));
         }
     }
 }
 
-template <int kMacP, int kM4Stages, int MINB>
-__global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const u64 *__restrict__ pt, const u64 *__restrict__ R,
+template <int kMacP, int kM4Stages, int MINB, int NINT = 2>
+__global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char *__restrict__ pt, const u64 *__restrict__ R,
                                                        u64 *__restrict__ acc, const int *__restrict__ ent_r,
                                                        const int *__restrict__ ent_start, int o0, int e_base, int n_o,
-                                                       int k, int logN, Primes pr) {
+                                                       int k, int logN, Primes pr, PtLayout lay) {
     constexpr int kM4StageWords = (kMacP + 2) * 512;
     extern __shared__ __align__(128) unsigned char smraw[];
     u64 *ring = reinterpret_cast<u64 *>(smraw);
@@ -417,6 +267,8 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const u64 *__restri
     const long long kN = (long long)k * N;
     const int e_lo = ent_start[o0 + oa], n_e = ent_start[o0 + oa + 1] - e_lo;
     const long long lx0 = (long long)l * N + tile * 2 * kTB;
+    const int w = lay.w[l];
+    const unsigned tb = 512u * (unsigned)w;  // bytes of one plaintext tile of this limb
     if (threadIdx.x == 0) {
         for (int s = 0; s < kM4Stages; s++) {
             mbar_init(&full[s], 1);
@@ -427,17 +279,17 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const u64 *__restri
     __syncthreads();
     if (threadIdx.x >= kTB) {  // producer warp
         if (threadIdx.x == kTB) {
-            const u64 *pp[kMacP];
+            const unsigned char *pp[kMacP];
 #pragma unroll
             for (int j = 0; j < kMacP; j++)
-                pp[j] = pt + (long long)(ent_start[o0 + oa + (j < nP ? j : 0)] - e_base) * kN + (long long)l * n_e * N +
-                        (long long)tile * n_e * 512;
+                pp[j] = pt + (long long)(ent_start[o0 + oa + (j < nP ? j : 0)] - e_base) * lay.bpp +
+                        (long long)n_e * lay.loff[l] + (long long)tile * n_e * tb;
             for (int s = 0; s < n_e; s++) {
                 const int slot = s % kM4Stages;
                 if (s >= kM4Stages) mbar_wait(&empty[slot], ((s / kM4Stages) - 1) & 1);
                 u64 *st = ring + (size_t)slot * kM4StageWords;
-                mbar_expect_tx(&full[slot], (unsigned)(nP + 2) * 4096);
-                for (int j = 0; j < nP; j++) bulk_g2s(st + j * 512, pp[j] + (long long)s * 512, 4096, &full[slot]);
+                mbar_expect_tx(&full[slot], (unsigned)nP * tb + 2u * 4096u);
+                for (int j = 0; j < nP; j++) bulk_g2s(st + j * 512, pp[j] + (long long)s * tb, tb, &full[slot]);
                 const int bi = ent_r[e_lo + s];
                 bulk_g2s(st + kMacP * 512, R + (long long)bi * 2 * kN + lx0, 4096, &full[slot]);
                 bulk_g2s(st + (kMacP + 1) * 512, R + ((long long)bi * 2 + 1) * kN + lx0, 4096, &full[slot]);
@@ -449,22 +301,46 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const u64 *__restri
 #pragma unroll
     for (int j = 0; j < kMacP; j++) outs[j] = acc + (long long)(oa + (j < nP ? j : 0)) * 2 * kN + lx0;
     const ModConst &mc = pr.m[l];
-    if (mc.q < (1ull << 41)) mac4_consume<true, kMacP, kM4Stages>(ring, full, empty, n_e, nP, outs, kN, mc);
-    else mac4_consume<false, kMacP, kM4Stages>(ring, full, empty, n_e, nP, outs, kN, mc);
+    if (w == 5) mac4_consume<true, true, kMacP, kM4Stages, NINT>(ring, full, empty, n_e, nP, outs, kN, mc);
+    else if (mc.q < (1ull << 41))
+        mac4_consume<true, false, kMacP, kM4Stages, NINT>(ring, full, empty, n_e, nP, outs, kN, mc);
+    else mac4_consume<false, false, kMacP, kM4Stages, 4>(ring, full, empty, n_e, nP, outs, kN, mc);
 }
 
-template <int PP, int STG, int MINB>
-static void launch_mac4(const u64 *pt, const u64 *R, u64 *acc, const int *ent_r, const int *ent_start, int o0,
-                        int e_base, int n_o, int k, int logN, const Primes &pr, int n_tiles, cudaStream_t st) {
+template <int PP, int STG, int MINB, int NINT = 2>
+static void launch_mac4(const unsigned char *pt, const u64 *R, u64 *acc, const int *ent_r, const int *ent_start, int o0,
+                        int e_base, int n_o, int k, int logN, const Primes &pr, int n_tiles, const PtLayout &lay,
+                        cudaStream_t st) {
     static bool attr = false;
     constexpr size_t smem = mac4_smem<PP, STG>();
     if (!attr) {
-        cudaFuncSetAttribute(k_mac_tma4<PP, STG, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_mac_tma4<PP, STG, MINB, NINT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
     const size_t n_grp = (size_t)(n_o + PP - 1) / PP;
-    k_mac_tma4<PP, STG, MINB><<<(unsigned)(n_grp * n_tiles * k), kTB + 32, smem, st>>>(pt, R, acc, ent_r, ent_start, o0,
-                                                                                      e_base, n_o, k, logN, pr);
+    k_mac_tma4<PP, STG, MINB, NINT><<<(unsigned)(n_grp * n_tiles * k), kTB + 32, smem, st>>>(pt, R, acc, ent_r, ent_start, o0,
+                                                                                      e_base, n_o, k, logN, pr, lay);
+}
+
+// scatter standard [cnt][k][N] plaintexts (entries e0..e0+cnt of the plan) into the blocked, width-packed layout
+__global__ void k_block_pts(const u64 *src, unsigned char *dst, const int *ent_start, const int *ent_o, int e0,
+                            int e_base, int k, int N, PtLayout lay) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int l = blockIdx.y, t = blockIdx.z;
+    if (x >= N) return;
+    const int e = e0 + t;
+    const int o = ent_o[e];
+    const int e_lo = ent_start[o], n_e = ent_start[o + 1] - e_lo;
+    const int w = lay.w[l];
+    unsigned char *tile = dst + (long long)(e_lo - e_base) * lay.bpp + (long long)n_e * lay.loff[l] +
+                          ((long long)(x >> 9) * n_e + (e - e_lo)) * 512 * w;
+    const u64 v = src[(long long)t * k * N + (long long)l * N + x];
+    if (w == 5) {
+        reinterpret_cast<uint32_t *>(tile)[x & 511] = (uint32_t)v;
+        tile[2048 + (x & 511)] = (unsigned char)(v >> 32);
+    } else {
+        reinterpret_cast<u64 *>(tile)[x & 511] = v;
+    }
 }
 
 // Indexed mask MAC for JG consecutive outputs that share their plaintext (mask) list and differ only
@@ -586,21 +462,6 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_j(const u64 *__restrict_
     const ModConst &mc = pr.m[l < kq ? l : Kfull + (l - kq)];
     if (mc.q < (1ull << 41)) macj_consume<true, JG>(ring, full, empty, n_e, outs, kN, mc);
     else macj_consume<false, JG>(ring, full, empty, n_e, outs, kN, mc);
-}
-
-// scatter standard [cnt][k][N] plaintexts (entries e0..e0+cnt of the plan) into the blocked layout
-__global__ void k_block_pts(const u64 *src, u64 *dst, const int *ent_start, const int *ent_o, int e0, int e_base,
-                            int k, int N) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int l = blockIdx.y, t = blockIdx.z;
-    if (x >= N) return;
-    const int e = e0 + t;
-    const int o = ent_o[e];
-    const int e_lo = ent_start[o], n_e = ent_start[o + 1] - e_lo;
-    const long long kN = (long long)k * N;
-    const long long off = (long long)(e_lo - e_base) * kN + (long long)l * n_e * N + (long long)(x >> 9) * n_e * 512 +
-                          (long long)(e - e_lo) * 512 + (x & 511);
-    dst[off] = src[(long long)t * kN + (long long)l * N + x];
 }
 
 // dst[o] += src[j] for the jobs of one giant batch (sequential per thread: no races)
@@ -855,6 +716,29 @@ static blb_status check_slice(const blb_matmul_plan *pl, int out_first, int out_
     return BLB_OK;
 }
 
+// width-packed blocked plaintext layout of the plan's level (see the weight MAC above)
+static PtLayout pt_layout(const blb_matmul_plan *pl) {
+    const blb_params *P = pl->P;
+    const int k = pl->level + 1;
+    PtLayout lay{};
+    long long off = 0;
+    for (int l = 0; l < k; l++) {
+        lay.w[l] = (P->pt_pack && P->mod[l] < (1ull << 40) && P->logN >= 9) ? 5 : 8;
+        lay.loff[l] = off;
+        off += (long long)lay.w[l] * P->N;
+    }
+    lay.bpp = off;
+    return lay;
+}
+
+extern "C" blb_status blb_matmul_pt_bytes(const blb_matmul_plan *pl, int out_first, int out_count, size_t *bytes) {
+    if (!pl || !bytes) return BLB_E_INVALID_ARG;
+    BLB_TRY(check_slice(pl, out_first, out_count));
+    const long long n = pl->ent_start[(out_first + out_count) * pl->G] - pl->ent_start[out_first * pl->G];
+    *bytes = (size_t)n * (size_t)pt_layout(pl).bpp;
+    return BLB_OK;
+}
+
 extern "C" blb_status blb_matmul_pt_count(const blb_matmul_plan *pl, int out_first, int out_count, int *n_pt) {
     if (!pl || !n_pt) return BLB_E_INVALID_ARG;
     BLB_TRY(check_slice(pl, out_first, out_count));
@@ -894,8 +778,9 @@ extern "C" blb_status blb_matmul_encode_weights(const blb_matmul_plan *pl, const
         BLB_COUNT_LAUNCH(1);
         s = launch_encode(P, slots, cnt, scale, pl->level, tmp, buf, flag, st);
         if (s == BLB_OK) {
-            k_block_pts<<<dim3((P->N + kTB - 1) / kTB, k, cnt), kTB, 0, st>>>(tmp, pt_dev, pl->d_ent_start,
-                                                                             pl->d_ent + ne_total, e, e0, k, P->N);
+            k_block_pts<<<dim3((P->N + kTB - 1) / kTB, k, cnt), kTB, 0, st>>>(
+                tmp, reinterpret_cast<unsigned char *>(pt_dev), pl->d_ent_start, pl->d_ent + ne_total, e, e0, k, P->N,
+                pt_layout(pl));
             BLB_COUNT_LAUNCH(1);
         }
     }
@@ -1048,35 +933,35 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
             u64 *acc_c = acc + (size_t)c0 * pl->G * ctN;
             if (n_o > 0) {
                 const int n_tiles = N / (2 * kTB);
+                const PtLayout lay = pt_layout(pl);
+                const unsigned char *ptb = reinterpret_cast<const unsigned char *>(pt_dev);
                 cudaEvent_t t0 = blb_timing_begin(st);
                 // groups of PP consecutive (b', g) with one entry list -> the multi-output kernel
                 // (BLB_MAC_TMA: 1 = 2 outputs x 3 CTAs/SM (default), 4 = 4 outputs x 1 CTA/SM x 8 stages,
-                //  2 = single-output TMA kernel, 0 = k_mac_w)
+                //  0 = one output per CTA); plans whose pairs differ fall back to one output per CTA
                 const int PP = P->mac_tma == 4 ? 4 : 2;
                 bool grouped = P->mac_tma == 1 || P->mac_tma == 4;
                 for (int j = 0; j < n_o && grouped; j++)
                     if (j % PP != PP - 1 && j + 1 < n_o && !pl->same_next[o0 + j]) grouped = false;
-                if (grouped && PP == 2)
-                    launch_mac4<2, 4, 3>(pt_dev, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
-                                         P->pr, n_tiles, st);
+                // BLB_MAC_NINT: accumulators per output on the integer pipe (0..2; the rest on FP64)
+                if (grouped && PP == 2 && P->mac_nint == 0)
+                    launch_mac4<2, 4, 3, 0>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
+                                            P->pr, n_tiles, lay, st);
+                else if (grouped && PP == 2 && P->mac_nint == 1)
+                    launch_mac4<2, 4, 3, 1>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
+                                            P->pr, n_tiles, lay, st);
+                else if (grouped && PP == 2)
+                    launch_mac4<2, 4, 3, 2>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
+                                            P->pr, n_tiles, lay, st);
                 else if (grouped)
-                    launch_mac4<4, 8, 1>(pt_dev, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
-                                         P->pr, n_tiles, st);
-                else if (P->mac_tma) {
-                    static bool attr = false;
-                    if (!attr) {
-                        cudaFuncSetAttribute(k_mac_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMacSmem);
-                        attr = true;
-                    }
-                    k_mac_tma<<<(unsigned)((size_t)n_o * n_tiles * k), kTB + 32, kMacSmem, st>>>(
-                        pt_dev, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN, P->pr);
-                } else
-                k_mac_w<<<(unsigned)((size_t)n_o * n_tiles * k), kTB, 0, st>>>(pt_dev, R, acc_c, pl->d_ent,
-                                                                              pl->d_ent_start, o0, e_base, n_o, k,
-                                                                              P->logN, P->pr);
+                    launch_mac4<4, 8, 1>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
+                                         P->pr, n_tiles, lay, st);
+                else
+                    launch_mac4<1, 4, 3>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
+                                         P->pr, n_tiles, lay, st);
                 BLB_COUNT_LAUNCH(1);
                 BLB_COUNT(3, n_entries);
-                blb_timing_end(0, t0, st, (double)n_entries * k * N * 8.0);
+                blb_timing_end(0, t0, st, (double)n_entries * (double)lay.bpp);  // packed plaintext bytes
                 BLB_CHECK_LAUNCH();
             }
         }
