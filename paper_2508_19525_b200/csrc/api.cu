@@ -253,6 +253,9 @@ extern "C" blb_status blb_params_create(blb_params **out, int log_n, const uint6
     if (const char *v = getenv("BLB_TSUM22")) P->tsum22 = atoi(v);
     if (const char *v = getenv("BLB_PT_PACK")) P->pt_pack = atoi(v);
     if (const char *v = getenv("BLB_MAC_NINT")) P->mac_nint = atoi(v);
+    if (const char *v = getenv("BLB_MACJ_ACC")) P->macj_acc = atoi(v);
+    if (const char *v = getenv("BLB_KS_ACC")) P->ks_acc = atoi(v);
+    if (const char *v = getenv("BLB_TSUM_ACC")) P->tsum_acc = atoi(v);
     if (const char *v = getenv("BLB_FUSE")) P->fuse = atoi(v);
     if (cudaStreamCreateWithFlags(&P->aux, cudaStreamNonBlocking) != cudaSuccess) P->aux = nullptr;
     for (auto &e : P->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);

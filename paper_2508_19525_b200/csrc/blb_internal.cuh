@@ -164,6 +164,59 @@ struct AccF64 {
     }
 };
 
+// Grid-split FP64 accumulator for residues < 2^41: no reduction per product.  The running sum
+// s = M + H 2^40 (M = 1.5 * 2^92) stays in [2^92, 2^93), where the double grid is 2^40: each product
+// is added with one fma, s' = fl(s + A B), and its rounding error A B + s - s' (|.| <= 2^39, exact:
+// s - s' is an exact multiple of 2^40) is recovered with a second fma and summed in l.  Per product:
+// 2 fma + 2 add on the FP64 pipe, nothing else (AccF64: 6 FP64 ops).  Exact for <= 512 products of
+// residues < 2^41 between folds (s < M + 2^91 = 2^93, l < 2^48); the value is (s - M) + l.
+struct AccG {
+    double s, l;
+    static constexpr double kM = 0x1.8p+92;  // 1.5 * 2^92
+    __device__ __forceinline__ void zero() { s = kM; l = 0.0; }
+    __device__ __forceinline__ void mac(u64 a, u64 b) { macd(AccF64::u2d(a), AccF64::u2d(b)); }
+    __device__ __forceinline__ void macd(double A, double B) {  // A, B: integers < 2^41
+        const double sn = __fma_rn(A, B, s);
+        l = __dadd_rn(l, __fma_rn(A, B, __dsub_rn(s, sn)));
+        s = sn;
+    }
+    // (s - M) + l mod q as a double with |value| < q + 2^49 (exact)
+    __device__ __forceinline__ double rem(double qd, double qinv) const {
+        const double magic = 6755399441055744.0;
+        const double Hd = __dmul_rn(__dsub_rn(s, kM), 0x1p-40);  // H < 2^51, exact
+        const double Hm = __fma_rn(-__dsub_rn(__fma_rn(Hd, qinv, magic), magic), qd, Hd);  // |Hm| <= q/2 + 1
+        const double two40 = 1099511627776.0;
+        const double c40 = __fma_rn(-__dsub_rn(__fma_rn(two40, qinv, magic), magic), qd, two40);  // 2^40 mod q, centred
+        const double p = __dmul_rn(Hm, c40);
+        const double e = __fma_rn(Hm, c40, -p);
+        const double c = __dsub_rn(__fma_rn(p, qinv, magic), magic);
+        return __dadd_rn(__dadd_rn(__fma_rn(-c, qd, p), e), l);
+    }
+    __device__ __forceinline__ void fold(double qd, double qinv) {
+        l = rem(qd, qinv);
+        s = kM;
+    }
+    __device__ __forceinline__ u64 reduce(double qd, double qinv) const {
+        AccF64 f;
+        f.r = rem(qd, qinv);
+        return f.reduce(qd, qinv);
+    }
+};
+
+// accumulator helpers with one call signature (Acc41 / Acc128 ignore the FP64 constants)
+__device__ __forceinline__ void accm(Acc41 &a, u64 x, u64 y, double, double) { a.mac(x, y); }
+__device__ __forceinline__ void accm(Acc128 &a, u64 x, u64 y, double, double) { a.mac(x, y); }
+__device__ __forceinline__ void accm(AccF64 &a, u64 x, u64 y, double qd, double qinv) { a.mac(x, y, qd, qinv); }
+__device__ __forceinline__ u64 accr(const Acc41 &a, const ModConst &mc, double, double) { return a.reduce(mc); }
+__device__ __forceinline__ u64 accr(const Acc128 &a, const ModConst &mc, double, double) { return a.reduce(mc); }
+__device__ __forceinline__ u64 accr(const AccF64 &a, const ModConst &, double qd, double qinv) { return a.reduce(qd, qinv); }
+__device__ __forceinline__ void accf(Acc41 &, const ModConst &, double, double) {}  // exact for < 2^14 products
+__device__ __forceinline__ void accf(Acc128 &a, const ModConst &mc, double, double) { a.fold(mc); }
+__device__ __forceinline__ void accf(AccF64 &a, const ModConst &, double qd, double qinv) { a.fold(qd, qinv); }
+__device__ __forceinline__ void accm(AccG &a, u64 x, u64 y, double, double) { a.mac(x, y); }
+__device__ __forceinline__ u64 accr(const AccG &a, const ModConst &, double qd, double qinv) { return a.reduce(qd, qinv); }
+__device__ __forceinline__ void accf(AccG &a, const ModConst &, double qd, double qinv) { a.fold(qd, qinv); }
+
 // ---------------------------------------------------------------------------
 // mbarrier + bulk-copy (TMA engine, cp.async.bulk) helpers
 // ---------------------------------------------------------------------------
@@ -222,7 +275,10 @@ struct blb_params {
     int mac_chunk = 3;            // outputs per MAC / giant-step chunk of the two-stream schedule (env BLB_CHUNK)
     int mac_tma = 1;              // warp-specialised bulk-copy MAC (env BLB_MAC_TMA=0: register double buffer)
     int pt_pack = 1;              // 5-byte packed plaintext limbs for primes < 2^40 (env BLB_PT_PACK=0: 8 bytes)
-    int mac_nint = 0;             // weight MAC: accumulators per output on the integer pipe, 0..2 (env BLB_MAC_NINT)
+    int tsum_acc = 1;             // tensor J-sum accumulators: 1 AccG, 0 Acc41 + AccF64 (env BLB_TSUM_ACC)
+    int ks_acc = 1;               // key-switch inner product accumulators (40-bit limbs), see k_ks_inner (env BLB_KS_ACC)
+    int macj_acc = 2;             // mask MAC accumulators: 0 Acc41 + AccF64, 1 Acc41 + AccG, 2 AccG (env BLB_MACJ_ACC)
+    int mac_nint = -1;            // weight MAC: accumulators per output on the integer pipe, 0..2 (env BLB_MAC_NINT)
     int tsum22 = 1;               // 2 x 2 register-blocked ct-ct tensor J-sum (env BLB_TSUM22=0: one output per thread)
     int mac_j = 2;                // mask MAC over groups of mac_j (2 or 4) outputs sharing their masks (env BLB_MAC_J; 0: k_mac)
     u64 mod[BLB_MAXP];

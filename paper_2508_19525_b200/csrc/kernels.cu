@@ -215,7 +215,9 @@ struct KsGroups {
 // jobs.j[t].out ([2][E][N]) -- the double-hoisted rotation (no ModDown).
 // SMALL (prime < 2^41): the a-part products run on the FP64 pipe (AccF64), the b-part on the
 // integer pipe, so the two pipes share the 2 beta products per job.
-template <int BETA, bool EXT, bool SMALL>
+// KA (SMALL only, env BLB_KS_ACC): 0 = b-part Acc128 + a-part AccF64, 1 = both AccG (FP64 pipe,
+// no per-product reduction), 2 = b-part Acc41 + a-part AccG
+template <int BETA, bool EXT, bool SMALL, int KA>
 __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups &grp, u64 *u, const Primes &pr, int k,
                                               int np, int K, int beta_rt, int logN, const PinvTab &pq, int x, int m,
                                               int gi) {
@@ -229,9 +231,11 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
     // contiguous and only the two outputs are scattered, to x = perm_{g^-1}(y)
     const uint32_t dst = J0.galois == 1 ? (uint32_t)x : galois_perm(x, J0.galois_inv, logN);
     const ModConst &mc = pr.m[pm];
-    using A1 = typename std::conditional<SMALL, AccF64, Acc128>::type;
+    using A1 = typename std::conditional<SMALL, typename std::conditional<(KA >= 1), AccG, AccF64>::type, Acc128>::type;
+    using A0 = typename std::conditional<SMALL && KA == 1, AccG,
+                                         typename std::conditional<SMALL && KA == 2, Acc41, Acc128>::type>::type;
     const double qd = (double)mc.q, qinv = 1.0 / qd;
-    Acc128 a0[kKsGroup];
+    A0 a0[kKsGroup];
     A1 a1[kKsGroup];
 #pragma unroll
     for (int q = 0; q < kKsGroup; q++) { a0[q].zero(); a1[q].zero(); }
@@ -251,9 +255,8 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
                 for (int j = 0; j < BETA; j++) e[j] = ext[(long long)j * E * N];
 #pragma unroll
                 for (int j = 0; j < BETA; j++) {
-                    a0[q].mac(e[j], kb[j]);
-                    if constexpr (SMALL) a1[q].mac(e[j], ka[j], qd, qinv);
-                    else a1[q].mac(e[j], ka[j]);
+                    accm(a0[q], e[j], kb[j], qd, qinv);
+                    accm(a1[q], e[j], ka[j], qd, qinv);
                 }
             }
         }
@@ -265,17 +268,13 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
             for (int q = 0; q < kKsGroup; q++) {
                 if (q < cnt) {
                     const u64 e = jobs.j[t0 + q].ext[((long long)j * E + m) * N + x];
-                    a0[q].mac(e, kb);
-                    if constexpr (SMALL) a1[q].mac(e, ka, qd, qinv);
-                    else a1[q].mac(e, ka);
+                    accm(a0[q], e, kb, qd, qinv);
+                    accm(a1[q], e, ka, qd, qinv);
                 }
             }
         }
     }
-    auto a1r = [&](int q) -> u64 {
-        if constexpr (SMALL) return a1[q].reduce(qd, qinv);
-        else return a1[q].reduce(mc);
-    };
+    auto a1r = [&](int q) -> u64 { return accr(a1[q], mc, qd, qinv); };
     // The additive terms: EXT adds P c0 (and P c1_add) over the Q limbs of the extended result.  The
     // ModDown path folds the rotation's sigma_g(c0) (add_mode 1) or the relinearisation's (c0, c1)
     // (add_mode 2) in the same way: ModDown(u + P c) = ModDown(u) + c exactly (P P^{-1} = 1 mod q_i;
@@ -298,7 +297,7 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
         if (q < cnt) {
             const int t = t0 + q;
             const KsJob &J = jobs.j[t];
-            u64 r0 = a0[q].reduce(mc), r1 = a1r(q);
+            u64 r0 = accr(a0[q], mc, qd, qinv), r1 = a1r(q);
             if (m < k) {
                 r0 = addmod(r0, shoup(c0v[q], pq.v[m], pq.sh[m], mc.q), mc.q);
                 r1 = addmod(r1, shoup(c1v[q], pq.v[m], pq.sh[m], mc.q), mc.q);
@@ -317,7 +316,7 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
 // grid (tiles * groups, E) with the group index fastest: the CTAs in flight cover every group of a
 // few (limb, tile) slices, so groups that share a key (or an input's hoisted digits) read each tile
 // from DRAM once and from L2 after that
-template <int BETA, bool EXT = false>
+template <int BETA, bool EXT = false, int KA = 0>
 __global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, int np, int K, int beta_rt,
                            int logN, PinvTab pq) {
     const int gi = blockIdx.x % grp.n;
@@ -325,8 +324,8 @@ __global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, 
     const int m = blockIdx.y;
     if (x >= (1 << logN)) return;
     const int pm = m < k ? m : K + (m - k);
-    if (pr.m[pm].q < (1ull << 41)) ks_inner_body<BETA, EXT, true>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi);
-    else ks_inner_body<BETA, EXT, false>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi);
+    if (pr.m[pm].q < (1ull << 41)) ks_inner_body<BETA, EXT, true, KA>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi);
+    else ks_inner_body<BETA, EXT, false, 0>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi);
 }
 
 // conv[t][b][i][x] = FastBConv_{P -> q_i}(INTT(u_P))   (u P-rows already INTT'd)
@@ -574,15 +573,20 @@ static blb_status ks_inner_launch(const blb_params *P, int level, const KsJobs &
     }
     cudaEvent_t t0 = blb_timing_begin(st);
     const dim3 gks((unsigned)(((N + kTB - 1) / kTB) * G.n), E);
-    switch (beta) {
-        case 1: k_ks_inner<1, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
-        case 2: k_ks_inner<2, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
-        case 3: k_ks_inner<3, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
-        case 4: k_ks_inner<4, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
-        case 5: k_ks_inner<5, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
-        case 6: k_ks_inner<6, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
-        default: k_ks_inner<0, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
+#define BLB_KS_SWITCH(KA_)                                                                                    \
+    switch (beta) {                                                                                          \
+        case 1: k_ks_inner<1, EXT, KA_><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break; \
+        case 2: k_ks_inner<2, EXT, KA_><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break; \
+        case 3: k_ks_inner<3, EXT, KA_><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break; \
+        case 4: k_ks_inner<4, EXT, KA_><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break; \
+        case 5: k_ks_inner<5, EXT, KA_><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break; \
+        case 6: k_ks_inner<6, EXT, KA_><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break; \
+        default: k_ks_inner<0, EXT, KA_><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break; \
     }
+    if (P->ks_acc == 1) { BLB_KS_SWITCH(1) }
+    else if (P->ks_acc == 2) { BLB_KS_SWITCH(2) }
+    else { BLB_KS_SWITCH(0) }
+#undef BLB_KS_SWITCH
     BLB_COUNT_LAUNCH(1);
     // algorithmic bytes: each distinct key once (groups sharing a key read it through L2)
     int n_keys = 0;

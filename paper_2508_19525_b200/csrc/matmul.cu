@@ -166,17 +166,6 @@ struct PtLayout {
 template <int PP, int STG>
 constexpr size_t mac4_smem() { return (size_t)STG * (PP + 2) * 512 * 8 + 2 * STG * 8; }
 
-// accumulator helpers with one call signature (Acc41 / Acc128 ignore the FP64 constants)
-__device__ __forceinline__ void accm(Acc41 &a, u64 x, u64 y, double, double) { a.mac(x, y); }
-__device__ __forceinline__ void accm(Acc128 &a, u64 x, u64 y, double, double) { a.mac(x, y); }
-__device__ __forceinline__ void accm(AccF64 &a, u64 x, u64 y, double qd, double qinv) { a.mac(x, y, qd, qinv); }
-__device__ __forceinline__ u64 accr(const Acc41 &a, const ModConst &mc, double, double) { return a.reduce(mc); }
-__device__ __forceinline__ u64 accr(const Acc128 &a, const ModConst &mc, double, double) { return a.reduce(mc); }
-__device__ __forceinline__ u64 accr(const AccF64 &a, const ModConst &, double qd, double qinv) { return a.reduce(qd, qinv); }
-__device__ __forceinline__ void accf(Acc41 &, const ModConst &, double, double) {}  // exact for < 2^14 products
-__device__ __forceinline__ void accf(Acc128 &a, const ModConst &mc, double, double) { a.fold(mc); }
-__device__ __forceinline__ void accf(AccF64 &a, const ModConst &, double qd, double qinv) { a.fold(qd, qinv); }
-
 // SPLIT41 (q < 2^41): NINT of the four accumulators of an output -- (c0, x), (c0, x+1), (c1, x),
 // (c1, x+1) in that order -- run on the integer pipe (Acc41), the others on the FP64 pipe (AccF64);
 // the split balances the fma-heavy and FP64 pipes.  Otherwise Acc128 throughout.
@@ -184,7 +173,8 @@ template <bool SPLIT41, bool PACKED, int kMacP, int kM4Stages, int NINT>
 __device__ __forceinline__ void mac4_consume(const u64 *ring, uint64_t *full, uint64_t *empty, int n_e, int nP,
                                              u64 *const *outs, long long kN, const ModConst &mc) {
     using I = typename std::conditional<SPLIT41, Acc41, Acc128>::type;
-    using F = typename std::conditional<SPLIT41, AccF64, Acc128>::type;
+    // NINT < 0: every product on the grid-split FP64 accumulator (AccG)
+    using F = typename std::conditional<SPLIT41, typename std::conditional<(NINT < 0), AccG, AccF64>::type, Acc128>::type;
     using T0 = typename std::conditional<(NINT >= 1), I, F>::type;
     using T1 = typename std::conditional<(NINT >= 2), I, F>::type;
     using T2 = typename std::conditional<(NINT >= 3), I, F>::type;
@@ -204,6 +194,31 @@ __device__ __forceinline__ void mac4_consume(const u64 *ring, uint64_t *full, ui
         const u64 *st = ring + (size_t)slot * kM4StageWords;
         const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + kMacP * 512 + 2 * t);
         const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + (kMacP + 1) * 512 + 2 * t);
+        if constexpr (SPLIT41 && NINT < 0) {
+            // every product on AccG: convert each staged residue to a double once (R values are
+            // shared by the kMacP outputs, plaintext values by c0 and c1)
+            const double R0x = AccF64::u2d(r0.x), R0y = AccF64::u2d(r0.y);
+            const double R1x = AccF64::u2d(r1.x), R1y = AccF64::u2d(r1.y);
+#pragma unroll
+            for (int j = 0; j < kMacP; j++) {
+                {  // unconditional (slot j >= nP holds stale data, its sums are never stored): no joins
+                    double Px, Py;
+                    if constexpr (PACKED) {  // high byte spliced under the 2^52 exponent with one PRMT
+                        const uint2 lo = *reinterpret_cast<const uint2 *>(reinterpret_cast<const uint32_t *>(st + j * 512) + 2 * t);
+                        const unsigned hi = *(reinterpret_cast<const unsigned short *>(
+                                                  reinterpret_cast<const unsigned char *>(st + j * 512) + 2048) + t);
+                        Px = __dsub_rn(__hiloint2double((int)__byte_perm(hi, 0x43300000u, 0x7650), (int)lo.x), 4503599627370496.0);
+                        Py = __dsub_rn(__hiloint2double((int)__byte_perm(hi, 0x43300000u, 0x7651), (int)lo.y), 4503599627370496.0);
+                    } else {
+                        const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(st + j * 512 + 2 * t);
+                        Px = AccF64::u2d(pv.x);
+                        Py = AccF64::u2d(pv.y);
+                    }
+                    a00[j].macd(Px, R0x); a01[j].macd(Py, R0y);
+                    a10[j].macd(Px, R1x); a11[j].macd(Py, R1y);
+                }
+            }
+        } else
 #pragma unroll
         for (int j = 0; j < kMacP; j++) {
             if (j < nP) {
@@ -352,11 +367,13 @@ constexpr int kMjStages = 3;
 template <int JG>
 constexpr size_t macj_smem() { return (size_t)kMjStages * (1 + 2 * JG) * 512 * 8 + 2 * kMjStages * 8; }
 
-template <bool SPLIT41, int JG>
+// SPLIT41 accumulators: AM = 0: (c0) Acc41 on the integer pipe + (c1) AccF64; AM = 1: Acc41 + AccG;
+// AM = 2: AccG for all four (env BLB_MACJ_ACC)
+template <bool SPLIT41, int JG, int AM>
 __device__ __forceinline__ void macj_consume(const u64 *ring, uint64_t *full, uint64_t *empty, int n_e, u64 *const *outs,
                                              long long kN, const ModConst &mc) {
-    using A = typename std::conditional<SPLIT41, Acc41, Acc128>::type;
-    using A1 = typename std::conditional<SPLIT41, AccF64, Acc128>::type;
+    using A = typename std::conditional<SPLIT41, typename std::conditional<(AM == 2), AccG, Acc41>::type, Acc128>::type;
+    using A1 = typename std::conditional<SPLIT41, typename std::conditional<(AM >= 1), AccG, AccF64>::type, Acc128>::type;
     const double qd = (double)mc.q, qinv = 1.0 / qd;
     A a00[JG], a01[JG];
     A1 a10[JG], a11[JG];
@@ -373,40 +390,30 @@ __device__ __forceinline__ void macj_consume(const u64 *ring, uint64_t *full, ui
         for (int j = 0; j < JG; j++) {
             const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + (1 + 2 * j) * 512 + 2 * t);
             const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + (2 + 2 * j) * 512 + 2 * t);
-            a00[j].mac(pv.x, r0.x); a01[j].mac(pv.y, r0.y);
-            if constexpr (SPLIT41) {
-                a10[j].mac(pv.x, r1.x, qd, qinv); a11[j].mac(pv.y, r1.y, qd, qinv);
-            } else {
-                a10[j].mac(pv.x, r1.x); a11[j].mac(pv.y, r1.y);
-            }
+            accm(a00[j], pv.x, r0.x, qd, qinv); accm(a01[j], pv.y, r0.y, qd, qinv);
+            accm(a10[j], pv.x, r1.x, qd, qinv); accm(a11[j], pv.y, r1.y, qd, qinv);
         }
         __syncwarp();
         if ((t & 31) == 0) mbar_arrive(&empty[slot]);
-        if constexpr (!SPLIT41) {
-            if ((s & 63) == 63) {  // 64 products < 2^126
+        // Acc128: 64 products < 2^126; FP64 accumulators: 512 products (Acc41: exact for < 2^14)
+        if ((!SPLIT41 && (s & 63) == 63) || (SPLIT41 && (s & 511) == 511)) {
 #pragma unroll
-                for (int j = 0; j < JG; j++) { a00[j].fold(mc); a01[j].fold(mc); a10[j].fold(mc); a11[j].fold(mc); }
-            }
-        } else {
-            if ((s & 511) == 511) {  // 512 products: FP64 sums below 2^51
-#pragma unroll
-                for (int j = 0; j < JG; j++) { a10[j].fold(qd, qinv); a11[j].fold(qd, qinv); }
+            for (int j = 0; j < JG; j++) {
+                accf(a00[j], mc, qd, qinv); accf(a01[j], mc, qd, qinv);
+                accf(a10[j], mc, qd, qinv); accf(a11[j], mc, qd, qinv);
             }
         }
     }
 #pragma unroll
     for (int j = 0; j < JG; j++) {
         u64 *out = outs[j] + 2 * t;
-        *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00[j].reduce(mc), a01[j].reduce(mc));
-        if constexpr (SPLIT41)
-            *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10[j].reduce(qd, qinv), a11[j].reduce(qd, qinv));
-        else
-            *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10[j].reduce(mc), a11[j].reduce(mc));
+        *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(accr(a00[j], mc, qd, qinv), accr(a01[j], mc, qd, qinv));
+        *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(accr(a10[j], mc, qd, qinv), accr(a11[j], mc, qd, qinv));
     }
 }
 
 // grid: (group fastest, tile, limb); group gi covers outputs o0 + gi*JG .. + JG - 1 (local o)
-template <int JG, int MINB>
+template <int JG, int MINB, int AM = 0>
 __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_j(const u64 *__restrict__ pt, const u64 *__restrict__ R,
                                                      u64 *__restrict__ acc, const int *__restrict__ ent_r,
                                                      const int *__restrict__ ent_pt, const int *__restrict__ ent_start,
@@ -460,8 +467,8 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_j(const u64 *__restrict_
 #pragma unroll
     for (int j = 0; j < JG; j++) outs[j] = acc + (long long)(oa + j) * 2 * kN + lx0;
     const ModConst &mc = pr.m[l < kq ? l : Kfull + (l - kq)];
-    if (mc.q < (1ull << 41)) macj_consume<true, JG>(ring, full, empty, n_e, outs, kN, mc);
-    else macj_consume<false, JG>(ring, full, empty, n_e, outs, kN, mc);
+    if (mc.q < (1ull << 41)) macj_consume<true, JG, AM>(ring, full, empty, n_e, outs, kN, mc);
+    else macj_consume<false, JG, AM>(ring, full, empty, n_e, outs, kN, mc);
 }
 
 // dst[o] += src[j] for the jobs of one giant batch (sequential per thread: no races)
@@ -508,14 +515,21 @@ blb_status launch_mac(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc
             k_mac_j<4, 2><<<grid, kTB + 32, smem, st>>>(pt, R, acc, ent_r, ent_pt, ent_start, o0, n_grp, k,
                                                         kq < 0 ? k : kq, P->K, P->logN, P->pr);
         } else {
-            static bool attr = false;
             constexpr size_t smem = macj_smem<2>();
+            static bool attr = false;
             if (!attr) {
-                cudaFuncSetAttribute(k_mac_j<2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                cudaFuncSetAttribute(k_mac_j<2, 3, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                cudaFuncSetAttribute(k_mac_j<2, 3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                cudaFuncSetAttribute(k_mac_j<2, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 attr = true;
             }
-            k_mac_j<2, 3><<<grid, kTB + 32, smem, st>>>(pt, R, acc, ent_r, ent_pt, ent_start, o0, n_grp, k,
-                                                        kq < 0 ? k : kq, P->K, P->logN, P->pr);
+            auto go = [&](auto kern) {
+                kern<<<grid, kTB + 32, smem, st>>>(pt, R, acc, ent_r, ent_pt, ent_start, o0, n_grp, k, kq < 0 ? k : kq,
+                                                   P->K, P->logN, P->pr);
+            };
+            if (P->macj_acc == 2) go(k_mac_j<2, 3, 2>);
+            else if (P->macj_acc == 1) go(k_mac_j<2, 3, 1>);
+            else go(k_mac_j<2, 3, 0>);
         }
         BLB_COUNT_LAUNCH(1);
         BLB_COUNT(3, n_entries);
@@ -944,7 +958,10 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
                 for (int j = 0; j < n_o && grouped; j++)
                     if (j % PP != PP - 1 && j + 1 < n_o && !pl->same_next[o0 + j]) grouped = false;
                 // BLB_MAC_NINT: accumulators per output on the integer pipe (0..2; the rest on FP64)
-                if (grouped && PP == 2 && P->mac_nint == 0)
+                if (grouped && PP == 2 && P->mac_nint < 0)
+                    launch_mac4<2, 4, 3, -1>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
+                                             P->pr, n_tiles, lay, st);
+                else if (grouped && PP == 2 && P->mac_nint == 0)
                     launch_mac4<2, 4, 3, 0>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
                                             P->pr, n_tiles, lay, st);
                 else if (grouped && PP == 2 && P->mac_nint == 1)

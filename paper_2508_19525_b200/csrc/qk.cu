@@ -133,9 +133,48 @@ __global__ void k_tensor_sum(const u64 *Qp, const u64 *Kp, u64 *D, Primes pr, in
 // Grid: (block (u0/2, i0/2) fastest, limb, x-tile).
 // SMALL (q < 2^41): d0 and d2 on the integer pipe (Acc41), the two d1 products on the FP64 pipe
 // (AccF64, exact for < 2^10 products): the two pipes share the work.  Otherwise Acc128 throughout.
-template <bool SMALL>
+// TA = 1 (SMALL only; env BLB_TSUM_ACC, default): every product on the grid-split FP64 accumulator
+// (AccG, 4 FP64 ops per product, each loaded word converted to a double once)
+template <bool SMALL, int TA>
 __device__ __forceinline__ void tsum22_body(const u64 *Qp, const u64 *Kp, u64 *D, int J, int B, long long kN,
                                             long long lx, int u0, int i0, const ModConst &mc) {
+    if constexpr (SMALL && TA == 1) {
+        const double qd = (double)mc.q, qinv = 1.0 / qd;
+        AccG d0[2][2], d1[2][2], d2[2][2];  // 2 J <= 512 products per accumulator
+#pragma unroll
+        for (int a = 0; a < 2; a++)
+#pragma unroll
+            for (int b = 0; b < 2; b++) { d0[a][b].zero(); d1[a][b].zero(); d2[a][b].zero(); }
+        for (int j = 0; j < J; j++) {
+            double q0[2], q1[2], k0[2], k1[2];
+#pragma unroll
+            for (int a = 0; a < 2; a++) {
+                const u64 *qa = Qp + (long long)((u0 + a) * J + j) * 2 * kN + lx;
+                const u64 *kb = Kp + (long long)((i0 + a) * J + j) * 2 * kN + lx;
+                q0[a] = AccF64::u2d(qa[0]); q1[a] = AccF64::u2d(qa[kN]);
+                k0[a] = AccF64::u2d(kb[0]); k1[a] = AccF64::u2d(kb[kN]);
+            }
+#pragma unroll
+            for (int a = 0; a < 2; a++)
+#pragma unroll
+                for (int b = 0; b < 2; b++) {
+                    d0[a][b].macd(q0[a], k0[b]);
+                    d2[a][b].macd(q1[a], k1[b]);
+                    d1[a][b].macd(q0[a], k1[b]);
+                    d1[a][b].macd(q1[a], k0[b]);
+                }
+        }
+#pragma unroll
+        for (int a = 0; a < 2; a++)
+#pragma unroll
+            for (int b = 0; b < 2; b++) {
+                u64 *out = D + (long long)((u0 + a) * B + i0 + b) * 3 * kN + lx;
+                out[0] = d0[a][b].reduce(qd, qinv);
+                out[kN] = d1[a][b].reduce(qd, qinv);
+                out[2 * kN] = d2[a][b].reduce(qd, qinv);
+            }
+        return;
+    }
     using A = typename std::conditional<SMALL, Acc41, Acc128>::type;
     using A1 = typename std::conditional<SMALL, AccF64, Acc128>::type;
     const double qd = (double)mc.q, qinv = 1.0 / qd;
@@ -179,6 +218,7 @@ __device__ __forceinline__ void tsum22_body(const u64 *Qp, const u64 *Kp, u64 *D
             out[2 * kN] = d2[a][b].reduce(mc);
         }
 }
+template <int TA>
 __global__ void __launch_bounds__(kTB, 2) k_tensor_sum22(const u64 *Qp, const u64 *Kp, u64 *D, Primes pr, int J, int G,
                                                       int B, int k, int N) {
     const int nb = (G / 2) * (B / 2);
@@ -192,8 +232,8 @@ __global__ void __launch_bounds__(kTB, 2) k_tensor_sum22(const u64 *Qp, const u6
     const long long kN = (long long)k * N, lx = (long long)l * N + x;
     const ModConst &mc = pr.m[l];
     // Acc41 holds < 2^14 products of 41-bit residues: 2 J per accumulator here
-    if (mc.q < (1ull << 41)) tsum22_body<true>(Qp, Kp, D, J, B, kN, lx, u0, i0, mc);
-    else tsum22_body<false>(Qp, Kp, D, J, B, kN, lx, u0, i0, mc);
+    if (mc.q < (1ull << 41)) tsum22_body<true, TA>(Qp, Kp, D, J, B, kN, lx, u0, i0, mc);
+    else tsum22_body<false, 0>(Qp, Kp, D, J, B, kN, lx, u0, i0, mc);
 }
 
 // dst[p][i][x] = src[p][i][x] for i < k_dst (src has k_src limbs per poly): exact level drop / copy
@@ -609,9 +649,11 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
     // 3. products summed over j, relinearisation (one per (u, i)), rescale
     cudaEvent_t tt0 = blb_timing_begin(st);
     // Acc128 without folds: <= 64 products of 61-bit residues; AccF64: < 2^10 products
-    if (G % 2 == 0 && B % 2 == 0 && 2 * J <= 64 && P->tsum22)
-        k_tensor_sum22<<<(unsigned)((size_t)((N + kTB - 1) / kTB) * k1 * (G / 2) * (B / 2)), kTB, 0, st>>>(
-            W + w.qp, W + w.kp, W + w.d, P->pr, J, G, B, k1, N);
+    if (G % 2 == 0 && B % 2 == 0 && 2 * J <= 64 && P->tsum22) {
+        const unsigned g22 = (unsigned)((size_t)((N + kTB - 1) / kTB) * k1 * (G / 2) * (B / 2));
+        if (P->tsum_acc == 1) k_tensor_sum22<1><<<g22, kTB, 0, st>>>(W + w.qp, W + w.kp, W + w.d, P->pr, J, G, B, k1, N);
+        else k_tensor_sum22<0><<<g22, kTB, 0, st>>>(W + w.qp, W + w.kp, W + w.d, P->pr, J, G, B, k1, N);
+    }
     else
         k_tensor_sum<<<(unsigned)((size_t)((N + kTB - 1) / kTB) * k1 * G * B), kTB, 0, st>>>(
             W + w.qp, W + w.kp, W + w.d, P->pr, J, B, k1, N, G * B);
