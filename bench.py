@@ -35,6 +35,10 @@ import blb_inputs as bi  # noqa: E402
 METRIC = "ms per BERT-base layer fused-linear CKKS eval"
 # BSGS baby-step counts B per ct-pt MatMul (C11, plan parameter S15); shared by both arms
 BSGS = {"qkv": 64, "oproj": 16, "ffn1": 64, "ffn2": 16}
+# tuning override, e.g. BLB_BSGS=qkv:32,ffn1:128 (each plan is parity-tested at any B by the toy tests)
+for _kv in filter(None, os.environ.get("BLB_BSGS", "").split(",")):
+    _k, _v = _kv.split(":")
+    BSGS[_k] = int(_v)
 UNIT = "ms"
 FALLBACK_HBM = 6650.0
 

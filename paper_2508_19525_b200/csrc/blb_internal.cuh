@@ -133,6 +133,34 @@ struct Acc41 {
     __device__ __forceinline__ void fold(const ModConst &) {}  // exact for < 2^14 products
 };
 
+// Accumulator for up to 7 products of residues < 2^60 (the 60-bit chain / special primes) with
+// 32-bit partial products: a = a1 2^32 + a0 (a1 < 2^28).  lo (96 bits) += a0 b0; mid (64 bits) +=
+// a1 b0 + a0 b1 (< 2^60 each, 14 terms < 2^64); hi (64 bits) += a1 b1: 6 IMAD-class instructions per
+// product instead of the ~11 of Acc128's 64x64->128 multiply + 128-bit add.
+struct Acc60 {
+    uint32_t l0, l1, l2;
+    u64 mid, hi;
+    __device__ __forceinline__ void zero() { l0 = l1 = l2 = 0; mid = 0; hi = 0; }
+    __device__ __forceinline__ void mac(u64 a, u64 b) {
+        const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32), b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
+        asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
+            "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+            "addc.u32 %2, %2, 0;"
+            : "+r"(l0), "+r"(l1), "+r"(l2)
+            : "r"(a0), "r"(b0));
+        mid += (u64)a1 * b0 + (u64)a0 * b1;
+        hi += (u64)a1 * b1;
+    }
+    __device__ __forceinline__ u64 reduce(const ModConst &c) const {
+        // total = (l2:l1:l0) + mid 2^32 + hi 2^64
+        const u64 lo = ((u64)l1 << 32) | l0;
+        const u64 m_lo = mid << 32, m_hi = mid >> 32;
+        const u64 s = lo + m_lo;
+        const u64 H = (u64)l2 + hi + m_hi + (s < lo ? 1 : 0);
+        return reduce128(H, s, c);
+    }
+};
+
 // Exact FP64-pipe accumulator for products of residues < 2^41 (offloads the fma-heavy pipe that
 // the integer accumulators saturate; the B200 FP64 pipe runs 64 DFMA/clk/SM beside it):
 // a b = p + e with p = fl(a b) and e = fma(a, b, -p) exact; c = round(p / q) by one fma against
@@ -206,6 +234,8 @@ struct AccG {
 // accumulator helpers with one call signature (Acc41 / Acc128 ignore the FP64 constants)
 __device__ __forceinline__ void accm(Acc41 &a, u64 x, u64 y, double, double) { a.mac(x, y); }
 __device__ __forceinline__ void accm(Acc128 &a, u64 x, u64 y, double, double) { a.mac(x, y); }
+__device__ __forceinline__ void accm(Acc60 &a, u64 x, u64 y, double, double) { a.mac(x, y); }
+__device__ __forceinline__ u64 accr(const Acc60 &a, const ModConst &mc, double, double) { return a.reduce(mc); }
 __device__ __forceinline__ void accm(AccF64 &a, u64 x, u64 y, double qd, double qinv) { a.mac(x, y, qd, qinv); }
 __device__ __forceinline__ u64 accr(const Acc41 &a, const ModConst &mc, double, double) { return a.reduce(mc); }
 __device__ __forceinline__ u64 accr(const Acc128 &a, const ModConst &mc, double, double) { return a.reduce(mc); }
@@ -275,6 +305,7 @@ struct blb_params {
     int mac_chunk = 3;            // outputs per MAC / giant-step chunk of the two-stream schedule (env BLB_CHUNK)
     int mac_tma = 1;              // warp-specialised bulk-copy MAC (env BLB_MAC_TMA=0: register double buffer)
     int pt_pack = 1;              // 5-byte packed plaintext limbs for primes < 2^40 (env BLB_PT_PACK=0: 8 bytes)
+    int ntt_2s = 1;               // two-stream NTT: integer-kernel rows on the auxiliary stream (env BLB_NTT_2S)
     int tsum_acc = 1;             // tensor J-sum accumulators: 1 AccG, 0 Acc41 + AccF64 (env BLB_TSUM_ACC)
     int ks_acc = 1;               // key-switch inner product accumulators (40-bit limbs), see k_ks_inner (env BLB_KS_ACC)
     int macj_acc = 2;             // mask MAC accumulators: 0 Acc41 + AccF64, 1 Acc41 + AccG, 2 AccG (env BLB_MACJ_ACC)

@@ -215,8 +215,8 @@ struct KsGroups {
 // jobs.j[t].out ([2][E][N]) -- the double-hoisted rotation (no ModDown).
 // SMALL (prime < 2^41): the a-part products run on the FP64 pipe (AccF64), the b-part on the
 // integer pipe, so the two pipes share the 2 beta products per job.
-// KA (SMALL only, env BLB_KS_ACC): 0 = b-part Acc128 + a-part AccF64, 1 = both AccG (FP64 pipe,
-// no per-product reduction), 2 = b-part Acc41 + a-part AccG
+// KA (env BLB_KS_ACC): 40-bit rows 0 = b-part Acc128 + a-part AccF64, 1 = both AccG (FP64 pipe, no
+// per-product reduction), 2 = b-part Acc41 + a-part AccG; 3 = as 1 with the 60-bit rows on Acc60
 template <int BETA, bool EXT, bool SMALL, int KA>
 __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups &grp, u64 *u, const Primes &pr, int k,
                                               int np, int K, int beta_rt, int logN, const PinvTab &pq, int x, int m,
@@ -231,9 +231,12 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
     // contiguous and only the two outputs are scattered, to x = perm_{g^-1}(y)
     const uint32_t dst = J0.galois == 1 ? (uint32_t)x : galois_perm(x, J0.galois_inv, logN);
     const ModConst &mc = pr.m[pm];
-    using A1 = typename std::conditional<SMALL, typename std::conditional<(KA >= 1), AccG, AccF64>::type, Acc128>::type;
-    using A0 = typename std::conditional<SMALL && KA == 1, AccG,
-                                         typename std::conditional<SMALL && KA == 2, Acc41, Acc128>::type>::type;
+    // KA = 3: as 1, and the 60-bit rows on Acc60 (32-bit partial products, <= 7 products; beta a
+    // compile-time <= 7), else Acc128
+    using W = typename std::conditional<(KA == 3 && BETA > 0 && BETA <= 7), Acc60, Acc128>::type;
+    using A1 = typename std::conditional<SMALL, typename std::conditional<(KA >= 1), AccG, AccF64>::type, W>::type;
+    using A0 = typename std::conditional<SMALL && (KA == 1 || KA == 3), AccG,
+                                         typename std::conditional<SMALL && KA == 2, Acc41, W>::type>::type;
     const double qd = (double)mc.q, qinv = 1.0 / qd;
     A0 a0[kKsGroup];
     A1 a1[kKsGroup];
@@ -325,7 +328,7 @@ __global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, 
     if (x >= (1 << logN)) return;
     const int pm = m < k ? m : K + (m - k);
     if (pr.m[pm].q < (1ull << 41)) ks_inner_body<BETA, EXT, true, KA>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi);
-    else ks_inner_body<BETA, EXT, false, 0>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi);
+    else ks_inner_body<BETA, EXT, false, KA>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi);
 }
 
 // conv[t][b][i][x] = FastBConv_{P -> q_i}(INTT(u_P))   (u P-rows already INTT'd)
@@ -584,6 +587,7 @@ static blb_status ks_inner_launch(const blb_params *P, int level, const KsJobs &
         default: k_ks_inner<0, EXT, KA_><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break; \
     }
     if (P->ks_acc == 1) { BLB_KS_SWITCH(1) }
+    else if (P->ks_acc == 3) { BLB_KS_SWITCH(3) }
     else if (P->ks_acc == 2) { BLB_KS_SWITCH(2) }
     else { BLB_KS_SWITCH(0) }
 #undef BLB_KS_SWITCH

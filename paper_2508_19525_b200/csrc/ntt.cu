@@ -432,9 +432,36 @@ static inline bool rb_small(const blb_params *P, const RowBatch &r) {
 }
 static inline int rb_rows(const RowBatch &r) { return r.n_polys * (r.nsel ? r.nsel : r.limbs); }
 
+// Two-stream NTT (env BLB_NTT_2S=1): the integer-kernel rows of a mixed batch run on the auxiliary
+// stream while the FP64-kernel rows run on the caller's stream -- the two kernels load different
+// pipes (fma-heavy vs FP64), so CTAs of both can share an SM.  fork() before the launches, join()
+// after; the stream of part h is part_stream(h).
+struct NttStreams {
+    const blb_params *P;
+    cudaStream_t st;
+    bool two;
+    NttStreams(const blb_params *P_, cudaStream_t st_, int np2) : P(P_), st(st_), two(np2 == 2 && P_->ntt_2s && P_->aux) {
+        if (two) {
+            cudaEvent_t e = P->ev[P->ev_next];
+            P->ev_next = (P->ev_next + 1) % 64;
+            cudaEventRecord(e, st);
+            cudaStreamWaitEvent(P->aux, e, 0);
+        }
+    }
+    cudaStream_t part_stream(int h) const { return two && h == 1 ? P->aux : st; }
+    void join() const {
+        if (!two) return;
+        cudaEvent_t e = P->ev[P->ev_next];
+        P->ev_next = (P->ev_next + 1) % 64;
+        cudaEventRecord(e, P->aux);
+        cudaStreamWaitEvent(st, e, 0);
+    }
+};
+
 }  // namespace
 
 blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cudaStream_t st) {
+    const cudaStream_t st0 = st;
     const int rows = rb.n_polys * rb.limbs;
     if (rows == 0) return BLB_OK;
     const int logN = P->logN;
@@ -466,8 +493,10 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
         const NttFuse fz{};
         RowBatch parts[2];
         const int np2 = split_rows(P, rb, parts);
+        const NttStreams ss(P, st0, np2);
         for (int h = 0; h < np2; h++) {
             const RowBatch &r = parts[h];
+            const cudaStream_t st = ss.part_stream(h);
             dim3 g(16, rb_rows(r));
             if (rb_small(P, r)) {
                 if (!inverse) {
@@ -487,8 +516,9 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
                 }
             }
         }
+        ss.join();
         BLB_COUNT_LAUNCH(2 * np2);
-        blb_timing_end(1, t0, st, alg);
+        blb_timing_end(1, t0, st0, alg);
         BLB_CHECK_LAUNCH();
         return BLB_OK;
     }
@@ -516,7 +546,8 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
 
 // Forward N = 2^16 NTT with a fused prologue (pro = 1) and / or ModDown epilogue (epi = 1).
 blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool inverse, const NttFuse &fz,
-                            cudaStream_t st) {
+                            cudaStream_t st0) {
+    const cudaStream_t st = st0;
     const int rows = rb.n_polys * rb.limbs;
     if (rows == 0) return BLB_OK;
     if (P->logN != 16 || rows > 65535 || (inverse && (fz.pro != 2 || fz.epi)) || (!inverse && fz.pro == 2)) {
@@ -527,8 +558,10 @@ blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool invers
     cudaEvent_t t0 = blb_timing_begin(st);
     RowBatch parts[2];
     const int np2 = split_rows(P, rb, parts);
+    const NttStreams ss(P, st0, np2);
     for (int h = 0; h < np2; h++) {
         const RowBatch &r = parts[h];
+        const cudaStream_t st = ss.part_stream(h);
         dim3 g(16, rb_rows(r));
         if (inverse) {  // pro = 2: first (contiguous) pass loads from the pointer table
             if (rb_small(P, r)) {
@@ -552,8 +585,9 @@ blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool invers
             else ntt16_int<false, false, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
         }
     }
+    ss.join();
     BLB_COUNT_LAUNCH(2 * np2);
-    blb_timing_end(1, t0, st, (double)rows * 16.0 * (1 << 16));
+    blb_timing_end(1, t0, st0, (double)rows * 16.0 * (1 << 16));
     BLB_CHECK_LAUNCH();
     return BLB_OK;
 }
