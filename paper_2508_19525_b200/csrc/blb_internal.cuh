@@ -307,7 +307,7 @@ struct blb_params {
     int pt_pack = 1;              // 5-byte packed plaintext limbs for primes < 2^40 (env BLB_PT_PACK=0: 8 bytes)
     int ntt_2s = 1;               // two-stream NTT: integer-kernel rows on the auxiliary stream (env BLB_NTT_2S)
     int tsum_acc = 1;             // tensor J-sum accumulators: 1 AccG, 0 Acc41 + AccF64 (env BLB_TSUM_ACC)
-    int ks_acc = 1;               // key-switch inner product accumulators (40-bit limbs), see k_ks_inner (env BLB_KS_ACC)
+    int ks_acc = 4;               // key-switch inner product accumulators (40-bit limbs), see k_ks_inner (env BLB_KS_ACC)
     int macj_acc = 2;             // mask MAC accumulators: 0 Acc41 + AccF64, 1 Acc41 + AccG, 2 AccG (env BLB_MACJ_ACC)
     int mac_nint = -1;            // weight MAC: accumulators per output on the integer pipe, 0..2 (env BLB_MAC_NINT)
     int tsum22 = 1;               // 2 x 2 register-blocked ct-ct tensor J-sum (env BLB_TSUM22=0: one output per thread)

@@ -216,7 +216,8 @@ struct KsGroups {
 // SMALL (prime < 2^41): the a-part products run on the FP64 pipe (AccF64), the b-part on the
 // integer pipe, so the two pipes share the 2 beta products per job.
 // KA (env BLB_KS_ACC): 40-bit rows 0 = b-part Acc128 + a-part AccF64, 1 = both AccG (FP64 pipe, no
-// per-product reduction), 2 = b-part Acc41 + a-part AccG; 3 = as 1 with the 60-bit rows on Acc60
+// per-product reduction), 2 = b-part Acc41 + a-part AccG; 3 = as 1 with the 60-bit rows on Acc60;
+// 4 = as 1 with the 60-bit rows one job at a time on Acc60 (ks_inner_body60)
 template <int BETA, bool EXT, bool SMALL, int KA>
 __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups &grp, u64 *u, const Primes &pr, int k,
                                               int np, int K, int beta_rt, int logN, const PinvTab &pq, int x, int m,
@@ -235,7 +236,7 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
     // compile-time <= 7), else Acc128
     using W = typename std::conditional<(KA == 3 && BETA > 0 && BETA <= 7), Acc60, Acc128>::type;
     using A1 = typename std::conditional<SMALL, typename std::conditional<(KA >= 1), AccG, AccF64>::type, W>::type;
-    using A0 = typename std::conditional<SMALL && (KA == 1 || KA == 3), AccG,
+    using A0 = typename std::conditional<SMALL && (KA == 1 || KA >= 3), AccG,
                                          typename std::conditional<SMALL && KA == 2, Acc41, W>::type>::type;
     const double qd = (double)mc.q, qinv = 1.0 / qd;
     A0 a0[kKsGroup];
@@ -316,6 +317,60 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
     }
 }
 
+// 60-bit rows with KA = 4: the group's jobs one at a time on Acc60 (6 IMAD-class instructions per
+// product instead of Acc128's ~11), so only one job's accumulators are live (Acc60 for all four jobs
+// at once needed 122 registers, KA = 3).  Same additive terms and stores as ks_inner_body.
+template <int BETA, bool EXT>
+__device__ __forceinline__ void ks_inner_body60(const KsJobs &jobs, const KsGroups &grp, u64 *u, const Primes &pr, int k,
+                                                int np, int K, int logN, const PinvTab &pq, int x, int m, int gi) {
+    const int N = 1 << logN;
+    const int t0 = grp.start[gi], cnt = grp.start[gi + 1] - t0;
+    const int E = k + np, Lk = K + np;
+    const int pm = m < k ? m : K + (m - k);
+    const KsJob &J0 = jobs.j[t0];
+    const uint32_t dst = J0.galois == 1 ? (uint32_t)x : galois_perm(x, J0.galois_inv, logN);
+    const ModConst &mc = pr.m[pm];
+    u64 kb[BETA], ka[BETA];
+#pragma unroll
+    for (int j = 0; j < BETA; j++) {
+        kb[j] = J0.key[(((long long)j * 2 + 0) * Lk + pm) * N + x];
+        ka[j] = J0.key[(((long long)j * 2 + 1) * Lk + pm) * N + x];
+    }
+#pragma unroll 1
+    for (int q = 0; q < cnt; q++) {
+        const int t = t0 + q;
+        const KsJob &J = jobs.j[t];
+        u64 e[BETA];
+        const u64 *ext = J.ext + (long long)m * N + x;
+#pragma unroll
+        for (int j = 0; j < BETA; j++) e[j] = ext[(long long)j * E * N];
+        u64 c0v = 0, c1v = 0;
+        if (m < k) {
+            if (EXT || J.add_mode != 0) c0v = J.c0[(long long)m * N + x];
+            if (J.c1_add && (EXT || J.add_mode == 2)) c1v = J.c1_add[(long long)m * N + x];
+        }
+        Acc60 a0, a1;
+        a0.zero(); a1.zero();
+#pragma unroll
+        for (int j = 0; j < BETA; j++) {
+            a0.mac(e[j], kb[j]);
+            a1.mac(e[j], ka[j]);
+        }
+        u64 r0 = a0.reduce(mc), r1 = a1.reduce(mc);
+        if (m < k) {
+            r0 = addmod(r0, shoup(c0v, pq.v[m], pq.sh[m], mc.q), mc.q);
+            r1 = addmod(r1, shoup(c1v, pq.v[m], pq.sh[m], mc.q), mc.q);
+        }
+        if (EXT) {
+            J.out[(long long)m * N + dst] = r0;
+            J.out[((long long)E + m) * N + dst] = r1;
+        } else {
+            u[(((long long)t * 2 + 0) * E + m) * N + dst] = r0;
+            u[(((long long)t * 2 + 1) * E + m) * N + dst] = r1;
+        }
+    }
+}
+
 // grid (tiles * groups, E) with the group index fastest: the CTAs in flight cover every group of a
 // few (limb, tile) slices, so groups that share a key (or an input's hoisted digits) read each tile
 // from DRAM once and from L2 after that
@@ -328,6 +383,7 @@ __global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, 
     if (x >= (1 << logN)) return;
     const int pm = m < k ? m : K + (m - k);
     if (pr.m[pm].q < (1ull << 41)) ks_inner_body<BETA, EXT, true, KA>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi);
+    else if constexpr (KA == 4 && BETA > 0 && BETA <= 7) ks_inner_body60<BETA, EXT>(jobs, grp, u, pr, k, np, K, logN, pq, x, m, gi);
     else ks_inner_body<BETA, EXT, false, KA>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi);
 }
 
@@ -588,6 +644,7 @@ static blb_status ks_inner_launch(const blb_params *P, int level, const KsJobs &
     }
     if (P->ks_acc == 1) { BLB_KS_SWITCH(1) }
     else if (P->ks_acc == 3) { BLB_KS_SWITCH(3) }
+    else if (P->ks_acc == 4) { BLB_KS_SWITCH(4) }
     else if (P->ks_acc == 2) { BLB_KS_SWITCH(2) }
     else { BLB_KS_SWITCH(0) }
 #undef BLB_KS_SWITCH

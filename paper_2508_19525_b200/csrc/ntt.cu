@@ -183,7 +183,7 @@ __device__ __forceinline__ void bfly_f64(double &X, double &Y, double w, double 
 }
 
 #ifndef BLB_NTT_MINB
-#define BLB_NTT_MINB 2
+#define BLB_NTT_MINB 3
 #endif
 template <bool INV, bool STRIDED, int PRO, int EPI, bool SMALL>
 __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u64 *__restrict__ tw_all,

@@ -214,15 +214,17 @@ class LayerPipeline:
     """Host-to-host serving loop over one FusedLinearLayer (the e2e path of bench.py).
 
     Every step copies that step's encrypted inputs from pinned host memory to the device and reads
-    the masked outputs + server shares back into pinned host memory.  The copies run on their own
-    stream and are double-buffered: the upload of step k+1 and the download of step k-1 overlap the
-    evaluation of step k on the compute stream (the copy engines are idle otherwise); the only
-    exposed transfers are the first upload and the last download.
+    the masked outputs + server shares back into pinned host memory.  Uploads and downloads run on
+    two streams of their own (one per copy direction: on a single copy stream the upload of step k+1
+    queued behind the download of step k, which waits for step k's evaluation, so every upload was
+    exposed) and the inputs are double-buffered: the upload of step k+1 and the download of step k-1
+    overlap the evaluation of step k on the compute stream; the only exposed transfers are the first
+    upload and the last download.
     """
 
     def __init__(self, layer: FusedLinearLayer, keys: blb.Keys, mask_key: bytes, like_inputs: dict):
         self.layer, self.keys, self.mask_key = layer, keys, mask_key
-        self.copy = torch.cuda.Stream()
+        self.up, self.down = torch.cuda.Stream(), torch.cuda.Stream()
         # two device input sets (ping-pong), each a dict like the inputs of FusedLinearLayer.step
         self.dev = [{k: [blb.Ciphertext(torch.empty_like(c.data), c.level, c.scale) for c in v]
                      for k, v in like_inputs.items()} for _ in range(2)]
@@ -235,13 +237,13 @@ class LayerPipeline:
         """Enqueue one step; returns the pinned host buffers its results land in (valid after sync)."""
         s = self.k % 2
         comp = torch.cuda.current_stream()
-        with torch.cuda.stream(self.copy):
+        with torch.cuda.stream(self.up):
             if self.k >= 2:
-                self.copy.wait_event(self.free[s])
+                self.up.wait_event(self.free[s])
             for name, hs in host_inputs.items():
                 for h, c in zip(hs, self.dev[s][name]):
                     c.data.copy_(h, non_blocking=True)
-            self.ready[s].record(self.copy)
+            self.ready[s].record(self.up)
         comp.wait_event(self.ready[s])
         res = self.layer.step(self.keys, self.dev[s], self.mask_key)
         if gather is not None:
@@ -254,14 +256,16 @@ class LayerPipeline:
             self.host_out[s] = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in tensors]
         done = torch.cuda.Event()
         done.record(comp)
-        with torch.cuda.stream(self.copy):
-            self.copy.wait_event(done)
+        with torch.cuda.stream(self.down):
+            self.down.wait_event(done)
             for h, t in zip(self.host_out[s], tensors):
-                t.record_stream(self.copy)
+                t.record_stream(self.down)
                 h.copy_(t, non_blocking=True)
         self.k += 1
         return self.host_out[s]
 
     def drain(self, stream=None):
         """Make the caller's stream wait for every outstanding copy."""
-        (stream or torch.cuda.current_stream()).wait_stream(self.copy)
+        st = stream or torch.cuda.current_stream()
+        st.wait_stream(self.up)
+        st.wait_stream(self.down)
