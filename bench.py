@@ -346,7 +346,8 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        pipe.copy.wait_stream(stream)
+        pipe.up.wait_stream(stream)
+        pipe.down.wait_stream(stream)
         d2h = 0
         for _ in range(args.steps):
             outs_host = pipe.submit(host_in, gather)
@@ -361,7 +362,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
         e2e = {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "pipeline": "copy stream double-buffered against compute (layer.LayerPipeline)"}
+               "pipeline": "upload and download streams double-buffered against compute (layer.LayerPipeline)"}
 
     if rank != 0:
         if world > 1:

@@ -305,6 +305,8 @@ struct blb_params {
     int mac_chunk = 3;            // outputs per MAC / giant-step chunk of the two-stream schedule (env BLB_CHUNK)
     int mac_tma = 1;              // warp-specialised bulk-copy MAC (env BLB_MAC_TMA=0: register double buffer)
     int pt_pack = 1;              // 5-byte packed plaintext limbs for primes < 2^40 (env BLB_PT_PACK=0: 8 bytes)
+    int mac_r = 0;                // ct-ct K' MAC on rotation-shared blocks of 4 outputs (k_mac_r; env BLB_MAC_R, 0 = k_mac_j)
+    int ks_sg = 0;                // key switch: groups per shared-digit chunk (k_ks_inner_sg; env BLB_KS_SG, 0 = off)
     int ntt_2s = 1;               // two-stream NTT: integer-kernel rows on the auxiliary stream (env BLB_NTT_2S)
     int tsum_acc = 1;             // tensor J-sum accumulators: 1 AccG, 0 Acc41 + AccF64 (env BLB_TSUM_ACC)
     int ks_acc = 4;               // key-switch inner product accumulators (40-bit limbs), see k_ks_inner (env BLB_KS_ACC)
@@ -471,6 +473,13 @@ size_t encode_scratch_doubles(const blb_params *P, int n_pts);
 blb_status launch_mac(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc, const int *ent_r, const int *ent_pt,
                       const int *ent_start, int o0, int e_base, int n_o, int n_entries, int k, cudaStream_t st,
                       int kq = -1, int jg = 1);
+
+// Rotation-shared mask MAC (IG = 4 outputs per block sharing each staged rotation pair; matmul.cu k_mac_r):
+// block b has stages rb_start[b] .. rb_start[b+1]-1 with rotation rb_r[s] and masks rb_m[s*4 + t] (-1 = none)
+// accumulated into acc output rb_out[b*4 + t] (-1 = none)
+blb_status launch_mac_r(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc, const int *rb_start, const int *rb_r,
+                        const int *rb_m, const int *rb_out, int n_blk, int n_stages, int n_products, int ig, int k,
+                        int kq, cudaStream_t st);
 
 // ChaCha / sampling
 enum { TAG_SECRET = 1, TAG_KEY_A = 2, TAG_KEY_E = 3, TAG_ENC_A = 4, TAG_ENC_E = 5, TAG_MASK = 6 };

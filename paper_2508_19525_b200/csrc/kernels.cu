@@ -1,3 +1,4 @@
+#include <algorithm>
 // kernels.cu -- RNS pointwise kernels of the B200 BLB library:
 //   ChaCha20 samplers (C4), key generation (C5), encrypt / decrypt (C6),
 //   FastBConv ModUp / ModDown and the key-switch inner product with the
@@ -215,13 +216,28 @@ struct KsGroups {
 // jobs.j[t].out ([2][E][N]) -- the double-hoisted rotation (no ModDown).
 // SMALL (prime < 2^41): the a-part products run on the FP64 pipe (AccF64), the b-part on the
 // integer pipe, so the two pipes share the 2 beta products per job.
+// Digit sources of the key-switch inner product: DigG loads job t's extended digit j straight from
+// global memory; DigS reads it from the CTA's shared-memory copy (k_ks_inner_sg: the groups of a
+// chunk share their digits, loaded once per CTA).
+struct DigG {
+    const KsJobs *jobs;
+    long long off;  // m * N + x
+    long long EN;   // E * N
+    __device__ __forceinline__ u64 operator()(int t, int, int j) const { return jobs->j[t].ext[j * EN + off]; }
+};
+struct DigS {
+    const u64 *s;
+    int stride_q, stride_j, tid;
+    __device__ __forceinline__ u64 operator()(int, int q, int j) const { return s[q * stride_q + j * stride_j + tid]; }
+};
+
 // KA (env BLB_KS_ACC): 40-bit rows 0 = b-part Acc128 + a-part AccF64, 1 = both AccG (FP64 pipe, no
 // per-product reduction), 2 = b-part Acc41 + a-part AccG; 3 = as 1 with the 60-bit rows on Acc60;
 // 4 = as 1 with the 60-bit rows one job at a time on Acc60 (ks_inner_body60)
-template <int BETA, bool EXT, bool SMALL, int KA>
+template <int BETA, bool EXT, bool SMALL, int KA, class DS>
 __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups &grp, u64 *u, const Primes &pr, int k,
                                               int np, int K, int beta_rt, int logN, const PinvTab &pq, int x, int m,
-                                              int gi) {
+                                              int gi, const DS &ds) {
     const int N = 1 << logN;
     const int beta = BETA > 0 ? BETA : beta_rt;
     const int t0 = grp.start[gi], cnt = grp.start[gi + 1] - t0;
@@ -254,9 +270,8 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
         for (int q = 0; q < kKsGroup; q++) {
             if (q < cnt) {
                 u64 e[BETA > 0 ? BETA : 1];
-                const u64 *ext = jobs.j[t0 + q].ext + (long long)m * N + x;
 #pragma unroll
-                for (int j = 0; j < BETA; j++) e[j] = ext[(long long)j * E * N];
+                for (int j = 0; j < BETA; j++) e[j] = ds(t0 + q, q, j);
 #pragma unroll
                 for (int j = 0; j < BETA; j++) {
                     accm(a0[q], e[j], kb[j], qd, qinv);
@@ -271,7 +286,7 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
 #pragma unroll
             for (int q = 0; q < kKsGroup; q++) {
                 if (q < cnt) {
-                    const u64 e = jobs.j[t0 + q].ext[((long long)j * E + m) * N + x];
+                    const u64 e = ds(t0 + q, q, j);
                     accm(a0[q], e, kb, qd, qinv);
                     accm(a1[q], e, ka, qd, qinv);
                 }
@@ -320,9 +335,10 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
 // 60-bit rows with KA = 4: the group's jobs one at a time on Acc60 (6 IMAD-class instructions per
 // product instead of Acc128's ~11), so only one job's accumulators are live (Acc60 for all four jobs
 // at once needed 122 registers, KA = 3).  Same additive terms and stores as ks_inner_body.
-template <int BETA, bool EXT>
+template <int BETA, bool EXT, class DS>
 __device__ __forceinline__ void ks_inner_body60(const KsJobs &jobs, const KsGroups &grp, u64 *u, const Primes &pr, int k,
-                                                int np, int K, int logN, const PinvTab &pq, int x, int m, int gi) {
+                                                int np, int K, int logN, const PinvTab &pq, int x, int m, int gi,
+                                                const DS &ds) {
     const int N = 1 << logN;
     const int t0 = grp.start[gi], cnt = grp.start[gi + 1] - t0;
     const int E = k + np, Lk = K + np;
@@ -341,9 +357,8 @@ __device__ __forceinline__ void ks_inner_body60(const KsJobs &jobs, const KsGrou
         const int t = t0 + q;
         const KsJob &J = jobs.j[t];
         u64 e[BETA];
-        const u64 *ext = J.ext + (long long)m * N + x;
 #pragma unroll
-        for (int j = 0; j < BETA; j++) e[j] = ext[(long long)j * E * N];
+        for (int j = 0; j < BETA; j++) e[j] = ds(t, q, j);
         u64 c0v = 0, c1v = 0;
         if (m < k) {
             if (EXT || J.add_mode != 0) c0v = J.c0[(long long)m * N + x];
@@ -382,9 +397,48 @@ __global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, 
     const int m = blockIdx.y;
     if (x >= (1 << logN)) return;
     const int pm = m < k ? m : K + (m - k);
-    if (pr.m[pm].q < (1ull << 41)) ks_inner_body<BETA, EXT, true, KA>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi);
-    else if constexpr (KA == 4 && BETA > 0 && BETA <= 7) ks_inner_body60<BETA, EXT>(jobs, grp, u, pr, k, np, K, logN, pq, x, m, gi);
-    else ks_inner_body<BETA, EXT, false, KA>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi);
+    const DigG ds{&jobs, (long long)m * (1 << logN) + x, (long long)(k + np) << logN};
+    if (pr.m[pm].q < (1ull << 41)) ks_inner_body<BETA, EXT, true, KA>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi, ds);
+    else if constexpr (KA == 4 && BETA > 0 && BETA <= 7) ks_inner_body60<BETA, EXT>(jobs, grp, u, pr, k, np, K, logN, pq, x, m, gi, ds);
+    else ks_inner_body<BETA, EXT, false, KA>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi, ds);
+}
+
+// Shared-digit variant: consecutive key groups whose jobs use the same extended digits (hoisted
+// rotations: the J ciphertexts of a ct-ct operand rotated by every step, or the inputs of a ct-pt
+// MatMul by every baby step) form chunks; a CTA loads its (tile, limb) slice of the chunk's digits
+// once into shared memory and runs the chunk's groups over it.  Without it every group re-read the
+// digits from DRAM (ncu: 1.9 GB read where keys + one pass over the digits are 0.7 GB).
+// grid (tiles, E, chunks); chunk c covers groups ch.gl[ch.g0[c]] .. ch.gl[ch.g0[c + 1] - 1].
+struct KsChunks {
+    int n;
+    int g0[kMaxJobs + 1];
+    int gl[kMaxJobs];
+};
+template <int BETA, bool EXT, int KA>
+__global__ void __launch_bounds__(kTB, 2) k_ks_inner_sg(KsJobs jobs, KsGroups grp, KsChunks ch, u64 *u, Primes pr, int k, int np, int K, int logN,
+                              PinvTab pq) {
+    extern __shared__ u64 sdig[];  // [kKsGroup][BETA][blockDim]
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int m = blockIdx.y, c = blockIdx.z;
+    const int N = 1 << logN, E = k + np;
+    const int c0 = ch.g0[c], c1 = ch.g0[c + 1];
+    const int t0 = grp.start[ch.gl[c0]], cnt = grp.start[ch.gl[c0] + 1] - t0;
+    const int bd = blockDim.x, tid = threadIdx.x;
+    // each thread stores and later reads only its own coefficient's slots: no barrier needed
+    for (int q = 0; q < cnt; q++) {
+        const u64 *ext = jobs.j[t0 + q].ext + (long long)m * N + x;
+#pragma unroll
+        for (int j = 0; j < BETA; j++) sdig[(q * BETA + j) * bd + tid] = ext[(long long)j * E * N];
+    }
+    const DigS ds{sdig, BETA * bd, bd, tid};
+    const int pm = m < k ? m : K + (m - k);
+    const bool small = pr.m[pm].q < (1ull << 41);
+    for (int ci = c0; ci < c1; ci++) {
+        const int gi = ch.gl[ci];
+        if (small) ks_inner_body<BETA, EXT, true, KA>(jobs, grp, u, pr, k, np, K, BETA, logN, pq, x, m, gi, ds);
+        else if constexpr (KA == 4) ks_inner_body60<BETA, EXT>(jobs, grp, u, pr, k, np, K, logN, pq, x, m, gi, ds);
+        else ks_inner_body<BETA, EXT, false, KA>(jobs, grp, u, pr, k, np, K, BETA, logN, pq, x, m, gi, ds);
+    }
 }
 
 // conv[t][b][i][x] = FastBConv_{P -> q_i}(INTT(u_P))   (u P-rows already INTT'd)
@@ -631,6 +685,52 @@ static blb_status ks_inner_launch(const blb_params *P, int level, const KsJobs &
         pq.sh[i] = blbh_shoup_dev_table(P, i);
     }
     cudaEvent_t t0 = blb_timing_begin(st);
+    // shared-digit chunks: runs of consecutive groups with the same job count and the same digit
+    // pointers (at most P->ks_sg groups per chunk)
+    KsChunks ch{};
+    ch.n = 0;
+    int longest = 0;
+    if (P->ks_sg > 1 && beta >= 1 && beta <= 6 && (P->ks_acc == 1 || P->ks_acc == 4) && N % kTB == 0) {
+        // greedy: each unassigned group opens a chunk and takes the later groups with its signature
+        // (job count + digit pointers), e.g. every step's group of the same input block
+        bool used[kMaxJobs] = {false};
+        int nl = 0;
+        for (int g = 0; g < G.n; g++) {
+            if (used[g]) continue;
+            const int cnt = G.start[g + 1] - G.start[g];
+            ch.g0[ch.n++] = nl;
+            int len = 0;
+            for (int h = g; h < G.n && len < P->ks_sg; h++) {
+                if (used[h] || G.start[h + 1] - G.start[h] != cnt) continue;
+                bool same = true;
+                for (int q = 0; q < cnt && same; q++) same = J.j[G.start[h] + q].ext == J.j[G.start[g] + q].ext;
+                if (!same) continue;
+                used[h] = true;
+                ch.gl[nl++] = h;
+                len++;
+            }
+            longest = std::max(longest, len);
+        }
+        ch.g0[ch.n] = nl;
+    }
+    if (longest >= 2) {
+        const dim3 gsg((unsigned)(N / kTB), E, ch.n);
+        const size_t smem = (size_t)kKsGroup * beta * kTB * 8;
+#define BLB_KS_SG(B_, KA_) k_ks_inner_sg<B_, EXT, KA_><<<gsg, kTB, smem, st>>>(J, G, ch, u, P->pr, k, np, P->K, P->logN, pq)
+#define BLB_KS_SG_SWITCH(KA_)                   \
+    switch (beta) {                             \
+        case 1: BLB_KS_SG(1, KA_); break;       \
+        case 2: BLB_KS_SG(2, KA_); break;       \
+        case 3: BLB_KS_SG(3, KA_); break;       \
+        case 4: BLB_KS_SG(4, KA_); break;       \
+        case 5: BLB_KS_SG(5, KA_); break;       \
+        default: BLB_KS_SG(6, KA_); break;      \
+    }
+        if (P->ks_acc == 4) { BLB_KS_SG_SWITCH(4) }
+        else { BLB_KS_SG_SWITCH(1) }
+#undef BLB_KS_SG_SWITCH
+#undef BLB_KS_SG
+    } else {
     const dim3 gks((unsigned)(((N + kTB - 1) / kTB) * G.n), E);
 #define BLB_KS_SWITCH(KA_)                                                                                    \
     switch (beta) {                                                                                          \
@@ -648,6 +748,7 @@ static blb_status ks_inner_launch(const blb_params *P, int level, const KsJobs &
     else if (P->ks_acc == 2) { BLB_KS_SWITCH(2) }
     else { BLB_KS_SWITCH(0) }
 #undef BLB_KS_SWITCH
+    }
     BLB_COUNT_LAUNCH(1);
     // algorithmic bytes: each distinct key once (groups sharing a key read it through L2)
     int n_keys = 0;

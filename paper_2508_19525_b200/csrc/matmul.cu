@@ -471,6 +471,129 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_j(const u64 *__restrict_
     else macj_consume<false, JG, AM>(ring, full, empty, n_e, outs, kN, mc);
 }
 
+// Rotation-shared mask MAC (ct-ct stage 1, K'_i = sum_c M_{c,i} (.) Rot_{c+i}(K), reading C13): the IG
+// consecutive outputs i0 .. i0 + IG - 1 of one ciphertext j use the same rotations shifted by one, so
+// a CTA walks the union of their rotations: per stage ONE (c0, c1) rotation tile pair + the IG masks
+// that select it (-1: that output does not use this rotation).  Staged bytes per product drop from
+// 10 (k_mac_j: a mask per output pair + a rotation pair per output) to ~6.  One coefficient per
+// thread (IG x 2 accumulators), 256-coefficient tiles on a 4-stage bulk-copy ring.
+// Block lists (host, qk.cu): stages rb_start[b] .. rb_start[b+1]-1, rotation rb_r[s], masks
+// rb_m[s * IG + t], outputs rb_out[b * IG + t] (acc index).
+constexpr int kMrStages = 4;
+#ifndef BLB_MACR_TILES
+#define BLB_MACR_TILES 1
+#endif
+constexpr int kMrTiles = BLB_MACR_TILES;  // 256-coefficient tiles per CTA (the ring stays full across them)
+template <int IG>
+constexpr size_t macr_smem() { return (size_t)kMrStages * (2 + IG) * 256 * 8 + 2 * kMrStages * 8; }
+
+template <bool SMALL, int IG>
+__device__ __forceinline__ void macr_consume(const u64 *ring, uint64_t *full, uint64_t *empty, const int *rb_m, int s0,
+                                             int n_s, u64 *const *outs, long long kN, const ModConst &mc, int sg0) {
+    using A = typename std::conditional<SMALL, AccG, Acc128>::type;
+    const double qd = (double)mc.q, qinv = 1.0 / qd;
+    A a0[IG], a1[IG];
+#pragma unroll
+    for (int t = 0; t < IG; t++) { a0[t].zero(); a1[t].zero(); }
+    constexpr int kStageWords = (2 + IG) * 256;
+    const int tid = threadIdx.x;
+    for (int s = 0; s < n_s; s++) {
+        const int sg = sg0 + s;  // ring position continues across the CTA's tiles
+        const int slot = sg % kMrStages;
+        mbar_wait(&full[slot], (sg / kMrStages) & 1);
+        const u64 *st = ring + (size_t)slot * kStageWords;
+        const u64 r0 = st[tid], r1 = st[256 + tid];
+#pragma unroll
+        for (int t = 0; t < IG; t++) {
+            if (rb_m[(s0 + s) * IG + t] >= 0) {  // uniform over the CTA
+                const u64 mv = st[(2 + t) * 256 + tid];
+                accm(a0[t], mv, r0, qd, qinv);
+                accm(a1[t], mv, r1, qd, qinv);
+            }
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[slot]);
+        if ((!SMALL && (s & 63) == 63) || (SMALL && (s & 511) == 511)) {
+#pragma unroll
+            for (int t = 0; t < IG; t++) { accf(a0[t], mc, qd, qinv); accf(a1[t], mc, qd, qinv); }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < IG; t++) {
+        if (outs[t]) {
+            outs[t][tid] = accr(a0[t], mc, qd, qinv);
+            outs[t][kN + tid] = accr(a1[t], mc, qd, qinv);
+        }
+    }
+}
+
+// grid: (block fastest, 256-coefficient tile, limb)
+template <int IG>
+__global__ void __launch_bounds__(256 + 32, 3) k_mac_r(const u64 *__restrict__ pt, const u64 *__restrict__ R,
+                                                  u64 *__restrict__ acc, const int *__restrict__ rb_start,
+                                                  const int *__restrict__ rb_r, const int *__restrict__ rb_m,
+                                                  const int *__restrict__ rb_out, int n_blk, int k, int kq, int Kfull,
+                                                  int logN, Primes pr) {
+    constexpr int kStageWords = (2 + IG) * 256;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    u64 *ring = reinterpret_cast<u64 *>(smraw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)kMrStages * kStageWords);
+    uint64_t *empty = full + kMrStages;
+    const int N = 1 << logN;
+    const int n_tg = N / (256 * kMrTiles);  // groups of kMrTiles consecutive 256-coefficient tiles
+    int bid = blockIdx.x;
+    const int b = bid % n_blk;
+    bid /= n_blk;
+    const int tg = bid % n_tg;
+    const int l = bid / n_tg;
+    const long long kN = (long long)k * N;
+    const int s0 = rb_start[b], n_s = rb_start[b + 1] - s0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kMrStages; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 256 / 32);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x >= 256) {  // producer warp: the stages of every tile of the CTA back to back
+        if (threadIdx.x == 256) {
+            for (int sg = 0; sg < kMrTiles * n_s; sg++) {
+                const int s = sg % n_s;
+                const long long lx0 = (long long)l * N + (tg * kMrTiles + sg / n_s) * 256;
+                const int slot = sg % kMrStages;
+                if (sg >= kMrStages) mbar_wait(&empty[slot], ((sg / kMrStages) - 1) & 1);
+                u64 *st = ring + (size_t)slot * kStageWords;
+                int nm = 0;
+#pragma unroll
+                for (int t = 0; t < IG; t++) nm += rb_m[(s0 + s) * IG + t] >= 0;
+                mbar_expect_tx(&full[slot], (unsigned)(2 + nm) * 2048u);
+                const int ri = rb_r[s0 + s];
+                bulk_g2s(st, R + (long long)ri * 2 * kN + lx0, 2048, &full[slot]);
+                bulk_g2s(st + 256, R + ((long long)ri * 2 + 1) * kN + lx0, 2048, &full[slot]);
+#pragma unroll
+                for (int t = 0; t < IG; t++) {
+                    const int mi = rb_m[(s0 + s) * IG + t];
+                    if (mi >= 0) bulk_g2s(st + (2 + t) * 256, pt + (long long)mi * kN + lx0, 2048, &full[slot]);
+                }
+            }
+        }
+        return;
+    }
+    const ModConst &mc = pr.m[l < kq ? l : Kfull + (l - kq)];
+    for (int ti = 0; ti < kMrTiles; ti++) {
+        const long long lx0 = (long long)l * N + (tg * kMrTiles + ti) * 256;
+        u64 *outs[IG];
+#pragma unroll
+        for (int t = 0; t < IG; t++) {
+            const int o = rb_out[b * IG + t];
+            outs[t] = o >= 0 ? acc + (long long)o * 2 * kN + lx0 : nullptr;
+        }
+        if (mc.q < (1ull << 41)) macr_consume<true, IG>(ring, full, empty, rb_m, s0, n_s, outs, kN, mc, ti * n_s);
+        else macr_consume<false, IG>(ring, full, empty, rb_m, s0, n_s, outs, kN, mc, ti * n_s);
+    }
+}
+
 // dst[o] += src[j] for the jobs of one giant batch (sequential per thread: no races)
 struct AccJobs {
     int n;
@@ -544,6 +667,36 @@ blb_status launch_mac(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc
     BLB_COUNT_LAUNCH(1);
     BLB_COUNT(3, n_entries);
     blb_timing_end(3, t0, st, 3.0 * n_entries * k * N * 8.0);  // category 3: ct-ct mask MAC (mask + c0, c1 bytes)
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+
+blb_status launch_mac_r(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc, const int *rb_start, const int *rb_r,
+                        const int *rb_m, const int *rb_out, int n_blk, int n_stages, int n_products, int ig, int k,
+                        int kq, cudaStream_t st) {
+    if (n_blk <= 0) return BLB_OK;
+    if (ig != 4 || P->N % 256 != 0) {
+        blb_set_error("launch_mac_r: IG = 4 and N %% 256 == 0 only");
+        return BLB_E_INVALID_ARG;
+    }
+    const int N = P->N;
+    cudaEvent_t t0 = blb_timing_begin(st);
+    constexpr size_t smem = macr_smem<4>();
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_mac_r<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    if (N % (256 * kMrTiles) != 0) {
+        blb_set_error("launch_mac_r: N must be a multiple of %d", 256 * kMrTiles);
+        return BLB_E_INVALID_ARG;
+    }
+    const unsigned grid = (unsigned)((size_t)n_blk * (N / (256 * kMrTiles)) * k);
+    k_mac_r<4><<<grid, 256 + 32, smem, st>>>(pt, R, acc, rb_start, rb_r, rb_m, rb_out, n_blk, k, kq, P->K, P->logN, P->pr);
+    BLB_COUNT_LAUNCH(1);
+    BLB_COUNT(3, n_products);
+    // bytes staged: one (c0, c1) rotation pair per stage + one mask tile per product
+    blb_timing_end(3, t0, st, (2.0 * n_stages + (double)n_products) * k * N * 8.0);
     BLB_CHECK_LAUNCH();
     return BLB_OK;
 }

@@ -1,3 +1,4 @@
+#include <array>
 // qk.cu -- BLB's rotation-efficient ct-ct MatMul Q_h K_h^T for all heads (row a7).
 //
 // Sec. 5.1: Observations 1-2, the three steps, multi-head packing
@@ -35,6 +36,10 @@ struct blb_qk_plan {
     std::vector<MaskDesc> m1, m3;                // stage-1 masks (level), stage-3 masks (level-2)
     // MAC entry lists (CSR): K' outputs o = i*J + j; Q outputs o = (u-1)*J + j; A outputs = accumulators
     std::vector<int> kp_start, kp_r, kp_pt, qp_start, qp_r, qp_pt, a_start, a_r, a_pt;
+    // rotation-shared blocks of the K' MAC (k_mac_r): 4 consecutive i of one j, stages = union of rotations
+    std::vector<int> rb_start, rb_r, rb_m, rb_out;
+    bool rb_ok = false;
+    size_t off_rb_start = 0, off_rb_r = 0, off_rb_m = 0, off_rb_out = 0;
     struct Acc {
         int u, w, f, out, rot;
     };
@@ -347,6 +352,30 @@ extern "C" blb_status blb_qk_plan_create(const blb_params *P, int L, int heads, 
             }
             pl->kp_start.push_back((int)pl->kp_r.size());
         }
+    // rotation-shared blocks (i0 .. i0+3, j) of the K' MAC: every output's entries keyed by rotation
+    if (B % 4 == 0) {
+        pl->rb_ok = true;
+        pl->rb_start.push_back(0);
+        for (int i0 = 0; i0 < B && pl->rb_ok; i0 += 4)
+            for (int j = 0; j < pl->J && pl->rb_ok; j++) {
+                std::map<int, std::array<int, 4>> stg;
+                for (int t = 0; t < 4; t++) {
+                    const int o = (i0 + t) * pl->J + j;
+                    for (int e = pl->kp_start[o]; e < pl->kp_start[o + 1]; e++) {
+                        auto it = stg.find(pl->kp_r[e]);
+                        if (it == stg.end()) it = stg.emplace(pl->kp_r[e], std::array<int, 4>{-1, -1, -1, -1}).first;
+                        if (it->second[t] >= 0) pl->rb_ok = false;  // two entries of one output on one rotation
+                        it->second[t] = pl->kp_pt[e];
+                    }
+                }
+                for (auto &kv : stg) {
+                    pl->rb_r.push_back(kv.first);
+                    for (int t = 0; t < 4; t++) pl->rb_m.push_back(kv.second[t]);
+                }
+                pl->rb_start.push_back((int)pl->rb_r.size());
+                for (int t = 0; t < 4; t++) pl->rb_out.push_back((i0 + t) * pl->J + j);
+            }
+    }
     // Q MAC: output o = (u-1)*J + j, two entries
     pl->qp_start.push_back(0);
     for (int u = 1; u < pl->G; u++)
@@ -399,6 +428,10 @@ extern "C" blb_status blb_qk_plan_create(const blb_params *P, int L, int heads, 
     pl->off_kp_start = put(pl->kp_start); pl->off_kp_r = put(pl->kp_r); pl->off_kp_pt = put(pl->kp_pt);
     pl->off_qp_start = put(pl->qp_start); pl->off_qp_r = put(pl->qp_r); pl->off_qp_pt = put(pl->qp_pt);
     pl->off_a_start = put(pl->a_start); pl->off_a_r = put(pl->a_r); pl->off_a_pt = put(pl->a_pt);
+    if (pl->rb_ok) {
+        pl->off_rb_start = put(pl->rb_start); pl->off_rb_r = put(pl->rb_r);
+        pl->off_rb_m = put(pl->rb_m); pl->off_rb_out = put(pl->rb_out);
+    }
     cudaError_t e = cudaMalloc(&pl->d_ent, sizeof(int) * std::max<size_t>(all.size(), 1));
     if (e == cudaSuccess) e = cudaMemcpy(pl->d_ent, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&pl->d_m1, sizeof(MaskDesc) * pl->m1.size());
@@ -632,8 +665,13 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
     };
     for (int j = 0; j < J; j++) BLB_TRY(launch_lift_ext(P, lvl, K[j].data, W + w.kr + (size_t)j * NKR * ct_e, st));
     BLB_TRY(rotate_ext_J(K, pl->k_rots, W + w.kr + ct_e, (size_t)NKR * ct_e));
-    BLB_TRY(launch_mac(P, m1, W + w.kr, W + w.kacc, E + pl->off_kp_r, E + pl->off_kp_pt, E + pl->off_kp_start, 0, 0,
-                       B * J, (int)pl->kp_r.size(), Ex, st, k, J));  // outputs i*J + j share their masks
+    if (P->mac_r && pl->rb_ok && P->N % 1024 == 0)  // blocks of 4 outputs i sharing each staged rotation
+        BLB_TRY(launch_mac_r(P, m1, W + w.kr, W + w.kacc, E + pl->off_rb_start, E + pl->off_rb_r, E + pl->off_rb_m,
+                             E + pl->off_rb_out, (int)pl->rb_start.size() - 1, (int)pl->rb_r.size(),
+                             (int)pl->kp_r.size(), 4, Ex, k, st));
+    else
+        BLB_TRY(launch_mac(P, m1, W + w.kr, W + w.kacc, E + pl->off_kp_r, E + pl->off_kp_pt, E + pl->off_kp_start, 0, 0,
+                           B * J, (int)pl->kp_r.size(), Ex, st, k, J));  // outputs i*J + j share their masks
     BLB_TRY(launch_moddown_rescale(P, lvl, W + w.kacc, B * J, W + w.kp, conv, st));  // C17
     // 2. giant side: Q_0 = level drop, Q_u = ModDown(MAC(masks, Rot_ext(Q))), rescale
     if (NQR) BLB_TRY(rotate_ext_J(Q, pl->q_rots, W + w.qr, (size_t)NQR * ct_e));

@@ -580,7 +580,8 @@ def test_batched_inputs_bit_exact(toy):
 
 @pytest.mark.parametrize("knobs", [{"BLB_MAC_NINT": "0", "BLB_MACJ_ACC": "0", "BLB_KS_ACC": "0", "BLB_TSUM_ACC": "0"},
                                    {"BLB_MAC_NINT": "2", "BLB_MACJ_ACC": "1", "BLB_KS_ACC": "2"},
-                                   {"BLB_KS_ACC": "3"}, {"BLB_KS_ACC": "4", "BLB_NTT_2S": "0"}])
+                                   {"BLB_KS_ACC": "3"}, {"BLB_KS_ACC": "4", "BLB_NTT_2S": "0", "BLB_KS_SG": "0"},
+                                   {"BLB_KS_ACC": "1", "BLB_KS_SG": "3", "BLB_MAC_R": "1"}])
 def test_accumulator_variants_bit_exact(monkeypatch, knobs):
     """The selectable accumulators (AccF64 / Acc41 / Acc128 instead of the default grid-split AccG,
     DESIGN §7) give the same bits: the toy ct-pt MatMul and a toy ct-ct Q K^T against the oracle."""
