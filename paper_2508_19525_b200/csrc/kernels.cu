@@ -414,8 +414,11 @@ struct KsChunks {
     int g0[kMaxJobs + 1];
     int gl[kMaxJobs];
 };
+#ifndef BLB_KS_SG_MINB
+#define BLB_KS_SG_MINB 2
+#endif
 template <int BETA, bool EXT, int KA>
-__global__ void __launch_bounds__(kTB, 2) k_ks_inner_sg(KsJobs jobs, KsGroups grp, KsChunks ch, u64 *u, Primes pr, int k, int np, int K, int logN,
+__global__ void __launch_bounds__(kTB, BLB_KS_SG_MINB) k_ks_inner_sg(KsJobs jobs, KsGroups grp, KsChunks ch, u64 *u, Primes pr, int k, int np, int K, int logN,
                               PinvTab pq) {
     extern __shared__ u64 sdig[];  // [kKsGroup][BETA][blockDim]
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
