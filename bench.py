@@ -184,7 +184,7 @@ def run_reference(args, dims):
         if s >= args.warmup:
             samples.append(r["ms_per_layer"])
     v = float(np.median(samples))
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+    line = {"impl": "reference", "metric": metric_name(dims), "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": config_dict(dims, args.gpus),
@@ -194,8 +194,16 @@ def run_reference(args, dims):
     print(json.dumps(line), flush=True)
 
 
+def model_name(dims):
+    return "BERT-base" if dims["d"] == 768 else "BERT-large"
+
+
+def metric_name(dims):
+    return METRIC.replace("BERT-base", model_name(dims))
+
+
 def config_dict(dims, world):
-    return {"workload": "BERT-base layer fused-linear CKKS (config 2 QKV + Q.K^T, Softmax.V + out-proj, config 3 "
+    return {"workload": model_name(dims) + " layer fused-linear CKKS (config 2 QKV + Q.K^T, Softmax.V + out-proj, config 3 "
                         "FFN1/FFN2, CKKS->MPC masks), N=2^16, Q={60,40x4}, P={60}, dnum=5",
             "L": dims["L"], "d": dims["d"], "heads": dims["H"], "ffn": dims["ffn"], "log_n": 16, "limbs": 5,
             "bsgs": dict(BSGS),
@@ -203,7 +211,7 @@ def config_dict(dims, world):
                           "softmaxV_ct_ct(pad+collapse)", "oproj_diag_ct_pt(level 1)", "mask", "ffn1_ct_pt", "mask",
                           "ffn2_ct_pt", "mask"],
             "not_included": "non-MatMul HE ops of Table 6 blocks 2-5 (row f2) and the MPC protocols",
-            "l2": "inputs larger than L2 (~76 GB of plaintexts streamed per step)",
+            "l2": "inputs larger than L2 (%s of plaintexts streamed per step)" % ("~57 GB" if dims["d"] == 768 else "~100 GB"),
             "parallelism": "dp%d (output-ciphertext sharding, NCCL all-gather of masked outputs)" % world}
 
 
@@ -380,7 +388,7 @@ def main():
         except Exception:
             traffic = None
     line = {
-        "metric": METRIC, "value": ms_step, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": metric_name(dims), "value": ms_step, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded N(0,1) activations, N(0,0.04^2) weights)",
         "config": config_dict(dims, world),

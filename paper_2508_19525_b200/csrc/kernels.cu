@@ -10,6 +10,9 @@
 
 namespace {
 constexpr int kTB = 256;
+#ifndef BLB_MIX
+#define BLB_MIX 0
+#endif
 
 // ---------------------------------------------------------------- ChaCha20
 __device__ __forceinline__ uint32_t rotl32(uint32_t x, int r) { return __funnelshift_l(x, x, r); }
@@ -394,7 +397,11 @@ __global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, 
                            int logN, PinvTab pq) {
     const int gi = blockIdx.x % grp.n;
     const int x = (blockIdx.x / grp.n) * blockDim.x + threadIdx.x;
+#if BLB_MIX
+    const int m = (blockIdx.y + blockIdx.x) % gridDim.y;  // limbs interleaved (60-bit / 40-bit rows mixed)
+#else
     const int m = blockIdx.y;
+#endif
     if (x >= (1 << logN)) return;
     const int pm = m < k ? m : K + (m - k);
     const DigG ds{&jobs, (long long)m * (1 << logN) + x, (long long)(k + np) << logN};

@@ -42,6 +42,9 @@ struct blb_matmul_plan {
 
 namespace {
 constexpr int kTB = 256;
+#ifndef BLB_MIX
+#define BLB_MIX 0
+#endif
 
 // Build the slot vectors of entries [e0, e0 + cnt) (plan order) into slots[cnt][n].
 struct PlanDev {
@@ -274,10 +277,19 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char
     const int n_tiles = N / (2 * kTB);
     const int n_grp = (n_o + kMacP - 1) / kMacP;
     int bid = blockIdx.x;
+#if BLB_MIX
+    // limb fastest: CTAs of the 60-bit limb (integer pipe) and of the 40-bit limbs (FP64 pipe) are
+    // in flight together instead of one limb after the other
+    const int l = bid % k;
+    bid /= k;
+    const int og = bid % n_grp;
+    const int tile = bid / n_grp;
+#else
     const int og = bid % n_grp;
     bid /= n_grp;
     const int tile = bid % n_tiles;
     const int l = bid / n_tiles;
+#endif
     const int oa = og * kMacP, nP = min(kMacP, n_o - oa);
     const long long kN = (long long)k * N;
     const int e_lo = ent_start[o0 + oa], n_e = ent_start[o0 + oa + 1] - e_lo;
@@ -426,10 +438,17 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_j(const u64 *__restrict_
     const int N = 1 << logN;
     const int n_tiles = N / (2 * kTB);
     int bid = blockIdx.x;
+#if BLB_MIX
+    const int l = bid % k;
+    bid /= k;
+    const int gi = bid % n_grp;
+    const int tile = bid / n_grp;
+#else
     const int gi = bid % n_grp;
     bid /= n_grp;
     const int tile = bid % n_tiles;
     const int l = bid / n_tiles;
+#endif
     const int oa = gi * JG;
     const long long kN = (long long)k * N;
     const int e_lo = ent_start[o0 + oa], n_e = ent_start[o0 + oa + 1] - e_lo;
