@@ -211,7 +211,7 @@ def config_dict(dims, world):
                           "softmaxV_ct_ct(pad+collapse)", "oproj_diag_ct_pt(level 1)", "mask", "ffn1_ct_pt", "mask",
                           "ffn2_ct_pt", "mask"],
             "not_included": "non-MatMul HE ops of Table 6 blocks 2-5 (row f2) and the MPC protocols",
-            "l2": "inputs larger than L2 (%s of plaintexts streamed per step)" % ("~57 GB" if dims["d"] == 768 else "~100 GB"),
+            "l2": "inputs larger than L2 (%s of plaintexts streamed per step)" % ("~57 GB" if dims["d"] == 768 else "~91 GB"),
             "parallelism": "dp%d (output-ciphertext sharding, NCCL all-gather of masked outputs)" % world}
 
 

@@ -153,10 +153,19 @@ constexpr double kTwo52 = 4503599627370496.0, kMagic = 6755399441055744.0;  // 2
 __device__ __forceinline__ double u2d(u64 x) {  // x < 2^52
     return __dsub_rn(__hiloint2double(0x43300000 | (int)(x >> 32), (int)(uint32_t)x), kTwo52);
 }
+#ifndef BLB_NTT_RND
+#define BLB_NTT_RND 0
+#endif
 __device__ __forceinline__ double mulr(double y, double w, double q, double qinv) {
     const double p = __dmul_rn(y, w);
     const double e = __fma_rn(y, w, -p);
+#if BLB_NTT_RND
+    // round(p / q) as fl(p * qinv) + 1.5 2^52 - 1.5 2^52: three FP64 ops but no register copies of
+    // the uniform qinv (DFMA cannot take a uniform-register B operand together with an immediate C)
+    const double c = __dsub_rn(__dadd_rn(__dmul_rn(p, qinv), kMagic), kMagic);
+#else
     const double c = __dsub_rn(__fma_rn(p, qinv, kMagic), kMagic);  // round(p / q): |c - y w / q| < 5/8
+#endif
     return __dadd_rn(__fma_rn(-c, q, p), e);
 }
 __device__ __forceinline__ double centre(double x, double q, double qinv) {  // x - round(x / q) q
