@@ -42,6 +42,12 @@ struct blb_matmul_plan {
 
 namespace {
 constexpr int kTB = 256;
+#ifndef BLB_MAC_STG
+#define BLB_MAC_STG 4
+#endif
+#ifndef BLB_MAC_MINB
+#define BLB_MAC_MINB 3
+#endif
 #ifndef BLB_MIX
 #define BLB_MIX 0
 #endif
@@ -1131,7 +1137,7 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
                     if (j % PP != PP - 1 && j + 1 < n_o && !pl->same_next[o0 + j]) grouped = false;
                 // BLB_MAC_NINT: accumulators per output on the integer pipe (0..2; the rest on FP64)
                 if (grouped && PP == 2 && P->mac_nint < 0)
-                    launch_mac4<2, 4, 3, -1>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
+                    launch_mac4<2, BLB_MAC_STG, BLB_MAC_MINB, -1>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
                                              P->pr, n_tiles, lay, st);
                 else if (grouped && PP == 2 && P->mac_nint == 0)
                     launch_mac4<2, 4, 3, 0>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
