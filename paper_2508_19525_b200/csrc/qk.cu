@@ -605,8 +605,8 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
             blb_set_error("blb_ct_ct_qk: operands must be at the plan level %d", lvl);
             return BLB_E_LEVEL;
         }
-    for (int32_t s : pl->steps)
-        if (!key_for(keys, blb_galois_element(P, s))) {
+    for (int32_t s : pl->steps)  // a step that is a multiple of n is the identity: no key (B > g)
+        if (blb_galois_element(P, s) != 1 && !key_for(keys, blb_galois_element(P, s))) {
             blb_set_error("missing rotation key for step %d", s);
             return BLB_E_MISSING_KEY;
         }
@@ -735,7 +735,8 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
             for (int u = 0; u < G; u++) {
                 const size_t o = (size_t)(u * B + i);
                 u64 *dst = W + w.t + o * 2 * E2 * N;
-                if (i == 0) {
+                // i = 0, and i H_p L a multiple of n (B > g), rotate by the identity: the lift
+                if ((i * pl->Hp * pl->L) % pl->n == 0) {
                     BLB_TRY(launch_lift_ext(P, lvl - 2, W + w.sr + o * ct_k2, dst, st));
                     continue;
                 }

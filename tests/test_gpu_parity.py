@@ -335,7 +335,7 @@ def qktoy():
     return Pair(bi.QKTOY)
 
 
-@pytest.mark.parametrize("H,L,dh,B", [(4, 32, 32, 0), (3, 32, 16, 0), (2, 32, 32, 32)])
+@pytest.mark.parametrize("H,L,dh,B", [(4, 32, 32, 0), (3, 32, 16, 0), (2, 32, 32, 32), (4, 32, 32, 32)])
 def test_qk_ct_ct_bit_exact(qktoy, H, L, dh, B):
     import oracle.matmul_cc as cc
     d = bi.qk_toy_inputs(H, L, dh)
