@@ -1,7 +1,8 @@
-"""NTT throughput microbenchmark (row a1): limb transforms per second at N = 2^16
-for several batch sizes, through the C ABI of a given libblb.so build.
+"""NTT throughput microbenchmark (row a1): limb transforms per second for several batch sizes,
+through the C ABI of a given libblb.so build (SURVEY 8(d) metric 2).
 
-    python tools/bench_ntt.py [--lib path/to/libblb.so] [--rows 64,320,960]
+    python tools/bench_ntt.py [--lib path/to/libblb.so] [--rows 64,320,960] [--logn 16] [--prime i]
+    python tools/bench_ntt.py --sweep      # N = 2^12, 2^14, 2^15, 2^16 x batches {1, 2k, 2(k+a)b, KS batch}
 """
 import argparse
 import ctypes
@@ -23,7 +24,21 @@ def main():
     ap.add_argument("--rows", default="60,300,960,1920")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--prime", type=int, default=-1, help="run every row on this prime index (default: all six)")
+    ap.add_argument("--logn", type=int, default=16)
+    ap.add_argument("--sweep", action="store_true")
     args = ap.parse_args()
+    if args.sweep:
+        # batches: 1 limb, 2k = 10 (a ciphertext), 2 (k + alpha) beta = 60 (one key switch's extended
+        # digits), and a 128-job key-switch batch's ModUp rows (128 x 25 = 3200 -> 3198 = 533 x 6)
+        for logn in (12, 14, 15, 16):
+            for prime, rows in ((1, "1"), (0, "1"), (-1, "12,60,3198")):
+                args.logn, args.prime, args.rows = logn, prime, rows
+                run(args)
+        return
+    run(args)
+
+
+def run(args):
     L = ctypes.CDLL(args.lib)
     vp = ctypes.c_void_p
     L.blb_params_create.argtypes = [vp, ctypes.c_int, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
@@ -33,12 +48,12 @@ def main():
     P = bi.BERT
     bits = list(P.q_bits) + list(P.p_bits)
     pr = (ctypes.c_uint64 * 6)()
-    assert L.blb_prime_chain(P.log_n, (ctypes.c_int * 6)(*bits), 6, pr) == 0
+    assert L.blb_prime_chain(args.logn, (ctypes.c_int * 6)(*bits), 6, pr) == 0
     h = ctypes.c_void_p()
     qa = (ctypes.c_uint64 * 5)(*pr[:5])
     pa = (ctypes.c_uint64 * 1)(pr[5])
-    assert L.blb_params_create(ctypes.byref(h), 16, qa, 5, pa, 1, 5, 0) == 0
-    N = 1 << 16
+    assert L.blb_params_create(ctypes.byref(h), args.logn, qa, 5, pa, 1, 5, 0) == 0
+    N = 1 << args.logn
     res = {}
     st = torch.cuda.current_stream()
     for rows in [int(r) for r in args.rows.split(",")]:
@@ -60,7 +75,8 @@ def main():
             limbs = polys * nl
             res["%s_%d" % (name, limbs)] = {"us": ms * 1e3, "limbs_per_s": limbs / (ms * 1e-3),
                                             "alg_GBps": limbs * 16 * N / (ms * 1e-3) / 1e9}
-    print(json.dumps({"lib": os.path.basename(args.lib), "results": res}))
+    print(json.dumps({"lib": os.path.basename(args.lib), "logN": args.logn,
+                      "prime": "mixed (6 chain primes)" if args.prime < 0 else args.prime, "results": res}))
 
 
 if __name__ == "__main__":
