@@ -314,16 +314,23 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
             if (J.c1_add && (EXT || J.add_mode == 2)) c1v[q] = J.c1_add[(long long)m * N + x];
         }
     }
+    // P c added as one more product in the accumulators (P mod q_m < q_m; one product more than
+    // beta stays inside every accumulator's bound) instead of a Shoup multiply + modular add
+    if (m < k) {
+#pragma unroll
+        for (int q = 0; q < kKsGroup; q++) {
+            if (q < cnt) {
+                accm(a0[q], c0v[q], pq.v[m], qd, qinv);
+                accm(a1[q], c1v[q], pq.v[m], qd, qinv);
+            }
+        }
+    }
 #pragma unroll
     for (int q = 0; q < kKsGroup; q++) {
         if (q < cnt) {
             const int t = t0 + q;
             const KsJob &J = jobs.j[t];
-            u64 r0 = accr(a0[q], mc, qd, qinv), r1 = a1r(q);
-            if (m < k) {
-                r0 = addmod(r0, shoup(c0v[q], pq.v[m], pq.sh[m], mc.q), mc.q);
-                r1 = addmod(r1, shoup(c1v[q], pq.v[m], pq.sh[m], mc.q), mc.q);
-            }
+            const u64 r0 = accr(a0[q], mc, qd, qinv), r1 = a1r(q);
             if (EXT) {
                 J.out[(long long)m * N + dst] = r0;
                 J.out[((long long)E + m) * N + dst] = r1;
@@ -374,10 +381,21 @@ __device__ __forceinline__ void ks_inner_body60(const KsJobs &jobs, const KsGrou
             a0.mac(e[j], kb[j]);
             a1.mac(e[j], ka[j]);
         }
-        u64 r0 = a0.reduce(mc), r1 = a1.reduce(mc);
-        if (m < k) {
-            r0 = addmod(r0, shoup(c0v, pq.v[m], pq.sh[m], mc.q), mc.q);
-            r1 = addmod(r1, shoup(c1v, pq.v[m], pq.sh[m], mc.q), mc.q);
+        u64 r0, r1;
+        if constexpr (BETA <= 6) {  // P c as a 7th product (Acc60 holds <= 7)
+            if (m < k) {
+                a0.mac(c0v, pq.v[m]);
+                a1.mac(c1v, pq.v[m]);
+            }
+            r0 = a0.reduce(mc);
+            r1 = a1.reduce(mc);
+        } else {
+            r0 = a0.reduce(mc);
+            r1 = a1.reduce(mc);
+            if (m < k) {
+                r0 = addmod(r0, shoup(c0v, pq.v[m], pq.sh[m], mc.q), mc.q);
+                r1 = addmod(r1, shoup(c1v, pq.v[m], pq.sh[m], mc.q), mc.q);
+            }
         }
         if (EXT) {
             J.out[(long long)m * N + dst] = r0;
