@@ -644,7 +644,6 @@ blb_status launch_modup(const blb_params *P, int level, const u64 *const *c1_ntt
         fz.pro = 1;
         fz.src = coef;
         fz.src_div = beta;
-        fz.src_q_mode = P->pro_red ? 1 : 0;  // alpha = 1: digit j holds residues mod q_j
         fz.src_hi = (long long)k * N;
         fz.src_lo = N;
         fz.copy_own = 1;
@@ -809,8 +808,6 @@ static blb_status moddown_launch(const blb_params *P, int level, const KsJobs &J
         fz.pro = 1;
         fz.src = u + (long long)k * N;
         fz.src_div = 1;
-        fz.src_q_mode = P->pro_red ? 2 : 0;  // residues mod the special prime
-        fz.src_q_idx = P->K;
         fz.src_hi = (long long)E * N;
         fz.epi = 1;
         fz.u = u;

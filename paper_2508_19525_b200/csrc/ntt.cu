@@ -241,15 +241,11 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
     } else if (PRO == 1) {
         const u64 *src = fz.src + (long long)(p / fz.src_div) * fz.src_hi + (long long)(p % fz.src_div) * fz.src_lo;
         const ModConst &mt = pr.m[pi];
-        const u64 qs = fz.src_q_mode == 1 ? pr.m[p % fz.src_div].q : fz.src_q_mode == 2 ? pr.m[fz.src_q_idx].q : 0;
-        // uniform per CTA: 0 = already reduced, 1 = one conditional subtraction, 2 = Barrett
-        const int red = qs == 0 ? 2 : (qs <= mt.q ? 0 : (qs <= 2 * mt.q ? 1 : 2));
 #pragma unroll
         for (int m = 0; m < 16; m++) {
             const int mid = tcA + 16 * m;
             const size_t addr = STRIDED ? (((size_t)mid << 8) + c0 + colA) : (((size_t)(c0 + colA) << 8) + mid);
-            const u64 x = src[addr];
-            v[m] = from_u64(red == 0 ? x : red == 1 ? (x >= mt.q ? x - mt.q : x) : mod64(x, mt));
+            v[m] = from_u64(mod64(src[addr], mt));
         }
     } else {
 #pragma unroll
