@@ -259,6 +259,7 @@ extern "C" blb_status blb_params_create(blb_params **out, int log_n, const uint6
     if (const char *v = getenv("BLB_NTT_2S")) P->ntt_2s = atoi(v);
     if (const char *v = getenv("BLB_KS_SG")) P->ks_sg = atoi(v);
     if (const char *v = getenv("BLB_MAC_R")) P->mac_r = atoi(v);
+    if (const char *v = getenv("BLB_PRO_RED")) P->pro_red = atoi(v);
     if (const char *v = getenv("BLB_FUSE")) P->fuse = atoi(v);
     if (cudaStreamCreateWithFlags(&P->aux, cudaStreamNonBlocking) != cudaSuccess) P->aux = nullptr;
     for (auto &e : P->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);

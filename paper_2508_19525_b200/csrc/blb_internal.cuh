@@ -307,6 +307,7 @@ struct blb_params {
     int pt_pack = 1;              // 5-byte packed plaintext limbs for primes < 2^40 (env BLB_PT_PACK=0: 8 bytes)
     int mac_r = 0;                // ct-ct K' MAC on rotation-shared blocks of 4 outputs (k_mac_r; env BLB_MAC_R, 0 = k_mac_j)
     int ks_sg = 0;                // key switch: groups per shared-digit chunk (k_ks_inner_sg; env BLB_KS_SG, 0 = off)
+    int pro_red = 1;              // fused ModUp / ModDown prologue: skip moot reductions (env BLB_PRO_RED)
     int ntt_2s = 1;               // two-stream NTT: integer-kernel rows on the auxiliary stream (env BLB_NTT_2S)
     int tsum_acc = 1;             // tensor J-sum accumulators: 1 AccG, 0 Acc41 + AccF64 (env BLB_TSUM_ACC)
     int ks_acc = 4;               // key-switch inner product accumulators (40-bit limbs), see k_ks_inner (env BLB_KS_ACC)
@@ -437,6 +438,12 @@ struct NttFuse {
     const u64 *src = nullptr;
     long long src_hi = 0, src_lo = 0;
     int src_div = 1;
+    // pro = 1, host side: the modulus of source digit j (row p reads digit p % src_div), 0 = unknown.
+    // launch_ntt_fused turns them into per-launch bit masks over j: red0 = already below every target
+    // prime of the launch (no reduction), red1 = below twice it (one conditional subtraction).
+    int src_nq = 0;
+    u64 src_q[8] = {};
+    uint32_t red0 = 0, red1 = 0;
     const u64 *u = nullptr;
     int E = 0, k = 0;
     PinvTab pinv;

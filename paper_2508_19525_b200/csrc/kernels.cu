@@ -644,6 +644,8 @@ blb_status launch_modup(const blb_params *P, int level, const u64 *const *c1_ntt
         fz.pro = 1;
         fz.src = coef;
         fz.src_div = beta;
+        fz.src_nq = beta;  // alpha = 1: digit j holds residues mod q_j
+        for (int j = 0; j < beta && j < 8; j++) fz.src_q[j] = P->mod[j];
         fz.src_hi = (long long)k * N;
         fz.src_lo = N;
         fz.copy_own = 1;
@@ -808,6 +810,8 @@ static blb_status moddown_launch(const blb_params *P, int level, const KsJobs &J
         fz.pro = 1;
         fz.src = u + (long long)k * N;
         fz.src_div = 1;
+        fz.src_nq = 1;  // residues mod the special prime
+        fz.src_q[0] = P->mod[P->K];
         fz.src_hi = (long long)E * N;
         fz.epi = 1;
         fz.u = u;

@@ -1,3 +1,4 @@
+#include <algorithm>
 // ntt.cu -- limb-batched negacyclic NTT / INTT for sm_100a (row a1; C2).
 //
 // NTT(a)[k] = a(psi^{2 brv(k) + 1}) mod q: the in-place Cooley-Tukey network
@@ -241,11 +242,29 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
     } else if (PRO == 1) {
         const u64 *src = fz.src + (long long)(p / fz.src_div) * fz.src_hi + (long long)(p % fz.src_div) * fz.src_lo;
         const ModConst &mt = pr.m[pi];
+        const int dj = p % fz.src_div;
+        if ((fz.red0 >> dj) & 1) {  // digit already below the target prime
 #pragma unroll
-        for (int m = 0; m < 16; m++) {
-            const int mid = tcA + 16 * m;
-            const size_t addr = STRIDED ? (((size_t)mid << 8) + c0 + colA) : (((size_t)(c0 + colA) << 8) + mid);
-            v[m] = from_u64(mod64(src[addr], mt));
+            for (int m = 0; m < 16; m++) {
+                const int mid = tcA + 16 * m;
+                const size_t addr = STRIDED ? (((size_t)mid << 8) + c0 + colA) : (((size_t)(c0 + colA) << 8) + mid);
+                v[m] = from_u64(src[addr]);
+            }
+        } else if ((fz.red1 >> dj) & 1) {  // below twice the target prime
+#pragma unroll
+            for (int m = 0; m < 16; m++) {
+                const int mid = tcA + 16 * m;
+                const size_t addr = STRIDED ? (((size_t)mid << 8) + c0 + colA) : (((size_t)(c0 + colA) << 8) + mid);
+                const u64 x = src[addr];
+                v[m] = from_u64(x >= mt.q ? x - mt.q : x);
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < 16; m++) {
+                const int mid = tcA + 16 * m;
+                const size_t addr = STRIDED ? (((size_t)mid << 8) + c0 + colA) : (((size_t)(c0 + colA) << 8) + mid);
+                v[m] = from_u64(mod64(src[addr], mt));
+            }
         }
     } else {
 #pragma unroll
@@ -572,6 +591,18 @@ blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool invers
         const RowBatch &r = parts[h];
         const cudaStream_t st = ss.part_stream(h);
         dim3 g(16, rb_rows(r));
+        NttFuse fzp = fz;  // this part's reduction masks (pro = 1)
+        fzp.red0 = fzp.red1 = 0;
+        if (!inverse && fz.pro == 1 && P->pro_red && fz.src_nq > 0 && fz.src_nq <= 8) {
+            u64 minq = ~0ull;
+            const int nl = r.nsel ? r.nsel : r.limbs;
+            for (int i = 0; i < nl; i++) minq = std::min<u64>(minq, P->mod[r.prime[r.nsel ? r.sel[i] : i]]);
+            for (int j = 0; j < fz.src_nq; j++) {
+                if (fz.src_q[j] == 0) continue;
+                if (fz.src_q[j] <= minq) fzp.red0 |= 1u << j;
+                else if (fz.src_q[j] / 2 < minq) fzp.red1 |= 1u << j;  // q_j <= 2 minq - 1 (odd primes)
+            }
+        }
         if (inverse) {  // pro = 2: first (contiguous) pass loads from the pointer table
             if (rb_small(P, r)) {
                 ntt16_f64<true, false, 2, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 0, fz);
@@ -583,12 +614,12 @@ blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool invers
             continue;
         }
         if (rb_small(P, r)) {
-            if (fz.pro == 1) ntt16_f64<false, true, 1, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
+            if (fz.pro == 1) ntt16_f64<false, true, 1, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fzp);
             else ntt16_f64<false, true, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
             if (fz.epi == 1) ntt16_f64<false, false, 0, 1><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
             else ntt16_f64<false, false, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
         } else {
-            if (fz.pro == 1) ntt16_int<false, true, 1, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
+            if (fz.pro == 1) ntt16_int<false, true, 1, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fzp);
             else ntt16_int<false, true, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
             if (fz.epi == 1) ntt16_int<false, false, 0, 1><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
             else ntt16_int<false, false, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
