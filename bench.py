@@ -33,12 +33,9 @@ import numpy as np  # noqa: E402
 import blb_inputs as bi  # noqa: E402
 
 METRIC = "ms per BERT-base layer fused-linear CKKS eval"
-# BSGS baby-step counts B per ct-pt MatMul (C11, plan parameter S15); shared by both arms
-BSGS = {"qkv": 64, "oproj": 16, "ffn1": 64, "ffn2": 16}
-# tuning override, e.g. BLB_BSGS=qkv:32,ffn1:128 (each plan is parity-tested at any B by the toy tests)
-for _kv in filter(None, os.environ.get("BLB_BSGS", "").split(",")):
-    _k, _v = _kv.split(":")
-    BSGS[_k] = int(_v)
+# BSGS baby-step counts B per MatMul (C11, plan parameter S15); shared by both arms and by the
+# full-size parity tests (tests/test_gpu_bert.py imports the same dict)
+BSGS = dict(bi.BENCH_BSGS)
 UNIT = "ms"
 FALLBACK_HBM = 6650.0
 

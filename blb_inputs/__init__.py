@@ -77,6 +77,11 @@ def toy_inputs():
 # ---- config 2: BERT-base attention (QKV + Q K^T) --------------------------
 BERT_BASE = dict(L=128, d=768, H=12, ffn=3072)
 BERT_LARGE = dict(L=128, d=1024, H=16, ffn=4096)
+GPT2_BASE = dict(L=128, d=768, H=12, ffn=3072)
+# BSGS baby-step counts B of the layer plans bench.py times (C11 plan parameter, reading S15;
+# 0 = the ct-ct default B = g).  A workload parameter, not arithmetic: bench.py and the
+# full-size parity tests (tests/test_gpu_bert.py) both read it, so they cannot drift apart.
+BENCH_BSGS = {"qkv": 64, "oproj": 16, "ffn1": 64, "ffn2": 16, "qk": 0}
 
 
 def bert_attention_inputs(L=128, d=768, config_id=2):

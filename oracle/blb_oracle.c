@@ -830,19 +830,27 @@ void orc_moddown_rescale(const orc_ctx *c, const u64 *in, int lvl, u64 *out) {
             memcpy(drop + (u64)t * N, x + (u64)(lvl + t) * N, N * sizeof(u64));  /* limbs lvl, k.. are q_lvl, P */
             intt_limb(c, drop + (u64)t * N, mi[t]);
         }
+        /* per-(s, t) inverses m_s^{-1} mod m_t and per-limb (M - 1)/2 mod q_i: constants of the loop */
+        u64 minv[ORC_MAXP][ORC_MAXP], hq[ORC_MAXP];
+        for (int t = 0; t < nd; t++)
+            for (int s = 0; s < t; s++) minv[t][s] = invmod(m[s] % m[t], m[t]);
+        for (int i = 0; i < lvl; i++) {
+            u64 q = c->mod[i], Mq = 1;
+            for (int t = 0; t < nd; t++) Mq = mulmod(Mq, m[t] % q, q);
+            hq[i] = mulmod(submod(Mq, 1, q), invmod(2, q), q);   /* (M - 1) / 2 mod q_i */
+        }
+#pragma omp parallel for
         for (u64 j = 0; j < N; j++) {
             u64 d[ORC_MAXP];
             for (int t = 0; t < nd; t++) {
                 u64 v = addmod(drop[(u64)t * N + j], (m[t] - 1) / 2, m[t]);  /* h = -1/2 mod m_t */
-                for (int s = 0; s < t; s++) v = mulmod(submod(v, d[s] % m[t], m[t]), invmod(m[s] % m[t], m[t]), m[t]);
+                for (int s = 0; s < t; s++) v = mulmod(submod(v, d[s] % m[t], m[t]), minv[t][s], m[t]);
                 d[t] = v;
             }
             for (int i = 0; i < lvl; i++) {
-                u64 q = c->mod[i], r = 0, Mq = 1;
+                u64 q = c->mod[i], r = 0;
                 for (int t = nd - 1; t >= 0; t--) r = addmod(mulmod(r, m[t] % q, q), d[t] % q, q);
-                for (int t = 0; t < nd; t++) Mq = mulmod(Mq, m[t] % q, q);
-                u64 h = mulmod(submod(Mq, 1, q), invmod(2, q), q);   /* (M - 1) / 2 mod q_i */
-                w[(u64)i * N + j] = submod(h, r, q);
+                w[(u64)i * N + j] = submod(hq[i], r, q);
             }
         }
         for (int i = 0; i < lvl; i++) {

@@ -217,10 +217,18 @@ def slot_level(Qz: list[np.ndarray], Kz: list[np.ndarray], plan: QKPlan) -> list
     return outs
 
 
-def qk_encrypted(ctx: Ctx, keys: Keys, Q: list[Ct], K: list[Ct], plan: QKPlan) -> list[Ct]:
-    """Evaluate the schedule on ciphertexts (all inputs at one level l >= 3)."""
+def qk_encrypted(ctx: Ctx, keys: Keys, Q: list[Ct], K: list[Ct], plan: QKPlan, out_ids=None) -> list[Ct]:
+    """Evaluate the schedule on ciphertexts (all inputs at one level l >= 3).
+
+    out_ids (optional): compute only these output ciphertexts (sampled parity at full size).  The
+    schedule of each computed output is unchanged; only the giant steps u and step-3 accumulators
+    that feed no requested output are skipped (every K'_i is still needed by every output)."""
     lvl = Q[0].level
     assert lvl >= 3 and all(c.level == lvl for c in Q + K)
+    accs = plan.accumulators()
+    if out_ids is not None:
+        accs = [a for a in accs if plan.out_index(a[0], a[1]) in set(out_ids)]
+    need_u = sorted({u for u, w, f in accs})
 
     def drop(ct: Ct) -> Ct:   # exact level drop (C9): keep limbs 0..level-1
         return Ct(ct.data[:, : ct.level].copy(), ct.level - 1, ct.scale)
@@ -252,7 +260,9 @@ def qk_encrypted(ctx: Ctx, keys: Keys, Q: list[Ct], K: list[Ct], plan: QKPlan) -
     Qu = {}
     for j in range(plan.J):
         Qu[(0, j)] = drop(Q[j])
-        for u in range(1, plan.G):
+        for u in need_u:
+            if u == 0:
+                continue
             a = u * plan.B
             t1 = O.mul_pt_ext(ctx, O.rotate_ext(ctx, Q[j], keys, -a), pt1(("q", u, False), plan.mask_q(u, False)), s1)
             t2 = O.mul_pt_ext(ctx, O.rotate_ext(ctx, Q[j], keys, plan.L - a),
@@ -260,7 +270,7 @@ def qk_encrypted(ctx: Ctx, keys: Keys, Q: list[Ct], K: list[Ct], plan: QKPlan) -
             Qu[(u, j)] = O.moddown_rescale(ctx, O.add_ext(ctx, t1, t2))
     # products, relinearisation (once per (u, i), lazy over j: reading S10), rescale -> lvl-2
     T = {}
-    for u in range(plan.G):
+    for u in need_u:
         for i in range(plan.B):
             d = None
             for j in range(plan.J):
@@ -274,7 +284,7 @@ def qk_encrypted(ctx: Ctx, keys: Keys, Q: list[Ct], K: list[Ct], plan: QKPlan) -
     l3 = lvl - 2
     s3 = float(ctx.q[l3])
     outs = [None] * plan.n_out
-    for u, w, f in plan.accumulators():
+    for u, w, f in accs:
         A = None
         for i in range(plan.B):
             m = plan.mask3(u, i, w, f)
@@ -286,6 +296,8 @@ def qk_encrypted(ctx: Ctx, keys: Keys, Q: list[Ct], K: list[Ct], plan: QKPlan) -
         Ae = O.rotate_ext(ctx, A, keys, plan.final_rot(u, f) % plan.n)
         o = plan.out_index(u, w)
         outs[o] = Ae if outs[o] is None else O.add_ext(ctx, outs[o], Ae)
+    if out_ids is not None:
+        return [O.moddown_ct(ctx, outs[o]) for o in out_ids]
     return [O.moddown_ct(ctx, e) for e in outs]
 
 

@@ -42,7 +42,17 @@ class Dims:
 BERT_BASE = Dims()
 BERT_LARGE = Dims(128, 1024, 16, 4096)
 BSGS = {"qkv": 64, "oproj": 16, "ffn1": 64, "ffn2": 16, "qk": 0}
-PLAN_ID = {"qkv": 0, "oproj": 1, "ffn1": 2, "ffn2": 3, "qk": 4}
+# mask object ids (reading C19): id = seq * 2^24 + block * 2^16 + output, so every
+# conversion of every inference draws a fresh mask (Alg. 1 line 1; Theorem 1)
+MASK_BLOCK = {"qkv": 0, "oproj": 1, "ffn1": 2, "ffn2": 3, "qk": 4}
+MAX_OUT = 1 << 16
+MAX_SEQ = 1 << 32
+
+
+def mask_id(seq: int, block: str, o: int) -> int:
+    if not (0 <= o < MAX_OUT and 0 <= seq < MAX_SEQ):
+        raise ValueError("mask id out of range: seq %d, output %d" % (seq, o))
+    return (seq << 24) | (MASK_BLOCK[block] << 16) | o
 
 
 def shard(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -103,7 +113,11 @@ class FusedLinearLayer:
         self.slices["qk"] = shard(self.qk.n_out, rank, world)
         # Softmax x V (row f1): inner dimension L (V zero-padded d_h -> L), replicated like Q K^T
         self.sv = blb.QKPlan(params, L, H, L, bsgs_B=b["qk"], level=self.level)
+        for name, n in [(k, pl.n_out) for k, pl in self.plans.items()] + [("qk", self.qk.n_out)]:
+            if n > MAX_OUT:
+                raise ValueError("%s: %d output ciphertexts exceed the mask-id range" % (name, n))
         self.pts, self.ws, self.outs = {}, None, {}
+        self.seq = 0      # inference counter: enters every mask id (fresh masks per step)
 
     # ---- setup (row a0) ----
     def rotation_steps(self) -> list[int]:
@@ -151,15 +165,17 @@ class FusedLinearLayer:
             out.append(len([o for o in range(f, f + c) if o >= lo]))
         return out
 
-    def mask_ids(self, name: str) -> list[int]:
-        """Global ciphertext ids of the masked outputs of this rank (PRNG key, C4)."""
+    def mask_outputs(self, name: str) -> list[int]:
+        """Plan output indices of the masked outputs of this rank."""
         first, count = self.slices[name]
-        if name == "qk":
-            return [PLAN_ID[name] * 1024 + o for o in range(first, first + count)]
         outs = range(first, first + count)
         if name == "qkv":   # only V is converted here; Q, K feed Q K^T (row a7)
             outs = [o for o in outs if o >= 2 * self.n_mhp]
-        return [PLAN_ID[name] * 1024 + o for o in outs]
+        return list(outs)
+
+    def mask_ids(self, name: str, seq: int) -> list[int]:
+        """Global mask object ids of this rank's masked outputs in inference seq (C4, C19)."""
+        return [mask_id(seq, name, o) for o in self.mask_outputs(name)]
 
     # ---- the hot path ----
     def gather_qk_operands(self, outs: list):
@@ -182,9 +198,13 @@ class FusedLinearLayer:
             blb.add_into(self.p, outs[o], outs[o + half], self.sv_dense[o])
         return self.sv_dense
 
-    def step(self, keys: blb.Keys, inputs: dict, mask_key: bytes) -> list:
+    def step(self, keys: blb.Keys, inputs: dict, mask_key: bytes, seq: int | None = None) -> list:
         """inputs: {'qkv': [ct]*3, 'sv_s': [ct]*J', 'sv_v': [ct]*J', 'ffn1': [...], 'ffn2': [...]}
-        -> [(name, first mask id, (masked, share))] per block."""
+        -> [(name, first mask id, (masked, share))] per block.  seq: the inference number entering the
+        mask ids (default: the layer's own counter, incremented per call, so masks are never reused)."""
+        if seq is None:
+            seq = self.seq
+        self.seq = seq + 1
         res = []
         for name in ("qkv", "oproj", "ffn1", "ffn2"):
             first, count = self.slices[name]
@@ -199,12 +219,12 @@ class FusedLinearLayer:
                 qk_out = self.qk(keys, qk_in[:J], qk_in[J:2 * J], self.qk_masks, ws=self.ws, outs=self.outs["qk"])
                 qf, qc = self.slices["qk"]
                 if qc:
-                    ids = self.mask_ids("qk")
+                    ids = self.mask_ids("qk", seq)
                     res.append(("qk", ids[0], blb.ckks_to_mpc(self.p, qk_out[qf:qf + qc], mask_key, ids[0])))
-            ids = self.mask_ids(name)
+            ids = self.mask_ids(name, seq)
             if not ids:
                 continue
-            sel = [outs[i - PLAN_ID[name] * 1024 - first] for i in ids]
+            sel = [outs[o - first] for o in self.mask_outputs(name)]
             # ids of one block are contiguous: one mask launch per block
             res.append((name, ids[0], blb.ckks_to_mpc(self.p, sel, mask_key, ids[0])))
         return res
@@ -233,7 +253,7 @@ class LayerPipeline:
         self.host_out = [None, None]
         self.k = 0
 
-    def submit(self, host_inputs: dict, gather=None) -> list:
+    def submit(self, host_inputs: dict, gather=None, seq: int | None = None) -> list:
         """Enqueue one step; returns the pinned host buffers its results land in (valid after sync)."""
         s = self.k % 2
         comp = torch.cuda.current_stream()
@@ -245,7 +265,7 @@ class LayerPipeline:
                     c.data.copy_(h, non_blocking=True)
             self.ready[s].record(self.up)
         comp.wait_event(self.ready[s])
-        res = self.layer.step(self.keys, self.dev[s], self.mask_key)
+        res = self.layer.step(self.keys, self.dev[s], self.mask_key, seq)
         if gather is not None:
             res = gather(res)
         self.free[s].record(comp)

@@ -1,109 +1,218 @@
-"""Full-size parity (BASELINE configs 2/3 at N = 2^16, the launch configuration
-bench.py times): the GPU computes every output ciphertext of the BERT-base QKV
-(C11 + MHP) and out-projection (C12) MatMuls; the oracle recomputes sampled
-output ciphertexts one by one and they must agree bit-exactly on every limb.
-Slow (the oracle runs 2^16-point NTTs in u128 C on the host)."""
+"""Full-size parity in the launch configuration bench.py times (BASELINE configs 2/3 at
+N = 2^16, the BSGS splits of blb_inputs.BENCH_BSGS, the plan objects of the benched
+layer.FusedLinearLayer): the GPU evaluates every output ciphertext, the oracle recomputes
+sampled output ciphertexts one by one, and they must agree bit-exactly on every limb.
+
+* QKV (C11 + MHP, B = 64): a Q output and a V output; the V output also through the layer
+  step's CKKS->MPC mask (masked ciphertext and server share);
+* FFN1 (B = 64) and FFN2 (12 inputs, B = 16): one output each, through the layer step's mask;
+* out-projection (C12, diagonal input with padded heads, B = 16) at level 1, where the layer
+  runs it;
+* Q K^T at the BERT-base shape (H = 12 -> H_p = 16, d_h = 64: g = 16, J = 4) at level 3;
+* Softmax x V (V zero-padded to L = 128: J = 8) at level 4.
+
+Inputs to every oracle call are fresh oracle encryptions of seeded synthetic data (never GPU
+outputs); the GPU side encrypts the same messages with the same ids (bit-exact encryption is
+pinned by test_gpu_parity).  Slow: the oracle runs 2^16-point u128 NTTs on the host."""
 import numpy as np
 import pytest
 import torch
 
 import blb_inputs as bi
 import oracle as O
+import oracle.layer as OL
 import oracle.matmul as mm
+import oracle.matmul_cc as cc
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 blb = pytest.importorskip("paper_2508_19525_b200")
 from paper_2508_19525_b200 import packing  # noqa: E402
+from paper_2508_19525_b200.layer import Dims, FusedLinearLayer  # noqa: E402
+
+DIMS = bi.BERT_BASE
+L, D, H, FFN = DIMS["L"], DIMS["d"], DIMS["H"], DIMS["ffn"]
+DELTA = 2.0 ** 40
+SEQ = 7
+
+
+class Okeys:
+    """Oracle rotation keys generated on demand (key material depends only on (seed, step))."""
+
+    def __init__(self, ctx, key):
+        self.ctx, self.key, self.keys = ctx, key, None
+
+    def get(self, steps, relin=False):
+        have = set(self.keys.rot) if self.keys else set()
+        need = [s for s in steps if self.ctx.galois(s) not in have]
+        want_rlk = relin and (self.keys is None or self.keys.rlk is None)
+        if self.keys is None or need or want_rlk:
+            k = O.keygen(self.ctx, self.key, need, relin=want_rlk)
+            if self.keys is None:
+                self.keys = k
+            else:
+                self.keys.rot.update(k.rot)
+                if k.rlk is not None:
+                    self.keys.rlk = k.rlk
+        return self.keys
 
 
 @pytest.fixture(scope="module")
 def bert():
     P = bi.BERT
     pr = O.prime_chain(P.log_n, list(P.q_bits) + list(P.p_bits))
-    return O.Ctx(P.log_n, pr[:5], pr[5:], P.dnum), blb.Params(P.log_n, pr[:5], pr[5:], P.dnum)
+    ctx = O.Ctx(P.log_n, pr[:5], pr[5:], P.dnum)
+    params = blb.Params.from_preset(P)
+    layer = FusedLinearLayer(params, Dims(**DIMS), bsgs=bi.BENCH_BSGS)
+    A = bi.bert_attention_inputs(L, D)
+    F = bi.bert_ffn_inputs(L, D, H, FFN)
+    keys_key = A["keys_key"]
+    gkeys, sk = blb.keygen(params, keys_key, layer.rotation_steps(), relin=True)
+    layer.load_weights(A["WQ"], A["WK"], A["WV"], F["WO"], F["W1"], F["W2"])
+    return dict(ctx=ctx, params=params, layer=layer, A=A, F=F, gkeys=gkeys, sk=sk, okeys=Okeys(ctx, keys_key))
 
 
-def run(octx, g, plan_o, plan_g, zs, W, sample):
-    lvl, delta = 4, 2.0 ** 40
-    key, ekey = bi.crypto_key(4, 2), bi.crypto_key(5, 2)
-    steps = plan_g.rotation_steps()
-    assert steps == plan_o.rotation_steps()
-    okeys = O.keygen(octx, key, steps)
-    gkeys, sk = blb.keygen(g, key, steps)
+def encrypt_both(b, zs, level, id0, enc_key):
+    ctx, params, okeys = b["ctx"], b["params"], b["okeys"]
     octs, gcts = [], []
-    for b, z in enumerate(zs):
-        pt = O.encode(octx, z, delta, lvl)
-        octs.append(O.encrypt(octx, ekey, okeys.s_ntt, pt, lvl, b, delta))
-        gcts.append(blb.encrypt(g, sk, g.encode(torch.tensor(z), delta, lvl), lvl, ekey, b, delta))
+    s_ntt = okeys.get([]).s_ntt
+    for t, z in enumerate(zs):
+        pt = O.encode(ctx, z, DELTA, level)
+        octs.append(O.encrypt(ctx, enc_key, s_ntt, pt, level, id0 + t, DELTA))
+        gcts.append(blb.encrypt(params, b["sk"], params.encode(torch.tensor(z), DELTA, level), level, enc_key,
+                                id0 + t, DELTA))
         assert np.array_equal(blb.to_numpy_u64(gcts[-1].data), octs[-1].data)
-    pts = plan_g.encode_weights(W)
-    gout = plan_g(gkeys, gcts, pts)
-    oout = mm.matmul_cp(octx, okeys, octs, plan_o, out_ids=sample)
+    return octs, gcts
+
+
+def same(g, o):
+    assert g.level == o.level and g.scale == o.scale
+    return np.array_equal(blb.to_numpy_u64(g.data), o.data)
+
+
+def layer_inputs(b):
+    """The bench step's encrypted inputs: both sides, same messages and ids."""
+    if "inputs" in b:
+        return b["inputs"]
+    A, F, layer, ctx = b["A"], b["F"], b["layer"], b["ctx"]
+    # client-side slot layouts from the oracle's packers (the product's packing.py must agree)
+    sv = cc.plan_sv(L, H, ctx.n)
+    S_, Kop = cc.sv_operands(F["S"], F["V"])
+    slots = {"qkv": mm.pack_spatial(A["X"], ctx.n), "sv_s": cc.pack_mhp(S_, sv), "sv_v": cc.pack_mhp(Kop, sv),
+             "ffn1": mm.pack_spatial(F["X2"], ctx.n), "ffn2": mm.pack_spatial(F["H1"], ctx.n)}
+    ps, pv = packing.softmax_v_operands(F["S"], F["V"], ctx.n)
+    assert np.array_equal(np.stack(slots["sv_s"]), ps) and np.array_equal(np.stack(slots["sv_v"]), pv)
+    assert np.array_equal(np.stack(slots["qkv"]), packing.spatial_slots(A["X"], ctx.n))
+    o_in, g_in, cid = {}, {}, 4096
+    for name, zs in slots.items():
+        o_in[name], g_in[name] = encrypt_both(b, list(zs), layer.level, cid, A["enc_key"])
+        cid += len(zs)
+    b["inputs"] = (o_in, g_in)
+    b["step"] = {name: (id0, m, s) for name, id0, (m, s) in layer.step(b["gkeys"], g_in, A["mask_key"], seq=SEQ)}
+    return b["inputs"]
+
+
+def check_masked(b, name, o, oct_out):
+    """Layer-step mask of output o of block name == oracle mask of the oracle's output."""
+    id0, m, s = b["step"][name]
+    first = b["layer"].mask_outputs(name)[0]
+    om, osh = O.mask(b["ctx"], oct_out, b["A"]["mask_key"], OL.mask_id(SEQ, name, o))
+    assert id0 == OL.mask_id(SEQ, name, first)
+    assert np.array_equal(blb.to_numpy_u64(m[o - first]), om)
+    assert np.array_equal(blb.to_numpy_u64(s[o - first]), osh)
+
+
+def test_bench_plans_are_the_tested_plans(bert):
+    """The layer bench.py times uses BENCH_BSGS; the oracle plans built from the same dict
+    have the same rotation sets and plaintext counts (QKV 8448 / FFN 9216 / O-proj 2304)."""
+    layer, ctx, F, A = bert["layer"], bert["ctx"], bert["F"], bert["A"]
+    spec = OL.build(ctx, OL.LayerSpec(L, D, H, FFN, bi.BENCH_BSGS, layer.level), A["WQ"], A["WK"], A["WV"],
+                    F["WO"], F["W1"], F["W2"])
+    assert OL.rotation_steps(spec) == layer.rotation_steps()
+    for name in ("qkv", "oproj", "ffn1", "ffn2"):
+        pg, po = layer.plans[name], spec.plans[name]
+        assert pg.n_pt == po.n_plaintexts and pg.n_rotations == po.n_rotations, name
+        assert pg.rotation_steps() == po.rotation_steps(), name
+    assert (layer.plans["qkv"].n_pt, layer.plans["ffn1"].n_pt, layer.plans["ffn2"].n_pt,
+            layer.plans["oproj"].n_pt) == (8448, 9216, 9216, 2304)
+    assert layer.qk.rotation_steps() == spec.plans["qk"].rotation_steps()
+    assert layer.sv.rotation_steps() == spec.plans["sv"].rotation_steps()
+    assert (spec.plans["qk"].J, spec.plans["sv"].J) == (4, 8)
+
+
+def test_qkv_b64_sampled_outputs_bit_exact(bert):
+    """QKV at B = 64: output 0 (Q, MHP) straight from the plan, output 9 (V) through the layer mask."""
+    o_in, g_in = layer_inputs(bert)
+    ctx, layer = bert["ctx"], bert["layer"]
+    A = bert["A"]
+    spec = OL.build(ctx, OL.LayerSpec(L, D, H, FFN, bi.BENCH_BSGS, layer.level), A["WQ"], A["WK"], A["WV"],
+                    bert["F"]["WO"], bert["F"]["W1"], bert["F"]["W2"])
+    plan_o = spec.plans["qkv"]
+    okeys = bert["okeys"].get(plan_o.rotation_steps())
+    sample = [0, 9]
+    oout = mm.matmul_cp(ctx, okeys, o_in["qkv"], plan_o, out_ids=sample)
+    gout = layer.plans["qkv"](bert["gkeys"], g_in["qkv"], layer.pts["qkv"])
     for o, ref in zip(sample, oout):
-        assert gout[o].level == ref.level == lvl - 1 and gout[o].scale == ref.scale
-        assert np.array_equal(blb.to_numpy_u64(gout[o].data), ref.data), o
-    return gout, sk
+        assert same(gout[o], ref), o
+    check_masked(bert, "qkv", 9, oout[1])
 
 
-def test_bert_qkv_sampled_outputs_bit_exact(bert):
-    octx, g = bert
-    A = bi.bert_attention_inputs()
-    L, d, H = 128, 768, 12
-    cm = blb.mhp_column_map(d, H, L, 16)
-    qkv_map = cm + [d + c if c >= 0 else -1 for c in cm] + list(range(2 * d, 3 * d))
-    W = np.concatenate([A["WQ"], A["WK"], A["WV"]], axis=1)
-    plan_g = blb.MatmulPlan(g, L, d, 3 * d, col_map=qkv_map, bsgs_B=32, level=4)
-    plan_o = mm.plan_spatial(W, L, octx.n, 32, col_map=qkv_map)
-    assert (plan_g.n_pt, plan_g.n_rotations) == (plan_o.n_plaintexts, plan_o.n_rotations) == (8448, 170)
-    zs = list(packing.spatial_slots(A["X"], octx.n))
-    gout, sk = run(octx, g, plan_o, plan_g, zs, W, sample=[0, 10])
-    # every output decodes to X W (float64) within the paper's MSE bound
-    Y = np.concatenate([packing.spatial_unslots(g.decode(blb.decrypt(g, sk, o), o.scale).cpu().numpy()[None], L, 256)
-                        for o in gout], axis=1)
-    ref = A["X"] @ W
-    full = np.zeros((L, len(qkv_map)))
-    for v, src in enumerate(qkv_map):
-        if src >= 0:
-            full[:, v] = ref[:, src]
-    assert float(((Y[:, :len(qkv_map)] - full) ** 2).mean()) <= 1e-11
+@pytest.mark.parametrize("name,o", [("ffn1", 5), ("ffn2", 1)])
+def test_ffn_sampled_output_through_layer_mask(bert, name, o):
+    o_in, _ = layer_inputs(bert)
+    ctx, layer, F = bert["ctx"], bert["layer"], bert["F"]
+    W = F["W1"] if name == "ffn1" else F["W2"]
+    plan_o = mm.plan_spatial(W, L, ctx.n, bi.BENCH_BSGS[name])
+    assert plan_o.n_plaintexts == layer.plans[name].n_pt
+    okeys = bert["okeys"].get(plan_o.rotation_steps())
+    (ref,) = mm.matmul_cp(ctx, okeys, o_in[name], plan_o, out_ids=[o])
+    check_masked(bert, name, o, ref)
 
 
-def test_bert_oproj_diagonal_sampled_output_bit_exact(bert):
-    octx, g = bert
-    F = bi.bert_ffn_inputs()
-    L, d, H = 128, 768, 12
-    plan_g = blb.MatmulPlan(g, L, d, d, packing=blb.PACK_DIAGONAL, heads=H, bsgs_B=16, level=4)
-    plan_o = mm.plan_diagonal(F["WO"], H, L, octx.n, 16)
-    assert (plan_g.n_pt, plan_g.n_rotations) == (plan_o.n_plaintexts, plan_o.n_rotations) == (2304, 90)
-    zs = list(packing.diagonal_slots(F["Att"], octx.n))
-    run(octx, g, plan_o, plan_g, zs, F["WO"], sample=[2])
+def test_oproj_level1_sampled_output_bit_exact(bert):
+    """Diagonal-input W_O (C12) with padded heads at level 1, as the layer runs it."""
+    ctx, layer, F = bert["ctx"], bert["layer"], bert["F"]
+    lvl = layer.level - 3
+    Hp = layer.Hp
+    Att = np.zeros((Hp, L, D // H))
+    Att[:H] = F["Att"]
+    zs = mm.pack_diagonal_mh(Att, ctx.n)
+    octs, gcts = encrypt_both(bert, zs, lvl, 900, bi.crypto_key(5, 33))
+    plan_o = mm.plan_diagonal(cc.pad_heads_rows(F["WO"], H, Hp), Hp, L, ctx.n, bi.BENCH_BSGS["oproj"])
+    okeys = bert["okeys"].get(plan_o.rotation_steps())
+    (ref,) = mm.matmul_cp(ctx, okeys, octs, plan_o, out_ids=[2])
+    gout = layer.plans["oproj"](bert["gkeys"], gcts, layer.pts["oproj"])
+    assert ref.level == 0 and same(gout[2], ref)
 
 
-def test_bert_size_qk_bit_exact(bert):
-    """Row a7 at N = 2^16, L = 128 (16 heads of d_h = 8: g = 16, J = 1, B = 16, G = 8): the
-    double-hoisted stage 1, relinearisation, step-3 rotations and deferred giant step on the
-    fused N = 2^16 kernels, bit-exact against the oracle."""
-    import oracle.matmul_cc as cc
-    octx, g = bert
-    L, H, dh = 128, 16, 8
+def test_qk_bert_base_shape_sampled_output_bit_exact(bert):
+    """Row a7 at the benched shape: H = 12 (padded to 16), d_h = 64, g = 16, J = 4, B = 16, level 3."""
+    ctx, layer = bert["ctx"], bert["layer"]
     rng = np.random.default_rng(5)
-    Q, K = rng.uniform(-1, 1, (H, L, dh)), rng.uniform(-1, 1, (H, L, dh))
-    plan_o = cc.plan_qk(L, H, dh, octx.n)
-    plan_g = blb.QKPlan(g, L, H, dh, level=3)
-    assert plan_g.rotation_steps() == plan_o.rotation_steps()
-    key, ekey = bi.crypto_key(4, 3), bi.crypto_key(5, 3)
-    steps = plan_g.rotation_steps()
-    okeys = O.keygen(octx, key, steps, relin=True)
-    gkeys, sk = blb.keygen(g, key, steps, relin=True)
-    lvl, delta = 3, 2.0 ** 40
-    oq, ok, gq, gk = [], [], [], []
-    for j, (zq, zk) in enumerate(zip(cc.pack_mhp(Q, plan_o), cc.pack_mhp(K, plan_o))):
-        for z, cid, ol, gl in ((zq, j, oq, gq), (zk, 10 + j, ok, gk)):
-            pt = O.encode(octx, z, delta, lvl)
-            ol.append(O.encrypt(octx, ekey, okeys.s_ntt, pt, lvl, cid, delta))
-            gl.append(blb.encrypt(g, sk, blb.from_numpy_u64(pt), lvl, ekey, cid, delta))
-    gout = plan_g(gkeys, gq, gk, plan_g.encode_masks())
-    oout = cc.qk_encrypted(octx, okeys, oq, ok, plan_o)
-    for a, b in zip(gout, oout):
-        assert a.scale == b.scale and np.array_equal(blb.to_numpy_u64(a.data), b.data)
+    Q, K = rng.normal(0, 1, (H, L, D // H)) / 8, rng.normal(0, 1, (H, L, D // H)) / 8
+    plan_o = cc.plan_qk(L, H, D // H, ctx.n)
+    assert (plan_o.J, plan_o.g, plan_o.B) == (4, 16, 16)
+    lvl = layer.level - 1
+    oq, gq = encrypt_both(bert, cc.pack_mhp(Q, plan_o), lvl, 700, bi.crypto_key(5, 34))
+    ok, gk = encrypt_both(bert, cc.pack_mhp(K, plan_o), lvl, 710, bi.crypto_key(5, 34))
+    okeys = bert["okeys"].get(plan_o.rotation_steps(), relin=True)
+    o = 3
+    (ref,) = cc.qk_encrypted(ctx, okeys, oq, ok, plan_o, out_ids=[o])
+    gout = layer.qk(bert["gkeys"], gq, gk, layer.qk_masks, ws=layer.ws)
+    assert len(gout) == plan_o.n_out and same(gout[o], ref)
+
+
+def test_softmax_v_j8_sampled_output_bit_exact(bert):
+    """Row f1 at the benched shape: S_h (x) Vpad_h^T with d_h padded to L = 128 (J = 8), level 4."""
+    ctx, layer, F = bert["ctx"], bert["layer"], bert["F"]
+    plan_o = cc.plan_sv(L, H, ctx.n)
+    assert plan_o.J == 8
+    A_, Kop = cc.sv_operands(F["S"], F["V"])
+    lvl = layer.level
+    os_, gs = encrypt_both(bert, cc.pack_mhp(A_, plan_o), lvl, 800, bi.crypto_key(5, 35))
+    ov, gv = encrypt_both(bert, cc.pack_mhp(Kop, plan_o), lvl, 820, bi.crypto_key(5, 35))
+    okeys = bert["okeys"].get(plan_o.rotation_steps(), relin=True)
+    o = 5
+    (ref,) = cc.qk_encrypted(ctx, okeys, os_, ov, plan_o, out_ids=[o])
+    gout = layer.sv(bert["gkeys"], gs, gv, layer.sv_masks, ws=layer.ws)
+    assert len(gout) == plan_o.n_out and same(gout[o], ref)

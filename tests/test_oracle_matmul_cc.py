@@ -122,3 +122,21 @@ def test_table5_softmax_v_counts():
     cnt = p.counts()
     assert cnt["cmult"] == 2048 == 128 ** 3 * 16 // 16384
     assert cnt["rotations"] <= 2 * 1056
+
+
+def test_sampled_outputs_equal_full_schedule(qktoy):
+    """qk_encrypted(out_ids=...) (used for sampled parity at N = 2^16) returns exactly the
+    ciphertexts the full schedule computes for those outputs."""
+    d = bi.qk_toy_inputs(H=4, L=32, dh=16)
+    plan = cc.plan_qk(32, 4, 16, qktoy.n)
+    keys = O.keygen(qktoy, d["keys_key"], plan.rotation_steps(), relin=True)
+    lvl, delta = 3, 2.0 ** 40
+    Q = [O.encrypt(qktoy, d["enc_key"], keys.s_ntt, O.encode(qktoy, z, delta, lvl), lvl, j, delta)
+         for j, z in enumerate(cc.pack_mhp(d["Q"], plan))]
+    K = [O.encrypt(qktoy, d["enc_key"], keys.s_ntt, O.encode(qktoy, z, delta, lvl), lvl, 10 + j, delta)
+         for j, z in enumerate(cc.pack_mhp(d["K"], plan))]
+    full = cc.qk_encrypted(qktoy, keys, Q, K, plan)
+    sample = [plan.n_out - 1, 0]
+    part = cc.qk_encrypted(qktoy, keys, Q, K, plan, out_ids=sample)
+    for o, ct in zip(sample, part):
+        assert np.array_equal(ct.data, full[o].data) and ct.scale == full[o].scale
