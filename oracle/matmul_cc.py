@@ -111,7 +111,8 @@ class QKPlan:
 
     def rotation_steps(self) -> list[int]:
         s = set(self.k_rots) | set(self.q_rots)
-        s |= {-i * self.Hp * self.L for i in range(1, self.B)}
+        # step-3 rotations by a multiple of n slots are the identity sigma_1 (no key, C13)
+        s |= {-i * self.Hp * self.L for i in range(1, self.B) if (i * self.Hp * self.L) % self.n}
         for u, w, f in self.accumulators():
             r = self.final_rot(u, f)
             if r % self.n:
@@ -122,7 +123,7 @@ class QKPlan:
     def counts(self) -> dict:
         n_k = self.J * len([r for r in self.k_rots if r % self.n])
         n_q = self.J * len([r for r in self.q_rots if r % self.n])
-        n_3 = self.G * (self.B - 1)
+        n_3 = self.G * len([i for i in range(1, self.B) if (i * self.Hp * self.L) % self.n])
         n_f = len([1 for u, w, f in self.accumulators() if self.final_rot(u, f) % self.n])
         return {"rotations": n_k + n_q + n_3 + n_f, "baby": n_k, "giant": n_q, "step3": n_3, "final": n_f,
                 "cmult": self.G * self.B * self.J, "relin": self.G * self.B}

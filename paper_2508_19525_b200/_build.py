@@ -9,8 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libblb.so")
-# tuning: load a variant build instead (e.g. build(defines=["BLB_NTT_MINB=3"], out=...)); default libblb.so
-SO = os.environ.get("BLB_SO", SO)
+# compile-time kernel variants for A/B measurements are separate files: build(defines=[...], out=path)
 ROOT = os.path.dirname(HERE)
 
 CU = ["ntt.cu", "kernels.cu", "encode.cu", "matmul.cu", "qk.cu", "api.cu"]

@@ -91,13 +91,18 @@ void blb_timing_end(int cat, cudaEvent_t start, cudaStream_t st, double bytes) {
     cudaEventRecord(e, st);
     g_tl[cat].push_back({start, e, bytes});
 }
-int blb_indep_batch() {
-    static int b = [] {
-        int v = kMaxJobs;  // measured: 32 -> 76.8 ms, 16 -> 78.3, 8 -> 82.3, 4 -> 91.1 ms per layer
-        if (const char *e = getenv("BLB_INDEP_BATCH")) v = atoi(e);
-        return v < 1 ? 1 : (v > kMaxJobs ? kMaxJobs : v);
-    }();
-    return b;
+// per-(kernel, device) record of the dynamic shared-memory opt-in (blb_smem_optin)
+bool blb_smem_optin_needed(const void *kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void *, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    (void)bytes;
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto &d : done)
+        if (d.first == kernel && d.second == dev) return false;
+    done.push_back({kernel, dev});
+    return true;
 }
 extern "C" void blb_timing_enable(int on) {
     std::lock_guard<std::mutex> lk(g_tmu);
@@ -246,21 +251,6 @@ extern "C" blb_status blb_params_create(blb_params **out, int log_n, const uint6
     BLB_CUDA_TRY(cudaSetDevice(cuda_device));
     auto *P = new blb_params();
     cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
-    if (const char *v = getenv("BLB_OVERLAP")) P->overlap = atoi(v);
-    if (const char *v = getenv("BLB_CHUNK")) P->mac_chunk = std::max(1, atoi(v));
-    if (const char *v = getenv("BLB_MAC_TMA")) P->mac_tma = atoi(v);
-    if (const char *v = getenv("BLB_MAC_J")) P->mac_j = atoi(v);
-    if (const char *v = getenv("BLB_TSUM22")) P->tsum22 = atoi(v);
-    if (const char *v = getenv("BLB_PT_PACK")) P->pt_pack = atoi(v);
-    if (const char *v = getenv("BLB_MAC_NINT")) P->mac_nint = atoi(v);
-    if (const char *v = getenv("BLB_MACJ_ACC")) P->macj_acc = atoi(v);
-    if (const char *v = getenv("BLB_KS_ACC")) P->ks_acc = atoi(v);
-    if (const char *v = getenv("BLB_TSUM_ACC")) P->tsum_acc = atoi(v);
-    if (const char *v = getenv("BLB_NTT_2S")) P->ntt_2s = atoi(v);
-    if (const char *v = getenv("BLB_KS_SG")) P->ks_sg = atoi(v);
-    if (const char *v = getenv("BLB_MAC_R")) P->mac_r = atoi(v);
-    if (const char *v = getenv("BLB_PRO_RED")) P->pro_red = atoi(v);
-    if (const char *v = getenv("BLB_FUSE")) P->fuse = atoi(v);
     if (cudaStreamCreateWithFlags(&P->aux, cudaStreamNonBlocking) != cudaSuccess) P->aux = nullptr;
     for (auto &e : P->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     P->logN = log_n; P->N = (int)N; P->K = nq; P->np = np; P->dnum = dnum; P->device = cuda_device;

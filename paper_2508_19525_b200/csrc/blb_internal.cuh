@@ -220,8 +220,13 @@ struct AccG {
         const double c = __dsub_rn(__fma_rn(p, qinv, magic), magic);
         return __dadd_rn(__dadd_rn(__fma_rn(-c, qd, p), e), l);
     }
+    // back to s = M and |l| <= q/2 + 1: rem() keeps the old l unreduced, so l is re-centred here
+    // (|rem| < q + 2^49 < 2^53: c = round(l / q) by one fma against 1.5 * 2^52 and l - c q by one
+    // exact fma), which keeps every period's bound l < 2^48 + q for any number of folds
     __device__ __forceinline__ void fold(double qd, double qinv) {
-        l = rem(qd, qinv);
+        const double r = rem(qd, qinv);
+        const double c = __dsub_rn(__fma_rn(r, qinv, 6755399441055744.0), 6755399441055744.0);
+        l = __fma_rn(-c, qd, r);
         s = kM;
     }
     __device__ __forceinline__ u64 reduce(double qd, double qinv) const {
@@ -279,6 +284,15 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
                  : "memory");
 }
 
+// Opt a kernel in to > 48 KB of dynamic shared memory on the CURRENT device, once per (kernel,
+// device): the attribute is per device context, so a process driving several GPUs sets it on each.
+bool blb_smem_optin_needed(const void *kernel, size_t bytes);  // api.cu: registry keyed by (kernel, device)
+template <class Kern>
+inline void blb_smem_optin(Kern kernel, size_t bytes) {
+    if (blb_smem_optin_needed((const void *)kernel, bytes))
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 // NTT-domain automorphism index: out[k] = in[perm(k)],
 // perm(k) = brv(((g * (2 brv(k) + 1)) mod 2N - 1) / 2)
 __device__ __forceinline__ uint32_t galois_perm(uint32_t k, uint32_t g, int logN) {
@@ -295,26 +309,11 @@ struct BconvTable;  // fwd
 struct blb_params {
     int logN, N, K, np, dnum, alpha, device;
     int num_sms = 148;
-    // auxiliary stream: integer-bound key switches overlap the HBM-bound MAC (matmul.cu)
+    // auxiliary stream: the integer-kernel (60-bit prime) rows of a mixed N = 2^16 NTT batch run on it
+    // beside the FP64-kernel rows on the caller's stream (ntt.cu)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev[64] = {};
     mutable int ev_next = 0;
-    int overlap = 0;              // two-stream MAC / giant-step schedule (env BLB_OVERLAP=1); measured slower once the
-                                  // batches grew (71.8 ms without vs 72.5-73.2 ms with, profiles/r1_overlap.log)
-    int fuse = 1;                 // fused ModUp / ModDown NTT prologue / epilogue (env BLB_FUSE=0 disables)
-    int mac_chunk = 3;            // outputs per MAC / giant-step chunk of the two-stream schedule (env BLB_CHUNK)
-    int mac_tma = 1;              // warp-specialised bulk-copy MAC (env BLB_MAC_TMA=0: register double buffer)
-    int pt_pack = 1;              // 5-byte packed plaintext limbs for primes < 2^40 (env BLB_PT_PACK=0: 8 bytes)
-    int mac_r = 0;                // ct-ct K' MAC on rotation-shared blocks of 4 outputs (k_mac_r; env BLB_MAC_R, 0 = k_mac_j)
-    int ks_sg = 0;                // key switch: groups per shared-digit chunk (k_ks_inner_sg; env BLB_KS_SG, 0 = off)
-    int pro_red = 1;              // fused ModUp / ModDown prologue: skip moot reductions (env BLB_PRO_RED)
-    int ntt_2s = 1;               // two-stream NTT: integer-kernel rows on the auxiliary stream (env BLB_NTT_2S)
-    int tsum_acc = 1;             // tensor J-sum accumulators: 1 AccG, 0 Acc41 + AccF64 (env BLB_TSUM_ACC)
-    int ks_acc = 4;               // key-switch inner product accumulators (40-bit limbs), see k_ks_inner (env BLB_KS_ACC)
-    int macj_acc = 2;             // mask MAC accumulators: 0 Acc41 + AccF64, 1 Acc41 + AccG, 2 AccG (env BLB_MACJ_ACC)
-    int mac_nint = -1;            // weight MAC: accumulators per output on the integer pipe, 0..2 (env BLB_MAC_NINT)
-    int tsum22 = 1;               // 2 x 2 register-blocked ct-ct tensor J-sum (env BLB_TSUM22=0: one output per thread)
-    int mac_j = 2;                // mask MAC over groups of mac_j (2 or 4) outputs sharing their masks (env BLB_MAC_J; 0: k_mac)
     u64 mod[BLB_MAXP];
     u64 psi[BLB_MAXP];
     Primes pr;                    // by-value copy for kernel args
@@ -388,10 +387,10 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
 // pointers, n <= kMaxJobs) -> ext [n][beta][E][N] (contiguous, NTT), using
 // coef_scratch [n][k][N].
 constexpr int kMaxJobs = 128;
-// independent rotations (each with its own ModUp) are key-switched in batches of this many jobs so
-// their extended digits (beta (k+np) N 8 bytes each, 15.7 MB at k = 5) are still in L2 when the inner
-// product reads them (env BLB_INDEP_BATCH overrides, 1..kMaxJobs)
-int blb_indep_batch();
+// independent rotations (each with its own ModUp) are key-switched in batches of this many jobs
+// (measured per layer: 128 best; 32 -> 76.8 ms, 16 -> 78.3, 8 -> 82.3, 4 -> 91.1 at the time,
+// profiles/r1_indep_batch.log: smaller batches are launch-bound)
+constexpr int kIndepBatch = kMaxJobs;
 blb_status launch_modup(const blb_params *P, int level, const u64 *const *c1_ntt, int n, u64 *ext,
                         u64 *coef_scratch, cudaStream_t st);
 inline int blb_beta(const blb_params *P, int level) { return (level + 1 + P->alpha - 1) / P->alpha; }
@@ -480,13 +479,6 @@ size_t encode_scratch_doubles(const blb_params *P, int n_pts);
 blb_status launch_mac(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc, const int *ent_r, const int *ent_pt,
                       const int *ent_start, int o0, int e_base, int n_o, int n_entries, int k, cudaStream_t st,
                       int kq = -1, int jg = 1);
-
-// Rotation-shared mask MAC (IG = 4 outputs per block sharing each staged rotation pair; matmul.cu k_mac_r):
-// block b has stages rb_start[b] .. rb_start[b+1]-1 with rotation rb_r[s] and masks rb_m[s*4 + t] (-1 = none)
-// accumulated into acc output rb_out[b*4 + t] (-1 = none)
-blb_status launch_mac_r(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc, const int *rb_start, const int *rb_r,
-                        const int *rb_m, const int *rb_out, int n_blk, int n_stages, int n_products, int ig, int k,
-                        int kq, cudaStream_t st);
 
 // ChaCha / sampling
 enum { TAG_SECRET = 1, TAG_KEY_A = 2, TAG_KEY_E = 3, TAG_ENC_A = 4, TAG_ENC_E = 5, TAG_MASK = 6 };

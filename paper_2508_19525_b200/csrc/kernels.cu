@@ -10,9 +10,6 @@
 
 namespace {
 constexpr int kTB = 256;
-#ifndef BLB_MIX
-#define BLB_MIX 0
-#endif
 
 // ---------------------------------------------------------------- ChaCha20
 __device__ __forceinline__ uint32_t rotl32(uint32_t x, int r) { return __funnelshift_l(x, x, r); }
@@ -217,27 +214,18 @@ struct KsGroups {
 // before the first multiply); BETA = 0: runtime beta.
 // EXT: write the extended-basis result (P sigma_g(c0) + u0, u1) over Q_l u P straight to
 // jobs.j[t].out ([2][E][N]) -- the double-hoisted rotation (no ModDown).
-// SMALL (prime < 2^41): the a-part products run on the FP64 pipe (AccF64), the b-part on the
-// integer pipe, so the two pipes share the 2 beta products per job.
-// Digit sources of the key-switch inner product: DigG loads job t's extended digit j straight from
-// global memory; DigS reads it from the CTA's shared-memory copy (k_ks_inner_sg: the groups of a
-// chunk share their digits, loaded once per CTA).
+// SMALL (prime < 2^41): both products of a digit run on the FP64 pipe (AccG, no per-product
+// reduction); 60-bit rows take ks_inner_body60 (Acc60, one job at a time) when beta is a compile-time
+// constant <= 7, else Acc128 here.
+// Digit source: DigG loads job t's extended digit j straight from global memory.
 struct DigG {
     const KsJobs *jobs;
     long long off;  // m * N + x
     long long EN;   // E * N
     __device__ __forceinline__ u64 operator()(int t, int, int j) const { return jobs->j[t].ext[j * EN + off]; }
 };
-struct DigS {
-    const u64 *s;
-    int stride_q, stride_j, tid;
-    __device__ __forceinline__ u64 operator()(int, int q, int j) const { return s[q * stride_q + j * stride_j + tid]; }
-};
 
-// KA (env BLB_KS_ACC): 40-bit rows 0 = b-part Acc128 + a-part AccF64, 1 = both AccG (FP64 pipe, no
-// per-product reduction), 2 = b-part Acc41 + a-part AccG; 3 = as 1 with the 60-bit rows on Acc60;
-// 4 = as 1 with the 60-bit rows one job at a time on Acc60 (ks_inner_body60)
-template <int BETA, bool EXT, bool SMALL, int KA, class DS>
+template <int BETA, bool EXT, bool SMALL, class DS>
 __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups &grp, u64 *u, const Primes &pr, int k,
                                               int np, int K, int beta_rt, int logN, const PinvTab &pq, int x, int m,
                                               int gi, const DS &ds) {
@@ -251,12 +239,8 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
     // contiguous and only the two outputs are scattered, to x = perm_{g^-1}(y)
     const uint32_t dst = J0.galois == 1 ? (uint32_t)x : galois_perm(x, J0.galois_inv, logN);
     const ModConst &mc = pr.m[pm];
-    // KA = 3: as 1, and the 60-bit rows on Acc60 (32-bit partial products, <= 7 products; beta a
-    // compile-time <= 7), else Acc128
-    using W = typename std::conditional<(KA == 3 && BETA > 0 && BETA <= 7), Acc60, Acc128>::type;
-    using A1 = typename std::conditional<SMALL, typename std::conditional<(KA >= 1), AccG, AccF64>::type, W>::type;
-    using A0 = typename std::conditional<SMALL && (KA == 1 || KA >= 3), AccG,
-                                         typename std::conditional<SMALL && KA == 2, Acc41, W>::type>::type;
+    using A1 = typename std::conditional<SMALL, AccG, Acc128>::type;
+    using A0 = A1;
     const double qd = (double)mc.q, qinv = 1.0 / qd;
     A0 a0[kKsGroup];
     A1 a1[kKsGroup];
@@ -342,9 +326,9 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
     }
 }
 
-// 60-bit rows with KA = 4: the group's jobs one at a time on Acc60 (6 IMAD-class instructions per
-// product instead of Acc128's ~11), so only one job's accumulators are live (Acc60 for all four jobs
-// at once needed 122 registers, KA = 3).  Same additive terms and stores as ks_inner_body.
+// 60-bit rows: the group's jobs one at a time on Acc60 (6 IMAD-class instructions per product instead
+// of Acc128's ~11), so only one job's accumulators are live (Acc60 for all four jobs at once needed
+// 122 registers and measured slower).  Same additive terms and stores as ks_inner_body.
 template <int BETA, bool EXT, class DS>
 __device__ __forceinline__ void ks_inner_body60(const KsJobs &jobs, const KsGroups &grp, u64 *u, const Primes &pr, int k,
                                                 int np, int K, int logN, const PinvTab &pq, int x, int m, int gi,
@@ -410,63 +394,18 @@ __device__ __forceinline__ void ks_inner_body60(const KsJobs &jobs, const KsGrou
 // grid (tiles * groups, E) with the group index fastest: the CTAs in flight cover every group of a
 // few (limb, tile) slices, so groups that share a key (or an input's hoisted digits) read each tile
 // from DRAM once and from L2 after that
-template <int BETA, bool EXT = false, int KA = 0>
+template <int BETA, bool EXT = false>
 __global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, int np, int K, int beta_rt,
                            int logN, PinvTab pq) {
     const int gi = blockIdx.x % grp.n;
     const int x = (blockIdx.x / grp.n) * blockDim.x + threadIdx.x;
-#if BLB_MIX
-    const int m = (blockIdx.y + blockIdx.x) % gridDim.y;  // limbs interleaved (60-bit / 40-bit rows mixed)
-#else
     const int m = blockIdx.y;
-#endif
     if (x >= (1 << logN)) return;
     const int pm = m < k ? m : K + (m - k);
     const DigG ds{&jobs, (long long)m * (1 << logN) + x, (long long)(k + np) << logN};
-    if (pr.m[pm].q < (1ull << 41)) ks_inner_body<BETA, EXT, true, KA>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi, ds);
-    else if constexpr (KA == 4 && BETA > 0 && BETA <= 7) ks_inner_body60<BETA, EXT>(jobs, grp, u, pr, k, np, K, logN, pq, x, m, gi, ds);
-    else ks_inner_body<BETA, EXT, false, KA>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi, ds);
-}
-
-// Shared-digit variant: consecutive key groups whose jobs use the same extended digits (hoisted
-// rotations: the J ciphertexts of a ct-ct operand rotated by every step, or the inputs of a ct-pt
-// MatMul by every baby step) form chunks; a CTA loads its (tile, limb) slice of the chunk's digits
-// once into shared memory and runs the chunk's groups over it.  Without it every group re-read the
-// digits from DRAM (ncu: 1.9 GB read where keys + one pass over the digits are 0.7 GB).
-// grid (tiles, E, chunks); chunk c covers groups ch.gl[ch.g0[c]] .. ch.gl[ch.g0[c + 1] - 1].
-struct KsChunks {
-    int n;
-    int g0[kMaxJobs + 1];
-    int gl[kMaxJobs];
-};
-#ifndef BLB_KS_SG_MINB
-#define BLB_KS_SG_MINB 2
-#endif
-template <int BETA, bool EXT, int KA>
-__global__ void __launch_bounds__(kTB, BLB_KS_SG_MINB) k_ks_inner_sg(KsJobs jobs, KsGroups grp, KsChunks ch, u64 *u, Primes pr, int k, int np, int K, int logN,
-                              PinvTab pq) {
-    extern __shared__ u64 sdig[];  // [kKsGroup][BETA][blockDim]
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int m = blockIdx.y, c = blockIdx.z;
-    const int N = 1 << logN, E = k + np;
-    const int c0 = ch.g0[c], c1 = ch.g0[c + 1];
-    const int t0 = grp.start[ch.gl[c0]], cnt = grp.start[ch.gl[c0] + 1] - t0;
-    const int bd = blockDim.x, tid = threadIdx.x;
-    // each thread stores and later reads only its own coefficient's slots: no barrier needed
-    for (int q = 0; q < cnt; q++) {
-        const u64 *ext = jobs.j[t0 + q].ext + (long long)m * N + x;
-#pragma unroll
-        for (int j = 0; j < BETA; j++) sdig[(q * BETA + j) * bd + tid] = ext[(long long)j * E * N];
-    }
-    const DigS ds{sdig, BETA * bd, bd, tid};
-    const int pm = m < k ? m : K + (m - k);
-    const bool small = pr.m[pm].q < (1ull << 41);
-    for (int ci = c0; ci < c1; ci++) {
-        const int gi = ch.gl[ci];
-        if (small) ks_inner_body<BETA, EXT, true, KA>(jobs, grp, u, pr, k, np, K, BETA, logN, pq, x, m, gi, ds);
-        else if constexpr (KA == 4) ks_inner_body60<BETA, EXT>(jobs, grp, u, pr, k, np, K, logN, pq, x, m, gi, ds);
-        else ks_inner_body<BETA, EXT, false, KA>(jobs, grp, u, pr, k, np, K, BETA, logN, pq, x, m, gi, ds);
-    }
+    if (pr.m[pm].q < (1ull << 41)) ks_inner_body<BETA, EXT, true>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi, ds);
+    else if constexpr (BETA > 0 && BETA <= 7) ks_inner_body60<BETA, EXT>(jobs, grp, u, pr, k, np, K, logN, pq, x, m, gi, ds);
+    else ks_inner_body<BETA, EXT, false>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi, ds);
 }
 
 // conv[t][b][i][x] = FastBConv_{P -> q_i}(INTT(u_P))   (u P-rows already INTT'd)
@@ -629,7 +568,7 @@ blb_status launch_modup(const blb_params *P, int level, const u64 *const *c1_ntt
     RowBatch rb{};
     rb.base = coef; rb.poly_stride = (long long)k * N; rb.n_polys = n; rb.limbs = k; rb.limb0 = 0;
     for (int i = 0; i < k; i++) rb.prime[i] = i;
-    if (P->logN == 16 && P->alpha == 1 && P->fuse) {
+    if (P->logN == 16 && P->alpha == 1) {
         // fused: the INTT's first pass reads the c1 rows in place (no gather copy); in the forward
         // NTT's first pass the own rows are copied and the others converted (x mod q_m)
         NttFuse gz{};
@@ -715,69 +654,15 @@ static blb_status ks_inner_launch(const blb_params *P, int level, const KsJobs &
         pq.sh[i] = blbh_shoup_dev_table(P, i);
     }
     cudaEvent_t t0 = blb_timing_begin(st);
-    // shared-digit chunks: runs of consecutive groups with the same job count and the same digit
-    // pointers (at most P->ks_sg groups per chunk)
-    KsChunks ch{};
-    ch.n = 0;
-    int longest = 0;
-    if (P->ks_sg > 1 && beta >= 1 && beta <= 6 && (P->ks_acc == 1 || P->ks_acc == 4) && N % kTB == 0) {
-        // greedy: each unassigned group opens a chunk and takes the later groups with its signature
-        // (job count + digit pointers), e.g. every step's group of the same input block
-        bool used[kMaxJobs] = {false};
-        int nl = 0;
-        for (int g = 0; g < G.n; g++) {
-            if (used[g]) continue;
-            const int cnt = G.start[g + 1] - G.start[g];
-            ch.g0[ch.n++] = nl;
-            int len = 0;
-            for (int h = g; h < G.n && len < P->ks_sg; h++) {
-                if (used[h] || G.start[h + 1] - G.start[h] != cnt) continue;
-                bool same = true;
-                for (int q = 0; q < cnt && same; q++) same = J.j[G.start[h] + q].ext == J.j[G.start[g] + q].ext;
-                if (!same) continue;
-                used[h] = true;
-                ch.gl[nl++] = h;
-                len++;
-            }
-            longest = std::max(longest, len);
-        }
-        ch.g0[ch.n] = nl;
-    }
-    if (longest >= 2) {
-        const dim3 gsg((unsigned)(N / kTB), E, ch.n);
-        const size_t smem = (size_t)kKsGroup * beta * kTB * 8;
-#define BLB_KS_SG(B_, KA_) k_ks_inner_sg<B_, EXT, KA_><<<gsg, kTB, smem, st>>>(J, G, ch, u, P->pr, k, np, P->K, P->logN, pq)
-#define BLB_KS_SG_SWITCH(KA_)                   \
-    switch (beta) {                             \
-        case 1: BLB_KS_SG(1, KA_); break;       \
-        case 2: BLB_KS_SG(2, KA_); break;       \
-        case 3: BLB_KS_SG(3, KA_); break;       \
-        case 4: BLB_KS_SG(4, KA_); break;       \
-        case 5: BLB_KS_SG(5, KA_); break;       \
-        default: BLB_KS_SG(6, KA_); break;      \
-    }
-        if (P->ks_acc == 4) { BLB_KS_SG_SWITCH(4) }
-        else { BLB_KS_SG_SWITCH(1) }
-#undef BLB_KS_SG_SWITCH
-#undef BLB_KS_SG
-    } else {
     const dim3 gks((unsigned)(((N + kTB - 1) / kTB) * G.n), E);
-#define BLB_KS_SWITCH(KA_)                                                                                    \
-    switch (beta) {                                                                                          \
-        case 1: k_ks_inner<1, EXT, KA_><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break; \
-        case 2: k_ks_inner<2, EXT, KA_><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break; \
-        case 3: k_ks_inner<3, EXT, KA_><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break; \
-        case 4: k_ks_inner<4, EXT, KA_><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break; \
-        case 5: k_ks_inner<5, EXT, KA_><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break; \
-        case 6: k_ks_inner<6, EXT, KA_><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break; \
-        default: k_ks_inner<0, EXT, KA_><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break; \
-    }
-    if (P->ks_acc == 1) { BLB_KS_SWITCH(1) }
-    else if (P->ks_acc == 3) { BLB_KS_SWITCH(3) }
-    else if (P->ks_acc == 4) { BLB_KS_SWITCH(4) }
-    else if (P->ks_acc == 2) { BLB_KS_SWITCH(2) }
-    else { BLB_KS_SWITCH(0) }
-#undef BLB_KS_SWITCH
+    switch (beta) {
+        case 1: k_ks_inner<1, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
+        case 2: k_ks_inner<2, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
+        case 3: k_ks_inner<3, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
+        case 4: k_ks_inner<4, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
+        case 5: k_ks_inner<5, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
+        case 6: k_ks_inner<6, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
+        default: k_ks_inner<0, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
     }
     BLB_COUNT_LAUNCH(1);
     // algorithmic bytes: each distinct key once (groups sharing a key read it through L2)
@@ -800,7 +685,7 @@ static blb_status moddown_launch(const blb_params *P, int level, const KsJobs &J
     rb.base = u; rb.poly_stride = (long long)E * N; rb.n_polys = 2 * n; rb.limbs = np; rb.limb0 = k;
     for (int d = 0; d < np; d++) rb.prime[d] = P->K + d;
     BLB_TRY(launch_ntt(P, rb, true, st));
-    if (P->logN == 16 && np == 1 && P->fuse) {
+    if (P->logN == 16 && np == 1) {
         // fused ModDown: conv = NTT(u_P mod q_i) with the reduction in the first pass and
         // (u_i - conv) * P^{-1} (+ sigma(c0) / (c0, c1)) in the last pass
         RowBatch cb{};
@@ -991,7 +876,7 @@ blb_status launch_moddown_rescale(const blb_params *P, int level, u64 *u, int n,
         RowBatch cb{};
         cb.base = conv; cb.poly_stride = (long long)level * N; cb.n_polys = 2 * cnt; cb.limbs = level; cb.limb0 = 0;
         for (int i = 0; i < level; i++) cb.prime[i] = i;
-        if (P->logN == 16 && P->fuse) {
+        if (P->logN == 16) {
             NttFuse fz{};
             fz.epi = 1;
             fz.u = ub;

@@ -48,9 +48,6 @@ constexpr int kTB = 256;
 #ifndef BLB_MAC_MINB
 #define BLB_MAC_MINB 3
 #endif
-#ifndef BLB_MIX
-#define BLB_MIX 0
-#endif
 
 // Build the slot vectors of entries [e0, e0 + cnt) (plan order) into slots[cnt][n].
 struct PlanDev {
@@ -175,24 +172,14 @@ struct PtLayout {
 template <int PP, int STG>
 constexpr size_t mac4_smem() { return (size_t)STG * (PP + 2) * 512 * 8 + 2 * STG * 8; }
 
-// SPLIT41 (q < 2^41): NINT of the four accumulators of an output -- (c0, x), (c0, x+1), (c1, x),
-// (c1, x+1) in that order -- run on the integer pipe (Acc41), the others on the FP64 pipe (AccF64);
-// the split balances the fma-heavy and FP64 pipes.  Otherwise Acc128 throughout.
-template <bool SPLIT41, bool PACKED, int kMacP, int kM4Stages, int NINT>
+// SPLIT41 (q < 2^41): every product on the grid-split FP64 accumulator (AccG, FP64 pipe, one
+// reduction per output); otherwise (60-bit limbs) Acc128 on the integer pipe, folded every 64.
+template <bool SPLIT41, bool PACKED, int kMacP, int kM4Stages>
 __device__ __forceinline__ void mac4_consume(const u64 *ring, uint64_t *full, uint64_t *empty, int n_e, int nP,
                                              u64 *const *outs, long long kN, const ModConst &mc) {
-    using I = typename std::conditional<SPLIT41, Acc41, Acc128>::type;
-    // NINT < 0: every product on the grid-split FP64 accumulator (AccG)
-    using F = typename std::conditional<SPLIT41, typename std::conditional<(NINT < 0), AccG, AccF64>::type, Acc128>::type;
-    using T0 = typename std::conditional<(NINT >= 1), I, F>::type;
-    using T1 = typename std::conditional<(NINT >= 2), I, F>::type;
-    using T2 = typename std::conditional<(NINT >= 3), I, F>::type;
-    using T3 = typename std::conditional<(NINT >= 4), I, F>::type;
+    using A = typename std::conditional<SPLIT41, AccG, Acc128>::type;
     const double qd = (double)mc.q, qinv = 1.0 / qd;
-    T0 a00[kMacP];
-    T1 a01[kMacP];
-    T2 a10[kMacP];
-    T3 a11[kMacP];
+    A a00[kMacP], a01[kMacP], a10[kMacP], a11[kMacP];
 #pragma unroll
     for (int j = 0; j < kMacP; j++) { a00[j].zero(); a01[j].zero(); a10[j].zero(); a11[j].zero(); }
     constexpr int kM4StageWords = (kMacP + 2) * 512;
@@ -203,9 +190,9 @@ __device__ __forceinline__ void mac4_consume(const u64 *ring, uint64_t *full, ui
         const u64 *st = ring + (size_t)slot * kM4StageWords;
         const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + kMacP * 512 + 2 * t);
         const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + (kMacP + 1) * 512 + 2 * t);
-        if constexpr (SPLIT41 && NINT < 0) {
-            // every product on AccG: convert each staged residue to a double once (R values are
-            // shared by the kMacP outputs, plaintext values by c0 and c1)
+        if constexpr (SPLIT41) {
+            // convert each staged residue to a double once (R values are shared by the kMacP
+            // outputs, plaintext values by c0 and c1)
             const double R0x = AccF64::u2d(r0.x), R0y = AccF64::u2d(r0.y);
             const double R1x = AccF64::u2d(r1.x), R1y = AccF64::u2d(r1.y);
 #pragma unroll
@@ -227,29 +214,19 @@ __device__ __forceinline__ void mac4_consume(const u64 *ring, uint64_t *full, ui
                     a10[j].macd(Px, R1x); a11[j].macd(Py, R1y);
                 }
             }
-        } else
+        } else {
 #pragma unroll
-        for (int j = 0; j < kMacP; j++) {
-            if (j < nP) {
-                ulonglong2 pv;
-                if constexpr (PACKED) {  // slot j: 512 low words, then 512 high bytes
-                    const uint2 lo = *reinterpret_cast<const uint2 *>(reinterpret_cast<const uint32_t *>(st + j * 512) + 2 * t);
-                    const unsigned short hi =
-                        *(reinterpret_cast<const unsigned short *>(reinterpret_cast<const unsigned char *>(st + j * 512) + 2048) + t);
-                    pv.x = ((u64)(hi & 0xFF) << 32) | lo.x;
-                    pv.y = ((u64)(hi >> 8) << 32) | lo.y;
-                } else {
-                    pv = *reinterpret_cast<const ulonglong2 *>(st + j * 512 + 2 * t);
+            for (int j = 0; j < kMacP; j++) {
+                if (j < nP) {
+                    const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(st + j * 512 + 2 * t);
+                    a00[j].mac(pv.x, r0.x); a01[j].mac(pv.y, r0.y);
+                    a10[j].mac(pv.x, r1.x); a11[j].mac(pv.y, r1.y);
                 }
-                accm(a00[j], pv.x, r0.x, qd, qinv);
-                accm(a01[j], pv.y, r0.y, qd, qinv);
-                accm(a10[j], pv.x, r1.x, qd, qinv);
-                accm(a11[j], pv.y, r1.y, qd, qinv);
             }
         }
         __syncwarp();
         if ((t & 31) == 0) mbar_arrive(&empty[slot]);
-        // Acc128: fold every 64 products (< 2^126); AccF64: every 512 (sums below 2^51)
+        // Acc128: fold every 64 products (< 2^126); AccG: every 512 (s < 2^93, l < 2^48)
         if ((!SPLIT41 && (s & 63) == 63) || (SPLIT41 && (s & 511) == 511)) {
 #pragma unroll
             for (int j = 0; j < kMacP; j++) {
@@ -269,7 +246,7 @@ __device__ __forceinline__ void mac4_consume(const u64 *ring, uint64_t *full, ui
     }
 }
 
-template <int kMacP, int kM4Stages, int MINB, int NINT = 2>
+template <int kMacP, int kM4Stages, int MINB>
 __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char *__restrict__ pt, const u64 *__restrict__ R,
                                                        u64 *__restrict__ acc, const int *__restrict__ ent_r,
                                                        const int *__restrict__ ent_start, int o0, int e_base, int n_o,
@@ -283,19 +260,10 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char
     const int n_tiles = N / (2 * kTB);
     const int n_grp = (n_o + kMacP - 1) / kMacP;
     int bid = blockIdx.x;
-#if BLB_MIX
-    // limb fastest: CTAs of the 60-bit limb (integer pipe) and of the 40-bit limbs (FP64 pipe) are
-    // in flight together instead of one limb after the other
-    const int l = bid % k;
-    bid /= k;
-    const int og = bid % n_grp;
-    const int tile = bid / n_grp;
-#else
     const int og = bid % n_grp;
     bid /= n_grp;
     const int tile = bid % n_tiles;
     const int l = bid / n_tiles;
-#endif
     const int oa = og * kMacP, nP = min(kMacP, n_o - oa);
     const long long kN = (long long)k * N;
     const int e_lo = ent_start[o0 + oa], n_e = ent_start[o0 + oa + 1] - e_lo;
@@ -334,25 +302,20 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char
 #pragma unroll
     for (int j = 0; j < kMacP; j++) outs[j] = acc + (long long)(oa + (j < nP ? j : 0)) * 2 * kN + lx0;
     const ModConst &mc = pr.m[l];
-    if (w == 5) mac4_consume<true, true, kMacP, kM4Stages, NINT>(ring, full, empty, n_e, nP, outs, kN, mc);
-    else if (mc.q < (1ull << 41))
-        mac4_consume<true, false, kMacP, kM4Stages, NINT>(ring, full, empty, n_e, nP, outs, kN, mc);
-    else mac4_consume<false, false, kMacP, kM4Stages, 4>(ring, full, empty, n_e, nP, outs, kN, mc);
+    if (w == 5) mac4_consume<true, true, kMacP, kM4Stages>(ring, full, empty, n_e, nP, outs, kN, mc);
+    else if (mc.q < (1ull << 41)) mac4_consume<true, false, kMacP, kM4Stages>(ring, full, empty, n_e, nP, outs, kN, mc);
+    else mac4_consume<false, false, kMacP, kM4Stages>(ring, full, empty, n_e, nP, outs, kN, mc);
 }
 
-template <int PP, int STG, int MINB, int NINT = 2>
+template <int PP, int STG, int MINB>
 static void launch_mac4(const unsigned char *pt, const u64 *R, u64 *acc, const int *ent_r, const int *ent_start, int o0,
                         int e_base, int n_o, int k, int logN, const Primes &pr, int n_tiles, const PtLayout &lay,
                         cudaStream_t st) {
-    static bool attr = false;
     constexpr size_t smem = mac4_smem<PP, STG>();
-    if (!attr) {
-        cudaFuncSetAttribute(k_mac_tma4<PP, STG, MINB, NINT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    blb_smem_optin(k_mac_tma4<PP, STG, MINB>, smem);
     const size_t n_grp = (size_t)(n_o + PP - 1) / PP;
-    k_mac_tma4<PP, STG, MINB, NINT><<<(unsigned)(n_grp * n_tiles * k), kTB + 32, smem, st>>>(pt, R, acc, ent_r, ent_start, o0,
-                                                                                      e_base, n_o, k, logN, pr, lay);
+    k_mac_tma4<PP, STG, MINB><<<(unsigned)(n_grp * n_tiles * k), kTB + 32, smem, st>>>(pt, R, acc, ent_r, ent_start, o0,
+                                                                                e_base, n_o, k, logN, pr, lay);
 }
 
 // scatter standard [cnt][k][N] plaintexts (entries e0..e0+cnt of the plan) into the blocked, width-packed layout
@@ -385,13 +348,12 @@ constexpr int kMjStages = 3;
 template <int JG>
 constexpr size_t macj_smem() { return (size_t)kMjStages * (1 + 2 * JG) * 512 * 8 + 2 * kMjStages * 8; }
 
-// SPLIT41 accumulators: AM = 0: (c0) Acc41 on the integer pipe + (c1) AccF64; AM = 1: Acc41 + AccG;
-// AM = 2: AccG for all four (env BLB_MACJ_ACC)
-template <bool SPLIT41, int JG, int AM>
+// SPLIT41 (q < 2^41): AccG for all four accumulators; else Acc128
+template <bool SPLIT41, int JG>
 __device__ __forceinline__ void macj_consume(const u64 *ring, uint64_t *full, uint64_t *empty, int n_e, u64 *const *outs,
                                              long long kN, const ModConst &mc) {
-    using A = typename std::conditional<SPLIT41, typename std::conditional<(AM == 2), AccG, Acc41>::type, Acc128>::type;
-    using A1 = typename std::conditional<SPLIT41, typename std::conditional<(AM >= 1), AccG, AccF64>::type, Acc128>::type;
+    using A = typename std::conditional<SPLIT41, AccG, Acc128>::type;
+    using A1 = A;
     const double qd = (double)mc.q, qinv = 1.0 / qd;
     A a00[JG], a01[JG];
     A1 a10[JG], a11[JG];
@@ -413,7 +375,7 @@ __device__ __forceinline__ void macj_consume(const u64 *ring, uint64_t *full, ui
         }
         __syncwarp();
         if ((t & 31) == 0) mbar_arrive(&empty[slot]);
-        // Acc128: 64 products < 2^126; FP64 accumulators: 512 products (Acc41: exact for < 2^14)
+        // Acc128: 64 products < 2^126; AccG: 512 products
         if ((!SPLIT41 && (s & 63) == 63) || (SPLIT41 && (s & 511) == 511)) {
 #pragma unroll
             for (int j = 0; j < JG; j++) {
@@ -431,7 +393,7 @@ __device__ __forceinline__ void macj_consume(const u64 *ring, uint64_t *full, ui
 }
 
 // grid: (group fastest, tile, limb); group gi covers outputs o0 + gi*JG .. + JG - 1 (local o)
-template <int JG, int MINB, int AM = 0>
+template <int JG, int MINB>
 __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_j(const u64 *__restrict__ pt, const u64 *__restrict__ R,
                                                      u64 *__restrict__ acc, const int *__restrict__ ent_r,
                                                      const int *__restrict__ ent_pt, const int *__restrict__ ent_start,
@@ -444,17 +406,10 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_j(const u64 *__restrict_
     const int N = 1 << logN;
     const int n_tiles = N / (2 * kTB);
     int bid = blockIdx.x;
-#if BLB_MIX
-    const int l = bid % k;
-    bid /= k;
-    const int gi = bid % n_grp;
-    const int tile = bid / n_grp;
-#else
     const int gi = bid % n_grp;
     bid /= n_grp;
     const int tile = bid % n_tiles;
     const int l = bid / n_tiles;
-#endif
     const int oa = gi * JG;
     const long long kN = (long long)k * N;
     const int e_lo = ent_start[o0 + oa], n_e = ent_start[o0 + oa + 1] - e_lo;
@@ -492,131 +447,8 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_j(const u64 *__restrict_
 #pragma unroll
     for (int j = 0; j < JG; j++) outs[j] = acc + (long long)(oa + j) * 2 * kN + lx0;
     const ModConst &mc = pr.m[l < kq ? l : Kfull + (l - kq)];
-    if (mc.q < (1ull << 41)) macj_consume<true, JG, AM>(ring, full, empty, n_e, outs, kN, mc);
-    else macj_consume<false, JG, AM>(ring, full, empty, n_e, outs, kN, mc);
-}
-
-// Rotation-shared mask MAC (ct-ct stage 1, K'_i = sum_c M_{c,i} (.) Rot_{c+i}(K), reading C13): the IG
-// consecutive outputs i0 .. i0 + IG - 1 of one ciphertext j use the same rotations shifted by one, so
-// a CTA walks the union of their rotations: per stage ONE (c0, c1) rotation tile pair + the IG masks
-// that select it (-1: that output does not use this rotation).  Staged bytes per product drop from
-// 10 (k_mac_j: a mask per output pair + a rotation pair per output) to ~6.  One coefficient per
-// thread (IG x 2 accumulators), 256-coefficient tiles on a 4-stage bulk-copy ring.
-// Block lists (host, qk.cu): stages rb_start[b] .. rb_start[b+1]-1, rotation rb_r[s], masks
-// rb_m[s * IG + t], outputs rb_out[b * IG + t] (acc index).
-constexpr int kMrStages = 4;
-#ifndef BLB_MACR_TILES
-#define BLB_MACR_TILES 1
-#endif
-constexpr int kMrTiles = BLB_MACR_TILES;  // 256-coefficient tiles per CTA (the ring stays full across them)
-template <int IG>
-constexpr size_t macr_smem() { return (size_t)kMrStages * (2 + IG) * 256 * 8 + 2 * kMrStages * 8; }
-
-template <bool SMALL, int IG>
-__device__ __forceinline__ void macr_consume(const u64 *ring, uint64_t *full, uint64_t *empty, const int *rb_m, int s0,
-                                             int n_s, u64 *const *outs, long long kN, const ModConst &mc, int sg0) {
-    using A = typename std::conditional<SMALL, AccG, Acc128>::type;
-    const double qd = (double)mc.q, qinv = 1.0 / qd;
-    A a0[IG], a1[IG];
-#pragma unroll
-    for (int t = 0; t < IG; t++) { a0[t].zero(); a1[t].zero(); }
-    constexpr int kStageWords = (2 + IG) * 256;
-    const int tid = threadIdx.x;
-    for (int s = 0; s < n_s; s++) {
-        const int sg = sg0 + s;  // ring position continues across the CTA's tiles
-        const int slot = sg % kMrStages;
-        mbar_wait(&full[slot], (sg / kMrStages) & 1);
-        const u64 *st = ring + (size_t)slot * kStageWords;
-        const u64 r0 = st[tid], r1 = st[256 + tid];
-#pragma unroll
-        for (int t = 0; t < IG; t++) {
-            if (rb_m[(s0 + s) * IG + t] >= 0) {  // uniform over the CTA
-                const u64 mv = st[(2 + t) * 256 + tid];
-                accm(a0[t], mv, r0, qd, qinv);
-                accm(a1[t], mv, r1, qd, qinv);
-            }
-        }
-        __syncwarp();
-        if ((tid & 31) == 0) mbar_arrive(&empty[slot]);
-        if ((!SMALL && (s & 63) == 63) || (SMALL && (s & 511) == 511)) {
-#pragma unroll
-            for (int t = 0; t < IG; t++) { accf(a0[t], mc, qd, qinv); accf(a1[t], mc, qd, qinv); }
-        }
-    }
-#pragma unroll
-    for (int t = 0; t < IG; t++) {
-        if (outs[t]) {
-            outs[t][tid] = accr(a0[t], mc, qd, qinv);
-            outs[t][kN + tid] = accr(a1[t], mc, qd, qinv);
-        }
-    }
-}
-
-// grid: (block fastest, 256-coefficient tile, limb)
-template <int IG>
-__global__ void __launch_bounds__(256 + 32, 3) k_mac_r(const u64 *__restrict__ pt, const u64 *__restrict__ R,
-                                                  u64 *__restrict__ acc, const int *__restrict__ rb_start,
-                                                  const int *__restrict__ rb_r, const int *__restrict__ rb_m,
-                                                  const int *__restrict__ rb_out, int n_blk, int k, int kq, int Kfull,
-                                                  int logN, Primes pr) {
-    constexpr int kStageWords = (2 + IG) * 256;
-    extern __shared__ __align__(128) unsigned char smraw[];
-    u64 *ring = reinterpret_cast<u64 *>(smraw);
-    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)kMrStages * kStageWords);
-    uint64_t *empty = full + kMrStages;
-    const int N = 1 << logN;
-    const int n_tg = N / (256 * kMrTiles);  // groups of kMrTiles consecutive 256-coefficient tiles
-    int bid = blockIdx.x;
-    const int b = bid % n_blk;
-    bid /= n_blk;
-    const int tg = bid % n_tg;
-    const int l = bid / n_tg;
-    const long long kN = (long long)k * N;
-    const int s0 = rb_start[b], n_s = rb_start[b + 1] - s0;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kMrStages; s++) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 256 / 32);
-        }
-        mbar_fence_init();
-    }
-    __syncthreads();
-    if (threadIdx.x >= 256) {  // producer warp: the stages of every tile of the CTA back to back
-        if (threadIdx.x == 256) {
-            for (int sg = 0; sg < kMrTiles * n_s; sg++) {
-                const int s = sg % n_s;
-                const long long lx0 = (long long)l * N + (tg * kMrTiles + sg / n_s) * 256;
-                const int slot = sg % kMrStages;
-                if (sg >= kMrStages) mbar_wait(&empty[slot], ((sg / kMrStages) - 1) & 1);
-                u64 *st = ring + (size_t)slot * kStageWords;
-                int nm = 0;
-#pragma unroll
-                for (int t = 0; t < IG; t++) nm += rb_m[(s0 + s) * IG + t] >= 0;
-                mbar_expect_tx(&full[slot], (unsigned)(2 + nm) * 2048u);
-                const int ri = rb_r[s0 + s];
-                bulk_g2s(st, R + (long long)ri * 2 * kN + lx0, 2048, &full[slot]);
-                bulk_g2s(st + 256, R + ((long long)ri * 2 + 1) * kN + lx0, 2048, &full[slot]);
-#pragma unroll
-                for (int t = 0; t < IG; t++) {
-                    const int mi = rb_m[(s0 + s) * IG + t];
-                    if (mi >= 0) bulk_g2s(st + (2 + t) * 256, pt + (long long)mi * kN + lx0, 2048, &full[slot]);
-                }
-            }
-        }
-        return;
-    }
-    const ModConst &mc = pr.m[l < kq ? l : Kfull + (l - kq)];
-    for (int ti = 0; ti < kMrTiles; ti++) {
-        const long long lx0 = (long long)l * N + (tg * kMrTiles + ti) * 256;
-        u64 *outs[IG];
-#pragma unroll
-        for (int t = 0; t < IG; t++) {
-            const int o = rb_out[b * IG + t];
-            outs[t] = o >= 0 ? acc + (long long)o * 2 * kN + lx0 : nullptr;
-        }
-        if (mc.q < (1ull << 41)) macr_consume<true, IG>(ring, full, empty, rb_m, s0, n_s, outs, kN, mc, ti * n_s);
-        else macr_consume<false, IG>(ring, full, empty, rb_m, s0, n_s, outs, kN, mc, ti * n_s);
-    }
+    if (mc.q < (1ull << 41)) macj_consume<true, JG>(ring, full, empty, n_e, outs, kN, mc);
+    else macj_consume<false, JG>(ring, full, empty, n_e, outs, kN, mc);
 }
 
 // dst[o] += src[j] for the jobs of one giant batch (sequential per thread: no races)
@@ -648,37 +480,15 @@ blb_status launch_mac(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc
     const int N = P->N;
     const int n_tiles = N / (2 * kTB);
     cudaEvent_t t0 = blb_timing_begin(st);
-    const int JGc = P->mac_j;  // outputs per CTA (2 or 4; 0 = per-output k_mac)
-    if (JGc > 0 && jg % JGc == 0 && n_o % JGc == 0 && ent_pt && P->logN >= 9) {
+    constexpr int JGc = 2;  // outputs per CTA sharing the mask list (4 measured slower)
+    if (jg % JGc == 0 && n_o % JGc == 0 && ent_pt && P->logN >= 9) {
         // groups of JGc outputs sharing the mask list (reading C13 stage 1): k_mac_j
         const int n_grp = n_o / JGc;
         const unsigned grid = (unsigned)((size_t)n_grp * n_tiles * k);
-        if (JGc == 4) {
-            static bool attr = false;
-            constexpr size_t smem = macj_smem<4>();
-            if (!attr) {
-                cudaFuncSetAttribute(k_mac_j<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                attr = true;
-            }
-            k_mac_j<4, 2><<<grid, kTB + 32, smem, st>>>(pt, R, acc, ent_r, ent_pt, ent_start, o0, n_grp, k,
-                                                        kq < 0 ? k : kq, P->K, P->logN, P->pr);
-        } else {
-            constexpr size_t smem = macj_smem<2>();
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(k_mac_j<2, 3, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                cudaFuncSetAttribute(k_mac_j<2, 3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                cudaFuncSetAttribute(k_mac_j<2, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                attr = true;
-            }
-            auto go = [&](auto kern) {
-                kern<<<grid, kTB + 32, smem, st>>>(pt, R, acc, ent_r, ent_pt, ent_start, o0, n_grp, k, kq < 0 ? k : kq,
-                                                   P->K, P->logN, P->pr);
-            };
-            if (P->macj_acc == 2) go(k_mac_j<2, 3, 2>);
-            else if (P->macj_acc == 1) go(k_mac_j<2, 3, 1>);
-            else go(k_mac_j<2, 3, 0>);
-        }
+        constexpr size_t smem = macj_smem<JGc>();
+        blb_smem_optin(k_mac_j<JGc, 3>, smem);
+        k_mac_j<JGc, 3><<<grid, kTB + 32, smem, st>>>(pt, R, acc, ent_r, ent_pt, ent_start, o0, n_grp, k,
+                                                      kq < 0 ? k : kq, P->K, P->logN, P->pr);
         BLB_COUNT_LAUNCH(1);
         BLB_COUNT(3, n_entries);
         // bytes staged: one mask tile per entry per group of JGc outputs + the (c0, c1) rotation tiles
@@ -692,36 +502,6 @@ blb_status launch_mac(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc
     BLB_COUNT_LAUNCH(1);
     BLB_COUNT(3, n_entries);
     blb_timing_end(3, t0, st, 3.0 * n_entries * k * N * 8.0);  // category 3: ct-ct mask MAC (mask + c0, c1 bytes)
-    BLB_CHECK_LAUNCH();
-    return BLB_OK;
-}
-
-blb_status launch_mac_r(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc, const int *rb_start, const int *rb_r,
-                        const int *rb_m, const int *rb_out, int n_blk, int n_stages, int n_products, int ig, int k,
-                        int kq, cudaStream_t st) {
-    if (n_blk <= 0) return BLB_OK;
-    if (ig != 4 || P->N % 256 != 0) {
-        blb_set_error("launch_mac_r: IG = 4 and N %% 256 == 0 only");
-        return BLB_E_INVALID_ARG;
-    }
-    const int N = P->N;
-    cudaEvent_t t0 = blb_timing_begin(st);
-    constexpr size_t smem = macr_smem<4>();
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_mac_r<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
-    if (N % (256 * kMrTiles) != 0) {
-        blb_set_error("launch_mac_r: N must be a multiple of %d", 256 * kMrTiles);
-        return BLB_E_INVALID_ARG;
-    }
-    const unsigned grid = (unsigned)((size_t)n_blk * (N / (256 * kMrTiles)) * k);
-    k_mac_r<4><<<grid, 256 + 32, smem, st>>>(pt, R, acc, rb_start, rb_r, rb_m, rb_out, n_blk, k, kq, P->K, P->logN, P->pr);
-    BLB_COUNT_LAUNCH(1);
-    BLB_COUNT(3, n_products);
-    // bytes staged: one (c0, c1) rotation pair per stage + one mask tile per product
-    blb_timing_end(3, t0, st, (2.0 * n_stages + (double)n_products) * k * N * 8.0);
     BLB_CHECK_LAUNCH();
     return BLB_OK;
 }
@@ -915,7 +695,7 @@ static PtLayout pt_layout(const blb_matmul_plan *pl) {
     PtLayout lay{};
     long long off = 0;
     for (int l = 0; l < k; l++) {
-        lay.w[l] = (P->pt_pack && P->mod[l] < (1ull << 40) && P->logN >= 9) ? 5 : 8;
+        lay.w[l] = (P->mod[l] < (1ull << 40) && P->logN >= 9) ? 5 : 8;
         lay.loff[l] = off;
         off += (long long)lay.w[l] * P->N;
     }
@@ -1104,19 +884,12 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
             BLB_TRY(launch_keyswitch(P, level, jobs.data() + j0, cnt, ks_u, ks_conv, st));
         }
     }
-    // 3-5. MAC, giant steps and rescale, in output chunks: the MAC of chunk c+1 (HBM-bound,
-    // main stream) overlaps the giant-step key switches + rescale of chunk c (integer-bound,
-    // auxiliary stream); the caller's stream waits for the auxiliary stream at the end.
-    const bool ovl = P->overlap && P->aux && out_count > 1;
-    cudaStream_t sa = ovl ? P->aux : st;
-    const int chunk = ovl ? std::max(1, std::min(P->mac_chunk, (out_count + 1) / 2)) : out_count;
-    auto next_event = [&]() {
-        cudaEvent_t e = P->ev[P->ev_next];
-        P->ev_next = (P->ev_next + 1) % 64;
-        return e;
-    };
-    for (int c0 = 0; c0 < out_count; c0 += chunk) {
-        const int cn = std::min(chunk, out_count - c0);
+    // 3-5. MAC, giant steps and rescale (one stream: a two-stream overlap of the MAC of output
+    // chunk c+1 with the giant steps of chunk c measured slower once the key-switch batches were
+    // 128 jobs, 71.8 vs 72.5-73.2 ms per layer, profiles/r1_overlap.log)
+    cudaStream_t sa = st;
+    {
+        const int c0 = 0, cn = out_count;
         // MAC
         {
             const int o0 = (out_first + c0) * pl->G, n_o = cn * pl->G;
@@ -1128,29 +901,14 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
                 const PtLayout lay = pt_layout(pl);
                 const unsigned char *ptb = reinterpret_cast<const unsigned char *>(pt_dev);
                 cudaEvent_t t0 = blb_timing_begin(st);
-                // groups of PP consecutive (b', g) with one entry list -> the multi-output kernel
-                // (BLB_MAC_TMA: 1 = 2 outputs x 3 CTAs/SM (default), 4 = 4 outputs x 1 CTA/SM x 8 stages,
-                //  0 = one output per CTA); plans whose pairs differ fall back to one output per CTA
-                const int PP = P->mac_tma == 4 ? 4 : 2;
-                bool grouped = P->mac_tma == 1 || P->mac_tma == 4;
+                // pairs of consecutive (b', g) with one entry list -> the two-output kernel (each R
+                // tile staged once for both); plans whose pairs differ take one output per CTA
+                bool grouped = true;
                 for (int j = 0; j < n_o && grouped; j++)
-                    if (j % PP != PP - 1 && j + 1 < n_o && !pl->same_next[o0 + j]) grouped = false;
-                // BLB_MAC_NINT: accumulators per output on the integer pipe (0..2; the rest on FP64)
-                if (grouped && PP == 2 && P->mac_nint < 0)
-                    launch_mac4<2, BLB_MAC_STG, BLB_MAC_MINB, -1>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
-                                             P->pr, n_tiles, lay, st);
-                else if (grouped && PP == 2 && P->mac_nint == 0)
-                    launch_mac4<2, 4, 3, 0>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
-                                            P->pr, n_tiles, lay, st);
-                else if (grouped && PP == 2 && P->mac_nint == 1)
-                    launch_mac4<2, 4, 3, 1>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
-                                            P->pr, n_tiles, lay, st);
-                else if (grouped && PP == 2)
-                    launch_mac4<2, 4, 3, 2>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
-                                            P->pr, n_tiles, lay, st);
-                else if (grouped)
-                    launch_mac4<4, 8, 1>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
-                                         P->pr, n_tiles, lay, st);
+                    if (j % 2 != 1 && j + 1 < n_o && !pl->same_next[o0 + j]) grouped = false;
+                if (grouped)
+                    launch_mac4<2, BLB_MAC_STG, BLB_MAC_MINB>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o,
+                                                              k, P->logN, P->pr, n_tiles, lay, st);
                 else
                     launch_mac4<1, 4, 3>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
                                          P->pr, n_tiles, lay, st);
@@ -1159,11 +917,6 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
                 blb_timing_end(0, t0, st, (double)n_entries * (double)lay.bpp);  // packed plaintext bytes
                 BLB_CHECK_LAUNCH();
             }
-        }
-        if (ovl) {
-            cudaEvent_t e = next_event();
-            BLB_CUDA_TRY(cudaEventRecord(e, st));
-            BLB_CUDA_TRY(cudaStreamWaitEvent(sa, e, 0));
         }
         // giant steps (reading C11, lazy ModDown): Y[b'] = lift(acc[b'][0]) + sum_g Rot_ext(acc[b'][g])
         // in Q_l u P, then ONE ModDown per output; g-major so outputs sharing a key are adjacent
@@ -1183,7 +936,7 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
             for (int t = c0; t < c0 + cn; t++)
                 if (std::binary_search(pl->giant[out_first + t].begin(), pl->giant[out_first + t].end(), g))
                     gj.push_back({t, g});
-        const int gb = blb_indep_batch();
+        const int gb = kIndepBatch;
         for (size_t j0 = 0; j0 < gj.size(); j0 += gb) {
             const int cnt = (int)std::min<size_t>(gb, gj.size() - j0);
             std::vector<const u64 *> c1(cnt);
@@ -1220,11 +973,6 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
             out[t].scale = in[0].scale;  // Delta * q_level / q_level, exact (reading S6)
         }
         if (n_y > 0) BLB_TRY(launch_moddown_rescale(P, level, yext, n_y, youts.data(), gks_conv, sa));
-    }
-    if (ovl) {
-        cudaEvent_t e = next_event();
-        BLB_CUDA_TRY(cudaEventRecord(e, sa));
-        BLB_CUDA_TRY(cudaStreamWaitEvent(st, e, 0));
     }
     return BLB_OK;
 }

@@ -460,7 +460,7 @@ static inline bool rb_small(const blb_params *P, const RowBatch &r) {
 }
 static inline int rb_rows(const RowBatch &r) { return r.n_polys * (r.nsel ? r.nsel : r.limbs); }
 
-// Two-stream NTT (env BLB_NTT_2S=1): the integer-kernel rows of a mixed batch run on the auxiliary
+// Two-stream NTT: the integer-kernel rows of a mixed batch run on the auxiliary
 // stream while the FP64-kernel rows run on the caller's stream -- the two kernels load different
 // pipes (fma-heavy vs FP64), so CTAs of both can share an SM.  fork() before the launches, join()
 // after; the stream of part h is part_stream(h).
@@ -468,7 +468,7 @@ struct NttStreams {
     const blb_params *P;
     cudaStream_t st;
     bool two;
-    NttStreams(const blb_params *P_, cudaStream_t st_, int np2) : P(P_), st(st_), two(np2 == 2 && P_->ntt_2s && P_->aux) {
+    NttStreams(const blb_params *P_, cudaStream_t st_, int np2) : P(P_), st(st_), two(np2 == 2 && P_->aux) {
         if (two) {
             cudaEvent_t e = P->ev[P->ev_next];
             P->ev_next = (P->ev_next + 1) % 64;
@@ -593,7 +593,7 @@ blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool invers
         dim3 g(16, rb_rows(r));
         NttFuse fzp = fz;  // this part's reduction masks (pro = 1)
         fzp.red0 = fzp.red1 = 0;
-        if (!inverse && fz.pro == 1 && P->pro_red && fz.src_nq > 0 && fz.src_nq <= 8) {
+        if (!inverse && fz.pro == 1 && fz.src_nq > 0 && fz.src_nq <= 8) {
             u64 minq = ~0ull;
             const int nl = r.nsel ? r.nsel : r.limbs;
             for (int i = 0; i < nl; i++) minq = std::min<u64>(minq, P->mod[r.prime[r.nsel ? r.sel[i] : i]]);

@@ -36,10 +36,6 @@ struct blb_qk_plan {
     std::vector<MaskDesc> m1, m3;                // stage-1 masks (level), stage-3 masks (level-2)
     // MAC entry lists (CSR): K' outputs o = i*J + j; Q outputs o = (u-1)*J + j; A outputs = accumulators
     std::vector<int> kp_start, kp_r, kp_pt, qp_start, qp_r, qp_pt, a_start, a_r, a_pt;
-    // rotation-shared blocks of the K' MAC (k_mac_r): 4 consecutive i of one j, stages = union of rotations
-    std::vector<int> rb_start, rb_r, rb_m, rb_out;
-    bool rb_ok = false;
-    size_t off_rb_start = 0, off_rb_r = 0, off_rb_m = 0, off_rb_out = 0;
     struct Acc {
         int u, w, f, out, rot;
     };
@@ -136,14 +132,12 @@ __global__ void k_tensor_sum(const u64 *Qp, const u64 *Kp, u64 *D, Primes pr, in
 // so each Q_u / K'_i word it loads feeds two outputs (half the L2 -> SM traffic of k_tensor_sum, which
 // is what bounds it: the whole J-sum is ~1.5 GB of DRAM but 8.6 GB of L2 reads one output at a time).
 // Grid: (block (u0/2, i0/2) fastest, limb, x-tile).
-// SMALL (q < 2^41): d0 and d2 on the integer pipe (Acc41), the two d1 products on the FP64 pipe
-// (AccF64, exact for < 2^10 products): the two pipes share the work.  Otherwise Acc128 throughout.
-// TA = 1 (SMALL only; env BLB_TSUM_ACC, default): every product on the grid-split FP64 accumulator
-// (AccG, 4 FP64 ops per product, each loaded word converted to a double once)
-template <bool SMALL, int TA>
+// SMALL (q < 2^41): every product on the grid-split FP64 accumulator (AccG, 4 FP64 ops per product,
+// each loaded word converted to a double once).  Otherwise Acc128 throughout.
+template <bool SMALL>
 __device__ __forceinline__ void tsum22_body(const u64 *Qp, const u64 *Kp, u64 *D, int J, int B, long long kN,
                                             long long lx, int u0, int i0, const ModConst &mc) {
-    if constexpr (SMALL && TA == 1) {
+    if constexpr (SMALL) {
         const double qd = (double)mc.q, qinv = 1.0 / qd;
         AccG d0[2][2], d1[2][2], d2[2][2];  // 2 J <= 512 products per accumulator
 #pragma unroll
@@ -180,11 +174,7 @@ __device__ __forceinline__ void tsum22_body(const u64 *Qp, const u64 *Kp, u64 *D
             }
         return;
     }
-    using A = typename std::conditional<SMALL, Acc41, Acc128>::type;
-    using A1 = typename std::conditional<SMALL, AccF64, Acc128>::type;
-    const double qd = (double)mc.q, qinv = 1.0 / qd;
-    A d0[2][2], d2[2][2];
-    A1 d1[2][2];
+    Acc128 d0[2][2], d1[2][2], d2[2][2];
 #pragma unroll
     for (int a = 0; a < 2; a++)
 #pragma unroll
@@ -203,13 +193,8 @@ __device__ __forceinline__ void tsum22_body(const u64 *Qp, const u64 *Kp, u64 *D
             for (int b = 0; b < 2; b++) {
                 d0[a][b].mac(q0[a], k0[b]);
                 d2[a][b].mac(q1[a], k1[b]);
-                if constexpr (SMALL) {
-                    d1[a][b].mac(q0[a], k1[b], qd, qinv);
-                    d1[a][b].mac(q1[a], k0[b], qd, qinv);
-                } else {
-                    d1[a][b].mac(q0[a], k1[b]);
-                    d1[a][b].mac(q1[a], k0[b]);
-                }
+                d1[a][b].mac(q0[a], k1[b]);
+                d1[a][b].mac(q1[a], k0[b]);
             }
     }
 #pragma unroll
@@ -218,12 +203,10 @@ __device__ __forceinline__ void tsum22_body(const u64 *Qp, const u64 *Kp, u64 *D
         for (int b = 0; b < 2; b++) {
             u64 *out = D + (long long)((u0 + a) * B + i0 + b) * 3 * kN + lx;
             out[0] = d0[a][b].reduce(mc);
-            if constexpr (SMALL) out[kN] = d1[a][b].reduce(qd, qinv);
-            else out[kN] = d1[a][b].reduce(mc);
+            out[kN] = d1[a][b].reduce(mc);
             out[2 * kN] = d2[a][b].reduce(mc);
         }
 }
-template <int TA>
 __global__ void __launch_bounds__(kTB, 2) k_tensor_sum22(const u64 *Qp, const u64 *Kp, u64 *D, Primes pr, int J, int G,
                                                       int B, int k, int N) {
     const int nb = (G / 2) * (B / 2);
@@ -236,9 +219,9 @@ __global__ void __launch_bounds__(kTB, 2) k_tensor_sum22(const u64 *Qp, const u6
     const int u0 = 2 * (ob / (B / 2)), i0 = 2 * (ob % (B / 2));
     const long long kN = (long long)k * N, lx = (long long)l * N + x;
     const ModConst &mc = pr.m[l];
-    // Acc41 holds < 2^14 products of 41-bit residues: 2 J per accumulator here
-    if (mc.q < (1ull << 41)) tsum22_body<true, TA>(Qp, Kp, D, J, B, kN, lx, u0, i0, mc);
-    else tsum22_body<false, 0>(Qp, Kp, D, J, B, kN, lx, u0, i0, mc);
+    // AccG holds <= 512 products (2 J per accumulator here); Acc128 <= 64 products of 61-bit residues
+    if (mc.q < (1ull << 41)) tsum22_body<true>(Qp, Kp, D, J, B, kN, lx, u0, i0, mc);
+    else tsum22_body<false>(Qp, Kp, D, J, B, kN, lx, u0, i0, mc);
 }
 
 // dst[p][i][x] = src[p][i][x] for i < k_dst (src has k_src limbs per poly): exact level drop / copy
@@ -352,30 +335,6 @@ extern "C" blb_status blb_qk_plan_create(const blb_params *P, int L, int heads, 
             }
             pl->kp_start.push_back((int)pl->kp_r.size());
         }
-    // rotation-shared blocks (i0 .. i0+3, j) of the K' MAC: every output's entries keyed by rotation
-    if (B % 4 == 0) {
-        pl->rb_ok = true;
-        pl->rb_start.push_back(0);
-        for (int i0 = 0; i0 < B && pl->rb_ok; i0 += 4)
-            for (int j = 0; j < pl->J && pl->rb_ok; j++) {
-                std::map<int, std::array<int, 4>> stg;
-                for (int t = 0; t < 4; t++) {
-                    const int o = (i0 + t) * pl->J + j;
-                    for (int e = pl->kp_start[o]; e < pl->kp_start[o + 1]; e++) {
-                        auto it = stg.find(pl->kp_r[e]);
-                        if (it == stg.end()) it = stg.emplace(pl->kp_r[e], std::array<int, 4>{-1, -1, -1, -1}).first;
-                        if (it->second[t] >= 0) pl->rb_ok = false;  // two entries of one output on one rotation
-                        it->second[t] = pl->kp_pt[e];
-                    }
-                }
-                for (auto &kv : stg) {
-                    pl->rb_r.push_back(kv.first);
-                    for (int t = 0; t < 4; t++) pl->rb_m.push_back(kv.second[t]);
-                }
-                pl->rb_start.push_back((int)pl->rb_r.size());
-                for (int t = 0; t < 4; t++) pl->rb_out.push_back((i0 + t) * pl->J + j);
-            }
-    }
     // Q MAC: output o = (u-1)*J + j, two entries
     pl->qp_start.push_back(0);
     for (int u = 1; u < pl->G; u++)
@@ -414,7 +373,8 @@ extern "C" blb_status blb_qk_plan_create(const blb_params *P, int L, int heads, 
     // rotation key set
     std::set<int32_t> st(pl->k_rots.begin(), pl->k_rots.end());
     st.insert(pl->q_rots.begin(), pl->q_rots.end());
-    for (int i = 1; i < B; i++) st.insert(-i * Hp * L);
+    for (int i = 1; i < B; i++)
+        if ((i * Hp * L) % n) st.insert(-i * Hp * L);  // a multiple of n slots is the identity (lift, no key)
     for (auto &A : pl->accs)
         if (((A.rot % n) + n) % n) st.insert(A.rot);
     pl->steps.assign(st.begin(), st.end());
@@ -428,10 +388,6 @@ extern "C" blb_status blb_qk_plan_create(const blb_params *P, int L, int heads, 
     pl->off_kp_start = put(pl->kp_start); pl->off_kp_r = put(pl->kp_r); pl->off_kp_pt = put(pl->kp_pt);
     pl->off_qp_start = put(pl->qp_start); pl->off_qp_r = put(pl->qp_r); pl->off_qp_pt = put(pl->qp_pt);
     pl->off_a_start = put(pl->a_start); pl->off_a_r = put(pl->a_r); pl->off_a_pt = put(pl->a_pt);
-    if (pl->rb_ok) {
-        pl->off_rb_start = put(pl->rb_start); pl->off_rb_r = put(pl->rb_r);
-        pl->off_rb_m = put(pl->rb_m); pl->off_rb_out = put(pl->rb_out);
-    }
     cudaError_t e = cudaMalloc(&pl->d_ent, sizeof(int) * std::max<size_t>(all.size(), 1));
     if (e == cudaSuccess) e = cudaMemcpy(pl->d_ent, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&pl->d_m1, sizeof(MaskDesc) * pl->m1.size());
@@ -461,7 +417,9 @@ extern "C" blb_status blb_qk_plan_info(const blb_qk_plan *pl, int *J, int *n_out
         int nf = 0;
         for (auto &A : pl->accs)
             if (((A.rot % pl->n) + pl->n) % pl->n) nf++;
-        *n_rotations = pl->J * (int)(pl->k_rots.size() + pl->q_rots.size()) + pl->G * (pl->B - 1) + nf;
+        int n3 = 0;  // step-3 rotations by i H_p L slots that are not the identity
+        for (int i = 1; i < pl->B; i++) n3 += ((i * pl->Hp * pl->L) % pl->n) != 0;
+        *n_rotations = pl->J * (int)(pl->k_rots.size() + pl->q_rots.size()) + pl->G * n3 + nf;
     }
     if (n_masks) *n_masks = (int)(pl->m1.size() + pl->m3.size());
     return BLB_OK;
@@ -568,7 +526,7 @@ static blb_status rotate_independent_ext(const blb_params *P, const blb_keys *ke
                                          const std::vector<const u64 *> &in, const std::vector<int32_t> &steps,
                                          const std::vector<u64 *> &out, u64 *ext, u64 *coef, cudaStream_t st) {
     const int k = level + 1, N = P->N, E = k + P->np, beta = blb_beta(P, level);
-    const int ib = blb_indep_batch();
+    const int ib = kIndepBatch;
     for (size_t t0 = 0; t0 < in.size(); t0 += ib) {
         const int cnt = (int)std::min<size_t>(ib, in.size() - t0);
         std::vector<const u64 *> c1(cnt);
@@ -665,12 +623,9 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
     };
     for (int j = 0; j < J; j++) BLB_TRY(launch_lift_ext(P, lvl, K[j].data, W + w.kr + (size_t)j * NKR * ct_e, st));
     BLB_TRY(rotate_ext_J(K, pl->k_rots, W + w.kr + ct_e, (size_t)NKR * ct_e));
-    if (P->mac_r && pl->rb_ok && P->N % 1024 == 0)  // blocks of 4 outputs i sharing each staged rotation
-        BLB_TRY(launch_mac_r(P, m1, W + w.kr, W + w.kacc, E + pl->off_rb_start, E + pl->off_rb_r, E + pl->off_rb_m,
-                             E + pl->off_rb_out, (int)pl->rb_start.size() - 1, (int)pl->rb_r.size(),
-                             (int)pl->kp_r.size(), 4, Ex, k, st));
-    else
-        BLB_TRY(launch_mac(P, m1, W + w.kr, W + w.kacc, E + pl->off_kp_r, E + pl->off_kp_pt, E + pl->off_kp_start, 0, 0,
+    // (a rotation-shared variant staging each rotation pair once for 4 outputs i measured slower:
+    // this MAC is latency-bound, not byte-bound, profiles/r1_macr_ab.log)
+    BLB_TRY(launch_mac(P, m1, W + w.kr, W + w.kacc, E + pl->off_kp_r, E + pl->off_kp_pt, E + pl->off_kp_start, 0, 0,
                            B * J, (int)pl->kp_r.size(), Ex, st, k, J));  // outputs i*J + j share their masks
     BLB_TRY(launch_moddown_rescale(P, lvl, W + w.kacc, B * J, W + w.kp, conv, st));  // C17
     // 2. giant side: Q_0 = level drop, Q_u = ModDown(MAC(masks, Rot_ext(Q))), rescale
@@ -687,10 +642,9 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
     // 3. products summed over j, relinearisation (one per (u, i)), rescale
     cudaEvent_t tt0 = blb_timing_begin(st);
     // Acc128 without folds: <= 64 products of 61-bit residues; AccF64: < 2^10 products
-    if (G % 2 == 0 && B % 2 == 0 && 2 * J <= 64 && P->tsum22) {
+    if (G % 2 == 0 && B % 2 == 0 && 2 * J <= 64) {
         const unsigned g22 = (unsigned)((size_t)((N + kTB - 1) / kTB) * k1 * (G / 2) * (B / 2));
-        if (P->tsum_acc == 1) k_tensor_sum22<1><<<g22, kTB, 0, st>>>(W + w.qp, W + w.kp, W + w.d, P->pr, J, G, B, k1, N);
-        else k_tensor_sum22<0><<<g22, kTB, 0, st>>>(W + w.qp, W + w.kp, W + w.d, P->pr, J, G, B, k1, N);
+        k_tensor_sum22<<<g22, kTB, 0, st>>>(W + w.qp, W + w.kp, W + w.d, P->pr, J, G, B, k1, N);
     }
     else
         k_tensor_sum<<<(unsigned)((size_t)((N + kTB - 1) / kTB) * k1 * G * B), kTB, 0, st>>>(
@@ -704,7 +658,7 @@ extern "C" blb_status blb_ct_ct_qk(const blb_qk_plan *pl, const blb_keys *keys, 
     const int E1 = k1 + P->np, E2 = k2 + P->np, E3 = k3 + P->np;
     {
         const int beta1 = blb_beta(P, lvl - 1);
-        const int rb = blb_indep_batch();
+        const int rb = kIndepBatch;
         for (int o0 = 0; o0 < G * B; o0 += rb) {
             const int cnt = std::min(rb, G * B - o0);
             std::vector<const u64 *> d2(cnt);

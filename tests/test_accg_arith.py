@@ -66,3 +66,32 @@ def test_accg_remainder_mod_q(seed):
     r = accg_rem(s, l, q)
     assert r == int(r) and abs(r) < q + 2 ** 49
     assert int(r) % q == sum(a * b for a, b in zip(A, B)) % q
+
+
+def accg_fold(s, l, q):
+    """AccG.fold: s = M, l = rem(s, l) re-centred mod q."""
+    qd, qinv = float(q), 1.0 / float(q)
+    r = accg_rem(s, l, q)
+    c = fma(r, qinv, MAGIC) - MAGIC
+    return M, fma(-c, qd, r)
+
+
+def test_accg_many_folds_stay_exact():
+    """64 fold periods of 512 top-range products (32k products per accumulator, twice the point
+    where an unreduced l would pass 2^53): every fold keeps |l| <= q/2 + 1 and the final
+    remainder is the exact sum mod q."""
+    import oracle as O
+    q = O.prime_chain(16, [60, 40])[1]
+    qd, qinv = float(q), 1.0 / float(q)
+    s, l = M, 0.0
+    exact = 0
+    a = float(q - 1)
+    for period in range(64):
+        for _ in range(512):
+            sn = fma(a, a, s)
+            l = l + fma(a, a, s - sn)
+            s = sn
+        exact += 512 * (q - 1) ** 2
+        s, l = accg_fold(s, l, q)
+        assert s == M and l == int(l) and abs(l) <= q / 2 + 1
+    assert int(accg_rem(s, l, q)) % q == exact % q

@@ -124,7 +124,8 @@ def check_masked(b, name, o, oct_out):
 
 def test_bench_plans_are_the_tested_plans(bert):
     """The layer bench.py times uses BENCH_BSGS; the oracle plans built from the same dict
-    have the same rotation sets and plaintext counts (QKV 8448 / FFN 9216 / O-proj 2304)."""
+    have the same rotation sets and plaintext counts (QKV 8448 / FFN 9216 / O-proj 3072: the
+    diagonal input carries the H_p = 16 padded heads of the Softmax x V collapse)."""
     layer, ctx, F, A = bert["layer"], bert["ctx"], bert["F"], bert["A"]
     spec = OL.build(ctx, OL.LayerSpec(L, D, H, FFN, bi.BENCH_BSGS, layer.level), A["WQ"], A["WK"], A["WV"],
                     F["WO"], F["W1"], F["W2"])
@@ -134,7 +135,7 @@ def test_bench_plans_are_the_tested_plans(bert):
         assert pg.n_pt == po.n_plaintexts and pg.n_rotations == po.n_rotations, name
         assert pg.rotation_steps() == po.rotation_steps(), name
     assert (layer.plans["qkv"].n_pt, layer.plans["ffn1"].n_pt, layer.plans["ffn2"].n_pt,
-            layer.plans["oproj"].n_pt) == (8448, 9216, 9216, 2304)
+            layer.plans["oproj"].n_pt) == (8448, 9216, 9216, 3072)
     assert layer.qk.rotation_steps() == spec.plans["qk"].rotation_steps()
     assert layer.sv.rotation_steps() == spec.plans["sv"].rotation_steps()
     assert (spec.plans["qk"].J, spec.plans["sv"].J) == (4, 8)

@@ -576,22 +576,3 @@ def test_batched_inputs_bit_exact(toy):
     Y = packing.spatial_unslots(dec, Bt * L, Dout)
     for b in range(Bt):
         assert np.abs(Y[b * L:(b + 1) * L] - Xs[b] @ W).max() < 1e-5
-
-
-@pytest.mark.parametrize("knobs", [{"BLB_MAC_NINT": "0", "BLB_MACJ_ACC": "0", "BLB_KS_ACC": "0", "BLB_TSUM_ACC": "0"},
-                                   {"BLB_MAC_NINT": "2", "BLB_MACJ_ACC": "1", "BLB_KS_ACC": "2"},
-                                   {"BLB_KS_ACC": "3"}, {"BLB_KS_ACC": "4", "BLB_NTT_2S": "0", "BLB_KS_SG": "0"},
-                                   {"BLB_KS_ACC": "1", "BLB_KS_SG": "3", "BLB_MAC_R": "1"}])
-def test_accumulator_variants_bit_exact(monkeypatch, knobs):
-    """The selectable accumulators (AccF64 / Acc41 / Acc128 instead of the default grid-split AccG,
-    DESIGN §7) give the same bits: the toy ct-pt MatMul and a toy ct-ct Q K^T against the oracle."""
-    for kv in knobs.items():
-        monkeypatch.setenv(*kv)
-    toy = Pair(bi.TOY)  # Params read the knobs at creation
-    d = bi.toy_inputs()
-    plan_o = mm.plan_spatial(d["W"], 16, toy.n, 16)
-    plan_g = blb.MatmulPlan(toy.g, 16, 16, 16, bsgs_B=16)
-    from paper_2508_19525_b200 import packing
-    _, _, oout, gout = run_both(toy, plan_o, plan_g, list(packing.spatial_slots(d["X"], toy.n)), d["W"])
-    assert np.array_equal(u64(gout[0].data), oout[0].data)
-    test_qk_ct_ct_bit_exact(Pair(bi.QKTOY), 3, 32, 16, 0)
