@@ -90,103 +90,166 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# --------------------------------------------------------------------------- oracle sample
-def oracle_sample_ms(dims, reps: int = 1) -> dict:
-    """Time the CPU oracle (as it stands) on a bounded sample of the layer at
-    N = 2^16, level 4, and extrapolate to ms per layer by operation counts:
-    one hoisted rotation (ModUp + key switch), P ct-pt products (mul + add), one
-    rescale, one mask.  Plaintext / key values do not change the work, so
-    uniform residues stand in for encoded weights (encode is row a0)."""
-    import oracle as O
+# --------------------------------------------------------------------------- oracle (CPU baseline)
+def cpu_info() -> dict:
+    model = "?"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count() or 1}
+
+
+def set_omp_threads(n: int):
+    """OpenMP threads of the oracle's C library for the calling thread's next parallel regions."""
+    import ctypes
+    import ctypes.util
+    name = ctypes.util.find_library("gomp") or "libgomp.so.1"
+    ctypes.CDLL(name).omp_set_num_threads(int(n))
+
+
+def layer_counts(dims) -> dict:
+    """Slice-equivalents of one layer step from the oracle's own plans (C11 / C12 / C13):
+    key switches (rotations + relinearisations), ct-pt products, ModDown+rescales, tensor products,
+    masks -- the same schedule the GPU step runs (launch counters in the bench line agree)."""
     import oracle.matmul as mm
+    import oracle.matmul_cc as cc
+    n = bi.BERT.n
+    L, d, H, ffn = dims["L"], dims["d"], dims["H"], dims["ffn"]
+    cm = mm.mhp_column_map(d, H, L, n)
+    qkv_map = cm + [d + c if c >= 0 else -1 for c in cm] + list(range(2 * d, 3 * d))
+    Hp = 1 << (H - 1).bit_length()
+    plans = [mm.plan_spatial(np.ones((d, 3 * d)), L, n, BSGS["qkv"], col_map=qkv_map),
+             mm.plan_diagonal(np.ones((Hp * (d // H), d)), Hp, L, n, BSGS["oproj"]),
+             mm.plan_spatial(np.ones((d, ffn)), L, n, BSGS["ffn1"]),
+             mm.plan_spatial(np.ones((ffn, d)), L, n, BSGS["ffn2"])]
+    c = {"ks": sum(p.n_rotations for p in plans), "prod": sum(p.n_plaintexts for p in plans),
+         "mdr": sum(p.n_out for p in plans), "tensor": 0, "mask": sum(p.n_out for p in plans)}
+    for qk in (cc.plan_qk(L, H, d // H, n), cc.plan_sv(L, H, n)):
+        qc = qk.counts()
+        acc3 = qk.accumulators()
+        c["ks"] += qc["rotations"] + qc["relin"]
+        c["prod"] += qk.J * qk.B * (2 * qk.g - 1) + 2 * qk.J * (qk.G - 1) + sum(
+            1 for (u, w, f) in acc3 for i in range(qk.B) if qk.mask3(u, i, w, f).any())
+        c["tensor"] += qc["cmult"]
+        c["mdr"] += qk.J * (qk.B + qk.G) + qk.G * qk.B + len(acc3)
+    qk0 = cc.plan_qk(L, H, d // H, n)
+    c["mask"] += qk0.n_out - 2 * qk0.J       # Q, K outputs of QKV feed Q K^T; its diagonals are masked
+    return c
+
+
+def oracle_slice(threads: int) -> dict:
+    """The CPU oracle, as it stands, on one stated slice of the layer at N = 2^16, level 4 (k = 5),
+    timed directly: one baby-step rotation (hoisted-form ModUp + key switch + ModDown, C8), one
+    (b', g) unit of the FFN1 MAC (3 inputs x B = 64 = 192 ct-pt products summed, C11), its giant
+    step kept in Q u P + the fused ModDown/rescale (C11 lazy giant sum, C17), one ct-ct (u, i)
+    stage of Q K^T (J = 4 tensor products summed + relinearisation in Q u P + ModDown/rescale,
+    C13), and one CKKS->MPC mask (C14).  Plaintext / key values do not change the work, so uniform
+    residues stand in for encoded weights and keys (encode is row a0)."""
+    import oracle as O
+    set_omp_threads(threads)
     P = bi.BERT
     primes = O.prime_chain(P.log_n, list(P.q_bits) + list(P.p_bits))
     ctx = O.Ctx(P.log_n, primes[:5], primes[5:], P.dnum)
     rng = np.random.default_rng(0)
-    lvl = 4
-    k = lvl + 1
+    lvl, k = 4, 5
 
-    def rnd(*shape_limbs):
-        polys, limbs = shape_limbs
+    def rnd(polys, limbs):
         return np.stack([np.stack([rng.integers(0, ctx.mods[i], ctx.N, dtype=np.uint64) for i in limbs])
                          for _ in range(polys)])
 
     ct = O.Ct(rnd(2, range(k)), lvl, 2.0 ** 40)
     g = ctx.galois(128)
-    key = np.stack([np.stack([rnd(1, range(6))[0] for _ in range(2)]) for _ in range(ctx.beta_top)])
-    keys = O.Keys(None, None, {g: key})
-    n_prod = 8
+    key = np.stack([rnd(2, range(6)) for _ in range(ctx.beta_top)])
+    keys = O.Keys(None, None, {g: key, ctx.galois(64 * 128): key}, key)
+    n_prod = 3 * BSGS["ffn1"]
     pts = [rnd(1, range(k))[0] for _ in range(n_prod)]
-    t = {"rot": 0.0, "prod": 0.0, "resc": 0.0, "mask": 0.0}
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        O.rotate(ctx, ct, keys, 128)
-        t1 = time.perf_counter()
-        acc = O.mul_pt(ctx, ct, pts[0], 1.0)
-        for p in pts[1:]:
-            acc = O.add(ctx, acc, O.mul_pt(ctx, ct, p, 1.0))
-        t2 = time.perf_counter()
-        r = O.rescale(ctx, acc)
-        t3 = time.perf_counter()
-        O.mask(ctx, r, bytes(32), 0)
-        t4 = time.perf_counter()
-        t["rot"] += (t1 - t0) / reps
-        t["prod"] += (t2 - t1) / (reps * n_prod)
-        t["resc"] += (t3 - t2) / reps
-        t["mask"] += (t4 - t3) / reps
-    # layer operation counts from the oracle's own plans (C11 / C12, SURVEY 8(d))
-    n = ctx.n
-    W = np.ones((dims["d"], dims["d"]))
-    cm = mm.mhp_column_map(dims["d"], dims["H"], dims["L"], n)
-    qkv_map = cm + [dims["d"] + c if c >= 0 else -1 for c in cm] + list(range(2 * dims["d"], 3 * dims["d"]))
-    Hp = 1 << (dims["H"] - 1).bit_length()
-    plans = [mm.plan_spatial(np.ones((dims["d"], 3 * dims["d"])), dims["L"], n, BSGS["qkv"], col_map=qkv_map),
-             mm.plan_diagonal(np.ones((Hp * (dims["d"] // dims["H"]), dims["d"])), Hp, dims["L"], n, BSGS["oproj"]),
-             mm.plan_spatial(np.ones((dims["d"], dims["ffn"])), dims["L"], n, BSGS["ffn1"]),
-             mm.plan_spatial(np.ones((dims["ffn"], dims["d"])), dims["L"], n, BSGS["ffn2"])]
-    import oracle.matmul_cc as cc
-    n_rot = sum(p.n_rotations for p in plans)
-    n_pt = sum(p.n_plaintexts for p in plans)
-    n_out = sum(p.n_out for p in plans)
-    n_mask = sum(p.n_out for p in plans)
-    for qk in (cc.plan_qk(dims["L"], dims["H"], dims["d"] // dims["H"], n), cc.plan_sv(dims["L"], dims["H"], n)):
-        qc = qk.counts()
-        acc3 = qk.accumulators()
-        qk_masks = qk.J * qk.B * (2 * qk.g - 1) + 2 * qk.J * (qk.G - 1) + sum(
-            1 for (u, w, f) in acc3 for i in range(qk.B) if qk.mask3(u, i, w, f).any())
-        n_rot += qc["rotations"] + qc["relin"]            # relinearisation ~ one key switch
-        n_pt += qk_masks + 3 * qc["cmult"]                # tensor ~ 3 ct-pt products
-        n_out += qk.J * (qk.B + qk.G) + qk.G * qk.B + len(acc3)
-    qk0 = cc.plan_qk(dims["L"], dims["H"], dims["d"] // dims["H"], n)
-    n_mask += qk0.n_out - 2 * qk0.J          # Q, K outputs of QKV feed Q K^T; its diagonals are masked
-    ms = 1e3 * (n_rot * t["rot"] + n_pt * t["prod"] + n_out * t["resc"] + n_mask * t["mask"])
-    return {"ms_per_layer": ms, "per_op_s": t, "counts": {"rotations": n_rot, "plaintexts": n_pt,
-                                                          "rescales": n_out, "masks": n_mask},
-            "sample": "oracle at N=2^16, level 4 (k=5): 1 hoisted rotation + %d ct-pt products + 1 rescale + 1 mask "
-                      "per rep, x%d reps; extrapolated by the layer's operation counts (%d key switches, %d ct-pt "
-                      "product equivalents, %d rescales, %d masks; all at k=5, an upper bound for the lower-level "
-                      "Q.K^T stages)" % (n_prod, reps, n_rot, n_pt, n_out, n_mask)}
+    ct3 = O.Ct(rnd(2, range(4)), 3, 2.0 ** 40)
+    t = {}
+    t0 = time.perf_counter()
+    O.rotate(ctx, ct, keys, 128)
+    t1 = time.perf_counter()
+    acc = O.mul_pt(ctx, ct, pts[0], 1.0)
+    for p in pts[1:]:
+        acc = O.add(ctx, acc, O.mul_pt(ctx, ct, p, 1.0))
+    t2 = time.perf_counter()
+    ye = O.rotate_ext(ctx, acc, keys, 64 * 128)
+    t3 = time.perf_counter()
+    y = O.moddown_rescale(ctx, ye)
+    t4 = time.perf_counter()
+    dsum = None
+    for _ in range(4):
+        tt = O.tensor(ctx, ct3, ct3)
+        dsum = tt if dsum is None else O.add(ctx, dsum, tt)
+    t5 = time.perf_counter()
+    O.moddown_rescale(ctx, O.relinearize_ext(ctx, dsum, keys))
+    t6 = time.perf_counter()
+    O.mask(ctx, y, bytes(32), 0)
+    t7 = time.perf_counter()
+    t = {"rotation": t1 - t0, "prod": (t2 - t1) / n_prod, "rotate_ext": t3 - t2, "mdr": t4 - t3,
+         "tensor": (t5 - t4) / 4, "relin_ext+mdr": t6 - t5, "mask": t7 - t6}
+    return {"ms": 1e3 * (t7 - t0), "per_op_s": t, "threads": threads}
 
 
-def omp_threads() -> int:
-    v = os.environ.get("OMP_NUM_THREADS")
-    return int(v) if v and v.isdigit() else (os.cpu_count() or 1)
+def slice_desc() -> str:
+    return ("oracle (u128 C + __float128, OpenMP) at N=2^16, k=5, directly timed per slice: 1 baby-step rotation "
+            "(ModUp + key switch + ModDown) + one FFN1 (b',g) MAC unit (192 ct-pt products) + its giant step in Q u P "
+            "with the fused ModDown/rescale + one Q.K^T (u,i) stage (4 tensor products + relinearisation + "
+            "ModDown/rescale) + 1 CKKS->MPC mask")
+
+
+def layer_estimate_ms(per_op: dict, counts: dict) -> float:
+    """Layer-equivalent of the timed slice: each timed operation kind times its count in one layer
+    step (every key switch at the full rotation's cost: an upper bound for the hoisted ones)."""
+    return 1e3 * (counts["ks"] * per_op["rotation"] + counts["prod"] * per_op["prod"] +
+                  counts["mdr"] * per_op["mdr"] + counts["tensor"] * per_op["tensor"] +
+                  counts["mask"] * per_op["mask"])
+
+
+def cpu_baseline(dims) -> dict:
+    """The oracle timed on the host: the slice at 1 thread and at all cores (bounded, ~10-30 s)."""
+    info = cpu_info()
+    allc = info["nproc"]
+    oracle_slice(allc)                       # warm: library load, table build
+    ra = oracle_slice(allc)
+    r1 = oracle_slice(1)
+    counts = layer_counts(dims)
+    return {"value": ra["ms"], "unit": "ms per slice", "cores": allc, "kind": "oracle", "sample": slice_desc(),
+            "ms_per_slice_1thread": r1["ms"], "cpu_model": info["cpu_model"], "nproc": info["nproc"],
+            "per_op_s_all_cores": ra["per_op_s"], "per_op_s_1thread": r1["per_op_s"],
+            "layer_counts": counts,
+            "ms_per_layer_est_all_cores": layer_estimate_ms(ra["per_op_s"], counts),
+            "ms_per_layer_est_1thread": layer_estimate_ms(r1["per_op_s"], counts),
+            "estimate_how": "sum over operation kinds of (directly timed op time x its count per layer step)"}
 
 
 def run_reference(args, dims):
-    """--impl reference: the oracle timed on host cores, each step a bounded sample."""
-    samples = []
+    """--impl reference: the oracle timed on host cores (all of them), each step one slice of the
+    layer (oracle_slice).  ms_per_step is the timed slice; value is its layer-equivalent in the
+    metric's unit (each timed operation times its count per layer step, stated in the line)."""
+    info = cpu_info()
+    counts = layer_counts(dims)
+    oracle_slice(info["nproc"])               # warm-up outside the timed steps (library load, tables)
+    steps, ests = [], []
     for s in range(args.warmup + args.steps):
-        r = oracle_sample_ms(dims, reps=1)
+        r = oracle_slice(info["nproc"])
         if s >= args.warmup:
-            samples.append(r["ms_per_layer"])
-    v = float(np.median(samples))
-    line = {"impl": "reference", "metric": metric_name(dims), "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            steps.append(r["ms"])
+            ests.append(layer_estimate_ms(r["per_op_s"], counts))
+    ms_step = float(np.median(steps))
+    v = float(np.median(ests))
+    line = {"impl": "reference", "metric": metric_name(dims), "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": config_dict(dims, args.gpus),
-            "cpu_baseline": {"kind": "oracle", "value": v, "unit": UNIT, "cores": omp_threads(),
-                             "sample": r["sample"]},
+            "timed_region": "each step = one directly timed oracle slice (ms_per_step); value = that slice's "
+                            "layer-equivalent (layer_counts x per-op times)",
+            "layer_counts": counts,
+            "cpu_baseline": {"kind": "oracle", "value": v, "unit": UNIT, "cores": info["nproc"],
+                             "cpu_model": info["cpu_model"], "sample": slice_desc(), "ms_per_slice": ms_step},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -210,6 +273,27 @@ def config_dict(dims, world):
             "not_included": "non-MatMul HE ops of Table 6 blocks 2-5 (row f2) and the MPC protocols",
             "l2": "inputs larger than L2 (%s of plaintexts streamed per step)" % ("~57 GB" if dims["d"] == 768 else "~91 GB"),
             "parallelism": "dp%d (output-ciphertext sharding, NCCL all-gather of masked outputs)" % world}
+
+
+def ntt_pipes(ctr: dict, ntt: dict, params, pipes: dict, steps: int) -> dict:
+    """The NTT's arithmetic-pipe fraction next to its HBM fraction: algorithmic
+    ops per butterfly -- 60-bit rows (integer kernel, truncated-quotient Shoup): 9 IMAD-class
+    multiplies (3 for the quotient, 3 + 3 for the two low 64-bit products); 40-bit rows (FP64
+    kernel): 8 FP64 ops (DMUL, 3 DFMA, 2 DADD in the product, DADD + DSUB in the butterfly) --
+    times the measured pipe peaks, against the live NTT time."""
+    if not ntt["ms"]:
+        return {}
+    bfly = (params.N // 2) * params.log_n
+    n_all, n_int = ctr["limb_ntts"], ctr.get("limb_ntts_int", 0)
+    t_int = n_int * bfly * 9 / pipes["imad_per_s"]
+    t_f64 = (n_all - n_int) * bfly * 8 / pipes["dfma_per_s"]
+    t = ntt["ms"] * 1e-3
+    return {"rows_int_per_step": n_int / steps, "rows_fp64_per_step": (n_all - n_int) / steps,
+            "pipe_peaks": pipes, "pipe_bound_ms_per_step": 1e3 * (t_int + t_f64) / steps,
+            "pipe_frac": (t_int + t_f64) / t,
+            "pipe_frac_how": "(int rows x 9 IMAD + FP64 rows x 8 FP64 ops per butterfly) at the measured peaks, "
+                             "the two pipes taken one after the other, / live NTT time",
+            "hbm_frac": ntt["alg_bytes"] / t / 1e9 / float(measured_peaks().get("hbm_gbs", FALLBACK_HBM))}
 
 
 # --------------------------------------------------------------------------- our arm
@@ -299,6 +383,7 @@ def main():
         step()
     torch.cuda.synchronize()
 
+    pipes = blb.pipe_peaks(local)   # measured IMAD / DFMA peaks (NTT pipe-fraction denominators)
     # ---- timed region (device events; max over ranks) ----
     blb.reset_counters()
     blb.timing_reset()
@@ -395,7 +480,8 @@ def main():
                      "alg_bytes_per_launch": mac["alg_bytes"] / max(1, mac["launches"]),
                      "ms_per_launch": mac["ms"] / max(1, mac["launches"]),
                      "share_of_step": mac["ms"] / ms_total if ms_total else None},
-        "ntt": {"limbs_per_s": (ntt["alg_bytes"] / (16.0 * params.N)) / (ntt["ms"] * 1e-3) if ntt["ms"] else None,
+        "ntt": {**ntt_pipes(ctr, ntt, params, pipes, args.steps),
+                "limbs_per_s": (ntt["alg_bytes"] / (16.0 * params.N)) / (ntt["ms"] * 1e-3) if ntt["ms"] else None,
                 "alg_gbs": ntt["alg_bytes"] / (ntt["ms"] * 1e-3) / 1e9 if ntt["ms"] else None,
                 "share_of_step": ntt["ms"] / ms_total if ms_total else None, "launches": ntt["launches"]},
         "ks_inner": {"alg_gbs": ksi["alg_bytes"] / (ksi["ms"] * 1e-3) / 1e9 if ksi["ms"] else None,
@@ -414,9 +500,7 @@ def main():
         "e2e": e2e,
     }
     if world == 1 and not args.no_cpu_baseline:
-        r = oracle_sample_ms(dims, reps=1)
-        line["cpu_baseline"] = {"value": r["ms_per_layer"], "unit": UNIT, "cores": omp_threads(), "kind": "oracle",
-                                "sample": r["sample"]}
+        line["cpu_baseline"] = cpu_baseline(dims)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

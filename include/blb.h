@@ -82,8 +82,9 @@ const char *blb_last_error(void);
 
 /* Process-wide counters: [0] kernel launches, [1] key switches (rotations +
  * relinearisations), [2] limb NTT/INTT transforms, [3] ct-pt products,
- * [4] rescales, [5] masks.  Host memory out[6]. */
-void blb_counters_get(uint64_t out[6]);
+ * [4] rescales, [5] masks, [6] limb transforms on primes >= 2^41 (integer NTT kernel),
+ * [7] reserved (0).  Host memory out[8]. */
+void blb_counters_get(uint64_t out[8]);
 void blb_counters_reset(void);
 
 /* Live kernel timing (bench instrumentation).  When enabled, the library
@@ -94,6 +95,12 @@ void blb_counters_reset(void);
  * number of launches and the summed ALGORITHMIC bytes (MAC: k*N*8 per
  * plaintext; NTT: 2*N*8 per limb; inner product: 2*beta*(k+np)*N*8 key bytes
  * per key switch).  Host outputs, nullable. */
+/* Measured arithmetic-pipe peaks of device `device` (the integer-pipe fraction of the
+ * NTT needs a denominator measured on the box): ops/s of 32-bit IMAD (fma-heavy pipe, mad.lo.u32)
+ * and of DFMA (FP64 pipe), best of 3 timed launches of independent dependency chains, 8 CTAs per
+ * SM.  Benchmark instrumentation, not a hot-path call; synchronises.  BLB_E_INVALID_ARG on null
+ * outputs, BLB_E_CUDA on a CUDA error. */
+blb_status blb_measure_pipe_peaks(int device, double *imad_per_s, double *dfma_per_s, void *stream);
 void blb_timing_enable(int on);
 void blb_timing_reset(void);
 blb_status blb_timing_read(int category, double *total_ms, uint64_t *launches, double *alg_bytes);

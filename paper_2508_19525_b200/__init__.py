@@ -56,6 +56,7 @@ def lib() -> ctypes.CDLL:
             "blb_counters_get": ([vp], None),
             "blb_counters_reset": ([], None),
             "blb_timing_enable": ([ctypes.c_int], None),
+            "blb_measure_pipe_peaks": ([ctypes.c_int, vp, vp, vp], ctypes.c_int),
             "blb_timing_reset": ([], None),
             "blb_timing_read": ([ctypes.c_int, vp, vp, vp], ctypes.c_int),
             "blb_prime_chain": ([ctypes.c_int, vp, ctypes.c_int, vp], ctypes.c_int),
@@ -134,9 +135,9 @@ def _ptr(t: torch.Tensor):
 
 
 def counters() -> dict:
-    out = (ctypes.c_uint64 * 6)()
+    out = (ctypes.c_uint64 * 8)()
     lib().blb_counters_get(out)
-    names = ["launches", "keyswitches", "limb_ntts", "ct_pt_products", "rescales", "masks"]
+    names = ["launches", "keyswitches", "limb_ntts", "ct_pt_products", "rescales", "masks", "limb_ntts_int"]
     return {n: int(v) for n, v in zip(names, out)}
 
 
@@ -145,6 +146,13 @@ def reset_counters():
 
 
 TIMING_MAC, TIMING_NTT, TIMING_KS_INNER, TIMING_MASK_MAC, TIMING_TENSOR = 0, 1, 2, 3, 4
+
+
+def pipe_peaks(device: int = 0) -> dict:
+    """Measured IMAD (fma-heavy pipe) and DFMA (FP64 pipe) ops/s of the device (bench denominators)."""
+    a, b = ctypes.c_double(), ctypes.c_double()
+    _check(lib().blb_measure_pipe_peaks(int(device), ctypes.byref(a), ctypes.byref(b), _stream()))
+    return {"imad_per_s": a.value, "dfma_per_s": b.value}
 
 
 def timing_enable(on: bool = True):

@@ -12,7 +12,7 @@ SO = os.path.join(HERE, "libblb.so")
 # compile-time kernel variants for A/B measurements are separate files: build(defines=[...], out=path)
 ROOT = os.path.dirname(HERE)
 
-CU = ["ntt.cu", "kernels.cu", "encode.cu", "matmul.cu", "qk.cu", "api.cu"]
+CU = ["ntt.cu", "kernels.cu", "encode.cu", "matmul.cu", "qk.cu", "api.cu", "peaks.cu"]
 CPP = ["host_tables.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -39,7 +39,7 @@ blb_status blb_launch_mask(const blb_params *P, const u64 *const *in, int n, int
 
 // ------------------------------------------------------------ errors
 static thread_local char g_err[512] = "";
-unsigned long long g_blb_counters[6] = {0, 0, 0, 0, 0, 0};
+unsigned long long g_blb_counters[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
 void blb_set_error(const char *fmt, ...) {
     va_list ap;
@@ -48,11 +48,11 @@ void blb_set_error(const char *fmt, ...) {
     va_end(ap);
 }
 extern "C" const char *blb_last_error(void) { return g_err; }
-extern "C" void blb_counters_get(uint64_t out[6]) {
-    for (int i = 0; i < 6; i++) out[i] = __atomic_load_n(&g_blb_counters[i], __ATOMIC_RELAXED);
+extern "C" void blb_counters_get(uint64_t out[8]) {
+    for (int i = 0; i < 8; i++) out[i] = __atomic_load_n(&g_blb_counters[i], __ATOMIC_RELAXED);
 }
 extern "C" void blb_counters_reset(void) {
-    for (int i = 0; i < 6; i++) __atomic_store_n(&g_blb_counters[i], 0ull, __ATOMIC_RELAXED);
+    for (int i = 0; i < 8; i++) __atomic_store_n(&g_blb_counters[i], 0ull, __ATOMIC_RELAXED);
 }
 
 // ------------------------------------------------------------ live timing

@@ -338,7 +338,7 @@ struct blb_keys {
 // error plumbing
 // ---------------------------------------------------------------------------
 void blb_set_error(const char *fmt, ...);
-extern unsigned long long g_blb_counters[6];
+extern unsigned long long g_blb_counters[8];
 #define BLB_COUNT_LAUNCH(n) (__atomic_fetch_add(&g_blb_counters[0], (unsigned long long)(n), __ATOMIC_RELAXED))
 #define BLB_COUNT(i, n) (__atomic_fetch_add(&g_blb_counters[i], (unsigned long long)(n), __ATOMIC_RELAXED))
 

@@ -455,6 +455,13 @@ static int split_rows(const blb_params *P, const RowBatch &rb, RowBatch out[2]) 
     if (g.nsel) { if (g.nsel == rb.limbs) g.nsel = 0; out[n++] = g; }
     return n;
 }
+// rows of a batch on primes >= 2^41 (the integer NTT kernel): counter [6]
+static long long rb_int_rows(const blb_params *P, const RowBatch &r) {
+    int n = 0;
+    const int nl = r.nsel ? r.nsel : r.limbs;
+    for (int i = 0; i < nl; i++) n += P->mod[r.prime[r.nsel ? r.sel[i] : i]] >= (1ull << 41);
+    return (long long)n * r.n_polys;
+}
 static inline bool rb_small(const blb_params *P, const RowBatch &r) {
     return P->mod[r.prime[r.nsel ? r.sel[0] : 0]] < (1ull << 41);
 }
@@ -505,6 +512,7 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
         return BLB_OK;
     }
     BLB_COUNT(2, rows);
+    BLB_COUNT(6, rb_int_rows(P, rb));
     cudaEvent_t t0 = blb_timing_begin(st);
     const double alg = (double)rows * 2.0 * 8.0 * (double)(1 << logN);
     if (logN <= 12) {
@@ -583,6 +591,7 @@ blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool invers
         return BLB_E_INVALID_ARG;
     }
     BLB_COUNT(2, rows);
+    BLB_COUNT(6, rb_int_rows(P, rb));
     cudaEvent_t t0 = blb_timing_begin(st);
     RowBatch parts[2];
     const int np2 = split_rows(P, rb, parts);
