@@ -12,8 +12,10 @@ its dense-diagonal collapse feeding the out-projection.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 is launched by torchrun (one rank per GPU, NCCL): outputs are sharded
-by output ciphertext, baby steps replicated, masked results all-gathered.
+N > 1 is launched by torchrun (one rank per GPU, NCCL; bench.py --gpus N spawns it when run
+directly): every MatMul is sharded by BSGS baby-step window, the partial accumulators are
+summed exactly by one NCCL all-reduce, each output's owner finishes and masks it, and the
+masked results are all-gathered.
 """
 from __future__ import annotations
 
@@ -272,7 +274,9 @@ def config_dict(dims, world):
                           "ffn2_ct_pt", "mask"],
             "not_included": "non-MatMul HE ops of Table 6 blocks 2-5 (row f2) and the MPC protocols",
             "l2": "inputs larger than L2 (%s of plaintexts streamed per step)" % ("~57 GB" if dims["d"] == 768 else "~91 GB"),
-            "parallelism": "dp%d (output-ciphertext sharding, NCCL all-gather of masked outputs)" % world}
+            "parallelism": ("dp%d: every MatMul sharded by BSGS baby-step window, exact NCCL all-reduce of the "
+                            "partial accumulators, owners finish + mask their output ciphertexts, NCCL all-gathers "
+                            "(Q/K, Softmax.V outputs, masked results)" % world) if world > 1 else "dp1"}
 
 
 def ntt_pipes(ctr: dict, ntt: dict, params, pipes: dict, steps: int) -> dict:
@@ -309,7 +313,18 @@ def main():
     args = ap.parse_args()
     dims = dict(L=128, d=768, H=12, ffn=3072) if args.dims == "base" else dict(L=128, d=1024, H=16, ffn=4096)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launched directly with --gpus N: spawn one rank per GPU (the driver launches through torchrun)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print("bench.py: --gpus %d but WORLD_SIZE=%d; using the launched world" % (args.gpus, world), file=sys.stderr)
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":

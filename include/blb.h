@@ -281,6 +281,16 @@ blb_status blb_matmul_plan_create(const blb_params *params, int L, int w_rows, i
                                   int heads, const int32_t *col_map, int D_out, int bsgs_B, int level,
                                   blb_matmul_plan **out);
 void blb_matmul_plan_destroy(blb_matmul_plan *plan);
+/* Multi-GPU form: the plan restricted to the baby-step window
+ * i in [i_first, i_first + i_count) of [0, B) (i_count = -1: to B).  Its plaintexts, baby steps and
+ * MAC entries are those of the window; its giant steps are the whole plan's.  Windows of the ranks
+ * partition [0, B): the MAC accumulators of all windows sum (exactly, mod q_l) to those of the
+ * whole plan, so blb_ct_pt_matmul_acc on every rank + a cross-rank sum + blb_ct_pt_matmul_finish
+ * at each output's owner gives the bits of blb_ct_pt_matmul at any number of ranks.
+ * BLB_E_INVALID_ARG for a window outside [0, B). */
+blb_status blb_matmul_plan_create_window(const blb_params *params, int L, int w_rows, int w_cols,
+                                         blb_packing packing, int heads, const int32_t *col_map, int D_out,
+                                         int bsgs_B, int level, int i_first, int i_count, blb_matmul_plan **out);
 
 /* Host outputs (nullable): number of input / output ciphertexts, total
  * non-zero plaintexts, baby / giant rotations, B, G. */
@@ -319,6 +329,22 @@ size_t blb_matmul_workspace_bytes(const blb_matmul_plan *plan, int out_count);
 blb_status blb_ct_pt_matmul(const blb_matmul_plan *plan, const blb_keys *keys, const blb_ct *in, int n_in,
                             const uint64_t *pt_dev, int out_first, int out_count, blb_ct *out, void *ws,
                             size_t ws_bytes, void *stream);
+
+/* The two phases of blb_ct_pt_matmul for a windowed plan (multi-GPU):
+ * _acc: hoisted ModUp of the inputs, the window's baby-step rotations and the MAC of its
+ *   plaintexts (pt_dev encoded for ALL outputs of the windowed plan) into acc_out, device
+ *   [n_out][G][2][level+1][N] u64 (NTT form, residues < q_i; entries the window does not touch are
+ *   0).  Needs the window's baby-step keys.  ws: blb_matmul_workspace_bytes(plan, 0).
+ * _finish: outputs [out_first, out_first + out_count) from acc_in, device
+ *   [out_count][G][2][level+1][N] u64 holding the SUM over the windows (u64 sums of residues,
+ *   < 2^64, reduced mod q_i here): giant steps in Q_l u P, the fused ModDown + rescale (C11, C17),
+ *   out[t] at level-1 with scale `scale` (the input scale).  Needs the giant-step keys.
+ *   ws: blb_matmul_workspace_bytes(plan, out_count).  acc_in is not modified. */
+blb_status blb_ct_pt_matmul_acc(const blb_matmul_plan *plan, const blb_keys *keys, const blb_ct *in, int n_in,
+                                const uint64_t *pt_dev, uint64_t *acc_out, void *ws, size_t ws_bytes, void *stream);
+blb_status blb_ct_pt_matmul_finish(const blb_matmul_plan *plan, const blb_keys *keys, const uint64_t *acc_in,
+                                   int out_first, int out_count, double scale, blb_ct *out, void *ws, size_t ws_bytes,
+                                   void *stream);
 
 /* ------------------------------------------------------------------ */
 /* row f2: other HE operators of the fused blocks                       */
@@ -376,6 +402,31 @@ size_t blb_qk_workspace_bytes(const blb_qk_plan *plan);
  * the scale of the prime their rescale drops). */
 blb_status blb_ct_ct_qk(const blb_qk_plan *plan, const blb_keys *keys, const blb_ct *Q, const blb_ct *K, int J,
                         const uint64_t *masks, blb_ct *out, void *ws, size_t ws_bytes, void *stream);
+
+/* Multi-GPU form: the plan restricted to the baby-index window
+ * i in [i_first, i_first + i_count) of [0, B) (i_count = -1: to B).  Windows of the ranks
+ * partition [0, B); the step-3 accumulators A_{u,w,f} (reading C13, before their ModDown +
+ * rescale) of all windows sum exactly (mod each prime of Q_{level-2} u P) to those of the whole
+ * plan, so blb_ct_ct_qk_acc on every rank + a cross-rank sum + blb_ct_ct_qk_finish at each
+ * output's owner gives the bits of blb_ct_ct_qk at any number of ranks. */
+blb_status blb_qk_plan_create_window(const blb_params *params, int L, int heads, int d_h, int bsgs_B, int level,
+                                     int i_first, int i_count, blb_qk_plan **out);
+/* Bytes of the accumulator array: [NA][2][level-1+np][N] u64, accumulators sorted by output. */
+size_t blb_qk_acc_bytes(const blb_qk_plan *plan);
+/* Accumulator slots [*slot_first, *slot_first + *slot_count) that outputs [out_first, +out_count)
+ * read (host outputs). */
+blb_status blb_qk_acc_range(const blb_qk_plan *plan, int out_first, int out_count, int *slot_first, int *slot_count);
+/* Phase A: the window's stages 1-3 (K'_i for i in the window, every Q_u, products, relinearisation,
+ * step-3 rotations and masks) into acc_out (device, blb_qk_acc_bytes; residues < q_i).
+ * Phase B: outputs [out_first, +out_count) from acc_in = the cross-rank SUM of the accumulator
+ * slots blb_qk_acc_range gives (u64 sums < 2^64 of residues, reduced here; acc_in points at the
+ * first of those slots): ModDown + rescale (C17), deferred giant rotations, one ModDown per output.
+ * scale_q / scale_k: the operands' scales.  Both need the plan's keys; ws: blb_qk_workspace_bytes. */
+blb_status blb_ct_ct_qk_acc(const blb_qk_plan *plan, const blb_keys *keys, const blb_ct *Q, const blb_ct *K, int J,
+                            const uint64_t *masks, uint64_t *acc_out, void *ws, size_t ws_bytes, void *stream);
+blb_status blb_ct_ct_qk_finish(const blb_qk_plan *plan, const blb_keys *keys, const uint64_t *acc_in, int out_first,
+                               int out_count, double scale_q, double scale_k, blb_ct *out, void *ws, size_t ws_bytes,
+                               void *stream);
 
 #ifdef __cplusplus
 }

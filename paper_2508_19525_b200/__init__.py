@@ -90,6 +90,12 @@ def lib() -> ctypes.CDLL:
             "blb_matmul_plan_create": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp,
                                         ctypes.c_int, ctypes.c_int, ctypes.c_int, vp], ctypes.c_int),
             "blb_matmul_plan_destroy": ([vp], None),
+            "blb_matmul_plan_create_window": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                               vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                               vp], ctypes.c_int),
+            "blb_ct_pt_matmul_acc": ([vp, vp, vp, ctypes.c_int, vp, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
+            "blb_ct_pt_matmul_finish": ([vp, vp, vp, ctypes.c_int, ctypes.c_int, dbl, vp, vp, ctypes.c_size_t, vp],
+                                        ctypes.c_int),
             "blb_matmul_plan_info": ([vp, ip, ip, ip, ip, ip, ip, ip], ctypes.c_int),
             "blb_matmul_plan_rotations": ([vp, vp, ip], ctypes.c_int),
             "blb_matmul_pt_count": ([vp, ctypes.c_int, ctypes.c_int, ip], ctypes.c_int),
@@ -111,6 +117,12 @@ def lib() -> ctypes.CDLL:
             "blb_qk_encode_masks": ([vp, vp, vp], ctypes.c_int),
             "blb_qk_workspace_bytes": ([vp], ctypes.c_size_t),
             "blb_ct_ct_qk": ([vp, vp, vp, vp, ctypes.c_int, vp, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
+            "blb_qk_plan_create_window": ([vp] + [ctypes.c_int] * 7 + [vp], ctypes.c_int),
+            "blb_qk_acc_bytes": ([vp], ctypes.c_size_t),
+            "blb_qk_acc_range": ([vp, ctypes.c_int, ctypes.c_int, ip, ip], ctypes.c_int),
+            "blb_ct_ct_qk_acc": ([vp, vp, vp, vp, ctypes.c_int, vp, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
+            "blb_ct_ct_qk_finish": ([vp, vp, vp, ctypes.c_int, ctypes.c_int, dbl, dbl, vp, vp, ctypes.c_size_t, vp],
+                                    ctypes.c_int),
         }
         for name, (args, res) in sigs.items():
             f = getattr(L, name)
@@ -444,8 +456,11 @@ class MatmulPlan:
     """blb_matmul_plan_create (C11 spatial / C12 diagonal ct-pt MatMul with BSGS)."""
 
     def __init__(self, params: Params, L: int, w_rows: int, w_cols: int, packing: int = PACK_SPATIAL, heads: int = 1,
-                 col_map=None, bsgs_B: int = 16, level: int | None = None):
+                 col_map=None, bsgs_B: int = 16, level: int | None = None, window: tuple | None = None):
+        """window = (i_first, i_count): the plan restricted to a baby-step window (multi-GPU, DESIGN
+        section 8); None = the whole plan."""
         self.params = params
+        self.window = window
         self.level = params.K - 1 if level is None else level
         self.w_shape = (w_rows, w_cols)
         cm = None
@@ -454,8 +469,13 @@ class MatmulPlan:
             cm = (ctypes.c_int32 * len(col_map))(*col_map)
             d_out = len(col_map)
         h = ctypes.c_void_p()
-        _check(lib().blb_matmul_plan_create(params.handle, L, w_rows, w_cols, packing, heads, cm, d_out, bsgs_B,
-                                            self.level, ctypes.byref(h)))
+        if window is None:
+            _check(lib().blb_matmul_plan_create(params.handle, L, w_rows, w_cols, packing, heads, cm, d_out, bsgs_B,
+                                                self.level, ctypes.byref(h)))
+        else:
+            _check(lib().blb_matmul_plan_create_window(params.handle, L, w_rows, w_cols, packing, heads, cm, d_out,
+                                                       bsgs_B, self.level, int(window[0]), int(window[1]),
+                                                       ctypes.byref(h)))
         self._h = h
         vals = [ctypes.c_int() for _ in range(7)]
         _check(lib().blb_matmul_plan_info(h, *[ctypes.byref(v) for v in vals]))
@@ -517,15 +537,52 @@ class MatmulPlan:
             o.level, o.scale = c.level, c.scale
         return outs
 
+    def acc_numel(self, n_out: int | None = None) -> int:
+        """u64 words of the MAC accumulators of n_out outputs: [n_out][G][2][level+1][N]."""
+        n_out = self.n_out if n_out is None else n_out
+        return n_out * self.G * 2 * (self.level + 1) * self.params.N
+
+    def acc(self, keys: Keys, cts: list, pts: torch.Tensor, acc_out: torch.Tensor | None = None,
+            ws: torch.Tensor | None = None) -> torch.Tensor:
+        """blb_ct_pt_matmul_acc: baby steps + MAC of this plan's window for every output."""
+        ws = self.workspace(0) if ws is None else ws
+        acc_out = torch.empty(self.acc_numel(), dtype=torch.int64, device="cuda") if acc_out is None else acc_out
+        assert acc_out.numel() >= self.acc_numel()
+        cin = (_Ct * len(cts))(*[c.c() for c in cts])
+        _check(lib().blb_ct_pt_matmul_acc(self._h, keys.handle, cin, len(cts), _ptr(pts), _ptr(acc_out), _ptr(ws),
+                                          ws.numel() * 8, _stream()))
+        return acc_out
+
+    def finish(self, keys: Keys, acc_in: torch.Tensor, out_first: int, out_count: int, scale: float,
+               ws: torch.Tensor | None = None, outs: list | None = None) -> list:
+        """blb_ct_pt_matmul_finish: giant steps + ModDown/rescale of outputs [out_first, +out_count) from
+        the cross-rank SUM of their accumulators."""
+        ws = self.workspace(out_count) if ws is None else ws
+        if outs is None:
+            outs = [Ciphertext.empty(self.params, self.level - 1) for _ in range(out_count)]
+        cout = (_Ct * max(1, out_count))(*[o.c() for o in outs])
+        _check(lib().blb_ct_pt_matmul_finish(self._h, keys.handle, _ptr(acc_in), out_first, out_count, float(scale),
+                                             cout, _ptr(ws), ws.numel() * 8, _stream()))
+        for o, c in zip(outs, cout):
+            o.level, o.scale = c.level, c.scale
+        return outs
+
 
 class QKPlan:
     """blb_qk_plan_create: ct-ct MatMul Q_h K_h^T for all heads (row a7, reading C13)."""
 
-    def __init__(self, params: Params, L: int, heads: int, d_h: int, bsgs_B: int = 0, level: int | None = None):
+    def __init__(self, params: Params, L: int, heads: int, d_h: int, bsgs_B: int = 0, level: int | None = None,
+                 window: tuple | None = None):
+        """window = (i_first, i_count): the plan restricted to a baby-index window (multi-GPU)."""
         self.params = params
         self.level = params.K - 2 if level is None else level
+        self.window = window
         h = ctypes.c_void_p()
-        _check(lib().blb_qk_plan_create(params.handle, L, heads, d_h, bsgs_B, self.level, ctypes.byref(h)))
+        if window is None:
+            _check(lib().blb_qk_plan_create(params.handle, L, heads, d_h, bsgs_B, self.level, ctypes.byref(h)))
+        else:
+            _check(lib().blb_qk_plan_create_window(params.handle, L, heads, d_h, bsgs_B, self.level, int(window[0]),
+                                                   int(window[1]), ctypes.byref(h)))
         self._h = h
         vals = [ctypes.c_int() for _ in range(7)]
         _check(lib().blb_qk_plan_info(h, *[ctypes.byref(v) for v in vals]))
@@ -562,6 +619,40 @@ class QKPlan:
         co = (_Ct * self.n_out)(*[o.c() for o in outs])
         _check(lib().blb_ct_ct_qk(self._h, keys.handle, cq, ck, len(Q), _ptr(masks), co, _ptr(ws), ws.numel() * 8,
                                   _stream()))
+        for o, c in zip(outs, co):
+            o.level, o.scale = c.level, c.scale
+        return outs
+
+    def acc_numel(self) -> int:
+        return int(lib().blb_qk_acc_bytes(self._h)) // 8
+
+    def acc_range(self, out_first: int, out_count: int) -> tuple:
+        """Accumulator slots (first, count) read by outputs [out_first, out_first + out_count)."""
+        a, b = ctypes.c_int(), ctypes.c_int()
+        _check(lib().blb_qk_acc_range(self._h, out_first, out_count, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def acc(self, keys: Keys, Q: list, K: list, masks: torch.Tensor, acc_out: torch.Tensor | None = None,
+            ws: torch.Tensor | None = None) -> torch.Tensor:
+        """blb_ct_ct_qk_acc: this window's step-3 accumulators (before ModDown + rescale)."""
+        ws = torch.empty(self.workspace_bytes() // 8 + 1, dtype=torch.int64, device="cuda") if ws is None else ws
+        acc_out = torch.empty(self.acc_numel(), dtype=torch.int64, device="cuda") if acc_out is None else acc_out
+        cq = (_Ct * len(Q))(*[c.c() for c in Q])
+        ck = (_Ct * len(K))(*[c.c() for c in K])
+        _check(lib().blb_ct_ct_qk_acc(self._h, keys.handle, cq, ck, len(Q), _ptr(masks), _ptr(acc_out), _ptr(ws),
+                                      ws.numel() * 8, _stream()))
+        return acc_out
+
+    def finish(self, keys: Keys, acc_in: torch.Tensor, out_first: int, out_count: int, scale_q: float, scale_k: float,
+               ws: torch.Tensor | None = None, outs: list | None = None) -> list:
+        """blb_ct_ct_qk_finish: outputs [out_first, +out_count) from the summed accumulator slots
+        acc_range(out_first, out_count) (acc_in starts at the first of them)."""
+        ws = torch.empty(self.workspace_bytes() // 8 + 1, dtype=torch.int64, device="cuda") if ws is None else ws
+        if outs is None:
+            outs = [Ciphertext.empty(self.params, self.level - 3) for _ in range(out_count)]
+        co = (_Ct * max(1, out_count))(*[o.c() for o in outs])
+        _check(lib().blb_ct_ct_qk_finish(self._h, keys.handle, _ptr(acc_in), out_first, out_count, float(scale_q),
+                                         float(scale_k), co, _ptr(ws), ws.numel() * 8, _stream()))
         for o, c in zip(outs, co):
             o.level, o.scale = c.level, c.scale
         return outs

@@ -28,6 +28,7 @@ extern "C" u64 blbh_shoup(u64 w, u64 q);
 struct blb_matmul_plan {
     const blb_params *P;
     int L, n, c, w_rows, w_cols, nblk_in, D_out, n_in, n_out, B, G, level, packing, heads, dh;
+    int i_first = 0, i_count = 0;                       // baby-step window of this rank (section 8(e))
     std::vector<int32_t> col_map;                       // D_out entries, -1 = zero column
     std::vector<int> ent_start;                         // CSR over (b', g): n_out*G + 1
     std::vector<int> ent_b, ent_i;                      // entries in plan order
@@ -524,6 +525,14 @@ static bool nz_entry(const blb_matmul_plan *pl, int b, int bp, int t) {
 extern "C" blb_status blb_matmul_plan_create(const blb_params *P, int L, int w_rows, int w_cols, blb_packing packing,
                                              int heads, const int32_t *col_map, int D_out, int bsgs_B, int level,
                                              blb_matmul_plan **out) {
+    return blb_matmul_plan_create_window(P, L, w_rows, w_cols, packing, heads, col_map, D_out, bsgs_B, level, 0, -1,
+                                         out);
+}
+
+extern "C" blb_status blb_matmul_plan_create_window(const blb_params *P, int L, int w_rows, int w_cols,
+                                                    blb_packing packing, int heads, const int32_t *col_map, int D_out,
+                                                    int bsgs_B, int level, int i_first, int i_count,
+                                                    blb_matmul_plan **out) {
     if (!P || !out || L <= 0 || w_rows <= 0 || w_cols <= 0 || bsgs_B <= 0) {
         blb_set_error("blb_matmul_plan_create: invalid argument");
         return BLB_E_INVALID_ARG;
@@ -542,6 +551,15 @@ extern "C" blb_status blb_matmul_plan_create(const blb_params *P, int L, int w_r
     pl->packing = packing; pl->level = level; pl->heads = heads > 0 ? heads : 1;
     pl->B = std::min(bsgs_B, pl->c);
     pl->G = (pl->c + pl->B - 1) / pl->B;
+    if (i_count < 0) i_count = pl->B - i_first;
+    if (i_first < 0 || i_first + i_count > pl->B) {
+        blb_set_error("blb_matmul_plan_create_window: window [%d, %d) outside [0, B = %d)", i_first, i_first + i_count,
+                      pl->B);
+        delete pl;
+        return BLB_E_INVALID_ARG;
+    }
+    pl->i_first = i_first;
+    pl->i_count = i_count;
     if (packing == BLB_PACK_SPATIAL) {
         if (col_map) {
             pl->D_out = D_out;
@@ -590,11 +608,12 @@ extern "C" blb_status blb_matmul_plan_create(const blb_params *P, int L, int w_r
                     const int t = g * pl->B + i;
                     if (t >= pl->c) continue;
                     if (!nz_entry(pl, b, bp, t)) continue;
+                    cnt++;  // giant steps follow the whole plan (the owner rotates the summed acc)
+                    if (i < pl->i_first || i >= pl->i_first + pl->i_count) continue;
                     pl->ent_b.push_back(b);
                     pl->ent_i.push_back(i);
                     ent_o.push_back(bp * pl->G + g);
                     baby_used[b][i] = 1;
-                    cnt++;
                 }
             if (cnt && g > 0) pl->giant[bp].push_back(g);
             pl->ent_start.push_back((int)pl->ent_b.size());
@@ -801,62 +820,77 @@ extern "C" size_t blb_matmul_workspace_bytes(const blb_matmul_plan *pl, int out_
     return matmul_ws(pl, out_count).total * sizeof(u64) + 256;
 }
 
-extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys *keys, const blb_ct *in, int n_in,
-                                       const u64 *pt_dev, int out_first, int out_count, blb_ct *out, void *ws,
-                                       size_t ws_bytes, void *stream) {
-    if (!pl || !keys || !in || !pt_dev || !out || !ws) {
-        blb_set_error("blb_ct_pt_matmul: null argument");
-        return BLB_E_INVALID_ARG;
-    }
-    BLB_TRY(check_slice(pl, out_first, out_count));
-    if (n_in != pl->n_in) {
-        blb_set_error("blb_ct_pt_matmul: %d inputs, plan needs %d", n_in, pl->n_in);
-        return BLB_E_LAYOUT;
-    }
+static const u64 *mm_key(const blb_params *P, const blb_keys *keys, int32_t step) {
+    const uint32_t g = blb_galois_element(P, step);
+    for (size_t i = 0; i < keys->galois.size(); i++)
+        if (keys->galois[i] == g) return keys->data[i];
+    return nullptr;
+}
+
+static blb_status mm_check(const blb_matmul_plan *pl, const blb_keys *keys, const blb_ct *in, int n_in, bool baby,
+                           bool giant) {
     const blb_params *P = pl->P;
-    const int level = pl->level, k = level + 1, N = P->N, E = k + P->np, beta = blb_beta(P, level);
-    for (int b = 0; b < n_in; b++)
-        if (in[b].level != level || !in[b].data) {
-            blb_set_error("input %d at level %d, plan level %d", b, in[b].level, level);
-            return BLB_E_LEVEL;
+    if (in) {
+        if (n_in != pl->n_in) {
+            blb_set_error("blb_ct_pt_matmul: %d inputs, plan needs %d", n_in, pl->n_in);
+            return BLB_E_LAYOUT;
         }
-    for (int t = 0; t < out_count; t++)
-        if (!out[t].data) return BLB_E_INVALID_ARG;
-    const MatmulWs w = matmul_ws(pl, out_count);
-    if (ws_bytes < w.total * sizeof(u64)) {
-        blb_set_error("workspace too small: %zu < %zu", ws_bytes, w.total * sizeof(u64));
-        return BLB_E_NOMEM;
+        for (int b = 0; b < n_in; b++)
+            if (in[b].level != pl->level || !in[b].data) {
+                blb_set_error("input %d at level %d, plan level %d", b, in[b].level, pl->level);
+                return BLB_E_LEVEL;
+            }
     }
-    // keys present?
-    auto find_key = [&](int32_t step) -> const u64 * {
-        const uint32_t g = blb_galois_element(P, step);
-        for (size_t i = 0; i < keys->galois.size(); i++)
-            if (keys->galois[i] == g) return keys->data[i];
-        return nullptr;
-    };
-    for (int32_t s : pl->rot_steps)
-        if (!find_key(s)) {
+    for (int32_t s : pl->rot_steps) {
+        const bool is_giant = s % (pl->B * pl->L) == 0 && s >= pl->B * pl->L;
+        if ((is_giant ? giant : baby) && !mm_key(P, keys, s)) {
             blb_set_error("missing rotation key for step %d", s);
             return BLB_E_MISSING_KEY;
         }
-    cudaStream_t st = (cudaStream_t)stream;
-    u64 *W = (u64 *)ws;
-    u64 *ext_in = W + w.ext_in, *coef = W + w.coef, *R = W + w.R, *ks = W + w.ks, *acc = W + w.acc;
-    u64 *gext = W + w.gext, *rot = W + w.rot, *resc = W + w.resc, *gcoef = W + w.gcoef;
-    u64 *yext = W + w.yext;
-    u64 *gks_conv = W + w.gks + (size_t)kMaxJobs * 2 * E * N;
+    }
+    return BLB_OK;
+}
+
+namespace {
+// acc[o][p][l][x] mod q_l for cross-rank sums of residues (< 2^64: at most 8 ranks of residues < 2^61)
+__global__ void k_reduce_acc(const u64 *src, u64 *dst, Primes pr, int k, int N, long long n_polys) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int l = blockIdx.y;
+    if (x >= N) return;
+    const ModConst &mc = pr.m[l];
+    for (long long p = blockIdx.z; p < n_polys; p += gridDim.z) {
+        const long long off = (p * k + l) * N + x;
+        dst[off] = mod64(src[off], mc);
+    }
+}
+}  // namespace
+
+// Phase A (rows a2 + a3): ModUp of every input once (hoisting, C8), the baby-step rotations of the
+// plan's window, and the MAC of the window's plaintexts into acc[o][g] for the outputs
+// [out_first, out_first + out_count) (pt_dev holds that slice's plaintexts).
+static blb_status mm_acc(const blb_matmul_plan *pl, const blb_keys *keys, const blb_ct *in, const u64 *pt_dev,
+                         int out_first, int out_count, u64 *acc, u64 *W, const MatmulWs &w, cudaStream_t st) {
+    const blb_params *P = pl->P;
+    const int n_in = pl->n_in, level = pl->level, k = level + 1, N = P->N, E = k + P->np, beta = blb_beta(P, level);
+    u64 *ext_in = W + w.ext_in, *coef = W + w.coef, *R = W + w.R, *ks = W + w.ks;
     const size_t ctN = (size_t)2 * k * N;
     u64 *ks_u = ks, *ks_conv = ks + (size_t)kMaxJobs * 2 * E * N;
-
+    auto find_key = [&](int32_t step) { return mm_key(P, keys, step); };
+    const bool has_baby = [&] {
+        for (auto &v : pl->baby)
+            if (!v.empty()) return true;
+        return false;
+    }();
+    const bool win0 = pl->i_first == 0;  // R[b][0] = X_b is in this window
     // 1. ModUp of every input c1 (hoisted) and R[b][0] = X_b
-    {
+    if (has_baby || win0) {
         std::vector<const u64 *> c1;
         for (int b = 0; b < n_in; b++) c1.push_back(in[b].data + (size_t)k * N);
-        for (int b0 = 0; b0 < n_in; b0 += kMaxJobs) {
+        for (int b0 = 0; b0 < n_in && has_baby; b0 += kMaxJobs) {
             const int cnt = std::min(kMaxJobs, n_in - b0);
             BLB_TRY(launch_modup(P, level, c1.data() + b0, cnt, ext_in + (size_t)b0 * beta * E * N, coef, st));
         }
-        for (int b = 0; b < n_in; b++) {
+        for (int b = 0; b < n_in && win0; b++) {
             k_copy_ct<<<(unsigned)((ctN + kTB - 1) / kTB), kTB, 0, st>>>(in[b].data, R + (size_t)b * pl->B * ctN,
                                                                         (long long)ctN);
             BLB_COUNT_LAUNCH(1);
@@ -884,40 +918,51 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
             BLB_TRY(launch_keyswitch(P, level, jobs.data() + j0, cnt, ks_u, ks_conv, st));
         }
     }
-    // 3-5. MAC, giant steps and rescale (one stream: a two-stream overlap of the MAC of output
-    // chunk c+1 with the giant steps of chunk c measured slower once the key-switch batches were
-    // 128 jobs, 71.8 vs 72.5-73.2 ms per layer, profiles/r1_overlap.log)
+    // 3. MAC: acc[b', g] = sum over the window's entries (b, i) of P (.) R[b][i]
+    const int o0 = out_first * pl->G, n_o = out_count * pl->G;
+    const int e_base = pl->ent_start[out_first * pl->G];
+    const int n_entries = pl->ent_start[o0 + n_o] - pl->ent_start[o0];
+    if (n_o > 0 && n_entries == 0) {
+        BLB_CUDA_TRY(cudaMemsetAsync(acc, 0, sizeof(u64) * (size_t)n_o * ctN, st));
+    } else if (n_o > 0) {
+        const int n_tiles = N / (2 * kTB);
+        const PtLayout lay = pt_layout(pl);
+        const unsigned char *ptb = reinterpret_cast<const unsigned char *>(pt_dev);
+        cudaEvent_t t0 = blb_timing_begin(st);
+        // pairs of consecutive (b', g) with one entry list -> the two-output kernel (each R tile
+        // staged once for both); plans whose pairs differ take one output per CTA.  An empty entry
+        // list (possible in a window) yields a zero accumulator.
+        bool grouped = true;
+        for (int j = 0; j < n_o && grouped; j++)
+            if (j % 2 != 1 && j + 1 < n_o && !pl->same_next[o0 + j]) grouped = false;
+        if (grouped)
+            launch_mac4<2, BLB_MAC_STG, BLB_MAC_MINB>(ptb, R, acc, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k,
+                                                      P->logN, P->pr, n_tiles, lay, st);
+        else
+            launch_mac4<1, 4, 3>(ptb, R, acc, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN, P->pr,
+                                 n_tiles, lay, st);
+        BLB_COUNT_LAUNCH(1);
+        BLB_COUNT(3, n_entries);
+        blb_timing_end(0, t0, st, (double)n_entries * (double)lay.bpp);  // packed plaintext bytes
+        BLB_CHECK_LAUNCH();
+    }
+    return BLB_OK;
+}
+
+// Phase B (rows a4 + a5): giant steps of the outputs [out_first, out_first + out_count) from their
+// accumulators acc[t][g] (reading C11: lazy giant sum in Q_l u P, one fused ModDown + rescale per
+// output, C17; outputs without giant steps are rescaled directly).
+static blb_status mm_finish(const blb_matmul_plan *pl, const blb_keys *keys, const u64 *acc, int out_first,
+                            int out_count, double scale, blb_ct *out, u64 *W, const MatmulWs &w, cudaStream_t st) {
+    const blb_params *P = pl->P;
+    const int level = pl->level, k = level + 1, N = P->N, E = k + P->np, beta = blb_beta(P, level);
+    u64 *gext = W + w.gext, *rot = W + w.rot, *resc = W + w.resc, *gcoef = W + w.gcoef, *yext = W + w.yext;
+    u64 *gks_conv = W + w.gks + (size_t)kMaxJobs * 2 * E * N;
+    const size_t ctN = (size_t)2 * k * N;
+    auto find_key = [&](int32_t step) { return mm_key(P, keys, step); };
     cudaStream_t sa = st;
+    const int c0 = 0, cn = out_count;
     {
-        const int c0 = 0, cn = out_count;
-        // MAC
-        {
-            const int o0 = (out_first + c0) * pl->G, n_o = cn * pl->G;
-            const int e_base = pl->ent_start[out_first * pl->G];
-            const int n_entries = pl->ent_start[o0 + n_o] - pl->ent_start[o0];
-            u64 *acc_c = acc + (size_t)c0 * pl->G * ctN;
-            if (n_o > 0) {
-                const int n_tiles = N / (2 * kTB);
-                const PtLayout lay = pt_layout(pl);
-                const unsigned char *ptb = reinterpret_cast<const unsigned char *>(pt_dev);
-                cudaEvent_t t0 = blb_timing_begin(st);
-                // pairs of consecutive (b', g) with one entry list -> the two-output kernel (each R
-                // tile staged once for both); plans whose pairs differ take one output per CTA
-                bool grouped = true;
-                for (int j = 0; j < n_o && grouped; j++)
-                    if (j % 2 != 1 && j + 1 < n_o && !pl->same_next[o0 + j]) grouped = false;
-                if (grouped)
-                    launch_mac4<2, BLB_MAC_STG, BLB_MAC_MINB>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o,
-                                                              k, P->logN, P->pr, n_tiles, lay, st);
-                else
-                    launch_mac4<1, 4, 3>(ptb, R, acc_c, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN,
-                                         P->pr, n_tiles, lay, st);
-                BLB_COUNT_LAUNCH(1);
-                BLB_COUNT(3, n_entries);
-                blb_timing_end(0, t0, st, (double)n_entries * (double)lay.bpp);  // packed plaintext bytes
-                BLB_CHECK_LAUNCH();
-            }
-        }
         // giant steps (reading C11, lazy ModDown): Y[b'] = lift(acc[b'][0]) + sum_g Rot_ext(acc[b'][g])
         // in Q_l u P, then ONE ModDown per output; g-major so outputs sharing a key are adjacent
         std::vector<int> yslot(cn, -1);
@@ -970,9 +1015,79 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
             if (yslot[t - c0] >= 0) youts.push_back(out[t].data);
             else BLB_TRY(launch_rescale(P, acc + (size_t)t * pl->G * ctN, level, 2, out[t].data, resc, sa));
             out[t].level = level - 1;
-            out[t].scale = in[0].scale;  // Delta * q_level / q_level, exact (reading S6)
+            out[t].scale = scale;  // Delta * q_level / q_level, exact (reading S6)
         }
         if (n_y > 0) BLB_TRY(launch_moddown_rescale(P, level, yext, n_y, youts.data(), gks_conv, sa));
     }
     return BLB_OK;
+}
+
+extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys *keys, const blb_ct *in, int n_in,
+                                       const u64 *pt_dev, int out_first, int out_count, blb_ct *out, void *ws,
+                                       size_t ws_bytes, void *stream) {
+    if (!pl || !keys || !in || !pt_dev || !out || !ws) {
+        blb_set_error("blb_ct_pt_matmul: null argument");
+        return BLB_E_INVALID_ARG;
+    }
+    BLB_TRY(check_slice(pl, out_first, out_count));
+    if (pl->i_first != 0 || pl->i_count != pl->B) {
+        blb_set_error("blb_ct_pt_matmul: a windowed plan needs blb_ct_pt_matmul_acc + blb_ct_pt_matmul_finish");
+        return BLB_E_INVALID_ARG;
+    }
+    BLB_TRY(mm_check(pl, keys, in, n_in, true, true));
+    for (int t = 0; t < out_count; t++)
+        if (!out[t].data) return BLB_E_INVALID_ARG;
+    const MatmulWs w = matmul_ws(pl, out_count);
+    if (ws_bytes < w.total * sizeof(u64)) {
+        blb_set_error("workspace too small: %zu < %zu", ws_bytes, w.total * sizeof(u64));
+        return BLB_E_NOMEM;
+    }
+    u64 *W = (u64 *)ws;
+    cudaStream_t st = (cudaStream_t)stream;
+    BLB_TRY(mm_acc(pl, keys, in, pt_dev, out_first, out_count, W + w.acc, W, w, st));
+    return mm_finish(pl, keys, W + w.acc, out_first, out_count, in[0].scale, out, W, w, st);
+}
+
+extern "C" blb_status blb_ct_pt_matmul_acc(const blb_matmul_plan *pl, const blb_keys *keys, const blb_ct *in,
+                                           int n_in, const u64 *pt_dev, u64 *acc_out, void *ws, size_t ws_bytes,
+                                           void *stream) {
+    if (!pl || !keys || !in || !pt_dev || !acc_out || !ws) {
+        blb_set_error("blb_ct_pt_matmul_acc: null argument");
+        return BLB_E_INVALID_ARG;
+    }
+    BLB_TRY(mm_check(pl, keys, in, n_in, true, false));
+    const MatmulWs w = matmul_ws(pl, 0);
+    if (ws_bytes < w.total * sizeof(u64)) {
+        blb_set_error("workspace too small: %zu < %zu", ws_bytes, w.total * sizeof(u64));
+        return BLB_E_NOMEM;
+    }
+    return mm_acc(pl, keys, in, pt_dev, 0, pl->n_out, acc_out, (u64 *)ws, w, (cudaStream_t)stream);
+}
+
+extern "C" blb_status blb_ct_pt_matmul_finish(const blb_matmul_plan *pl, const blb_keys *keys, const u64 *acc_in,
+                                              int out_first, int out_count, double scale, blb_ct *out, void *ws,
+                                              size_t ws_bytes, void *stream) {
+    if (!pl || !keys || (out_count > 0 && (!acc_in || !out)) || !ws) {
+        blb_set_error("blb_ct_pt_matmul_finish: null argument");
+        return BLB_E_INVALID_ARG;
+    }
+    BLB_TRY(check_slice(pl, out_first, out_count));
+    BLB_TRY(mm_check(pl, keys, nullptr, 0, false, true));
+    for (int t = 0; t < out_count; t++)
+        if (!out[t].data) return BLB_E_INVALID_ARG;
+    const MatmulWs w = matmul_ws(pl, out_count);
+    if (ws_bytes < w.total * sizeof(u64)) {
+        blb_set_error("workspace too small: %zu < %zu", ws_bytes, w.total * sizeof(u64));
+        return BLB_E_NOMEM;
+    }
+    if (out_count == 0) return BLB_OK;
+    u64 *W = (u64 *)ws;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int k = pl->level + 1, N = pl->P->N;
+    const long long n_polys = (long long)out_count * pl->G * 2;
+    k_reduce_acc<<<dim3((N + kTB - 1) / kTB, k, (unsigned)std::min<long long>(n_polys, 1024)), kTB, 0, st>>>(
+        acc_in, W + w.acc, pl->P->pr, k, N, n_polys);
+    BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    return mm_finish(pl, keys, W + w.acc, out_first, out_count, scale, out, W, w, st);
 }

@@ -11,11 +11,20 @@ Blocks (fig:fusion_pattern P:699-704, Table 6):
     with the MHP row reorder of W_O (P:466) -> mask;
   * FFN1 (d -> 4d) -> mask; FFN2 (4d -> d) -> mask.
 Each MatMul starts from a fresh ciphertext at the top level (SURVEY 8(d)
-config 3).  Work is sharded by output ciphertext (section 8(e)): rank r owns a
-contiguous slice of every plan's outputs, holds only the plaintexts of that
-slice, recomputes the (replicated) baby steps, and the masked results are
-all-gathered at the end of the layer.  The BSGS split is fixed independently of
-the number of ranks, so outputs are bit-identical at every GPU count.
+config 3).
+
+Multi-GPU: every MatMul -- ct-pt and ct-ct -- is
+sharded by its BSGS baby-step index i: rank r owns the contiguous window
+shard(B, r, world) of [0, B), holds only the plaintexts of its window, computes the
+baby-step rotations, MAC entries, products and step-3 terms of its window, and
+writes its partial accumulators (ct-pt: acc_{b',g}; ct-ct: the step-3 A_{u,w,f} in
+Q u P).  One exact all-reduce (u64 sums of residues < 2^61: no overflow for <= 8
+ranks) adds the windows; the owner of each output ciphertext (shard(n_out, r,
+world)) reduces mod q and runs the giant steps / ModDown / rescale and the mask.
+Ciphertexts a later MatMul consumes whole (Q, K for Q K^T; the Softmax x V outputs
+for the out-projection) are all-gathered.  The BSGS split does not depend on the
+number of ranks and the sums are exact, so outputs are bit-identical at every GPU
+count (tests/test_gpu_multirank.py).
 """
 from __future__ import annotations
 
@@ -87,6 +96,40 @@ def allgather_ragged(local: list, counts: list, like=None) -> list:
     return out
 
 
+def _coll_tensor(t: torch.Tensor):
+    """gloo (CPU tests, or two ranks sharing one GPU) reduces host tensors; NCCL device tensors."""
+    import torch.distributed as dist
+    return t.cpu() if (t.is_cuda and dist.get_backend() == "gloo") else t
+
+
+def allreduce_sum_(t: torch.Tensor) -> torch.Tensor:
+    """In-place exact u64 sum over the ranks (int64 two's-complement add = u64 add)."""
+    import torch.distributed as dist
+    h = _coll_tensor(t)
+    dist.all_reduce(h, op=dist.ReduceOp.SUM)
+    if h is not t:
+        t.copy_(h)
+    return t
+
+
+def allgather_cts(params: blb.Params, local: list, counts: list, level: int) -> list:
+    """All-gather ciphertexts (rank r holds counts[r] of them, in rank order) onto every rank."""
+    import torch.distributed as dist
+    like = torch.empty(2 * (level + 1) * params.N, dtype=torch.int64, device="cuda")
+    items = [c.data.reshape(-1) for c in local]
+    if dist.get_backend() == "gloo":
+        items = [x.cpu() for x in items]
+        like = like.cpu()
+    full = allgather_ragged(items, counts, like=like)
+    scales = [None] * len(counts)
+    dist.all_gather_object(scales, [c.scale for c in local])   # per-output scales (exact doubles)
+    flat = [x for r in scales for x in r]
+    out = []
+    for x, sc in zip(full, flat):
+        out.append(blb.Ciphertext(x.to("cuda").reshape(2, level + 1, params.N).contiguous(), level, sc))
+    return out
+
+
 class FusedLinearLayer:
     def __init__(self, params: blb.Params, dims: Dims = BERT_BASE, rank: int = 0, world: int = 1,
                  bsgs: dict | None = None, level: int | None = None):
@@ -98,25 +141,41 @@ class FusedLinearLayer:
         self.Hp = 1 << (H - 1).bit_length()
         qkv_map = cm + [d + c if c >= 0 else -1 for c in cm] + list(range(2 * d, 3 * d))
         self.n_mhp = len(cm) // (params.n // L)   # ciphertexts of Q (and of K)
+        c = params.n // L
+
+        def win(B: int):
+            """this rank's baby-step window of [0, B) (None: one rank, the whole plan)"""
+            if world == 1:
+                return None
+            if world > B:
+                raise ValueError("%d ranks exceed the BSGS baby-step count B = %d" % (world, B))
+            return shard(B, rank, world)
+
         self.plans = {
-            "qkv": blb.MatmulPlan(params, L, d, 3 * d, col_map=qkv_map, bsgs_B=b["qkv"], level=self.level),
+            "qkv": blb.MatmulPlan(params, L, d, 3 * d, col_map=qkv_map, bsgs_B=b["qkv"], level=self.level,
+                                  window=win(min(b["qkv"], c))),
             "oproj": blb.MatmulPlan(params, L, self.Hp * (d // H), d, packing=blb.PACK_DIAGONAL, heads=self.Hp,
-                                    bsgs_B=b["oproj"], level=self.level - 3),
-            "ffn1": blb.MatmulPlan(params, L, d, ffn, bsgs_B=b["ffn1"], level=self.level),
-            "ffn2": blb.MatmulPlan(params, L, ffn, d, bsgs_B=b["ffn2"], level=self.level),
+                                    bsgs_B=b["oproj"], level=self.level - 3, window=win(min(b["oproj"], c))),
+            "ffn1": blb.MatmulPlan(params, L, d, ffn, bsgs_B=b["ffn1"], level=self.level,
+                                   window=win(min(b["ffn1"], c))),
+            "ffn2": blb.MatmulPlan(params, L, ffn, d, bsgs_B=b["ffn2"], level=self.level,
+                                   window=win(min(b["ffn2"], c))),
         }
+        # output ownership: rank r finishes (giant steps, ModDown, rescale) and masks a contiguous slice
         self.slices = {k: shard(pl.n_out, rank, world) for k, pl in self.plans.items()}
-        # Q K^T consumes the 2 J MHP outputs of QKV at level-1 (row a7); with more than one
-        # rank the Q / K ciphertexts are all-gathered first and Q K^T is replicated (its
-        # outputs are masked by their owner only) -- see DESIGN.md section 8.
-        self.qk = blb.QKPlan(params, L, H, d // H, bsgs_B=b["qk"], level=self.level - 1)
+        g = params.n // (L * self.Hp)
+        B_qk = b["qk"] or g
+        # Q K^T consumes the 2 J MHP outputs of QKV at level-1 (row a7); Softmax x V (row f1) has inner
+        # dimension L (V zero-padded d_h -> L); both sharded by baby-index window like the ct-pt plans
+        self.qk = blb.QKPlan(params, L, H, d // H, bsgs_B=b["qk"], level=self.level - 1, window=win(B_qk))
+        self.sv = blb.QKPlan(params, L, H, L, bsgs_B=b["qk"], level=self.level, window=win(B_qk))
         self.slices["qk"] = shard(self.qk.n_out, rank, world)
-        # Softmax x V (row f1): inner dimension L (V zero-padded d_h -> L), replicated like Q K^T
-        self.sv = blb.QKPlan(params, L, H, L, bsgs_B=b["qk"], level=self.level)
+        self.slices["sv"] = shard(self.sv.n_out, rank, world)
         for name, n in [(k, pl.n_out) for k, pl in self.plans.items()] + [("qk", self.qk.n_out)]:
             if n > MAX_OUT:
                 raise ValueError("%s: %d output ciphertexts exceed the mask-id range" % (name, n))
         self.pts, self.ws, self.outs = {}, None, {}
+        self.acc = None
         self.seq = 0      # inference counter: enters every mask id (fresh masks per step)
 
     # ---- setup (row a0) ----
@@ -134,16 +193,21 @@ class FusedLinearLayer:
         WOp[:WO.shape[0]] = WO
         WO = WOp
         for name, W in (("qkv", Wqkv), ("oproj", WO), ("ffn1", W1), ("ffn2", W2)):
-            first, count = self.slices[name]
-            self.pts[name] = self.plans[name].encode_weights(W, first, count)
+            if self.world == 1:
+                first, count = self.slices[name]
+                self.pts[name] = self.plans[name].encode_weights(W, first, count)
+            else:   # the window's plaintexts of every output
+                self.pts[name] = self.plans[name].encode_weights(W)
         self.qk_masks = self.qk.encode_masks()
         self.sv_masks = self.sv.encode_masks()
-        nbytes = max([pl.workspace_bytes(self.slices[k][1]) for k, pl in self.plans.items()] +
+        nbytes = max([pl.workspace_bytes(pl.n_out) for k, pl in self.plans.items()] +
                      [self.qk.workspace_bytes(), self.sv.workspace_bytes()])
         self.ws = torch.empty(nbytes // 8 + 1, dtype=torch.int64, device="cuda")
+        if self.world > 1:
+            n_acc = max([pl.acc_numel() for pl in self.plans.values()] + [self.qk.acc_numel(), self.sv.acc_numel()])
+            self.acc = torch.empty(n_acc, dtype=torch.int64, device="cuda")
         for k, pl in self.plans.items():
             self.outs[k] = [blb.Ciphertext.empty(self.p, self.level - 1) for _ in range(self.slices[k][1])]
-        self.qkv_full = [blb.Ciphertext.empty(self.p, self.level - 1) for _ in range(2 * self.n_mhp)]
         self.outs["qk"] = [blb.Ciphertext.empty(self.p, self.level - 4) for _ in range(self.qk.n_out)]
         self.outs["sv"] = [blb.Ciphertext.empty(self.p, self.level - 3) for _ in range(self.sv.n_out)]
         self.sv_dense = [blb.Ciphertext.empty(self.p, self.level - 3) for _ in range(self.sv.n_out // 2)]
@@ -153,6 +217,8 @@ class FusedLinearLayer:
                 int(self.sv_masks.numel()) * 8)
 
     def n_plaintexts(self) -> int:
+        if self.world > 1:
+            return sum(self.plans[k].pt_count() for k in self.plans)
         return sum(self.plans[k].pt_count(*self.slices[k]) for k in self.plans)
 
     def mask_counts(self, name: str) -> list[int]:
@@ -178,21 +244,46 @@ class FusedLinearLayer:
         return [mask_id(seq, name, o) for o in self.mask_outputs(name)]
 
     # ---- the hot path ----
+    def ct_pt(self, keys: blb.Keys, name: str, src: list) -> list:
+        """One ct-pt MatMul -> this rank's output slice (world 1: the fused single call)."""
+        pl = self.plans[name]
+        first, count = self.slices[name]
+        if self.world == 1:
+            return pl(keys, src, self.pts[name], first, count, ws=self.ws, outs=self.outs[name])
+        n = pl.acc_numel()
+        acc = pl.acc(keys, src, self.pts[name], acc_out=self.acc[:n], ws=self.ws)
+        allreduce_sum_(acc)
+        per = pl.acc_numel(1)
+        return pl.finish(keys, acc[first * per:(first + count) * per], first, count, src[0].scale, ws=self.ws,
+                         outs=self.outs[name][:count])
+
+    def ct_ct(self, keys: blb.Keys, plan: blb.QKPlan, masks, Q: list, K: list, outs: list, name: str) -> list:
+        """One ct-ct MatMul (C13) -> this rank's output slice (world 1: all outputs)."""
+        if self.world == 1:
+            return plan(keys, Q, K, masks, ws=self.ws, outs=outs)
+        n = plan.acc_numel()
+        acc = plan.acc(keys, Q, K, masks, acc_out=self.acc[:n], ws=self.ws)
+        allreduce_sum_(acc)
+        first, count = self.slices[name]
+        a0, na = plan.acc_range(first, count)
+        per = n // max(1, plan.acc_range(0, plan.n_out)[1])
+        return plan.finish(keys, acc[a0 * per:(a0 + na) * per], first, count, Q[0].scale, K[0].scale, ws=self.ws,
+                           outs=outs[first:first + count])
+
     def gather_qk_operands(self, outs: list):
         """Q and K ciphertexts (QKV outputs 0 .. 2J-1) on every rank."""
         if self.world == 1:
             return outs[:2 * self.n_mhp]
         counts = [shard(self.plans["qkv"].n_out, r, self.world)[1] for r in range(self.world)]
-        full = allgather_ragged([o.data for o in outs], counts, like=self.qkv_full[0].data)
-        scale = outs[0].scale if outs else 2.0 ** bi_log_delta()
-        for g in range(2 * self.n_mhp):
-            self.qkv_full[g].data.copy_(full[g])
-            self.qkv_full[g].scale = scale
-        return self.qkv_full
+        full = allgather_cts(self.p, outs, counts, self.level - 1)
+        return full[:2 * self.n_mhp]
 
     def softmax_v(self, keys: blb.Keys, S_cts: list, Vt_cts: list) -> list:
         """Row f1: S_h (x) Vpad_h by the ct-ct protocol, then the dense-diagonal collapse."""
-        outs = self.sv(keys, S_cts, Vt_cts, self.sv_masks, ws=self.ws, outs=self.outs["sv"])
+        outs = self.ct_ct(keys, self.sv, self.sv_masks, S_cts, Vt_cts, self.outs["sv"], "sv")
+        if self.world > 1:   # the out-projection consumes every collapsed diagonal
+            counts = [shard(self.sv.n_out, r, self.world)[1] for r in range(self.world)]
+            outs = allgather_cts(self.p, outs, counts, self.level - 3)
         half = len(outs) // 2
         for o in range(half):
             blb.add_into(self.p, outs[o], outs[o + half], self.sv_dense[o])
@@ -200,27 +291,28 @@ class FusedLinearLayer:
 
     def step(self, keys: blb.Keys, inputs: dict, mask_key: bytes, seq: int | None = None) -> list:
         """inputs: {'qkv': [ct]*3, 'sv_s': [ct]*J', 'sv_v': [ct]*J', 'ffn1': [...], 'ffn2': [...]}
-        -> [(name, first mask id, (masked, share))] per block.  seq: the inference number entering the
-        mask ids (default: the layer's own counter, incremented per call, so masks are never reused)."""
+        -> [(name, first mask id, (masked, share))] per block, this rank's outputs.  seq: the inference
+        number entering the mask ids (default: the layer's own counter, incremented per call, so masks
+        are never reused)."""
         if seq is None:
             seq = self.seq
         self.seq = seq + 1
         res = []
         for name in ("qkv", "oproj", "ffn1", "ffn2"):
             first, count = self.slices[name]
-            if count == 0 and not (name == "qkv" and self.world > 1):
+            if count == 0 and self.world == 1:
                 continue
             src = self.softmax_v(keys, inputs["sv_s"], inputs["sv_v"]) if name == "oproj" else inputs[name]
-            outs = self.plans[name](keys, src, self.pts[name], first, count, ws=self.ws,
-                                    outs=self.outs[name]) if count else []
+            outs = self.ct_pt(keys, name, src)
             if name == "qkv":
                 qk_in = self.gather_qk_operands(outs)
                 J = self.n_mhp
-                qk_out = self.qk(keys, qk_in[:J], qk_in[J:2 * J], self.qk_masks, ws=self.ws, outs=self.outs["qk"])
+                qk_out = self.ct_ct(keys, self.qk, self.qk_masks, qk_in[:J], qk_in[J:2 * J], self.outs["qk"], "qk")
                 qf, qc = self.slices["qk"]
                 if qc:
                     ids = self.mask_ids("qk", seq)
-                    res.append(("qk", ids[0], blb.ckks_to_mpc(self.p, qk_out[qf:qf + qc], mask_key, ids[0])))
+                    mine = qk_out if self.world > 1 else qk_out[qf:qf + qc]
+                    res.append(("qk", ids[0], blb.ckks_to_mpc(self.p, mine, mask_key, ids[0])))
             ids = self.mask_ids(name, seq)
             if not ids:
                 continue

@@ -1,7 +1,9 @@
-"""World-size-2 gloo tests (CPU) of the multi-GPU host logic (SURVEY 8(e)):
-output-ciphertext sharding covers every output exactly once, and the padded
-ragged all-gather used at the end of each layer (and for the Q / K operands of
-Q K^T) reassembles the rank-ordered list bit-exactly."""
+"""World-size-2 gloo tests (CPU) of the multi-GPU host logic (SURVEY 8(e), DESIGN section 8):
+output-ciphertext and baby-step-window sharding cover every index exactly once, the exact
+all-reduce of partial accumulators adds residues as u64 (two's-complement int64 wrap-around
+gives the u64 bits; 8 residues < 2^61 never exceed 2^64), and the padded ragged all-gather used
+for the Q / K operands, the Softmax x V outputs and the end-of-layer results reassembles the
+rank-ordered list bit-exactly."""
 import os
 import socket
 
@@ -53,6 +55,15 @@ def _worker(rank, world, port, q):
         local = [torch.arange(5) + 10 * t for t in range(counts[rank])]
         full = allgather_ragged(local, counts, like=torch.zeros(5, dtype=torch.int64))
         ok &= [x.tolist() for x in full] == [(torch.arange(5) + 10 * t).tolist() for t in range(3)]
+        # exact sum of partial accumulators: residues just below 2^61 on every rank (the int64 sum
+        # wraps past 2^63 once 4+ such residues are added; the u64 bits are the exact sum)
+        from paper_2508_19525_b200.layer import allreduce_sum_
+        big = (1 << 61) - 1 - rank
+        t = torch.tensor([big, 5 + rank, (1 << 61) - 7], dtype=torch.int64)
+        allreduce_sum_(t)
+        exact = [sum((1 << 61) - 1 - r for r in range(world)), sum(5 + r for r in range(world)),
+                 world * ((1 << 61) - 7)]
+        ok &= [int(v) % (1 << 64) for v in t.tolist()] == [e % (1 << 64) for e in exact]
         q.put((rank, ok))
     finally:
         dist.destroy_process_group()
@@ -69,3 +80,27 @@ def test_allgather_ragged_gloo_world2():
         p.join(timeout=120)
     res = dict(q.get(timeout=5) for _ in range(2))
     assert res == {0: True, 1: True}
+
+
+def test_u64_sum_via_int64_wraparound():
+    """8 ranks' residues < 2^61 summed in int64 (wrapping past 2^63) give the exact u64 sum."""
+    vals = [(1 << 61) - 1 - r for r in range(8)]
+    t = torch.zeros(1, dtype=torch.int64)
+    for v in vals:
+        t += torch.tensor([v], dtype=torch.int64)
+    assert int(t.item()) % (1 << 64) == sum(vals) and sum(vals) < (1 << 64)
+
+
+def test_window_partition_of_baby_steps():
+    """The baby-step windows of the ranks partition [0, B) for every plan B at every GPU count."""
+    from paper_2508_19525_b200.layer import shard
+    for B in [4, 8, 16, 64]:
+        for world in [1, 2, 4, 8]:
+            if world > B:
+                continue
+            seen = []
+            for r in range(world):
+                f, c = shard(B, r, world)
+                assert c >= 1
+                seen += list(range(f, f + c))
+            assert seen == list(range(B))
