@@ -254,6 +254,17 @@ blb_status blb_mpc_to_ckks(const blb_params *params, blb_ct *ct, const uint64_t 
  * 1 <= ft <= 52, 0 <= s_out <= 126, else BLB_E_INVALID_ARG; BLB_E_NOMEM (workspace). */
 blb_status blb_share_decode(const blb_params *params, const uint64_t *x, int ft, int s_out, uint64_t *y, void *ws,
                             size_t ws_bytes, void *stream);
+/* Row f3, local fixed-point Encode of a share (Alg. 2 line 1: each party "locally evaluates
+ * the CKKS encoding"; P:684-685 / App. C.4: FFT with local truncations on the extended
+ * ring; reading C20).  y: device [N/2][2] u64 = little-endian Z_{2^128} share of the real slot
+ * vector (fixed point).  The value of slot j is placed at zeta^{5^j} and its conjugate (C3), the
+ * Gentleman-Sande network over Z_{2^128}[i] runs with conj(W), W = round(2^ft zeta^{brv(m+i)}), and
+ * an arithmetic right shift by ft after every twiddle product; coefficient k = Re_k >>_a s_out
+ * (s_out = log N + f - log2 Delta for a share with f fractional bits).  x: device [N][2] u64, the
+ * share of the integer coefficients of Encode.  ws >= 48 N bytes.  1 <= ft <= 52,
+ * 0 <= s_out <= 126, else BLB_E_INVALID_ARG; BLB_E_NOMEM (workspace). */
+blb_status blb_share_encode(const blb_params *params, const uint64_t *y, int ft, int s_out, uint64_t *x, void *ws,
+                            size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------ */
 /* ct-pt MatMul (rows a2-a6; C11 / C12; BSGS App. C.1)      */

@@ -120,6 +120,7 @@ def lib():
                                      ctypes.c_void_p]
         L.orc_moddown_rescale.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
         L.orc_share_decode.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+        L.orc_share_encode.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
         L.orc_share_to_rns.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_void_p]
         L.orc_relinearize_ext.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
@@ -606,6 +607,16 @@ def share_decode(ctx: Ctx, x: np.ndarray, ft: int, s_out: int) -> np.ndarray:
     y = np.empty((ctx.n, 2), dtype=np.uint64)
     lib().orc_share_decode(ctx._h, _p(x), int(ft), int(s_out), _p(y))
     return y
+
+
+def share_encode(ctx: Ctx, y: np.ndarray, ft: int, s_out: int) -> np.ndarray:
+    """Row f3 (Alg. 2 line 1): local fixed-point Encode of a slot-vector share over Z_{2^128}
+    (y: uint64 [N/2][2]) -> uint64 [N][2] share of the integer coefficients (reading C20)."""
+    y = np.ascontiguousarray(y, dtype=np.uint64)
+    assert y.shape == (ctx.n, 2) and 1 <= ft <= 62 and 0 <= s_out < 127
+    x = np.empty((ctx.N, 2), dtype=np.uint64)
+    lib().orc_share_encode(ctx._h, _p(y), int(ft), int(s_out), _p(x))
+    return x
 
 
 def u128_to_int(a: np.ndarray) -> list[int]:

@@ -949,3 +949,53 @@ void orc_share_decode(const orc_ctx *c, const u64 *x, int ft, int s_out, u64 *y)
     }
     free(re); free(im);
 }
+
+/* ------------------------------------------------------------------ */
+/* f3: local fixed-point Encode of a share over Z_{2^128}               */
+/* (Alg. 2 line 1: "P_b locally evaluates the CKKS encoding";      */
+/* P:684-685 O(N log N) FFT with local truncations on the extended ring;  */
+/* App. C.4 P:1246-1262 SecureML truncation >>_a; reading C20)            */
+/* ------------------------------------------------------------------ */
+/* y: [N/2][2] u64 = little-endian u128 share of the real slot vector (fixed point).  The CKKS
+ * encode pi^{-1} (C3): the slot value is placed at the evaluation points zeta^{5^j} and its
+ * conjugate zeta^{-5^j} (real slots, footnote P:540), then the inverse transform
+ * m_k = (1/N) sum_e a_e zeta^{-e k} as the Gentleman-Sande network over Z_{2^128}[i]
+ * (stage m = N/2, .., 2, 1, block i, twiddle conj(W), W = round(2^ft zeta^{brv(m+i)})):
+ * X' = X + Y, Y' = ((X - Y) * conj(W)) >>_a ft (each component); then coefficient
+ * x_k = Re_k >>_a s_out (s_out folds the 1/N = 2^-logN and the scale change of the fixed point).
+ * x: [N][2] u64 share of the integer coefficient vector. */
+void orc_share_encode(const orc_ctx *c, const u64 *y, int ft, int s_out, u64 *x) {
+    u64 N = c->N, twoN = 2 * N;
+    int logN = c->logN;
+    u128 *re = (u128 *)calloc(N, sizeof(u128)), *im = (u128 *)calloc(N, sizeof(u128));
+    u64 e = 1;  /* 5^j mod 2N */
+    for (u64 j = 0; j < N / 2; j++) {
+        u64 k = brv((e - 1) / 2, logN);               /* position of zeta^{5^j}: 2 brv(k) + 1 = 5^j */
+        u64 kc = brv((twoN - e - 1) / 2, logN);       /* position of zeta^{-5^j} = conj */
+        u128 v = (u128)y[2 * j] | ((u128)y[2 * j + 1] << 64);
+        re[k] = v; re[kc] = v;
+        e = (e * 5) % twoN;
+    }
+    __float128 sc = ldexpq(1.0Q, ft);
+    for (u64 m = N / 2; m >= 1; m >>= 1) {
+        u64 t = N / (2 * m);
+        for (u64 i = 0; i < m; i++) {
+            __float128 ang = M_PIq * (__float128)brv(m + i, logN) / (__float128)N;
+            long long wr = (long long)roundq(sc * cosq(ang)), wi = (long long)roundq(sc * sinq(ang));
+            u128 Wr = (u128)(i128)wr, Wi = (u128)(i128)(-wi);   /* conj(W) */
+            for (u64 j = 2 * i * t; j < 2 * i * t + t; j++) {
+                u128 xr = re[j], xi = im[j], yr = re[j + t], yi = im[j + t];
+                u128 dr = xr - yr, di = xi - yi;
+                re[j] = xr + yr; im[j] = xi + yi;
+                re[j + t] = ashr128(dr * Wr - di * Wi, ft);
+                im[j + t] = ashr128(dr * Wi + di * Wr, ft);
+            }
+        }
+        if (m == 1) break;
+    }
+    for (u64 k = 0; k < N; k++) {
+        u128 v = ashr128(re[k], s_out);
+        x[2 * k] = (u64)v; x[2 * k + 1] = (u64)(v >> 64);
+    }
+    free(re); free(im);
+}

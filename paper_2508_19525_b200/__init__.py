@@ -87,6 +87,7 @@ def lib() -> ctypes.CDLL:
             "blb_share_to_rns": ([vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp], ctypes.c_int),
             "blb_mpc_to_ckks": ([vp, vp, vp, ctypes.c_int, vp, ctypes.c_size_t, vp], ctypes.c_int),
             "blb_share_decode": ([vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
+            "blb_share_encode": ([vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
             "blb_matmul_plan_create": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp,
                                         ctypes.c_int, ctypes.c_int, ctypes.c_int, vp], ctypes.c_int),
             "blb_matmul_plan_destroy": ([vp], None),
@@ -414,6 +415,16 @@ def share_decode(params: Params, x: torch.Tensor, ft: int, s_out: int) -> torch.
     _check(lib().blb_share_decode(params.handle, _ptr(x.contiguous()), int(ft), int(s_out), _ptr(y), _ptr(ws),
                                   ws.numel() * 8, _stream()))
     return y
+
+
+def share_encode(params: Params, y: torch.Tensor, ft: int, s_out: int) -> torch.Tensor:
+    """Row f3 (Alg. 2 line 1): local fixed-point Encode of a Z_{2^128} slot share (int64 [N/2][2] CUDA)
+    -> int64 [N][2] share of the integer coefficients (reading C20)."""
+    x = torch.empty(params.N, 2, dtype=torch.int64, device="cuda")
+    ws = torch.empty(params.N * 6, dtype=torch.int64, device="cuda")
+    _check(lib().blb_share_encode(params.handle, _ptr(y.contiguous()), int(ft), int(s_out), _ptr(x), _ptr(ws),
+                                  ws.numel() * 8, _stream()))
+    return x
 
 
 def _f2_ws(params: Params, level: int) -> torch.Tensor:

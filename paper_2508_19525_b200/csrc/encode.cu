@@ -210,6 +210,40 @@ __global__ void k_fxp_extract(const u128d *re, const int32_t *slot_pos, u64 *y, 
     y[2 * j] = (u64)v;
     y[2 * j + 1] = (u64)(v >> 64);
 }
+// Row f3: local fixed-point Encode of a slot-vector share (reading C20; Alg. 2 line 1 P:647): the
+// slot value at zeta^{5^j} and at its conjugate position, then the Gentleman-Sande network (the
+// encode's k_stage inverse order) with conj(W) twiddles and >>_a ft after each twiddle product.
+__global__ void k_fxp_scatter(const u64 *y, const int32_t *slot_pos, u128d *re, u128d *im, int N) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N / 2) return;
+    const u128d v = (u128d)y[2 * j] | ((u128d)y[2 * j + 1] << 64);
+    const int pos = slot_pos[j];
+    re[pos] = v;
+    re[N - 1 - pos] = v;  // zeta^{-5^j}: 2 brv(N-1-pos) + 1 = 2N - 5^j
+    im[pos] = 0;
+    im[N - 1 - pos] = 0;
+}
+__global__ void k_fxp_stage_inv(u128d *re, u128d *im, const long long *tw, int m, int N, int ft) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= N / 2) return;
+    const int t = N / (2 * m);
+    const int i = b / t, jj = b - i * t;
+    const int j = 2 * i * t + jj;
+    const u128d Wr = (u128d)(i128d)tw[2 * (m + i)], Wi = (u128d)(i128d)(-tw[2 * (m + i) + 1]);  // conj(W)
+    const u128d xr = re[j], xi = im[j], yr = re[j + t], yi = im[j + t];
+    const u128d dr = xr - yr, di = xi - yi;
+    re[j] = xr + yr;
+    im[j] = xi + yi;
+    re[j + t] = (u128d)((i128d)(dr * Wr - di * Wi) >> ft);
+    im[j + t] = (u128d)((i128d)(dr * Wi + di * Wr) >> ft);
+}
+__global__ void k_fxp_coef(const u128d *re, u64 *x, int N, int s_out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= N) return;
+    const u128d v = (u128d)((i128d)re[k] >> s_out);
+    x[2 * k] = (u64)v;
+    x[2 * k + 1] = (u64)(v >> 64);
+}
 }  // namespace
 
 size_t encode_scratch_doubles(const blb_params *P, int n_pts) { return (size_t)n_pts * P->N * 4; }
@@ -267,6 +301,27 @@ extern "C" blb_status blb_share_decode(const blb_params *P, const uint64_t *x, i
     for (int m = 1; m < N; m <<= 1) k_fxp_stage<<<(N / 2 + kTB - 1) / kTB, kTB, 0, st>>>(re, im, tw, m, N, ft);
     k_fxp_extract<<<(N / 2 + kTB - 1) / kTB, kTB, 0, st>>>(re, P->d_slot_pos, y, N, s_out);
     BLB_COUNT_LAUNCH(3 + logN);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_share_encode(const blb_params *P, const uint64_t *y, int ft, int s_out, uint64_t *x, void *ws,
+                                       size_t ws_bytes, void *stream) {
+    if (!P || !x || !y || !ws || ft < 1 || ft > 52 || s_out < 0 || s_out > 126) return BLB_E_INVALID_ARG;
+    const int N = P->N;
+    if (ws_bytes < (size_t)N * 48) {
+        blb_set_error("blb_share_encode: workspace needs %zu bytes", (size_t)N * 48);
+        return BLB_E_NOMEM;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    u128d *re = (u128d *)ws, *im = re + N;
+    long long *tw = (long long *)(im + N);
+    k_fxp_tw<<<(N + kTB - 1) / kTB, kTB, 0, st>>>(P->d_zeta, tw, ft, N);
+    k_fxp_scatter<<<(N / 2 + kTB - 1) / kTB, kTB, 0, st>>>(y, P->d_slot_pos, re, im, N);
+    for (int m = N / 2; m >= 1; m >>= 1)
+        k_fxp_stage_inv<<<(N / 2 + kTB - 1) / kTB, kTB, 0, st>>>(re, im, tw, m, N, ft);
+    k_fxp_coef<<<(N + kTB - 1) / kTB, kTB, 0, st>>>(re, x, N, s_out);
+    BLB_COUNT_LAUNCH(3 + P->logN);
     BLB_CHECK_LAUNCH();
     return BLB_OK;
 }

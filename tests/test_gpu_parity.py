@@ -519,6 +519,29 @@ def test_share_decode_bit_exact(name, request):
         assert np.array_equal(got, O.share_decode(pair.o, xs, ft, s_out))
 
 
+@pytest.mark.parametrize("name", ["toy", "bert"])
+def test_share_encode_bit_exact(name, request):
+    """Row f3 local fixed-point Encode (Alg. 2 line 1, C20): bit-exact over Z_{2^128} for a uniform
+    share, a fixed-point message, and the extreme words; the GPU encode then GPU decode round trip
+    returns Delta z."""
+    pair = request.getfixturevalue(name)
+    rng = np.random.default_rng(71)
+    y = rng.integers(0, 2 ** 63, (pair.n, 2), dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, (pair.n, 2),
+                                                                                            dtype=np.uint64)
+    y[0] = [0, 0]
+    y[1] = [2 ** 64 - 1, 2 ** 64 - 1]
+    y[2] = [0, 2 ** 63]
+    z = rng.uniform(-1, 1, pair.n)
+    f = 50
+    m = O.int_to_u128([int(round(v * 2.0 ** f)) for v in z])
+    s_out = f + pair.o.log_n - 40
+    for ys, ft, so in ((y, 50, s_out), (m, 50, s_out), (m, 30, 0), (y, 52, 126)):
+        got = u64(blb.share_encode(pair.g, dev(ys), ft, so))
+        assert np.array_equal(got, O.share_encode(pair.o, ys, ft, so))
+    back = O.u128_to_int(u64(blb.share_decode(pair.g, blb.share_encode(pair.g, dev(m), 50, s_out), 30, 0)))
+    assert np.abs(np.array(back, dtype=np.float64) - z * 2.0 ** 40).max() < 2.0 ** 12
+
+
 # ---------------------------------------------------------------- error behaviour (include/blb.h)
 def test_api_error_statuses(toy):
     """Each documented error status is raised before any launch, and degenerate calls are no-ops."""

@@ -99,3 +99,55 @@ def test_share_decode_two_party_reconstruction(toy):
     ym = O.u128_to_int(O.share_decode(toy, O.int_to_u128(m), ft, s_out))
     rec = [((a + b + (1 << 127)) % (1 << 128)) - (1 << 127) for a, b in zip(y0, y1)]
     assert max(abs(r - t) for r, t in zip(rec, ym)) <= 2
+
+
+# ---------------------------------------------------------------- f3: local fixed-point Encode (C20)
+def _fx(z, f):
+    return [int(round(v * 2.0 ** f)) for v in z]
+
+
+def test_share_encode_single_party_is_the_ckks_encode(toy):
+    """One party holding the whole slot vector y = round(2^f z): the local fixed-point Encode
+    (Alg. 2 line 1) equals the correctly rounded CKKS encode Delta pi^{-1}(y / 2^f) (C3, the
+    oracle's __float128 encode) within 1, for Delta = 2^(f + log N - s_out)."""
+    rng = np.random.default_rng(44)
+    z = rng.uniform(-1, 1, toy.n)
+    f, ft = 50, 50
+    s_out = f + toy.log_n - 40                     # Delta = 2^40
+    y = _fx(z, f)
+    x = O.u128_to_int(O.share_encode(toy, O.int_to_u128(y), ft, s_out))
+    exact = [int(v) for v in O.encode_coeffs(toy, np.array(y, dtype=np.float64) / 2.0 ** f, 2.0 ** 40)]
+    assert max(abs(a - b) for a, b in zip(x, exact)) <= 1
+    # constants encode to Delta c at coefficient 0 only (S:56); zero to zero
+    c = O.u128_to_int(O.share_encode(toy, O.int_to_u128([3 << (f - 2)] * toy.n), ft, s_out))
+    assert abs(c[0] - 3 * 2 ** 38) <= 1 and max(abs(v) for v in c[1:]) <= 1
+    assert O.u128_to_int(O.share_encode(toy, O.int_to_u128([0] * toy.n), ft, s_out)) == [0] * toy.N
+
+
+def test_share_encode_two_party_reconstruction(toy):
+    """Additive shares y0 + y1 = y over Z_{2^128}: the two local encodes add up to the encode of y
+    within the SecureML local-truncation error (App. C.4)."""
+    rng = np.random.default_rng(45)
+    z = rng.uniform(-1, 1, toy.n)
+    f, ft = 50, 50
+    s_out = f + toy.log_n - 40
+    y = _fx(z, f)
+    y0 = [int(a) | (int(b) << 64) for a, b in zip(rng.integers(0, 2 ** 63, toy.n, dtype=np.uint64),
+                                                  rng.integers(0, 2 ** 63, toy.n, dtype=np.uint64))]
+    y1 = [(v - a) % (1 << 128) for v, a in zip(y, y0)]
+    x0 = O.u128_to_int(O.share_encode(toy, O.int_to_u128(y0), ft, s_out))
+    x1 = O.u128_to_int(O.share_encode(toy, O.int_to_u128(y1), ft, s_out))
+    x = O.u128_to_int(O.share_encode(toy, O.int_to_u128(y), ft, s_out))
+    rec = [((a + b + (1 << 127)) % (1 << 128)) - (1 << 127) for a, b in zip(x0, x1)]
+    assert max(abs(r - t) for r, t in zip(rec, x)) <= 2
+
+
+def test_share_encode_then_decode_round_trip(toy):
+    """share_decode(share_encode(y)) returns Delta z (C18 after C20) within the fixed-point error."""
+    rng = np.random.default_rng(46)
+    z = rng.uniform(-1, 1, toy.n)
+    f, ft = 50, 50
+    s_out = f + toy.log_n - 40
+    x = O.share_encode(toy, O.int_to_u128(_fx(z, f)), ft, s_out)
+    back = O.u128_to_int(O.share_decode(toy, x, 30, 0))        # sum_k x_k Re(zeta^{k 5^j}) = Delta z_j
+    assert np.abs(np.array(back, dtype=np.float64) - z * 2.0 ** 40).max() < 2.0 ** 12   # |err| < 2^-28 of 1.0
