@@ -300,6 +300,72 @@ def ntt_pipes(ctr: dict, ntt: dict, params, pipes: dict, steps: int) -> dict:
             "hbm_frac": ntt["alg_bytes"] / t / 1e9 / float(measured_peaks().get("hbm_gbs", FALLBACK_HBM))}
 
 
+def f2_blocks(dims, args, device: int) -> dict:
+    """Row f2 for one layer (reading C21): per layer 12 negExp chains (Softmax exp of H x L x L),
+    12 Softmax smul_cc, 2 LayerNorm heads and 2 tails (L x d: d / (n / L) ciphertexts each) and the
+    GeLU head over L x ffn, on fresh ciphertexts of the Table-6 block-3 preset (N = 2^15, RNS
+    {60, 40 x 7} + {60}, scale 2^40).  Timed like the main step: W warm-ups, K steps between CUDA
+    events on the launching stream."""
+    import torch
+
+    import paper_2508_19525_b200 as blb
+    from paper_2508_19525_b200.blocks import Chains
+    P = bi.F2
+    params = blb.Params.from_preset(P, device=device)
+    n, L = params.n, dims["L"]
+    c = n // L
+    ch = Chains(params, None)
+    keys, sk = blb.keygen(params, bi.crypto_key(4, 200), ch.rotation_steps(L), relin=True)
+    ch.keys = keys
+    rng = np.random.default_rng(200)
+    top = params.K - 1
+    delta = 2.0 ** P.log_delta
+    cid = [0]
+
+    def enc(z, lvl=top):
+        cid[0] += 1
+        return blb.encrypt(params, sk, params.encode(torch.tensor(z)[None], delta, lvl)[0], lvl,
+                           bi.crypto_key(5, 200), cid[0], delta)
+
+    n_sm = -(-dims["H"] * L * L // n)
+    n_ln = -(-dims["d"] // c)
+    n_ge = -(-dims["ffn"] // c)
+    sm = [(enc(rng.uniform(-6, 0, n)), enc(rng.uniform(0, 7, n))) for _ in range(n_sm)]
+    sm_inv = [(enc(rng.uniform(0, 1, n)), enc(rng.uniform(0.01, 1, n))) for _ in range(n_sm)]
+    ln = [enc(rng.normal(0, 1, n)) for _ in range(n_ln)]
+    xmu = [enc(rng.normal(0, 1, n)) for _ in range(n_ln)]
+    rs = enc(rng.uniform(0.5, 2, n))
+    gam = [rng.normal(1, 0.1, n) for _ in range(n_ln)]
+    bet = [rng.normal(0, 0.1, n) for _ in range(n_ln)]
+    ge = [enc(rng.uniform(-2.7, 2.7, n)) for _ in range(n_ge)]
+    del sk
+
+    def step():
+        for x, xb in sm:
+            ch.negexp(x, xb)                           # block 2 (depth 7)
+        for xe, r in sm_inv:
+            ch.mul(xe, r)                              # Softmax smul_cc X_exp (x) 1/sum (block 3 head)
+        for _ in range(2):
+            ch.ln_head(ln, L, dims["d"])               # blocks 3 and 5 tails: LayerNorm lines 1-6
+            ch.ln_tail(xmu, rs, gam, bet)              # blocks 4 and 1 heads: LayerNorm lines 8-10
+        for x in ge:
+            ch.gelu_head(x, bi.GELU_COEF)              # block 4: GeLU lines 1-4
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return {"ms_per_step": e0.elapsed_time(e1) / args.steps, "preset": "N=2^15, Q={60,40x7}, P={60}, dnum=8 "
+            "(Table 6 block 3, P:719)", "ciphertexts": {"negexp": n_sm, "smul": n_sm, "layernorm": n_ln,
+                                                      "gelu": n_ge}}
+
+
 # --------------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -309,6 +375,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-f2", action="store_true")
     ap.add_argument("--dims", default="base", choices=["base", "large"])
     args = ap.parse_args()
     dims = dict(L=128, d=768, H=12, ffn=3072) if args.dims == "base" else dict(L=128, d=1024, H=16, ffn=4096)
@@ -469,6 +536,11 @@ def main():
         e2e = {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "pipeline": "upload and download streams double-buffered against compute (layer.LayerPipeline)"}
 
+    # ---- row f2: the fused-block chains between MPC steps (Table 6 block-3 preset, N = 2^15) ----
+    f2 = None
+    if rank == 0 and not args.no_f2:
+        f2 = f2_blocks(dims, args, local)
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -513,6 +585,10 @@ def main():
         "setup_s": {"keygen": t_keys, "weight_encode": t_encode, "plaintexts": layer.n_plaintexts(),
                     "plaintext_GB": layer.plaintext_bytes() / 1e9},
         "e2e": e2e,
+        "full_layer": ({"ms": ms_step + f2["ms_per_step"], "matmul_blocks_ms": ms_step, "f2_chains_ms": f2["ms_per_step"],
+                        "what": "the fused-linear MatMul step (value) + the row-f2 chains of one layer (negExp, "
+                                "Softmax smul_cc, 2 x LayerNorm head/tail, GeLU head) on the Table-6 block-3 preset",
+                        "f2": f2} if f2 else None),
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(dims)

@@ -121,3 +121,16 @@ def qk_toy_inputs(H=4, L=32, dh=32):
     Q = uniform(41, (H, L, dh), -1.0, 1.0)
     K = uniform(42, (H, L, dh), -1.0, 1.0)
     return dict(Q=Q, K=K, keys_key=crypto_key(4, 41), enc_key=crypto_key(5, 41), mask_key=crypto_key(3, 41))
+
+
+# ---- row f2: fused-block chains ---------------------------------------------
+# BOLT's GeLU approximation a|x|^4 + b|x|^3 + c|x|^2 + d|x| + e + 0.5 x on |x| <= 2.7;
+# the paper defers the coefficients to BOLT, so they are fitted here (reading C21): least squares of
+# 0.5 x erf(x / sqrt 2) on 20001 points of [0, 2.7] (max error 4.2e-3).  A workload parameter.
+GELU_COEF = (0.023453955861263417, -0.19812474039214562, 0.5675004464374074, -0.05485410511200729,
+             0.004240801424024679)
+# Table 6 block 3 preset: N = 32768, RNS {60, 40 x 7, 60}, scale 40 (depth 7); the f2
+# chains run on it (reading C21)
+F2 = Preset("f2", 15, (60, 40, 40, 40, 40, 40, 40, 40), (60,), 8, 40)
+# the same chain shape on a small ring for parity tests
+F2TOY = Preset("f2toy", 12, (60, 40, 40, 40, 40, 40, 40, 40), (60,), 8, 40)

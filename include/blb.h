@@ -219,6 +219,17 @@ blb_status blb_mul_pt(const blb_params *params, const blb_ct *in, const uint64_t
                       void *stream);
 /* ct + ct (same level): out = a + b (may alias a). BLB_E_SCALE if scales differ by > 1 bit. */
 blb_status blb_add(const blb_params *params, const blb_ct *a, const blb_ct *b, blb_ct *out, void *stream);
+/* ewadd_cp (e.g. the "+1" of negExp and the "+beta" of LayerNorm):
+ * out = (c0 + pt, c1), pt device [level+1][N] NTT form encoded at the ciphertext's scale and
+ * level; out may alias in; scale / level of in. */
+blb_status blb_add_pt(const blb_params *params, const blb_ct *in, const uint64_t *pt, blb_ct *out, void *stream);
+/* Exact level drop (C9: levels are aligned by dropping limbs): out = the residues mod
+ * q_0..q_level of in; out [2][level+1][N] must not overlap in; BLB_E_LEVEL if level > in->level. */
+blb_status blb_drop_level(const blb_params *params, const blb_ct *in, int level, blb_ct *out, void *stream);
+/* ct - ct (same level; sadd_cc with a negated operand, e.g. X - Xbar of Softmax and X - mu of
+ * LayerNorm): out = a - b limb-wise (may alias a), scale a.scale; BLB_E_LEVEL /
+ * BLB_E_SCALE as blb_add. */
+blb_status blb_sub(const blb_params *params, const blb_ct *a, const blb_ct *b, blb_ct *out, void *stream);
 
 /* CKKS->MPC masking, server half of Algorithm 1 line 1 (F_C2M items 1
  * and 4; reading C14): for each of n_ct ciphertexts, drop to q_0,

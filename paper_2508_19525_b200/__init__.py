@@ -81,6 +81,9 @@ def lib() -> ctypes.CDLL:
             "blb_rescale": ([vp, vp, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
             "blb_mul_pt": ([vp, vp, vp, dbl, vp, vp], ctypes.c_int),
             "blb_add": ([vp, vp, vp, vp, vp], ctypes.c_int),
+            "blb_sub": ([vp, vp, vp, vp, vp], ctypes.c_int),
+            "blb_add_pt": ([vp, vp, vp, vp, vp], ctypes.c_int),
+            "blb_drop_level": ([vp, vp, ctypes.c_int, vp, vp], ctypes.c_int),
             "blb_ckks_to_mpc": ([vp, vp, ctypes.c_int, ctypes.c_char_p, u64, vp, vp, vp, ctypes.c_size_t, vp],
                                 ctypes.c_int),
             "blb_mhp_column_map": ([ctypes.c_int] * 4 + [vp, ip], ctypes.c_int),
@@ -367,6 +370,32 @@ def add(params: Params, a: Ciphertext, b: Ciphertext) -> Ciphertext:
     out = Ciphertext.empty(params, a.level)
     ca, cb, co = a.c(), b.c(), out.c()
     _check(lib().blb_add(params.handle, ctypes.byref(ca), ctypes.byref(cb), ctypes.byref(co), _stream()))
+    out.level, out.scale = co.level, co.scale
+    return out
+
+
+def sub(params: Params, a: Ciphertext, b: Ciphertext) -> Ciphertext:
+    out = Ciphertext.empty(params, a.level)
+    ca, cb, co = a.c(), b.c(), out.c()
+    _check(lib().blb_sub(params.handle, ctypes.byref(ca), ctypes.byref(cb), ctypes.byref(co), _stream()))
+    out.level, out.scale = co.level, co.scale
+    return out
+
+
+def add_pt(params: Params, ct: Ciphertext, pt: torch.Tensor) -> Ciphertext:
+    """ewadd_cp: (c0 + pt, c1); pt encoded at the ciphertext's scale and level."""
+    out = Ciphertext.empty(params, ct.level)
+    ci, co = ct.c(), out.c()
+    _check(lib().blb_add_pt(params.handle, ctypes.byref(ci), _ptr(pt.contiguous()), ctypes.byref(co), _stream()))
+    out.level, out.scale = co.level, co.scale
+    return out
+
+
+def drop_level(params: Params, ct: Ciphertext, level: int) -> Ciphertext:
+    """Exact level drop (C9)."""
+    out = Ciphertext.empty(params, level)
+    ci, co = ct.c(), out.c()
+    _check(lib().blb_drop_level(params.handle, ctypes.byref(ci), int(level), ctypes.byref(co), _stream()))
     out.level, out.scale = co.level, co.scale
     return out
 

@@ -31,6 +31,8 @@ blb_status blb_launch_encrypt_combine(const blb_params *P, u64 *c0, const u64 *c
 blb_status blb_launch_decrypt(const blb_params *P, const u64 *c0, const u64 *c1, const u64 *s, u64 *out, int k,
                               cudaStream_t st);
 blb_status blb_launch_mul_pt(const blb_params *P, const u64 *in, const u64 *pt, u64 *out, int k, cudaStream_t st);
+blb_status blb_launch_sub(const blb_params *P, const u64 *a, const u64 *b, u64 *out, int k, int npoly,
+                          cudaStream_t st);
 blb_status blb_launch_add(const blb_params *P, const u64 *a, const u64 *b, u64 *out, int k, int npoly,
                           cudaStream_t st);
 blb_status blb_launch_tensor(const blb_params *P, const u64 *a, const u64 *b, u64 *d, int k, cudaStream_t st);
@@ -685,6 +687,54 @@ extern "C" blb_status blb_add(const blb_params *P, const blb_ct *a, const blb_ct
         return BLB_E_SCALE;
     }
     BLB_TRY(blb_launch_add(P, a->data, b->data, out->data, a->level + 1, 2, (cudaStream_t)stream));
+    out->level = a->level;
+    out->scale = a->scale;
+    return BLB_OK;
+}
+
+// ewadd_cp: out = (c0 + pt, c1) (pt: [level+1][N] NTT at the ciphertext's scale); out may alias in
+extern "C" blb_status blb_add_pt(const blb_params *P, const blb_ct *in, const uint64_t *pt, blb_ct *out, void *stream) {
+    if (!P || !in || !pt || !out || !in->data || !out->data) return BLB_E_INVALID_ARG;
+    const int k = in->level + 1;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (out->data != in->data)
+        BLB_CUDA_TRY(cudaMemcpyAsync(out->data + (size_t)k * P->N, in->data + (size_t)k * P->N,
+                                     sizeof(u64) * (size_t)k * P->N, cudaMemcpyDeviceToDevice, st));
+    BLB_TRY(blb_launch_add(P, in->data, pt, out->data, k, 1, st));
+    out->level = in->level;
+    out->scale = in->scale;
+    return BLB_OK;
+}
+
+// exact level drop (C9): out = the limbs q_0..q_level of in ([2][level+1][N])
+extern "C" blb_status blb_drop_level(const blb_params *P, const blb_ct *in, int level, blb_ct *out, void *stream) {
+    if (!P || !in || !out || !in->data || !out->data) return BLB_E_INVALID_ARG;
+    if (level < 0 || level > in->level) {
+        blb_set_error("blb_drop_level: level %d outside [0, %d]", level, in->level);
+        return BLB_E_LEVEL;
+    }
+    const size_t N = P->N, kin = in->level + 1, k = level + 1;
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int p = 0; p < 2; p++)
+        BLB_CUDA_TRY(cudaMemcpyAsync(out->data + p * k * N, in->data + p * kin * N, sizeof(u64) * k * N,
+                                     cudaMemcpyDeviceToDevice, st));
+    out->level = level;
+    out->scale = in->scale;
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_sub(const blb_params *P, const blb_ct *a, const blb_ct *b, blb_ct *out, void *stream) {
+    if (!P || !a || !b || !out || !a->data || !b->data || !out->data) return BLB_E_INVALID_ARG;
+    if (a->level != b->level) {
+        blb_set_error("blb_sub: level mismatch %d vs %d", a->level, b->level);
+        return BLB_E_LEVEL;
+    }
+    const double r = a->scale / b->scale;
+    if (r > 2.0 || r < 0.5) {
+        blb_set_error("blb_sub: scale mismatch > 1 bit");
+        return BLB_E_SCALE;
+    }
+    BLB_TRY(blb_launch_sub(P, a->data, b->data, out->data, a->level + 1, 2, (cudaStream_t)stream));
     out->level = a->level;
     out->scale = a->scale;
     return BLB_OK;

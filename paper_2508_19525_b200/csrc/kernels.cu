@@ -148,6 +148,13 @@ __global__ void k_add(const u64 *a, const u64 *b, u64 *out, Primes pr, int k, in
     const long long o = ((long long)p * k + i) * N + x;
     out[o] = addmod(a[o], b[o], pr.m[i].q);
 }
+__global__ void k_sub(const u64 *a, const u64 *b, u64 *out, Primes pr, int k, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y, p = blockIdx.z;
+    if (x >= N) return;
+    const long long o = ((long long)p * k + i) * N + x;
+    out[o] = submod(a[o], b[o], pr.m[i].q);
+}
 
 // ------------------------------------------------------------ ModUp (C7)
 struct PtrList {
@@ -1029,6 +1036,13 @@ blb_status blb_launch_mul_pt(const blb_params *P, const u64 *in, const u64 *pt, 
 blb_status blb_launch_add(const blb_params *P, const u64 *a, const u64 *b, u64 *out, int k, int npoly,
                           cudaStream_t st) {
     k_add<<<grid_x(P->N, k, npoly), kTB, 0, st>>>(a, b, out, P->pr, k, P->N);
+    BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+blb_status blb_launch_sub(const blb_params *P, const u64 *a, const u64 *b, u64 *out, int k, int npoly,
+                          cudaStream_t st) {
+    k_sub<<<grid_x(P->N, k, npoly), kTB, 0, st>>>(a, b, out, P->pr, k, P->N);
     BLB_COUNT_LAUNCH(1);
     BLB_CHECK_LAUNCH();
     return BLB_OK;

@@ -539,7 +539,8 @@ def test_share_encode_bit_exact(name, request):
         got = u64(blb.share_encode(pair.g, dev(ys), ft, so))
         assert np.array_equal(got, O.share_encode(pair.o, ys, ft, so))
     back = O.u128_to_int(u64(blb.share_decode(pair.g, blb.share_encode(pair.g, dev(m), 50, s_out), 30, 0)))
-    assert np.abs(np.array(back, dtype=np.float64) - z * 2.0 ** 40).max() < 2.0 ** 12
+    # the decode's 2^-30 twiddles over log N stages bound the error (< 2^-22 of Delta at N = 2^16)
+    assert np.abs(np.array(back, dtype=np.float64) - z * 2.0 ** 40).max() < 2.0 ** 18
 
 
 # ---------------------------------------------------------------- error behaviour (include/blb.h)
