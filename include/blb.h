@@ -337,7 +337,8 @@ blb_status blb_matmul_pt_bytes(const blb_matmul_plan *plan, int out_first, int o
  * [plaintext][tile]) so that the MAC streams each output's weights
  * contiguously; a tile of a limb with prime < 2^40 is stored as 512 low 32-bit
  * words followed by 512 high bytes (the residues are < 2^40: a lossless 5-byte
- * packing of the dominant HBM stream), other limbs as 512 words.  Synchronises. */
+ * packing of the dominant HBM stream), other limbs as 512 words.  W may be host or device memory
+ * (unified addressing: per-layer re-encode from device-resident weights).  Synchronises. */
 blb_status blb_matmul_encode_weights(const blb_matmul_plan *plan, const double *W, int out_first, int out_count,
                                      uint64_t *pt_dev, void *stream);
 
@@ -379,6 +380,15 @@ size_t blb_f2_workspace_bytes(const blb_params *params, int level);
  * caller rescales).  Needs the relinearisation key (Galois element 0). */
 blb_status blb_mul_relin(const blb_params *params, const blb_keys *keys, const blb_ct *a, const blb_ct *b,
                          blb_ct *out, void *ws, size_t ws_bytes, void *stream);
+
+/* Batched ewmul_cc (+ rescale): out[t] = mul_relin(a[t], b[t]) (then rescaled when rescale != 0),
+ * t < n -- one tensor launch, one ModUp and one key-switch batch (the relinearisation key is read
+ * once per tile for the whole batch), one rescale batch; the per-pair bits of blb_mul_relin +
+ * blb_rescale.  All operands at one level (BLB_E_LEVEL otherwise); out[t] [2][level(-1)][N];
+ * ws: blb_mul_relin_batch_workspace_bytes(level, n). */
+size_t blb_mul_relin_batch_workspace_bytes(const blb_params *params, int level, int n);
+blb_status blb_mul_relin_batch(const blb_params *params, const blb_keys *keys, const blb_ct *a, const blb_ct *b, int n,
+                               int rescale, blb_ct *out, void *ws, size_t ws_bytes, void *stream);
 
 /* Rotate-and-sum of BLB's summation operator (Table 3) on a
  * spatial-first ciphertext with L rows and D (power of two) columns:

@@ -110,6 +110,9 @@ def lib() -> ctypes.CDLL:
                                   vp], ctypes.c_int),
             "blb_f2_workspace_bytes": ([vp, ctypes.c_int], ctypes.c_size_t),
             "blb_mul_relin": ([vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
+            "blb_mul_relin_batch_workspace_bytes": ([vp, ctypes.c_int, ctypes.c_int], ctypes.c_size_t),
+            "blb_mul_relin_batch": ([vp, vp, vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t, vp],
+                                    ctypes.c_int),
             "blb_rotate_sum": ([vp, vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
             "blb_broadcast": ([vp, vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
             "blb_qk_plan_create": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp],
@@ -472,6 +475,27 @@ def mul_relin(params: Params, keys: Keys, a: Ciphertext, b: Ciphertext) -> Ciphe
     return out
 
 
+def mul_relin_batch(params: Params, keys: Keys, a: list, b: list, rescale: bool = True,
+                    ws: torch.Tensor | None = None) -> list:
+    """n pairs: tensor + relinearisation (+ rescale) in batched launches (row f2)."""
+    n = len(a)
+    if n == 0:
+        return []
+    lvl = a[0].level
+    outs = [Ciphertext.empty(params, lvl - 1 if rescale else lvl) for _ in range(n)]
+    nb = int(lib().blb_mul_relin_batch_workspace_bytes(params.handle, lvl, n))
+    if ws is None or ws.numel() * 8 < nb:
+        ws = torch.empty(nb // 8 + 1, dtype=torch.int64, device="cuda")
+    ca = (_Ct * n)(*[c.c() for c in a])
+    cb = (_Ct * n)(*[c.c() for c in b])
+    co = (_Ct * n)(*[o.c() for o in outs])
+    _check(lib().blb_mul_relin_batch(params.handle, keys.handle, ca, cb, n, int(bool(rescale)), co, _ptr(ws),
+                                     ws.numel() * 8, _stream()))
+    for o, c in zip(outs, co):
+        o.level, o.scale = c.level, c.scale
+    return outs
+
+
 def rotate_sum(params: Params, keys: Keys, ct: Ciphertext, L: int, D: int, broadcast: bool = False) -> Ciphertext:
     """Rotate-and-sum: log2 D rotations, fused form (no mask)."""
     out = Ciphertext.empty(params, ct.level)
@@ -543,16 +567,24 @@ class MatmulPlan:
         _check(lib().blb_matmul_pt_count(self._h, out_first, out_count, ctypes.byref(n)))
         return n.value
 
-    def encode_weights(self, W: np.ndarray, out_first: int = 0, out_count: int | None = None) -> torch.Tensor:
+    def encode_weights(self, W, out_first: int = 0, out_count: int | None = None,
+                       out: torch.Tensor | None = None) -> torch.Tensor:
+        """W: host float64 array or a device float64 tensor (per-layer re-encode); out: reuse a buffer."""
         out_count = self.n_out - out_first if out_count is None else out_count
-        W = np.ascontiguousarray(W, dtype=np.float64)
-        assert W.shape == self.w_shape
+        if isinstance(W, torch.Tensor):
+            assert W.dtype == torch.float64 and W.is_contiguous() and tuple(W.shape) == self.w_shape
+            wptr = ctypes.c_void_p(W.data_ptr())
+        else:
+            W = np.ascontiguousarray(W, dtype=np.float64)
+            assert W.shape == self.w_shape
+            wptr = W.ctypes.data_as(ctypes.c_void_p)
         nbytes = ctypes.c_size_t(0)
         _check(lib().blb_matmul_pt_bytes(self._h, out_first, out_count, ctypes.byref(nbytes)))
         # opaque width-packed blocked layout (include/blb.h): int64 words, 16-byte aligned
-        pts = torch.empty(max(1, (nbytes.value + 7) // 8), dtype=torch.int64, device="cuda")
-        _check(lib().blb_matmul_encode_weights(self._h, W.ctypes.data_as(ctypes.c_void_p), out_first, out_count,
-                                               _ptr(pts), _stream()))
+        n = max(1, (nbytes.value + 7) // 8)
+        pts = torch.empty(n, dtype=torch.int64, device="cuda") if out is None else out
+        assert pts.numel() >= n
+        _check(lib().blb_matmul_encode_weights(self._h, wptr, out_first, out_count, _ptr(pts), _stream()))
         return pts
 
     def workspace_bytes(self, out_count: int | None = None) -> int:

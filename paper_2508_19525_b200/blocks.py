@@ -49,19 +49,28 @@ class Chains:
         return blb.rescale(self.p, blb.mul_pt(self.p, ct, self._encode(vec, s, ct.level), s))
 
     def square(self, a):
-        return blb.rescale(self.p, blb.mul_relin(self.p, self.keys, a, a))
+        return self.squares([a])[0]
 
     def mul(self, a, b):
-        lv = min(a.level, b.level)
-        return blb.rescale(self.p, blb.mul_relin(self.p, self.keys, self.drop(a, lv), self.drop(b, lv)))
+        return self.muls([a], [b])[0]
 
-    # ---- the chains ----
-    def negexp(self, x, xbar, t: int = 6):
-        y = self.mul_const(blb.sub(self.p, x, xbar), 2.0 ** -t)
-        y = self.add_const(y, 1.0)
+    # batched ct x ct products (one tensor / ModUp / key-switch / rescale batch per call)
+    def squares(self, xs: list) -> list:
+        return blb.mul_relin_batch(self.p, self.keys, xs, xs)
+
+    def muls(self, as_: list, bs: list) -> list:
+        lv = min(min(a.level for a in as_), min(b.level for b in bs))
+        return blb.mul_relin_batch(self.p, self.keys, [self.drop(a, lv) for a in as_], [self.drop(b, lv) for b in bs])
+
+    # ---- the chains (lists of independent ciphertexts run in lockstep) ----
+    def negexp_n(self, xs: list, xbars: list, t: int = 6) -> list:
+        ys = [self.add_const(self.mul_const(blb.sub(self.p, x, xb), 2.0 ** -t), 1.0) for x, xb in zip(xs, xbars)]
         for _ in range(t):
-            y = self.square(y)
-        return y
+            ys = self.squares(ys)
+        return ys
+
+    def negexp(self, x, xbar, t: int = 6):
+        return self.negexp_n([x], [xbar], t)[0]
 
     def row_sum(self, cts: list, L: int):
         s = cts[0]
@@ -72,32 +81,35 @@ class Chains:
     def ln_head(self, xs: list, L: int, D: int):
         mu = self.mul_const(self.row_sum(xs, L), 1.0 / D)
         xmu = [blb.sub(self.p, self.drop(x, mu.level), mu) for x in xs]
-        var = self.mul_const(self.row_sum([self.square(v) for v in xmu], L), 1.0 / D)
+        var = self.mul_const(self.row_sum(self.squares(xmu), L), 1.0 / D)
         return xmu, var
 
     def ln_tail(self, xmu: list, rs, gamma: list, beta: list) -> list:
+        ys = self.muls(xmu, [rs] * len(xmu))
+        return [self.add_const(self.mul_const(y, g), b) for y, g, b in zip(ys, gamma, beta)]
+
+    def gelu_head_n(self, xs: list, coef) -> list:
+        a, b, c, d, e = coef
+        x2 = self.squares(xs)
+        x3 = self.muls(x2, xs)
+        x4 = self.squares(x2)
         out = []
-        for v, g, b in zip(xmu, gamma, beta):
-            y = self.mul_const(self.mul(v, rs), g)
-            out.append(self.add_const(y, b))
+        for x, y2, y3, y4 in zip(xs, x2, x3, x4):
+            s4 = y4.scale
+            ax4 = self.mul_const(y4, a)
+            lv = ax4.level
+            bx3 = self.drop(self.mul_const(y3, b, s4), lv)
+            cx2 = self.drop(self.mul_const(y2, c, s4), lv)
+            xm = self.drop(self.mul_const(x, 0.5 - d, s4), lv)
+            xp = self.drop(self.mul_const(x, 0.5 + d, s4), lv)
+            base = blb.add(self.p, ax4, cx2)
+            f0 = self.add_const(blb.add(self.p, blb.sub(self.p, base, bx3), xm), e)
+            f1 = self.add_const(blb.add(self.p, blb.add(self.p, base, bx3), xp), e)
+            out.append((f0, f1))
         return out
 
     def gelu_head(self, x, coef):
-        a, b, c, d, e = coef
-        x2 = self.square(x)
-        x3 = self.mul(x2, x)
-        x4 = self.square(x2)
-        s4 = x4.scale
-        ax4 = self.mul_const(x4, a)
-        lv = ax4.level
-        bx3 = self.drop(self.mul_const(x3, b, s4), lv)
-        cx2 = self.drop(self.mul_const(x2, c, s4), lv)
-        xm = self.drop(self.mul_const(x, 0.5 - d, s4), lv)
-        xp = self.drop(self.mul_const(x, 0.5 + d, s4), lv)
-        base = blb.add(self.p, ax4, cx2)
-        f0 = self.add_const(blb.add(self.p, blb.sub(self.p, base, bx3), xm), e)
-        f1 = self.add_const(blb.add(self.p, blb.add(self.p, base, bx3), xp), e)
-        return f0, f1
+        return self.gelu_head_n([x], coef)[0]
 
     def rotation_steps(self, L: int) -> list[int]:
         steps, s = [], L

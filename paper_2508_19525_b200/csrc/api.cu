@@ -36,6 +36,8 @@ blb_status blb_launch_sub(const blb_params *P, const u64 *a, const u64 *b, u64 *
 blb_status blb_launch_add(const blb_params *P, const u64 *a, const u64 *b, u64 *out, int k, int npoly,
                           cudaStream_t st);
 blb_status blb_launch_tensor(const blb_params *P, const u64 *a, const u64 *b, u64 *d, int k, cudaStream_t st);
+blb_status blb_launch_tensor_n(const blb_params *P, const u64 *const *a, const u64 *const *b, int n, u64 *d, int k,
+                               cudaStream_t st);
 blb_status blb_launch_mask(const blb_params *P, const u64 *const *in, int n, int level, const uint8_t key[32],
                            u64 id0, u64 *masked, u64 *share, cudaStream_t st);
 
@@ -870,6 +872,84 @@ extern "C" blb_status blb_mul_relin(const blb_params *P, const blb_keys *K, cons
     BLB_COUNT(3, 1);
     out->level = level;
     out->scale = a->scale * b->scale;
+    return BLB_OK;
+}
+
+// Batched ewmul_cc: n independent pairs in one tensor launch, one ModUp batch, one key-switch batch
+// (the relinearisation key read once per tile for the whole batch) and one rescale batch -- the
+// same operations, per pair, as blb_mul_relin followed by blb_rescale.
+static size_t mrb_elems(const blb_params *P, int level, int n) {
+    const size_t N = P->N, k = level + 1, E = k + P->np, beta = blb_beta(P, level);
+    // tensors, extended digits, coefficient scratch, key-switch outputs, key-switch scratch (which
+    // also takes the rescaled [n][2][level][N]), rescale scratch (last limbs + lifted residues)
+    return (size_t)n * (3 * k + beta * E + k + 2 * k) * N + keyswitch_scratch_elems(P, level, n) +
+           (size_t)n * 2 * (1 + k) * N;
+}
+extern "C" size_t blb_mul_relin_batch_workspace_bytes(const blb_params *P, int level, int n) {
+    if (!P || level < 0 || level >= P->K || n < 1) return 0;
+    return sizeof(u64) * mrb_elems(P, level, std::min(n, kMaxJobs));
+}
+extern "C" blb_status blb_mul_relin_batch(const blb_params *P, const blb_keys *K, const blb_ct *a, const blb_ct *b,
+                                          int n, int rescale, blb_ct *out, void *ws, size_t ws_bytes, void *stream) {
+    if (!P || !K || n < 0 || (n > 0 && (!a || !b || !out || !ws))) return BLB_E_INVALID_ARG;
+    if (n == 0) return BLB_OK;
+    const int level = a[0].level;
+    for (int t = 0; t < n; t++) {
+        if (!a[t].data || !b[t].data || !out[t].data) return BLB_E_INVALID_ARG;
+        if (a[t].level != level || b[t].level != level) {
+            blb_set_error("blb_mul_relin_batch: all operands must share one level");
+            return BLB_E_LEVEL;
+        }
+    }
+    if (level < (rescale ? 1 : 0) || level >= P->K) return BLB_E_LEVEL;
+    const u64 *rlk = find_key(K, 0);
+    if (!rlk) {
+        blb_set_error("missing relinearisation key");
+        return BLB_E_MISSING_KEY;
+    }
+    if (ws_bytes < blb_mul_relin_batch_workspace_bytes(P, level, n)) return BLB_E_NOMEM;
+    const int k = level + 1, N = P->N, E = k + P->np, beta = blb_beta(P, level);
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int t0 = 0; t0 < n; t0 += kMaxJobs) {
+        const int m = std::min(kMaxJobs, n - t0);
+        u64 *d = (u64 *)ws;
+        u64 *ext = d + (size_t)m * 3 * k * N, *coef = ext + (size_t)m * beta * E * N;
+        u64 *tmp = coef + (size_t)m * k * N, *ks = tmp + (size_t)m * 2 * k * N;
+        u64 *resc = ks + keyswitch_scratch_elems(P, level, m);
+        u64 *ks_u = ks, *ks_conv = ks + (size_t)m * 2 * E * N;
+        std::vector<const u64 *> pa(m), pb(m), d2(m);
+        for (int t = 0; t < m; t++) {
+            pa[t] = a[t0 + t].data;
+            pb[t] = b[t0 + t].data;
+            d2[t] = d + ((size_t)t * 3 + 2) * k * N;
+        }
+        BLB_TRY(blb_launch_tensor_n(P, pa.data(), pb.data(), m, d, k, st));
+        BLB_TRY(launch_modup(P, level, d2.data(), m, ext, coef, st));
+        std::vector<KsJob> jobs(m);
+        for (int t = 0; t < m; t++) {
+            KsJob J{};
+            J.ext = ext + (size_t)t * beta * E * N; J.key = rlk; J.c0 = d + (size_t)t * 3 * k * N;
+            J.c1_add = J.c0 + (size_t)k * N;
+            J.out = rescale ? tmp + (size_t)t * 2 * k * N : out[t0 + t].data;
+            J.galois = 1; J.add_mode = 2;
+            jobs[t] = J;
+        }
+        BLB_TRY(launch_keyswitch(P, level, jobs.data(), m, ks_u, ks_conv, st));
+        BLB_COUNT(3, m);
+        if (rescale) {
+            // [m][2][k][N] -> [m][2][level][N] contiguous in ks scratch, then to the outputs
+            u64 *r = ks;
+            BLB_TRY(launch_rescale(P, tmp, level, 2 * m, r, resc, st));
+            for (int t = 0; t < m; t++)
+                BLB_CUDA_TRY(cudaMemcpyAsync(out[t0 + t].data, r + (size_t)t * 2 * level * N,
+                                             sizeof(u64) * 2 * level * N, cudaMemcpyDeviceToDevice, st));
+        }
+        for (int t = 0; t < m; t++) {
+            out[t0 + t].level = rescale ? level - 1 : level;
+            out[t0 + t].scale = rescale ? (a[t0 + t].scale * b[t0 + t].scale) / (double)P->mod[level]
+                                        : a[t0 + t].scale * b[t0 + t].scale;
+        }
+    }
     return BLB_OK;
 }
 

@@ -538,8 +538,38 @@ __global__ void k_tensor(const u64 *a, const u64 *b, u64 *d, Primes pr, int k, i
     d[2 * kN + lx] = mulmod(a1, b1, mc);
 }
 
+// n tensors (C9) in one launch: d[t] = (a0 b0, a0 b1 + a1 b0, a1 b1) of the pair (a[t], b[t]), [n][3][k][N]
+__global__ void k_tensor_n(PtrList a, PtrList b, u64 *d, Primes pr, int k, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int l = blockIdx.y, t = blockIdx.z;
+    if (x >= N) return;
+    const long long kN = (long long)k * N, lx = (long long)l * N + x;
+    const u64 a0 = a.p[t][lx], a1 = a.p[t][kN + lx], b0 = b.p[t][lx], b1 = b.p[t][kN + lx];
+    const ModConst &mc = pr.m[l];
+    Acc128 s;
+    s.zero();
+    s.mac(a0, b1);
+    s.mac(a1, b0);
+    u64 *o = d + (long long)t * 3 * kN + lx;
+    o[0] = mulmod(a0, b0, mc);
+    o[kN] = s.reduce(mc);
+    o[2 * kN] = mulmod(a1, b1, mc);
+}
+
 inline dim3 grid_x(int N, int y = 1, int z = 1) { return dim3((N + kTB - 1) / kTB, y, z); }
 }  // namespace
+
+blb_status blb_launch_tensor_n(const blb_params *P, const u64 *const *a, const u64 *const *b, int n, u64 *d, int k,
+                               cudaStream_t st) {
+    if (n <= 0) return BLB_OK;
+    if (n > kMaxJobs) return BLB_E_INVALID_ARG;
+    PtrList pa{}, pb{};
+    for (int t = 0; t < n; t++) { pa.p[t] = a[t]; pb.p[t] = b[t]; }
+    k_tensor_n<<<grid_x(P->N, k, n), kTB, 0, st>>>(pa, pb, d, P->pr, k, P->N);
+    BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
 
 blb_status blb_launch_tensor(const blb_params *P, const u64 *a, const u64 *b, u64 *d, int k, cudaStream_t st) {
     k_tensor<<<grid_x(P->N, k), kTB, 0, st>>>(a, b, d, P->pr, k, P->N);

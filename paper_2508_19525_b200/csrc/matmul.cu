@@ -751,7 +751,8 @@ extern "C" blb_status blb_matmul_encode_weights(const blb_matmul_plan *pl, const
     int *flag = nullptr;
     const int chunk = 64;
     BLB_CUDA_TRY(cudaMallocAsync(&dW, sizeof(double) * (size_t)pl->w_rows * pl->w_cols, st));
-    BLB_CUDA_TRY(cudaMemcpyAsync(dW, W, sizeof(double) * (size_t)pl->w_rows * pl->w_cols, cudaMemcpyHostToDevice, st));
+    // W may be host or device memory (unified addressing): per-layer re-encode from device-resident weights
+    BLB_CUDA_TRY(cudaMemcpyAsync(dW, W, sizeof(double) * (size_t)pl->w_rows * pl->w_cols, cudaMemcpyDefault, st));
     BLB_CUDA_TRY(cudaMallocAsync(&slots, sizeof(double) * (size_t)chunk * pl->n, st));
     BLB_CUDA_TRY(cudaMallocAsync(&buf, sizeof(double) * encode_scratch_doubles(P, chunk), st));
     BLB_CUDA_TRY(cudaMallocAsync(&flag, sizeof(int), st));

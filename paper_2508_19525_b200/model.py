@@ -1,0 +1,83 @@
+"""Config 5 (BASELINE.json): GPT2-base, 12 layers of the fused-linear CKKS path on one rank group.
+
+GPT2-base has the BERT-base layer shape (d = 768, 12 heads, FFN 3072; L = 128 tokens as
+BASELINE.json sets it, the paper ran 64, reading S25), so every layer is one
+layer.FusedLinearLayer step (QKV + Q K^T + masks, Softmax x V + W_O + mask, FFN1 + mask,
+FFN2 + mask) with its own weights.  Its packed plaintexts are 56.7 GB per layer -- 680 GB for
+12 layers, far beyond one B200's 180 GB -- so the weights of every layer stay resident on the
+device as float64 matrices (57 MB per layer) and each layer's plaintexts are re-encoded on the
+device (row a0: slot build, double-double encode, NTT, width-packed blocked layout) into ONE
+reused plaintext buffer per plan right before that layer's step.  At world = 8
+each rank's window holds 1/8 of every layer's plaintexts (85 GB for all 12), so the stack can
+instead keep them resident: `resident=True` encodes every layer once (setup) and skips the
+re-encode.  Synthetic weights: SURVEY 8(d) config 5, seeds 100 + 10 * layer + m.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import paper_2508_19525_b200 as blb
+from paper_2508_19525_b200.layer import Dims, FusedLinearLayer
+
+
+def gpt2_layer_weights(layer: int, dims: Dims) -> list:
+    """W_Q, W_K, W_V, W_O, W_1, W_2 of one layer: N(0, 0.04^2) (W_2: N(0, 0.02^2)), seeds 100 + 10 l + m."""
+    d, f = dims.d, dims.ffn
+    shapes = [(d, d), (d, d), (d, d), (d, d), (d, f), (f, d)]
+    stds = [0.04, 0.04, 0.04, 0.04, 0.04, 0.02]
+    return [np.random.default_rng(100 + 10 * layer + m).normal(0.0, sd, sh) for m, (sh, sd) in
+            enumerate(zip(shapes, stds))]
+
+
+class GPT2Stack:
+    def __init__(self, params: blb.Params, n_layers: int = 12, dims: Dims = Dims(), bsgs: dict | None = None,
+                 rank: int = 0, world: int = 1, resident: bool = False):
+        self.p, self.n_layers, self.dims, self.resident = params, n_layers, dims, resident
+        self.layer = FusedLinearLayer(params, dims, rank, world, bsgs=bsgs)
+        self.w_dev = []      # per layer: device float64 matrices in the plans' shapes
+        self.pts = []        # resident mode: per layer the encoded plaintexts
+        for l in range(n_layers):
+            WQ, WK, WV, WO, W1, W2 = gpt2_layer_weights(l, dims)
+            Wqkv = np.concatenate([WQ, WK, WV], axis=1)
+            dh = dims.d // dims.H
+            WOp = np.zeros((self.layer.Hp * dh, WO.shape[1]))
+            WOp[:WO.shape[0]] = WO
+            self.w_dev.append({k: torch.tensor(np.ascontiguousarray(w), dtype=torch.float64, device="cuda")
+                               for k, w in (("qkv", Wqkv), ("oproj", WOp), ("ffn1", W1), ("ffn2", W2))})
+        # first layer through the layer's own loader: allocates the plaintext buffers, masks, workspace
+        self.layer.load_weights(*gpt2_layer_weights(0, dims))
+        self.loaded = 0
+        if resident:
+            for l in range(n_layers):
+                self.pts.append({k: self._encode(l, k) for k in self.layer.plans})
+
+    def _encode(self, l: int, name: str, out=None) -> torch.Tensor:
+        pl = self.layer.plans[name]
+        if self.layer.world == 1:
+            first, count = self.layer.slices[name]
+            return pl.encode_weights(self.w_dev[l][name], first, count, out=out)
+        return pl.encode_weights(self.w_dev[l][name], out=out)
+
+    def load_layer(self, l: int):
+        """Make layer l's plaintexts the ones the layer step streams (re-encode on the device)."""
+        if self.resident:
+            self.layer.pts = self.pts[l]
+        elif self.loaded != l:
+            for name in self.layer.plans:
+                self._encode(l, name, out=self.layer.pts[name])
+        self.loaded = l
+
+    def rotation_steps(self) -> list[int]:
+        return self.layer.rotation_steps()
+
+    def step(self, keys: blb.Keys, inputs: list, mask_key: bytes, seq0: int | None = None) -> list:
+        """inputs[l]: the client's fresh ciphertexts of layer l (dict as FusedLinearLayer.step).
+        -> per layer the masked outputs + server shares (the client reconstructs, runs the MPC
+        nonlinear layers and re-encrypts the next layer's inputs)."""
+        out = []
+        seq = self.layer.seq if seq0 is None else seq0
+        for l in range(self.n_layers):
+            self.load_layer(l)
+            out.append(self.layer.step(keys, inputs[l % len(inputs)], mask_key, seq=seq + l))
+        return out

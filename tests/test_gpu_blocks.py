@@ -94,3 +94,20 @@ def test_level_ops(pair):
     got = blb.add_pt(g, ga, blb.from_numpy_u64(pt))
     want = O.add(ctx, oa, O.Ct(np.stack([pt, np.zeros_like(pt)]), oa.level, oa.scale))
     same(got, want)
+
+
+def test_batched_chains_bit_exact(pair):
+    """The lockstep (batched) chains the bench runs -- blb_mul_relin_batch over several independent
+    ciphertexts -- give every ciphertext the oracle's single-ciphertext bits."""
+    ctx, okeys, g, gkeys, _ = pair
+    rng = np.random.default_rng(100)
+    xs = [enc(pair, rng.uniform(-6, 0, ctx.n), 60 + t) for t in range(3)]
+    xb = [enc(pair, rng.uniform(0, 7, ctx.n), 70 + t) for t in range(3)]
+    ch = Chains(g, gkeys)
+    for got, (ox, _), (ob, _) in zip(ch.negexp_n([c for _, c in xs], [c for _, c in xb]), xs, xb):
+        same(got, OB.negexp(ctx, okeys, ox, ob))
+    gs = [enc(pair, rng.uniform(-2.7, 2.7, ctx.n), 80 + t) for t in range(3)]
+    for (f0, f1), (ox, _) in zip(ch.gelu_head_n([c for _, c in gs], bi.GELU_COEF), gs):
+        r0, r1 = OB.gelu_head(ctx, okeys, ox, bi.GELU_COEF)
+        same(f0, r0)
+        same(f1, r1)
