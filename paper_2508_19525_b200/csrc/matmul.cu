@@ -49,6 +49,9 @@ constexpr int kTB = 256;
 #ifndef BLB_MAC_MINB
 #define BLB_MAC_MINB 3
 #endif
+#ifndef BLB_MAC_P
+#define BLB_MAC_P 2   // outputs (b', g) per CTA sharing each staged R tile (compile-time A/B: 2 or 4)
+#endif
 
 // Build the slot vectors of entries [e0, e0 + cnt) (plan order) into slots[cnt][n].
 struct PlanDev {
@@ -935,10 +938,10 @@ static blb_status mm_acc(const blb_matmul_plan *pl, const blb_keys *keys, const 
         // list (possible in a window) yields a zero accumulator.
         bool grouped = true;
         for (int j = 0; j < n_o && grouped; j++)
-            if (j % 2 != 1 && j + 1 < n_o && !pl->same_next[o0 + j]) grouped = false;
+            if (j % BLB_MAC_P != BLB_MAC_P - 1 && j + 1 < n_o && !pl->same_next[o0 + j]) grouped = false;
         if (grouped)
-            launch_mac4<2, BLB_MAC_STG, BLB_MAC_MINB>(ptb, R, acc, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k,
-                                                      P->logN, P->pr, n_tiles, lay, st);
+            launch_mac4<BLB_MAC_P, BLB_MAC_STG, BLB_MAC_MINB>(ptb, R, acc, pl->d_ent, pl->d_ent_start, o0, e_base,
+                                                              n_o, k, P->logN, P->pr, n_tiles, lay, st);
         else
             launch_mac4<1, 4, 3>(ptb, R, acc, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN, P->pr,
                                  n_tiles, lay, st);
