@@ -241,6 +241,20 @@ blb_status blb_ckks_to_mpc(const blb_params *params, const blb_ct *in, int n_ct,
                            uint64_t first_ct_id, uint64_t *masked, uint64_t *share, void *ws, size_t ws_bytes,
                            void *stream);
 
+/* Optional re-randomisation before the mask (S13; the paper is silent on circuit privacy: Alg. 1
+ * sends (c0 + r, c1), while the proof simulates P0's view as a fresh encryption, P:1031;
+ * reading C22).  Each input is dropped to q_0 and a fresh public-key encryption of zero is added:
+ * (c0 + v b + e0, c1 + v a + e1) mod q_0 with pk = (b, a) the client's encryption of zero (blb_encrypt
+ * of 0 at the top level, id 2^55), v ternary (ChaCha tag 7), e1 centred binomial (tag 9) and e0 the
+ * flooding noise (tag 8): uniform in [-2^f, 2^f) from the low f+1 bits of each draw (f = flood_bits
+ * in [1, 58]) or centred binomial for f = 0; every draw keyed by rr_seed and the conversion's id
+ * first_ct_id + t; then exactly the mask of blb_ckks_to_mpc.  ws >= n_ct * 5 N * 8 bytes
+ * (blb_ckks_to_mpc_rr_workspace_bytes).  Errors as blb_ckks_to_mpc, BLB_E_INVALID_ARG for f > 58. */
+size_t blb_ckks_to_mpc_rr_workspace_bytes(const blb_params *params, int n_ct);
+blb_status blb_ckks_to_mpc_rr(const blb_params *params, const blb_ct *pk, const blb_ct *in, int n_ct,
+                              const uint8_t mask_key[32], const uint8_t rr_seed[32], uint64_t first_ct_id, int flood_bits,
+                              uint64_t *masked, uint64_t *share, void *ws, size_t ws_bytes, void *stream);
+
 /* Row f3, MPC -> CKKS ingest (Algorithm 2; ring-to-field, App. C.3).
  * blb_share_to_rns: a secret share x over Z_{2^w} (device u64 [N], values < 2^w, 1 <= w <= 64,
  * coefficient order) mapped to the field per limb i <= level: x mod q_i (P0's share, sub = 0)

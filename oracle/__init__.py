@@ -29,6 +29,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 
 TAG_SECRET, TAG_KEY_A, TAG_KEY_E, TAG_ENC_A, TAG_ENC_E, TAG_MASK = 1, 2, 3, 4, 5, 6
+TAG_RR_V, TAG_RR_E0, TAG_RR_E1 = 7, 8, 9     # S13 re-randomisation draws (reading C22)
+PK_ID = 1 << 55                               # ciphertext id of the public key (an encryption of zero)
 
 
 def build(force: bool = False) -> str:
@@ -487,6 +489,44 @@ def mask(ctx: Ctx, ct: Ct, mask_key: bytes, ct_id: int):
     share = np.empty(ctx.N, dtype=np.uint64)
     lib().orc_mask(ctx._h, _p(_u64(ct.data)), ct.level, mask_key, ct_id, _p(masked), _p(share))
     return masked, share
+
+
+# ---------------------------------------------------------------------------
+# S13: optional re-randomisation before the mask (reading C22)
+# ---------------------------------------------------------------------------
+def public_key(ctx: Ctx, key: bytes, s_ntt: np.ndarray) -> Ct:
+    """The client's public key: a symmetric encryption of zero (C6) at the top level, id PK_ID:
+    (b, a) = (-a s + e, a)."""
+    zero = np.zeros((ctx.K, ctx.N), dtype=np.uint64)
+    return encrypt(ctx, key, s_ntt, zero, ctx.K - 1, PK_ID, 1.0)
+
+
+def flood_draws(key: bytes, objid: int, N: int, flood_bits: int) -> np.ndarray:
+    """e0: uniform integers in [-2^f, 2^f) from the low bits of the 128-bit draws (f >= 1), or the
+    centred binomial of C4 for f = 0 (plain re-randomisation)."""
+    if flood_bits == 0:
+        return sample_cbd(key, TAG_RR_E0, objid, N)
+    m = (1 << (flood_bits + 1)) - 1
+    return np.array([(draw128(key, TAG_RR_E0, objid, x) & m) - (1 << flood_bits) for x in range(N)], dtype=np.int64)
+
+
+def rerandomize(ctx: Ctx, ct: Ct, pk: Ct, rr_key: bytes, ct_id: int, flood_bits: int) -> Ct:
+    """S13 (paper silent, reading C22): drop to q_0, then add a fresh public-key encryption of zero
+    with flooding noise, (v b + e0, v a + e1) mod q_0, v ternary, e1 centred binomial, e0 flooding
+    (flood_draws); all draws keyed by the conversion's own id (ct_id << 8)."""
+    oid = ct_id << 8
+    c = Ct(ct.data[:, :1].copy(), 0, ct.scale)
+    q0 = ctx.mods[0]
+
+    def ntt0(v):
+        return ctx.ntt(np.array([int(x) % q0 for x in v], dtype=np.uint64)[None, :], [0])[0]
+
+    v = ntt0(sample_ternary(rr_key, TAG_RR_V, oid, ctx.N))
+    e0 = ntt0(flood_draws(rr_key, oid, ctx.N, flood_bits))
+    e1 = ntt0(sample_cbd(rr_key, TAG_RR_E1, oid, ctx.N))
+    vpk = mul_pt(ctx, Ct(pk.data[:, :1].copy(), 0, 1.0), v[None, :], 1.0)
+    z = add(ctx, vpk, Ct(np.stack([e0, e1])[:, None, :], 0, 1.0))
+    return Ct(add(ctx, c, Ct(z.data, 0, c.scale)).data, 0, ct.scale)
 
 
 # ---------------------------------------------------------------------------

@@ -86,6 +86,9 @@ def lib() -> ctypes.CDLL:
             "blb_drop_level": ([vp, vp, ctypes.c_int, vp, vp], ctypes.c_int),
             "blb_ckks_to_mpc": ([vp, vp, ctypes.c_int, ctypes.c_char_p, u64, vp, vp, vp, ctypes.c_size_t, vp],
                                 ctypes.c_int),
+            "blb_ckks_to_mpc_rr_workspace_bytes": ([vp, ctypes.c_int], ctypes.c_size_t),
+            "blb_ckks_to_mpc_rr": ([vp, vp, vp, ctypes.c_int, ctypes.c_char_p, ctypes.c_char_p, u64, ctypes.c_int, vp, vp,
+                                    vp, ctypes.c_size_t, vp], ctypes.c_int),
             "blb_mhp_column_map": ([ctypes.c_int] * 4 + [vp, ip], ctypes.c_int),
             "blb_share_to_rns": ([vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp], ctypes.c_int),
             "blb_mpc_to_ckks": ([vp, vp, vp, ctypes.c_int, vp, ctypes.c_size_t, vp], ctypes.c_int),
@@ -418,6 +421,31 @@ def ckks_to_mpc(params: Params, cts: list, mask_key: bytes, first_ct_id: int):
     share = params.empty(n, params.N)
     _check(lib().blb_ckks_to_mpc(params.handle, arr, n, mask_key, first_ct_id, _ptr(masked), _ptr(share), None, 0,
                                  _stream()))
+    return masked, share
+
+
+PK_ID = 1 << 55
+
+
+def public_key(params: Params, secret: torch.Tensor, seed: bytes) -> Ciphertext:
+    """The client's public key for S13: an encryption of zero at the top level, ciphertext id 2^55."""
+    zero = params.empty(params.K, params.N).zero_()
+    return encrypt(params, secret, zero, params.K - 1, seed, PK_ID, 1.0)
+
+
+def ckks_to_mpc_rr(params: Params, pk: Ciphertext, cts: list, mask_key: bytes, rr_seed: bytes, first_ct_id: int,
+                   flood_bits: int = 0):
+    """S13 (reading C22): re-randomise with a fresh public-key encryption of zero (flooding noise of
+    flood_bits), then the mask of Alg. 1.  Returns (masked int64 [n][2][N], share int64 [n][N])."""
+    n = len(cts)
+    arr = (_Ct * max(1, n))(*[c.c() for c in cts])
+    masked = params.empty(n, 2, params.N)
+    share = params.empty(n, params.N)
+    nb = int(lib().blb_ckks_to_mpc_rr_workspace_bytes(params.handle, n))
+    ws = torch.empty(max(1, nb // 8), dtype=torch.int64, device="cuda")
+    pc = pk.c()
+    _check(lib().blb_ckks_to_mpc_rr(params.handle, ctypes.byref(pc), arr, n, mask_key, rr_seed, first_ct_id,
+                                    int(flood_bits), _ptr(masked), _ptr(share), _ptr(ws), ws.numel() * 8, _stream()))
     return masked, share
 
 

@@ -725,6 +725,47 @@ extern "C" blb_status blb_drop_level(const blb_params *P, const blb_ct *in, int 
     return BLB_OK;
 }
 
+blb_status blb_launch_rerand(const blb_params *P, u64 *const *rr, int n, const u64 *pk, int kpk, const uint8_t seed[32],
+                             u64 id0, int flood_bits, u64 *vee, cudaStream_t st);
+
+// S13 (reading C22): CKKS->MPC with re-randomisation -- each input dropped to q_0, plus a fresh
+// public-key encryption of zero with flooding noise, then the mask of blb_ckks_to_mpc
+extern "C" size_t blb_ckks_to_mpc_rr_workspace_bytes(const blb_params *P, int n_ct) {
+    return P && n_ct > 0 ? sizeof(u64) * (size_t)n_ct * 5 * P->N : 0;
+}
+extern "C" blb_status blb_ckks_to_mpc_rr(const blb_params *P, const blb_ct *pk, const blb_ct *in, int n_ct,
+                                         const uint8_t mask_key[32], const uint8_t rr_seed[32], uint64_t first_ct_id,
+                                         int flood_bits, uint64_t *masked, uint64_t *share, void *ws, size_t ws_bytes,
+                                         void *stream) {
+    if (!P || n_ct < 0) return BLB_E_INVALID_ARG;
+    if (n_ct == 0) return BLB_OK;
+    if (!pk || !pk->data || !in || !mask_key || !rr_seed || !masked || !share || !ws) return BLB_E_INVALID_ARG;
+    if (flood_bits < 0 || flood_bits > 58) {
+        blb_set_error("blb_ckks_to_mpc_rr: flood_bits must be in [0, 58]");
+        return BLB_E_INVALID_ARG;
+    }
+    if ((first_ct_id + (u64)n_ct) >> 56) {
+        blb_set_error("blb_ckks_to_mpc_rr: ct ids must be < 2^56");
+        return BLB_E_INVALID_ARG;
+    }
+    if (ws_bytes < blb_ckks_to_mpc_rr_workspace_bytes(P, n_ct)) return BLB_E_NOMEM;
+    const int N = P->N;
+    cudaStream_t st = (cudaStream_t)stream;
+    u64 *rrb = (u64 *)ws, *vee = rrb + (size_t)n_ct * 2 * N;
+    std::vector<u64 *> rr(n_ct);
+    std::vector<const u64 *> rrc(n_ct);
+    for (int t = 0; t < n_ct; t++) {
+        if (!in[t].data || in[t].level < 0) return BLB_E_INVALID_ARG;
+        rr[t] = rrb + (size_t)t * 2 * N;
+        rrc[t] = rr[t];
+        const size_t kN = (size_t)(in[t].level + 1) * N;
+        BLB_CUDA_TRY(cudaMemcpyAsync(rr[t], in[t].data, sizeof(u64) * N, cudaMemcpyDeviceToDevice, st));
+        BLB_CUDA_TRY(cudaMemcpyAsync(rr[t] + N, in[t].data + kN, sizeof(u64) * N, cudaMemcpyDeviceToDevice, st));
+    }
+    BLB_TRY(blb_launch_rerand(P, rr.data(), n_ct, pk->data, pk->level + 1, rr_seed, first_ct_id, flood_bits, vee, st));
+    return blb_launch_mask(P, rrc.data(), n_ct, 0, mask_key, first_ct_id, masked, share, st);
+}
+
 extern "C" blb_status blb_sub(const blb_params *P, const blb_ct *a, const blb_ct *b, blb_ct *out, void *stream) {
     if (!P || !a || !b || !out || !a->data || !b->data || !out->data) return BLB_E_INVALID_ARG;
     if (a->level != b->level) {

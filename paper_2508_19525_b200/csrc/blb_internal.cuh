@@ -481,7 +481,8 @@ blb_status launch_mac(const blb_params *P, const u64 *pt, const u64 *R, u64 *acc
                       int kq = -1, int jg = 1);
 
 // ChaCha / sampling
-enum { TAG_SECRET = 1, TAG_KEY_A = 2, TAG_KEY_E = 3, TAG_ENC_A = 4, TAG_ENC_E = 5, TAG_MASK = 6 };
+enum { TAG_SECRET = 1, TAG_KEY_A = 2, TAG_KEY_E = 3, TAG_ENC_A = 4, TAG_ENC_E = 5, TAG_MASK = 6,
+       TAG_RR_V = 7, TAG_RR_E0 = 8, TAG_RR_E1 = 9 };  // 7-9: S13 re-randomisation draws (reading C22)
 struct ChachaKey {
     uint32_t k[8];
 };

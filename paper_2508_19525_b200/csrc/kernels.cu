@@ -161,6 +161,35 @@ struct PtrList {
     const u64 *p[kMaxJobs];
 };
 
+// S13 flooding noise (reading C22): e0[x] = (lo64(draw x) mod 2^(f+1)) - 2^f as a residue mod q_0,
+// rows t of n_ct conversions (object id (id0 + t) << 8), coefficient domain
+__global__ void k_sample_flood(u64 *out, Primes pr, ChachaKey key, u64 id0, int flood_bits, int N) {
+    const int blk = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.y;
+    if (blk >= N / 4) return;
+    u64 lo[4], hi[4];
+    draw_block(key, TAG_RR_E0, (id0 + (u64)t) << 8, blk, lo, hi);
+    const u64 q = pr.m[0].q, m = (2ull << flood_bits) - 1, h = 1ull << flood_bits;
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        const u64 u = lo[d] & m;
+        out[(long long)t * N + 4 * blk + d] = u >= h ? u - h : q - (h - u);
+    }
+}
+// c0 += v b0 + e0, c1 += v a0 + e1 (mod q_0, NTT): rows [t][3][N] = (v, e0, e1); pk [2][kpk][N]
+__global__ void k_rr_combine(PtrList cts, const u64 *vee, const u64 *pk, long long kpkN, Primes pr, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.y;
+    if (x >= N) return;
+    const ModConst &mc = pr.m[0];
+    u64 *c = const_cast<u64 *>(cts.p[t]);
+    const u64 v = vee[((long long)t * 3 + 0) * N + x], e0 = vee[((long long)t * 3 + 1) * N + x],
+              e1 = vee[((long long)t * 3 + 2) * N + x];
+    c[x] = addmod(addmod(c[x], mulmod(v, pk[x], mc), mc.q), e0, mc.q);
+    c[N + x] = addmod(addmod(c[N + x], mulmod(v, pk[kpkN + x], mc), mc.q), e1, mc.q);
+}
+
+
 // coef[t][i][x] = c1[t][i][x] for i < k (copy before the INTT)
 __global__ void k_gather_rows(PtrList src, u64 *dst, int k, int N) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1074,6 +1103,45 @@ blb_status blb_launch_sub(const blb_params *P, const u64 *a, const u64 *b, u64 *
                           cudaStream_t st) {
     k_sub<<<grid_x(P->N, k, npoly), kTB, 0, st>>>(a, b, out, P->pr, k, P->N);
     BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+// S13 re-randomisation of n level-0 ciphertexts rr[t] ([2][N], NTT, modified in place) with the public
+// key pk ([2][kpk][N]); vee: scratch [n][3][N]
+blb_status blb_launch_rerand(const blb_params *P, u64 *const *rr, int n, const u64 *pk, int kpk, const uint8_t seed[32],
+                             u64 id0, int flood_bits, u64 *vee, cudaStream_t st) {
+    const int N = P->N;
+    const ChachaKey key = chacha_key_from_bytes(seed);
+    LimbList ll{};
+    ll.n = 1;
+    ll.prime[0] = 0;
+    for (int t = 0; t < n; t++) {
+        u64 *r = vee + (size_t)t * 3 * N;
+        k_sample_small<<<(N / 4 + kTB - 1) / kTB, kTB, 0, st>>>(r, N, ll, P->pr, key, TAG_RR_V, id0 + t, 0, N);
+        k_sample_small<<<(N / 4 + kTB - 1) / kTB, kTB, 0, st>>>(r + 2 * (size_t)N, N, ll, P->pr, key, TAG_RR_E1, id0 + t, 1, N);
+        if (flood_bits == 0)
+            k_sample_small<<<(N / 4 + kTB - 1) / kTB, kTB, 0, st>>>(r + N, N, ll, P->pr, key, TAG_RR_E0, id0 + t, 1, N);
+        BLB_COUNT_LAUNCH(flood_bits == 0 ? 3 : 2);
+    }
+    if (flood_bits > 0) {
+        // e0 rows of all conversions: row t of a [n][N] view with stride 3N -> write per conversion
+        for (int t = 0; t < n; t++) {
+            k_sample_flood<<<dim3((N / 4 + kTB - 1) / kTB, 1), kTB, 0, st>>>(vee + ((size_t)t * 3 + 1) * N, P->pr, key,
+                                                                            id0 + t, flood_bits, N);
+            BLB_COUNT_LAUNCH(1);
+        }
+    }
+    BLB_CHECK_LAUNCH();
+    RowBatch rb{};
+    rb.base = vee; rb.poly_stride = N; rb.n_polys = 3 * n; rb.limbs = 1; rb.limb0 = 0; rb.prime[0] = 0;
+    BLB_TRY(launch_ntt(P, rb, false, st));
+    for (int t0 = 0; t0 < n; t0 += kMaxJobs) {
+        const int cnt = std::min(kMaxJobs, n - t0);
+        PtrList pl{};
+        for (int t = 0; t < cnt; t++) pl.p[t] = rr[t0 + t];
+        k_rr_combine<<<grid_x(N, cnt), kTB, 0, st>>>(pl, vee + (size_t)t0 * 3 * N, pk, (long long)kpk * N, P->pr, N);
+        BLB_COUNT_LAUNCH(1);
+    }
     BLB_CHECK_LAUNCH();
     return BLB_OK;
 }

@@ -600,3 +600,30 @@ def test_batched_inputs_bit_exact(toy):
     Y = packing.spatial_unslots(dec, Bt * L, Dout)
     for b in range(Bt):
         assert np.abs(Y[b * L:(b + 1) * L] - Xs[b] @ W).max() < 1e-5
+
+
+# ---------------------------------------------------------------- S13 re-randomisation (C22)
+@pytest.mark.parametrize("name,flood", [("toy", 0), ("toy", 20), ("bert", 30)])
+def test_ckks_to_mpc_rerandomised_bit_exact(name, flood, request):
+    """Optional re-randomisation before the mask: the public key, the re-randomised masked
+    ciphertexts and the server shares are bit-exact against the oracle (two conversions, so the
+    per-conversion ids are exercised)."""
+    pair = request.getfixturevalue(name)
+    okeys = O.keygen(pair.o, bi.crypto_key(4, 62))
+    gkeys, sk = blb.keygen(pair.g, bi.crypto_key(4, 62), [])
+    lvl = min(2, pair.K - 1)
+    rng = np.random.default_rng(63)
+    octs, gcts = [], []
+    for t in range(2):
+        pt = O.encode(pair.o, rng.uniform(-1, 1, pair.n), 2.0 ** 40, lvl)
+        octs.append(O.encrypt(pair.o, bi.crypto_key(5, 62), okeys.s_ntt, pt, lvl, 20 + t, 2.0 ** 40))
+        gcts.append(blb.encrypt(pair.g, sk, dev(pt), lvl, bi.crypto_key(5, 62), 20 + t, 2.0 ** 40))
+    opk = O.public_key(pair.o, bi.crypto_key(5, 62), okeys.s_ntt)
+    gpk = blb.public_key(pair.g, sk, bi.crypto_key(5, 62))
+    assert np.array_equal(u64(gpk.data), opk.data)
+    mk, rk = bi.crypto_key(3, 62), bi.crypto_key(6, 62)
+    m, s = blb.ckks_to_mpc_rr(pair.g, gpk, gcts, mk, rk, 500, flood)
+    for t in range(2):
+        rr = O.rerandomize(pair.o, octs[t], opk, rk, 500 + t, flood)
+        om, osh = O.mask(pair.o, rr, mk, 500 + t)
+        assert np.array_equal(u64(m[t]), om) and np.array_equal(u64(s[t]), osh)
