@@ -50,7 +50,10 @@ constexpr int kTB = 256;
 #define BLB_MAC_MINB 3
 #endif
 #ifndef BLB_MAC_P
-#define BLB_MAC_P 2   // outputs (b', g) per CTA sharing each staged R tile (compile-time A/B: 2 or 4)
+#define BLB_MAC_P 2   // outputs (b', g) per CTA sharing each staged R tile (4 measured slower)
+#endif
+#ifndef BLB_MAC_STGP
+#define BLB_MAC_STGP 5   // ring stages for the width-packed (5-byte) limbs
 #endif
 
 // Build the slot vectors of entries [e0, e0 + cnt) (plan order) into slots[cnt][n].
@@ -173,27 +176,39 @@ struct PtLayout {
     long long loff[BLB_MAXP];  // sum_{l' < l} w_l' * N (times n_e: the limb offset inside an output block)
     long long bpp;           // bytes per plaintext = sum_l w_l N
 };
-template <int PP, int STG>
-constexpr size_t mac4_smem() { return (size_t)STG * (PP + 2) * 512 * 8 + 2 * STG * 8; }
+// Ring geometry: a stage holds PP plaintext tiles (512 * w bytes each) + the two R tiles (4096 bytes
+// each).  Packed limbs (w = 5) run STGP stages, 8-byte limbs STG stages, in the same shared memory
+// (the packed stages are smaller, so the deeper ring keeps more plaintext bytes in flight).
+template <int PP>
+__host__ __device__ constexpr unsigned mac4_stage_bytes(int w) { return (unsigned)(PP * 512 * w + 2 * 4096); }
+template <int PP, int STG, int STGP>
+__host__ __device__ constexpr size_t mac4_ring_bytes() {
+    return (size_t)(STG * mac4_stage_bytes<PP>(8) > STGP * mac4_stage_bytes<PP>(5) ? STG * mac4_stage_bytes<PP>(8)
+                                                                                    : STGP * mac4_stage_bytes<PP>(5));
+}
+template <int PP, int STG, int STGP>
+constexpr size_t mac4_smem() { return mac4_ring_bytes<PP, STG, STGP>() + 2 * (STG > STGP ? STG : STGP) * 8; }
 
 // SPLIT41 (q < 2^41): every product on the grid-split FP64 accumulator (AccG, FP64 pipe, one
 // reduction per output); otherwise (60-bit limbs) Acc128 on the integer pipe, folded every 64.
-template <bool SPLIT41, bool PACKED, int kMacP, int kM4Stages>
-__device__ __forceinline__ void mac4_consume(const u64 *ring, uint64_t *full, uint64_t *empty, int n_e, int nP,
-                                             u64 *const *outs, long long kN, const ModConst &mc) {
+template <bool SPLIT41, bool PACKED, int kMacP>
+__device__ __forceinline__ void mac4_consume(const unsigned char *ring, uint64_t *full, uint64_t *empty, int n_e, int nP,
+                                             u64 *const *outs, long long kN, const ModConst &mc, int nst,
+                                             unsigned stage_bytes, unsigned tb) {
     using A = typename std::conditional<SPLIT41, AccG, Acc128>::type;
     const double qd = (double)mc.q, qinv = 1.0 / qd;
     A a00[kMacP], a01[kMacP], a10[kMacP], a11[kMacP];
 #pragma unroll
     for (int j = 0; j < kMacP; j++) { a00[j].zero(); a01[j].zero(); a10[j].zero(); a11[j].zero(); }
-    constexpr int kM4StageWords = (kMacP + 2) * 512;
     const int t = threadIdx.x;
+    int slot = 0;
+    unsigned phase = 0;
     for (int s = 0; s < n_e; s++) {
-        const int slot = s % kM4Stages;
-        mbar_wait(&full[slot], (s / kM4Stages) & 1);
-        const u64 *st = ring + (size_t)slot * kM4StageWords;
-        const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + kMacP * 512 + 2 * t);
-        const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + (kMacP + 1) * 512 + 2 * t);
+        mbar_wait(&full[slot], phase);
+        const unsigned char *stb = ring + (size_t)slot * stage_bytes;
+        const u64 *rt = reinterpret_cast<const u64 *>(stb + kMacP * tb);
+        const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(rt + 2 * t);
+        const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(rt + 512 + 2 * t);
         if constexpr (SPLIT41) {
             // convert each staged residue to a double once (R values are shared by the kMacP
             // outputs, plaintext values by c0 and c1)
@@ -204,13 +219,12 @@ __device__ __forceinline__ void mac4_consume(const u64 *ring, uint64_t *full, ui
                 {  // unconditional (slot j >= nP holds stale data, its sums are never stored): no joins
                     double Px, Py;
                     if constexpr (PACKED) {  // high byte spliced under the 2^52 exponent with one PRMT
-                        const uint2 lo = *reinterpret_cast<const uint2 *>(reinterpret_cast<const uint32_t *>(st + j * 512) + 2 * t);
-                        const unsigned hi = *(reinterpret_cast<const unsigned short *>(
-                                                  reinterpret_cast<const unsigned char *>(st + j * 512) + 2048) + t);
+                        const uint2 lo = *reinterpret_cast<const uint2 *>(reinterpret_cast<const uint32_t *>(stb + j * tb) + 2 * t);
+                        const unsigned hi = *(reinterpret_cast<const unsigned short *>(stb + j * tb + 2048) + t);
                         Px = __dsub_rn(__hiloint2double((int)__byte_perm(hi, 0x43300000u, 0x7650), (int)lo.x), 4503599627370496.0);
                         Py = __dsub_rn(__hiloint2double((int)__byte_perm(hi, 0x43300000u, 0x7651), (int)lo.y), 4503599627370496.0);
                     } else {
-                        const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(st + j * 512 + 2 * t);
+                        const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(stb + j * tb + 16 * t);
                         Px = AccF64::u2d(pv.x);
                         Py = AccF64::u2d(pv.y);
                     }
@@ -222,7 +236,7 @@ __device__ __forceinline__ void mac4_consume(const u64 *ring, uint64_t *full, ui
 #pragma unroll
             for (int j = 0; j < kMacP; j++) {
                 if (j < nP) {
-                    const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(st + j * 512 + 2 * t);
+                    const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(stb + j * tb + 16 * t);
                     a00[j].mac(pv.x, r0.x); a01[j].mac(pv.y, r0.y);
                     a10[j].mac(pv.x, r1.x); a11[j].mac(pv.y, r1.y);
                 }
@@ -230,6 +244,7 @@ __device__ __forceinline__ void mac4_consume(const u64 *ring, uint64_t *full, ui
         }
         __syncwarp();
         if ((t & 31) == 0) mbar_arrive(&empty[slot]);
+        if (++slot == nst) { slot = 0; phase ^= 1u; }
         // Acc128: fold every 64 products (< 2^126); AccG: every 512 (s < 2^93, l < 2^48)
         if ((!SPLIT41 && (s & 63) == 63) || (SPLIT41 && (s & 511) == 511)) {
 #pragma unroll
@@ -250,16 +265,16 @@ __device__ __forceinline__ void mac4_consume(const u64 *ring, uint64_t *full, ui
     }
 }
 
-template <int kMacP, int kM4Stages, int MINB>
+template <int kMacP, int kM4Stages, int MINB, int kM4StagesP = kM4Stages>
 __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char *__restrict__ pt, const u64 *__restrict__ R,
                                                        u64 *__restrict__ acc, const int *__restrict__ ent_r,
                                                        const int *__restrict__ ent_start, int o0, int e_base, int n_o,
                                                        int k, int logN, Primes pr, PtLayout lay) {
-    constexpr int kM4StageWords = (kMacP + 2) * 512;
+    constexpr int kMaxStg = kM4Stages > kM4StagesP ? kM4Stages : kM4StagesP;
     extern __shared__ __align__(128) unsigned char smraw[];
-    u64 *ring = reinterpret_cast<u64 *>(smraw);
-    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)kM4Stages * kM4StageWords);
-    uint64_t *empty = full + kM4Stages;
+    unsigned char *ring = smraw;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smraw + mac4_ring_bytes<kMacP, kM4Stages, kM4StagesP>());
+    uint64_t *empty = full + kMaxStg;
     const int N = 1 << logN;
     const int n_tiles = N / (2 * kTB);
     const int n_grp = (n_o + kMacP - 1) / kMacP;
@@ -274,8 +289,10 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char
     const long long lx0 = (long long)l * N + tile * 2 * kTB;
     const int w = lay.w[l];
     const unsigned tb = 512u * (unsigned)w;  // bytes of one plaintext tile of this limb
+    const int nst = w == 5 ? kM4StagesP : kM4Stages;
+    const unsigned stage_bytes = (unsigned)kMacP * tb + 2u * 4096u;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kM4Stages; s++) {
+        for (int s = 0; s < nst; s++) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kTB / 32);
         }
@@ -289,15 +306,20 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char
             for (int j = 0; j < kMacP; j++)
                 pp[j] = pt + (long long)(ent_start[o0 + oa + (j < nP ? j : 0)] - e_base) * lay.bpp +
                         (long long)n_e * lay.loff[l] + (long long)tile * n_e * tb;
+            int slot = 0;
+            unsigned phase = 0;  // parity of the empty-barrier round being waited for
             for (int s = 0; s < n_e; s++) {
-                const int slot = s % kM4Stages;
-                if (s >= kM4Stages) mbar_wait(&empty[slot], ((s / kM4Stages) - 1) & 1);
-                u64 *st = ring + (size_t)slot * kM4StageWords;
+                if (s >= nst) mbar_wait(&empty[slot], phase);
+                unsigned char *stb = ring + (size_t)slot * stage_bytes;
                 mbar_expect_tx(&full[slot], (unsigned)nP * tb + 2u * 4096u);
-                for (int j = 0; j < nP; j++) bulk_g2s(st + j * 512, pp[j] + (long long)s * tb, tb, &full[slot]);
+                for (int j = 0; j < nP; j++) bulk_g2s(stb + j * tb, pp[j] + (long long)s * tb, tb, &full[slot]);
                 const int bi = ent_r[e_lo + s];
-                bulk_g2s(st + kMacP * 512, R + (long long)bi * 2 * kN + lx0, 4096, &full[slot]);
-                bulk_g2s(st + (kMacP + 1) * 512, R + ((long long)bi * 2 + 1) * kN + lx0, 4096, &full[slot]);
+                bulk_g2s(stb + kMacP * tb, R + (long long)bi * 2 * kN + lx0, 4096, &full[slot]);
+                bulk_g2s(stb + kMacP * tb + 4096, R + ((long long)bi * 2 + 1) * kN + lx0, 4096, &full[slot]);
+                if (++slot == nst) {
+                    slot = 0;
+                    if (s >= nst) phase ^= 1u;
+                }
             }
         }
         return;
@@ -306,20 +328,21 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char
 #pragma unroll
     for (int j = 0; j < kMacP; j++) outs[j] = acc + (long long)(oa + (j < nP ? j : 0)) * 2 * kN + lx0;
     const ModConst &mc = pr.m[l];
-    if (w == 5) mac4_consume<true, true, kMacP, kM4Stages>(ring, full, empty, n_e, nP, outs, kN, mc);
-    else if (mc.q < (1ull << 41)) mac4_consume<true, false, kMacP, kM4Stages>(ring, full, empty, n_e, nP, outs, kN, mc);
-    else mac4_consume<false, false, kMacP, kM4Stages>(ring, full, empty, n_e, nP, outs, kN, mc);
+    if (w == 5) mac4_consume<true, true, kMacP>(ring, full, empty, n_e, nP, outs, kN, mc, nst, stage_bytes, tb);
+    else if (mc.q < (1ull << 41))
+        mac4_consume<true, false, kMacP>(ring, full, empty, n_e, nP, outs, kN, mc, nst, stage_bytes, tb);
+    else mac4_consume<false, false, kMacP>(ring, full, empty, n_e, nP, outs, kN, mc, nst, stage_bytes, tb);
 }
 
-template <int PP, int STG, int MINB>
+template <int PP, int STG, int MINB, int STGP = STG>
 static void launch_mac4(const unsigned char *pt, const u64 *R, u64 *acc, const int *ent_r, const int *ent_start, int o0,
                         int e_base, int n_o, int k, int logN, const Primes &pr, int n_tiles, const PtLayout &lay,
                         cudaStream_t st) {
-    constexpr size_t smem = mac4_smem<PP, STG>();
-    blb_smem_optin(k_mac_tma4<PP, STG, MINB>, smem);
+    constexpr size_t smem = mac4_smem<PP, STG, STGP>();
+    blb_smem_optin(k_mac_tma4<PP, STG, MINB, STGP>, smem);
     const size_t n_grp = (size_t)(n_o + PP - 1) / PP;
-    k_mac_tma4<PP, STG, MINB><<<(unsigned)(n_grp * n_tiles * k), kTB + 32, smem, st>>>(pt, R, acc, ent_r, ent_start, o0,
-                                                                                e_base, n_o, k, logN, pr, lay);
+    k_mac_tma4<PP, STG, MINB, STGP><<<(unsigned)(n_grp * n_tiles * k), kTB + 32, smem, st>>>(pt, R, acc, ent_r, ent_start,
+                                                                                      o0, e_base, n_o, k, logN, pr, lay);
 }
 
 // scatter standard [cnt][k][N] plaintexts (entries e0..e0+cnt of the plan) into the blocked, width-packed layout
@@ -940,8 +963,9 @@ static blb_status mm_acc(const blb_matmul_plan *pl, const blb_keys *keys, const 
         for (int j = 0; j < n_o && grouped; j++)
             if (j % BLB_MAC_P != BLB_MAC_P - 1 && j + 1 < n_o && !pl->same_next[o0 + j]) grouped = false;
         if (grouped)
-            launch_mac4<BLB_MAC_P, BLB_MAC_STG, BLB_MAC_MINB>(ptb, R, acc, pl->d_ent, pl->d_ent_start, o0, e_base,
-                                                              n_o, k, P->logN, P->pr, n_tiles, lay, st);
+            launch_mac4<BLB_MAC_P, BLB_MAC_STG, BLB_MAC_MINB, BLB_MAC_STGP>(ptb, R, acc, pl->d_ent, pl->d_ent_start, o0,
+                                                                            e_base, n_o, k, P->logN, P->pr, n_tiles,
+                                                                            lay, st);
         else
             launch_mac4<1, 4, 3>(ptb, R, acc, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN, P->pr,
                                  n_tiles, lay, st);
