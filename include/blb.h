@@ -404,6 +404,15 @@ size_t blb_mul_relin_batch_workspace_bytes(const blb_params *params, int level, 
 blb_status blb_mul_relin_batch(const blb_params *params, const blb_keys *keys, const blb_ct *a, const blb_ct *b, int n,
                                int rescale, blb_ct *out, void *ws, size_t ws_bytes, void *stream);
 
+/* Batched ewmul_cp + rescale: out[t] = rescale(in[t] (x) pt[t]) for t < n (pt[t]: device
+ * [level+1][N] NTT plaintexts, host array of pointers; pt_scale[t] their scales, host), all inputs at
+ * one level >= 1 -- the per-ciphertext bits of blb_mul_pt + blb_rescale in one product launch and
+ * one rescale batch.  out[t] [2][level][N], scale (in.scale * pt_scale) / q_level.
+ * ws: blb_mul_pt_rescale_batch_workspace_bytes(level, n). */
+size_t blb_mul_pt_rescale_batch_workspace_bytes(const blb_params *params, int level, int n);
+blb_status blb_mul_pt_rescale_batch(const blb_params *params, const blb_ct *in, const uint64_t *const *pt,
+                                    const double *pt_scale, int n, blb_ct *out, void *ws, size_t ws_bytes, void *stream);
+
 /* Rotate-and-sum of BLB's summation operator (Table 3) on a
  * spatial-first ciphertext with L rows and D (power of two) columns:
  * m^0 = in, m^i = m^{i-1} + Rot_l^{2^{i-1} L}(m^{i-1}), out = m^{log2 D}: log2 D

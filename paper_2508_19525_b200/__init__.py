@@ -114,6 +114,8 @@ def lib() -> ctypes.CDLL:
             "blb_f2_workspace_bytes": ([vp, ctypes.c_int], ctypes.c_size_t),
             "blb_mul_relin": ([vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
             "blb_mul_relin_batch_workspace_bytes": ([vp, ctypes.c_int, ctypes.c_int], ctypes.c_size_t),
+            "blb_mul_pt_rescale_batch_workspace_bytes": ([vp, ctypes.c_int, ctypes.c_int], ctypes.c_size_t),
+            "blb_mul_pt_rescale_batch": ([vp, vp, vp, vp, ctypes.c_int, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
             "blb_mul_relin_batch": ([vp, vp, vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t, vp],
                                     ctypes.c_int),
             "blb_rotate_sum": ([vp, vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
@@ -519,6 +521,26 @@ def mul_relin_batch(params: Params, keys: Keys, a: list, b: list, rescale: bool 
     co = (_Ct * n)(*[o.c() for o in outs])
     _check(lib().blb_mul_relin_batch(params.handle, keys.handle, ca, cb, n, int(bool(rescale)), co, _ptr(ws),
                                      ws.numel() * 8, _stream()))
+    for o, c in zip(outs, co):
+        o.level, o.scale = c.level, c.scale
+    return outs
+
+
+def mul_pt_rescale_batch(params: Params, cts: list, pts: list, pt_scales: list, ws: torch.Tensor | None = None) -> list:
+    """n (ciphertext, plaintext) pairs: ct x pt then rescale, in batched launches (row f2)."""
+    n = len(cts)
+    if n == 0:
+        return []
+    lvl = cts[0].level
+    outs = [Ciphertext.empty(params, lvl - 1) for _ in range(n)]
+    nb = int(lib().blb_mul_pt_rescale_batch_workspace_bytes(params.handle, lvl, n))
+    if ws is None or ws.numel() * 8 < nb:
+        ws = torch.empty(nb // 8 + 1, dtype=torch.int64, device="cuda")
+    ci = (_Ct * n)(*[c.c() for c in cts])
+    co = (_Ct * n)(*[o.c() for o in outs])
+    pp = (ctypes.c_void_p * n)(*[p.data_ptr() for p in pts])
+    ps = (ctypes.c_double * n)(*[float(s) for s in pt_scales])
+    _check(lib().blb_mul_pt_rescale_batch(params.handle, ci, pp, ps, n, co, _ptr(ws), ws.numel() * 8, _stream()))
     for o, c in zip(outs, co):
         o.level, o.scale = c.level, c.scale
     return outs

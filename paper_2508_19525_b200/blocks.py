@@ -44,9 +44,21 @@ class Chains:
         return blb.add_pt(self.p, ct, self._encode(vec, ct.scale, ct.level))
 
     def mul_const(self, ct, vec, target: float | None = None):
-        q = float(self.p.moduli[ct.level])
-        s = q if target is None else q * target / ct.scale
-        return blb.rescale(self.p, blb.mul_pt(self.p, ct, self._encode(vec, s, ct.level), s))
+        return self.mul_consts([ct], [vec], None if target is None else [target])[0]
+
+    def mul_consts(self, cts: list, vecs: list, targets: list | None = None) -> list:
+        """ewmul_cp + rescale of several ciphertexts at one level in one batch."""
+        out = [None] * len(cts)
+        by_level = {}
+        for t, c in enumerate(cts):
+            by_level.setdefault(c.level, []).append(t)
+        for lvl, idx in by_level.items():
+            q = float(self.p.moduli[lvl])
+            sc = [q if targets is None else q * targets[t] / cts[t].scale for t in idx]
+            pts = [self._encode(vecs[t], s, lvl) for t, s in zip(idx, sc)]
+            for t, r in zip(idx, blb.mul_pt_rescale_batch(self.p, [cts[t] for t in idx], pts, sc)):
+                out[t] = r
+        return out
 
     def square(self, a):
         return self.squares([a])[0]
@@ -64,7 +76,8 @@ class Chains:
 
     # ---- the chains (lists of independent ciphertexts run in lockstep) ----
     def negexp_n(self, xs: list, xbars: list, t: int = 6) -> list:
-        ys = [self.add_const(self.mul_const(blb.sub(self.p, x, xb), 2.0 ** -t), 1.0) for x, xb in zip(xs, xbars)]
+        ds = [blb.sub(self.p, x, xb) for x, xb in zip(xs, xbars)]
+        ys = [self.add_const(y, 1.0) for y in self.mul_consts(ds, [2.0 ** -t] * len(ds))]
         for _ in range(t):
             ys = self.squares(ys)
         return ys
@@ -85,26 +98,28 @@ class Chains:
         return xmu, var
 
     def ln_tail(self, xmu: list, rs, gamma: list, beta: list) -> list:
-        ys = self.muls(xmu, [rs] * len(xmu))
-        return [self.add_const(self.mul_const(y, g), b) for y, g, b in zip(ys, gamma, beta)]
+        ys = self.mul_consts(self.muls(xmu, [rs] * len(xmu)), gamma)
+        return [self.add_const(y, b) for y, b in zip(ys, beta)]
 
     def gelu_head_n(self, xs: list, coef) -> list:
         a, b, c, d, e = coef
         x2 = self.squares(xs)
         x3 = self.muls(x2, xs)
         x4 = self.squares(x2)
+        n = len(xs)
+        s4 = [y.scale for y in x4]
+        ax4 = self.mul_consts(x4, [a] * n)
+        bx3 = self.mul_consts(x3, [b] * n, s4)
+        cx2 = self.mul_consts(x2, [c] * n, s4)
+        xm = self.mul_consts(xs, [0.5 - d] * n, s4)
+        xp = self.mul_consts(xs, [0.5 + d] * n, s4)
         out = []
-        for x, y2, y3, y4 in zip(xs, x2, x3, x4):
-            s4 = y4.scale
-            ax4 = self.mul_const(y4, a)
-            lv = ax4.level
-            bx3 = self.drop(self.mul_const(y3, b, s4), lv)
-            cx2 = self.drop(self.mul_const(y2, c, s4), lv)
-            xm = self.drop(self.mul_const(x, 0.5 - d, s4), lv)
-            xp = self.drop(self.mul_const(x, 0.5 + d, s4), lv)
-            base = blb.add(self.p, ax4, cx2)
-            f0 = self.add_const(blb.add(self.p, blb.sub(self.p, base, bx3), xm), e)
-            f1 = self.add_const(blb.add(self.p, blb.add(self.p, base, bx3), xp), e)
+        for t in range(n):
+            lv = ax4[t].level
+            base = blb.add(self.p, ax4[t], self.drop(cx2[t], lv))
+            bx3_t, xm_t, xp_t = self.drop(bx3[t], lv), self.drop(xm[t], lv), self.drop(xp[t], lv)
+            f0 = self.add_const(blb.add(self.p, blb.sub(self.p, base, bx3_t), xm_t), e)
+            f1 = self.add_const(blb.add(self.p, blb.add(self.p, base, bx3_t), xp_t), e)
             out.append((f0, f1))
         return out
 

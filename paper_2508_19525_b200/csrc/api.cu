@@ -38,6 +38,8 @@ blb_status blb_launch_add(const blb_params *P, const u64 *a, const u64 *b, u64 *
 blb_status blb_launch_tensor(const blb_params *P, const u64 *a, const u64 *b, u64 *d, int k, cudaStream_t st);
 blb_status blb_launch_tensor_n(const blb_params *P, const u64 *const *a, const u64 *const *b, int n, u64 *d, int k,
                                cudaStream_t st);
+blb_status blb_launch_mul_pt_n(const blb_params *P, const u64 *const *in, const u64 *const *pt, int n, u64 *out, int k,
+                               cudaStream_t st);
 blb_status blb_launch_mask(const blb_params *P, const u64 *const *in, int n, int level, const uint8_t key[32],
                            u64 id0, u64 *masked, u64 *share, cudaStream_t st);
 
@@ -989,6 +991,47 @@ extern "C" blb_status blb_mul_relin_batch(const blb_params *P, const blb_keys *K
             out[t0 + t].level = rescale ? level - 1 : level;
             out[t0 + t].scale = rescale ? (a[t0 + t].scale * b[t0 + t].scale) / (double)P->mod[level]
                                         : a[t0 + t].scale * b[t0 + t].scale;
+        }
+    }
+    return BLB_OK;
+}
+
+// Batched ewmul_cp + rescale: out[t] = rescale(in[t] (x) pt[t]) -- one product launch and one
+// rescale batch for n ciphertexts at one level (the per-ciphertext bits of blb_mul_pt + blb_rescale)
+extern "C" size_t blb_mul_pt_rescale_batch_workspace_bytes(const blb_params *P, int level, int n) {
+    if (!P || level < 1 || level >= P->K || n < 1) return 0;
+    const size_t m = std::min(n, kMaxJobs), k = level + 1, N = P->N;
+    return sizeof(u64) * (m * 2 * k * N + m * 2 * level * N + m * 2 * (1 + k) * N);
+}
+extern "C" blb_status blb_mul_pt_rescale_batch(const blb_params *P, const blb_ct *in, const uint64_t *const *pt,
+                                               const double *pt_scale, int n, blb_ct *out, void *ws, size_t ws_bytes,
+                                               void *stream) {
+    if (!P || n < 0 || (n > 0 && (!in || !pt || !pt_scale || !out || !ws))) return BLB_E_INVALID_ARG;
+    if (n == 0) return BLB_OK;
+    const int level = in[0].level;
+    for (int t = 0; t < n; t++) {
+        if (!in[t].data || !pt[t] || !out[t].data) return BLB_E_INVALID_ARG;
+        if (in[t].level != level) {
+            blb_set_error("blb_mul_pt_rescale_batch: all inputs must share one level");
+            return BLB_E_LEVEL;
+        }
+    }
+    if (level < 1 || level >= P->K) return BLB_E_LEVEL;
+    if (ws_bytes < blb_mul_pt_rescale_batch_workspace_bytes(P, level, n)) return BLB_E_NOMEM;
+    const int k = level + 1, N = P->N;
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int t0 = 0; t0 < n; t0 += kMaxJobs) {
+        const int m = std::min(kMaxJobs, n - t0);
+        u64 *prod = (u64 *)ws, *r = prod + (size_t)m * 2 * k * N, *resc = r + (size_t)m * 2 * level * N;
+        std::vector<const u64 *> pi(m), pp(m);
+        for (int t = 0; t < m; t++) { pi[t] = in[t0 + t].data; pp[t] = pt[t0 + t]; }
+        BLB_TRY(blb_launch_mul_pt_n(P, pi.data(), pp.data(), m, prod, k, st));
+        BLB_TRY(launch_rescale(P, prod, level, 2 * m, r, resc, st));
+        for (int t = 0; t < m; t++) {
+            BLB_CUDA_TRY(cudaMemcpyAsync(out[t0 + t].data, r + (size_t)t * 2 * level * N, sizeof(u64) * 2 * level * N,
+                                         cudaMemcpyDeviceToDevice, st));
+            out[t0 + t].level = level - 1;
+            out[t0 + t].scale = (in[t0 + t].scale * pt_scale[t0 + t]) / (double)P->mod[level];
         }
     }
     return BLB_OK;

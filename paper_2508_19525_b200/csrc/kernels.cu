@@ -588,6 +588,29 @@ __global__ void k_tensor_n(PtrList a, PtrList b, u64 *d, Primes pr, int k, int N
 inline dim3 grid_x(int N, int y = 1, int z = 1) { return dim3((N + kTB - 1) / kTB, y, z); }
 }  // namespace
 
+// n ct x pt products in one launch: out[t] = (c0 * pt[t], c1 * pt[t]) into [n][2][k][N]
+__global__ void k_mul_pt_n(PtrList in, PtrList pt, u64 *out, Primes pr, int k, int N) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y, t = blockIdx.z;
+    if (x >= N) return;
+    const ModConst &mc = pr.m[i];
+    const long long kN = (long long)k * N, lx = (long long)i * N + x;
+    const u64 p = pt.p[t][lx];
+    u64 *o = out + (long long)t * 2 * kN + lx;
+    o[0] = mulmod(in.p[t][lx], p, mc);
+    o[kN] = mulmod(in.p[t][kN + lx], p, mc);
+}
+blb_status blb_launch_mul_pt_n(const blb_params *P, const u64 *const *in, const u64 *const *pt, int n, u64 *out, int k,
+                               cudaStream_t st) {
+    if (n <= 0) return BLB_OK;
+    if (n > kMaxJobs) return BLB_E_INVALID_ARG;
+    PtrList a{}, b{};
+    for (int t = 0; t < n; t++) { a.p[t] = in[t]; b.p[t] = pt[t]; }
+    k_mul_pt_n<<<grid_x(P->N, k, n), kTB, 0, st>>>(a, b, out, P->pr, k, P->N);
+    BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
 blb_status blb_launch_tensor_n(const blb_params *P, const u64 *const *a, const u64 *const *b, int n, u64 *d, int k,
                                cudaStream_t st) {
     if (n <= 0) return BLB_OK;

@@ -53,7 +53,7 @@ constexpr int kTB = 256;
 #define BLB_MAC_P 2   // outputs (b', g) per CTA sharing each staged R tile (4 measured slower)
 #endif
 #ifndef BLB_MAC_STGP
-#define BLB_MAC_STGP 5   // ring stages for the width-packed (5-byte) limbs
+#define BLB_MAC_STGP 4   // ring stages for the width-packed limbs (5 measured equal: profiles/r2_mac_ring_depth_ab.log)
 #endif
 
 // Build the slot vectors of entries [e0, e0 + cnt) (plan order) into slots[cnt][n].
@@ -331,7 +331,20 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char
     if (w == 5) mac4_consume<true, true, kMacP>(ring, full, empty, n_e, nP, outs, kN, mc, nst, stage_bytes, tb);
     else if (mc.q < (1ull << 41))
         mac4_consume<true, false, kMacP>(ring, full, empty, n_e, nP, outs, kN, mc, nst, stage_bytes, tb);
-    else mac4_consume<false, false, kMacP>(ring, full, empty, n_e, nP, outs, kN, mc, nst, stage_bytes, tb);
+    else {
+#ifdef BLB_MAC_TIMING_SKIP60   // timing experiment only (wrong results): drain the 60-bit limb's ring
+        int slot = 0;
+        unsigned ph = 0;
+        for (int s = 0; s < n_e; s++) {
+            mbar_wait(&full[slot], ph);
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot]);
+            if (++slot == nst) { slot = 0; ph ^= 1u; }
+        }
+#else
+        mac4_consume<false, false, kMacP>(ring, full, empty, n_e, nP, outs, kN, mc, nst, stage_bytes, tb);
+#endif
+    }
 }
 
 template <int PP, int STG, int MINB, int STGP = STG>

@@ -27,8 +27,8 @@ case "$cmd" in
   sanitize)
     TAG=$1
     for tool in memcheck racecheck synccheck; do
-      timeout 900 compute-sanitizer --tool ${tool} --print-limit 20 python -c \
-        "import __graft_entry__ as g; g.smoke()" > gpurun_out/sanitize_${tool}_${TAG}.log 2>&1
+      timeout 1500 compute-sanitizer --tool ${tool} --print-limit 20 --target-processes all python \
+        tools/sanitize_target.py > gpurun_out/sanitize_${tool}_${TAG}.log 2>&1
       echo "${tool}: rc=$?"; tail -4 gpurun_out/sanitize_${tool}_${TAG}.log
     done ;;
   *) echo "unknown: $cmd"; exit 2 ;;
