@@ -482,9 +482,16 @@ def main():
     if args.model == "gpt2":
         return run_gpt2(args, rank, world, local)
 
+    ngpu = max(1, torch.cuda.device_count())
+    shared_gpu = world > ngpu      # more ranks than GPUs: functional run of the multi-rank path only
+    local = local % ngpu
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    coll_dev = "cpu" if shared_gpu else "cuda"
     t_setup0 = time.perf_counter()
     params = blb.Params.from_preset(bi.BERT, device=local)
     layer = FusedLinearLayer(params, Dims(**dims), rank, world, bsgs=BSGS)
@@ -519,15 +526,21 @@ def main():
     from paper_2508_19525_b200.layer import allgather_ragged
 
     def gather(res):
-        """End-of-layer exchange: every rank receives all masked outputs + server shares."""
+        """End-of-layer exchange: every rank receives all masked outputs + server shares.  Every rank
+        walks the same block list (a rank may own no masked output of a block)."""
         if world == 1:
             return res
+        mine = {name: (id0, m, s) for name, id0, (m, s) in res}
         out = []
-        for name, id0, (m, s) in res:
-            items = [torch.cat([m[t].reshape(-1), s[t].reshape(-1)]) for t in range(m.shape[0])]
-            out.append((name, id0, allgather_ragged(items, layer.mask_counts(name),
-                                                    like=torch.empty(3 * params.N, dtype=torch.int64,
-                                                                     device="cuda"))))
+        for name in ("qk", "qkv", "oproj", "ffn1", "ffn2"):
+            counts = layer.mask_counts(name)
+            if sum(counts) == 0:
+                continue
+            id0, m, s = mine.get(name, (None, None, None))
+            items = [] if m is None else [torch.cat([m[t].reshape(-1), s[t].reshape(-1)]).to(coll_dev)
+                                          for t in range(m.shape[0])]
+            out.append((name, id0, allgather_ragged(items, counts, like=torch.empty(3 * params.N, dtype=torch.int64,
+                                                                                    device=coll_dev))))
         return out
 
     def step():
@@ -570,7 +583,7 @@ def main():
     tsum = blb.timing_read(blb.TIMING_TENSOR)
     ms_step = ms_total / args.steps
     if world > 1:
-        t = torch.tensor([ms_step], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms_step], device=coll_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
 
@@ -606,7 +619,7 @@ def main():
         barrier()
         e2e_ms = e0.elapsed_time(e1) / args.steps
         if world > 1:
-            t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+            t = torch.tensor([e2e_ms], device=coll_dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
         e2e = {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
@@ -661,6 +674,7 @@ def main():
         "setup_s": {"keygen": t_keys, "weight_encode": t_encode, "plaintexts": layer.n_plaintexts(),
                     "plaintext_GB": layer.plaintext_bytes() / 1e9},
         "e2e": e2e,
+        "shared_gpu": shared_gpu or None,   # true: ranks shared one GPU (functional check, not a scaling number)
         "full_layer": ({"ms": ms_step + f2["ms_per_step"], "matmul_blocks_ms": ms_step, "f2_chains_ms": f2["ms_per_step"],
                         "what": "the fused-linear MatMul step (value) + the row-f2 chains of one layer (negExp, "
                                 "Softmax smul_cc, 2 x LayerNorm head/tail, GeLU head) on the Table-6 block-3 preset",

@@ -241,7 +241,10 @@ __global__ void k_bconv_modup(PtrList c1_ntt, const u64 *coef, u64 *ext, const u
 // Jobs sharing one switching key (same Galois element) form a group of <= 4:
 // every key word is loaded once per group and re-used from registers (the key
 // stream is the dominant HBM traffic of a key switch).
-constexpr int kKsGroup = 4;
+#ifndef BLB_KS_GROUP
+#define BLB_KS_GROUP 4
+#endif
+constexpr int kKsGroup = BLB_KS_GROUP;  // jobs sharing one key per CTA (compile-time A/B)
 struct KsGroups {
     int n;
     int start[kMaxJobs + 1];
