@@ -277,6 +277,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
         "r"(phase)
         : "memory");
 }
+// generic-proxy reads of a ring slot (the consumers, ordered by the empty mbarrier) before the
+// async-proxy (cp.async.bulk) writes that refill it
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(dst)),

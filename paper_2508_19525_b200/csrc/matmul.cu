@@ -309,7 +309,10 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char
             int slot = 0;
             unsigned phase = 0;  // parity of the empty-barrier round being waited for
             for (int s = 0; s < n_e; s++) {
-                if (s >= nst) mbar_wait(&empty[slot], phase);
+                if (s >= nst) {
+                    mbar_wait(&empty[slot], phase);
+                    fence_proxy_async_smem();
+                }
                 unsigned char *stb = ring + (size_t)slot * stage_bytes;
                 mbar_expect_tx(&full[slot], (unsigned)nP * tb + 2u * 4096u);
                 for (int j = 0; j < nP; j++) bulk_g2s(stb + j * tb, pp[j] + (long long)s * tb, tb, &full[slot]);
@@ -469,7 +472,10 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_j(const u64 *__restrict_
             for (int j = 0; j < JG; j++) eb[j] = ent_start[o0 + oa + j];
             for (int s = 0; s < n_e; s++) {
                 const int slot = s % kMjStages;
-                if (s >= kMjStages) mbar_wait(&empty[slot], ((s / kMjStages) - 1) & 1);
+                if (s >= kMjStages) {
+                    mbar_wait(&empty[slot], ((s / kMjStages) - 1) & 1);
+                    fence_proxy_async_smem();
+                }
                 u64 *st = ring + (size_t)slot * kStageWords;
                 mbar_expect_tx(&full[slot], (unsigned)(1 + 2 * JG) * 4096);
                 bulk_g2s(st, pt + (long long)ent_pt[e_lo + s] * kN + lx0, 4096, &full[slot]);
