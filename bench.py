@@ -365,8 +365,9 @@ def run_gpt2(args, rank: int, world: int, local: int):
             "data": "synthetic (seeded N(0,1) activations, N(0,0.04^2) weights, seeds 100 + 10 layer + m)",
             "config": {"workload": "GPT2-base 12 layers, L=128, d=768, 12 heads, FFN 3072; per layer the fused-linear "
                                    "step of the BERT-base bench; N=2^16, Q={60,40x4}, P={60}, dnum=5",
-                       "plaintexts": "re-encoded on the device per layer from resident float64 weights (680 GB of "
-                                     "packed plaintexts for 12 layers exceed one GPU; resident at 8 GPUs)",
+                       "plaintexts": ("resident (this rank's share of all 12 layers fits)" if stack.resident else
+                                      "re-encoded on the device per layer from resident float64 weights (680 GB of "
+                                      "packed plaintexts for 12 layers exceed one GPU; resident at 8 GPUs)"),
                        "bsgs": dict(BSGS), "parallelism": "dp%d" % world},
             "gpu_launches": ctr["launches"], "counters_per_step": {k: v / args.steps for k, v in ctr.items()},
             "clocks": clk, "setup_s": t_setup}), flush=True)

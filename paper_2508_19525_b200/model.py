@@ -32,8 +32,10 @@ def gpt2_layer_weights(layer: int, dims: Dims) -> list:
 
 class GPT2Stack:
     def __init__(self, params: blb.Params, n_layers: int = 12, dims: Dims = Dims(), bsgs: dict | None = None,
-                 rank: int = 0, world: int = 1, resident: bool = False):
-        self.p, self.n_layers, self.dims, self.resident = params, n_layers, dims, resident
+                 rank: int = 0, world: int = 1, resident: bool | None = None, budget_bytes: float = 120e9):
+        """resident: keep every layer's plaintexts on the device (None: when this rank's share of all
+        layers fits budget_bytes -- e.g. 1/8 of 680 GB at 8 GPUs -- else re-encode per layer)."""
+        self.p, self.n_layers, self.dims = params, n_layers, dims
         self.layer = FusedLinearLayer(params, dims, rank, world, bsgs=bsgs)
         self.w_dev = []      # per layer: device float64 matrices in the plans' shapes
         self.pts = []        # resident mode: per layer the encoded plaintexts
@@ -48,7 +50,9 @@ class GPT2Stack:
         # first layer through the layer's own loader: allocates the plaintext buffers, masks, workspace
         self.layer.load_weights(*gpt2_layer_weights(0, dims))
         self.loaded = 0
-        if resident:
+        per_layer = sum(int(t.numel()) * 8 for t in self.layer.pts.values())
+        self.resident = (per_layer * n_layers <= budget_bytes) if resident is None else resident
+        if self.resident:
             for l in range(n_layers):
                 self.pts.append({k: self._encode(l, k) for k in self.layer.plans})
 
