@@ -99,6 +99,62 @@ __global__ void k_stage(double *buf, const double *zeta, int m, int logN, int in
     }
 }
 
+// N = 2^16 encode: the 16 Gentleman-Sande stages in two shared-memory passes instead of 16 global
+// passes (the stage kernel above reads and writes the whole 32-byte-per-element buffer per stage).
+// Pass A: stages t = 1 .. 128 (pairs inside 256-element blocks); pass B: t = 256 .. N/2 (pairs inside
+// the stride-256 columns).  A CTA holds 2048 elements (64 KB); every butterfly is the stage kernel's
+// (same double-double operations in the same order), so the results are identical.
+constexpr int kEncElems = 2048;
+__device__ __forceinline__ void gs_bfly(double *sm, int a, int b, const double *zeta, int widx) {
+    cdd X = cld(sm + 4 * a), Y = cld(sm + 4 * b);
+    cdd W = cld(zeta + 4ll * widx);
+    W.im = dd_neg(W.im);
+    cst(sm + 4 * a, cadd(X, Y));
+    cst(sm + 4 * b, cmul(csub(X, Y), W));
+}
+__global__ void __launch_bounds__(kTB) k_enc16_A(double *buf, const double *zeta) {
+    extern __shared__ double esm[];
+    constexpr int N = 1 << 16;
+    double *b = buf + (long long)blockIdx.y * N * 4 + (long long)blockIdx.x * kEncElems * 4;
+    for (int i = threadIdx.x; i < kEncElems * 4; i += kTB) esm[i] = b[i];
+    __syncthreads();
+    const int e0 = blockIdx.x * kEncElems;
+    for (int t = 1; t <= 128; t <<= 1) {
+        const int m = N / (2 * t);
+        for (int bf = threadIdx.x; bf < kEncElems / 2; bf += kTB) {
+            const int jl = (bf / t) * 2 * t + (bf % t);
+            gs_bfly(esm, jl, jl + t, zeta, m + (e0 + jl) / (2 * t));
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < kEncElems * 4; i += kTB) b[i] = esm[i];
+}
+// pass B: the CTA's 8 columns lo0 .. lo0 + 7 (element j = mid * 256 + lo), smem [mid][8][4]
+__global__ void __launch_bounds__(kTB) k_enc16_B(double *buf, const double *zeta) {
+    extern __shared__ double esm[];
+    constexpr int N = 1 << 16, C = kEncElems / 256;
+    double *b = buf + (long long)blockIdx.y * N * 4;
+    const int lo0 = blockIdx.x * C;
+    for (int i = threadIdx.x; i < kEncElems * 4; i += kTB) {
+        const int mid = i / (C * 4), r = i % (C * 4);
+        esm[i] = b[((long long)mid * 256 + lo0) * 4 + r];
+    }
+    __syncthreads();
+    for (int tp = 1; tp <= 128; tp <<= 1) {       // t = 256 tp
+        const int m = N / (2 * 256 * tp);
+        for (int bf = threadIdx.x; bf < kEncElems / 2; bf += kTB) {
+            const int c = bf % C, q = bf / C;       // q < 128: butterfly within the column
+            const int mid = (q / tp) * 2 * tp + (q % tp);
+            gs_bfly(esm, mid * C + c, (mid + tp) * C + c, zeta, m + mid / (2 * tp));
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < kEncElems * 4; i += kTB) {
+        const int mid = i / (C * 4), r = i % (C * 4);
+        b[((long long)mid * 256 + lo0) * 4 + r] = esm[i];
+    }
+}
+
 // coefficient k = round_half_even(Re(buf[k]) * scale / N), residues mod q_0..q_level
 __global__ void k_encode_finalize(const double *buf, u64 *out, Primes pr, double scale, int level, int logN,
                                   int *flag, int np_ext, int Kfull) {
@@ -254,10 +310,18 @@ blb_status launch_encode(const blb_params *P, const double *slots, int n_pts, do
     if (n_pts <= 0) return BLB_OK;
     dim3 gs((N / 2 + kTB - 1) / kTB, n_pts);
     k_scatter<<<gs, kTB, 0, st>>>(slots, P->d_slot_pos, buf, n_pts, N);
-    for (int m = N / 2; m >= 1; m >>= 1) k_stage<<<gs, kTB, 0, st>>>(buf, P->d_zeta, m, logN, 1);
+    if (logN == 16) {
+        constexpr size_t smem = (size_t)kEncElems * 32;
+        blb_smem_optin(k_enc16_A, smem);
+        blb_smem_optin(k_enc16_B, smem);
+        k_enc16_A<<<dim3(N / kEncElems, n_pts), kTB, smem, st>>>(buf, P->d_zeta);
+        k_enc16_B<<<dim3(256 / (kEncElems / 256), n_pts), kTB, smem, st>>>(buf, P->d_zeta);
+    } else {
+        for (int m = N / 2; m >= 1; m >>= 1) k_stage<<<gs, kTB, 0, st>>>(buf, P->d_zeta, m, logN, 1);
+    }
     k_encode_finalize<<<dim3((N + kTB - 1) / kTB, n_pts), kTB, 0, st>>>(buf, out, P->pr, scale, level, logN, d_flag,
                                                                         np_ext, P->K);
-    BLB_COUNT_LAUNCH(2 + logN);
+    BLB_COUNT_LAUNCH(logN == 16 ? 4 : 2 + logN);
     BLB_CHECK_LAUNCH();
     RowBatch rb{};
     rb.base = out; rb.poly_stride = (long long)(level + 1 + np_ext) * N; rb.n_polys = n_pts; rb.limbs = level + 1 + np_ext;
