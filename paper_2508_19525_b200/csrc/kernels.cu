@@ -433,8 +433,15 @@ __device__ __forceinline__ void ks_inner_body60(const KsJobs &jobs, const KsGrou
 // grid (tiles * groups, E) with the group index fastest: the CTAs in flight cover every group of a
 // few (limb, tile) slices, so groups that share a key (or an input's hoisted digits) read each tile
 // from DRAM once and from L2 after that
+#ifndef BLB_KS_MINB
+#define BLB_KS_MINB 0   // 0: no launch bound (the compiler picks 64 registers); else CTAs per SM
+#endif
 template <int BETA, bool EXT = false>
-__global__ void k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, int np, int K, int beta_rt,
+__global__ void
+#if BLB_KS_MINB > 0
+__launch_bounds__(256, BLB_KS_MINB)
+#endif
+k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, int np, int K, int beta_rt,
                            int logN, PinvTab pq) {
     const int gi = blockIdx.x % grp.n;
     const int x = (blockIdx.x / grp.n) * blockDim.x + threadIdx.x;
