@@ -415,13 +415,37 @@ def f2_blocks(dims, args, device: int) -> dict:
     ge = [enc(rng.uniform(-2.7, 2.7, n)) for _ in range(n_ge)]
     del sk
 
-    def step():
+    parts = ["negexp", "smul", "ln_head", "ln_tail", "gelu_head"]
+    evs = {p: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for p in parts}
+    acc_ms = {p: 0.0 for p in parts}
+
+    def step(timed=False):
+        st_ = torch.cuda.current_stream()
+
+        def mark(p, i):
+            if timed:
+                evs[p][i].record(st_)
+        mark("negexp", 0)
         ch.negexp_n([x for x, _ in sm], [xb for _, xb in sm])             # block 2 (depth 7)
+        mark("negexp", 1)
+        mark("smul", 0)
         ch.muls([xe for xe, _ in sm_inv], [r for _, r in sm_inv])         # Softmax smul_cc (block 3 head)
+        mark("smul", 1)
+        mark("ln_head", 0)
         for _ in range(2):
             ch.ln_head(ln, L, dims["d"])               # blocks 3 and 5 tails: LayerNorm lines 1-6
+        mark("ln_head", 1)
+        mark("ln_tail", 0)
+        for _ in range(2):
             ch.ln_tail(xmu, rs, gam, bet)              # blocks 4 and 1 heads: LayerNorm lines 8-10
+        mark("ln_tail", 1)
+        mark("gelu_head", 0)
         ch.gelu_head_n(ge, bi.GELU_COEF)               # block 4: GeLU lines 1-4
+        mark("gelu_head", 1)
+        if timed:
+            torch.cuda.synchronize()
+            for p in parts:
+                acc_ms[p] += evs[p][0].elapsed_time(evs[p][1])
 
     for _ in range(args.warmup):
         step()
@@ -433,7 +457,9 @@ def f2_blocks(dims, args, device: int) -> dict:
         step()
     e1.record(st)
     torch.cuda.synchronize()
-    return {"ms_per_step": e0.elapsed_time(e1) / args.steps, "preset": "N=2^15, Q={60,40x7}, P={60}, dnum=8 "
+    step(timed=True)   # one more step with per-chain events (the breakdown, not the headline)
+    return {"ms_per_step": e0.elapsed_time(e1) / args.steps, "breakdown_ms": acc_ms,
+            "preset": "N=2^15, Q={60,40x7}, P={60}, dnum=8 "
             "(Table 6 block 3, P:719)", "ciphertexts": {"negexp": n_sm, "smul": n_sm, "layernorm": n_ln,
                                                       "gelu": n_ge}}
 
