@@ -268,6 +268,12 @@ blb_status blb_share_to_rns(const blb_params *params, const uint64_t *x, int w, 
                             void *stream);
 blb_status blb_mpc_to_ckks(const blb_params *params, blb_ct *ct, const uint64_t *x1, int w, void *ws,
                            size_t ws_bytes, void *stream);
+/* The same for shares over Z_{2^w} with w <= 128 (the paper's ring-to-field runs on Z_{2^{l+40}},
+ * l = 43 -> w = 83): x / x1 device [N][2] u64 little-endian words (x < 2^w). */
+blb_status blb_share_to_rns128(const blb_params *params, const uint64_t *x, int w, int sub, int level, uint64_t *out,
+                               void *stream);
+blb_status blb_mpc_to_ckks128(const blb_params *params, blb_ct *ct, const uint64_t *x1, int w, void *ws,
+                              size_t ws_bytes, void *stream);
 /* Row f3, local fixed-point Decode of a share ("O(N log N) FFT ... extend the shares to
  * a larger ring and conduct local truncations"; App. C.4; reading C18).  Each MPC party
  * runs it on its own share; the outputs are additive shares of the real slots of Decode(m) scaled

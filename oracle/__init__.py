@@ -123,6 +123,8 @@ def lib():
         L.orc_moddown_rescale.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
         L.orc_share_decode.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
         L.orc_share_encode.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+        L.orc_share_to_rns128.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_void_p]
         L.orc_share_to_rns.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_void_p]
         L.orc_relinearize_ext.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
@@ -621,10 +623,15 @@ def moddown_ct(ctx: Ctx, a: CtExt) -> Ct:
 # f3: MPC -> CKKS ingest (Algorithm 2, P:641-657; ring-to-field, App. C.3 P:1222-1232)
 # ---------------------------------------------------------------------------
 def share_to_rns(ctx: Ctx, x, w: int, sub: bool, level: int) -> np.ndarray:
-    """[x]^q = x mod q (P0) or x - 2^w mod q (P1, sub) per limb, NTT form [level+1][N]."""
+    """[x]^q = x mod q (P0) or x - 2^w mod q (P1, sub) per limb, NTT form [level+1][N].
+    x: uint64 [N] (w <= 64) or [N][2] little-endian words (w <= 128, e.g. l + 40 = 83)."""
     x = np.ascontiguousarray(x, dtype=np.uint64)
-    assert x.shape == (ctx.N,) and 1 <= w <= 64
     out = np.empty((level + 1, ctx.N), dtype=np.uint64)
+    if x.ndim == 2:
+        assert x.shape == (ctx.N, 2) and 1 <= w <= 128
+        lib().orc_share_to_rns128(ctx._h, _p(x), int(w), int(bool(sub)), level, _p(out))
+        return out
+    assert x.shape == (ctx.N,) and 1 <= w <= 64
     lib().orc_share_to_rns(ctx._h, _p(x), int(w), int(bool(sub)), level, _p(out))
     return out
 

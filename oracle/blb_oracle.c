@@ -905,6 +905,23 @@ void orc_share_to_rns(const orc_ctx *c, const u64 *x, int w, int sub, int lvl, u
     }
 }
 
+/* The same for a share in Z_{2^w} with w <= 128 (x: [N][2] u64 little-endian words, x < 2^w): the
+ * paper's ring-to-field runs on Z_{2^{l+40}}, l = 43, wider than one word. */
+void orc_share_to_rns128(const orc_ctx *c, const u64 *x, int w, int sub, int lvl, u64 *out) {
+    u64 N = c->N;
+    for (int i = 0; i <= lvl; i++) {
+        u64 q = c->mod[i];
+        u64 r64 = (u64)(((u128)1 << 64) % q);
+        u64 two_w = w < 128 ? (u64)(((u128)1 << w) % q) : mulmod(r64, r64, q);
+        u64 *o = out + (u64)i * N;
+        for (u64 j = 0; j < N; j++) {
+            u64 v = (u64)((((u128)x[2 * j + 1] << 64) | x[2 * j]) % q);
+            o[j] = sub ? submod(v, two_w, q) : v;
+        }
+        ntt_limb(c, o, i);
+    }
+}
+
 /* ------------------------------------------------------------------ */
 /* f3: local fixed-point Decode of a share over Z_{2^128}               */
 /* ("O(N log N) FFT ... extend the shares to a larger ring and  */

@@ -93,6 +93,8 @@ def lib() -> ctypes.CDLL:
             "blb_share_to_rns": ([vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp], ctypes.c_int),
             "blb_mpc_to_ckks": ([vp, vp, vp, ctypes.c_int, vp, ctypes.c_size_t, vp], ctypes.c_int),
             "blb_share_decode": ([vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
+            "blb_share_to_rns128": ([vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp], ctypes.c_int),
+            "blb_mpc_to_ckks128": ([vp, vp, vp, ctypes.c_int, vp, ctypes.c_size_t, vp], ctypes.c_int),
             "blb_share_encode": ([vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
             "blb_matmul_plan_create": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp,
                                         ctypes.c_int, ctypes.c_int, ctypes.c_int, vp], ctypes.c_int),
@@ -455,6 +457,10 @@ def share_to_rns(params: Params, x: torch.Tensor, w: int, sub: bool, level: int)
     """Row f3: a share over Z_{2^w} (int64 [N] CUDA, the u64 bit pattern) -> NTT residues [level+1][N]
     of x mod q_i (P0) or x - 2^w mod q_i (P1, sub)."""
     out = params.empty(level + 1, params.N)
+    if x.dim() == 2:   # 128-bit shares [N][2] (w <= 128)
+        _check(lib().blb_share_to_rns128(params.handle, _ptr(x.contiguous()), int(w), int(bool(sub)), level,
+                                         _ptr(out), _stream()))
+        return out
     _check(lib().blb_share_to_rns(params.handle, _ptr(x.contiguous()), int(w), int(bool(sub)), level, _ptr(out),
                                   _stream()))
     return out
@@ -464,8 +470,8 @@ def mpc_to_ckks(params: Params, ct: Ciphertext, x1: torch.Tensor, w: int) -> Cip
     """Row f3, server half of Alg. 2 line 4: ct (+) [tmp]_1^q, in place (c0 += NTT(x1 - 2^w mod q_i))."""
     ws = params.empty(ct.level + 1, params.N)
     c = ct.c()
-    _check(lib().blb_mpc_to_ckks(params.handle, ctypes.byref(c), _ptr(x1.contiguous()), int(w), _ptr(ws),
-                                 ws.numel() * 8, _stream()))
+    fn = lib().blb_mpc_to_ckks128 if x1.dim() == 2 else lib().blb_mpc_to_ckks
+    _check(fn(params.handle, ctypes.byref(c), _ptr(x1.contiguous()), int(w), _ptr(ws), ws.numel() * 8, _stream()))
     return ct
 
 

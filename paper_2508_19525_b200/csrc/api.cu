@@ -851,6 +851,52 @@ extern "C" blb_status blb_mpc_to_ckks(const blb_params *P, blb_ct *ct, const uin
     return blb_launch_add(P, ct->data, s, ct->data, k, 1, (cudaStream_t)stream);
 }
 
+// 128-bit shares (w <= 128): x [N][2] little-endian words; v = (hi * 2^64 + lo) mod q_i
+namespace {
+__global__ void k_share_rns128(const u64 *x, u64 *out, Primes pr, PinvTab two_w, int sub, int N) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y;
+    if (j >= N) return;
+    const ModConst &mc = pr.m[i];
+    const u64 v = reduce128(x[2 * j + 1], x[2 * j], mc);
+    out[(long long)i * N + j] = sub ? submod(v, two_w.v[i], mc.q) : v;
+}
+}  // namespace
+
+extern "C" blb_status blb_share_to_rns128(const blb_params *P, const uint64_t *x, int w, int sub, int level,
+                                          uint64_t *out, void *stream) {
+    if (!P || !x || !out || w < 1 || w > 128) return BLB_E_INVALID_ARG;
+    if (level < 0 || level >= P->K) return BLB_E_LEVEL;
+    const int k = level + 1, N = P->N;
+    PinvTab tw{};
+    for (int i = 0; i < k; i++) {
+        const u64 q = P->mod[i];
+        const u64 r64 = (u64)(((u128)1 << 64) % q);
+        tw.v[i] = w < 128 ? (u64)(((u128)1 << w) % q) : (u64)(((u128)r64 * r64) % q);
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    k_share_rns128<<<dim3((N + 255) / 256, k), 256, 0, st>>>(x, out, P->pr, tw, sub ? 1 : 0, N);
+    BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    RowBatch rb{};
+    rb.base = out; rb.poly_stride = (long long)k * N; rb.n_polys = 1; rb.limbs = k; rb.limb0 = 0;
+    for (int i = 0; i < k; i++) rb.prime[i] = i;
+    return launch_ntt(P, rb, false, st);
+}
+
+extern "C" blb_status blb_mpc_to_ckks128(const blb_params *P, blb_ct *ct, const uint64_t *x1, int w, void *ws,
+                                         size_t ws_bytes, void *stream) {
+    if (!P || !ct || !ct->data || !x1 || !ws) return BLB_E_INVALID_ARG;
+    const int k = ct->level + 1;
+    if (ws_bytes < (size_t)k * P->N * sizeof(u64)) {
+        blb_set_error("blb_mpc_to_ckks128: workspace needs %zu bytes", (size_t)k * P->N * sizeof(u64));
+        return BLB_E_NOMEM;
+    }
+    u64 *s = (u64 *)ws;
+    BLB_TRY(blb_share_to_rns128(P, x1, w, 1, ct->level, s, stream));
+    return blb_launch_add(P, ct->data, s, ct->data, k, 1, (cudaStream_t)stream);
+}
+
 extern "C" blb_status blb_mhp_column_map(int d, int heads, int L, int log_n, int32_t *map_out, int *len) {
     if (!len || d <= 0 || heads <= 0 || d % heads || L <= 0 || log_n < 2) return BLB_E_INVALID_ARG;
     const int n = 1 << (log_n - 1);

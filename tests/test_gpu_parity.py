@@ -627,3 +627,41 @@ def test_ckks_to_mpc_rerandomised_bit_exact(name, flood, request):
         rr = O.rerandomize(pair.o, octs[t], opk, rk, 500 + t, flood)
         om, osh = O.mask(pair.o, rr, mk, 500 + t)
         assert np.array_equal(u64(m[t]), om) and np.array_equal(u64(s[t]), osh)
+
+
+@pytest.mark.parametrize("name", ["toy", "bert"])
+def test_algorithm2_chain_bit_exact(name, request):
+    """Alg. 2 on the GPU: local fixed-point encode of both slot shares (C20), zero-sharing
+    re-randomisation, reduction to Z_{2^83} (w = l + 40), ring-to-field of both shares on 128-bit
+    words, P0's encryption + P1's ingest: every limb bit-exact against the oracle, and the result
+    decodes to the shared vector."""
+    pair = request.getfixturevalue(name)
+    rng = np.random.default_rng(72)
+    z = rng.uniform(-1, 1, pair.n)
+    f, ft, w = 50, 50, 83
+    s_out = f + pair.o.log_n - 40
+    y = [int(round(v * 2.0 ** f)) for v in z]
+    rnd = lambda n: [int(a) | (int(b) << 64) for a, b in zip(rng.integers(0, 2 ** 63, n, dtype=np.uint64),  # noqa
+                                                          rng.integers(0, 2 ** 63, n, dtype=np.uint64))]
+    y0 = rnd(pair.n)
+    y1 = [(v - a) % (1 << 128) for v, a in zip(y, y0)]
+    e0 = u64(blb.share_encode(pair.g, dev(O.int_to_u128(y0)), ft, s_out))
+    e1 = u64(blb.share_encode(pair.g, dev(O.int_to_u128(y1)), ft, s_out))
+    assert np.array_equal(e0, O.share_encode(pair.o, O.int_to_u128(y0), ft, s_out))
+    assert np.array_equal(e1, O.share_encode(pair.o, O.int_to_u128(y1), ft, s_out))
+    u = rnd(pair.N)
+    x0 = O.int_to_u128([(a + r) % (1 << w) for a, r in zip(O.u128_to_int(e0), u)])
+    x1 = O.int_to_u128([(b - r) % (1 << w) for b, r in zip(O.u128_to_int(e1), u)])
+    lvl = min(2, pair.K - 1)
+    for sub, xs in ((False, x0), (True, x1)):
+        assert np.array_equal(u64(blb.share_to_rns(pair.g, dev(xs), w, sub, lvl)),
+                              O.share_to_rns(pair.o, xs, w, sub, lvl))
+    okeys = O.keygen(pair.o, bi.crypto_key(4, 73))
+    gkeys, sk = blb.keygen(pair.g, bi.crypto_key(4, 73), [])
+    f0 = O.share_to_rns(pair.o, x0, w, False, lvl)
+    oct_ = O.mpc_to_ckks(pair.o, O.encrypt(pair.o, bi.crypto_key(5, 73), okeys.s_ntt, f0, lvl, 9, 2.0 ** 40), x1, w)
+    gct = blb.mpc_to_ckks(pair.g, blb.encrypt(pair.g, sk, dev(f0), lvl, bi.crypto_key(5, 73), 9, 2.0 ** 40),
+                          dev(x1), w)
+    assert np.array_equal(u64(gct.data), oct_.data)
+    dec = pair.g.decode(blb.decrypt(pair.g, sk, gct), gct.scale).cpu().numpy()
+    assert np.abs(dec - z).max() < 1e-6

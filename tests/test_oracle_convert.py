@@ -151,3 +151,51 @@ def test_share_encode_then_decode_round_trip(toy):
     x = O.share_encode(toy, O.int_to_u128(_fx(z, f)), ft, s_out)
     back = O.u128_to_int(O.share_decode(toy, x, 30, 0))        # sum_k x_k Re(zeta^{k 5^j}) = Delta z_j
     assert np.abs(np.array(back, dtype=np.float64) - z * 2.0 ** 40).max() < 2.0 ** 12   # |err| < 2^-28 of 1.0
+
+
+def test_share_to_rns_wide_residues(toy):
+    """Ring-to-field on Z_{2^w}, w = l + 40 = 83 (l = 43) and w = 128: residues of
+    the 128-bit shares, the P1 variant subtracting 2^w mod q_i (Python integers)."""
+    rng = np.random.default_rng(47)
+    for w in (83, 128):
+        xs = [int(a) | (int(b) << 64) for a, b in zip(rng.integers(0, 2 ** 63, toy.N, dtype=np.uint64),
+                                                      rng.integers(0, 2 ** 63, toy.N, dtype=np.uint64))]
+        xs = [v % (1 << w) for v in xs]
+        x = O.int_to_u128(xs)
+        for sub in (False, True):
+            got = toy.intt(O.share_to_rns(toy, x, w, sub, 2), [0, 1, 2])
+            for i in range(3):
+                q = int(toy.mods[i])
+                assert [int(v) for v in got[i, :64]] == [(v - (2 ** w if sub else 0)) % q for v in xs[:64]]
+
+
+def test_algorithm2_chain_encode_ring_to_field_ingest(toy):
+    """Alg. 2 end to end on the toy ring: each party encodes its slot share locally
+    (C20), the shares are reduced to Z_{2^w} with w = l + 40 = 83, ring-to-field maps them to the
+    field (App. C.3), P0 encrypts its field share and P1 adds its own: the ciphertext decodes to the
+    shared vector (the paper's success event x0 + x1 >= 2^w holds for these shares)."""
+    rng = np.random.default_rng(48)
+    z = rng.uniform(-1, 1, toy.n)
+    f, ft, w = 50, 50, 83
+    s_out = f + toy.log_n - 40                     # Delta = 2^40
+    y = [int(round(v * 2.0 ** f)) for v in z]
+    y0 = [int(a) | (int(b) << 64) for a, b in zip(rng.integers(0, 2 ** 63, toy.n, dtype=np.uint64),
+                                                  rng.integers(0, 2 ** 63, toy.n, dtype=np.uint64))]
+    y1 = [(v - a) % (1 << 128) for v, a in zip(y, y0)]
+    x0 = [v % (1 << w) for v in O.u128_to_int(O.share_encode(toy, O.int_to_u128(y0), ft, s_out))]
+    x1 = [v % (1 << w) for v in O.u128_to_int(O.share_encode(toy, O.int_to_u128(y1), ft, s_out))]
+    # coefficient N/2 of the encode of ANY real vector is exactly 0 (zeta^{-N/2 5^j} = +-i), so both
+    # local encodes are 0 there and ring-to-field's success event x0 + x1 >= 2^w fails; the parties
+    # re-randomise with a zero sharing (u from a shared PRF) first (reading C20)
+    assert x0[toy.N // 2] == 0 and x1[toy.N // 2] == 0
+    u = [int(a) | (int(b) << 64) for a, b in zip(rng.integers(0, 2 ** 63, toy.N, dtype=np.uint64),
+                                                 rng.integers(0, 2 ** 63, toy.N, dtype=np.uint64))]
+    x0 = [(a + r) % (1 << w) for a, r in zip(x0, u)]
+    x1 = [(b - r) % (1 << w) for b, r in zip(x1, u)]
+    keys = O.keygen(toy, bi.crypto_key(4, 49))
+    lvl = 2
+    f0 = O.share_to_rns(toy, O.int_to_u128(x0), w, False, lvl)
+    ct = O.encrypt(toy, bi.crypto_key(5, 49), keys.s_ntt, f0, lvl, 3, 2.0 ** 40)
+    out = O.mpc_to_ckks(toy, ct, O.int_to_u128(x1), w)
+    dec = O.decode(toy, O.decrypt(toy, keys.s_ntt, out), out.scale)
+    assert np.abs(dec - z).max() < 1e-6
