@@ -20,6 +20,7 @@ masked results are all-gathered.
 from __future__ import annotations
 
 import argparse
+import itertools
 import json
 import os
 import subprocess
@@ -143,7 +144,7 @@ def layer_counts(dims) -> dict:
     return c
 
 
-def oracle_slice(threads: int) -> dict:
+def oracle_slice(threads: int, preset=bi.BERT) -> dict:
     """The CPU oracle, as it stands, on one stated slice of the layer at N = 2^16, level 4 (k = 5),
     timed directly: one baby-step rotation (hoisted-form ModUp + key switch + ModDown, C8), one
     (b', g) unit of the FFN1 MAC (3 inputs x B = 64 = 192 ct-pt products summed, C11), its giant
@@ -153,7 +154,7 @@ def oracle_slice(threads: int) -> dict:
     residues stand in for encoded weights and keys (encode is row a0)."""
     import oracle as O
     set_omp_threads(threads)
-    P = bi.BERT
+    P = preset
     primes = O.prime_chain(P.log_n, list(P.q_bits) + list(P.p_bits))
     ctx = O.Ctx(P.log_n, primes[:5], primes[5:], P.dnum)
     rng = np.random.default_rng(0)
@@ -165,7 +166,7 @@ def oracle_slice(threads: int) -> dict:
 
     ct = O.Ct(rnd(2, range(k)), lvl, 2.0 ** 40)
     g = ctx.galois(128)
-    key = np.stack([rnd(2, range(6)) for _ in range(ctx.beta_top)])
+    key = np.stack([rnd(2, range(len(primes))) for _ in range(ctx.beta_top)])
     keys = O.Keys(None, None, {g: key, ctx.galois(64 * 128): key}, key)
     n_prod = 3 * BSGS["ffn1"]
     pts = [rnd(1, range(k))[0] for _ in range(n_prod)]
@@ -211,13 +212,13 @@ def layer_estimate_ms(per_op: dict, counts: dict) -> float:
                   counts["mask"] * per_op["mask"])
 
 
-def cpu_baseline(dims) -> dict:
+def cpu_baseline(dims, preset=bi.BERT) -> dict:
     """The oracle timed on the host: the slice at 1 thread and at all cores (bounded, ~10-30 s)."""
     info = cpu_info()
     allc = info["nproc"]
-    oracle_slice(allc)                       # warm: library load, table build
-    ra = oracle_slice(allc)
-    r1 = oracle_slice(1)
+    oracle_slice(allc, preset)               # warm: library load, table build
+    ra = oracle_slice(allc, preset)
+    r1 = oracle_slice(1, preset)
     counts = layer_counts(dims)
     return {"value": ra["ms"], "unit": "ms per slice", "cores": allc, "kind": "oracle", "sample": slice_desc(),
             "ms_per_slice_1thread": r1["ms"], "cpu_model": info["cpu_model"], "nproc": info["nproc"],
@@ -228,16 +229,16 @@ def cpu_baseline(dims) -> dict:
             "estimate_how": "sum over operation kinds of (directly timed op time x its count per layer step)"}
 
 
-def run_reference(args, dims):
+def run_reference(args, dims, preset=bi.BERT):
     """--impl reference: the oracle timed on host cores (all of them), each step one slice of the
     layer (oracle_slice).  ms_per_step is the timed slice; value is its layer-equivalent in the
     metric's unit (each timed operation times its count per layer step, stated in the line)."""
     info = cpu_info()
     counts = layer_counts(dims)
-    oracle_slice(info["nproc"])               # warm-up outside the timed steps (library load, tables)
+    oracle_slice(info["nproc"], preset)       # warm-up outside the timed steps (library load, tables)
     steps, ests = [], []
     for s in range(args.warmup + args.steps):
-        r = oracle_slice(info["nproc"])
+        r = oracle_slice(info["nproc"], preset)
         if s >= args.warmup:
             steps.append(r["ms"])
             ests.append(layer_estimate_ms(r["per_op_s"], counts))
@@ -246,7 +247,7 @@ def run_reference(args, dims):
     line = {"impl": "reference", "metric": metric_name(dims), "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": config_dict(dims, args.gpus),
+            "config": config_dict(dims, args.gpus, preset),
             "timed_region": "each step = one directly timed oracle slice (ms_per_step); value = that slice's "
                             "layer-equivalent (layer_counts x per-op times)",
             "layer_counts": counts,
@@ -264,10 +265,19 @@ def metric_name(dims):
     return METRIC.replace("BERT-base", model_name(dims))
 
 
-def config_dict(dims, world):
+def preset_desc(preset) -> str:
+    def fmt(bits):
+        return ",".join("%dx%d" % (b, n) if n > 1 else str(b)
+                        for b, n in ((b, len(list(g))) for b, g in itertools.groupby(bits)))
+    return "N=2^%d, Q={%s}, P={%s}, dnum=%d" % (preset.log_n, fmt(preset.q_bits), fmt(preset.p_bits), preset.dnum)
+
+
+def config_dict(dims, world, preset=bi.BERT):
     return {"workload": model_name(dims) + " layer fused-linear CKKS (config 2 QKV + Q.K^T, Softmax.V + out-proj, config 3 "
-                        "FFN1/FFN2, CKKS->MPC masks), N=2^16, Q={60,40x4}, P={60}, dnum=5",
-            "L": dims["L"], "d": dims["d"], "heads": dims["H"], "ffn": dims["ffn"], "log_n": 16, "limbs": 5,
+                        "FFN1/FFN2, CKKS->MPC masks), " + preset_desc(preset) +
+                        ("" if preset is bi.BERT else " (the config-2 dnum=1 variant, reading C23)"),
+            "L": dims["L"], "d": dims["d"], "heads": dims["H"], "ffn": dims["ffn"], "log_n": preset.log_n,
+            "limbs": len(preset.q_bits), "special_primes": len(preset.p_bits), "dnum": preset.dnum,
             "bsgs": dict(BSGS),
             "layer_ops": ["qkv_ct_pt(MHP)", "qk_ct_ct(MHP+BSGS)", "mask(QK^T)", "mask(V)",
                           "softmaxV_ct_ct(pad+collapse)", "oproj_diag_ct_pt(level 1)", "mask", "ffn1_ct_pt", "mask",
@@ -465,6 +475,129 @@ def f2_blocks(dims, args, device: int) -> dict:
 
 
 # --------------------------------------------------------------------------- our arm
+TOY_METRIC = "ms per config-1 toy step (ct-pt MatMul 16x16x16 + CKKS->MPC mask)"
+
+
+def toy_oracle_step(threads: int) -> float:
+    """The whole config-1 step in the oracle (no extrapolation): MatMul of the encrypted X with W
+    (C11, B = 16) and the CKKS->MPC mask of the output.  -> seconds."""
+    import oracle as O
+    import oracle.matmul as mm
+    set_omp_threads(threads)
+    P, d = bi.TOY, bi.toy_inputs()
+    primes = O.prime_chain(P.log_n, list(P.q_bits) + list(P.p_bits))
+    ctx = O.Ctx(P.log_n, primes[:3], primes[3:], P.dnum)
+    plan = mm.plan_spatial(d["W"], 16, ctx.n, 16)
+    keys = O.keygen(ctx, d["keys_key"], plan.rotation_steps())
+    delta = 2.0 ** P.log_delta
+    cts = [O.encrypt(ctx, d["enc_key"], keys.s_ntt, O.encode(ctx, z, delta, ctx.K - 1), ctx.K - 1, t, delta)
+           for t, z in enumerate(mm.pack_spatial(d["X"], ctx.n))]
+    t0 = time.perf_counter()
+    (y,) = mm.matmul_cp(ctx, keys, cts, plan)
+    O.mask(ctx, y, d["mask_key"], 0)
+    return time.perf_counter() - t0
+
+
+def run_toy(args):
+    """BASELINE config 1: N = 2^12, Q = {60, 40, 40}, P = {60}, dnum = 3; X in R^{16x16} ~ U(-1, 1)
+    (seed 1), W ~ U(-1/2, 1/2) (seed 2); one step = the ct-pt MatMul (15 baby + 1 giant rotation,
+    31 plaintexts, fused ModDown + rescale) + the CKKS->MPC mask of its output.  Launch-latency bound
+    at this size (a handful of microsecond kernels); reported for completeness of the config list."""
+    info = cpu_info()
+    if args.impl == "reference":
+        toy_oracle_step(info["nproc"])
+        ts = [toy_oracle_step(info["nproc"]) for _ in range(args.warmup + args.steps)][args.warmup:]
+        v = 1e3 * float(np.median(ts))
+        print(json.dumps({"impl": "reference", "metric": TOY_METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
+                          "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                          "config": {"workload": "config 1 toy: " + preset_desc(bi.TOY) + ", X W 16x16x16 + mask"},
+                          "cpu_baseline": {"kind": "oracle", "value": v, "unit": UNIT, "cores": info["nproc"],
+                                           "cpu_model": info["cpu_model"], "sample": "the whole toy step"},
+                          "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+              flush=True)
+        return
+    import torch
+    import paper_2508_19525_b200 as blb
+    from paper_2508_19525_b200 import packing
+    P, d = bi.TOY, bi.toy_inputs()
+    params = blb.Params.from_preset(P)
+    plan = blb.MatmulPlan(params, 16, 16, 16, bsgs_B=16)
+    keys, sk = blb.keygen(params, d["keys_key"], plan.rotation_steps())
+    pts = plan.encode_weights(d["W"])
+    delta = 2.0 ** P.log_delta
+    zs = packing.spatial_slots(d["X"], params.n)
+    cts = [blb.encrypt(params, sk, params.encode(torch.tensor(z), delta, params.K - 1), params.K - 1, d["enc_key"],
+                       t, delta) for t, z in enumerate(zs)]
+    stream = torch.cuda.current_stream()
+
+    def step(inp, seq):
+        out = plan(keys, inp, pts)
+        return blb.ckks_to_mpc(params, out, d["mask_key"], seq)
+
+    for s in range(args.warmup):
+        step(cts, s)
+    torch.cuda.synchronize()
+    blb.reset_counters()
+    blb.timing_reset()
+    blb.timing_enable(True)
+    clocks = Clocks(0)
+    clocks.start()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for s in range(args.steps):
+        step(cts, 1000 + s)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    blb.timing_enable(False)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ctr = blb.counters()
+    mac = blb.timing_read(blb.TIMING_MAC)
+    # e2e: input ciphertexts from pinned host memory, masked output + share back to pinned memory
+    host_in = [c.data.cpu().pin_memory() for c in cts]
+    dev_in = [torch.empty_like(c.data) for c in cts]
+    host_m = torch.empty(2 * params.N, dtype=torch.int64).pin_memory()
+    host_s = torch.empty(params.N, dtype=torch.int64).pin_memory()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for s in range(args.steps):
+        for h, dv in zip(host_in, dev_in):
+            dv.copy_(h, non_blocking=True)
+        m, sh = step([blb.Ciphertext(dv, c.level, c.scale) for dv, c in zip(dev_in, cts)], 2000 + s)
+        host_m.copy_(m.reshape(-1), non_blocking=True)
+        host_s.copy_(sh.reshape(-1), non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    peaks = measured_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", FALLBACK_HBM))
+    mac_gbs = mac["alg_bytes"] / (mac["ms"] * 1e-3) / 1e9 if mac["ms"] > 0 else None
+    line = {"metric": TOY_METRIC, "value": ms, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (X ~ U(-1,1) seed 1, W ~ U(-1/2,1/2) seed 2)",
+            "config": {"workload": "config 1 toy: " + preset_desc(P) + ", X W 16x16x16 + CKKS->MPC mask",
+                       "bsgs_B": 16, "plaintexts": plan.n_pt, "rotations": plan.n_rotations,
+                       "l2": "working set (< 2 MB) is L2-resident: a latency-bound configuration"},
+            "roofline": {"kernel": "k_mac_tma4 (ct-pt weight MAC)", "bound": "hbm", "achieved": mac_gbs,
+                         "peak": hbm_peak, "unit": "GB/s", "frac": mac_gbs / hbm_peak if mac_gbs else None,
+                         "traffic": None, "note": "31 plaintexts of 2^12 coefficients: launch latency, not HBM"},
+            "gpu_launches": ctr["launches"], "counters_per_step": {k: v / args.steps for k, v in ctr.items()},
+            "clocks": clk,
+            "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(sum(h.numel() * 8 for h in host_in)),
+                    "d2h_bytes_per_step": int((host_m.numel() + host_s.numel()) * 8)}}
+    if not args.no_cpu_baseline:
+        toy_oracle_step(info["nproc"])
+        ta = toy_oracle_step(info["nproc"])
+        t1 = toy_oracle_step(1)
+        line["cpu_baseline"] = {"value": 1e3 * ta, "unit": UNIT, "cores": info["nproc"], "kind": "oracle",
+                                "sample": "the whole toy step (MatMul + mask), directly timed",
+                                "ms_1thread": 1e3 * t1, "cpu_model": info["cpu_model"]}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -477,7 +610,12 @@ def main():
     ap.add_argument("--dims", default="base", choices=["base", "large"])
     ap.add_argument("--model", default="layer", choices=["layer", "gpt2"],
                     help="gpt2: config 5, the 12-layer GPT2-base stack with per-layer on-device re-encode")
+    ap.add_argument("--preset", default="bert", choices=["bert", "bert_dnum1"],
+                    help="bert_dnum1: the config-2 dnum = 1 variant (one digit, four special primes; C23)")
+    ap.add_argument("--config", default="layer", choices=["layer", "toy"],
+                    help="toy: BASELINE config 1 (N=2^12, ct-pt MatMul 16x16x16 + CKKS->MPC mask)")
     args = ap.parse_args()
+    preset = {"bert": bi.BERT, "bert_dnum1": bi.BERT_DNUM1}[args.preset]
     dims = dict(L=128, d=768, H=12, ffn=3072) if args.dims == "base" else dict(L=128, d=1024, H=16, ffn=4096)
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -494,9 +632,13 @@ def main():
         print("bench.py: --gpus %d but WORLD_SIZE=%d; using the launched world" % (args.gpus, world), file=sys.stderr)
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.config == "toy":
+        if rank == 0:
+            run_toy(args)
+        return
     if args.impl == "reference":
         if rank == 0:
-            run_reference(args, dims)
+            run_reference(args, dims, preset)
         return
 
     import torch
@@ -520,7 +662,7 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     coll_dev = "cpu" if shared_gpu else "cuda"
     t_setup0 = time.perf_counter()
-    params = blb.Params.from_preset(bi.BERT, device=local)
+    params = blb.Params.from_preset(preset, device=local)
     layer = FusedLinearLayer(params, Dims(**dims), rank, world, bsgs=BSGS)
     A = bi.bert_attention_inputs(dims["L"], dims["d"])
     F = bi.bert_ffn_inputs(dims["L"], dims["d"], dims["H"], dims["ffn"])
@@ -533,7 +675,7 @@ def main():
     t_encode = time.perf_counter() - t0
 
     # client-side inputs: encrypt once (fresh ciphertexts at the top level)
-    delta = 2.0 ** bi.BERT.log_delta
+    delta = 2.0 ** preset.log_delta
     lvl = layer.level
     sv_s, sv_v = packing.softmax_v_operands(F["S"], F["V"], params.n)
     slots = {"qkv": packing.spatial_slots(A["X"], params.n), "sv_s": sv_s, "sv_v": sv_v,
@@ -676,7 +818,7 @@ def main():
         "metric": metric_name(dims), "value": ms_step, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded N(0,1) activations, N(0,0.04^2) weights)",
-        "config": config_dict(dims, world),
+        "config": config_dict(dims, world, preset),
         "roofline": {"kernel": "k_mac_tma4 (ct-pt weight MAC, row a3)", "bound": "hbm", "achieved": mac_gbs, "peak": hbm_peak,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
                      "unit": "GB/s", "frac": (mac_gbs / hbm_peak) if mac_gbs else None, "traffic": traffic,
@@ -708,7 +850,7 @@ def main():
                         "f2": f2} if f2 else None),
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(dims)
+        line["cpu_baseline"] = cpu_baseline(dims, preset)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -41,6 +41,9 @@ class Preset:
 TOY = Preset("toy", 12, (60, 40, 40), (60,), 3, 40)
 # configs 2-5: N = 2^16, Q = {60, 40 x 4}, P = {60}, dnum = 5 (alpha = 1), Delta = 2^40
 BERT = Preset("bert", 16, (60, 40, 40, 40, 40), (60,), 5, 40)
+# the config-2 dnum = 1 variant (reading C23): one key-switch digit = all of Q (220 bits),
+# so P must exceed it: four 60-bit special primes (240 bits; log QP = 460, inside the N = 2^16 bound)
+BERT_DNUM1 = Preset("bert_dnum1", 16, (60, 40, 40, 40, 40), (60, 60, 60, 60), 1, 40)
 # small presets used only by tests (a ragged/tiny ring, and alpha = 2 digits)
 TINY = Preset("tiny", 5, (50, 40, 40), (60,), 3, 30)
 MID = Preset("mid", 10, (60, 40, 40, 40), (61, 61), 2, 36)
@@ -115,6 +118,7 @@ def bert_ffn_inputs(L=128, d=768, H=12, ffn=3072, config_id=3):
 
 # a toy ring with the BERT chain shape (5 ciphertext primes): room for QKV + Q K^T (depth 4)
 QKTOY = Preset("qktoy", 12, (60, 40, 40, 40, 40), (60,), 5, 40)
+QKTOY_DNUM1 = Preset("qktoy_dnum1", 12, (60, 40, 40, 40, 40), (60, 60, 60, 60), 1, 40)
 
 
 def qk_toy_inputs(H=4, L=32, dh=32):

@@ -870,7 +870,7 @@ blb_status launch_moddown(const blb_params *P, int level, u64 *u, int n, u64 *ou
 // y = (X + h - r) / M with h = (M - 1) / 2 and r = (X + h) mod M rebuilt exactly from the
 // residues at the M-moduli by Garner's mixed radix (digits d_t < m_t), reduced mod q_i by Horner.
 // ---------------------------------------------------------------------------
-constexpr int kMdrMax = 4;
+constexpr int kMdrMax = 5;  // q_l + up to 4 special primes (dnum = 1 at k = 5, reading C23)
 struct MdrTab {
     int nd;
     ModConst md[kMdrMax];                          // m_0 = q_l, m_1.. = p_0..

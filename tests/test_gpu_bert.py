@@ -217,3 +217,37 @@ def test_softmax_v_j8_sampled_output_bit_exact(bert):
     (ref,) = cc.qk_encrypted(ctx, okeys, os_, ov, plan_o, out_ids=[o])
     gout = layer.sv(bert["gkeys"], gs, gv, layer.sv_masks, ws=layer.ws)
     assert len(gout) == plan_o.n_out and same(gout[o], ref)
+
+
+@pytest.fixture(scope="module")
+def bert_dnum1():
+    P = bi.BERT_DNUM1
+    pr = O.prime_chain(P.log_n, list(P.q_bits) + list(P.p_bits))
+    return dict(ctx=O.Ctx(P.log_n, pr[:5], pr[5:], P.dnum), params=blb.Params.from_preset(P))
+
+
+def test_dnum1_matmul_sampled_output_bit_exact(bert_dnum1):
+    """The config-2 dnum = 1 variant (C23: one digit = all of Q, four special primes) at N = 2^16:
+    a spatial ct-pt MatMul (3 input ciphertexts of X in R^{128 x 768}, W in R^{768 x 256}, B = 16)
+    through the generic ModUp / ModDown base conversions and the fused ModDown + rescale with
+    nd = 5 moduli -- one output bit-exact against the oracle."""
+    ctx, params = bert_dnum1["ctx"], bert_dnum1["params"]
+    rng = np.random.default_rng(61)
+    X = np.clip(rng.normal(0, 1, (L, D)), -4, 4)
+    W = rng.normal(0, 0.04, (D, 256))
+    plan_o = mm.plan_spatial(W, L, ctx.n, 16)
+    plan_g = blb.MatmulPlan(params, L, D, 256, bsgs_B=16, level=4)
+    assert plan_g.n_pt == plan_o.n_plaintexts
+    key = bi.crypto_key(4, 62)
+    okeys = O.keygen(ctx, key, plan_o.rotation_steps())
+    gkeys, sk = blb.keygen(params, key, plan_g.rotation_steps())
+    zs = mm.pack_spatial(X, ctx.n)
+    enc_key = bi.crypto_key(5, 62)
+    octs, gcts = [], []
+    for t, z in enumerate(zs):
+        octs.append(O.encrypt(ctx, enc_key, okeys.s_ntt, O.encode(ctx, z, DELTA, 4), 4, 50 + t, DELTA))
+        gcts.append(blb.encrypt(params, sk, params.encode(torch.tensor(z), DELTA, 4), 4, enc_key, 50 + t, DELTA))
+        assert np.array_equal(blb.to_numpy_u64(gcts[-1].data), octs[-1].data)
+    gout = plan_g(gkeys, gcts, plan_g.encode_weights(W))
+    (ref,) = mm.matmul_cp(ctx, okeys, octs, plan_o, out_ids=[0])
+    assert same(gout[0], ref)

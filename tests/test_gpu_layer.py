@@ -1,7 +1,7 @@
 """The layer step (layer.FusedLinearLayer, what bench.py times) and its serving pipeline
 (layer.LayerPipeline, the e2e path of bench.py) on a small ring with the BERT chain shape:
 
-* the whole step -- QKV (MHP) -> Q K^T -> masks, Softmax x V -> collapse -> W_O -> mask,
+* the whole step (dnum = 5 and the dnum = 1 variant) -- QKV (MHP) -> Q K^T -> masks, Softmax x V -> collapse -> W_O -> mask,
   FFN1 -> mask, FFN2 -> mask -- is bit-exact against the oracle's layer step
   (oracle/layer.py) on every masked ciphertext and every server share, including the
   per-inference mask ids (reading C19);
@@ -33,9 +33,9 @@ def flat(res):
     return out
 
 
-@pytest.fixture(scope="module")
-def setup():
-    P = bi.QKTOY
+@pytest.fixture(scope="module", params=["qktoy", "qktoy_dnum1"])
+def setup(request):
+    P = {"qktoy": bi.QKTOY, "qktoy_dnum1": bi.QKTOY_DNUM1}[request.param]
     params = blb.Params.from_preset(P)
     layer = FusedLinearLayer(params, Dims(L, D, H, FFN), bsgs=BSGS)
     rng = np.random.default_rng(7)
@@ -58,11 +58,13 @@ def setup():
             inputs[name].append(blb.encrypt(params, sk, pts[b], layer.level, enc_key, 100 + cid, delta))
             cid += 1
     return dict(params=params, layer=layer, W=W, keys=keys, inputs=inputs, mask_key=mask_key, keys_key=keys_key,
-                slots=slots)
+                slots=slots, preset=P)
 
 
 def test_layer_step_matches_oracle(setup):
-    P = bi.QKTOY
+    """dnum = 5 (alpha = 1, the fused ModUp / ModDown paths) and the dnum = 1 variant (one digit of
+    all five ciphertext primes, four special primes: the generic base-conversion paths, C23)."""
+    P = setup["preset"]
     pr = O.prime_chain(P.log_n, list(P.q_bits) + list(P.p_bits))
     ctx = O.Ctx(P.log_n, pr[:5], pr[5:], P.dnum)
     layer = setup["layer"]

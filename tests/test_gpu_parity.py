@@ -57,6 +57,11 @@ def bert():
     return Pair(bi.BERT)
 
 
+@pytest.fixture(scope="module")
+def bert_dnum1():
+    return Pair(bi.BERT_DNUM1)
+
+
 def rand_limbs(pair, shape_polys, limbs, seed):
     rng = np.random.default_rng(seed)
     out = np.empty((shape_polys, len(limbs), pair.N), dtype=np.uint64)
@@ -433,9 +438,12 @@ def test_f2_ops_bit_exact(qktoy):
         assert np.array_equal(u64(r.data), O.rotate_sum(qktoy.o, oa, okeys, L, D, broadcast=bc).data)
 
 
-def test_bert_size_keyswitch_bit_exact(bert):
-    """N = 2^16 (the fused ModUp / ModDown NTT path): rotation at every level, relinearised
-    product, rotate-and-sum, rescale -- bit-exact against the oracle."""
+@pytest.mark.parametrize("name", ["bert", "bert_dnum1"])
+def test_bert_size_keyswitch_bit_exact(name, request):
+    """N = 2^16: rotation at every level, relinearised product, rotate-and-sum -- bit-exact against
+    the oracle; dnum = 5 takes the fused ModUp / ModDown NTT path, the dnum = 1 variant (C23) the
+    generic base conversions with four special primes."""
+    bert = request.getfixturevalue(name)
     key = bi.crypto_key(4, 99)
     steps = [128, -256, 5]
     okeys = O.keygen(bert.o, key, steps, relin=True)
