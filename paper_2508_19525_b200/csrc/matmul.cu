@@ -191,69 +191,87 @@ constexpr size_t mac4_smem() { return mac4_ring_bytes<PP, STG, STGP>() + 2 * (ST
 
 // SPLIT41 (q < 2^41): every product on the grid-split FP64 accumulator (AccG, FP64 pipe, one
 // reduction per output); otherwise (60-bit limbs) Acc128 on the integer pipe, folded every 64.
-template <bool SPLIT41, bool PACKED, int kMacP>
+// The ring geometry is compile-time (tile TB bytes, NST stages) and the stage loop is unrolled by
+// NST, so every ring access is a shared load at a constant offset from one per-thread base and the
+// barrier addresses are constants: the loop body is the multiply-accumulate and little else.
+template <bool SPLIT41, bool PACKED, int kMacP, int NST>
 __device__ __forceinline__ void mac4_consume(const unsigned char *ring, uint64_t *full, uint64_t *empty, int n_e, int nP,
-                                             u64 *const *outs, long long kN, const ModConst &mc, int nst,
-                                             unsigned stage_bytes, unsigned tb) {
+                                             u64 *const *outs, long long kN, const ModConst &mc) {
     using A = typename std::conditional<SPLIT41, AccG, Acc128>::type;
+    constexpr unsigned TB = PACKED ? 5u * 512u : 8u * 512u;   // bytes of one plaintext tile
+    constexpr unsigned SB = (unsigned)kMacP * TB + 2u * 4096u;  // bytes of one stage
     const double qd = (double)mc.q, qinv = 1.0 / qd;
     A a00[kMacP], a01[kMacP], a10[kMacP], a11[kMacP];
 #pragma unroll
     for (int j = 0; j < kMacP; j++) { a00[j].zero(); a01[j].zero(); a10[j].zero(); a11[j].zero(); }
     const int t = threadIdx.x;
-    int slot = 0;
-    unsigned phase = 0;
-    for (int s = 0; s < n_e; s++) {
-        mbar_wait(&full[slot], phase);
-        const unsigned char *stb = ring + (size_t)slot * stage_bytes;
-        const u64 *rt = reinterpret_cast<const u64 *>(stb + kMacP * tb);
-        const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(rt + 2 * t);
-        const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(rt + 512 + 2 * t);
+    const unsigned full0 = smem_u32(full), empty0 = smem_u32(empty);
+    const unsigned char *rt_t = ring + kMacP * TB + 16 * t;               // R tiles: c0, then c1 at +4096
+    const unsigned char *lo_t = ring + (PACKED ? 8 * t : 16 * t);        // plaintext words (low planes)
+    const unsigned char *hi_t = ring + 2048 + 2 * t;                      // packed high bytes
+    auto stage = [&](int slot, unsigned phase) {
+        mbar_wait_sa(full0 + 8u * slot, phase);
+        const unsigned off = (unsigned)slot * SB;
+        const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(rt_t + off);
+        const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(rt_t + off + 4096);
         if constexpr (SPLIT41) {
-            // convert each staged residue to a double once (R values are shared by the kMacP
+            // each staged residue converted to a double once (R values are shared by the kMacP
             // outputs, plaintext values by c0 and c1)
             const double R0x = AccF64::u2d(r0.x), R0y = AccF64::u2d(r0.y);
             const double R1x = AccF64::u2d(r1.x), R1y = AccF64::u2d(r1.y);
 #pragma unroll
             for (int j = 0; j < kMacP; j++) {
-                {  // unconditional (slot j >= nP holds stale data, its sums are never stored): no joins
-                    double Px, Py;
-                    if constexpr (PACKED) {  // high byte spliced under the 2^52 exponent with one PRMT
-                        const uint2 lo = *reinterpret_cast<const uint2 *>(reinterpret_cast<const uint32_t *>(stb + j * tb) + 2 * t);
-                        const unsigned hi = *(reinterpret_cast<const unsigned short *>(stb + j * tb + 2048) + t);
-                        Px = __dsub_rn(__hiloint2double((int)__byte_perm(hi, 0x43300000u, 0x7650), (int)lo.x), 4503599627370496.0);
-                        Py = __dsub_rn(__hiloint2double((int)__byte_perm(hi, 0x43300000u, 0x7651), (int)lo.y), 4503599627370496.0);
-                    } else {
-                        const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(stb + j * tb + 16 * t);
-                        Px = AccF64::u2d(pv.x);
-                        Py = AccF64::u2d(pv.y);
-                    }
-                    a00[j].macd(Px, R0x); a01[j].macd(Py, R0y);
-                    a10[j].macd(Px, R1x); a11[j].macd(Py, R1y);
+                // unconditional (slot j >= nP holds stale data, its sums are never stored): no joins
+                double Px, Py;
+                if constexpr (PACKED) {  // high byte spliced under the 2^52 exponent with one PRMT
+                    const uint2 lo = *reinterpret_cast<const uint2 *>(lo_t + off + j * TB);
+                    const unsigned hi = *reinterpret_cast<const unsigned short *>(hi_t + off + j * TB);
+                    Px = __dsub_rn(__hiloint2double((int)__byte_perm(hi, 0x43300000u, 0x7650), (int)lo.x), 4503599627370496.0);
+                    Py = __dsub_rn(__hiloint2double((int)__byte_perm(hi, 0x43300000u, 0x7651), (int)lo.y), 4503599627370496.0);
+                } else {
+                    const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(lo_t + off + j * TB);
+                    Px = AccF64::u2d(pv.x);
+                    Py = AccF64::u2d(pv.y);
                 }
+                a00[j].macd(Px, R0x); a01[j].macd(Py, R0y);
+                a10[j].macd(Px, R1x); a11[j].macd(Py, R1y);
             }
         } else {
 #pragma unroll
             for (int j = 0; j < kMacP; j++) {
                 if (j < nP) {
-                    const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(stb + j * tb + 16 * t);
+                    const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(lo_t + off + j * TB);
                     a00[j].mac(pv.x, r0.x); a01[j].mac(pv.y, r0.y);
                     a10[j].mac(pv.x, r1.x); a11[j].mac(pv.y, r1.y);
                 }
             }
         }
-        __syncwarp();
-        if ((t & 31) == 0) mbar_arrive(&empty[slot]);
-        if (++slot == nst) { slot = 0; phase ^= 1u; }
-        // Acc128: fold every 64 products (< 2^126); AccG: every 512 (s < 2^93, l < 2^48)
-        if ((!SPLIT41 && (s & 63) == 63) || (SPLIT41 && (s & 511) == 511)) {
+        // every consumer thread arrives (count kTB) once its own reads of the slot are done
+        mbar_arrive_sa(empty0 + 8u * slot);
+    };
+    auto fold = [&]() {
 #pragma unroll
-            for (int j = 0; j < kMacP; j++) {
-                accf(a00[j], mc, qd, qinv); accf(a01[j], mc, qd, qinv);
-                accf(a10[j], mc, qd, qinv); accf(a11[j], mc, qd, qinv);
-            }
+        for (int j = 0; j < kMacP; j++) {
+            accf(a00[j], mc, qd, qinv); accf(a01[j], mc, qd, qinv);
+            accf(a10[j], mc, qd, qinv); accf(a11[j], mc, qd, qinv);
         }
+    };
+    // folds at chunk boundaries (Acc128: every 64 products < 2^126; AccG: every 512, s < 2^93,
+    // l < 2^48); chunks are whole ring rounds, so stage s of a round uses slot s (constant)
+    constexpr int kFold = ((SPLIT41 ? 512 : 64) / NST) * NST;
+    const int n_full = n_e - n_e % NST;
+    unsigned phase = 0;
+    int s = 0;
+    while (s < n_full) {
+        const int s1 = n_full - s < kFold ? n_full : s + kFold;
+        for (; s < s1; s += NST) {
+#pragma unroll
+            for (int i = 0; i < NST; i++) stage(i, phase);
+            phase ^= 1u;
+        }
+        if (s < n_e && s % kFold == 0) fold();
     }
+    for (int i = 0; s < n_e; s++, i++) stage(i, phase);  // last partial round (< NST stages)
 #pragma unroll
     for (int j = 0; j < kMacP; j++) {
         if (j < nP) {
@@ -294,7 +312,7 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char
     if (threadIdx.x == 0) {
         for (int s = 0; s < nst; s++) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kTB / 32);
+            mbar_init(&empty[s], kTB);  // one arrival per consumer thread (mac4_consume)
         }
         mbar_fence_init();
     }
@@ -331,23 +349,9 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char
 #pragma unroll
     for (int j = 0; j < kMacP; j++) outs[j] = acc + (long long)(oa + (j < nP ? j : 0)) * 2 * kN + lx0;
     const ModConst &mc = pr.m[l];
-    if (w == 5) mac4_consume<true, true, kMacP>(ring, full, empty, n_e, nP, outs, kN, mc, nst, stage_bytes, tb);
-    else if (mc.q < (1ull << 41))
-        mac4_consume<true, false, kMacP>(ring, full, empty, n_e, nP, outs, kN, mc, nst, stage_bytes, tb);
-    else {
-#ifdef BLB_MAC_TIMING_SKIP60   // timing experiment only (wrong results): drain the 60-bit limb's ring
-        int slot = 0;
-        unsigned ph = 0;
-        for (int s = 0; s < n_e; s++) {
-            mbar_wait(&full[slot], ph);
-            __syncwarp();
-            if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot]);
-            if (++slot == nst) { slot = 0; ph ^= 1u; }
-        }
-#else
-        mac4_consume<false, false, kMacP>(ring, full, empty, n_e, nP, outs, kN, mc, nst, stage_bytes, tb);
-#endif
-    }
+    if (w == 5) mac4_consume<true, true, kMacP, kM4StagesP>(ring, full, empty, n_e, nP, outs, kN, mc);
+    else if (mc.q < (1ull << 41)) mac4_consume<true, false, kMacP, kM4Stages>(ring, full, empty, n_e, nP, outs, kN, mc);
+    else mac4_consume<false, false, kMacP, kM4Stages>(ring, full, empty, n_e, nP, outs, kN, mc);
 }
 
 template <int PP, int STG, int MINB, int STGP = STG>
@@ -391,35 +395,58 @@ constexpr int kMjStages = 3;
 template <int JG>
 constexpr size_t macj_smem() { return (size_t)kMjStages * (1 + 2 * JG) * 512 * 8 + 2 * kMjStages * 8; }
 
-// SPLIT41 (q < 2^41): AccG for all four accumulators; else Acc128
+// SPLIT41 (q < 2^41): AccG for all four accumulators; else Acc128.  Ring slots are compile-time in the
+// stage loop (unrolled by kMjStages), as in mac4_consume.
 template <bool SPLIT41, int JG>
 __device__ __forceinline__ void macj_consume(const u64 *ring, uint64_t *full, uint64_t *empty, int n_e, u64 *const *outs,
                                              long long kN, const ModConst &mc) {
     using A = typename std::conditional<SPLIT41, AccG, Acc128>::type;
-    using A1 = A;
+    constexpr int NST = kMjStages;
     const double qd = (double)mc.q, qinv = 1.0 / qd;
-    A a00[JG], a01[JG];
-    A1 a10[JG], a11[JG];
+    A a00[JG], a01[JG], a10[JG], a11[JG];
 #pragma unroll
     for (int j = 0; j < JG; j++) { a00[j].zero(); a01[j].zero(); a10[j].zero(); a11[j].zero(); }
     constexpr int kStageWords = (1 + 2 * JG) * 512;
     const int t = threadIdx.x;
-    for (int s = 0; s < n_e; s++) {
-        const int slot = s % kMjStages;
-        mbar_wait(&full[slot], (s / kMjStages) & 1);
-        const u64 *st = ring + (size_t)slot * kStageWords;
-        const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(st + 2 * t);
+    const unsigned full0 = smem_u32(full), empty0 = smem_u32(empty);
+    const u64 *ring_t = ring + 2 * t;
+    auto stage = [&](int slot, unsigned phase) {
+        mbar_wait_sa(full0 + 8u * slot, phase);
+        const u64 *st = ring_t + slot * kStageWords;
+        const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(st);
+        if constexpr (SPLIT41) {
+            const double Px = AccF64::u2d(pv.x), Py = AccF64::u2d(pv.y);
 #pragma unroll
-        for (int j = 0; j < JG; j++) {
-            const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + (1 + 2 * j) * 512 + 2 * t);
-            const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + (2 + 2 * j) * 512 + 2 * t);
-            accm(a00[j], pv.x, r0.x, qd, qinv); accm(a01[j], pv.y, r0.y, qd, qinv);
-            accm(a10[j], pv.x, r1.x, qd, qinv); accm(a11[j], pv.y, r1.y, qd, qinv);
+            for (int j = 0; j < JG; j++) {
+                const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + (1 + 2 * j) * 512);
+                const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + (2 + 2 * j) * 512);
+                a00[j].macd(Px, AccF64::u2d(r0.x)); a01[j].macd(Py, AccF64::u2d(r0.y));
+                a10[j].macd(Px, AccF64::u2d(r1.x)); a11[j].macd(Py, AccF64::u2d(r1.y));
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < JG; j++) {
+                const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + (1 + 2 * j) * 512);
+                const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + (2 + 2 * j) * 512);
+                a00[j].mac(pv.x, r0.x); a01[j].mac(pv.y, r0.y);
+                a10[j].mac(pv.x, r1.x); a11[j].mac(pv.y, r1.y);
+            }
         }
-        __syncwarp();
-        if ((t & 31) == 0) mbar_arrive(&empty[slot]);
-        // Acc128: 64 products < 2^126; AccG: 512 products
-        if ((!SPLIT41 && (s & 63) == 63) || (SPLIT41 && (s & 511) == 511)) {
+        mbar_arrive_sa(empty0 + 8u * slot);  // count kTB: every consumer thread, after its own reads
+    };
+    // folds after whole ring rounds: Acc128 <= 64 products (< 2^126), AccG <= 512 (s < 2^93, l < 2^48)
+    constexpr int kFold = ((SPLIT41 ? 512 : 64) / NST) * NST;
+    const int n_full = n_e - n_e % NST;
+    unsigned phase = 0;
+    int s = 0;
+    while (s < n_full) {
+        const int s1 = n_full - s < kFold ? n_full : s + kFold;
+        for (; s < s1; s += NST) {
+#pragma unroll
+            for (int i = 0; i < NST; i++) stage(i, phase);
+            phase ^= 1u;
+        }
+        if (s < n_e && s % kFold == 0) {
 #pragma unroll
             for (int j = 0; j < JG; j++) {
                 accf(a00[j], mc, qd, qinv); accf(a01[j], mc, qd, qinv);
@@ -427,6 +454,7 @@ __device__ __forceinline__ void macj_consume(const u64 *ring, uint64_t *full, ui
             }
         }
     }
+    for (int i = 0; s < n_e; s++, i++) stage(i, phase);  // last partial round
 #pragma unroll
     for (int j = 0; j < JG; j++) {
         u64 *out = outs[j] + 2 * t;
@@ -460,7 +488,7 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_j(const u64 *__restrict_
     if (threadIdx.x == 0) {
         for (int s = 0; s < kMjStages; s++) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kTB / 32);
+            mbar_init(&empty[s], kTB);  // one arrival per consumer thread (macj_consume)
         }
         mbar_fence_init();
     }
