@@ -397,6 +397,8 @@ struct RowBatch {
     // optional limb selection (N = 2^16 kernels): nsel > 0 -> rows = n_polys * nsel, row -> limb sel[row % nsel]
     int nsel = 0;
     int sel[BLB_MAXP];
+    // N = 2^16 kernels: polynomial index of grid row 0 (a launch over a chunk of the batch's polys)
+    int p0 = 0;
 };
 blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cudaStream_t st);
 

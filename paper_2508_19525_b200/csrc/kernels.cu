@@ -454,6 +454,148 @@ k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, int np, int K, i
     else ks_inner_body<BETA, EXT, false>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi, ds);
 }
 
+// Bulk-staged key-switch inner product (the default for 1 <= beta <= 6).  A CTA owns a tile of
+// kKsTile coefficients x of limb m for the jobs of one key group.  Thread 0 issues every input the
+// tile needs -- the 2 beta key rows, the group's beta digit rows per job, the jobs' c0 / c1 rows -- as
+// 1 KB cp.async.bulk copies into shared memory on one mbarrier, so a CTA keeps all of its ~38 KB in
+// flight at once (the per-thread load version was bound by the loads its 64 registers could hold:
+// long-scoreboard stalls first, 0.3 of HBM).  The products then run from shared memory one job at a
+// time: AccG (FP64 pipe) on primes < 2^41, Acc60 on the 60-bit ones; same sums, additive P c term
+// and scattered stores as ks_inner_body.
+#ifndef BLB_KS_TILE
+#define BLB_KS_TILE 128
+#endif
+constexpr int kKsTile = BLB_KS_TILE;  // coefficients per CTA
+template <int BETA>
+__host__ __device__ constexpr int ks_bulk_words(int T) { return (2 * BETA + kKsGroup * BETA + 2 * kKsGroup) * T; }
+template <int BETA, bool EXT>
+__global__ void __launch_bounds__(kKsTile) k_ks_bulk(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, int np,
+                                                     int K, int logN, PinvTab pq) {
+    extern __shared__ __align__(16) u64 ksm[];
+    __shared__ uint64_t bar;
+    const int N = 1 << logN, T = blockDim.x;
+    const int gi = blockIdx.x % grp.n;
+    const int x0 = (blockIdx.x / grp.n) * T;
+    const int m = blockIdx.y;
+    const int t0 = grp.start[gi], cnt = grp.start[gi + 1] - t0;
+    const int E = k + np, Lk = K + np;
+    const int pm = m < k ? m : K + (m - k);
+    u64 *skey = ksm;                          // [2 BETA][T]: (j, b) -> 2 j + b
+    u64 *sdig = ksm + 2 * BETA * T;           // [kKsGroup][BETA][T]
+    u64 *sc = sdig + kKsGroup * BETA * T;     // [kKsGroup][2][T]: c0, c1
+    const KsJob &J0 = jobs.j[t0];
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        // warp 0 issues the copies, one per lane at a time (lane 0 first registers the byte count)
+        const unsigned tb = (unsigned)T * 8u;
+        const int lane = threadIdx.x;
+        const int nk = 2 * BETA, nd = cnt * BETA;
+        int nc = 0;  // c0 / c1 rows present, in job order
+        uint32_t cmask = 0;
+        for (int q = 0; q < cnt; q++) {
+            const KsJob &J = jobs.j[t0 + q];
+            if (m < k && (EXT || J.add_mode != 0)) { cmask |= 1u << (2 * q); nc++; }
+            if (m < k && J.c1_add && (EXT || J.add_mode == 2)) { cmask |= 1u << (2 * q + 1); nc++; }
+        }
+        if (lane == 0) mbar_expect_tx(&bar, (unsigned)(nk + nd + nc) * tb);
+        __syncwarp();
+        for (int c = lane; c < nk + nd + nc; c += 32) {
+            if (c < nk) {
+                const int j = c >> 1, b = c & 1;
+                bulk_g2s(skey + c * T, J0.key + (((long long)j * 2 + b) * Lk + pm) * N + x0, tb, &bar);
+            } else if (c < nk + nd) {
+                const int q = (c - nk) / BETA, j = (c - nk) - q * BETA;
+                bulk_g2s(sdig + (q * BETA + j) * T, jobs.j[t0 + q].ext + ((long long)j * E + m) * N + x0, tb, &bar);
+            } else {
+                int r = c - nk - nd, slot = 0;  // the r-th set bit of cmask
+                for (uint32_t mm = cmask;; mm &= mm - 1) {
+                    slot = __ffs(mm) - 1;
+                    if (r-- == 0) break;
+                }
+                const KsJob &J = jobs.j[t0 + (slot >> 1)];
+                bulk_g2s(sc + slot * T, ((slot & 1) ? J.c1_add : J.c0) + (long long)m * N + x0, tb, &bar);
+            }
+        }
+    }
+    const int x = x0 + threadIdx.x;
+    const uint32_t dst = J0.galois == 1 ? (uint32_t)x : galois_perm(x, J0.galois_inv, logN);
+    const ModConst &mc = pr.m[pm];
+    const bool small = mc.q < (1ull << 41);
+    mbar_wait(&bar, 0);
+    auto store = [&](int q, u64 r0, u64 r1) {
+        const int t = t0 + q;
+        if (EXT) {
+            const KsJob &J = jobs.j[t];
+            J.out[(long long)m * N + dst] = r0;
+            J.out[((long long)E + m) * N + dst] = r1;
+        } else {
+            u[(((long long)t * 2 + 0) * E + m) * N + dst] = r0;
+            u[(((long long)t * 2 + 1) * E + m) * N + dst] = r1;
+        }
+    };
+    // an absent c0 / c1 row contributes 0 (its slot was not filled)
+    auto cval = [&](int q, int b) -> u64 {
+        const KsJob &J = jobs.j[t0 + q];
+        const bool has = b == 0 ? (EXT || J.add_mode != 0) : (J.c1_add && (EXT || J.add_mode == 2));
+        return has ? sc[(2 * q + b) * T + threadIdx.x] : 0ull;
+    };
+    if (small) {
+        const double qd = (double)mc.q, qinv = 1.0 / qd;
+        double kb[BETA], ka[BETA];
+#pragma unroll
+        for (int j = 0; j < BETA; j++) {
+            kb[j] = AccF64::u2d(skey[(2 * j) * T + threadIdx.x]);
+            ka[j] = AccF64::u2d(skey[(2 * j + 1) * T + threadIdx.x]);
+        }
+        const double pc = m < k ? AccF64::u2d(pq.v[m]) : 0.0;
+#pragma unroll 1
+        for (int q = 0; q < cnt; q++) {
+            AccG a0, a1;
+            a0.zero();
+            a1.zero();
+#pragma unroll
+            for (int j = 0; j < BETA; j++) {
+                const double e = AccF64::u2d(sdig[(q * BETA + j) * T + threadIdx.x]);
+                a0.macd(e, kb[j]);
+                a1.macd(e, ka[j]);
+            }
+            if (m < k) {
+                a0.macd(AccF64::u2d(cval(q, 0)), pc);
+                a1.macd(AccF64::u2d(cval(q, 1)), pc);
+            }
+            store(q, a0.reduce(qd, qinv), a1.reduce(qd, qinv));
+        }
+    } else {
+        u64 kb[BETA], ka[BETA];
+#pragma unroll
+        for (int j = 0; j < BETA; j++) {
+            kb[j] = skey[(2 * j) * T + threadIdx.x];
+            ka[j] = skey[(2 * j + 1) * T + threadIdx.x];
+        }
+#pragma unroll 1
+        for (int q = 0; q < cnt; q++) {
+            Acc60 a0, a1;  // <= BETA + 1 <= 7 products
+            a0.zero();
+            a1.zero();
+#pragma unroll
+            for (int j = 0; j < BETA; j++) {
+                const u64 e = sdig[(q * BETA + j) * T + threadIdx.x];
+                a0.mac(e, kb[j]);
+                a1.mac(e, ka[j]);
+            }
+            if (m < k) {
+                a0.mac(cval(q, 0), pq.v[m]);
+                a1.mac(cval(q, 1), pq.v[m]);
+            }
+            store(q, a0.reduce(mc), a1.reduce(mc));
+        }
+    }
+}
+
 // conv[t][b][i][x] = FastBConv_{P -> q_i}(INTT(u_P))   (u P-rows already INTT'd)
 __global__ void k_bconv_moddown(const u64 *u, u64 *conv, const u64 *tb, Primes pr, int k, int np, int K, int N) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -753,8 +895,27 @@ static blb_status ks_inner_launch(const blb_params *P, int level, const KsJobs &
         pq.sh[i] = blbh_shoup_dev_table(P, i);
     }
     cudaEvent_t t0 = blb_timing_begin(st);
+#ifndef BLB_KS_BULK
+#define BLB_KS_BULK 1
+#endif
+    const int T = N < kKsTile ? N : kKsTile;
+    const dim3 gb((unsigned)((N / T) * G.n), E);
+    bool done = BLB_KS_BULK && beta >= 1 && beta <= 6;
+    if (done) {
+        switch (beta) {
+#define KSB(B)                                                                                               \
+    case B: {                                                                                                \
+        const size_t sm = (size_t)ks_bulk_words<B>(T) * 8;                                                    \
+        if (sm > 48 * 1024) blb_smem_optin(k_ks_bulk<B, EXT>, sm);                                            \
+        k_ks_bulk<B, EXT><<<gb, T, sm, st>>>(J, G, u, P->pr, k, np, P->K, P->logN, pq);                       \
+        break;                                                                                               \
+    }
+            KSB(1) KSB(2) KSB(3) KSB(4) KSB(5) KSB(6)
+#undef KSB
+        }
+    }
     const dim3 gks((unsigned)(((N + kTB - 1) / kTB) * G.n), E);
-    switch (beta) {
+    if (!done) switch (beta) {
         case 1: k_ks_inner<1, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
         case 2: k_ks_inner<2, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
         case 3: k_ks_inner<3, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
