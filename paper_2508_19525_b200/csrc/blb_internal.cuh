@@ -397,8 +397,6 @@ struct RowBatch {
     // optional limb selection (N = 2^16 kernels): nsel > 0 -> rows = n_polys * nsel, row -> limb sel[row % nsel]
     int nsel = 0;
     int sel[BLB_MAXP];
-    // N = 2^16 kernels: polynomial index of grid row 0 (a launch over a chunk of the batch's polys)
-    int p0 = 0;
 };
 blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cudaStream_t st);
 
@@ -429,6 +427,9 @@ struct KsJob {
     uint32_t galois;  // 1 = identity
     uint32_t galois_inv;  // g^{-1} mod 2N (filled by the key-switch launcher)
     int add_mode;     // 0 = none, 1 = add sigma_g(c0) to out0 (rotation), 2 = add c0 / c1 pair (relin)
+    // 1: limbs whose prime is < 2^41 are written as the bits of the residue as a double (the weight
+    // MAC's baby-step buffer R: its FP64 accumulators then read R without a conversion)
+    int out_f64;
     const u64 *c1_add;
 };
 blb_status launch_keyswitch(const blb_params *P, int level, const KsJob *jobs, int n_jobs, u64 *u_scratch,

@@ -472,7 +472,7 @@ template <int BETA, bool EXT>
 __global__ void __launch_bounds__(kKsTile) k_ks_bulk(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, int np,
                                                      int K, int logN, PinvTab pq) {
     extern __shared__ __align__(16) u64 ksm[];
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar[kKsGroup];  // bar[q]: job q's rows (and, for q = 0, the key rows)
     const int N = 1 << logN, T = blockDim.x;
     const int gi = blockIdx.x % grp.n;
     const int x0 = (blockIdx.x / grp.n) * T;
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(kKsTile) k_ks_bulk(KsJobs jobs, KsGroups grp, 
     u64 *sc = sdig + kKsGroup * BETA * T;     // [kKsGroup][2][T]: c0, c1
     const KsJob &J0 = jobs.j[t0];
     if (threadIdx.x == 0) {
-        mbar_init(&bar, 1);
+        for (int q = 0; q < kKsGroup; q++) mbar_init(&bar[q], 1);
         mbar_fence_init();
     }
     __syncthreads();
@@ -501,23 +501,31 @@ __global__ void __launch_bounds__(kKsTile) k_ks_bulk(KsJobs jobs, KsGroups grp, 
             if (m < k && (EXT || J.add_mode != 0)) { cmask |= 1u << (2 * q); nc++; }
             if (m < k && J.c1_add && (EXT || J.add_mode == 2)) { cmask |= 1u << (2 * q + 1); nc++; }
         }
-        if (lane == 0) mbar_expect_tx(&bar, (unsigned)(nk + nd + nc) * tb);
+        if (lane < cnt) {  // lane q registers job q's bytes (job 0 also carries the keys)
+            const int q = lane;
+            const int ncq = ((cmask >> (2 * q)) & 1) + ((cmask >> (2 * q + 1)) & 1);
+            mbar_expect_tx(&bar[q], (unsigned)((q == 0 ? nk : 0) + BETA + ncq) * tb);
+        }
         __syncwarp();
+        // job-major copy order (keys, then each job's digit and c rows), so job 0 lands first
         for (int c = lane; c < nk + nd + nc; c += 32) {
             if (c < nk) {
                 const int j = c >> 1, b = c & 1;
-                bulk_g2s(skey + c * T, J0.key + (((long long)j * 2 + b) * Lk + pm) * N + x0, tb, &bar);
-            } else if (c < nk + nd) {
-                const int q = (c - nk) / BETA, j = (c - nk) - q * BETA;
-                bulk_g2s(sdig + (q * BETA + j) * T, jobs.j[t0 + q].ext + ((long long)j * E + m) * N + x0, tb, &bar);
+                bulk_g2s(skey + c * T, J0.key + (((long long)j * 2 + b) * Lk + pm) * N + x0, tb, &bar[0]);
+                continue;
+            }
+            int r = c - nk, q = 0;
+            for (;; q++) {
+                const int nq = BETA + ((cmask >> (2 * q)) & 1) + ((cmask >> (2 * q + 1)) & 1);
+                if (r < nq) break;
+                r -= nq;
+            }
+            const KsJob &J = jobs.j[t0 + q];
+            if (r < BETA) {
+                bulk_g2s(sdig + (q * BETA + r) * T, J.ext + ((long long)r * E + m) * N + x0, tb, &bar[q]);
             } else {
-                int r = c - nk - nd, slot = 0;  // the r-th set bit of cmask
-                for (uint32_t mm = cmask;; mm &= mm - 1) {
-                    slot = __ffs(mm) - 1;
-                    if (r-- == 0) break;
-                }
-                const KsJob &J = jobs.j[t0 + (slot >> 1)];
-                bulk_g2s(sc + slot * T, ((slot & 1) ? J.c1_add : J.c0) + (long long)m * N + x0, tb, &bar);
+                const int slot = (r == BETA && ((cmask >> (2 * q)) & 1)) ? 2 * q : 2 * q + 1;
+                bulk_g2s(sc + slot * T, ((slot & 1) ? J.c1_add : J.c0) + (long long)m * N + x0, tb, &bar[q]);
             }
         }
     }
@@ -525,7 +533,7 @@ __global__ void __launch_bounds__(kKsTile) k_ks_bulk(KsJobs jobs, KsGroups grp, 
     const uint32_t dst = J0.galois == 1 ? (uint32_t)x : galois_perm(x, J0.galois_inv, logN);
     const ModConst &mc = pr.m[pm];
     const bool small = mc.q < (1ull << 41);
-    mbar_wait(&bar, 0);
+    mbar_wait(&bar[0], 0);  // keys + job 0
     auto store = [&](int q, u64 r0, u64 r1) {
         const int t = t0 + q;
         if (EXT) {
@@ -554,6 +562,7 @@ __global__ void __launch_bounds__(kKsTile) k_ks_bulk(KsJobs jobs, KsGroups grp, 
         const double pc = m < k ? AccF64::u2d(pq.v[m]) : 0.0;
 #pragma unroll 1
         for (int q = 0; q < cnt; q++) {
+            if (q > 0) mbar_wait(&bar[q], 0);
             AccG a0, a1;
             a0.zero();
             a1.zero();
@@ -578,6 +587,7 @@ __global__ void __launch_bounds__(kKsTile) k_ks_bulk(KsJobs jobs, KsGroups grp, 
         }
 #pragma unroll 1
         for (int q = 0; q < cnt; q++) {
+            if (q > 0) mbar_wait(&bar[q], 0);
             Acc60 a0, a1;  // <= BETA + 1 <= 7 products
             a0.zero();
             a1.zero();
@@ -637,6 +647,7 @@ __global__ void k_ks_combine(KsJobs jobs, const u64 *u, const u64 *conv, PinvTab
         const u64 *c = b == 0 ? J.c0 : J.c1_add;
         r = addmod(r, c[(long long)i * N + x], q);
     }
+    if (J.out_f64 && q < (1ull << 41)) r = (u64)__double_as_longlong((double)r);
     J.out[((long long)b * k + i) * N + x] = r;
 }
 

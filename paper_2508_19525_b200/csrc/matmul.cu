@@ -212,13 +212,12 @@ __device__ __forceinline__ void mac4_consume(const unsigned char *ring, uint64_t
     auto stage = [&](int slot, unsigned phase) {
         mbar_wait_sa(full0 + 8u * slot, phase);
         const unsigned off = (unsigned)slot * SB;
-        const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(rt_t + off);
-        const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(rt_t + off + 4096);
         if constexpr (SPLIT41) {
-            // each staged residue converted to a double once (R values are shared by the kMacP
-            // outputs, plaintext values by c0 and c1)
-            const double R0x = AccF64::u2d(r0.x), R0y = AccF64::u2d(r0.y);
-            const double R1x = AccF64::u2d(r1.x), R1y = AccF64::u2d(r1.y);
+            // R limbs below 2^41 are stored as doubles by their producers (KsJob::out_f64,
+            // k_copy_ct_f64); plaintext values are converted once (shared by c0 and c1)
+            const double2 r0 = *reinterpret_cast<const double2 *>(rt_t + off);
+            const double2 r1 = *reinterpret_cast<const double2 *>(rt_t + off + 4096);
+            const double R0x = r0.x, R0y = r0.y, R1x = r1.x, R1y = r1.y;
 #pragma unroll
             for (int j = 0; j < kMacP; j++) {
                 // unconditional (slot j >= nP holds stale data, its sums are never stored): no joins
@@ -237,6 +236,8 @@ __device__ __forceinline__ void mac4_consume(const unsigned char *ring, uint64_t
                 a10[j].macd(Px, R1x); a11[j].macd(Py, R1y);
             }
         } else {
+            const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(rt_t + off);
+            const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(rt_t + off + 4096);
 #pragma unroll
             for (int j = 0; j < kMacP; j++) {
                 if (j < nP) {
@@ -541,9 +542,13 @@ __global__ void k_accumulate(AccJobs jobs, Primes pr, int k, int N, int kq, int 
     for (int j = 0; j < jobs.n; j++) jobs.dst[j][off] = addmod(jobs.dst[j][off], jobs.src[j][off], q);
 }
 
-__global__ void k_copy_ct(const u64 *src, u64 *dst, long long n) {
+// R[b][0] = X_b in the baby-step buffer's format: limbs with q < 2^41 as double bits (KsJob::out_f64)
+__global__ void k_copy_ct_f64(const u64 *src, u64 *dst, Primes pr, int k, int logN) {
     const long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (x < n) dst[x] = src[x];
+    if (x >= (2ll * k) << logN) return;
+    const int l = (int)((x >> logN) % k);
+    const u64 v = src[x];
+    dst[x] = pr.m[l].q < (1ull << 41) ? (u64)__double_as_longlong((double)v) : v;
 }
 }  // namespace
 
@@ -965,8 +970,8 @@ static blb_status mm_acc(const blb_matmul_plan *pl, const blb_keys *keys, const 
             BLB_TRY(launch_modup(P, level, c1.data() + b0, cnt, ext_in + (size_t)b0 * beta * E * N, coef, st));
         }
         for (int b = 0; b < n_in && win0; b++) {
-            k_copy_ct<<<(unsigned)((ctN + kTB - 1) / kTB), kTB, 0, st>>>(in[b].data, R + (size_t)b * pl->B * ctN,
-                                                                        (long long)ctN);
+            k_copy_ct_f64<<<(unsigned)((ctN + kTB - 1) / kTB), kTB, 0, st>>>(in[b].data, R + (size_t)b * pl->B * ctN,
+                                                                            P->pr, k, P->logN);
             BLB_COUNT_LAUNCH(1);
         }
     }
@@ -985,6 +990,7 @@ static blb_status mm_acc(const blb_matmul_plan *pl, const blb_keys *keys, const 
                 J.out = R + ((size_t)b * pl->B + i) * ctN;
                 J.galois = blb_galois_element(P, i * pl->L);
                 J.add_mode = 1;
+                J.out_f64 = 1;
                 jobs.push_back(J);
             }
         for (size_t j0 = 0; j0 < jobs.size(); j0 += kMaxJobs) {

@@ -117,10 +117,17 @@ __device__ __forceinline__ int swz(int col, int mid) { return (col << 8) | (mid 
 // Integer butterflies with the truncated-quotient Shoup product (shoup_lazy4, result in [0, 4q)):
 // forward values stay in [0, 8q) (X is brought below 4q, X + t < 8q, X - t + 4q in (0, 8q)),
 // inverse values in [0, 4q); 8q < 2^64 for every prime < 2^61.
-template <bool INV>
+// LZ forward (primes < 2^60, so 16q <= 2^64): X is corrected only on every other stage, by 8q:
+// a stage adds < 4q to the bound, so inputs < 12q -> outputs < 16q -> (corrected X < 8q) -> < 12q.
+// MODE: 0 = no correction, 1 = X >= 8q -> X - 8q, 2 = X >= 4q -> X - 4q.
+template <bool INV, int MODE = 2>
 __device__ __forceinline__ void bfly(u64 &X, u64 &Y, u64 w, u64 wsh, u64 q, u64 q4) {
     if (!INV) {
-        if (X >= q4) X -= q4;
+        if constexpr (MODE == 2) {
+            if (X >= q4) X -= q4;
+        } else if constexpr (MODE == 1) {
+            if (X >= 2 * q4) X -= 2 * q4;
+        }
         const u64 t = shoup_lazy4(Y, w, wsh, q);
         Y = X - t + q4;
         X = X + t;
@@ -138,6 +145,11 @@ __device__ __forceinline__ u64 canon8(u64 x, u64 q) {
     if (x >= 2 * q) x -= 2 * q;
     if (x >= q) x -= q;
     return x;
+}
+// [0, 16q) -> [0, q)
+__device__ __forceinline__ u64 canon16(u64 x, u64 q) {
+    if (x >= 8 * q) x -= 8 * q;
+    return canon8(x, q);
 }
 
 // ---------------------------------------------------------------------------
@@ -195,7 +207,7 @@ __device__ __forceinline__ void bfly_f64(double &X, double &Y, double w, double 
 #ifndef BLB_NTT_MINB
 #define BLB_NTT_MINB 3
 #endif
-template <bool INV, bool STRIDED, int PRO, int EPI, bool SMALL>
+template <bool INV, bool STRIDED, int PRO, int EPI, bool SMALL, bool LZ = false>
 __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u64 *__restrict__ tw_all,
                                            const double *__restrict__ twd_all, const Primes &pr, int, int,
                                            const NttFuse &fz, int p, int l) {
@@ -289,7 +301,12 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
                 bfly_f64<INV>(v[m], v[m + dist], twd[widx], qd, qinv);
             } else {
                 const ulonglong2 tv = twp[widx];
-                bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q4);
+                if (LZ && !INV) {
+                    if (r & 1) bfly<INV, 1>(v[m], v[m + dist], tv.x, tv.y, q, q4);
+                    else bfly<INV, 0>(v[m], v[m + dist], tv.x, tv.y, q, q4);
+                } else {
+                    bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q4);
+                }
             }
         }
     };
@@ -304,7 +321,12 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
                 bfly_f64<INV>(v[m], v[m + dist], twd[widx], qd, qinv);
             } else {
                 const ulonglong2 tv = twp[widx];
-                bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q4);
+                if (LZ && !INV) {
+                    if (r & 1) bfly<INV, 1>(v[m], v[m + dist], tv.x, tv.y, q, q4);
+                    else bfly<INV, 0>(v[m], v[m + dist], tv.x, tv.y, q, q4);
+                } else {
+                    bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q4);
+                }
             }
         }
     };
@@ -350,7 +372,7 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
         for (int m = 0; m < 16; m++) {
             u64 x;
             if constexpr (SMALL) x = canon(v[m], qd, qinv);
-            else x = canon8(v[m], q);
+            else x = LZ ? canon16(v[m], q) : canon8(v[m], q);
             const int mid = tcA + 16 * m;
             const uint32_t gx = (uint32_t)((c0 + colA) << 8) + mid;
             u64 r = shoup(uv[m] + q - x, pv, psh, q);
@@ -360,6 +382,9 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
             } else if (J.add_mode == 2) {
                 const u64 *c = b == 0 ? J.c0 : J.c1_add;
                 r = addmod(r, c[(long long)l * N + gx], q);
+            }
+            if constexpr (SMALL) {
+                if (J.out_f64) r = (u64)__double_as_longlong(u2d(r));
             }
             out[gx] = r;
         }
@@ -374,7 +399,7 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
                 x = v[m];
                 if (last) {
                     if (!INV) {
-                        x = canon8(x, q);
+                        x = LZ ? canon16(x, q) : canon8(x, q);
                     } else {
                         x = shoup_lazy(x, mc.ninv, mc.ninv_sh, q);
                         if (x >= q) x -= q;
@@ -397,7 +422,6 @@ __device__ __forceinline__ bool ntt16_row(const RowBatch &rb, int &p, int &l) {
         p = row / rb.limbs;
         l = row - p * rb.limbs;
     }
-    p += rb.p0;
     if (rb.skip_alpha) {
         const int dig = p % rb.skip_beta;
         if (l < rb.skip_kmax && l >= dig * rb.skip_alpha && l < (dig + 1) * rb.skip_alpha) return false;
@@ -422,7 +446,7 @@ __device__ __forceinline__ void copy_own_tile(const RowBatch &rb, const NttFuse 
 #endif
 // integer (Shoup) kernel for the primes >= 2^41, FP64 kernel for the others; a launch covers
 // rows of one kind (launch_ntt splits a mixed batch with RowBatch::sel)
-template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0>
+template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0, bool LZ = false>
 __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_int(RowBatch rb, const u64 *__restrict__ tw_all,
                                                                 const double *__restrict__ twd, Primes pr, int s0,
                                                                 int last, const NttFuse fz) {
@@ -432,7 +456,7 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_int(RowBatch rb, cons
         if (PRO == 1 && STRIDED) copy_own_tile(rb, fz, p, l);
         return;
     }
-    ntt16_body<INV, STRIDED, PRO, EPI, false>(sm, rb, tw_all, twd, pr, s0, last, fz, p, l);
+    ntt16_body<INV, STRIDED, PRO, EPI, false, LZ>(sm, rb, tw_all, twd, pr, s0, last, fz, p, l);
 }
 template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0>
 __global__ void __launch_bounds__(256, BLB_NTT_F64_MINB) ntt16_f64(RowBatch rb, const u64 *__restrict__ tw_all,
@@ -447,306 +471,27 @@ __global__ void __launch_bounds__(256, BLB_NTT_F64_MINB) ntt16_f64(RowBatch rb, 
     ntt16_body<INV, STRIDED, PRO, EPI, true>(sm, rb, tw_all, twd, pr, s0, last, fz, p, l);
 }
 
-// ---------------------------------------------------------------------------
-// N = 2^16 single-pass NTT on a 16-CTA thread-block cluster (one cluster per limb, DSMEM exchange).
-// CTA c (cluster rank = blockIdx.x) of the cluster of row (p, l):
-//   R0  stages 0..3   thread t holds j = lo + 4096 m (lo = 256 c + t, m = 0..15): the 16-point
-//       transforms over the top 4 index bits, straight from the coalesced global load;
-//   --  DSMEM all-to-all: v[m] goes to CTA m, so that CTA c then owns the contiguous block
-//       [4096 c, 4096 c + 4096) -- the remaining 12 stages never leave it;
-//   R1  stages 4..7   o = t + 256 m within the block;
-//   R2  stages 8..11  and R3 stages 12..15: the contiguous pass of ntt16_body (A / B mappings,
-//       swizzled shared-memory exchanges, 256-blocks h = 16 c + col), then the coalesced store.
-// The inverse runs the same rounds backwards (contiguous load, R3..R1, DSMEM, R0, strided store).
-// Each residue is read from and written to global memory once (ntt16_body's two passes: twice);
-// the shared-memory traffic is the same four exchanges.  Twiddle index of stage s for element j:
-// (1 << s) + (j >> (16 - s)).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t cl_mapa(uint32_t saddr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-    return r;
+// integer-kernel launch: forward rows whose primes are all < 2^60 take the LZ butterflies
+static bool rb_below60(const blb_params *P, const RowBatch &r) {
+    const int nl = r.nsel ? r.nsel : r.limbs;
+    for (int i = 0; i < nl; i++)
+        if (P->mod[r.prime[r.nsel ? r.sel[i] : i]] >= (1ull << 60)) return false;
+    return true;
 }
-__device__ __forceinline__ void cl_st64(uint32_t addr, u64 v) {
-    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
-}
-__device__ __forceinline__ void cl_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
-__device__ __forceinline__ void cl_arrive_release() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
-__device__ __forceinline__ void cl_wait_acquire() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
-
-template <bool INV, int PRO, int EPI, bool SMALL>
-__device__ __forceinline__ void ntt_cl16_body(u64 *sm, const RowBatch &rb, const u64 *__restrict__ tw_all,
-                                              const double *__restrict__ twd_all, const Primes &pr,
-                                              const NttFuse &fz, int p, int l) {
-    constexpr int logN = 16, N = 1 << logN;
-    u64 *a = rb.base + (long long)p * rb.poly_stride + (long long)(rb.limb0 + l) * N;
-    const int pi = rb.prime[l];
-    const u64 q = pr.m[pi].q, q4 = 4 * q;
-    const ulonglong2 *twp = reinterpret_cast<const ulonglong2 *>(tw_all + (size_t)pi * 4 * N + (INV ? 2 * N : 0));
-    const double *twd = twd_all + (size_t)pi * 2 * N + (INV ? N : 0);
-    const int t = threadIdx.x;
-    const int c = blockIdx.x;        // cluster rank
-    const int c0 = c * 16;           // first 256-block of the CTA's contiguous 4096-block
-    const int lo = 256 * c + t;      // R0: j = lo + 4096 m
-    const int colA = t >> 4, tcA = t & 15, colB = t >> 4, tcB = t & 15;
-    const int hA = c0 + colA, hB = c0 + colB;
-    using V = typename std::conditional<SMALL, double, u64>::type;
-    const double qd = (double)q, qinv = 1.0 / qd;
-    V v[16];
-    auto from_u64 = [&](u64 x) -> V {
-        if constexpr (SMALL) return u2d(x);
-        else return x;
-    };
-    auto to_bits = [&](V x) -> u64 {
-        if constexpr (SMALL) return (u64)__double_as_longlong(x);
-        else return x;
-    };
-    auto from_bits = [&](u64 x) -> V {
-        if constexpr (SMALL) return __longlong_as_double((long long)x);
-        else return x;
-    };
-    auto bf = [&](int m, int dist, int widx) {
-        if constexpr (SMALL) {
-            bfly_f64<INV>(v[m], v[m + dist], twd[widx], qd, qinv);
-        } else {
-            const ulonglong2 tv = twp[widx];
-            bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q4);
-        }
-    };
-    auto round0 = [&](int s) {  // stages 0..3, twiddles uniform over the grid
-        const int dist = 8 >> s;
-#pragma unroll
-        for (int m = 0; m < 16; m++)
-            if (!(m & dist)) bf(m, dist, (1 << s) + (m >> (4 - s)));
-    };
-    auto round1 = [&](int r) {  // stage 4 + r, j = 4096 c + t + 256 m
-        const int dist = 8 >> r;
-#pragma unroll
-        for (int m = 0; m < 16; m++)
-            if (!(m & dist)) bf(m, dist, (1 << (4 + r)) + (c << r) + (m >> (4 - r)));
-    };
-    auto roundA = [&](int r) {  // stage 8 + r, j = 256 hA + tcA + 16 m
-        const int dist = 8 >> r;
-#pragma unroll
-        for (int m = 0; m < 16; m++)
-            if (!(m & dist)) bf(m, dist, (1 << (8 + r)) + (hA << r) + (m >> (4 - r)));
-    };
-    auto roundB = [&](int r) {  // stage 8 + r (r = 4..7), j = 256 hB + 16 tcB + m
-        const int dist = 8 >> (r - 4);
-#pragma unroll
-        for (int m = 0; m < 16; m++)
-            if (!(m & dist)) bf(m, dist, (1 << (8 + r)) + (hB << r) + ((16 * tcB + m) >> (8 - r)));
-    };
-    const uint32_t sbase = smem_u32(sm);
-    const ModConst &mc = pr.m[pi];
-    if constexpr (!INV) {
-        // every CTA of the cluster must be running before any DSMEM store: arrive now, wait just before
-        cl_arrive_relaxed();
-        // ---- load (strided, coalesced over t), R0
-        if constexpr (PRO == 1) {
-            const u64 *src = fz.src + (long long)(p / fz.src_div) * fz.src_hi + (long long)(p % fz.src_div) * fz.src_lo;
-            const int dj = p % fz.src_div;
-            if ((fz.red0 >> dj) & 1) {
-#pragma unroll
-                for (int m = 0; m < 16; m++) v[m] = from_u64(src[lo + 4096 * m]);
-            } else if ((fz.red1 >> dj) & 1) {
-#pragma unroll
-                for (int m = 0; m < 16; m++) {
-                    const u64 x = src[lo + 4096 * m];
-                    v[m] = from_u64(x >= mc.q ? x - mc.q : x);
-                }
-            } else {
-#pragma unroll
-                for (int m = 0; m < 16; m++) v[m] = from_u64(mod64(src[lo + 4096 * m], mc));
-            }
-        } else {
-#pragma unroll
-            for (int m = 0; m < 16; m++) v[m] = from_u64(a[lo + 4096 * m]);
-        }
-#pragma unroll
-        for (int s = 0; s < 4; s++) round0(s);
-        // ---- DSMEM all-to-all: j = 4096 m + lo -> CTA m, block offset lo = 256 c + t (swizzled)
-        cl_wait_acquire();
-#pragma unroll
-        for (int m = 0; m < 16; m++) cl_st64(cl_mapa(sbase, m) + 8u * swz(c, t), to_bits(v[m]));
-        cl_arrive_release();
-        cl_wait_acquire();
-        // ---- R1 (o = t + 256 m: col m, mid t), written back in place
-#pragma unroll
-        for (int m = 0; m < 16; m++) v[m] = from_bits(sm[swz(m, t)]);
-#pragma unroll
-        for (int r = 0; r < 4; r++) round1(r);
-#pragma unroll
-        for (int m = 0; m < 16; m++) sm[swz(m, t)] = to_bits(v[m]);
-        __syncthreads();
-        // ---- R2 (A mapping), R3 (B mapping)
-#pragma unroll
-        for (int m = 0; m < 16; m++) v[m] = from_bits(sm[swz(colA, tcA + 16 * m)]);
-#pragma unroll
-        for (int r = 0; r < 4; r++) roundA(r);
-#pragma unroll
-        for (int m = 0; m < 16; m++) sm[swz(colA, tcA + 16 * m)] = to_bits(v[m]);
-        __syncthreads();
-#pragma unroll
-        for (int m = 0; m < 16; m++) v[m] = from_bits(sm[swz(colB, 16 * tcB + m)]);
-#pragma unroll
-        for (int r = 4; r < 8; r++) roundB(r);
-        __syncthreads();
-#pragma unroll
-        for (int m = 0; m < 16; m++) sm[swz(colB, 16 * tcB + m)] = to_bits(v[m]);
-        __syncthreads();
-#pragma unroll
-        for (int m = 0; m < 16; m++) v[m] = from_bits(sm[swz(colA, tcA + 16 * m)]);
-        // ---- epilogue: canonical residues, coalesced store (A mapping)
-        if constexpr (EPI == 1) {  // ModDown combine (see ntt16_body)
-            const int tj = p >> 1, b = p & 1;
-            const KsJob &J = fz.jobs.j[tj];
-            const u64 *ui = fz.u + ((long long)p * fz.E + l) * N;
-            u64 *out = J.out + ((long long)b * fz.k + l) * N;
-            const u64 pv = fz.pinv.v[l], psh = fz.pinv.sh[l];
-            u64 uv[16];
-#pragma unroll
-            for (int m = 0; m < 16; m++) uv[m] = ui[(uint32_t)(hA << 8) + tcA + 16 * m];
-#pragma unroll
-            for (int m = 0; m < 16; m++) {
-                u64 x;
-                if constexpr (SMALL) x = canon(v[m], qd, qinv);
-                else x = canon8(v[m], q);
-                const uint32_t gx = (uint32_t)(hA << 8) + tcA + 16 * m;
-                u64 r = shoup(uv[m] + q - x, pv, psh, q);
-                if (J.add_mode == 1 && b == 0) {
-                    const uint32_t src = J.galois == 1 ? gx : galois_perm(gx, J.galois, logN);
-                    r = addmod(r, J.c0[(long long)l * N + src], q);
-                } else if (J.add_mode == 2) {
-                    const u64 *cc = b == 0 ? J.c0 : J.c1_add;
-                    r = addmod(r, cc[(long long)l * N + gx], q);
-                }
-                out[gx] = r;
-            }
-        } else {
-#pragma unroll
-            for (int m = 0; m < 16; m++) {
-                u64 x;
-                if constexpr (SMALL) x = canon(v[m], qd, qinv);
-                else x = canon8(v[m], q);
-                a[(hA << 8) + tcA + 16 * m] = x;
-            }
-        }
-    } else {
-        // ---- contiguous load (A mapping), R3, R2 (inverse order)
-        const u64 *src = PRO == 2 ? fz.srcp.p[p] + (long long)(rb.limb0 + l) * N : a;
-#pragma unroll
-        for (int m = 0; m < 16; m++) v[m] = from_u64(src[(hA << 8) + tcA + 16 * m]);
-#pragma unroll
-        for (int m = 0; m < 16; m++) sm[swz(colA, tcA + 16 * m)] = to_bits(v[m]);
-        __syncthreads();
-#pragma unroll
-        for (int m = 0; m < 16; m++) v[m] = from_bits(sm[swz(colB, 16 * tcB + m)]);
-#pragma unroll
-        for (int r = 7; r >= 4; r--) roundB(r);
-        __syncthreads();
-#pragma unroll
-        for (int m = 0; m < 16; m++) sm[swz(colB, 16 * tcB + m)] = to_bits(v[m]);
-        __syncthreads();
-#pragma unroll
-        for (int m = 0; m < 16; m++) v[m] = from_bits(sm[swz(colA, tcA + 16 * m)]);
-#pragma unroll
-        for (int r = 3; r >= 0; r--) roundA(r);
-        if constexpr (SMALL) {  // inverse sums double per stage: re-centre after 8 stages
-#pragma unroll
-            for (int m = 0; m < 16; m++) v[m] = centre(v[m], qd, qinv);
-        }
-#pragma unroll
-        for (int m = 0; m < 16; m++) sm[swz(colA, tcA + 16 * m)] = to_bits(v[m]);
-        __syncthreads();
-        // ---- R1 (o = t + 256 m)
-#pragma unroll
-        for (int m = 0; m < 16; m++) v[m] = from_bits(sm[swz(m, t)]);
-        // the DSMEM stores below overwrite other CTAs' buffers: they wait until every CTA has read its
-        // R1 values (release orders these reads before the arrival)
-        cl_arrive_release();
-#pragma unroll
-        for (int r = 3; r >= 0; r--) round1(r);
-        // ---- DSMEM all-to-all: j = 4096 c + t + 256 m -> CTA m, slot (m' = c, t') = 256 c + t
-        cl_wait_acquire();
-#pragma unroll
-        for (int m = 0; m < 16; m++) cl_st64(cl_mapa(sbase, m) + 8u * (256u * c + t), to_bits(v[m]));
-        cl_arrive_release();
-        cl_wait_acquire();
-        // ---- R0 (j = lo + 4096 m), epilogue N^{-1}, strided store
-#pragma unroll
-        for (int m = 0; m < 16; m++) v[m] = from_bits(sm[256 * m + t]);
-#pragma unroll
-        for (int s = 3; s >= 0; s--) round0(s);
-#pragma unroll
-        for (int m = 0; m < 16; m++) {
-            u64 x;
-            if constexpr (SMALL) {
-                x = canon(mulr(v[m], (double)mc.ninv, qd, qinv), qd, qinv);
-            } else {
-                x = shoup_lazy(v[m], mc.ninv, mc.ninv_sh, q);
-                if (x >= q) x -= q;
-            }
-            a[lo + 4096 * m] = x;
-        }
-    }
-}
-// a skipped (own-digit) row of a ModUp batch: this CTA's 4096 residues of the NTT-form input row
-__device__ __forceinline__ void copy_own_cl(const RowBatch &rb, const NttFuse &fz, int p, int l) {
-    if (!fz.copy_own) return;
-    constexpr int N = 1 << 16;
-    const u64 *src = fz.srcp.p[p / fz.src_div] + (long long)l * N;
-    u64 *a = rb.base + (long long)p * rb.poly_stride + (long long)(rb.limb0 + l) * N;
-    const int base = blockIdx.x * 4096 + threadIdx.x;
-#pragma unroll
-    for (int m = 0; m < 16; m++) a[base + 256 * m] = src[base + 256 * m];
-}
-template <bool INV, int PRO = 0, int EPI = 0>
-__global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt_cl16_int(RowBatch rb, const u64 *__restrict__ tw_all,
-                                                                   const double *__restrict__ twd, Primes pr,
-                                                                   const NttFuse fz) {
-    __shared__ u64 sm[16 * 256];
-    int p, l;
-    if (!ntt16_row(rb, p, l)) {  // the whole cluster (one row) skips together
-        if (PRO == 1) copy_own_cl(rb, fz, p, l);
-        return;
-    }
-    ntt_cl16_body<INV, PRO, EPI, false>(sm, rb, tw_all, twd, pr, fz, p, l);
-}
-template <bool INV, int PRO = 0, int EPI = 0>
-__global__ void __launch_bounds__(256, BLB_NTT_F64_MINB) ntt_cl16_f64(RowBatch rb, const u64 *__restrict__ tw_all,
-                                                                       const double *__restrict__ twd, Primes pr,
-                                                                       const NttFuse fz) {
-    __shared__ u64 sm[16 * 256];
-    int p, l;
-    if (!ntt16_row(rb, p, l)) {
-        if (PRO == 1) copy_own_cl(rb, fz, p, l);
-        return;
-    }
-    ntt_cl16_body<INV, PRO, EPI, true>(sm, rb, tw_all, twd, pr, fz, p, l);
-}
-// launch one cluster (16 CTAs along x) per row
-template <class Kern>
-static void launch_cl16(Kern kern, int rows, cudaStream_t st, const RowBatch &r, const blb_params *P, const NttFuse &fz) {
-    if (blb_smem_optin_needed((const void *)kern, 0))
-        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(16, rows);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 16;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kern, r, (const u64 *)P->d_tw, (const double *)P->d_twd, P->pr, fz);
-}
-#ifndef BLB_NTT_CL
-#define BLB_NTT_CL 0   // measured slower (profiles/r2_ntt_cluster_ab.log): 2-pass kernels stay
+template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0>
+static void launch_int(const blb_params *P, const RowBatch &r, dim3 g, cudaStream_t st, int s0, int last,
+                       const NttFuse &fz) {
+#ifndef BLB_NTT_LZ
+#define BLB_NTT_LZ 1
 #endif
+    if constexpr (!INV) {
+        if (BLB_NTT_LZ && rb_below60(P, r)) {
+            ntt16_int<INV, STRIDED, PRO, EPI, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, s0, last, fz);
+            return;
+        }
+    }
+    ntt16_int<INV, STRIDED, PRO, EPI, false><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, s0, last, fz);
+}
 
 // split the limbs of a batch by prime size: out[0] = FP64 rows (q < 2^41), out[1] = integer rows
 static int split_rows(const blb_params *P, const RowBatch &rb, RowBatch out[2]) {
@@ -772,28 +517,6 @@ static inline bool rb_small(const blb_params *P, const RowBatch &r) {
     return P->mod[r.prime[r.nsel ? r.sel[0] : 0]] < (1ull << 41);
 }
 static inline int rb_rows(const RowBatch &r) { return r.n_polys * (r.nsel ? r.nsel : r.limbs); }
-
-// L2-resident pass chaining: a large batch runs as chunks of about BLB_NTT_CHUNK rows, each chunk's two
-// passes back to back, so the intermediate written by pass 1 is read by pass 2 from L2 and overwritten
-// there (in place): one DRAM read and one write per residue instead of two.  0 = one launch pair.
-#ifndef BLB_NTT_CHUNK
-#define BLB_NTT_CHUNK 0
-#endif
-template <class F>
-static void for_chunks(const RowBatch &r, F &&f) {
-    const int per_poly = r.nsel ? r.nsel : r.limbs;
-    int cp = BLB_NTT_CHUNK > 0 ? std::max(1, BLB_NTT_CHUNK / per_poly) : r.n_polys;
-    if (cp >= r.n_polys) { f(r, dim3(16, rb_rows(r))); return; }
-    // equal chunks (no small tail launch)
-    const int nch = (r.n_polys + cp - 1) / cp;
-    cp = (r.n_polys + nch - 1) / nch;
-    for (int p0 = 0; p0 < r.n_polys; p0 += cp) {
-        RowBatch c = r;
-        c.p0 = r.p0 + p0;
-        c.n_polys = std::min(cp, r.n_polys - p0);
-        f(c, dim3(16, rb_rows(c)));
-    }
-}
 
 // Two-stream NTT: the integer-kernel rows of a mixed batch run on the auxiliary
 // stream while the FP64-kernel rows run on the caller's stream -- the two kernels load different
@@ -860,35 +583,28 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
         const NttStreams ss(P, st0, np2);
         for (int h = 0; h < np2; h++) {
             const cudaStream_t st = ss.part_stream(h);
-            const bool small = rb_small(P, parts[h]);
-            for_chunks(parts[h], [&](const RowBatch &r, dim3 g) {
-                if (BLB_NTT_CL) {
-                    if (small) launch_cl16(inverse ? ntt_cl16_f64<true> : ntt_cl16_f64<false>, g.y, st, r, P, fz);
-                    else launch_cl16(inverse ? ntt_cl16_int<true> : ntt_cl16_int<false>, g.y, st, r, P, fz);
-                    BLB_COUNT_LAUNCH(1);
-                    return;
-                }
-                if (small) {
-                    if (!inverse) {
-                        ntt16_f64<false, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
-                        ntt16_f64<false, false><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
-                    } else {
-                        ntt16_f64<true, false><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 0, fz);
-                        ntt16_f64<true, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 1, fz);
-                    }
+            const RowBatch &r = parts[h];
+            const dim3 g(16, rb_rows(r));
+            if (rb_small(P, r)) {
+                if (!inverse) {
+                    ntt16_f64<false, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
+                    ntt16_f64<false, false><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
                 } else {
-                    if (!inverse) {
-                        ntt16_int<false, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
-                        ntt16_int<false, false><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
-                    } else {
-                        ntt16_int<true, false><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 0, fz);
-                        ntt16_int<true, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 1, fz);
-                    }
+                    ntt16_f64<true, false><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 0, fz);
+                    ntt16_f64<true, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 1, fz);
                 }
-                BLB_COUNT_LAUNCH(2);
-            });
+            } else {
+                if (!inverse) {
+                    launch_int<false, true>(P, r, g, st, 0, 0, fz);
+                    launch_int<false, false>(P, r, g, st, 8, 1, fz);
+                } else {
+                    launch_int<true, false>(P, r, g, st, 8, 0, fz);
+                    launch_int<true, true>(P, r, g, st, 0, 1, fz);
+                }
+            }
         }
         ss.join();
+        BLB_COUNT_LAUNCH(2 * np2);
         blb_timing_end(1, t0, st0, alg);
         BLB_CHECK_LAUNCH();
         return BLB_OK;
@@ -946,57 +662,33 @@ blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool invers
                 else if (fz.src_q[j] / 2 < minq) fzp.red1 |= 1u << j;  // q_j <= 2 minq - 1 (odd primes)
             }
         }
-        const bool small = rb_small(P, rp);
-        for_chunks(rp, [&](const RowBatch &r, dim3 g) {
-            if (BLB_NTT_CL) {
-                BLB_COUNT_LAUNCH(1);
-                if (inverse) {
-                    if (small) launch_cl16(ntt_cl16_f64<true, 2, 0>, g.y, st, r, P, fz);
-                    else launch_cl16(ntt_cl16_int<true, 2, 0>, g.y, st, r, P, fz);
-                } else if (fz.pro == 1) {
-                    if (fz.epi == 1) {
-                        if (small) launch_cl16(ntt_cl16_f64<false, 1, 1>, g.y, st, r, P, fzp);
-                        else launch_cl16(ntt_cl16_int<false, 1, 1>, g.y, st, r, P, fzp);
-                    } else {
-                        if (small) launch_cl16(ntt_cl16_f64<false, 1, 0>, g.y, st, r, P, fzp);
-                        else launch_cl16(ntt_cl16_int<false, 1, 0>, g.y, st, r, P, fzp);
-                    }
-                } else {
-                    if (fz.epi == 1) {
-                        if (small) launch_cl16(ntt_cl16_f64<false, 0, 1>, g.y, st, r, P, fz);
-                        else launch_cl16(ntt_cl16_int<false, 0, 1>, g.y, st, r, P, fz);
-                    } else {
-                        if (small) launch_cl16(ntt_cl16_f64<false, 0, 0>, g.y, st, r, P, fz);
-                        else launch_cl16(ntt_cl16_int<false, 0, 0>, g.y, st, r, P, fz);
-                    }
-                }
-                return;
-            }
-            BLB_COUNT_LAUNCH(2);
-            if (inverse) {  // pro = 2: first (contiguous) pass loads from the pointer table
-                if (small) {
-                    ntt16_f64<true, false, 2, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 0, fz);
-                    ntt16_f64<true, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 1, fz);
-                } else {
-                    ntt16_int<true, false, 2, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 0, fz);
-                    ntt16_int<true, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 1, fz);
-                }
-                return;
-            }
+        const RowBatch &r = rp;
+        const dim3 g(16, rb_rows(r));
+        const bool small = rb_small(P, r);
+        if (inverse) {  // pro = 2: first (contiguous) pass loads from the pointer table
             if (small) {
-                if (fz.pro == 1) ntt16_f64<false, true, 1, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fzp);
-                else ntt16_f64<false, true, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
-                if (fz.epi == 1) ntt16_f64<false, false, 0, 1><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
-                else ntt16_f64<false, false, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
+                ntt16_f64<true, false, 2, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 0, fz);
+                ntt16_f64<true, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 1, fz);
             } else {
-                if (fz.pro == 1) ntt16_int<false, true, 1, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fzp);
-                else ntt16_int<false, true, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
-                if (fz.epi == 1) ntt16_int<false, false, 0, 1><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
-                else ntt16_int<false, false, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
+                launch_int<true, false, 2, 0>(P, r, g, st, 8, 0, fz);
+                launch_int<true, true>(P, r, g, st, 0, 1, fz);
             }
-        });
+            continue;
+        }
+        if (small) {
+            if (fz.pro == 1) ntt16_f64<false, true, 1, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fzp);
+            else ntt16_f64<false, true, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
+            if (fz.epi == 1) ntt16_f64<false, false, 0, 1><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
+            else ntt16_f64<false, false, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
+        } else {
+            if (fz.pro == 1) launch_int<false, true, 1, 0>(P, r, g, st, 0, 0, fzp);
+            else launch_int<false, true, 0, 0>(P, r, g, st, 0, 0, fz);
+            if (fz.epi == 1) launch_int<false, false, 0, 1>(P, r, g, st, 8, 1, fz);
+            else launch_int<false, false, 0, 0>(P, r, g, st, 8, 1, fz);
+        }
     }
     ss.join();
+    BLB_COUNT_LAUNCH(2 * np2);
     blb_timing_end(1, t0, st0, (double)rows * 16.0 * (1 << 16));
     BLB_CHECK_LAUNCH();
     return BLB_OK;
