@@ -454,7 +454,8 @@ blb_status blb_qk_plan_info(const blb_qk_plan *plan, int *J, int *n_out, int *g,
 /* Rotation steps needed (the relinearisation key, Galois element 0, is needed too). */
 blb_status blb_qk_plan_rotations(const blb_qk_plan *plan, int32_t *steps, int *n);
 /* Offline precompute (row a0): encode all mask plaintexts into `masks` (device,
- * blb_qk_mask_bytes bytes).  Synchronises. */
+ * blb_qk_mask_bytes bytes; an opaque buffer for blb_ct_ct_qk: the residues of limbs
+ * whose prime is below 2^41 are stored as IEEE doubles).  Synchronises. */
 size_t blb_qk_mask_bytes(const blb_qk_plan *plan);
 blb_status blb_qk_encode_masks(const blb_qk_plan *plan, uint64_t *masks, void *stream);
 size_t blb_qk_workspace_bytes(const blb_qk_plan *plan);

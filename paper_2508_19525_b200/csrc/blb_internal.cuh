@@ -427,8 +427,9 @@ struct KsJob {
     uint32_t galois;  // 1 = identity
     uint32_t galois_inv;  // g^{-1} mod 2N (filled by the key-switch launcher)
     int add_mode;     // 0 = none, 1 = add sigma_g(c0) to out0 (rotation), 2 = add c0 / c1 pair (relin)
-    // 1: limbs whose prime is < 2^41 are written as the bits of the residue as a double (the weight
-    // MAC's baby-step buffer R: its FP64 accumulators then read R without a conversion)
+    // 1: limbs whose prime is < 2^41 are written as the bits of the residue as a double (the MACs'
+    // rotation buffers -- the weight MAC's baby steps R, the ct-ct stage-1 / step-3 rotations: their
+    // FP64 accumulators then read them without a conversion)
     int out_f64;
     const u64 *c1_add;
 };
@@ -475,7 +476,8 @@ blb_status launch_keyswitch_ext(const blb_params *P, int level, const KsJob *job
 blb_status launch_moddown(const blb_params *P, int level, u64 *u, int n, u64 *out, u64 *conv, cudaStream_t st);
 blb_status launch_moddown(const blb_params *P, int level, u64 *u, int n, u64 *const *outs, u64 *conv,
                           cudaStream_t st);
-blb_status launch_lift_ext(const blb_params *P, int level, const u64 *in, u64 *out, cudaStream_t st);
+// f64: limbs with q < 2^41 written as double bits (the ct-ct mask MACs' rotation buffers, KsJob::out_f64)
+blb_status launch_lift_ext(const blb_params *P, int level, const u64 *in, u64 *out, cudaStream_t st, bool f64 = false);
 // ModDown fused with rescale (reading C17): u [n][2][level+1+np][N] (its q_level and P limbs are
 // INTT'd in place) -> round(X / (q_level P)) as [2][level][N] NTT ciphertexts; conv scratch
 // kMaxJobs x [2][level][N]

@@ -355,77 +355,13 @@ __device__ __forceinline__ void ks_inner_body(const KsJobs &jobs, const KsGroups
             const KsJob &J = jobs.j[t];
             const u64 r0 = accr(a0[q], mc, qd, qinv), r1 = a1r(q);
             if (EXT) {
-                J.out[(long long)m * N + dst] = r0;
-                J.out[((long long)E + m) * N + dst] = r1;
+                const bool f = SMALL && J.out_f64;
+                J.out[(long long)m * N + dst] = f ? (u64)__double_as_longlong((double)r0) : r0;
+                J.out[((long long)E + m) * N + dst] = f ? (u64)__double_as_longlong((double)r1) : r1;
             } else {
                 u[(((long long)t * 2 + 0) * E + m) * N + dst] = r0;
                 u[(((long long)t * 2 + 1) * E + m) * N + dst] = r1;
             }
-        }
-    }
-}
-
-// 60-bit rows: the group's jobs one at a time on Acc60 (6 IMAD-class instructions per product instead
-// of Acc128's ~11), so only one job's accumulators are live (Acc60 for all four jobs at once needed
-// 122 registers and measured slower).  Same additive terms and stores as ks_inner_body.
-template <int BETA, bool EXT, class DS>
-__device__ __forceinline__ void ks_inner_body60(const KsJobs &jobs, const KsGroups &grp, u64 *u, const Primes &pr, int k,
-                                                int np, int K, int logN, const PinvTab &pq, int x, int m, int gi,
-                                                const DS &ds) {
-    const int N = 1 << logN;
-    const int t0 = grp.start[gi], cnt = grp.start[gi + 1] - t0;
-    const int E = k + np, Lk = K + np;
-    const int pm = m < k ? m : K + (m - k);
-    const KsJob &J0 = jobs.j[t0];
-    const uint32_t dst = J0.galois == 1 ? (uint32_t)x : galois_perm(x, J0.galois_inv, logN);
-    const ModConst &mc = pr.m[pm];
-    u64 kb[BETA], ka[BETA];
-#pragma unroll
-    for (int j = 0; j < BETA; j++) {
-        kb[j] = J0.key[(((long long)j * 2 + 0) * Lk + pm) * N + x];
-        ka[j] = J0.key[(((long long)j * 2 + 1) * Lk + pm) * N + x];
-    }
-#pragma unroll 1
-    for (int q = 0; q < cnt; q++) {
-        const int t = t0 + q;
-        const KsJob &J = jobs.j[t];
-        u64 e[BETA];
-#pragma unroll
-        for (int j = 0; j < BETA; j++) e[j] = ds(t, q, j);
-        u64 c0v = 0, c1v = 0;
-        if (m < k) {
-            if (EXT || J.add_mode != 0) c0v = J.c0[(long long)m * N + x];
-            if (J.c1_add && (EXT || J.add_mode == 2)) c1v = J.c1_add[(long long)m * N + x];
-        }
-        Acc60 a0, a1;
-        a0.zero(); a1.zero();
-#pragma unroll
-        for (int j = 0; j < BETA; j++) {
-            a0.mac(e[j], kb[j]);
-            a1.mac(e[j], ka[j]);
-        }
-        u64 r0, r1;
-        if constexpr (BETA <= 6) {  // P c as a 7th product (Acc60 holds <= 7)
-            if (m < k) {
-                a0.mac(c0v, pq.v[m]);
-                a1.mac(c1v, pq.v[m]);
-            }
-            r0 = a0.reduce(mc);
-            r1 = a1.reduce(mc);
-        } else {
-            r0 = a0.reduce(mc);
-            r1 = a1.reduce(mc);
-            if (m < k) {
-                r0 = addmod(r0, shoup(c0v, pq.v[m], pq.sh[m], mc.q), mc.q);
-                r1 = addmod(r1, shoup(c1v, pq.v[m], pq.sh[m], mc.q), mc.q);
-            }
-        }
-        if (EXT) {
-            J.out[(long long)m * N + dst] = r0;
-            J.out[((long long)E + m) * N + dst] = r1;
-        } else {
-            u[(((long long)t * 2 + 0) * E + m) * N + dst] = r0;
-            u[(((long long)t * 2 + 1) * E + m) * N + dst] = r1;
         }
     }
 }
@@ -450,7 +386,6 @@ k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, int np, int K, i
     const int pm = m < k ? m : K + (m - k);
     const DigG ds{&jobs, (long long)m * (1 << logN) + x, (long long)(k + np) << logN};
     if (pr.m[pm].q < (1ull << 41)) ks_inner_body<BETA, EXT, true>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi, ds);
-    else if constexpr (BETA > 0 && BETA <= 7) ks_inner_body60<BETA, EXT>(jobs, grp, u, pr, k, np, K, logN, pq, x, m, gi, ds);
     else ks_inner_body<BETA, EXT, false>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi, ds);
 }
 
@@ -538,6 +473,10 @@ __global__ void __launch_bounds__(kKsTile) k_ks_bulk(KsJobs jobs, KsGroups grp, 
         const int t = t0 + q;
         if (EXT) {
             const KsJob &J = jobs.j[t];
+            if (small && J.out_f64) {  // the ct-ct mask MACs read these limbs as doubles
+                r0 = (u64)__double_as_longlong(AccF64::u2d(r0));
+                r1 = (u64)__double_as_longlong(AccF64::u2d(r1));
+            }
             J.out[(long long)m * N + dst] = r0;
             J.out[((long long)E + m) * N + dst] = r1;
         } else {
@@ -906,14 +845,9 @@ static blb_status ks_inner_launch(const blb_params *P, int level, const KsJobs &
         pq.sh[i] = blbh_shoup_dev_table(P, i);
     }
     cudaEvent_t t0 = blb_timing_begin(st);
-#ifndef BLB_KS_BULK
-#define BLB_KS_BULK 1
-#endif
     const int T = N < kKsTile ? N : kKsTile;
     const dim3 gb((unsigned)((N / T) * G.n), E);
-    bool done = BLB_KS_BULK && beta >= 1 && beta <= 6;
-    if (done) {
-        switch (beta) {
+    switch (beta) {
 #define KSB(B)                                                                                               \
     case B: {                                                                                                \
         const size_t sm = (size_t)ks_bulk_words<B>(T) * 8;                                                    \
@@ -921,19 +855,12 @@ static blb_status ks_inner_launch(const blb_params *P, int level, const KsJobs &
         k_ks_bulk<B, EXT><<<gb, T, sm, st>>>(J, G, u, P->pr, k, np, P->K, P->logN, pq);                       \
         break;                                                                                               \
     }
-            KSB(1) KSB(2) KSB(3) KSB(4) KSB(5) KSB(6)
+        KSB(1) KSB(2) KSB(3) KSB(4) KSB(5) KSB(6)
 #undef KSB
+        default: {  // beta > 6: the per-thread kernel with a runtime digit count
+            const dim3 gks((unsigned)(((N + kTB - 1) / kTB) * G.n), E);
+            k_ks_inner<0, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq);
         }
-    }
-    const dim3 gks((unsigned)(((N + kTB - 1) / kTB) * G.n), E);
-    if (!done) switch (beta) {
-        case 1: k_ks_inner<1, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
-        case 2: k_ks_inner<2, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
-        case 3: k_ks_inner<3, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
-        case 4: k_ks_inner<4, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
-        case 5: k_ks_inner<5, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
-        case 6: k_ks_inner<6, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
-        default: k_ks_inner<0, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq); break;
     }
     BLB_COUNT_LAUNCH(1);
     // algorithmic bytes: each distinct key once (groups sharing a key read it through L2)
@@ -1190,20 +1117,23 @@ blb_status launch_moddown(const blb_params *P, int level, u64 *u, int n, u64 *co
 }
 
 // lift a Q_l ciphertext to Q_l u P: (P c0, P c1) on the q limbs, 0 on the p limbs
-__global__ void k_lift_ext(const u64 *in, u64 *out, PinvTab pq, Primes pr, int k, int np, int N) {
+__global__ void k_lift_ext(const u64 *in, u64 *out, PinvTab pq, Primes pr, int k, int np, int N, int f64) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int m = blockIdx.y, p = blockIdx.z;
     if (x >= N) return;
     const int E = k + np;
     u64 v = 0;
-    if (m < k) v = shoup(in[((long long)p * k + m) * N + x], pq.v[m], pq.sh[m], pr.m[m].q);
-    out[((long long)p * E + m) * N + x] = v;
+    if (m < k) {
+        v = shoup(in[((long long)p * k + m) * N + x], pq.v[m], pq.sh[m], pr.m[m].q);
+        if (f64 && pr.m[m].q < (1ull << 41)) v = (u64)__double_as_longlong((double)v);
+    }
+    out[((long long)p * E + m) * N + x] = v;  // P limbs: 0 (also as a double)
 }
-blb_status launch_lift_ext(const blb_params *P, int level, const u64 *in, u64 *out, cudaStream_t st) {
+blb_status launch_lift_ext(const blb_params *P, int level, const u64 *in, u64 *out, cudaStream_t st, bool f64) {
     const int k = level + 1;
     PinvTab pq{};
     for (int i = 0; i < k; i++) { pq.v[i] = P->P_mod_q[i]; pq.sh[i] = blbh_shoup_dev_table(P, i); }
-    k_lift_ext<<<grid_x(P->N, k + P->np, 2), kTB, 0, st>>>(in, out, pq, P->pr, k, P->np, P->N);
+    k_lift_ext<<<grid_x(P->N, k + P->np, 2), kTB, 0, st>>>(in, out, pq, P->pr, k, P->np, P->N, f64 ? 1 : 0);
     BLB_COUNT_LAUNCH(1);
     BLB_CHECK_LAUNCH();
     return BLB_OK;

@@ -116,28 +116,27 @@ __global__ void __launch_bounds__(kTB) k_mac(const u64 *__restrict__ pt, const u
     const ModConst &mc = pr.m[l < kq ? l : Kfull + (l - kq)];
     u64 *out = acc + (long long)o * 2 * kN + lx;
     if (mc.q < (1ull << 41)) {
-        // 40-bit limb: c0 products with split 32-bit partial products (Acc41, integer pipe),
-        // c1 products on the FP64 pipe (AccF64)
+        // limbs below 2^41: masks and rotations stored as doubles (blb_qk_encode_masks,
+        // KsJob::out_f64), all four sums on the grid-split FP64 accumulator
         const double qd = (double)mc.q, qinv = 1.0 / qd;
-        Acc41 a00, a01;
-        AccF64 a10, a11;
+        AccG a00, a01, a10, a11;
         a00.zero(); a01.zero(); a10.zero(); a11.zero();
         int cnt = 0;
 #pragma unroll 4
         for (int e = e_lo; e < e_hi; e++) {
             const int bi = ent_r[e];
             const int pe = ent_pt ? ent_pt[e] : e - e_base;
-            const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(pt + (long long)pe * kN + lx);
-            const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(R + (long long)bi * 2 * kN + lx);
-            const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(R + ((long long)bi * 2 + 1) * kN + lx);
-            a00.mac(pv.x, r0.x); a01.mac(pv.y, r0.y);
-            a10.mac(pv.x, r1.x, qd, qinv); a11.mac(pv.y, r1.y, qd, qinv);
-            if (++cnt == 512) {  // keep the FP64 sums below 2^51
-                a10.fold(qd, qinv); a11.fold(qd, qinv);
+            const double2 pv = *reinterpret_cast<const double2 *>(pt + (long long)pe * kN + lx);
+            const double2 r0 = *reinterpret_cast<const double2 *>(R + (long long)bi * 2 * kN + lx);
+            const double2 r1 = *reinterpret_cast<const double2 *>(R + ((long long)bi * 2 + 1) * kN + lx);
+            a00.macd(pv.x, r0.x); a01.macd(pv.y, r0.y);
+            a10.macd(pv.x, r1.x); a11.macd(pv.y, r1.y);
+            if (++cnt == 512) {  // AccG bound: <= 512 products between folds
+                a00.fold(qd, qinv); a01.fold(qd, qinv); a10.fold(qd, qinv); a11.fold(qd, qinv);
                 cnt = 0;
             }
         }
-        *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00.reduce(mc), a01.reduce(mc));
+        *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(a00.reduce(qd, qinv), a01.reduce(qd, qinv));
         *reinterpret_cast<ulonglong2 *>(out + kN) = make_ulonglong2(a10.reduce(qd, qinv), a11.reduce(qd, qinv));
         return;
     }
@@ -414,17 +413,17 @@ __device__ __forceinline__ void macj_consume(const u64 *ring, uint64_t *full, ui
     auto stage = [&](int slot, unsigned phase) {
         mbar_wait_sa(full0 + 8u * slot, phase);
         const u64 *st = ring_t + slot * kStageWords;
-        const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(st);
-        if constexpr (SPLIT41) {
-            const double Px = AccF64::u2d(pv.x), Py = AccF64::u2d(pv.y);
+        if constexpr (SPLIT41) {  // masks and rotations of these limbs are stored as doubles
+            const double2 pv = *reinterpret_cast<const double2 *>(st);
 #pragma unroll
             for (int j = 0; j < JG; j++) {
-                const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + (1 + 2 * j) * 512);
-                const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(st + (2 + 2 * j) * 512);
-                a00[j].macd(Px, AccF64::u2d(r0.x)); a01[j].macd(Py, AccF64::u2d(r0.y));
-                a10[j].macd(Px, AccF64::u2d(r1.x)); a11[j].macd(Py, AccF64::u2d(r1.y));
+                const double2 r0 = *reinterpret_cast<const double2 *>(st + (1 + 2 * j) * 512);
+                const double2 r1 = *reinterpret_cast<const double2 *>(st + (2 + 2 * j) * 512);
+                a00[j].macd(pv.x, r0.x); a01[j].macd(pv.y, r0.y);
+                a10[j].macd(pv.x, r1.x); a11[j].macd(pv.y, r1.y);
             }
         } else {
+            const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(st);
 #pragma unroll
             for (int j = 0; j < JG; j++) {
                 const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(st + (1 + 2 * j) * 512);

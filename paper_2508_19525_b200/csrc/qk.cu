@@ -501,6 +501,19 @@ static size_t qk_mask_elems(const blb_qk_plan *pl) {
 }
 extern "C" size_t blb_qk_mask_bytes(const blb_qk_plan *pl) { return pl ? qk_mask_elems(pl) * sizeof(u64) : 0; }
 
+namespace {
+// the limbs of extended-basis plaintexts whose prime is < 2^41 -> double bits (the mask MACs' format)
+__global__ void k_ext_to_f64(u64 *buf, long long n_polys, int E, int kq, int K, int N, Primes pr) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int l = blockIdx.y;
+    if (x >= N || pr.m[l < kq ? l : K + (l - kq)].q >= (1ull << 41)) return;
+    for (long long p = blockIdx.z; p < n_polys; p += gridDim.z) {
+        const long long off = (p * E + l) * N + x;
+        buf[off] = (u64)__double_as_longlong((double)buf[off]);
+    }
+}
+}  // namespace
+
 extern "C" blb_status blb_qk_encode_masks(const blb_qk_plan *pl, uint64_t *masks, void *stream) {
     if (!pl || !masks) return BLB_E_INVALID_ARG;
     const blb_params *P = pl->P;
@@ -527,6 +540,12 @@ extern "C" blb_status blb_qk_encode_masks(const blb_qk_plan *pl, uint64_t *masks
             BLB_COUNT_LAUNCH(1);
             s = launch_encode(P, slots, cnt, (double)P->mod[lvl], lvl, base + (size_t)m0 * (lvl + 1 + npx) * P->N, buf,
                               flag, st, npx);
+        }
+        // opaque mask format: limbs below 2^41 as doubles, read by the FP64 accumulators of the mask MACs
+        if (cnt_all > 0 && s == BLB_OK) {
+            k_ext_to_f64<<<dim3((P->N + kTB - 1) / kTB, lvl + 1 + npx, (unsigned)std::min(cnt_all, 1024)), kTB, 0, st>>>(
+                base, cnt_all, lvl + 1 + npx, lvl + 1, P->K, P->N, P->pr);
+            BLB_COUNT_LAUNCH(1);
         }
     }
     cudaFreeAsync(slots, st);
@@ -582,7 +601,8 @@ static const u64 *key_for(const blb_keys *K, uint32_t g) {
 // rotations of independent inputs (each its own ModUp) kept in Q u P: out[t] [2][E][N]
 static blb_status rotate_independent_ext(const blb_params *P, const blb_keys *keys, int level,
                                          const std::vector<const u64 *> &in, const std::vector<int32_t> &steps,
-                                         const std::vector<u64 *> &out, u64 *ext, u64 *coef, cudaStream_t st) {
+                                         const std::vector<u64 *> &out, u64 *ext, u64 *coef, cudaStream_t st,
+                                         bool f64) {
     const int k = level + 1, N = P->N, E = k + P->np, beta = blb_beta(P, level);
     const int ib = kIndepBatch;
     for (size_t t0 = 0; t0 < in.size(); t0 += ib) {
@@ -598,6 +618,7 @@ static blb_status rotate_independent_ext(const blb_params *P, const blb_keys *ke
             J.c0 = in[t0 + t];
             J.out = out[t0 + t];
             J.galois = g;
+            J.out_f64 = f64 ? 1 : 0;
             jobs[t] = J;
         }
         BLB_TRY(launch_modup(P, level, c1.data(), cnt, ext, coef, st));
@@ -689,6 +710,7 @@ static blb_status qk_acc(const blb_qk_plan *pl, const blb_keys *keys, const blb_
                 Jb.c0 = cts[j].data;
                 Jb.out = base + j * j_stride + slot[t] * ct_e;
                 Jb.galois = g;
+                Jb.out_f64 = 1;  // read by the mask MAC (k_mac_j) as doubles
                 jobs.push_back(Jb);
             }
         }
@@ -701,7 +723,8 @@ static blb_status qk_acc(const blb_qk_plan *pl, const blb_keys *keys, const blb_
     {
         std::vector<int32_t> ksteps;
         for (int sl : pl->kw_slot) ksteps.push_back(pl->k_rots[sl - 1]);
-        for (int j = 0; j < J; j++) BLB_TRY(launch_lift_ext(P, lvl, K[j].data, W + w.kr + (size_t)j * NKR * ct_e, st));
+        for (int j = 0; j < J; j++)
+            BLB_TRY(launch_lift_ext(P, lvl, K[j].data, W + w.kr + (size_t)j * NKR * ct_e, st, true));
         BLB_TRY(rotate_ext_J(K, ksteps, pl->kw_slot, W + w.kr, (size_t)NKR * ct_e));
     }
     // K' MAC of the window's outputs o = i*J + j, i in [iw0, iw1) (outputs i*J + j share their masks)
@@ -790,14 +813,14 @@ static blb_status qk_acc(const blb_qk_plan *pl, const blb_keys *keys, const blb_
                 u64 *dst = W + w.t + o * 2 * E2 * N;
                 // i = 0, and i H_p L a multiple of n (B > g), rotate by the identity: the lift
                 if ((i * pl->Hp * pl->L) % pl->n == 0) {
-                    BLB_TRY(launch_lift_ext(P, lvl - 2, W + w.sr + o * ct_k2, dst, st));
+                    BLB_TRY(launch_lift_ext(P, lvl - 2, W + w.sr + o * ct_k2, dst, st, true));
                     continue;
                 }
                 in.push_back(W + w.sr + o * ct_k2);
                 steps.push_back(-i * pl->Hp * pl->L);
                 outp.push_back(dst);
             }
-        BLB_TRY(rotate_independent_ext(P, keys, lvl - 2, in, steps, outp, W + w.ext, W + w.coef, st));
+        BLB_TRY(rotate_independent_ext(P, keys, lvl - 2, in, steps, outp, W + w.ext, W + w.coef, st, true));
     }
     // 5. step-3 masks of the window (MAC into the accumulators, Q_{l-2} u P)
     BLB_TRY(launch_mac(P, m3, W + w.t, acc_out, E + pl->off_aw_r, E + pl->off_aw_pt, E + pl->off_aw_start, 0, 0, NA,
@@ -843,7 +866,7 @@ static blb_status qk_finish(const blb_qk_plan *pl, const blb_keys *keys, const u
             steps.push_back(r);
             outp.push_back(dst);
         }
-        BLB_TRY(rotate_independent_ext(P, keys, lvl - 3, in, steps, outp, W + w.ext, W + w.coef, st));
+        BLB_TRY(rotate_independent_ext(P, keys, lvl - 3, in, steps, outp, W + w.ext, W + w.coef, st, false));
     }
     std::vector<u64 *> outs(n_o);
     for (int t = 0; t < n_o; t++) {
