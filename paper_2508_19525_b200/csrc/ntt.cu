@@ -207,10 +207,15 @@ __device__ __forceinline__ void bfly_f64(double &X, double &Y, double w, double 
 #ifndef BLB_NTT_MINB
 #define BLB_NTT_MINB 3
 #endif
+// FP64 contiguous pass: the CTA's 16 x 255 twiddles of stages 8..15 are staged in shared memory by 8
+// bulk copies at the start (twd_s[16 (2^r - 1) + (h - c0) 2^r + j] = twd[2^(8+r) + h 2^r + j]), so the
+// rounds read them from shared memory instead of waiting on dependent L2 loads
+constexpr int kTwsWords = 16 * 255;
 template <bool INV, bool STRIDED, int PRO, int EPI, bool SMALL, bool LZ = false>
 __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u64 *__restrict__ tw_all,
                                            const double *__restrict__ twd_all, const Primes &pr, int, int,
-                                           const NttFuse &fz, int p, int l) {
+                                           const NttFuse &fz, int p, int l, double *tws = nullptr,
+                                           uint64_t *twbar = nullptr) {
     constexpr int logN = 16, N = 1 << logN;
     // the strided pass runs stages [0, 8), the contiguous one [8, 16); the last pass of a transform is
     // the contiguous one forward and the strided one inverse (compile-time: no dead epilogue selects)
@@ -231,6 +236,17 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
     const int colB = t >> 4, tcB = t & 15;
     const int hA = STRIDED ? 0 : (c0 + colA);
     const int hB = STRIDED ? 0 : (c0 + colB);
+    // (the integer kernel's 16-byte (w, w') pairs staged the same way need 96 KB per CTA: measured no faster)
+    constexpr bool TWS = SMALL && !STRIDED;
+    if constexpr (TWS) {  // stage the twiddles (bulk copies, completion on twbar), waited for before round 1
+        if (t == 0) {
+            const double *src = twd_all + (size_t)pi * 2 * N + (INV ? N : 0);
+            mbar_expect_tx(twbar, kTwsWords * 8u);
+#pragma unroll
+            for (int r = 0; r < 8; r++)
+                bulk_g2s(tws + 16 * ((1 << r) - 1), src + (1 << (8 + r)) + (c0 << r), (16u << r) * 8u, twbar);
+        }
+    }
     // SMALL (q < 2^41): values are doubles; between the two passes they are stored as double bits
     using V = typename std::conditional<SMALL, double, u64>::type;
     const double qd = (double)q, qinv = 1.0 / qd;
@@ -297,7 +313,9 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
         for (int m = 0; m < 16; m++) {
             if (m & dist) continue;
             const int widx = (1 << s) + (hA << r) + (m >> (4 - r));
-            if constexpr (SMALL) {
+            if constexpr (TWS) {
+                bfly_f64<INV>(v[m], v[m + dist], tws[16 * ((1 << r) - 1) + (colA << r) + (m >> (4 - r))], qd, qinv);
+            } else if constexpr (SMALL) {
                 bfly_f64<INV>(v[m], v[m + dist], twd[widx], qd, qinv);
             } else {
                 const ulonglong2 tv = twp[widx];
@@ -317,7 +335,10 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
         for (int m = 0; m < 16; m++) {
             if (m & dist) continue;
             const int widx = (1 << s) + (hB << r) + ((16 * tcB + m) >> (8 - r));
-            if constexpr (SMALL) {
+            if constexpr (TWS) {
+                bfly_f64<INV>(v[m], v[m + dist], tws[16 * ((1 << r) - 1) + (colB << r) + ((16 * tcB + m) >> (8 - r))],
+                              qd, qinv);
+            } else if constexpr (SMALL) {
                 bfly_f64<INV>(v[m], v[m + dist], twd[widx], qd, qinv);
             } else {
                 const ulonglong2 tv = twp[widx];
@@ -330,6 +351,7 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
             }
         }
     };
+    if constexpr (TWS) mbar_wait(twbar, 0);
     if (!INV) {
 #pragma unroll
         for (int r = 0; r < 4; r++) roundA(r);
@@ -458,19 +480,40 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_int(RowBatch rb, cons
     }
     ntt16_body<INV, STRIDED, PRO, EPI, false, LZ>(sm, rb, tw_all, twd, pr, s0, last, fz, p, l);
 }
+// dynamic shared memory: 4096 residues, then (contiguous pass) the staged twiddles and their mbarrier
+template <bool STRIDED>
+constexpr size_t ntt16_f64_smem() { return STRIDED ? 4096 * 8 : 4096 * 8 + kTwsWords * 8 + 16; }
 template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0>
 __global__ void __launch_bounds__(256, BLB_NTT_F64_MINB) ntt16_f64(RowBatch rb, const u64 *__restrict__ tw_all,
                                                                     const double *__restrict__ twd, Primes pr, int s0,
                                                                     int last, const NttFuse fz) {
-    __shared__ u64 sm[16 * 256];
+    extern __shared__ __align__(16) u64 dsm[];
     int p, l;
     if (!ntt16_row(rb, p, l)) {
         if (PRO == 1 && STRIDED) copy_own_tile(rb, fz, p, l);
         return;
     }
-    ntt16_body<INV, STRIDED, PRO, EPI, true>(sm, rb, tw_all, twd, pr, s0, last, fz, p, l);
+    if constexpr (STRIDED) {
+        ntt16_body<INV, STRIDED, PRO, EPI, true>(dsm, rb, tw_all, twd, pr, s0, last, fz, p, l);
+    } else {
+        double *tws = reinterpret_cast<double *>(dsm + 4096);
+        uint64_t *bar = reinterpret_cast<uint64_t *>(dsm + 4096 + kTwsWords);
+        if (threadIdx.x == 0) {
+            mbar_init(bar, 1);
+            mbar_fence_init();
+        }
+        __syncthreads();
+        ntt16_body<INV, STRIDED, PRO, EPI, true>(dsm, rb, tw_all, twd, pr, s0, last, fz, p, l, tws, bar);
+    }
 }
 
+template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0>
+static void launch_f64(const blb_params *P, const RowBatch &r, dim3 g, cudaStream_t st, int s0, int last,
+                       const NttFuse &fz) {
+    constexpr size_t smem = ntt16_f64_smem<STRIDED>();
+    if (smem > 48 * 1024) blb_smem_optin(ntt16_f64<INV, STRIDED, PRO, EPI>, smem);
+    ntt16_f64<INV, STRIDED, PRO, EPI><<<g, 256, smem, st>>>(r, P->d_tw, P->d_twd, P->pr, s0, last, fz);
+}
 // integer-kernel launch: forward rows whose primes are all < 2^60 take the LZ butterflies
 static bool rb_below60(const blb_params *P, const RowBatch &r) {
     const int nl = r.nsel ? r.nsel : r.limbs;
@@ -587,11 +630,11 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
             const dim3 g(16, rb_rows(r));
             if (rb_small(P, r)) {
                 if (!inverse) {
-                    ntt16_f64<false, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
-                    ntt16_f64<false, false><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
+                    launch_f64<false, true>(P, r, g, st, 0, 0, fz);
+                    launch_f64<false, false>(P, r, g, st, 8, 1, fz);
                 } else {
-                    ntt16_f64<true, false><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 0, fz);
-                    ntt16_f64<true, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 1, fz);
+                    launch_f64<true, false>(P, r, g, st, 8, 0, fz);
+                    launch_f64<true, true>(P, r, g, st, 0, 1, fz);
                 }
             } else {
                 if (!inverse) {
@@ -667,8 +710,8 @@ blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool invers
         const bool small = rb_small(P, r);
         if (inverse) {  // pro = 2: first (contiguous) pass loads from the pointer table
             if (small) {
-                ntt16_f64<true, false, 2, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 0, fz);
-                ntt16_f64<true, true><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 1, fz);
+                launch_f64<true, false, 2, 0>(P, r, g, st, 8, 0, fz);
+                launch_f64<true, true>(P, r, g, st, 0, 1, fz);
             } else {
                 launch_int<true, false, 2, 0>(P, r, g, st, 8, 0, fz);
                 launch_int<true, true>(P, r, g, st, 0, 1, fz);
@@ -676,10 +719,10 @@ blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool invers
             continue;
         }
         if (small) {
-            if (fz.pro == 1) ntt16_f64<false, true, 1, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fzp);
-            else ntt16_f64<false, true, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 0, 0, fz);
-            if (fz.epi == 1) ntt16_f64<false, false, 0, 1><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
-            else ntt16_f64<false, false, 0, 0><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, 8, 1, fz);
+            if (fz.pro == 1) launch_f64<false, true, 1, 0>(P, r, g, st, 0, 0, fzp);
+            else launch_f64<false, true, 0, 0>(P, r, g, st, 0, 0, fz);
+            if (fz.epi == 1) launch_f64<false, false, 0, 1>(P, r, g, st, 8, 1, fz);
+            else launch_f64<false, false, 0, 0>(P, r, g, st, 8, 1, fz);
         } else {
             if (fz.pro == 1) launch_int<false, true, 1, 0>(P, r, g, st, 0, 0, fzp);
             else launch_int<false, true, 0, 0>(P, r, g, st, 0, 0, fz);
