@@ -312,9 +312,11 @@ def ntt_pipes(ctr: dict, ntt: dict, params, pipes: dict, steps: int) -> dict:
 
 def run_gpt2(args, rank: int, world: int, local: int):
     """Config 5: GPT2-base, 12 layers (d 768, 12 heads, FFN 3072, L = 128), each layer one fused-linear
-    step with its own weights; the 680 GB of per-layer plaintexts do not fit one GPU, so each layer's
-    plaintexts are re-encoded on the device from resident float64 weights before its step (timed:
-    it is per-inference work at 1 GPU).  One step = 12 layers."""
+    step with its own weights; the 680 GB of per-layer plaintexts do not fit one GPU, so (model.GPT2Stack
+    mode "coeffs") every layer's weights stay resident as compact 5-byte integer coefficients and each
+    MatMul's plaintexts are expanded on the device (residues, NTT, packing) right before it -- timed: it is
+    per-inference work at 1 GPU ("reencode": the older full re-encode from float64 weights).
+    One step = 12 layers."""
     import torch
     import torch.distributed as dist
 
@@ -328,7 +330,7 @@ def run_gpt2(args, rank: int, world: int, local: int):
     dims = Dims(**bi.GPT2_BASE)
     params = blb.Params.from_preset(bi.BERT, device=local)
     t0 = time.perf_counter()
-    stack = GPT2Stack(params, 12, dims, bsgs=BSGS, rank=rank, world=world)
+    stack = GPT2Stack(params, 12, dims, bsgs=BSGS, rank=rank, world=world, mode=args.gpt2_mode)
     keys, sk = blb.keygen(params, bi.crypto_key(4, 5), stack.rotation_steps(), relin=True)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
@@ -375,9 +377,15 @@ def run_gpt2(args, rank: int, world: int, local: int):
             "data": "synthetic (seeded N(0,1) activations, N(0,0.04^2) weights, seeds 100 + 10 layer + m)",
             "config": {"workload": "GPT2-base 12 layers, L=128, d=768, 12 heads, FFN 3072; per layer the fused-linear "
                                    "step of the BERT-base bench; N=2^16, Q={60,40x4}, P={60}, dnum=5",
-                       "plaintexts": ("resident (this rank's share of all 12 layers fits)" if stack.resident else
-                                      "re-encoded on the device per layer from resident float64 weights (680 GB of "
-                                      "packed plaintexts for 12 layers exceed one GPU; resident at 8 GPUs)"),
+                       "plaintexts": {
+                           "resident": "resident (this rank's share of all 12 layers fits)",
+                           "coeffs": "680 GB of packed plaintexts for 12 layers exceed one GPU: the weights stay "
+                                     "resident as 5-byte rounded encode coefficients (118 GB for 12 layers) and each "
+                                     "MatMul's plaintexts are expanded on the device (residues, NTT, packing) right "
+                                     "before it, inside the timed step",
+                           "reencode": "re-encoded on the device per layer from resident float64 weights (680 GB of "
+                                       "packed plaintexts for 12 layers exceed one GPU)"}[stack.mode],
+                       "gpt2_mode": stack.mode,
                        "bsgs": dict(BSGS), "parallelism": "dp%d" % world},
             "gpu_launches": ctr["launches"], "counters_per_step": {k: v / args.steps for k, v in ctr.items()},
             "clocks": clk, "setup_s": t_setup}), flush=True)
@@ -608,6 +616,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-f2", action="store_true")
     ap.add_argument("--dims", default="base", choices=["base", "large"])
+    ap.add_argument("--gpt2-mode", default=None, choices=[None, "resident", "coeffs", "reencode"],
+                    help="config 5 plaintext storage (model.GPT2Stack; default: by memory budget)")
     ap.add_argument("--model", default="layer", choices=["layer", "gpt2"],
                     help="gpt2: config 5, the 12-layer GPT2-base stack with per-layer on-device re-encode")
     ap.add_argument("--preset", default="bert", choices=["bert", "bert_dnum1"],

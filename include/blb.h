@@ -362,6 +362,20 @@ blb_status blb_matmul_pt_bytes(const blb_matmul_plan *plan, int out_first, int o
 blb_status blb_matmul_encode_weights(const blb_matmul_plan *plan, const double *W, int out_first, int out_count,
                                      uint64_t *pt_dev, void *stream);
 
+/* Config 5 (many layers on one GPU): the weights of a slice in
+ * a compact, prime-independent form -- the rounded integer coefficients m_k = round(scale * iDFT(z))_k
+ * of each plaintext (the first half of blb_matmul_encode_weights: slots, inverse embedding, rounding),
+ * 5 bytes each (40-bit two's complement: per plaintext N low 32-bit words then N high bytes; opaque).
+ * blb_matmul_coeff_bytes gives the size.  blb_matmul_encode_coeffs (offline, synchronises) fails with
+ * BLB_E_OVERFLOW if some |m_k| >= 2^39.  blb_matmul_coeffs_to_pts (no synchronisation) expands them --
+ * residues mod q_0..q_level, NTT, the blocked width-packed layout -- into pt_dev, bit-identical to
+ * blb_matmul_encode_weights of the same W and slice.  coef_dev, pt_dev: device memory, caller-owned. */
+blb_status blb_matmul_coeff_bytes(const blb_matmul_plan *plan, int out_first, int out_count, size_t *bytes);
+blb_status blb_matmul_encode_coeffs(const blb_matmul_plan *plan, const double *W, int out_first, int out_count,
+                                    void *coef_dev, void *stream);
+blb_status blb_matmul_coeffs_to_pts(const blb_matmul_plan *plan, const void *coef_dev, int out_first, int out_count,
+                                    uint64_t *pt_dev, void *stream);
+
 size_t blb_matmul_workspace_bytes(const blb_matmul_plan *plan, int out_count);
 
 /* Evaluate outputs [out_first, out_first+out_count) of the plan on the n_in

@@ -109,6 +109,9 @@ def lib() -> ctypes.CDLL:
             "blb_matmul_plan_rotations": ([vp, vp, ip], ctypes.c_int),
             "blb_matmul_pt_count": ([vp, ctypes.c_int, ctypes.c_int, ip], ctypes.c_int),
             "blb_matmul_encode_weights": ([vp, vp, ctypes.c_int, ctypes.c_int, vp, vp], ctypes.c_int),
+            "blb_matmul_coeff_bytes": ([vp, ctypes.c_int, ctypes.c_int, vp], ctypes.c_int),
+            "blb_matmul_encode_coeffs": ([vp, vp, ctypes.c_int, ctypes.c_int, vp, vp], ctypes.c_int),
+            "blb_matmul_coeffs_to_pts": ([vp, vp, ctypes.c_int, ctypes.c_int, vp, vp], ctypes.c_int),
             "blb_matmul_pt_bytes": ([vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
             "blb_matmul_workspace_bytes": ([vp, ctypes.c_int], ctypes.c_size_t),
             "blb_ct_pt_matmul": ([vp, vp, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t,
@@ -641,6 +644,38 @@ class MatmulPlan:
         pts = torch.empty(n, dtype=torch.int64, device="cuda") if out is None else out
         assert pts.numel() >= n
         _check(lib().blb_matmul_encode_weights(self._h, wptr, out_first, out_count, _ptr(pts), _stream()))
+        return pts
+
+    def _wptr(self, W):
+        if isinstance(W, torch.Tensor):
+            assert W.dtype == torch.float64 and W.is_contiguous() and tuple(W.shape) == self.w_shape
+            return W, ctypes.c_void_p(W.data_ptr())
+        W = np.ascontiguousarray(W, dtype=np.float64)
+        assert W.shape == self.w_shape
+        return W, W.ctypes.data_as(ctypes.c_void_p)
+
+    def encode_coeffs(self, W, out_first: int = 0, out_count: int | None = None,
+                      out: torch.Tensor | None = None) -> torch.Tensor:
+        """Compact prime-independent weights of the slice (5-byte coefficients, opaque uint8 buffer)."""
+        out_count = self.n_out - out_first if out_count is None else out_count
+        W, wptr = self._wptr(W)
+        nbytes = ctypes.c_size_t(0)
+        _check(lib().blb_matmul_coeff_bytes(self._h, out_first, out_count, ctypes.byref(nbytes)))
+        coef = torch.empty(max(1, nbytes.value), dtype=torch.uint8, device="cuda") if out is None else out
+        assert coef.numel() >= nbytes.value
+        _check(lib().blb_matmul_encode_coeffs(self._h, wptr, out_first, out_count, _ptr(coef), _stream()))
+        return coef
+
+    def coeffs_to_pts(self, coef: torch.Tensor, out_first: int = 0, out_count: int | None = None,
+                      out: torch.Tensor | None = None) -> torch.Tensor:
+        """Expand encode_coeffs output into the plaintext buffer encode_weights would produce (no sync)."""
+        out_count = self.n_out - out_first if out_count is None else out_count
+        nbytes = ctypes.c_size_t(0)
+        _check(lib().blb_matmul_pt_bytes(self._h, out_first, out_count, ctypes.byref(nbytes)))
+        n = max(1, (nbytes.value + 7) // 8)
+        pts = torch.empty(n, dtype=torch.int64, device="cuda") if out is None else out
+        assert pts.numel() >= n
+        _check(lib().blb_matmul_coeffs_to_pts(self._h, _ptr(coef), out_first, out_count, _ptr(pts), _stream()))
         return pts
 
     def workspace_bytes(self, out_count: int | None = None) -> int:

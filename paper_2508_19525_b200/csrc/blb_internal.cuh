@@ -495,6 +495,10 @@ blb_status launch_rescale(const blb_params *P, const u64 *in, int level, int n_p
 blb_status launch_encode(const blb_params *P, const double *slots, int n_pts, double scale, int level, u64 *out,
                          double *dd_scratch, int *d_flag, cudaStream_t st, int np_ext = 0);
 size_t encode_scratch_doubles(const blb_params *P, int n_pts);
+blb_status launch_encode_coef5(const blb_params *P, const double *slots, int n_pts, double scale, unsigned char *coef,
+                               double *buf, int *d_flag, cudaStream_t st);
+blb_status launch_coef5_to_rns(const blb_params *P, const unsigned char *coef, int n_pts, int level, u64 *out,
+                               cudaStream_t st);
 
 // MAC: acc[o] = sum_{e in [ent_start[o0+o], ent_start[o0+o+1])} pt[ent_pt[e] or e - e_base] (.) R[ent_r[e]]
 // (pt entries [k][N], R entries [2][k][N], acc [n_o][2][k][N]; 128-bit lazy accumulation)

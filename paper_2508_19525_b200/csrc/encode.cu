@@ -155,27 +155,26 @@ __global__ void __launch_bounds__(kTB) k_enc16_B(double *buf, const double *zeta
     }
 }
 
-// coefficient k = round_half_even(Re(buf[k]) * scale / N), residues mod q_0..q_level
-__global__ void k_encode_finalize(const double *buf, u64 *out, Primes pr, double scale, int level, int logN,
-                                  int *flag, int np_ext, int Kfull) {
-    const int N = 1 << logN;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const int p = blockIdx.y;
-    if (k >= N) return;
-    const double *b = buf + ((long long)p * N + k) * 4;
+// coefficient k = round_half_even(Re(buf[k]) * scale / N) (false: |.| >= 2^52, flag set)
+__device__ __forceinline__ bool enc_round(const double *b, double scale, int logN, int *flag, long long &c) {
     dd v = {b[0], b[1]};
     v = dd_mul_d(v, scale);
     v = {ldexp(v.hi, -logN), ldexp(v.lo, -logN)};  // exact division by N
     if (!(fabs(v.hi) < 4503599627370496.0)) {     // 2^52
         atomicExch(flag, 1);
-        return;
+        return false;
     }
     double r = rint(v.hi);
     const double d = (v.hi - r) + v.lo;  // v.hi - r is exact
     const bool odd = fmod(r, 2.0) != 0.0;
     if (d > 0.5 || (d == 0.5 && odd)) r += 1.0;
     else if (d < -0.5 || (d == -0.5 && odd)) r -= 1.0;
-    const long long c = (long long)r;
+    c = (long long)r;
+    return true;
+}
+// residues of the signed coefficient c mod q_0..q_level (and the np_ext special primes) of plaintext p
+__device__ __forceinline__ void enc_residues(long long c, u64 *out, const Primes &pr, int level, int np_ext, int Kfull,
+                                             int p, int k, int N) {
     const int k1 = level + 1 + np_ext;
     for (int i = 0; i < k1; i++) {
         const ModConst &mc = pr.m[i <= level ? i : Kfull + (i - level - 1)];
@@ -187,6 +186,46 @@ __global__ void k_encode_finalize(const double *buf, u64 *out, Primes pr, double
         }
         out[((long long)p * k1 + i) * N + k] = res;
     }
+}
+// coefficient k = round_half_even(Re(buf[k]) * scale / N), residues mod q_0..q_level
+__global__ void k_encode_finalize(const double *buf, u64 *out, Primes pr, double scale, int level, int logN,
+                                  int *flag, int np_ext, int Kfull) {
+    const int N = 1 << logN;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int p = blockIdx.y;
+    if (k >= N) return;
+    long long c;
+    if (!enc_round(buf + ((long long)p * N + k) * 4, scale, logN, flag, c)) return;
+    enc_residues(c, out, pr, level, np_ext, Kfull, p, k, N);
+}
+// Compact coefficient form (config 5, blb_matmul_encode_coeffs): the same rounded coefficient c,
+// stored as 40-bit two's complement in 5 bytes -- plaintext p: N low 32-bit words, then N high bytes --
+// when |c| < 2^39 (flag = 2 otherwise)
+__global__ void k_encode_coef5(const double *buf, unsigned char *coef, double scale, int logN, int *flag) {
+    const int N = 1 << logN;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int p = blockIdx.y;
+    if (k >= N) return;
+    long long c;
+    if (!enc_round(buf + ((long long)p * N + k) * 4, scale, logN, flag, c)) return;
+    if (c >= (1ll << 39) || c < -(1ll << 39)) {
+        atomicExch(flag, 2);
+        return;
+    }
+    unsigned char *b = coef + (long long)p * 5 * N;
+    reinterpret_cast<uint32_t *>(b)[k] = (uint32_t)(unsigned long long)c;
+    b[4 * N + k] = (unsigned char)((unsigned long long)c >> 32);
+}
+__global__ void k_coef5_residues(const unsigned char *coef, u64 *out, Primes pr, int level, int logN) {
+    const int N = 1 << logN;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int p = blockIdx.y;
+    if (k >= N) return;
+    const unsigned char *b = coef + (long long)p * 5 * N;
+    const unsigned long long u = (unsigned long long)reinterpret_cast<const uint32_t *>(b)[k] |
+                                 ((unsigned long long)b[4 * N + k] << 32);
+    const long long c = (long long)(u << 24) >> 24;  // sign-extend bit 39
+    enc_residues(c, out, pr, level, 0, 0, p, k, N);
 }
 
 // centred lift of the q_0 residue -> double-double complex (imag 0)
@@ -327,6 +366,42 @@ blb_status launch_encode(const blb_params *P, const double *slots, int n_pts, do
     rb.base = out; rb.poly_stride = (long long)(level + 1 + np_ext) * N; rb.n_polys = n_pts; rb.limbs = level + 1 + np_ext;
     rb.limb0 = 0;
     for (int i = 0; i < rb.limbs; i++) rb.prime[i] = i <= level ? i : P->K + (i - level - 1);
+    return launch_ntt(P, rb, false, st);
+}
+
+// slots -> compact 5-byte coefficients (k_encode_coef5); flag: 1 = |c| >= 2^52, 2 = |c| >= 2^39
+blb_status launch_encode_coef5(const blb_params *P, const double *slots, int n_pts, double scale, unsigned char *coef,
+                               double *buf, int *d_flag, cudaStream_t st) {
+    const int N = P->N, logN = P->logN;
+    if (n_pts <= 0) return BLB_OK;
+    dim3 gs((N / 2 + kTB - 1) / kTB, n_pts);
+    k_scatter<<<gs, kTB, 0, st>>>(slots, P->d_slot_pos, buf, n_pts, N);
+    if (logN == 16) {
+        constexpr size_t smem = (size_t)kEncElems * 32;
+        blb_smem_optin(k_enc16_A, smem);
+        blb_smem_optin(k_enc16_B, smem);
+        k_enc16_A<<<dim3(N / kEncElems, n_pts), kTB, smem, st>>>(buf, P->d_zeta);
+        k_enc16_B<<<dim3(256 / (kEncElems / 256), n_pts), kTB, smem, st>>>(buf, P->d_zeta);
+    } else {
+        for (int m = N / 2; m >= 1; m >>= 1) k_stage<<<gs, kTB, 0, st>>>(buf, P->d_zeta, m, logN, 1);
+    }
+    k_encode_coef5<<<dim3((N + kTB - 1) / kTB, n_pts), kTB, 0, st>>>(buf, coef, scale, logN, d_flag);
+    BLB_COUNT_LAUNCH(logN == 16 ? 4 : 2 + logN);
+    BLB_CHECK_LAUNCH();
+    return BLB_OK;
+}
+// compact coefficients -> NTT-form residues mod q_0..q_level (out [n_pts][level+1][N]): identical to
+// launch_encode's output for the same slots
+blb_status launch_coef5_to_rns(const blb_params *P, const unsigned char *coef, int n_pts, int level, u64 *out,
+                               cudaStream_t st) {
+    const int N = P->N;
+    if (n_pts <= 0) return BLB_OK;
+    k_coef5_residues<<<dim3((N + kTB - 1) / kTB, n_pts), kTB, 0, st>>>(coef, out, P->pr, level, P->logN);
+    BLB_COUNT_LAUNCH(1);
+    BLB_CHECK_LAUNCH();
+    RowBatch rb{};
+    rb.base = out; rb.poly_stride = (long long)(level + 1) * N; rb.n_polys = n_pts; rb.limbs = level + 1; rb.limb0 = 0;
+    for (int i = 0; i < rb.limbs; i++) rb.prime[i] = i;
     return launch_ntt(P, rb, false, st);
 }
 

@@ -869,6 +869,94 @@ extern "C" blb_status blb_matmul_encode_weights(const blb_matmul_plan *pl, const
     return BLB_OK;
 }
 
+// Config 5 (12 layers on one GPU): the prime-independent half of the encode kept in compact form.
+extern "C" blb_status blb_matmul_coeff_bytes(const blb_matmul_plan *pl, int out_first, int out_count, size_t *bytes) {
+    if (!pl || !bytes) return BLB_E_INVALID_ARG;
+    BLB_TRY(check_slice(pl, out_first, out_count));
+    const size_t n = (size_t)(pl->ent_start[(out_first + out_count) * pl->G] - pl->ent_start[out_first * pl->G]);
+    *bytes = n * 5 * (size_t)pl->P->N;
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_matmul_encode_coeffs(const blb_matmul_plan *pl, const double *W, int out_first, int out_count,
+                                               void *coef_dev, void *stream) {
+    if (!pl || !W || !coef_dev) return BLB_E_INVALID_ARG;
+    BLB_TRY(check_slice(pl, out_first, out_count));
+    const blb_params *P = pl->P;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int e0 = pl->ent_start[out_first * pl->G];
+    const int e1 = pl->ent_start[(out_first + out_count) * pl->G];
+    const size_t ne_total = pl->ent_b.size();
+    double *dW = nullptr, *slots = nullptr, *buf = nullptr;
+    int *flag = nullptr;
+    const int chunk = 64;
+    BLB_CUDA_TRY(cudaMallocAsync(&dW, sizeof(double) * (size_t)pl->w_rows * pl->w_cols, st));
+    BLB_CUDA_TRY(cudaMemcpyAsync(dW, W, sizeof(double) * (size_t)pl->w_rows * pl->w_cols, cudaMemcpyDefault, st));
+    BLB_CUDA_TRY(cudaMallocAsync(&slots, sizeof(double) * (size_t)chunk * pl->n, st));
+    BLB_CUDA_TRY(cudaMallocAsync(&buf, sizeof(double) * encode_scratch_doubles(P, chunk), st));
+    BLB_CUDA_TRY(cudaMallocAsync(&flag, sizeof(int), st));
+    BLB_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    PlanDev pd{pl->L, pl->n, pl->c, pl->B, pl->G, pl->w_rows, pl->w_cols, pl->nblk_in, pl->D_out, pl->packing,
+               pl->heads, pl->dh};
+    const double scale = (double)P->mod[pl->level];  // reading S6: plaintext scale = q_level
+    unsigned char *cb = reinterpret_cast<unsigned char *>(coef_dev);
+    blb_status s = BLB_OK;
+    for (int e = e0; e < e1 && s == BLB_OK; e += chunk) {
+        const int cnt = std::min(chunk, e1 - e);
+        k_build_slots<<<dim3((pl->n + kTB - 1) / kTB, cnt), kTB, 0, st>>>(pd, pl->d_ent, pl->d_ent + ne_total, e, dW,
+                                                                         pl->d_col_map, slots);
+        BLB_COUNT_LAUNCH(1);
+        s = launch_encode_coef5(P, slots, cnt, scale, cb + (size_t)(e - e0) * 5 * P->N, buf, flag, st);
+    }
+    int h_flag = 0;
+    cudaMemcpyAsync(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(dW, st);
+    cudaFreeAsync(slots, st);
+    cudaFreeAsync(buf, st);
+    cudaFreeAsync(flag, st);
+    BLB_CUDA_TRY(cudaStreamSynchronize(st));
+    if (s != BLB_OK) return s;
+    if (h_flag == 1) {
+        blb_set_error("encode overflow: |scale * m_k| >= 2^52");
+        return BLB_E_OVERFLOW;
+    }
+    if (h_flag == 2) {
+        blb_set_error("blb_matmul_encode_coeffs: a coefficient needs more than 40 bits (use blb_matmul_encode_weights)");
+        return BLB_E_OVERFLOW;
+    }
+    return BLB_OK;
+}
+
+extern "C" blb_status blb_matmul_coeffs_to_pts(const blb_matmul_plan *pl, const void *coef_dev, int out_first,
+                                               int out_count, uint64_t *pt_dev, void *stream) {
+    if (!pl || !coef_dev || !pt_dev) return BLB_E_INVALID_ARG;
+    BLB_TRY(check_slice(pl, out_first, out_count));
+    const blb_params *P = pl->P;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int e0 = pl->ent_start[out_first * pl->G];
+    const int e1 = pl->ent_start[(out_first + out_count) * pl->G];
+    const size_t ne_total = pl->ent_b.size();
+    const int k = pl->level + 1;
+    const int chunk = 256;  // 256 plaintexts x k limbs per NTT batch
+    u64 *tmp = nullptr;
+    BLB_CUDA_TRY(cudaMallocAsync(&tmp, sizeof(u64) * (size_t)std::min(chunk, std::max(1, e1 - e0)) * k * P->N, st));
+    const unsigned char *cb = reinterpret_cast<const unsigned char *>(coef_dev);
+    blb_status s = BLB_OK;
+    for (int e = e0; e < e1 && s == BLB_OK; e += chunk) {
+        const int cnt = std::min(chunk, e1 - e);
+        s = launch_coef5_to_rns(P, cb + (size_t)(e - e0) * 5 * P->N, cnt, pl->level, tmp, st);
+        if (s == BLB_OK) {
+            k_block_pts<<<dim3((P->N + kTB - 1) / kTB, k, cnt), kTB, 0, st>>>(
+                tmp, reinterpret_cast<unsigned char *>(pt_dev), pl->d_ent_start, pl->d_ent + ne_total, e, e0, k, P->N,
+                pt_layout(pl));
+            BLB_COUNT_LAUNCH(1);
+        }
+    }
+    cudaFreeAsync(tmp, st);
+    BLB_CHECK_LAUNCH();
+    return s;
+}
+
 // workspace layout (u64 elements)
 struct MatmulWs {
     size_t ext_in, coef, R, ks, acc, gext, gcoef, gks, rot, yext, resc, total;

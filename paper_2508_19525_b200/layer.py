@@ -175,6 +175,7 @@ class FusedLinearLayer:
             if n > MAX_OUT:
                 raise ValueError("%s: %d output ciphertexts exceed the mask-id range" % (name, n))
         self.pts, self.ws, self.outs = {}, None, {}
+        self.pre_ct_pt = None   # optional hook(name) run right before each ct-pt MatMul (model.GPT2Stack)
         self.acc = None
         self.seq = 0      # inference counter: enters every mask id (fresh masks per step)
 
@@ -303,6 +304,8 @@ class FusedLinearLayer:
             if count == 0 and self.world == 1:
                 continue
             src = self.softmax_v(keys, inputs["sv_s"], inputs["sv_v"]) if name == "oproj" else inputs[name]
+            if self.pre_ct_pt is not None:
+                self.pre_ct_pt(name)
             outs = self.ct_pt(keys, name, src)
             if name == "qkv":
                 qk_in = self.gather_qk_operands(outs)

@@ -4,13 +4,17 @@ GPT2-base has the BERT-base layer shape (d = 768, 12 heads, FFN 3072; L = 128 to
 BASELINE.json sets it, the paper ran 64, reading S25), so every layer is one
 layer.FusedLinearLayer step (QKV + Q K^T + masks, Softmax x V + W_O + mask, FFN1 + mask,
 FFN2 + mask) with its own weights.  Its packed plaintexts are 56.7 GB per layer -- 680 GB for
-12 layers, far beyond one B200's 180 GB -- so the weights of every layer stay resident on the
-device as float64 matrices (57 MB per layer) and each layer's plaintexts are re-encoded on the
-device (row a0: slot build, double-double encode, NTT, width-packed blocked layout) into ONE
-reused plaintext buffer per plan right before that layer's step.  At world = 8
-each rank's window holds 1/8 of every layer's plaintexts (85 GB for all 12), so the stack can
-instead keep them resident: `resident=True` encodes every layer once (setup) and skips the
-re-encode.  Synthetic weights: SURVEY 8(d) config 5, seeds 100 + 10 * layer + m.
+12 layers, far beyond one B200's 180 GB.  Three storage modes (`mode`):
+* "resident": every layer's packed plaintexts stay on the device (e.g. 1/8 per rank at world 8:
+  85 GB for all 12 layers) -- no per-layer work;
+* "coeffs" (the 1-GPU default): every layer's weights are kept as their compact, prime-independent
+  encode -- the rounded integer coefficients of each plaintext, 5 bytes each
+  (blb_matmul_encode_coeffs: 9.8 GB per layer, 118 GB for 12) -- and right before each ct-pt
+  MatMul its plaintexts are expanded on the device (residues mod q_0..q_l, NTT, packed layout:
+  blb_matmul_coeffs_to_pts) into ONE buffer shared by the four MatMuls (17 GB);
+* "reencode": float64 weights resident (57 MB per layer), each layer re-encoded from them
+  (slot build, double-double inverse embedding, rounding, NTT, packing) before its step.
+Synthetic weights: SURVEY 8(d) config 5, seeds 100 + 10 * layer + m.
 """
 from __future__ import annotations
 
@@ -32,13 +36,17 @@ def gpt2_layer_weights(layer: int, dims: Dims) -> list:
 
 class GPT2Stack:
     def __init__(self, params: blb.Params, n_layers: int = 12, dims: Dims = Dims(), bsgs: dict | None = None,
-                 rank: int = 0, world: int = 1, resident: bool | None = None, budget_bytes: float = 120e9):
-        """resident: keep every layer's plaintexts on the device (None: when this rank's share of all
-        layers fits budget_bytes -- e.g. 1/8 of 680 GB at 8 GPUs -- else re-encode per layer)."""
+                 rank: int = 0, world: int = 1, resident: bool | None = None, budget_bytes: float = 120e9,
+                 mode: str | None = None):
+        """mode: "resident" / "coeffs" / "reencode" (module docstring); None picks resident when this
+        rank's packed plaintexts of all layers fit budget_bytes, else coeffs when the compact
+        coefficients fit it, else reencode.  resident=True/False is the older spelling of
+        mode="resident" / the default non-resident mode."""
         self.p, self.n_layers, self.dims = params, n_layers, dims
         self.layer = FusedLinearLayer(params, dims, rank, world, bsgs=bsgs)
         self.w_dev = []      # per layer: device float64 matrices in the plans' shapes
         self.pts = []        # resident mode: per layer the encoded plaintexts
+        self.coefs = []      # coeffs mode: per layer the compact coefficients of every plan
         for l in range(n_layers):
             WQ, WK, WV, WO, W1, W2 = gpt2_layer_weights(l, dims)
             Wqkv = np.concatenate([WQ, WK, WV], axis=1)
@@ -51,23 +59,54 @@ class GPT2Stack:
         self.layer.load_weights(*gpt2_layer_weights(0, dims))
         self.loaded = 0
         per_layer = sum(int(t.numel()) * 8 for t in self.layer.pts.values())
-        self.resident = (per_layer * n_layers <= budget_bytes) if resident is None else resident
-        if self.resident:
+        coef_layer = sum(self._coef_bytes(name) for name in self.layer.plans)
+        if mode is None:
+            if resident is not None:
+                mode = "resident" if resident else "coeffs"
+            elif per_layer * n_layers <= budget_bytes:
+                mode = "resident"
+            else:
+                mode = "coeffs" if coef_layer * n_layers <= budget_bytes else "reencode"
+        self.mode = mode
+        self.resident = mode == "resident"
+        if mode == "resident":
             for l in range(n_layers):
                 self.pts.append({k: self._encode(l, k) for k in self.layer.plans})
+        elif mode == "coeffs":
+            # one plaintext buffer shared by the four MatMuls (the largest plan's size)
+            big = max(int(t.numel()) for t in self.layer.pts.values())
+            shared = torch.empty(big, dtype=torch.int64, device="cuda")
+            self.layer.pts = {k: shared[:int(t.numel())] for k, t in self.layer.pts.items()}
+            torch.cuda.empty_cache()
+            for l in range(n_layers):
+                self.coefs.append({k: self._slice_call(k, "encode_coeffs", self.w_dev[l][k]) for k in self.layer.plans})
+            self.layer.pre_ct_pt = self._expand
+            self.loaded = -1
 
-    def _encode(self, l: int, name: str, out=None) -> torch.Tensor:
+    def _slice_call(self, name: str, method: str, arg, out=None):
         pl = self.layer.plans[name]
         if self.layer.world == 1:
             first, count = self.layer.slices[name]
-            return pl.encode_weights(self.w_dev[l][name], first, count, out=out)
-        return pl.encode_weights(self.w_dev[l][name], out=out)
+            return getattr(pl, method)(arg, first, count, out=out)
+        return getattr(pl, method)(arg, out=out)
+
+    def _coef_bytes(self, name: str) -> int:
+        pl = self.layer.plans[name]
+        first, count = self.layer.slices[name] if self.layer.world == 1 else (0, pl.n_out)
+        return pl.pt_count(first, count) * 5 * self.p.N
+
+    def _encode(self, l: int, name: str, out=None) -> torch.Tensor:
+        return self._slice_call(name, "encode_weights", self.w_dev[l][name], out=out)
+
+    def _expand(self, name: str):
+        """coeffs mode, right before the ct-pt MatMul `name` of the loaded layer."""
+        self._slice_call(name, "coeffs_to_pts", self.coefs[self.loaded][name], out=self.layer.pts[name])
 
     def load_layer(self, l: int):
-        """Make layer l's plaintexts the ones the layer step streams (re-encode on the device)."""
-        if self.resident:
+        """Make layer l's plaintexts the ones the layer step streams."""
+        if self.mode == "resident":
             self.layer.pts = self.pts[l]
-        elif self.loaded != l:
+        elif self.mode == "reencode" and self.loaded != l:
             for name in self.layer.plans:
                 self._encode(l, name, out=self.layer.pts[name])
         self.loaded = l

@@ -1,8 +1,9 @@
-"""Config 5 (GPT2-base, 12 layers): the stack re-encodes each layer's plaintexts on the device
-from device-resident float64 weights into one reused buffer (model.GPT2Stack).  The device
-encode equals the host-weight encode bit for bit, and a 2-layer stack returns, layer by layer,
-exactly what a freshly built layer with that layer's weights returns (itself pinned against the
-oracle layer step in test_gpu_layer)."""
+"""Config 5 (GPT2-base, 12 layers): model.GPT2Stack keeps every layer's weights on the device (as compact
+encode coefficients expanded before each MatMul, as float64 weights re-encoded per layer, or as resident
+plaintexts).  The device encode equals the host-weight encode bit for bit, the compact coefficients
+expand to exactly the encoded plaintexts, and a 2-layer stack returns, layer by layer and in every mode,
+exactly what a freshly built layer with that layer's weights returns (itself pinned against the oracle
+layer step in test_gpu_layer)."""
 import numpy as np
 import pytest
 import torch
@@ -47,10 +48,27 @@ def inputs_for(params, layer, sk, seed):
     return out
 
 
-@pytest.mark.parametrize("resident", [False, True])
-def test_two_layer_stack_matches_per_layer(resident):
+def test_compact_coeffs_expand_to_encode_weights():
+    """blb_matmul_coeffs_to_pts(blb_matmul_encode_coeffs(W)) is bit-identical to blb_matmul_encode_weights(W),
+    for a whole plan and for an output slice, at the toy ring and at N = 2^16."""
+    for preset, (L, din, dout, B, lvl) in ((bi.QKTOY, (32, 64, 96, 8, 4)), (bi.BERT, (128, 256, 128, 4, 4))):
+        params = blb.Params.from_preset(preset)
+        W = np.random.default_rng(4).normal(0, 0.05, (din, dout))
+        pl = blb.MatmulPlan(params, L, din, dout, bsgs_B=B, level=lvl)
+        slices = [(0, pl.n_out)] + ([(1, pl.n_out - 2)] if pl.n_out >= 3 else [])
+        for first, count in slices:
+            ref = pl.encode_weights(W, first, count)
+            coef = pl.encode_coeffs(torch.tensor(W, dtype=torch.float64, device="cuda"), first, count)
+            got = pl.coeffs_to_pts(coef, first, count, out=torch.zeros_like(ref))
+            torch.cuda.synchronize()
+            assert torch.equal(got, ref)
+
+
+@pytest.mark.parametrize("mode", ["reencode", "resident", "coeffs"])
+def test_two_layer_stack_matches_per_layer(mode):
     params = blb.Params.from_preset(bi.QKTOY)
-    stack = GPT2Stack(params, 2, DIMS, bsgs=BSGS, resident=resident)
+    stack = GPT2Stack(params, 2, DIMS, bsgs=BSGS, mode=mode)
+    assert stack.mode == mode
     keys, sk = blb.keygen(params, bi.crypto_key(4, 81), stack.rotation_steps(), relin=True)
     ins = [inputs_for(params, stack.layer, sk, 1 + l) for l in range(2)]
     mk = bi.crypto_key(3, 81)
