@@ -469,6 +469,17 @@ struct NttFuse {
     int E = 0, k = 0;
     PinvTab pinv;
     KsJobs jobs;
+    // pro = 3 (blb_matmul_coeffs_to_pts): row (p, l) is plaintext p's compact 5-byte coefficients
+    //          (coef + p 5N: N low words, N high bytes) reduced mod the row's prime;
+    // epi = 2: the last (forward) pass writes plaintext p (plan entry pk_e0 + p) limb l straight into the
+    //          blocked width-packed MAC layout (k_block_pts's addressing)
+    const unsigned char *coef = nullptr;
+    unsigned char *pk_dst = nullptr;
+    const int *pk_ent_o = nullptr, *pk_ent_start = nullptr;
+    int pk_e0 = 0, pk_ebase = 0;
+    long long pk_bpp = 0;
+    long long pk_loff[BLB_MAXP] = {};
+    int pk_w[BLB_MAXP] = {};
 };
 // double hoisting: rotations kept in Q_l u P written to jobs[t].out ([2][E][N]);
 // ModDown of n contiguous extended ciphertexts u [n][2][E][N] -> out [n][2][k][N]

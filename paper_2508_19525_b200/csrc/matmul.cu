@@ -942,13 +942,32 @@ extern "C" blb_status blb_matmul_coeffs_to_pts(const blb_matmul_plan *pl, const 
     BLB_CUDA_TRY(cudaMallocAsync(&tmp, sizeof(u64) * (size_t)std::min(chunk, std::max(1, e1 - e0)) * k * P->N, st));
     const unsigned char *cb = reinterpret_cast<const unsigned char *>(coef_dev);
     blb_status s = BLB_OK;
+    const PtLayout lay = pt_layout(pl);
     for (int e = e0; e < e1 && s == BLB_OK; e += chunk) {
         const int cnt = std::min(chunk, e1 - e);
+        if (P->logN == 16) {
+            // one fused launch pair: residues in the first NTT pass, packed layout in the last
+            RowBatch rb{};
+            rb.base = tmp; rb.poly_stride = (long long)k * P->N; rb.n_polys = cnt; rb.limbs = k; rb.limb0 = 0;
+            for (int i = 0; i < k; i++) rb.prime[i] = i;
+            NttFuse fz{};
+            fz.pro = 3;
+            fz.epi = 2;
+            fz.coef = cb + (size_t)(e - e0) * 5 * P->N;
+            fz.pk_dst = reinterpret_cast<unsigned char *>(pt_dev);
+            fz.pk_ent_o = pl->d_ent + ne_total;
+            fz.pk_ent_start = pl->d_ent_start;
+            fz.pk_e0 = e;
+            fz.pk_ebase = e0;
+            fz.pk_bpp = lay.bpp;
+            for (int i = 0; i < k; i++) { fz.pk_loff[i] = lay.loff[i]; fz.pk_w[i] = lay.w[i]; }
+            s = launch_ntt_fused(P, rb, false, fz, st);
+            continue;
+        }
         s = launch_coef5_to_rns(P, cb + (size_t)(e - e0) * 5 * P->N, cnt, pl->level, tmp, st);
         if (s == BLB_OK) {
             k_block_pts<<<dim3((P->N + kTB - 1) / kTB, k, cnt), kTB, 0, st>>>(
-                tmp, reinterpret_cast<unsigned char *>(pt_dev), pl->d_ent_start, pl->d_ent + ne_total, e, e0, k, P->N,
-                pt_layout(pl));
+                tmp, reinterpret_cast<unsigned char *>(pt_dev), pl->d_ent_start, pl->d_ent + ne_total, e, e0, k, P->N, lay);
             BLB_COUNT_LAUNCH(1);
         }
     }

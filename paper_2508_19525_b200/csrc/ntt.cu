@@ -271,6 +271,20 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
             const size_t addr = STRIDED ? (((size_t)mid << 8) + c0 + colA) : (((size_t)(c0 + colA) << 8) + mid);
             v[m] = from_u64(src[addr]);
         }
+    } else if (PRO == 3) {  // compact 5-byte signed coefficients -> residues mod the row's prime
+        const unsigned char *cb = fz.coef + (long long)p * 5 * N;
+        const ModConst &mt = pr.m[pi];
+#pragma unroll
+        for (int m = 0; m < 16; m++) {
+            const int mid = tcA + 16 * m;
+            const uint32_t kx = STRIDED ? (((uint32_t)mid << 8) + c0 + colA) : (((uint32_t)(c0 + colA) << 8) + mid);
+            const unsigned long long ub =
+                (unsigned long long)reinterpret_cast<const uint32_t *>(cb)[kx] | ((unsigned long long)cb[4 * N + kx] << 32);
+            const long long c = (long long)(ub << 24) >> 24;
+            u64 a = c < 0 ? (u64)(-c) : (u64)c;
+            if (a >= mt.q) a = mod64(a, mt);
+            v[m] = from_u64(c < 0 && a ? mt.q - a : a);
+        }
     } else if (PRO == 1) {
         const u64 *src = fz.src + (long long)(p / fz.src_div) * fz.src_hi + (long long)(p % fz.src_div) * fz.src_lo;
         const ModConst &mt = pr.m[pi];
@@ -409,6 +423,27 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
                 if (J.out_f64) r = (u64)__double_as_longlong(u2d(r));
             }
             out[gx] = r;
+        }
+    } else if constexpr (EPI == 2) {  // blocked width-packed MAC layout (blb_matmul_coeffs_to_pts)
+        const int e = fz.pk_e0 + p;
+        const int o = fz.pk_ent_o[e];
+        const int e_lo = fz.pk_ent_start[o], n_e = fz.pk_ent_start[o + 1] - e_lo;
+        const int w = fz.pk_w[l];
+        const uint32_t g0 = (uint32_t)(c0 + colA) << 8;  // the thread's 16 coefficients lie in one 512-tile
+        unsigned char *tile = fz.pk_dst + (long long)(e_lo - fz.pk_ebase) * fz.pk_bpp + (long long)n_e * fz.pk_loff[l] +
+                              ((long long)(g0 >> 9) * n_e + (e - e_lo)) * 512 * w;
+#pragma unroll
+        for (int m = 0; m < 16; m++) {
+            u64 x;
+            if constexpr (SMALL) x = canon(v[m], qd, qinv);
+            else x = LZ ? canon16(v[m], q) : canon8(v[m], q);
+            const uint32_t pos = (g0 + tcA + 16 * m) & 511;
+            if (w == 5) {
+                reinterpret_cast<uint32_t *>(tile)[pos] = (uint32_t)x;
+                tile[2048 + pos] = (unsigned char)(x >> 32);
+            } else {
+                reinterpret_cast<u64 *>(tile)[pos] = x;
+            }
         }
     } else {
 #pragma unroll
@@ -680,7 +715,8 @@ blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool invers
     const cudaStream_t st = st0;
     const int rows = rb.n_polys * rb.limbs;
     if (rows == 0) return BLB_OK;
-    if (P->logN != 16 || rows > 65535 || (inverse && (fz.pro != 2 || fz.epi)) || (!inverse && fz.pro == 2)) {
+    if (P->logN != 16 || rows > 65535 || (inverse && (fz.pro != 2 || fz.epi)) || (!inverse && fz.pro == 2) ||
+        ((fz.pro == 3 || fz.epi == 2) && (fz.pro != 3 || fz.epi != 2))) {
         blb_set_error("launch_ntt_fused: N = 2^16 forward batches (or inverse with pro = 2) only");
         return BLB_E_INVALID_ARG;
     }
@@ -715,6 +751,16 @@ blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool invers
             } else {
                 launch_int<true, false, 2, 0>(P, r, g, st, 8, 0, fz);
                 launch_int<true, true>(P, r, g, st, 0, 1, fz);
+            }
+            continue;
+        }
+        if (fz.pro == 3) {  // compact coefficients -> packed plaintexts (blb_matmul_coeffs_to_pts)
+            if (small) {
+                launch_f64<false, true, 3, 0>(P, r, g, st, 0, 0, fz);
+                launch_f64<false, false, 0, 2>(P, r, g, st, 8, 1, fz);
+            } else {
+                launch_int<false, true, 3, 0>(P, r, g, st, 0, 0, fz);
+                launch_int<false, false, 0, 2>(P, r, g, st, 8, 1, fz);
             }
             continue;
         }
