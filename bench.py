@@ -470,10 +470,12 @@ def f2_blocks(dims, args, device: int) -> dict:
     torch.cuda.synchronize()
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("f2_steps")
     e0.record(st)
     for _ in range(args.steps):
         step()
     e1.record(st)
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     step(timed=True)   # one more step with per-chain events (the breakdown, not the headline)
     return {"ms_per_step": e0.elapsed_time(e1) / args.steps, "breakdown_ms": acc_ms,

@@ -211,15 +211,23 @@ __device__ __forceinline__ void bfly_f64(double &X, double &Y, double w, double 
 // bulk copies at the start (twd_s[16 (2^r - 1) + (h - c0) 2^r + j] = twd[2^(8+r) + h 2^r + j]), so the
 // rounds read them from shared memory instead of waiting on dependent L2 loads
 constexpr int kTwsWords = 16 * 255;
-template <bool INV, bool STRIDED, int PRO, int EPI, bool SMALL, bool LZ = false>
+template <bool INV, bool SMALL>
+__device__ __forceinline__ void ntt15_strided(u64 *sm, const RowBatch &rb, const u64 *__restrict__ tw_all,
+                                              const double *__restrict__ twd_all, const Primes &pr, int p, int l);
+template <bool INV, bool STRIDED, int PRO, int EPI, bool SMALL, bool LZ = false, int LOGN = 16>
 __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u64 *__restrict__ tw_all,
                                            const double *__restrict__ twd_all, const Primes &pr, int, int,
                                            const NttFuse &fz, int p, int l, double *tws = nullptr,
                                            uint64_t *twbar = nullptr) {
-    constexpr int logN = 16, N = 1 << logN;
-    // the strided pass runs stages [0, 8), the contiguous one [8, 16); the last pass of a transform is
-    // the contiguous one forward and the strided one inverse (compile-time: no dead epilogue selects)
-    constexpr int s0 = STRIDED ? 0 : 8;
+    if constexpr (LOGN == 15 && STRIDED) {  // N = 2^15: 128-point strided columns (ntt15_strided)
+        ntt15_strided<INV, SMALL>(sm, rb, tw_all, twd_all, pr, p, l);
+        return;
+    }
+    constexpr int logN = LOGN, N = 1 << logN;
+    // the strided pass runs stages [0, 8), the contiguous one [logN - 8, logN) (256-point blocks); the
+    // last pass of a transform is the contiguous one forward and the strided one inverse (compile-time:
+    // no dead epilogue selects)
+    constexpr int s0 = STRIDED ? 0 : logN - 8;
     constexpr bool last = INV == STRIDED;
     u64 *a = rb.base + (long long)p * rb.poly_stride + (long long)(rb.limb0 + l) * N;
     const int pi = rb.prime[l];
@@ -244,7 +252,7 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
             mbar_expect_tx(twbar, kTwsWords * 8u);
 #pragma unroll
             for (int r = 0; r < 8; r++)
-                bulk_g2s(tws + 16 * ((1 << r) - 1), src + (1 << (8 + r)) + (c0 << r), (16u << r) * 8u, twbar);
+                bulk_g2s(tws + 16 * ((1 << r) - 1), src + (1 << (s0 + r)) + (c0 << r), (16u << r) * 8u, twbar);
         }
     }
     // SMALL (q < 2^41): values are doubles; between the two passes they are stored as double bits
@@ -470,6 +478,106 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
     }
 }
 
+// N = 2^15 = 128 x 256: the strided pass transforms 128-point columns (stages 0..6, element
+// j = mid * 256 + lo) for 32 consecutive lo per CTA: round A (stages 0..3) on mid = tc + 8 m, round B
+// (stages 4..6) on mid = 16 tc + m, shared-memory tile [mid][32 columns] with the column index XORed
+// by 2 ((mid >> 4) & 7) (conflict-free for both mappings); the contiguous pass is ntt16_body's with
+// s0 = 7.  Plain transforms only (no fused prologue / epilogue).
+template <bool INV, bool SMALL>
+__device__ __forceinline__ void ntt15_strided(u64 *sm, const RowBatch &rb, const u64 *__restrict__ tw_all,
+                                              const double *__restrict__ twd_all, const Primes &pr, int p, int l) {
+    constexpr int N = 1 << 15;
+    u64 *a = rb.base + (long long)p * rb.poly_stride + (long long)(rb.limb0 + l) * N;
+    const int pi = rb.prime[l];
+    const u64 q = pr.m[pi].q, q4 = 4 * q;
+    const ulonglong2 *twp = reinterpret_cast<const ulonglong2 *>(tw_all + (size_t)pi * 4 * N + (INV ? 2 * N : 0));
+    const double *twd = twd_all + (size_t)pi * 2 * N + (INV ? N : 0);
+    const int t = threadIdx.x;
+    const int c0 = blockIdx.x * 32;
+    const int colA = t & 31, tcA = t >> 5;  // A: mid = tcA + 8 m (a warp: 32 consecutive lo)
+    const int colB = t >> 3, tcB = t & 7;   // B: mid = 16 tcB + m
+    auto ph = [](int mid, int col) { return mid * 32 + (col ^ (((mid >> 4) & 7) << 1)); };
+    using V = typename std::conditional<SMALL, double, u64>::type;
+    const double qd = (double)q, qinv = 1.0 / qd;
+    V v[16];
+    auto to_bits = [&](V x) -> u64 {
+        if constexpr (SMALL) return (u64)__double_as_longlong(x);
+        else return x;
+    };
+    auto from_bits = [&](u64 x) -> V {
+        if constexpr (SMALL) return __longlong_as_double((long long)x);
+        else return x;
+    };
+    auto bf = [&](int m, int dist, int widx) {
+        if constexpr (SMALL) {
+            bfly_f64<INV>(v[m], v[m + dist], twd[widx], qd, qinv);
+        } else {
+            const ulonglong2 tv = twp[widx];
+            bfly<INV>(v[m], v[m + dist], tv.x, tv.y, q, q4);
+        }
+    };
+    auto roundA = [&](int s) {  // stages 0..3: mid distance 64 >> s = 8 (8 >> s)
+        const int dist = 8 >> s;
+#pragma unroll
+        for (int m = 0; m < 16; m++)
+            if (!(m & dist)) bf(m, dist, (1 << s) + (m >> (4 - s)));
+    };
+    auto roundB = [&](int s) {  // stages 4..6: mid distance 4 >> (s - 4)
+        const int dist = 4 >> (s - 4);
+#pragma unroll
+        for (int m = 0; m < 16; m++)
+            if (!(m & dist)) bf(m, dist, (1 << s) + ((16 * tcB + m) >> (7 - s)));
+    };
+    // inverse: the second pass reads the first (contiguous) pass's format (FP64 rows: double bits)
+#pragma unroll
+    for (int m = 0; m < 16; m++) {
+        const u64 x = a[((tcA + 8 * m) << 8) + c0 + colA];
+        if constexpr (SMALL) v[m] = INV ? from_bits(x) : u2d(x);
+        else v[m] = x;
+    }
+    if (!INV) {
+#pragma unroll
+        for (int s = 0; s < 4; s++) roundA(s);
+    }
+#pragma unroll
+    for (int m = 0; m < 16; m++) sm[ph(tcA + 8 * m, colA)] = to_bits(v[m]);
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 16; m++) v[m] = from_bits(sm[ph(16 * tcB + m, colB)]);
+    if (!INV) {
+#pragma unroll
+        for (int s = 4; s < 7; s++) roundB(s);
+    } else {
+#pragma unroll
+        for (int s = 6; s >= 4; s--) roundB(s);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 16; m++) sm[ph(16 * tcB + m, colB)] = to_bits(v[m]);
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 16; m++) v[m] = from_bits(sm[ph(tcA + 8 * m, colA)]);
+    const ModConst &mc = pr.m[pi];
+    if (INV) {
+#pragma unroll
+        for (int s = 3; s >= 0; s--) roundA(s);
+    }
+#pragma unroll
+    for (int m = 0; m < 16; m++) {
+        u64 x;
+        if constexpr (SMALL) {
+            x = INV ? canon(mulr(v[m], (double)mc.ninv, qd, qinv), qd, qinv) : to_bits(v[m]);
+        } else {
+            x = v[m];
+            if (INV) {
+                x = shoup_lazy(x, mc.ninv, mc.ninv_sh, q);
+                if (x >= q) x -= q;
+            }
+        }
+        a[((tcA + 8 * m) << 8) + c0 + colA] = x;
+    }
+}
+
 __device__ __forceinline__ bool ntt16_row(const RowBatch &rb, int &p, int &l) {
     const int row = blockIdx.y;
     if (rb.nsel > 0) {
@@ -503,7 +611,7 @@ __device__ __forceinline__ void copy_own_tile(const RowBatch &rb, const NttFuse 
 #endif
 // integer (Shoup) kernel for the primes >= 2^41, FP64 kernel for the others; a launch covers
 // rows of one kind (launch_ntt splits a mixed batch with RowBatch::sel)
-template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0, bool LZ = false>
+template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0, bool LZ = false, int LOGN = 16>
 __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_int(RowBatch rb, const u64 *__restrict__ tw_all,
                                                                 const double *__restrict__ twd, Primes pr, int s0,
                                                                 int last, const NttFuse fz) {
@@ -513,12 +621,12 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_int(RowBatch rb, cons
         if (PRO == 1 && STRIDED) copy_own_tile(rb, fz, p, l);
         return;
     }
-    ntt16_body<INV, STRIDED, PRO, EPI, false, LZ>(sm, rb, tw_all, twd, pr, s0, last, fz, p, l);
+    ntt16_body<INV, STRIDED, PRO, EPI, false, LZ, LOGN>(sm, rb, tw_all, twd, pr, s0, last, fz, p, l);
 }
 // dynamic shared memory: 4096 residues, then (contiguous pass) the staged twiddles and their mbarrier
 template <bool STRIDED>
 constexpr size_t ntt16_f64_smem() { return STRIDED ? 4096 * 8 : 4096 * 8 + kTwsWords * 8 + 16; }
-template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0>
+template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0, int LOGN = 16>
 __global__ void __launch_bounds__(256, BLB_NTT_F64_MINB) ntt16_f64(RowBatch rb, const u64 *__restrict__ tw_all,
                                                                     const double *__restrict__ twd, Primes pr, int s0,
                                                                     int last, const NttFuse fz) {
@@ -529,7 +637,7 @@ __global__ void __launch_bounds__(256, BLB_NTT_F64_MINB) ntt16_f64(RowBatch rb, 
         return;
     }
     if constexpr (STRIDED) {
-        ntt16_body<INV, STRIDED, PRO, EPI, true>(dsm, rb, tw_all, twd, pr, s0, last, fz, p, l);
+        ntt16_body<INV, STRIDED, PRO, EPI, true, false, LOGN>(dsm, rb, tw_all, twd, pr, s0, last, fz, p, l);
     } else {
         double *tws = reinterpret_cast<double *>(dsm + 4096);
         uint64_t *bar = reinterpret_cast<uint64_t *>(dsm + 4096 + kTwsWords);
@@ -538,16 +646,16 @@ __global__ void __launch_bounds__(256, BLB_NTT_F64_MINB) ntt16_f64(RowBatch rb, 
             mbar_fence_init();
         }
         __syncthreads();
-        ntt16_body<INV, STRIDED, PRO, EPI, true>(dsm, rb, tw_all, twd, pr, s0, last, fz, p, l, tws, bar);
+        ntt16_body<INV, STRIDED, PRO, EPI, true, false, LOGN>(dsm, rb, tw_all, twd, pr, s0, last, fz, p, l, tws, bar);
     }
 }
 
-template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0>
+template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0, int LOGN = 16>
 static void launch_f64(const blb_params *P, const RowBatch &r, dim3 g, cudaStream_t st, int s0, int last,
                        const NttFuse &fz) {
     constexpr size_t smem = ntt16_f64_smem<STRIDED>();
-    if (smem > 48 * 1024) blb_smem_optin(ntt16_f64<INV, STRIDED, PRO, EPI>, smem);
-    ntt16_f64<INV, STRIDED, PRO, EPI><<<g, 256, smem, st>>>(r, P->d_tw, P->d_twd, P->pr, s0, last, fz);
+    if (smem > 48 * 1024) blb_smem_optin(ntt16_f64<INV, STRIDED, PRO, EPI, LOGN>, smem);
+    ntt16_f64<INV, STRIDED, PRO, EPI, LOGN><<<g, 256, smem, st>>>(r, P->d_tw, P->d_twd, P->pr, s0, last, fz);
 }
 // integer-kernel launch: forward rows whose primes are all < 2^60 take the LZ butterflies
 static bool rb_below60(const blb_params *P, const RowBatch &r) {
@@ -556,9 +664,13 @@ static bool rb_below60(const blb_params *P, const RowBatch &r) {
         if (P->mod[r.prime[r.nsel ? r.sel[i] : i]] >= (1ull << 60)) return false;
     return true;
 }
-template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0>
+template <bool INV, bool STRIDED, int PRO = 0, int EPI = 0, int LOGN = 16>
 static void launch_int(const blb_params *P, const RowBatch &r, dim3 g, cudaStream_t st, int s0, int last,
                        const NttFuse &fz) {
+    if constexpr (LOGN != 16) {  // N = 2^15: no LZ (pass 1 has 7 stages; the LZ bound needs whole rounds)
+        ntt16_int<INV, STRIDED, PRO, EPI, false, LOGN><<<g, 256, 0, st>>>(r, P->d_tw, P->d_twd, P->pr, s0, last, fz);
+        return;
+    }
 #ifndef BLB_NTT_LZ
 #define BLB_NTT_LZ 1
 #endif
@@ -651,6 +763,39 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
         else ntt_pass<true><<<grid, kThreads, smem, st>>>(rb, P->d_tw, P->pr, logN, 0, logN, 0, 0, 1);
         BLB_COUNT_LAUNCH(1);
         blb_timing_end(1, t0, st, alg);
+        BLB_CHECK_LAUNCH();
+        return BLB_OK;
+    }
+    if (logN == 15) {  // 128-point strided columns (32 per CTA) + 256-point contiguous blocks (16 per CTA)
+        const NttFuse fz{};
+        RowBatch parts[2];
+        const int np2 = split_rows(P, rb, parts);
+        const NttStreams ss(P, st0, np2);
+        for (int h = 0; h < np2; h++) {
+            const cudaStream_t st = ss.part_stream(h);
+            const RowBatch &r = parts[h];
+            const dim3 g(8, rb_rows(r));
+            if (rb_small(P, r)) {
+                if (!inverse) {
+                    launch_f64<false, true, 0, 0, 15>(P, r, g, st, 0, 0, fz);
+                    launch_f64<false, false, 0, 0, 15>(P, r, g, st, 7, 1, fz);
+                } else {
+                    launch_f64<true, false, 0, 0, 15>(P, r, g, st, 7, 0, fz);
+                    launch_f64<true, true, 0, 0, 15>(P, r, g, st, 0, 1, fz);
+                }
+            } else {
+                if (!inverse) {
+                    launch_int<false, true, 0, 0, 15>(P, r, g, st, 0, 0, fz);
+                    launch_int<false, false, 0, 0, 15>(P, r, g, st, 7, 1, fz);
+                } else {
+                    launch_int<true, false, 0, 0, 15>(P, r, g, st, 7, 0, fz);
+                    launch_int<true, true, 0, 0, 15>(P, r, g, st, 0, 1, fz);
+                }
+            }
+        }
+        ss.join();
+        BLB_COUNT_LAUNCH(2 * np2);
+        blb_timing_end(1, t0, st0, alg);
         BLB_CHECK_LAUNCH();
         return BLB_OK;
     }

@@ -58,6 +58,12 @@ def bert():
 
 
 @pytest.fixture(scope="module")
+def f2():
+    """N = 2^15 (the row-f2 Table-6 block-3 preset): the 128 x 256 two-pass NTT kernels."""
+    return Pair(bi.F2)
+
+
+@pytest.fixture(scope="module")
 def bert_dnum1():
     return Pair(bi.BERT_DNUM1)
 
@@ -79,7 +85,7 @@ def test_params_psi_match(name, request):
     assert pair.g.psi == pair.o.psi
 
 
-@pytest.mark.parametrize("name", ["tiny", "toy", "mid", "bert"])
+@pytest.mark.parametrize("name", ["tiny", "toy", "mid", "f2", "bert"])
 def test_ntt_intt_bit_exact(name, request):
     pair = request.getfixturevalue(name)
     limbs = list(range(len(pair.o.mods)))
@@ -92,17 +98,22 @@ def test_ntt_intt_bit_exact(name, request):
     assert np.array_equal(u64(t), a)
 
 
-def test_ntt_edge_values(bert):
-    """all-zero, all q-1 and delta inputs at N = 2^16 (max residues exercise the lazy ranges)."""
-    limbs = list(range(6))
-    a = np.zeros((3, 6, bert.N), dtype=np.uint64)
-    for j, m in enumerate(bert.o.mods):
+@pytest.mark.parametrize("name", ["f2", "bert"])
+def test_ntt_edge_values(name, request):
+    """all-zero, all q-1 and delta inputs at N = 2^15 / 2^16 (max residues exercise the lazy ranges),
+    forward and back."""
+    pair = request.getfixturevalue(name)
+    limbs = list(range(len(pair.o.mods)))
+    a = np.zeros((3, len(limbs), pair.N), dtype=np.uint64)
+    for j, m in enumerate(pair.o.mods):
         a[1, j] = m - 1
         a[2, j, 0] = m - 1
         a[2, j, -1] = 1
     t = dev(a)
-    bert.g.ntt(t, limbs)
-    assert np.array_equal(u64(t), np.stack([bert.o.ntt(a[p], limbs) for p in range(3)]))
+    pair.g.ntt(t, limbs)
+    assert np.array_equal(u64(t), np.stack([pair.o.ntt(a[p], limbs) for p in range(3)]))
+    pair.g.intt(t, limbs)
+    assert np.array_equal(u64(t), a)
 
 
 # ---------------------------------------------------------------- encode
