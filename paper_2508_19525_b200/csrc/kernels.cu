@@ -389,7 +389,7 @@ k_ks_inner(KsJobs jobs, KsGroups grp, u64 *u, Primes pr, int k, int np, int K, i
     else ks_inner_body<BETA, EXT, false>(jobs, grp, u, pr, k, np, K, beta_rt, logN, pq, x, m, gi, ds);
 }
 
-// Bulk-staged key-switch inner product (the default for 1 <= beta <= 6).  A CTA owns a tile of
+// Bulk-staged key-switch inner product (the default for 1 <= beta <= 8).  A CTA owns a tile of
 // kKsTile coefficients x of limb m for the jobs of one key group.  Thread 0 issues every input the
 // tile needs -- the 2 beta key rows, the group's beta digit rows per job, the jobs' c0 / c1 rows -- as
 // 1 KB cp.async.bulk copies into shared memory on one mbarrier, so a CTA keeps all of its ~38 KB in
@@ -524,10 +524,12 @@ __global__ void __launch_bounds__(kKsTile) k_ks_bulk(KsJobs jobs, KsGroups grp, 
             kb[j] = skey[(2 * j) * T + threadIdx.x];
             ka[j] = skey[(2 * j + 1) * T + threadIdx.x];
         }
+        // Acc60 holds <= 7 products (BETA <= 6 plus the P c term), Acc128 any number up to 64
+        using A60 = typename std::conditional<(BETA <= 6), Acc60, Acc128>::type;
 #pragma unroll 1
         for (int q = 0; q < cnt; q++) {
             if (q > 0) mbar_wait(&bar[q], 0);
-            Acc60 a0, a1;  // <= BETA + 1 <= 7 products
+            A60 a0, a1;
             a0.zero();
             a1.zero();
 #pragma unroll
@@ -855,9 +857,9 @@ static blb_status ks_inner_launch(const blb_params *P, int level, const KsJobs &
         k_ks_bulk<B, EXT><<<gb, T, sm, st>>>(J, G, u, P->pr, k, np, P->K, P->logN, pq);                       \
         break;                                                                                               \
     }
-        KSB(1) KSB(2) KSB(3) KSB(4) KSB(5) KSB(6)
+        KSB(1) KSB(2) KSB(3) KSB(4) KSB(5) KSB(6) KSB(7) KSB(8)
 #undef KSB
-        default: {  // beta > 6: the per-thread kernel with a runtime digit count
+        default: {  // beta > 8: the per-thread kernel with a runtime digit count
             const dim3 gks((unsigned)(((N + kTB - 1) / kTB) * G.n), E);
             k_ks_inner<0, EXT><<<gks, kTB, 0, st>>>(J, G, u, P->pr, k, np, P->K, beta, P->logN, pq);
         }
