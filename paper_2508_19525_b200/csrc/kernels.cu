@@ -761,7 +761,7 @@ blb_status launch_modup(const blb_params *P, int level, const u64 *const *c1_ntt
     RowBatch rb{};
     rb.base = coef; rb.poly_stride = (long long)k * N; rb.n_polys = n; rb.limbs = k; rb.limb0 = 0;
     for (int i = 0; i < k; i++) rb.prime[i] = i;
-    if (P->logN == 16 && P->alpha == 1) {
+    if ((P->logN == 16 || P->logN == 15) && P->alpha == 1) {
         // fused: the INTT's first pass reads the c1 rows in place (no gather copy); in the forward
         // NTT's first pass the own rows are copied and the others converted (x mod q_m)
         NttFuse gz{};
@@ -885,7 +885,7 @@ static blb_status moddown_launch(const blb_params *P, int level, const KsJobs &J
     rb.base = u; rb.poly_stride = (long long)E * N; rb.n_polys = 2 * n; rb.limbs = np; rb.limb0 = k;
     for (int d = 0; d < np; d++) rb.prime[d] = P->K + d;
     BLB_TRY(launch_ntt(P, rb, true, st));
-    if (P->logN == 16 && np == 1) {
+    if ((P->logN == 16 || P->logN == 15) && np == 1) {
         // fused ModDown: conv = NTT(u_P mod q_i) with the reduction in the first pass and
         // (u_i - conv) * P^{-1} (+ sigma(c0) / (c0, c1)) in the last pass
         RowBatch cb{};
@@ -1076,7 +1076,7 @@ blb_status launch_moddown_rescale(const blb_params *P, int level, u64 *u, int n,
         RowBatch cb{};
         cb.base = conv; cb.poly_stride = (long long)level * N; cb.n_polys = 2 * cnt; cb.limbs = level; cb.limb0 = 0;
         for (int i = 0; i < level; i++) cb.prime[i] = i;
-        if (P->logN == 16) {
+        if (P->logN == 16 || P->logN == 15) {
             NttFuse fz{};
             fz.epi = 1;
             fz.u = ub;

@@ -211,16 +211,17 @@ __device__ __forceinline__ void bfly_f64(double &X, double &Y, double w, double 
 // bulk copies at the start (twd_s[16 (2^r - 1) + (h - c0) 2^r + j] = twd[2^(8+r) + h 2^r + j]), so the
 // rounds read them from shared memory instead of waiting on dependent L2 loads
 constexpr int kTwsWords = 16 * 255;
-template <bool INV, bool SMALL>
+template <bool INV, bool SMALL, int PRO>
 __device__ __forceinline__ void ntt15_strided(u64 *sm, const RowBatch &rb, const u64 *__restrict__ tw_all,
-                                              const double *__restrict__ twd_all, const Primes &pr, int p, int l);
+                                              const double *__restrict__ twd_all, const Primes &pr, const NttFuse &fz,
+                                              int p, int l);
 template <bool INV, bool STRIDED, int PRO, int EPI, bool SMALL, bool LZ = false, int LOGN = 16>
 __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u64 *__restrict__ tw_all,
                                            const double *__restrict__ twd_all, const Primes &pr, int, int,
                                            const NttFuse &fz, int p, int l, double *tws = nullptr,
                                            uint64_t *twbar = nullptr) {
     if constexpr (LOGN == 15 && STRIDED) {  // N = 2^15: 128-point strided columns (ntt15_strided)
-        ntt15_strided<INV, SMALL>(sm, rb, tw_all, twd_all, pr, p, l);
+        ntt15_strided<INV, SMALL, PRO>(sm, rb, tw_all, twd_all, pr, fz, p, l);
         return;
     }
     constexpr int logN = LOGN, N = 1 << logN;
@@ -482,10 +483,12 @@ __device__ __forceinline__ void ntt16_body(u64 *sm, const RowBatch &rb, const u6
 // j = mid * 256 + lo) for 32 consecutive lo per CTA: round A (stages 0..3) on mid = tc + 8 m, round B
 // (stages 4..6) on mid = 16 tc + m, shared-memory tile [mid][32 columns] with the column index XORed
 // by 2 ((mid >> 4) & 7) (conflict-free for both mappings); the contiguous pass is ntt16_body's with
-// s0 = 7.  Plain transforms only (no fused prologue / epilogue).
-template <bool INV, bool SMALL>
+// s0 = 7.  PRO = 1 (forward): the ModUp / ModDown prologue of ntt16_body (row read from fz.src and
+// reduced mod the row's prime).
+template <bool INV, bool SMALL, int PRO>
 __device__ __forceinline__ void ntt15_strided(u64 *sm, const RowBatch &rb, const u64 *__restrict__ tw_all,
-                                              const double *__restrict__ twd_all, const Primes &pr, int p, int l) {
+                                              const double *__restrict__ twd_all, const Primes &pr, const NttFuse &fz,
+                                              int p, int l) {
     constexpr int N = 1 << 15;
     u64 *a = rb.base + (long long)p * rb.poly_stride + (long long)(rb.limb0 + l) * N;
     const int pi = rb.prime[l];
@@ -528,12 +531,30 @@ __device__ __forceinline__ void ntt15_strided(u64 *sm, const RowBatch &rb, const
         for (int m = 0; m < 16; m++)
             if (!(m & dist)) bf(m, dist, (1 << s) + ((16 * tcB + m) >> (7 - s)));
     };
-    // inverse: the second pass reads the first (contiguous) pass's format (FP64 rows: double bits)
+    auto from_u64 = [&](u64 x) -> V {
+        if constexpr (SMALL) return u2d(x);
+        else return x;
+    };
+    if constexpr (PRO == 1) {
+        const u64 *src = fz.src + (long long)(p / fz.src_div) * fz.src_hi + (long long)(p % fz.src_div) * fz.src_lo;
+        const ModConst &mt = pr.m[pi];
+        const int dj = p % fz.src_div;
+        const int mode = ((fz.red0 >> dj) & 1) ? 0 : (((fz.red1 >> dj) & 1) ? 1 : 2);
 #pragma unroll
-    for (int m = 0; m < 16; m++) {
-        const u64 x = a[((tcA + 8 * m) << 8) + c0 + colA];
-        if constexpr (SMALL) v[m] = INV ? from_bits(x) : u2d(x);
-        else v[m] = x;
+        for (int m = 0; m < 16; m++) {
+            u64 x = src[((tcA + 8 * m) << 8) + c0 + colA];
+            if (mode == 1) x = x >= mt.q ? x - mt.q : x;
+            else if (mode == 2) x = mod64(x, mt);
+            v[m] = from_u64(x);
+        }
+    } else {
+        // inverse: the second pass reads the first (contiguous) pass's format (FP64 rows: double bits)
+#pragma unroll
+        for (int m = 0; m < 16; m++) {
+            const u64 x = a[((tcA + 8 * m) << 8) + c0 + colA];
+            if constexpr (SMALL) v[m] = INV ? from_bits(x) : u2d(x);
+            else v[m] = x;
+        }
     }
     if (!INV) {
 #pragma unroll
@@ -594,15 +615,19 @@ __device__ __forceinline__ bool ntt16_row(const RowBatch &rb, int &p, int &l) {
     return true;
 }
 // a skipped (own-digit) row of a ModUp batch: copy this CTA's 16 columns of the NTT-form input row
+template <int LOGN = 16>
 __device__ __forceinline__ void copy_own_tile(const RowBatch &rb, const NttFuse &fz, int p, int l) {
     if (!fz.copy_own) return;
-    constexpr int N = 1 << 16;
+    constexpr int N = 1 << LOGN;
     const u64 *src = fz.srcp.p[p / fz.src_div] + (long long)l * N;
     u64 *a = rb.base + (long long)p * rb.poly_stride + (long long)(rb.limb0 + l) * N;
-    const int t = threadIdx.x, c0 = blockIdx.x * 16;
+    const int t = threadIdx.x;
+    // this CTA's strided tile: 16 columns x 256 (2^16) or 32 columns x 128 (2^15) of j = mid * 256 + lo
+    constexpr int C = LOGN == 16 ? 16 : 32;
+    const int c0 = blockIdx.x * C;
 #pragma unroll
     for (int m = 0; m < 16; m++) {
-        const size_t addr = ((size_t)((t >> 4) + 16 * m) << 8) + c0 + (t & 15);
+        const size_t addr = ((size_t)(t / C + (256 / C) * m) << 8) + c0 + (t % C);
         a[addr] = src[addr];
     }
 }
@@ -618,7 +643,7 @@ __global__ void __launch_bounds__(256, BLB_NTT_MINB) ntt16_int(RowBatch rb, cons
     __shared__ u64 sm[16 * 256];
     int p, l;
     if (!ntt16_row(rb, p, l)) {
-        if (PRO == 1 && STRIDED) copy_own_tile(rb, fz, p, l);
+        if (PRO == 1 && STRIDED) copy_own_tile<LOGN>(rb, fz, p, l);
         return;
     }
     ntt16_body<INV, STRIDED, PRO, EPI, false, LZ, LOGN>(sm, rb, tw_all, twd, pr, s0, last, fz, p, l);
@@ -633,7 +658,7 @@ __global__ void __launch_bounds__(256, BLB_NTT_F64_MINB) ntt16_f64(RowBatch rb, 
     extern __shared__ __align__(16) u64 dsm[];
     int p, l;
     if (!ntt16_row(rb, p, l)) {
-        if (PRO == 1 && STRIDED) copy_own_tile(rb, fz, p, l);
+        if (PRO == 1 && STRIDED) copy_own_tile<LOGN>(rb, fz, p, l);
         return;
     }
     if constexpr (STRIDED) {
@@ -855,14 +880,56 @@ blb_status launch_ntt(const blb_params *P, const RowBatch &rb, bool inverse, cud
 }
 
 // Forward N = 2^16 NTT with a fused prologue (pro = 1) and / or ModDown epilogue (epi = 1).
+// the fused launch pair of one part (prime kind) of a batch at N = 2^LOGN (15 or 16)
+template <int LOGN>
+static void fused_pair(const blb_params *P, const RowBatch &r, cudaStream_t st, bool inverse, const NttFuse &fz,
+                       const NttFuse &fzp) {
+    constexpr int S2 = LOGN - 8;                      // first stage of the contiguous pass
+    const dim3 g(LOGN == 16 ? 16 : 8, rb_rows(r));
+    const bool small = rb_small(P, r);
+    if (inverse) {  // pro = 2: first (contiguous) pass loads from the pointer table
+        if (small) {
+            launch_f64<true, false, 2, 0, LOGN>(P, r, g, st, S2, 0, fz);
+            launch_f64<true, true, 0, 0, LOGN>(P, r, g, st, 0, 1, fz);
+        } else {
+            launch_int<true, false, 2, 0, LOGN>(P, r, g, st, S2, 0, fz);
+            launch_int<true, true, 0, 0, LOGN>(P, r, g, st, 0, 1, fz);
+        }
+        return;
+    }
+    if constexpr (LOGN == 16) {
+        if (fz.pro == 3) {  // compact coefficients -> packed plaintexts (blb_matmul_coeffs_to_pts)
+            if (small) {
+                launch_f64<false, true, 3, 0>(P, r, g, st, 0, 0, fz);
+                launch_f64<false, false, 0, 2>(P, r, g, st, 8, 1, fz);
+            } else {
+                launch_int<false, true, 3, 0>(P, r, g, st, 0, 0, fz);
+                launch_int<false, false, 0, 2>(P, r, g, st, 8, 1, fz);
+            }
+            return;
+        }
+    }
+    if (small) {
+        if (fz.pro == 1) launch_f64<false, true, 1, 0, LOGN>(P, r, g, st, 0, 0, fzp);
+        else launch_f64<false, true, 0, 0, LOGN>(P, r, g, st, 0, 0, fz);
+        if (fz.epi == 1) launch_f64<false, false, 0, 1, LOGN>(P, r, g, st, S2, 1, fz);
+        else launch_f64<false, false, 0, 0, LOGN>(P, r, g, st, S2, 1, fz);
+    } else {
+        if (fz.pro == 1) launch_int<false, true, 1, 0, LOGN>(P, r, g, st, 0, 0, fzp);
+        else launch_int<false, true, 0, 0, LOGN>(P, r, g, st, 0, 0, fz);
+        if (fz.epi == 1) launch_int<false, false, 0, 1, LOGN>(P, r, g, st, S2, 1, fz);
+        else launch_int<false, false, 0, 0, LOGN>(P, r, g, st, S2, 1, fz);
+    }
+}
+
 blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool inverse, const NttFuse &fz,
                             cudaStream_t st0) {
     const cudaStream_t st = st0;
     const int rows = rb.n_polys * rb.limbs;
     if (rows == 0) return BLB_OK;
-    if (P->logN != 16 || rows > 65535 || (inverse && (fz.pro != 2 || fz.epi)) || (!inverse && fz.pro == 2) ||
-        ((fz.pro == 3 || fz.epi == 2) && (fz.pro != 3 || fz.epi != 2))) {
-        blb_set_error("launch_ntt_fused: N = 2^16 forward batches (or inverse with pro = 2) only");
+    if ((P->logN != 16 && P->logN != 15) || rows > 65535 || (inverse && (fz.pro != 2 || fz.epi)) ||
+        (!inverse && fz.pro == 2) || ((fz.pro == 3 || fz.epi == 2) && (fz.pro != 3 || fz.epi != 2 || P->logN != 16))) {
+        blb_set_error("launch_ntt_fused: N = 2^15 / 2^16 forward batches (or inverse with pro = 2) only");
         return BLB_E_INVALID_ARG;
     }
     BLB_COUNT(2, rows);
@@ -886,44 +953,12 @@ blb_status launch_ntt_fused(const blb_params *P, const RowBatch &rb, bool invers
                 else if (fz.src_q[j] / 2 < minq) fzp.red1 |= 1u << j;  // q_j <= 2 minq - 1 (odd primes)
             }
         }
-        const RowBatch &r = rp;
-        const dim3 g(16, rb_rows(r));
-        const bool small = rb_small(P, r);
-        if (inverse) {  // pro = 2: first (contiguous) pass loads from the pointer table
-            if (small) {
-                launch_f64<true, false, 2, 0>(P, r, g, st, 8, 0, fz);
-                launch_f64<true, true>(P, r, g, st, 0, 1, fz);
-            } else {
-                launch_int<true, false, 2, 0>(P, r, g, st, 8, 0, fz);
-                launch_int<true, true>(P, r, g, st, 0, 1, fz);
-            }
-            continue;
-        }
-        if (fz.pro == 3) {  // compact coefficients -> packed plaintexts (blb_matmul_coeffs_to_pts)
-            if (small) {
-                launch_f64<false, true, 3, 0>(P, r, g, st, 0, 0, fz);
-                launch_f64<false, false, 0, 2>(P, r, g, st, 8, 1, fz);
-            } else {
-                launch_int<false, true, 3, 0>(P, r, g, st, 0, 0, fz);
-                launch_int<false, false, 0, 2>(P, r, g, st, 8, 1, fz);
-            }
-            continue;
-        }
-        if (small) {
-            if (fz.pro == 1) launch_f64<false, true, 1, 0>(P, r, g, st, 0, 0, fzp);
-            else launch_f64<false, true, 0, 0>(P, r, g, st, 0, 0, fz);
-            if (fz.epi == 1) launch_f64<false, false, 0, 1>(P, r, g, st, 8, 1, fz);
-            else launch_f64<false, false, 0, 0>(P, r, g, st, 8, 1, fz);
-        } else {
-            if (fz.pro == 1) launch_int<false, true, 1, 0>(P, r, g, st, 0, 0, fzp);
-            else launch_int<false, true, 0, 0>(P, r, g, st, 0, 0, fz);
-            if (fz.epi == 1) launch_int<false, false, 0, 1>(P, r, g, st, 8, 1, fz);
-            else launch_int<false, false, 0, 0>(P, r, g, st, 8, 1, fz);
-        }
+        if (P->logN == 16) fused_pair<16>(P, rp, st, inverse, fz, fzp);
+        else fused_pair<15>(P, rp, st, inverse, fz, fzp);
     }
     ss.join();
     BLB_COUNT_LAUNCH(2 * np2);
-    blb_timing_end(1, t0, st0, (double)rows * 16.0 * (1 << 16));
+    blb_timing_end(1, t0, st0, (double)rows * 16.0 * (double)(1 << P->logN));
     BLB_CHECK_LAUNCH();
     return BLB_OK;
 }

@@ -449,6 +449,25 @@ def test_f2_ops_bit_exact(qktoy):
         assert np.array_equal(u64(r.data), O.rotate_sum(qktoy.o, oa, okeys, L, D, broadcast=bc).data)
 
 
+def test_f2_preset_keyswitch_bit_exact(f2):
+    """N = 2^15 (row f2's Table-6 block-3 preset, dnum = 8): rotations (fused ModUp / ModDown NTT passes
+    of the 2^15 kernels, bulk key switch with beta up to 8) and the relinearised product (fused
+    ModDown + rescale, C17), bit-exact against the oracle."""
+    key = bi.crypto_key(9, 15)
+    okeys = O.keygen(f2.o, key, [5], relin=True)
+    gkeys, sk = blb.keygen(f2.g, key, [5], relin=True)
+    for lvl in (f2.K - 1, 4, 1):
+        data = rand_limbs(f2, 2, list(range(lvl + 1)), seed=30 + lvl)
+        got = blb.rotate(f2.g, gkeys, blb.Ciphertext(dev(data), lvl, 1.0), 5)
+        assert np.array_equal(u64(got.data), O.rotate(f2.o, O.Ct(data, lvl, 1.0), okeys, 5).data), lvl
+    lvl = f2.K - 1
+    a = rand_limbs(f2, 2, list(range(lvl + 1)), 41)
+    b = rand_limbs(f2, 2, list(range(lvl + 1)), 42)
+    r = blb.mul_relin(f2.g, gkeys, blb.Ciphertext(dev(a), lvl, 2.0 ** 40), blb.Ciphertext(dev(b), lvl, 2.0 ** 40))
+    ref = O.mul_relin(f2.o, O.Ct(a, lvl, 2.0 ** 40), O.Ct(b, lvl, 2.0 ** 40), okeys)
+    assert np.array_equal(u64(r.data), ref.data)
+
+
 @pytest.mark.parametrize("name", ["bert", "bert_dnum1"])
 def test_bert_size_keyswitch_bit_exact(name, request):
     """N = 2^16: rotation at every level, relinearised product, rotate-and-sum -- bit-exact against
