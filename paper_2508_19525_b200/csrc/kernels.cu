@@ -1004,6 +1004,20 @@ __global__ void k_mdr_lift(const u64 *u, u64 *conv, MdrTab T, Primes pr, int k, 
         }
         d[t] = v;
     }
+    if (T.nd == 2) {
+        // one special prime: r = d1 m0 + d0 mod q_i.  The Shoup product takes d1 < 2^64 directly (no
+        // reduction of d1 first), and d0 < m0 = q_l is below 2 q_i for the chain's same-size primes
+        // (one conditional subtraction; the general reduction only if it is not)
+        for (int i = 0; i < level; i++) {
+            const ModConst &mc = pr.m[i];
+            u64 d0 = d[0];
+            if (d0 >= mc.q) d0 -= mc.q;
+            if (d0 >= mc.q) d0 = mod64(d0, mc);
+            const u64 r = addmod(shoup(d[1], T.mq[0][i], T.mqsh[0][i], mc.q), d0, mc.q);
+            conv[((long long)pp * level + i) * N + x] = submod(r, T.hq[i], mc.q);
+        }
+        return;
+    }
     for (int i = 0; i < level; i++) {
         const ModConst &mc = pr.m[i];
         u64 r = mod64(d[T.nd - 1], mc);
