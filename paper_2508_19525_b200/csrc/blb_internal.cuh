@@ -302,6 +302,26 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
                  : "memory");
 }
 
+// the same with an L2 cache policy (createpolicy): streamed-once data (the weight plaintexts) marked
+// evict_first so it does not push the re-read operands (the baby-step rotations R) out of L2
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, unsigned bytes, uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
 // Opt a kernel in to > 48 KB of dynamic shared memory on the CURRENT device, once per (kernel,
 // device): the attribute is per device context, so a process driving several GPUs sets it on each.
 bool blb_smem_optin_needed(const void *kernel, size_t bytes);  // api.cu: registry keyed by (kernel, device)

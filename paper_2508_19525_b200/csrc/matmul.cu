@@ -326,6 +326,10 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char
                         (long long)n_e * lay.loff[l] + (long long)tile * n_e * tb;
             int slot = 0;
             unsigned phase = 0;  // parity of the empty-barrier round being waited for
+#ifndef BLB_MAC_L2HINT
+#define BLB_MAC_L2HINT 1
+#endif
+            const uint64_t pol_pt = l2_policy_evict_first(), pol_r = l2_policy_evict_last();
             for (int s = 0; s < n_e; s++) {
                 if (s >= nst) {
                     mbar_wait(&empty[slot], phase);
@@ -333,10 +337,18 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char
                 }
                 unsigned char *stb = ring + (size_t)slot * stage_bytes;
                 mbar_expect_tx(&full[slot], (unsigned)nP * tb + 2u * 4096u);
-                for (int j = 0; j < nP; j++) bulk_g2s(stb + j * tb, pp[j] + (long long)s * tb, tb, &full[slot]);
                 const int bi = ent_r[e_lo + s];
-                bulk_g2s(stb + kMacP * tb, R + (long long)bi * 2 * kN + lx0, 4096, &full[slot]);
-                bulk_g2s(stb + kMacP * tb + 4096, R + ((long long)bi * 2 + 1) * kN + lx0, 4096, &full[slot]);
+                if (BLB_MAC_L2HINT) {  // plaintexts are read once: evict first; R tiles are re-read by other CTAs
+                    for (int j = 0; j < nP; j++)
+                        bulk_g2s_hint(stb + j * tb, pp[j] + (long long)s * tb, tb, &full[slot], pol_pt);
+                    bulk_g2s_hint(stb + kMacP * tb, R + (long long)bi * 2 * kN + lx0, 4096, &full[slot], pol_r);
+                    bulk_g2s_hint(stb + kMacP * tb + 4096, R + ((long long)bi * 2 + 1) * kN + lx0, 4096, &full[slot],
+                                  pol_r);
+                } else {
+                    for (int j = 0; j < nP; j++) bulk_g2s(stb + j * tb, pp[j] + (long long)s * tb, tb, &full[slot]);
+                    bulk_g2s(stb + kMacP * tb, R + (long long)bi * 2 * kN + lx0, 4096, &full[slot]);
+                    bulk_g2s(stb + kMacP * tb + 4096, R + ((long long)bi * 2 + 1) * kN + lx0, 4096, &full[slot]);
+                }
                 if (++slot == nst) {
                     slot = 0;
                     if (s >= nst) phase ^= 1u;
