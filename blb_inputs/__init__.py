@@ -84,7 +84,8 @@ GPT2_BASE = dict(L=128, d=768, H=12, ffn=3072)
 # BSGS baby-step counts B of the layer plans bench.py times (C11 plan parameter, reading S15;
 # 0 = the ct-ct default B = g).  A workload parameter, not arithmetic: bench.py and the
 # full-size parity tests (tests/test_gpu_bert.py) both read it, so they cannot drift apart.
-BENCH_BSGS = {"qkv": 64, "oproj": 16, "ffn1": 64, "ffn2": 16, "qk": 0}
+# (QKV at B = 32: 7.6-7.7 vs 7.8-8.0 ms per layer at B = 64, profiles/r2s2_bsgs_sweep.log; FFN1 equal)
+BENCH_BSGS = {"qkv": 32, "oproj": 16, "ffn1": 64, "ffn2": 16, "qk": 0}
 
 
 def bert_attention_inputs(L=128, d=768, config_id=2):

@@ -50,7 +50,7 @@ class Dims:
 
 BERT_BASE = Dims()
 BERT_LARGE = Dims(128, 1024, 16, 4096)
-BSGS = {"qkv": 64, "oproj": 16, "ffn1": 64, "ffn2": 16, "qk": 0}
+BSGS = {"qkv": 32, "oproj": 16, "ffn1": 64, "ffn2": 16, "qk": 0}
 # mask object ids (reading C19): id = seq * 2^24 + block * 2^16 + output, so every
 # conversion of every inference draws a fresh mask (Alg. 1 line 1; Theorem 1)
 MASK_BLOCK = {"qkv": 0, "oproj": 1, "ffn1": 2, "ffn2": 3, "qk": 4}

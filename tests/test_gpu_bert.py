@@ -141,8 +141,9 @@ def test_bench_plans_are_the_tested_plans(bert):
     assert (spec.plans["qk"].J, spec.plans["sv"].J) == (4, 8)
 
 
-def test_qkv_b64_sampled_outputs_bit_exact(bert):
-    """QKV at B = 64: output 0 (Q, MHP) straight from the plan, output 9 (V) through the layer mask."""
+def test_qkv_bench_bsgs_sampled_outputs_bit_exact(bert):
+    """QKV at the bench's B (BENCH_BSGS): output 0 (Q, MHP) straight from the plan, output 9 (V) through
+    the layer mask."""
     o_in, g_in = layer_inputs(bert)
     ctx, layer = bert["ctx"], bert["layer"]
     A = bert["A"]

@@ -22,13 +22,14 @@ import paper_2508_19525_b200 as blb  # noqa: E402
 from paper_2508_19525_b200 import packing  # noqa: E402
 from paper_2508_19525_b200.layer import Dims, FusedLinearLayer  # noqa: E402
 
-BSGS = {"qkv": 64, "oproj": 16, "ffn1": 64, "ffn2": 16}
+BSGS = dict(bi.BENCH_BSGS)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--bsgs", default="", help='JSON overrides of the BSGS dict, e.g. {"qkv": 32}')
     ap.add_argument("--only", default="", choices=["", "sv", "qk"],
                     help="run only Softmax.V (sv) or Q.K^T (qk), one call inside the NVTX range 'only' "
                          "(for an ncu launch list of that block)")
@@ -37,7 +38,8 @@ def main():
     dims = dict(L=128, d=768, H=12, ffn=3072)
     preset = bi.BERT
     params = blb.Params.from_preset(preset, device=0)
-    layer = FusedLinearLayer(params, Dims(**dims), 0, 1, bsgs=BSGS)
+    bsgs = dict(BSGS, **(json.loads(args.bsgs) if args.bsgs else {}))
+    layer = FusedLinearLayer(params, Dims(**dims), 0, 1, bsgs=bsgs)
     A = bi.bert_attention_inputs(dims["L"], dims["d"])
     F = bi.bert_ffn_inputs(dims["L"], dims["d"], dims["H"], dims["ffn"])
     keys, sk = blb.keygen(params, A["keys_key"], layer.rotation_steps(), relin=True)
@@ -117,7 +119,9 @@ def main():
     torch.cuda.synchronize()
     out = {k: sum(a.elapsed_time(b) for a, b in v) / args.steps for k, v in times.items()}
     out["step_total"] = e0.elapsed_time(e1) / args.steps
-    print(json.dumps({k: round(v, 3) for k, v in out.items()}))
+    out = {k: round(v, 3) for k, v in out.items()}
+    out["bsgs"] = bsgs
+    print(json.dumps(out))
 
 
 if __name__ == "__main__":
