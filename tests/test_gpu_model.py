@@ -64,6 +64,15 @@ def test_compact_coeffs_expand_to_encode_weights():
             assert torch.equal(got, ref)
 
 
+def test_compact_coeffs_overflow_is_an_error():
+    """Coefficients that need more than 40 bits are refused (BLB_E_OVERFLOW), never truncated."""
+    params = blb.Params.from_preset(bi.QKTOY)
+    pl = blb.MatmulPlan(params, 32, 64, 96, bsgs_B=8, level=4)
+    W = np.random.default_rng(5).normal(0, 300.0, (64, 96))   # |scale * w| far above 2^39
+    with pytest.raises(blb.BLBError):
+        pl.encode_coeffs(W)
+
+
 @pytest.mark.parametrize("mode", ["reencode", "resident", "coeffs"])
 def test_two_layer_stack_matches_per_layer(mode):
     params = blb.Params.from_preset(bi.QKTOY)
