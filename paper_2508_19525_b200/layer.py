@@ -374,7 +374,8 @@ class LayerPipeline:
         with torch.cuda.stream(self.down):
             self.down.wait_event(done)
             for h, t in zip(self.host_out[s], tensors):
-                t.record_stream(self.down)
+                if t.is_cuda:  # (results gathered over gloo on a shared GPU are host tensors already)
+                    t.record_stream(self.down)
                 h.copy_(t, non_blocking=True)
         self.k += 1
         return self.host_out[s]
