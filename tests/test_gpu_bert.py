@@ -3,7 +3,7 @@ N = 2^16, the BSGS splits of blb_inputs.BENCH_BSGS, the plan objects of the benc
 layer.FusedLinearLayer): the GPU evaluates every output ciphertext, the oracle recomputes
 sampled output ciphertexts one by one, and they must agree bit-exactly on every limb.
 
-* QKV (C11 + MHP, B = 64): a Q output and a V output; the V output also through the layer
+* QKV (C11 + MHP, B from BENCH_BSGS): a Q output and a V output; the V output also through the layer
   step's CKKS->MPC mask (masked ciphertext and server share);
 * FFN1 (B = 64) and FFN2 (12 inputs, B = 16): one output each, through the layer step's mask;
 * out-projection (C12, diagonal input with padded heads, B = 16) at level 1, where the layer
