@@ -397,6 +397,15 @@ blb_status blb_ct_pt_matmul(const blb_matmul_plan *plan, const blb_keys *keys, c
  *   < 2^64, reduced mod q_i here): giant steps in Q_l u P, the fused ModDown + rescale (C11, C17),
  *   out[t] at level-1 with scale `scale` (the input scale).  Needs the giant-step keys.
  *   ws: blb_matmul_workspace_bytes(plan, out_count).  acc_in is not modified. */
+/* Row f4 (throughput variant): n_batch independent input sets in[b * n_in .. (b+1) * n_in) against the
+ * SAME plaintexts -- each set's ModUp / baby steps / giant steps as blb_ct_pt_matmul, but ONE
+ * weight-stationary MAC whose every staged plaintext tile feeds two input sets (the plaintext stream,
+ * the step's dominant HBM traffic, is read once per pair of sets).  out[b * out_count + t] receives
+ * output out_first + t of set b, bit-identical to blb_ct_pt_matmul on that set alone.  ws: n_batch times
+ * blb_matmul_workspace_bytes(plan, out_count).  Full (non-windowed) plans only. */
+blb_status blb_ct_pt_matmul_batch(const blb_matmul_plan *plan, const blb_keys *keys, const blb_ct *in, int n_in,
+                                  int n_batch, const uint64_t *pt_dev, int out_first, int out_count, blb_ct *out,
+                                  void *ws, size_t ws_bytes, void *stream);
 blb_status blb_ct_pt_matmul_acc(const blb_matmul_plan *plan, const blb_keys *keys, const blb_ct *in, int n_in,
                                 const uint64_t *pt_dev, uint64_t *acc_out, void *ws, size_t ws_bytes, void *stream);
 blb_status blb_ct_pt_matmul_finish(const blb_matmul_plan *plan, const blb_keys *keys, const uint64_t *acc_in,

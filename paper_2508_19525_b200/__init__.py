@@ -116,6 +116,8 @@ def lib() -> ctypes.CDLL:
             "blb_matmul_workspace_bytes": ([vp, ctypes.c_int], ctypes.c_size_t),
             "blb_ct_pt_matmul": ([vp, vp, vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t,
                                   vp], ctypes.c_int),
+            "blb_ct_pt_matmul_batch": ([vp, vp, vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp, vp,
+                                        ctypes.c_size_t, vp], ctypes.c_int),
             "blb_f2_workspace_bytes": ([vp, ctypes.c_int], ctypes.c_size_t),
             "blb_mul_relin": ([vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
             "blb_mul_relin_batch_workspace_bytes": ([vp, ctypes.c_int, ctypes.c_int], ctypes.c_size_t),
@@ -697,6 +699,27 @@ class MatmulPlan:
         _check(lib().blb_ct_pt_matmul(self._h, keys.handle, cin, len(cts), _ptr(pts), out_first, out_count, cout,
                                       _ptr(ws), ws.numel() * 8, _stream()))
         for o, c in zip(outs, cout):
+            o.level, o.scale = c.level, c.scale
+        return outs
+
+    def batch(self, keys: Keys, cts_sets: list, pts: torch.Tensor, out_first: int = 0, out_count: int | None = None,
+              ws: torch.Tensor | None = None) -> list:
+        """blb_ct_pt_matmul_batch: several input sets against the same plaintexts (one weight-stationary
+        MAC); -> one list of outputs per set."""
+        out_count = self.n_out - out_first if out_count is None else out_count
+        nb = len(cts_sets)
+        n_in = len(cts_sets[0])
+        assert all(len(c) == n_in for c in cts_sets)
+        per = self.workspace_bytes(out_count)
+        ws = torch.empty(nb * per // 8 + 1, dtype=torch.int64, device="cuda") if ws is None else ws
+        outs = [[Ciphertext.empty(self.params, self.level - 1) for _ in range(out_count)] for _ in range(nb)]
+        flat_in = [c for cs in cts_sets for c in cs]
+        flat_out = [o for os_ in outs for o in os_]
+        cin = (_Ct * len(flat_in))(*[c.c() for c in flat_in])
+        cout = (_Ct * max(1, len(flat_out)))(*[o.c() for o in flat_out])
+        _check(lib().blb_ct_pt_matmul_batch(self._h, keys.handle, cin, n_in, nb, _ptr(pts), out_first, out_count, cout,
+                                            _ptr(ws), ws.numel() * 8, _stream()))
+        for o, c in zip(flat_out, cout):
             o.level, o.scale = c.level, c.scale
         return outs
 

@@ -377,6 +377,169 @@ static void launch_mac4(const unsigned char *pt, const u64 *R, u64 *acc, const i
                                                                                       o0, e_base, n_o, k, logN, pr, lay);
 }
 
+// Weight-stationary batched MAC (row f4, blb_ct_pt_matmul_batch): kB independent input sets (each with
+// its own baby-step buffer R_b and accumulators acc_b, at a fixed stride) against ONE stream of the
+// output's plaintexts -- per pipeline stage one plaintext tile + kB (c0, c1) rotation tile pairs, so each
+// plaintext byte read from HBM feeds kB inputs (the single-input kernel above shares R between two
+// outputs instead).  Same accumulators, folds and final reduction as mac4_consume.
+constexpr int kMbB = 2;       // inputs per CTA
+constexpr int kMbStages = 3;  // ring stages (3 x ~20 KB: 3 CTAs per SM)
+__host__ __device__ constexpr unsigned macb_stage_bytes(int w) { return (unsigned)(512 * w + kMbB * 8192); }
+constexpr size_t macb_smem() { return (size_t)kMbStages * macb_stage_bytes(8) + 2 * kMbStages * 8; }
+template <bool SPLIT41, bool PACKED>
+__device__ __forceinline__ void macb_consume(const unsigned char *ring, uint64_t *full, uint64_t *empty, int n_e, int nB,
+                                             u64 *const *outs, long long kN, const ModConst &mc) {
+    using A = typename std::conditional<SPLIT41, AccG, Acc128>::type;
+    constexpr int NST = kMbStages;
+    constexpr unsigned TB = PACKED ? 5u * 512u : 8u * 512u;
+    constexpr unsigned SB = TB + kMbB * 8192u;
+    const double qd = (double)mc.q, qinv = 1.0 / qd;
+    A a00[kMbB], a01[kMbB], a10[kMbB], a11[kMbB];
+#pragma unroll
+    for (int b = 0; b < kMbB; b++) { a00[b].zero(); a01[b].zero(); a10[b].zero(); a11[b].zero(); }
+    const int t = threadIdx.x;
+    const unsigned full0 = smem_u32(full), empty0 = smem_u32(empty);
+    const unsigned char *rt_t = ring + TB + 16 * t;                       // R tiles of input b at + 8192 b
+    const unsigned char *lo_t = ring + (PACKED ? 8 * t : 16 * t);
+    const unsigned char *hi_t = ring + 2048 + 2 * t;
+    auto stage = [&](int slot, unsigned phase) {
+        mbar_wait_sa(full0 + 8u * slot, phase);
+        const unsigned off = (unsigned)slot * SB;
+        if constexpr (SPLIT41) {
+            double Px, Py;
+            if constexpr (PACKED) {
+                const uint2 lo = *reinterpret_cast<const uint2 *>(lo_t + off);
+                const unsigned hi = *reinterpret_cast<const unsigned short *>(hi_t + off);
+                Px = __dsub_rn(__hiloint2double((int)__byte_perm(hi, 0x43300000u, 0x7650), (int)lo.x), 4503599627370496.0);
+                Py = __dsub_rn(__hiloint2double((int)__byte_perm(hi, 0x43300000u, 0x7651), (int)lo.y), 4503599627370496.0);
+            } else {
+                const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(lo_t + off);
+                Px = AccF64::u2d(pv.x);
+                Py = AccF64::u2d(pv.y);
+            }
+#pragma unroll
+            for (int b = 0; b < kMbB; b++) {  // unconditional: a missing input's slot holds stale data, never stored
+                const double2 r0 = *reinterpret_cast<const double2 *>(rt_t + off + b * 8192);
+                const double2 r1 = *reinterpret_cast<const double2 *>(rt_t + off + b * 8192 + 4096);
+                a00[b].macd(Px, r0.x); a01[b].macd(Py, r0.y);
+                a10[b].macd(Px, r1.x); a11[b].macd(Py, r1.y);
+            }
+        } else {
+            const ulonglong2 pv = *reinterpret_cast<const ulonglong2 *>(lo_t + off);
+#pragma unroll
+            for (int b = 0; b < kMbB; b++) {
+                if (b < nB) {
+                    const ulonglong2 r0 = *reinterpret_cast<const ulonglong2 *>(rt_t + off + b * 8192);
+                    const ulonglong2 r1 = *reinterpret_cast<const ulonglong2 *>(rt_t + off + b * 8192 + 4096);
+                    a00[b].mac(pv.x, r0.x); a01[b].mac(pv.y, r0.y);
+                    a10[b].mac(pv.x, r1.x); a11[b].mac(pv.y, r1.y);
+                }
+            }
+        }
+        mbar_arrive_sa(empty0 + 8u * slot);
+    };
+    constexpr int kFold = ((SPLIT41 ? 512 : 64) / NST) * NST;
+    const int n_full = n_e - n_e % NST;
+    unsigned phase = 0;
+    int s = 0;
+    while (s < n_full) {
+        const int s1 = n_full - s < kFold ? n_full : s + kFold;
+        for (; s < s1; s += NST) {
+#pragma unroll
+            for (int i = 0; i < NST; i++) stage(i, phase);
+            phase ^= 1u;
+        }
+        if (s < n_e && s % kFold == 0) {
+#pragma unroll
+            for (int b = 0; b < kMbB; b++) {
+                accf(a00[b], mc, qd, qinv); accf(a01[b], mc, qd, qinv);
+                accf(a10[b], mc, qd, qinv); accf(a11[b], mc, qd, qinv);
+            }
+        }
+    }
+    for (int i = 0; s < n_e; s++, i++) stage(i, phase);
+#pragma unroll
+    for (int b = 0; b < kMbB; b++) {
+        if (b < nB) {
+            u64 *out = outs[b] + 2 * t;
+            *reinterpret_cast<ulonglong2 *>(out) = make_ulonglong2(accr(a00[b], mc, qd, qinv), accr(a01[b], mc, qd, qinv));
+            *reinterpret_cast<ulonglong2 *>(out + kN) =
+                make_ulonglong2(accr(a10[b], mc, qd, qinv), accr(a11[b], mc, qd, qinv));
+        }
+    }
+}
+// grid: (output fastest, tile, limb, input group); R_b = R + b r_stride, acc_b = acc + b acc_stride (u64)
+__global__ void __launch_bounds__(kTB + 32, 3) k_mac_tma4b(const unsigned char *__restrict__ pt, const u64 *__restrict__ R,
+                                                          long long r_stride, u64 *__restrict__ acc, long long acc_stride,
+                                                          int n_batch, const int *__restrict__ ent_r,
+                                                          const int *__restrict__ ent_start, int o0, int e_base, int n_o,
+                                                          int k, int logN, Primes pr, PtLayout lay) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    unsigned char *ring = smraw;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smraw + (size_t)kMbStages * macb_stage_bytes(8));
+    uint64_t *empty = full + kMbStages;
+    const int N = 1 << logN;
+    const int n_tiles = N / (2 * kTB);
+    int bid = blockIdx.x;
+    const int o = bid % n_o;
+    bid /= n_o;
+    const int tile = bid % n_tiles;
+    bid /= n_tiles;
+    const int l = bid % k;
+    const int b0 = (bid / k) * kMbB, nB = min(kMbB, n_batch - b0);
+    const long long kN = (long long)k * N;
+    const int e_lo = ent_start[o0 + o], n_e = ent_start[o0 + o + 1] - e_lo;
+    const long long lx0 = (long long)l * N + tile * 2 * kTB;
+    const int w = lay.w[l];
+    const unsigned tb = 512u * (unsigned)w;
+    const unsigned stage_bytes = tb + kMbB * 8192u;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kMbStages; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kTB);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x >= kTB) {  // producer warp
+        if (threadIdx.x == kTB) {
+            const unsigned char *pp = pt + (long long)(e_lo - e_base) * lay.bpp + (long long)n_e * lay.loff[l] +
+                                      (long long)tile * n_e * tb;
+            const uint64_t pol_pt = l2_policy_evict_first(), pol_r = l2_policy_evict_last();
+            int slot = 0;
+            unsigned phase = 0;
+            for (int s = 0; s < n_e; s++) {
+                if (s >= kMbStages) {
+                    mbar_wait(&empty[slot], phase);
+                    fence_proxy_async_smem();
+                }
+                unsigned char *stb = ring + (size_t)slot * stage_bytes;
+                mbar_expect_tx(&full[slot], tb + (unsigned)nB * 8192u);
+                bulk_g2s_hint(stb, pp + (long long)s * tb, tb, &full[slot], pol_pt);
+                const int bi = ent_r[e_lo + s];
+                for (int b = 0; b < nB; b++) {
+                    const u64 *Rb = R + (b0 + b) * r_stride;
+                    bulk_g2s_hint(stb + tb + b * 8192, Rb + (long long)bi * 2 * kN + lx0, 4096, &full[slot], pol_r);
+                    bulk_g2s_hint(stb + tb + b * 8192 + 4096, Rb + ((long long)bi * 2 + 1) * kN + lx0, 4096, &full[slot],
+                                  pol_r);
+                }
+                if (++slot == kMbStages) {
+                    slot = 0;
+                    if (s >= kMbStages) phase ^= 1u;
+                }
+            }
+        }
+        return;
+    }
+    u64 *outs[kMbB];
+#pragma unroll
+    for (int b = 0; b < kMbB; b++) outs[b] = acc + (b0 + (b < nB ? b : 0)) * acc_stride + (long long)o * 2 * kN + lx0;
+    const ModConst &mc = pr.m[l];
+    if (w == 5) macb_consume<true, true>(ring, full, empty, n_e, nB, outs, kN, mc);
+    else if (mc.q < (1ull << 41)) macb_consume<true, false>(ring, full, empty, n_e, nB, outs, kN, mc);
+    else macb_consume<false, false>(ring, full, empty, n_e, nB, outs, kN, mc);
+}
+
 // scatter standard [cnt][k][N] plaintexts (entries e0..e0+cnt of the plan) into the blocked, width-packed layout
 __global__ void k_block_pts(const u64 *src, unsigned char *dst, const int *ent_start, const int *ent_o, int e0,
                             int e_base, int k, int N, PtLayout lay) {
@@ -1066,7 +1229,8 @@ __global__ void k_reduce_acc(const u64 *src, u64 *dst, Primes pr, int k, int N, 
 // plan's window, and the MAC of the window's plaintexts into acc[o][g] for the outputs
 // [out_first, out_first + out_count) (pt_dev holds that slice's plaintexts).
 static blb_status mm_acc(const blb_matmul_plan *pl, const blb_keys *keys, const blb_ct *in, const u64 *pt_dev,
-                         int out_first, int out_count, u64 *acc, u64 *W, const MatmulWs &w, cudaStream_t st) {
+                         int out_first, int out_count, u64 *acc, u64 *W, const MatmulWs &w, cudaStream_t st,
+                         bool do_mac = true) {
     const blb_params *P = pl->P;
     const int n_in = pl->n_in, level = pl->level, k = level + 1, N = P->N, E = k + P->np, beta = blb_beta(P, level);
     u64 *ext_in = W + w.ext_in, *coef = W + w.coef, *R = W + w.R, *ks = W + w.ks;
@@ -1117,6 +1281,7 @@ static blb_status mm_acc(const blb_matmul_plan *pl, const blb_keys *keys, const 
         }
     }
     // 3. MAC: acc[b', g] = sum over the window's entries (b, i) of P (.) R[b][i]
+    if (!do_mac) return BLB_OK;  // (blb_ct_pt_matmul_batch: one MAC launch for all input sets)
     const int o0 = out_first * pl->G, n_o = out_count * pl->G;
     const int e_base = pl->ent_start[out_first * pl->G];
     const int n_entries = pl->ent_start[o0 + n_o] - pl->ent_start[o0];
@@ -1245,6 +1410,67 @@ extern "C" blb_status blb_ct_pt_matmul(const blb_matmul_plan *pl, const blb_keys
     cudaStream_t st = (cudaStream_t)stream;
     BLB_TRY(mm_acc(pl, keys, in, pt_dev, out_first, out_count, W + w.acc, W, w, st));
     return mm_finish(pl, keys, W + w.acc, out_first, out_count, in[0].scale, out, W, w, st);
+}
+
+extern "C" blb_status blb_ct_pt_matmul_batch(const blb_matmul_plan *pl, const blb_keys *keys, const blb_ct *in,
+                                             int n_in, int n_batch, const u64 *pt_dev, int out_first, int out_count,
+                                             blb_ct *out, void *ws, size_t ws_bytes, void *stream) {
+    if (!pl || !keys || !in || !pt_dev || !out || !ws || n_batch < 1) {
+        blb_set_error("blb_ct_pt_matmul_batch: null argument or n_batch < 1");
+        return BLB_E_INVALID_ARG;
+    }
+    BLB_TRY(check_slice(pl, out_first, out_count));
+    if (pl->i_first != 0 || pl->i_count != pl->B) {
+        blb_set_error("blb_ct_pt_matmul_batch: windowed plans are not supported");
+        return BLB_E_INVALID_ARG;
+    }
+    for (int b = 0; b < n_batch; b++) BLB_TRY(mm_check(pl, keys, in + (size_t)b * n_in, n_in, true, true));
+    for (int t = 0; t < n_batch * out_count; t++)
+        if (!out[t].data) return BLB_E_INVALID_ARG;
+    const MatmulWs w = matmul_ws(pl, out_count);
+    if (ws_bytes < (size_t)n_batch * w.total * sizeof(u64)) {
+        blb_set_error("workspace too small: %zu < %zu", ws_bytes, (size_t)n_batch * w.total * sizeof(u64));
+        return BLB_E_NOMEM;
+    }
+    u64 *W = (u64 *)ws;
+    cudaStream_t st = (cudaStream_t)stream;
+    const blb_params *P = pl->P;
+    // 1-2 per input set: ModUp and the baby-step rotations into its own R
+    for (int b = 0; b < n_batch; b++) {
+        u64 *Wb = W + (size_t)b * w.total;
+        BLB_TRY(mm_acc(pl, keys, in + (size_t)b * n_in, pt_dev, out_first, out_count, Wb + w.acc, Wb, w, st, false));
+    }
+    // 3. one weight-stationary MAC for all input sets
+    const int k = pl->level + 1, N = P->N;
+    const int o0 = out_first * pl->G, n_o = out_count * pl->G;
+    const int e_base = pl->ent_start[o0];
+    const int n_entries = pl->ent_start[o0 + n_o] - e_base;
+    if (n_o > 0 && n_entries == 0) {
+        for (int b = 0; b < n_batch; b++)
+            BLB_CUDA_TRY(cudaMemsetAsync(W + (size_t)b * w.total + w.acc, 0, sizeof(u64) * (size_t)n_o * 2 * k * N, st));
+    } else if (n_o > 0) {
+        const int n_tiles = N / (2 * kTB);
+        const PtLayout lay = pt_layout(pl);
+        constexpr size_t smem = macb_smem();
+        blb_smem_optin(k_mac_tma4b, smem);
+        cudaEvent_t t0 = blb_timing_begin(st);
+        const size_t grid = (size_t)n_o * n_tiles * k * ((n_batch + kMbB - 1) / kMbB);
+        k_mac_tma4b<<<(unsigned)grid, kTB + 32, smem, st>>>(reinterpret_cast<const unsigned char *>(pt_dev), W + w.R,
+                                                            (long long)w.total, W + w.acc, (long long)w.total, n_batch,
+                                                            pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN, P->pr,
+                                                            lay);
+        BLB_COUNT_LAUNCH(1);
+        BLB_COUNT(3, (long long)n_entries * n_batch);
+        blb_timing_end(0, t0, st, (double)n_entries * (double)lay.bpp);  // packed plaintext bytes (read once)
+        BLB_CHECK_LAUNCH();
+    }
+    // 4-5 per input set: giant steps, fused ModDown + rescale
+    for (int b = 0; b < n_batch; b++) {
+        u64 *Wb = W + (size_t)b * w.total;
+        BLB_TRY(mm_finish(pl, keys, Wb + w.acc, out_first, out_count, in[(size_t)b * n_in].scale,
+                          out + (size_t)b * out_count, Wb, w, st));
+    }
+    return BLB_OK;
 }
 
 extern "C" blb_status blb_ct_pt_matmul_acc(const blb_matmul_plan *pl, const blb_keys *keys, const blb_ct *in,
