@@ -161,6 +161,43 @@ struct Acc60 {
     }
 };
 
+// Carry-save accumulator for many products of residues < 2^60 (the weight MAC's q0 limb): a = a1 2^32 +
+// a0 (a1 < 2^28); L (96 bits, carry chain) += a0 b0, M (96 bits) += a0 b1 + a1 b0, H (64 bits) += a1 b1
+// (< 2^56): 10 instructions per product, no compare / select.  total = L + M 2^32 + H 2^64 < P 2^120
+// stays below 2^128 for P < 256 products (fold every 128).
+struct Acc60W {
+    uint32_t l0, l1, l2, m0, m1, m2;
+    u64 h;
+    __device__ __forceinline__ void zero() { l0 = l1 = l2 = m0 = m1 = m2 = 0; h = 0; }
+    __device__ __forceinline__ void mac(u64 a, u64 b) {
+        const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32), b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
+        asm("mad.lo.cc.u32 %0, %6, %8, %0;\n\t"
+            "madc.hi.cc.u32 %1, %6, %8, %1;\n\t"
+            "addc.u32 %2, %2, 0;\n\t"
+            "mad.lo.cc.u32 %3, %6, %9, %3;\n\t"
+            "madc.hi.cc.u32 %4, %6, %9, %4;\n\t"
+            "addc.u32 %5, %5, 0;\n\t"
+            "mad.lo.cc.u32 %3, %7, %8, %3;\n\t"
+            "madc.hi.cc.u32 %4, %7, %8, %4;\n\t"
+            "addc.u32 %5, %5, 0;"
+            : "+r"(l0), "+r"(l1), "+r"(l2), "+r"(m0), "+r"(m1), "+r"(m2)
+            : "r"(a0), "r"(a1), "r"(b0), "r"(b1));
+        h += (u64)a1 * b1;
+    }
+    __device__ __forceinline__ u64 reduce(const ModConst &c) const {
+        const u64 lo = ((u64)l1 << 32) | l0;
+        const u64 s = lo + ((u64)m0 << 32);
+        const u64 H = (u64)l2 + (((u64)m2 << 32) | m1) + h + (s < lo ? 1 : 0);
+        return reduce128(H, s, c);
+    }
+    __device__ __forceinline__ void fold(const ModConst &c) {
+        const u64 r = reduce(c);
+        zero();
+        l0 = (uint32_t)r;
+        l1 = (uint32_t)(r >> 32);
+    }
+};
+
 // Exact FP64-pipe accumulator for products of residues < 2^41 (offloads the fma-heavy pipe that
 // the integer accumulators saturate; the B200 FP64 pipe runs 64 DFMA/clk/SM beside it):
 // a b = p + e with p = fl(a b) and e = fma(a, b, -p) exact; c = round(p / q) by one fma against

@@ -287,7 +287,7 @@ template <int kMacP, int kM4Stages, int MINB, int kM4StagesP = kM4Stages>
 __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char *__restrict__ pt, const u64 *__restrict__ R,
                                                        u64 *__restrict__ acc, const int *__restrict__ ent_r,
                                                        const int *__restrict__ ent_start, int o0, int e_base, int n_o,
-                                                       int k, int logN, Primes pr, PtLayout lay) {
+                                                       int k, int logN, Primes pr, PtLayout lay, int skip_l) {
     constexpr int kMaxStg = kM4Stages > kM4StagesP ? kM4Stages : kM4StagesP;
     extern __shared__ __align__(128) unsigned char smraw[];
     unsigned char *ring = smraw;
@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char
     bid /= n_grp;
     const int tile = bid % n_tiles;
     const int l = bid / n_tiles;
+    if (l == skip_l) return;  // that limb runs in k_mac_q0 (whole CTA exits before any barrier)
     const int oa = og * kMacP, nP = min(kMacP, n_o - oa);
     const long long kN = (long long)k * N;
     const int e_lo = ent_start[o0 + oa], n_e = ent_start[o0 + oa + 1] - e_lo;
@@ -369,12 +370,112 @@ __global__ void __launch_bounds__(kTB + 32, MINB) k_mac_tma4(const unsigned char
 template <int PP, int STG, int MINB, int STGP = STG>
 static void launch_mac4(const unsigned char *pt, const u64 *R, u64 *acc, const int *ent_r, const int *ent_start, int o0,
                         int e_base, int n_o, int k, int logN, const Primes &pr, int n_tiles, const PtLayout &lay,
-                        cudaStream_t st) {
+                        cudaStream_t st, int skip_l = -1) {
     constexpr size_t smem = mac4_smem<PP, STG, STGP>();
     blb_smem_optin(k_mac_tma4<PP, STG, MINB, STGP>, smem);
     const size_t n_grp = (size_t)(n_o + PP - 1) / PP;
     k_mac_tma4<PP, STG, MINB, STGP><<<(unsigned)(n_grp * n_tiles * k), kTB + 32, smem, st>>>(pt, R, acc, ent_r, ent_start,
-                                                                                      o0, e_base, n_o, k, logN, pr, lay);
+                                                                                      o0, e_base, n_o, k, logN, pr, lay,
+                                                                                      skip_l);
+}
+
+// The weight MAC of one 8-byte limb whose prime is >= 2^41 (the 60-bit q0) as its own kernel: 512
+// consumers with ONE coefficient each, so the four sums of a thread (2 outputs x c0 / c1) fit the
+// carry-save accumulator Acc60W (8 registers each, 10 instructions per product instead of Acc128's
+// 64 x 64 -> 128-bit multiply and compare-carried add); launched on the auxiliary stream beside the
+// FP64-pipe kernel of the other limbs (the two load different pipes).
+constexpr int kQ0Cons = 512, kQ0Stages = 4;
+constexpr unsigned kQ0StageBytes = 2u * 4096u + 2u * 4096u;  // 2 plaintext tiles + (c0, c1) R tiles
+__global__ void __launch_bounds__(kQ0Cons + 32, 2) k_mac_q0(const unsigned char *__restrict__ pt, const u64 *__restrict__ R,
+                                                           u64 *__restrict__ acc, const int *__restrict__ ent_r,
+                                                           const int *__restrict__ ent_start, int o0, int e_base, int n_o,
+                                                           int k, int l, int logN, Primes pr, PtLayout lay) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    unsigned char *ring = smraw;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smraw + (size_t)kQ0Stages * kQ0StageBytes);
+    uint64_t *empty = full + kQ0Stages;
+    const int N = 1 << logN;
+    const int n_tiles = N / 512;
+    const int n_grp = (n_o + 1) / 2;
+    const int og = blockIdx.x % n_grp, tile = blockIdx.x / n_grp;
+    const int oa = og * 2, nP = min(2, n_o - oa);
+    const long long kN = (long long)k * N;
+    const int e_lo = ent_start[o0 + oa], n_e = ent_start[o0 + oa + 1] - e_lo;
+    const long long lx0 = (long long)l * N + tile * 512;
+    constexpr unsigned tb = 4096u;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kQ0Stages; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kQ0Cons);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x >= kQ0Cons) {  // producer warp
+        if (threadIdx.x == kQ0Cons) {
+            const unsigned char *pp[2];
+            for (int j = 0; j < 2; j++)
+                pp[j] = pt + (long long)(ent_start[o0 + oa + (j < nP ? j : 0)] - e_base) * lay.bpp +
+                        (long long)n_e * lay.loff[l] + (long long)tile * n_e * tb;
+            const uint64_t pol_pt = l2_policy_evict_first(), pol_r = l2_policy_evict_last();
+            int slot = 0;
+            unsigned phase = 0;
+            for (int s = 0; s < n_e; s++) {
+                if (s >= kQ0Stages) {
+                    mbar_wait(&empty[slot], phase);
+                    fence_proxy_async_smem();
+                }
+                unsigned char *stb = ring + (size_t)slot * kQ0StageBytes;
+                mbar_expect_tx(&full[slot], (unsigned)nP * tb + 2u * 4096u);
+                for (int j = 0; j < nP; j++) bulk_g2s_hint(stb + j * tb, pp[j] + (long long)s * tb, tb, &full[slot], pol_pt);
+                const int bi = ent_r[e_lo + s];
+                bulk_g2s_hint(stb + 2 * tb, R + (long long)bi * 2 * kN + lx0, 4096, &full[slot], pol_r);
+                bulk_g2s_hint(stb + 2 * tb + 4096, R + ((long long)bi * 2 + 1) * kN + lx0, 4096, &full[slot], pol_r);
+                if (++slot == kQ0Stages) {
+                    slot = 0;
+                    if (s >= kQ0Stages) phase ^= 1u;
+                }
+            }
+        }
+        return;
+    }
+    const int t = threadIdx.x;
+    const ModConst &mc = pr.m[l];
+    Acc60W a00, a01, a10, a11;  // [output j][c0 / c1]
+    a00.zero(); a01.zero(); a10.zero(); a11.zero();
+    const unsigned full0 = smem_u32(full), empty0 = smem_u32(empty);
+    const unsigned char *p_t = ring + 8 * t, *r_t = ring + 2 * tb + 8 * t;
+    auto stage = [&](int slot, unsigned ph) {
+        mbar_wait_sa(full0 + 8u * slot, ph);
+        const unsigned off = (unsigned)slot * kQ0StageBytes;
+        const u64 p0 = *reinterpret_cast<const u64 *>(p_t + off), p1 = *reinterpret_cast<const u64 *>(p_t + off + tb);
+        const u64 r0 = *reinterpret_cast<const u64 *>(r_t + off), r1 = *reinterpret_cast<const u64 *>(r_t + off + 4096);
+        a00.mac(p0, r0); a01.mac(p0, r1);
+        a10.mac(p1, r0); a11.mac(p1, r1);   // (slot 1 of a single-output group is stale, never stored)
+        mbar_arrive_sa(empty0 + 8u * slot);
+    };
+    constexpr int kFold = (128 / kQ0Stages) * kQ0Stages;
+    const int n_full = n_e - n_e % kQ0Stages;
+    unsigned phase = 0;
+    int s = 0;
+    while (s < n_full) {
+        const int s1 = n_full - s < kFold ? n_full : s + kFold;
+        for (; s < s1; s += kQ0Stages) {
+#pragma unroll
+            for (int i = 0; i < kQ0Stages; i++) stage(i, phase);
+            phase ^= 1u;
+        }
+        if (s < n_e && s % kFold == 0) { a00.fold(mc); a01.fold(mc); a10.fold(mc); a11.fold(mc); }
+    }
+    for (int i = 0; s < n_e; s++, i++) stage(i, phase);
+    u64 *out0 = acc + (long long)oa * 2 * kN + lx0 + t;
+    out0[0] = a00.reduce(mc);
+    out0[kN] = a01.reduce(mc);
+    if (nP > 1) {
+        u64 *out1 = out0 + 2 * kN;
+        out1[0] = a10.reduce(mc);
+        out1[kN] = a11.reduce(mc);
+    }
 }
 
 // Weight-stationary batched MAC (row f4, blb_ct_pt_matmul_batch): kB independent input sets (each with
@@ -1298,13 +1399,39 @@ static blb_status mm_acc(const blb_matmul_plan *pl, const blb_keys *keys, const 
         bool grouped = true;
         for (int j = 0; j < n_o && grouped; j++)
             if (j % BLB_MAC_P != BLB_MAC_P - 1 && j + 1 < n_o && !pl->same_next[o0 + j]) grouped = false;
+#ifndef BLB_MAC_Q0
+#define BLB_MAC_Q0 1
+#endif
+        // the 8-byte limb with a prime >= 2^41 (q0) in its own kernel on the auxiliary stream
+        int q0l = -1;
+        if (BLB_MAC_Q0 && grouped && P->aux && BLB_MAC_P == 2)
+            for (int l = 0; l < k && q0l < 0; l++)
+                if (lay.w[l] == 8 && P->mod[l] >= (1ull << 41)) q0l = l;
+        if (q0l >= 0) {
+            cudaEvent_t ef = P->ev[P->ev_next];
+            P->ev_next = (P->ev_next + 1) % 64;
+            cudaEventRecord(ef, st);
+            cudaStreamWaitEvent(P->aux, ef, 0);
+            constexpr size_t qsm = (size_t)kQ0Stages * kQ0StageBytes + 2 * kQ0Stages * 8;
+            blb_smem_optin(k_mac_q0, qsm);
+            const unsigned gq = (unsigned)(((n_o + 1) / 2) * (size_t)(P->N / 512));
+            k_mac_q0<<<gq, kQ0Cons + 32, qsm, P->aux>>>(ptb, R, acc, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, q0l,
+                                                        P->logN, P->pr, lay);
+            BLB_COUNT_LAUNCH(1);
+        }
         if (grouped)
             launch_mac4<BLB_MAC_P, BLB_MAC_STG, BLB_MAC_MINB, BLB_MAC_STGP>(ptb, R, acc, pl->d_ent, pl->d_ent_start, o0,
                                                                             e_base, n_o, k, P->logN, P->pr, n_tiles,
-                                                                            lay, st);
+                                                                            lay, st, q0l);
         else
             launch_mac4<1, 4, 3>(ptb, R, acc, pl->d_ent, pl->d_ent_start, o0, e_base, n_o, k, P->logN, P->pr,
                                  n_tiles, lay, st);
+        if (q0l >= 0) {
+            cudaEvent_t ej = P->ev[P->ev_next];
+            P->ev_next = (P->ev_next + 1) % 64;
+            cudaEventRecord(ej, P->aux);
+            cudaStreamWaitEvent(st, ej, 0);
+        }
         BLB_COUNT_LAUNCH(1);
         BLB_COUNT(3, n_entries);
         blb_timing_end(0, t0, st, (double)n_entries * (double)lay.bpp);  // packed plaintext bytes
