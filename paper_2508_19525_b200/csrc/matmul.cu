@@ -395,7 +395,6 @@ __global__ void __launch_bounds__(kQ0Cons + 32, 2) k_mac_q0(const unsigned char 
     uint64_t *full = reinterpret_cast<uint64_t *>(smraw + (size_t)kQ0Stages * kQ0StageBytes);
     uint64_t *empty = full + kQ0Stages;
     const int N = 1 << logN;
-    const int n_tiles = N / 512;
     const int n_grp = (n_o + 1) / 2;
     const int og = blockIdx.x % n_grp, tile = blockIdx.x / n_grp;
     const int oa = og * 2, nP = min(2, n_o - oa);
