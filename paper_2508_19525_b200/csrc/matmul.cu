@@ -384,7 +384,10 @@ static void launch_mac4(const unsigned char *pt, const u64 *R, u64 *acc, const i
 // carry-save accumulator Acc60W (8 registers each, 10 instructions per product instead of Acc128's
 // 64 x 64 -> 128-bit multiply and compare-carried add); launched on the auxiliary stream beside the
 // FP64-pipe kernel of the other limbs (the two load different pipes).
-constexpr int kQ0Cons = 512, kQ0Stages = 4;
+#ifndef BLB_Q0_STG
+#define BLB_Q0_STG 4
+#endif
+constexpr int kQ0Cons = 512, kQ0Stages = BLB_Q0_STG;
 constexpr unsigned kQ0StageBytes = 2u * 4096u + 2u * 4096u;  // 2 plaintext tiles + (c0, c1) R tiles
 __global__ void __launch_bounds__(kQ0Cons + 32, 2) k_mac_q0(const unsigned char *__restrict__ pt, const u64 *__restrict__ R,
                                                            u64 *__restrict__ acc, const int *__restrict__ ent_r,
