@@ -591,7 +591,7 @@ def run_toy(args):
             "config": {"workload": "config 1 toy: " + preset_desc(P) + ", X W 16x16x16 + CKKS->MPC mask",
                        "bsgs_B": 16, "plaintexts": plan.n_pt, "rotations": plan.n_rotations,
                        "l2": "working set (< 2 MB) is L2-resident: a latency-bound configuration"},
-            "roofline": {"kernel": "k_mac_tma4 (ct-pt weight MAC)", "bound": "hbm", "achieved": mac_gbs,
+            "roofline": {"kernel": "k_mac_tma4 + k_mac_q0 (ct-pt weight MAC: packed limbs + the q0 limb, concurrent)", "bound": "hbm", "achieved": mac_gbs,
                          "peak": hbm_peak, "unit": "GB/s", "frac": mac_gbs / hbm_peak if mac_gbs else None,
                          "traffic": None, "note": "31 plaintexts of 2^12 coefficients: launch latency, not HBM"},
             "gpu_launches": ctr["launches"], "counters_per_step": {k: v / args.steps for k, v in ctr.items()},
@@ -831,7 +831,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded N(0,1) activations, N(0,0.04^2) weights)",
         "config": config_dict(dims, world, preset),
-        "roofline": {"kernel": "k_mac_tma4 (ct-pt weight MAC, row a3)", "bound": "hbm", "achieved": mac_gbs, "peak": hbm_peak,
+        "roofline": {"kernel": "k_mac_tma4 + k_mac_q0 (ct-pt weight MAC, row a3: packed limbs + the q0 limb, concurrent)", "bound": "hbm", "achieved": mac_gbs, "peak": hbm_peak,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
                      "unit": "GB/s", "frac": (mac_gbs / hbm_peak) if mac_gbs else None, "traffic": traffic,
                      "alg_bytes_per_launch": mac["alg_bytes"] / max(1, mac["launches"]),
